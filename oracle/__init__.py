@@ -1,0 +1,195 @@
+"""CPU oracle of the DSI Monte Carlo latency simulator (arXiv 2405.14105).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product (``include/dsi_sim.h`` + ``paper_2405_14105_b200``) never
+imports it and shares no code with it.
+
+The arithmetic lives in ``dsi_oracle.c`` (plain C, single-threaded): the SI
+pseudocode loop of App. F.4 and an event simulation of
+Algorithm 1 with the App. D lookahead.  This module only
+marshals arguments through ctypes and converts user units to integer ticks.
+
+Pins (tests/test_oracle_pins.py): Philox known-answer vectors, Table 1,
+Proposition 1, Theorem 1, the non-SI example,
+the SI closed form E[n+1] = (1-a^{k+1})/(1-a), exhaustive
+enumeration of acceptance patterns against exact rational expectations, and
+hand-derived worked examples.  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dsi_oracle.c")
+_HDR = os.path.join(_HERE, "dsi_oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O2, no intrinsics)."""
+    stale = (not os.path.exists(_LIB)) or any(
+        os.path.getmtime(s) > os.path.getmtime(_LIB) for s in (_SRC, _HDR))
+    if force or stale:
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", "-shared", "-fPIC",
+                               "-o", _LIB, _SRC])
+    return _LIB
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("t_target", ctypes.c_int64), ("t_drafter", ctypes.c_int64),
+                ("accept_rate", ctypes.c_double), ("lookahead", ctypes.c_int32),
+                ("sp_degree", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
+                ("stream_id", ctypes.c_uint32)]
+
+
+class _TrialOut(ctypes.Structure):
+    _fields_ = [("acc", ctypes.c_int32), ("m", ctypes.c_int32), ("iters", ctypes.c_int32),
+                ("nonsi", ctypes.c_int64), ("si", ctypes.c_int64), ("dsi", ctypes.c_int64),
+                ("dsi_segments", ctypes.c_int32), ("dsi_peak_busy", ctypes.c_int32),
+                ("dsi_max_queue", ctypes.c_int32), ("dsi_forwards", ctypes.c_int32)]
+
+
+class _Sums(ctypes.Structure):
+    _fields_ = [("trials", ctypes.c_uint64), ("sum_acc", ctypes.c_int64),
+                ("sum_m", ctypes.c_int64), ("sum_iters", ctypes.c_int64),
+                ("sum_si", ctypes.c_int64), ("sum_dsi", ctypes.c_int64),
+                ("sumsq_si", ctypes.c_uint64), ("sumsq_dsi", ctypes.c_uint64),
+                ("n_dsi_gt_nonsi", ctypes.c_int64), ("n_dsi_gt_si", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.POINTER
+        lib.oracle_philox4x32_10.argtypes = [P(ctypes.c_uint32), P(ctypes.c_uint32), P(ctypes.c_uint32)]
+        lib.oracle_philox4x32_10.restype = None
+        lib.oracle_threshold.argtypes = [ctypes.c_double]
+        lib.oracle_threshold.restype = ctypes.c_uint64
+        lib.oracle_trial.argtypes = [P(_Config), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                     P(_TrialOut), ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_trial.restype = ctypes.c_int
+        lib.oracle_run.argtypes = [P(_Config), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                   ctypes.c_int, P(_Sums)] + [ctypes.c_void_p] * 7
+        lib.oracle_run.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+@dataclass(frozen=True)
+class Config:
+    """One grid point in integer ticks (the paper's quantities, Table 2 cols P:249-256)."""
+    t_target: int
+    t_drafter: int
+    accept_rate: float
+    lookahead: int
+    sp_degree: int
+    n_tokens: int
+    stream_id: int = 0
+
+    def _c(self) -> _Config:
+        return _Config(int(self.t_target), int(self.t_drafter), float(self.accept_rate),
+                       int(self.lookahead), int(self.sp_degree), int(self.n_tokens),
+                       int(self.stream_id))
+
+
+def ticks(x: float, tick: float) -> int:
+    """User latency -> integer ticks: round(x/tick), must be within 1e-9 relative."""
+    r = x / tick
+    t = int(round(r))
+    if t < 1 or abs(r - t) > 1e-9 * abs(r):
+        raise ValueError(f"latency {x} is not an integer number of ticks of {tick}")
+    return t
+
+
+def philox4x32_10(ctr, key):
+    lib = _load()
+    c = (ctypes.c_uint32 * 4)(*[int(v) & 0xFFFFFFFF for v in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(v) & 0xFFFFFFFF for v in key])
+    o = (ctypes.c_uint32 * 4)()
+    lib.oracle_philox4x32_10(c, k, o)
+    return tuple(int(v) for v in o)
+
+
+def threshold(a: float) -> int:
+    return int(_load().oracle_threshold(float(a)))
+
+
+def trial(cfg: Config, seed: int, index: int, pattern: bool = False, hist: bool = False) -> dict:
+    """One trial: acc, m, iters, nonsi, si, dsi (+ event-sim debug counters)."""
+    lib = _load()
+    out = _TrialOut()
+    si_hist = np.zeros(cfg.lookahead + 1, np.int64) if hist else None
+    seg_hist = np.zeros(64, np.int64) if hist else None
+    rc = lib.oracle_trial(ctypes.byref(cfg._c()), seed, index, int(pattern), ctypes.byref(out),
+                          si_hist.ctypes.data if hist else None,
+                          seg_hist.ctypes.data if hist else None)
+    if rc:
+        raise ValueError(f"oracle_trial failed for {cfg}")
+    d = {f: getattr(out, f) for f, _ in _TrialOut._fields_}
+    if hist:
+        d["si_hist"], d["seg_hist"] = si_hist, seg_hist
+    return d
+
+
+def run(cfg: Config, seed: int, first: int = 0, count: int = 1, pattern: bool = False,
+        per_trial: bool = True, hist: bool = False) -> dict:
+    """Trials first..first+count-1 -> exact integer sums (+ per-trial arrays, histograms)."""
+    lib = _load()
+    sums = _Sums()
+    arrs = {}
+    ptrs = [None] * 5
+    if per_trial:
+        for i, (name, dt) in enumerate([("acc", np.int32), ("m", np.int32), ("iters", np.int32),
+                                        ("si", np.int64), ("dsi", np.int64)]):
+            arrs[name] = np.zeros(count, dt)
+            ptrs[i] = arrs[name].ctypes.data
+    si_hist = np.zeros(cfg.lookahead + 1, np.int64) if hist else None
+    seg_hist = np.zeros(64, np.int64) if hist else None
+    rc = lib.oracle_run(ctypes.byref(cfg._c()), seed, first, count, int(pattern),
+                        ctypes.byref(sums), *ptrs,
+                        si_hist.ctypes.data if hist else None,
+                        seg_hist.ctypes.data if hist else None)
+    if rc:
+        raise ValueError(f"oracle_run failed for {cfg}")
+    out = {f: int(getattr(sums, f)) for f, _ in _Sums._fields_}
+    out["nonsi"] = cfg.n_tokens * cfg.t_target
+    out.update(arrs)
+    if hist:
+        out["si_hist"], out["seg_hist"] = si_hist, seg_hist
+    return out
+
+
+def means(sums: dict, tick: float = 1.0) -> dict:
+    """FP64 per-config means in user units: ((double)sum / (double)T) * tick."""
+    T = float(sums["trials"])
+    return {"mean_nonsi": float(sums["nonsi"]) * tick,
+            "mean_si": (float(sums["sum_si"]) / T) * tick,
+            "mean_dsi": (float(sums["sum_dsi"]) / T) * tick}
+
+
+def eq1_feasible(t_target: int, t_drafter: int, k: int, sp: int) -> bool:
+    """Eq. 1: ceil(t_t / (k t_d)) <= SP, in exact integers."""
+    return -(-t_target // (k * t_drafter)) <= sp
+
+
+def min_lookahead(t_target: int, t_drafter: int, sp: int) -> int:
+    """Smallest k >= 1 with ceil(t_t/(k t_d)) <= SP."""
+    k = 1
+    while not eq1_feasible(t_target, t_drafter, k, sp):
+        k += 1
+    return k
+
+
+def required_processors(t_target: int, t_drafter: int, k: int) -> int:
+    """1 + ceil(t_t / (k t_d)): one drafter GPU plus the target servers."""
+    return 1 + -(-t_target // (k * t_drafter))

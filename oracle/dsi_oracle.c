@@ -1,0 +1,373 @@
+/*
+ * dsi_oracle.c -- plain, slow, single-threaded CPU oracle of the DSI Monte
+ * Carlo latency simulator (arXiv 2405.14105).
+ *
+ * TEST INFRASTRUCTURE ONLY (see dsi_oracle.h).  Shares no code with the
+ * product path.  It is deliberately literal: the SI latency comes from the
+ * paper's pseudocode loop and the DSI latency from an event simulation of
+ * Algorithm 1; neither uses the per-segment closed form the GPU evaluates.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n.
+ */
+#include "dsi_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11).  One round maps        */
+/* (c0,c1,c2,c3) with key (k0,k1) to                                         */
+/*   (hi(M1*c2) ^ c1 ^ k0, lo(M1*c2), hi(M0*c0) ^ c3 ^ k1, lo(M0*c0)),      */
+/* M0 = 0xD2511F53, M1 = 0xCD9E8D57; the key is bumped by the Weyl constants */
+/* W0 = 0x9E3779B9, W1 = 0xBB67AE85 between rounds.  Pinned by the Random123 */
+/* known-answer vectors in tests/golden/philox4x32_10_kat.txt.               */
+/* ------------------------------------------------------------------------ */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  int round;
+  for (round = 0; round < 10; round++) {
+    uint64_t p0, p1;
+    uint32_t n0, n1, n2, n3;
+    if (round > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+    p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+    n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    n1 = (uint32_t)p1;
+    n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    n3 = (uint32_t)p0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* A_p = [u < floor(a * 2^32)]: a = 0 never accepts, a = 1 always accepts.  */
+/* a * 2^32 is an exact scaling of a double, so the floor is exact.          */
+uint64_t oracle_threshold(double a) {
+  double x = a * 4294967296.0;
+  uint64_t t;
+  if (!(a >= 0.0) || a > 1.0) return 0;
+  t = (uint64_t)x; /* truncation == floor for x >= 0 */
+  return t;
+}
+
+/* The indicator stream of one trial.                                        */
+/*   key = (seed_lo, seed_hi); counter = (q_lo, q_hi, trial, stream_id);     */
+/*   position p >= 1 uses q = (p-1) >> 2 and output word (p-1) & 3.          */
+typedef struct {
+  uint32_t key[2];
+  uint32_t trial_lo;
+  uint32_t stream_id;
+  uint64_t thr;
+  int pattern;
+  uint64_t pattern_bits;
+} indicator_stream;
+
+static int indicator(const indicator_stream *s, int64_t p) {
+  uint32_t ctr[4], out[4];
+  uint64_t q;
+  if (s->pattern) {
+    /* enumeration mode: A_p = bit (p-1) of the trial index */
+    if (p - 1 >= 64) return 0;
+    return (int)((s->pattern_bits >> (p - 1)) & 1u);
+  }
+  q = (uint64_t)(p - 1) >> 2;
+  ctr[0] = (uint32_t)q;
+  ctr[1] = (uint32_t)(q >> 32);
+  ctr[2] = s->trial_lo;
+  ctr[3] = s->stream_id;
+  oracle_philox4x32_10(ctr, s->key, out);
+  return (uint64_t)out[(p - 1) & 3] < s->thr;
+}
+
+/* ------------------------------------------------------------------------ */
+/* SI: the pseudocode of App. F.4, literally.                     */
+/*   while total_toks < N: n = get_num_accepted(); total_toks += n + 1;      */
+/*                         total_cost += k * t_d + t_t                        */
+/* get_num_accepted() = number of leading accepted drafts among the next k   */
+/* (n = min{i | A_i = 0} - 1, capped at k).  Indicators beyond    */
+/* position N-1 may be read; the result does not depend on them (any read    */
+/* of A(p), p >= N, ends the loop whatever its value).                       */
+/* ------------------------------------------------------------------------ */
+static void si_literal(const indicator_stream *s, int32_t N, int32_t k, int64_t t_t, int64_t t_d,
+                       int32_t *iters_out, int64_t *cost_out, int64_t *si_hist) {
+  int64_t total_toks = 0;
+  int64_t total_cost = 0;
+  int32_t iters = 0;
+  while (total_toks < N) {
+    int32_t n = 0;
+    int64_t start = total_toks;
+    while (n < k && indicator(s, total_toks + n + 1) == 1) n += 1;
+    total_toks += n + 1;
+    total_cost += (int64_t)k * t_d + t_t;
+    iters += 1;
+    /* unbiased accepted-drafts histogram: only iterations whose whole k-draft
+       window lies in positions 1..N-1 (north_star's SI pin) */
+    if (si_hist && start + k + 1 <= N) si_hist[n] += 1;
+  }
+  *iters_out = iters;
+  *cost_out = total_cost;
+}
+
+/* ------------------------------------------------------------------------ */
+/* DSI: event simulation of Algorithm 1 + App. D lookahead       */
+/* on SP identical FIFO target servers.                           */
+/*                                                                            */
+/* Reading (R1-R4, R7-R10): within a segment that starts at time T  */
+/* with c tokens committed                                                    */
+/*  - thread 0, a target forward on the committed prefix, is requested at T  */
+/*    (Alg.1 line 2 at t=0; line 6's child C_{J+(m,m)} after a rejection);   */
+/*  - the single drafter never blocks: draft of position c+j is done at      */
+/*    T + j*t_d (Assumption 3);                                        */
+/*  - verification task b >= 1 is requested when its k drafts are done, at   */
+/*    T + b*k*t_d, while its first draft position c+(b-1)k+1 <= N-1;         */
+/*  - a target forward on the prefix ending at e yields the target's tokens  */
+/*    up to position e+1; thread 0 has e = c, thread b has e = c + b*k;      */
+/*  - positions are settled in order; a mismatch (A_p = 0) commits the        */
+/*    target's token p and terminates every other thread, queued task and    */
+/*    draft (Alg.1 lines 8 and 10), restarting at the completion time;       */
+/*  - the run ends when position N is settled (Alg.1 line 17 returns only    */
+/*    from a target thread).                                       */
+/* Events at equal times: server release (TARGET_DONE) before claims         */
+/* (REQUEST); R8.                                                   */
+/* ------------------------------------------------------------------------ */
+enum { EV_TARGET_DONE = 0, EV_REQUEST = 1 };
+
+typedef struct {
+  int64_t time;
+  int32_t cls;
+  int64_t b;      /* thread index within the segment */
+  int64_t epoch;  /* segment the event belongs to (stale => cancelled) */
+} event;
+
+typedef struct {
+  event *v;
+  size_t n, cap;
+} heap;
+
+static int ev_less(const event *x, const event *y) {
+  if (x->time != y->time) return x->time < y->time;
+  if (x->cls != y->cls) return x->cls < y->cls;
+  return x->b < y->b;
+}
+
+static int heap_push(heap *h, event e) {
+  size_t i;
+  if (h->n == h->cap) {
+    size_t nc = h->cap ? 2 * h->cap : 64;
+    event *nv = (event *)realloc(h->v, nc * sizeof(event));
+    if (!nv) return -1;
+    h->v = nv;
+    h->cap = nc;
+  }
+  i = h->n++;
+  h->v[i] = e;
+  while (i > 0) {
+    size_t parent = (i - 1) / 2;
+    if (!ev_less(&h->v[i], &h->v[parent])) break;
+    {
+      event t = h->v[i];
+      h->v[i] = h->v[parent];
+      h->v[parent] = t;
+    }
+    i = parent;
+  }
+  return 0;
+}
+
+static event heap_pop(heap *h) {
+  event top = h->v[0];
+  size_t i = 0;
+  h->v[0] = h->v[--h->n];
+  for (;;) {
+    size_t l = 2 * i + 1, r = l + 1, s = i;
+    if (l < h->n && ev_less(&h->v[l], &h->v[s])) s = l;
+    if (r < h->n && ev_less(&h->v[r], &h->v[s])) s = r;
+    if (s == i) break;
+    {
+      event t = h->v[i];
+      h->v[i] = h->v[s];
+      h->v[s] = t;
+    }
+    i = s;
+  }
+  return top;
+}
+
+typedef struct {
+  int64_t *v;
+  size_t head, tail, cap;
+} fifo;
+
+static int fifo_push(fifo *q, int64_t b) {
+  if (q->tail == q->cap) {
+    size_t nc = q->cap ? 2 * q->cap : 64;
+    int64_t *nv = (int64_t *)realloc(q->v, nc * sizeof(int64_t));
+    if (!nv) return -1;
+    q->v = nv;
+    q->cap = nc;
+  }
+  q->v[q->tail++] = b;
+  return 0;
+}
+
+static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_t SP, int64_t t_t,
+                         int64_t t_d, oracle_trial_out *out) {
+  heap h = {0, 0, 0};
+  fifo q = {0, 0, 0, 0};
+  int64_t T = 0;   /* segment start time */
+  int64_t c = 0;   /* committed tokens */
+  int64_t epoch = 0;
+  int32_t segments = 0, peak_busy = 0, max_queue = 0, forwards = 0;
+  int rc = -1;
+
+  for (;;) { /* one iteration per segment */
+    int64_t r = c + 1;          /* next unresolved position */
+    int64_t next_done = 0;      /* threads must complete in index order */
+    int32_t busy = 0;
+    int64_t b;
+    int restarted = 0;
+    epoch += 1;
+    segments += 1;
+    q.head = q.tail = 0;        /* cancelled tasks leave the queue */
+
+    h.n = 0; /* cancellation: every pending thread, task and draft is dropped */
+    if (heap_push(&h, (event){T, EV_REQUEST, 0, epoch})) goto done;
+
+    while (!restarted) {
+      event e;
+      if (h.n == 0) goto done; /* cannot happen: position N is always settled */
+      e = heap_pop(&h);
+      if (e.epoch != epoch) continue; /* cancelled thread / task */
+      if (e.cls == EV_REQUEST) {
+        /* the drafter keeps drafting: task b+1 is requested once its k drafts
+           are done, while its first draft position c+b*k+1 is <= N-1 */
+        b = e.b + 1;
+        if (c + (b - 1) * (int64_t)k + 1 <= (int64_t)N - 1)
+          if (heap_push(&h, (event){T + b * (int64_t)k * t_d, EV_REQUEST, b, epoch})) goto done;
+        if (busy < SP) {
+          busy += 1;
+          forwards += 1;
+          if (busy > peak_busy) peak_busy = busy;
+          if (heap_push(&h, (event){e.time + t_t, EV_TARGET_DONE, e.b, epoch})) goto done;
+        } else {
+          if (fifo_push(&q, e.b)) goto done;
+          if ((int32_t)(q.tail - q.head) > max_queue) max_queue = (int32_t)(q.tail - q.head);
+        }
+      } else { /* EV_TARGET_DONE */
+        int64_t hi, p;
+        busy -= 1;
+        if (q.head < q.tail) { /* FIFO: the head of the queue starts now */
+          int64_t nb = q.v[q.head++];
+          busy += 1;
+          forwards += 1;
+          if (busy > peak_busy) peak_busy = busy;
+          if (heap_push(&h, (event){e.time + t_t, EV_TARGET_DONE, nb, epoch})) goto done;
+        }
+        if (e.b != next_done) goto done; /* assertion: completion in index order */
+        next_done += 1;
+        hi = (e.b == 0) ? c + 1 : c + e.b * (int64_t)k + 1;
+        for (p = r; p <= hi; p++) {
+          if (p == N) { /* the N-th token is committed: L_DSI */
+            out->dsi = e.time;
+            rc = 0;
+            goto done;
+          }
+          /* assertion: the draft of position p exists by now (t_d <= t_t) */
+          if (T + (p - c) * t_d > e.time) goto done;
+          if (indicator(s, p) == 0) { /* rejection: restart from the target's token */
+            T = e.time;
+            c = p;
+            restarted = 1;
+            break;
+          }
+        }
+        if (!restarted) r = hi + 1;
+      }
+    }
+  }
+done:
+  out->dsi_segments = segments;
+  out->dsi_peak_busy = peak_busy;
+  out->dsi_max_queue = max_queue;
+  out->dsi_forwards = forwards;
+  free(h.v);
+  free(q.v);
+  return rc;
+}
+
+static int valid(const oracle_config *cfg) {
+  if (!cfg) return 0;
+  if (cfg->n_tokens < 1 || cfg->lookahead < 1 || cfg->sp_degree < 1) return 0;
+  if (cfg->t_drafter < 1 || cfg->t_target < cfg->t_drafter) return 0; /* Assumption 2 */
+  if (!(cfg->accept_rate >= 0.0 && cfg->accept_rate <= 1.0)) return 0;
+  return 1;
+}
+
+int oracle_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pattern,
+                 oracle_trial_out *out, int64_t *si_hist, int64_t *seg_hist) {
+  indicator_stream s;
+  int32_t N, p, last_zero = 0;
+  if (!valid(cfg) || !out) return -1;
+  if (pattern && cfg->n_tokens > 33) return -1;
+  N = cfg->n_tokens;
+  memset(out, 0, sizeof(*out));
+  s.key[0] = (uint32_t)seed;
+  s.key[1] = (uint32_t)(seed >> 32);
+  s.trial_lo = (uint32_t)trial;
+  s.stream_id = cfg->stream_id;
+  s.thr = oracle_threshold(cfg->accept_rate);
+  s.pattern = pattern;
+  s.pattern_bits = trial;
+
+  /* per-trial counts over positions 1..N-1 (position N has no indicator) */
+  out->m = 1;
+  for (p = 1; p <= N - 1; p++) {
+    if (indicator(&s, p)) {
+      out->acc += 1;
+    } else {
+      out->m += 1;
+      if (seg_hist) seg_hist[(p - last_zero) < 63 ? (p - last_zero) : 63] += 1;
+      last_zero = p;
+    }
+  }
+  if (seg_hist) seg_hist[(N - last_zero) < 63 ? (N - last_zero) : 63] += 1;
+
+  out->nonsi = (int64_t)N * cfg->t_target;
+  si_literal(&s, N, cfg->lookahead, cfg->t_target, cfg->t_drafter, &out->iters, &out->si, si_hist);
+  if (dsi_event_sim(&s, N, cfg->lookahead, cfg->sp_degree, cfg->t_target, cfg->t_drafter, out))
+    return -1;
+  if (out->dsi_segments != out->m) return -1;
+  return 0;
+}
+
+int oracle_run(const oracle_config *cfg, uint64_t seed, uint64_t first, uint64_t count,
+               int pattern, oracle_sums *sums,
+               int32_t *acc, int32_t *m, int32_t *iters, int64_t *si, int64_t *dsi,
+               int64_t *si_hist, int64_t *seg_hist) {
+  uint64_t i;
+  if (!sums) return -1;
+  for (i = 0; i < count; i++) {
+    oracle_trial_out o;
+    if (oracle_trial(cfg, seed, first + i, pattern, &o, si_hist, seg_hist)) return -1;
+    if (acc) acc[i] = o.acc;
+    if (m) m[i] = o.m;
+    if (iters) iters[i] = o.iters;
+    if (si) si[i] = o.si;
+    if (dsi) dsi[i] = o.dsi;
+    sums->trials += 1;
+    sums->sum_acc += o.acc;
+    sums->sum_m += o.m;
+    sums->sum_iters += o.iters;
+    sums->sum_si += o.si;
+    sums->sum_dsi += o.dsi;
+    sums->sumsq_si += (uint64_t)o.si * (uint64_t)o.si;
+    sums->sumsq_dsi += (uint64_t)o.dsi * (uint64_t)o.dsi;
+    sums->n_dsi_gt_nonsi += o.dsi > o.nonsi;
+    sums->n_dsi_gt_si += o.dsi > o.si;
+  }
+  return 0;
+}

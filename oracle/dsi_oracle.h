@@ -1,0 +1,87 @@
+/*
+ * dsi_oracle.h -- the CPU oracle of the DSI Monte Carlo latency simulator.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * The product path (include/dsi_sim.h, paper_2405_14105_b200/) never links,
+ * imports or executes anything under oracle/, and the oracle shares no code
+ * with it (no headers, no helpers, no tables).
+ *
+ * What it computes, for one configuration (target latency t_t, drafter latency
+ * t_d, acceptance rate a, lookahead k, SP degree, N tokens) and one trial:
+ *   - the acceptance indicators A_1..A_{N-1} (paper P:434: i.i.d.
+ *     Bernoulli(a) per draft token) drawn from a Philox4x32-10 stream;
+ *   - non-SI latency  N*t_t;
+ *   - SI latency by the literal pseudocode loop;
+ *   - DSI latency by a literal event simulation of Algorithm 1
+ *     with the lookahead generalisation of Appendix D on SP
+ *     FIFO target servers.
+ * Times are integer ticks.  See DESIGN.md "Readings" for every place where the
+ * paper is silent and the reading adopted (R1..R22 of SURVEY.md 8(c).4).
+ */
+#ifndef DSI_ORACLE_H
+#define DSI_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int64_t  t_target;     /* target forward latency t_2, integer ticks >= 1      */
+  int64_t  t_drafter;    /* drafter forward latency t_1, 1 <= t_d <= t_t ticks  */
+  double   accept_rate;  /* a in [0,1]                                          */
+  int32_t  lookahead;    /* k >= 1                                              */
+  int32_t  sp_degree;    /* SP >= 1 target servers                              */
+  int32_t  n_tokens;     /* N >= 1                                              */
+  uint32_t stream_id;    /* Philox counter word 3                               */
+} oracle_config;
+
+typedef struct {
+  int32_t acc;       /* #{p in 1..N-1 : A_p = 1}                            */
+  int32_t m;         /* #segments = #rejections in 1..N-1 + 1              */
+  int32_t iters;     /* SI iterations I (= SI target forwards)             */
+  int64_t nonsi;     /* N * t_t                                            */
+  int64_t si;        /* SI latency, ticks                                  */
+  int64_t dsi;       /* DSI latency, ticks                                 */
+  /* debug counters of the DSI event simulation */
+  int32_t dsi_segments;        /* restarts + 1, must equal m                 */
+  int32_t dsi_peak_busy;       /* max concurrently busy target servers       */
+  int32_t dsi_max_queue;       /* max FIFO queue length (0 <=> never waited) */
+  int32_t dsi_forwards;        /* target forwards started                    */
+} oracle_trial_out;
+
+typedef struct {
+  uint64_t trials;
+  int64_t  sum_acc, sum_m, sum_iters;
+  int64_t  sum_si, sum_dsi;
+  uint64_t sumsq_si, sumsq_dsi;
+  int64_t  n_dsi_gt_nonsi, n_dsi_gt_si;
+} oracle_sums;
+
+/* Philox4x32-10 block function (Salmon et al., SC'11, "Parallel random
+ * numbers: as easy as 1, 2, 3").  ctr[4], key[2] -> out[4]. */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+/* Bernoulli threshold thr = floor(a * 2^32) in [0, 2^32]; A_p = [u_p < thr]. */
+uint64_t oracle_threshold(double a);
+
+/* One trial.  pattern != 0: A_p = bit (p-1) of `trial` (enumeration mode, N <= 33).
+ * si_hist (k+1 bins, may be NULL): SI accepted-drafts-per-iteration counts,
+ *   only iterations whose k-draft window lies in positions <= N-1.
+ * seg_hist (64 bins, may be NULL): segment lengths g, bin min(g, 63).
+ * Returns 0, or -1 on invalid input / internal assertion failure. */
+int oracle_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pattern,
+                 oracle_trial_out *out, int64_t *si_hist, int64_t *seg_hist);
+
+/* Trials first..first+count-1: optional per-trial arrays (may be NULL),
+ * sums accumulated into *sums (zero it first).  Returns 0 or -1. */
+int oracle_run(const oracle_config *cfg, uint64_t seed, uint64_t first, uint64_t count,
+               int pattern, oracle_sums *sums,
+               int32_t *acc, int32_t *m, int32_t *iters, int64_t *si, int64_t *dsi,
+               int64_t *si_hist, int64_t *seg_hist);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

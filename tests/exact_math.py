@@ -1,0 +1,96 @@
+"""Exact-math pins for the DSI latency models (test infrastructure, Python fractions).
+
+Nothing here is imported by the product or by the oracle.  These are derived
+closed forms that pin both of them from outside:
+
+* Segments.  The rejected positions z_1 < ... < z_{m-1} among 1..N-1 cut a trial
+  into segments g_s = z_s - z_{s-1} (z_0 = 0, z_m = N).  Every segment starts with
+  all servers free (a rejection terminates every thread, Alg. 1 lines 8/10,
+  P:128-130), so its DSI cost depends on g only.
+* DSI segment cost (Alg. 1 P:112-142 + App. D, R1-R10):
+  thread b (b = 0 on the committed prefix, b >= 1 after b*k drafts) is requested
+  at b*k*t_d; with SP FIFO servers and equal service t_t it starts at
+  S(b) = max(b*k*t_d, S(b-SP) + t_t) = max(b k t_d, (b mod SP) k t_d + floor(b/SP) t_t);
+  position j of a segment is settled by thread ceil((j-1)/k), hence
+  C(g) = t_t + S(ceil((g-1)/k)).
+* SI: an iteration ends at min(next zero, start+k+1), so
+  I = sum_s ceil(g_s/(k+1)) and L_SI = I (k t_d + t_t).
+* Expected number of segments of length g (i.i.d. Bernoulli(a)):
+  h(g) = (1-a) a^(g-1) [2 + (1-a)(N-1-g)] for g <= N-1, h(N) = a^(N-1).
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+from itertools import product
+
+
+def segments(A, N):
+    """Segment lengths of an indicator vector A[0..N-2] (A[p-1] = A_p)."""
+    out, last = [], 0
+    for p in range(1, N):
+        if A[p - 1] == 0:
+            out.append(p - last)
+            last = p
+    out.append(N - last)
+    return out
+
+
+def S(b, k, t_d, t_t, sp):
+    return max(b * k * t_d, (b % sp) * k * t_d + (b // sp) * t_t)
+
+
+def C(g, k, t_d, t_t, sp):
+    b = -(-(g - 1) // k)
+    return t_t + S(b, k, t_d, t_t, sp)
+
+
+def closed_form(A, N, k, t_d, t_t, sp):
+    """Per-trial (acc, m, I, L_SI, L_DSI, L_non) from the closed form."""
+    gs = segments(A, N)
+    iters = sum(-(-g // (k + 1)) for g in gs)
+    return {"acc": sum(A[: N - 1]), "m": len(gs), "iters": iters,
+            "si": iters * (k * t_d + t_t), "dsi": sum(C(g, k, t_d, t_t, sp) for g in gs),
+            "nonsi": N * t_t}
+
+
+def h(g, N, a):
+    a = Fraction(a)
+    if g == N:
+        return a ** (N - 1)
+    return (1 - a) * a ** (g - 1) * (2 + (1 - a) * (N - 1 - g))
+
+
+def expectations(N, k, t_d, t_t, sp, a):
+    """Exact E[L_DSI], E[I], E[L_SI], E[m], E[acc] as Fractions."""
+    a = Fraction(a)
+    e_dsi = sum(h(g, N, a) * C(g, k, t_d, t_t, sp) for g in range(1, N + 1))
+    e_i = sum(h(g, N, a) * (-(-g // (k + 1))) for g in range(1, N + 1))
+    return {"dsi": e_dsi, "iters": e_i, "si": e_i * (k * t_d + t_t),
+            "m": 1 + (1 - a) * (N - 1), "acc": a * (N - 1), "nonsi": Fraction(N * t_t)}
+
+
+def enumerate_expectations(N, a, per_pattern):
+    """E[f] by brute force over all 2^(N-1) patterns with weights a^acc (1-a)^(N-1-acc).
+
+    per_pattern(A) -> dict of numbers; returns dict of Fractions."""
+    a = Fraction(a)
+    tot = {}
+    for A in product((0, 1), repeat=N - 1):
+        acc = sum(A)
+        w = a ** acc * (1 - a) ** (N - 1 - acc)
+        for key, v in per_pattern(list(A)).items():
+            tot[key] = tot.get(key, Fraction(0)) + w * v
+    return tot
+
+
+def pattern_index(A):
+    """Trial index whose bits are the indicators (enumeration mode: A_p = bit p-1)."""
+    return sum(int(v) << i for i, v in enumerate(A))
+
+
+def si_tokens_per_iteration(a, k):
+    """E[n+1] = (1 - a^(k+1)) / (1 - a): truncated geometric."""
+    a = Fraction(a)
+    if a == 1:
+        return Fraction(k + 1)
+    return (1 - a ** (k + 1)) / (1 - a)
