@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the DSI Monte Carlo latency simulator (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3] [--impl ours|reference]
+
+A step is one full pass of the hot path over the workload: dsi_sim_run (Philox ->
+Bernoulli -> segment walk -> SI/DSI latencies -> per-config moments) followed by
+dsi_sim_reduce (NCCL all-reduce across ranks, D2H, FP64 means).  The default
+workload is BASELINE configs[2], the paper's heatmap: 100 drafter
+latencies x 101 acceptance rates x k = 1..200 at SP 7, N = 100, 1e4 trials per
+point = 2.02e6 configs, 2.02e12 trial-tokens.  Metric: simulated trial-tokens/s.
+
+N > 1 is launched with torch.distributed.run; each rank simulates a cost-balanced
+contiguous share of the (config, trial-tile) units and the per-config integer
+moments are summed with one NCCL all-reduce inside dsi_sim_reduce.  Total work is
+fixed as N grows, so the line reports "scaling": "strong".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2405_14105_b200 import workloads as W  # noqa: E402
+
+METRIC = "simulated trial-tokens/sec"
+UNIT = "trial-tokens/s"
+SM_COUNT = 148
+LANES_PER_SM_CLK = 4 * 32  # 4 SMSPs x 32 lanes issue one thread-instruction each per clock
+
+
+def workload(name: str, min_lookahead):
+    if name == "cfg1":
+        return W.cfg1()
+    if name == "cfg2":
+        return W.cfg2()
+    if name == "cfg3":
+        return W.cfg3()
+    if name == "cfg3-fast":
+        return W.cfg3(k_max=20)
+    if name == "cfg4":
+        return W.cfg4()
+    if name == "cfg5":
+        return W.cfg5(min_lookahead)
+    raise SystemExit(f"unknown workload {name}")
+
+
+WORKLOAD_DESC = {
+    "cfg1": "BASELINE configs[0]: single point t_t=1.0 t_d=0.1 a=0.8 k=5 SP=2 N=50, 1e3 trials",
+    "cfg2": "BASELINE configs[1]: Table-2 pairs (P:258-267) x k{1,5,10}, SP=8, N=100, 1e5 trials",
+    "cfg3": "BASELINE configs[2]: heatmap t_d 0.01..1.00 x a 0.00..1.00 x k 1..200, SP=7, N=100, 1e4 trials",
+    "cfg3-fast": "heatmap with k 1..20 (BASELINE configs[2] fast variant)",
+    "cfg4": "BASELINE configs[3]: k 1..20 x SP 2..8 at t_d=0.1 a=0.8, N=500, 1e5 trials",
+    "cfg5": "BASELINE configs[4]: 10100 heatmap cells, k=Eq.1 min_lookahead, SP=7, N=1000, 1e5 trials",
+}
+
+
+def trial_tokens(cfgs) -> int:
+    return int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"].astype(np.int64)))
+
+
+def alg_instructions(cfgs) -> float:
+    """Algorithmic thread-instructions of one pass: per trial-token
+    10 (Philox4x32-10: 10 rounds x (2 mul-wide + 2 xor) / 4 words) + 1 (Bernoulli compare)
+    + 10 per rejection (segment walk + SI/DSI cost), (1 - a) rejections per token."""
+    tt = cfgs["n_trials"].astype(np.float64) * cfgs["n_tokens"].astype(np.float64)
+    return float(np.sum(tt * (11.0 + 10.0 * (1.0 - cfgs["accept_rate"]))))
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle baseline
+def run_oracle_sample(cfgs, tick, seconds: float):
+    import oracle as O
+
+    sub = W.subsample(cfgs, 100)
+    ocfgs = [O.Config(O.ticks(float(r["t_target"]), tick), O.ticks(float(r["t_drafter"]), tick),
+                      float(r["accept_rate"]), int(r["lookahead"]), int(r["sp_degree"]),
+                      int(r["n_tokens"]), int(r["stream_id"])) for r in sub]
+    # calibrate: 2 trials of each sampled config
+    t0 = time.perf_counter()
+    for c in ocfgs:
+        O.run(c, W.SEED, 0, 2, per_trial=False)
+    per_trial = (time.perf_counter() - t0) / (2 * len(ocfgs))
+    S = int(max(1, min(min(int(r["n_trials"]) for r in sub), seconds / (per_trial * len(ocfgs)))))
+    t0 = time.perf_counter()
+    tt = 0
+    for c, r in zip(ocfgs, sub):
+        O.run(c, W.SEED, 0, S, per_trial=False)
+        tt += S * int(r["n_tokens"])
+    dt = time.perf_counter() - t0
+    return {"value": tt / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {S} trials of {len(ocfgs)} evenly spaced configs of the workload "
+                      f"({tt} trial-tokens, {dt:.1f} s, single-threaded C oracle: literal SI loop + "
+                      f"DSI event simulation)"}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as O
+    O.build()
+    cfgs, tick = workload(args.workload, _min_lookahead_plain)
+    per_step = max(1.0, args.reference_seconds / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        run_oracle_sample(cfgs, tick, per_step / 4)
+    vals = []
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = run_oracle_sample(cfgs, tick, per_step)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/int64",
+            "data": "synthetic", "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": last["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def _min_lookahead_plain(t_t, t_d, sp):
+    k = 1
+    while -(-t_t // (k * t_d)) > sp:
+        k += 1
+    return k
+
+
+# ----------------------------------------------------------------------------- our arm
+def ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_14105_b200 import dsi_sim as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfgs, tick = workload(args.workload, D.dsi_min_lookahead)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: int) -> int:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return int(t.item())
+
+    nccl_id = None
+    if world > 1:
+        obj = [D.dsi_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    kw = dict(tick=tick, seed=W.SEED, device=local, rank=rank, world=world, nccl_id=nccl_id)
+
+    t_create = time.perf_counter()
+    sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING, **kw)
+    create_s = time.perf_counter() - t_create
+    stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    for _ in range(args.warmup):
+        sim.run()
+        sim.reduce()
+
+    step_ms, kernel_ms = [], []
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            torch.cuda.synchronize()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            sim.run()
+            res = sim.reduce()
+            ev1.record(stream)
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            kernel_ms.append(sim.kernel_ms())
+            launches += sim.launches()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    barrier()
+    total_ms = max_over_ranks(sum(step_ms))
+    kern_ms = max_over_ranks(statistics.mean(kernel_ms))
+    launches = sum_over_ranks(launches)
+    tt = trial_tokens(cfgs)
+    value = tt * args.steps / (total_ms / 1000.0)
+
+    # e2e through the public API with host buffers: update (validate + pinned H2D of the
+    # config table) + run + reduce (all-reduce + D2H of the moments + FP64 finalise)
+    h2d, d2h = sim.io_bytes()
+    sim.update(cfgs)
+    sim.run()
+    sim.reduce()
+    barrier()
+    torch.cuda.synchronize()
+    e2e_s = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        sim.update(cfgs)
+        sim.run()
+        sim.reduce()
+        e2e_s.append(time.perf_counter() - t0)
+    barrier()
+    e2e_total = max_over_ranks(sum(e2e_s))
+    e2e_value = tt * args.steps / e2e_total
+
+    peaks = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_instr = SM_COUNT * LANES_PER_SM_CLK * sm_max * 1e6  # thread-instr/s per GPU
+    # dominant kernel = the trial kernel; algorithmic instructions of this rank's share
+    achieved = alg_instructions(cfgs) / world / (kern_ms / 1000.0)
+    clk = clocks.summary()
+    prof = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "latest_ncu_summary.json")) as f:
+            prof = json.load(f)
+    except OSError:
+        pass
+    traffic = prof.get("dram_bytes_per_launch") if prof.get("workload") == args.workload else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        O.build()
+        cpu = run_oracle_sample(cfgs, tick, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32/int64", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload],
+                       "configs": int(cfgs.size), "trials": int(cfgs["n_trials"].sum()),
+                       "trial_tokens_per_step": tt, "tick": tick, "seed": W.SEED,
+                       "l2": "flushed between timed steps (256 MiB memset)", "parallelism": f"dp{world}"},
+            "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_instr / 1e9,
+                         "unit": "Ginstr/s", "frac": achieved / peak_instr, "traffic": traffic,
+                         "kernel": "dsi_trial_kernel", "kernel_ms": kern_ms,
+                         "kernel_share_of_step": kern_ms / (total_ms / args.steps),
+                         "peak_source": f"148 SM x 4 SMSP x 32 lanes x sm_max_mhz {sm_max:.0f} "
+                                        "(MEASURED_PEAKS.json) = issue slots; algorithmic "
+                                        "instructions per trial-token 11 + 10(1-a)",
+                         "frac_at_measured_clock": (achieved / (peak_instr * clk["sm_mhz"] / sm_max)
+                                                    if clk.get("sm_mhz") else None)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "create_s": create_s,
+            "wall_s_timed": wall,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOAD_DESC))
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--reference-seconds", type=float, default=90.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

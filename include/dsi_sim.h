@@ -1,0 +1,202 @@
+/*
+ * dsi_sim.h -- C ABI of the B200-native Monte Carlo latency simulator of
+ * Distributed Speculative Inference (DSI, arXiv 2405.14105).
+ *
+ * For every grid point (target latency, drafter latency, acceptance rate,
+ * lookahead k, SP degree, N tokens) the library runs n_trials independent
+ * trials on sm_100a GPUs.  One trial draws the acceptance indicators
+ * A_1..A_{N-1} (i.i.d. Bernoulli(a) per draft token)
+ * from a counter-based Philox4x32-10 stream and computes three latencies in
+ * integer ticks:
+ *   non-SI  N * t_target
+ *   SI      the draft-then-verify loop of App. F.4
+ *   DSI     Algorithm 1 with the App. D lookahead:
+ *           a verification task every k drafts on SP FIFO target servers,
+ *           a rejection terminates all threads and restarts.
+ * Per configuration it returns exact integer sums over trials and FP64 means.
+ * DESIGN.md lists the readings of the paper this ABI commits to (R1-R22).
+ *
+ * Random-number contract (bit-exact, any device count and partition):
+ *   key = (seed & 0xffffffff, seed >> 32)
+ *   counter = (q, 0, trial, stream_id), q = (p-1) >> 2, output word (p-1) & 3
+ *   A_p = [word < floor(a * 2^32)]   (a = 1 always accepts, a = 0 never)
+ * trial runs over 0..n_trials-1 of its configuration.
+ *
+ * Conventions
+ *  - Every function returns dsi_status; no C++ exception crosses the ABI.
+ *  - A failing call writes nothing to caller-owned outputs.
+ *  - All validation happens in dsi_sim_create, before any device work.
+ *  - dsi_sim_create copies cfg[]; the library owns all device memory, streams
+ *    and NCCL communicators until dsi_sim_destroy.  Output arrays are
+ *    caller-owned host memory.
+ *  - A handle is used by one host thread at a time; handles are independent.
+ *  - Eq. 1 violation is legal (FIFO queueing is simulated, R7)
+ *    unless DSI_F_STRICT_EQ1 is set.
+ */
+#ifndef DSI_SIM_H
+#define DSI_SIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSI_ABI_VERSION 1u
+
+typedef enum {
+  DSI_OK = 0,
+  DSI_E_NULL = 1,       /* a required pointer was NULL                                   */
+  DSI_E_RANGE = 2,      /* a not in [0,1]; k < 1; SP < 1; N not in [1, 32768]; n_trials not
+                           in [1, 2^32]; latency <= 0 or not finite; t_drafter > t_target
+                           (Assumption 2); bad option field; n_cfg == 0        */
+  DSI_E_TICK = 3,       /* latency / tick not within 1e-9 (relative) of an integer >= 1  */
+  DSI_E_OVERFLOW = 4,   /* N*(k*t_d + t_t) >= 2^31 ticks, or n_trials*bound^2 >= 2^64     */
+  DSI_E_STRICT_EQ1 = 5, /* DSI_F_STRICT_EQ1 set and ceil(t_t/(k*t_d)) > SP                */
+  DSI_E_DEVICE = 6,     /* CUDA error, or fewer usable sm_100 devices than requested      */
+  DSI_E_COMM = 7,       /* NCCL could not be loaded or an NCCL call failed                */
+  DSI_E_STATE = 8,      /* call order violated (reduce before run, trials without
+                           DSI_F_PER_TRIAL, hist without DSI_F_HIST, ...)                 */
+  DSI_E_NOMEM = 9       /* host or device allocation failed                               */
+} dsi_status;
+
+/* Option flags */
+#define DSI_F_PER_TRIAL 0x1u  /* keep per-trial records {acc, m, I, L_SI, L_DSI} (test mode) */
+#define DSI_F_HIST 0x2u       /* per-config histograms: segment lengths (64 bins, last = >=63)
+                                 and SI accepted drafts per iteration (k+1 bins, iterations
+                                 whose k-draft window lies in 1..N-1 only)                   */
+#define DSI_F_PATTERN 0x4u    /* enumeration mode: A_p = bit (p-1) of the trial index; N <= 33 */
+#define DSI_F_STRICT_EQ1 0x8u /* reject configs violating Eq. 1                               */
+#define DSI_F_TIMING 0x10u    /* record CUDA events around the trial kernels of each run      */
+
+/* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
+typedef struct {
+  double t_target;    /* target forward latency (t_2, "Target Latency"), user units > 0   */
+  double t_drafter;   /* drafter forward latency (t_1), 0 < t_drafter <= t_target          */
+  double accept_rate; /* a in [0,1]: P(draft token accepted), i.i.d. per token             */
+  int32_t lookahead;  /* k >= 1: drafts per verification task (App. D)               */
+  int32_t sp_degree;  /* SP >= 1: concurrent target servers                        */
+  int32_t n_tokens;   /* N in [1, 32768]: tokens to generate                               */
+  uint32_t stream_id; /* Philox counter word 3; equal ids => common random numbers         */
+  uint64_t n_trials;  /* T in [1, 2^32]                                                    */
+} dsi_config;         /* 48 bytes */
+
+typedef struct {
+  uint32_t abi_version;   /* must equal DSI_ABI_VERSION                                     */
+  uint32_t flags;         /* DSI_F_* */
+  double tick;            /* time quantum in latency units, > 0 (e.g. 0.01 relative, 0.1 ms) */
+  uint64_t seed;          /* Philox key                                                     */
+  int32_t device;         /* first CUDA device ordinal of this process (e.g. LOCAL_RANK)    */
+  int32_t n_devices;      /* 1..8 devices [device, device+n) driven by this process         */
+  int32_t rank, world;    /* multi-process mode: this process is rank of world (world >= 1) */
+  const uint8_t *nccl_id; /* 128-byte ncclUniqueId shared by all ranks when the total device
+                             count world*n_devices > 1; NULL otherwise.  Obtain it with
+                             dsi_nccl_unique_id on one rank and broadcast it.              */
+  int32_t n_shards;       /* 0 or 1: normal.  > 1 (test only, single device): split the work
+                             into n_shards cost-balanced shards run back to back on one
+                             device, exercising the same partition code as multi-GPU.     */
+  int32_t block_threads;  /* 0 = default (128); else 32..256, multiple of 32               */
+  void *stream;           /* cudaStream_t for the first device, or NULL (library-owned)    */
+} dsi_options;
+
+/* Per configuration, after dsi_sim_reduce.  Integers are exact; doubles derive from them. */
+typedef struct {
+  uint64_t trials;
+  int64_t t_target_ticks, t_drafter_ticks;
+  int64_t nonsi_ticks;              /* N * t_t (per trial, constant)                       */
+  int64_t sum_si_ticks, sum_dsi_ticks;
+  uint64_t sumsq_si_ticks, sumsq_dsi_ticks;
+  int64_t sum_si_iters;             /* sum of I = SI target forwards                       */
+  int64_t sum_accepts;              /* sum of acc = #{p <= N-1 : A_p = 1}                  */
+  int64_t sum_segments;             /* sum of m = #rejections + 1                          */
+  int64_t n_dsi_gt_nonsi;           /* trials with L_DSI > L_non (Thm 1 counter)           */
+  int64_t n_dsi_gt_si;              /* trials with L_DSI > L_SI  (Thm 2 counter)           */
+  uint64_t threshold;               /* floor(a * 2^32)                                     */
+  int32_t eq1_feasible;             /* ceil(t_t/(k t_d)) <= SP  (Eq. 1)                    */
+  int32_t min_lookahead;            /* smallest k with ceil(t_t/(k t_d)) <= SP             */
+  double mean_nonsi, mean_si, mean_dsi; /* user units: ((double)sum / (double)T) * tick    */
+  double std_si, std_dsi;           /* population std, user units, from the exact integer
+                                       numerator T*sumsq - sum^2 (128-bit)                  */
+} dsi_result;
+
+typedef struct dsi_sim dsi_sim; /* opaque handle */
+
+/* Validate options and configs, convert to ticks, plan shards, allocate device
+ * memory, upload the config table, initialise NCCL when world*n_devices > 1
+ * (collective: every rank must call it).  On error *out is set to NULL. */
+dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t n_cfg,
+                          dsi_sim **out);
+
+/* Replace the configuration values of an existing handle (same n_cfg, same
+ * n_trials per config; with DSI_F_HIST also the same min(k, N)).  Validates like
+ * create, waits for any previous run, then copies the table host -> device from
+ * pinned staging.  On error the handle keeps its previous configs. */
+dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg);
+
+/* Enqueue one full simulation on every device of this process (asynchronous). */
+dsi_status dsi_sim_run(dsi_sim *h);
+
+/* Wait for the run, sum the per-config integer moments across devices and ranks
+ * (one NCCL all-reduce), copy them to the host and derive FP64 means/std.
+ * n must equal n_cfg.  Blocking.  Every rank must call it. */
+dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n);
+
+/* Per-trial records of trials [first, first+count) of config cfg (needs
+ * DSI_F_PER_TRIAL, one device, world == 1).  Any output pointer may be NULL. */
+dsi_status dsi_sim_trials(dsi_sim *h, size_t cfg, uint64_t first, uint64_t count,
+                          int32_t *acc, int32_t *m, int32_t *iters, int32_t *si_ticks,
+                          int32_t *dsi_ticks);
+
+/* Histograms of config cfg after reduce (needs DSI_F_HIST).  seg_hist: 64 bins,
+ * bin g = segments of length g (bin 63 = length >= 63, bin 0 unused).
+ * si_hist: si_bins must be k+1; bin j = SI iterations with j accepted drafts. */
+dsi_status dsi_sim_hist(dsi_sim *h, size_t cfg, int64_t *seg_hist, int64_t *si_hist,
+                        size_t si_bins);
+
+/* CUDA stream of the i-th device of this handle (cudaStream_t as void*). */
+dsi_status dsi_sim_stream(dsi_sim *h, int32_t device_index, void **stream);
+
+/* Trial-kernel launches enqueued by the last dsi_sim_run on this process. */
+dsi_status dsi_sim_launches(dsi_sim *h, int32_t *launches);
+
+/* With DSI_F_TIMING: device time (ms) of the trial kernels of the last run on
+ * device_index, measured with CUDA events on the launching stream (blocks). */
+dsi_status dsi_sim_kernel_ms(dsi_sim *h, int32_t device_index, float *ms);
+
+/* Host<->device bytes moved per create+run+reduce on this process: the config
+ * table and unit prefix uploaded by create (h2d) and the per-config moments (and
+ * histograms) read back by reduce (d2h). */
+dsi_status dsi_sim_io_bytes(dsi_sim *h, uint64_t *h2d, uint64_t *d2h);
+
+/* Work units (config, trial tile) of this process: [first, first+count) of total. */
+dsi_status dsi_sim_units(dsi_sim *h, uint64_t *first, uint64_t *count, uint64_t *total);
+
+void dsi_sim_destroy(dsi_sim *h); /* NULL-safe */
+
+const char *dsi_status_str(dsi_status s);
+const char *dsi_sim_last_error(const dsi_sim *h); /* handle-owned; "" if none */
+const char *dsi_last_create_error(void);          /* thread-local message of the last failed
+                                                     dsi_sim_create                          */
+uint32_t dsi_abi_version(void);
+
+/* 128-byte NCCL unique id for multi-GPU runs (call on one rank, broadcast). */
+dsi_status dsi_nccl_unique_id(uint8_t id[128]);
+
+/* Pure planner helpers of Eq. 1, exact integers.
+ * Return -1 on invalid input (ticks < 1, sp < 1, k < 1). */
+int32_t dsi_min_lookahead(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t sp);
+int32_t dsi_required_processors(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k);
+int32_t dsi_eq1_feasible(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k, int32_t sp);
+
+/* Pure sharder (host only, no device): split per-unit costs into `parts`
+ * contiguous ranges of near-equal total cost.  cost_units[i] >= 0.
+ * bounds must hold parts+1 entries; bounds[0] = 0, bounds[parts] = n.
+ * Used by dsi_sim_create for devices x ranks x shards; exported for tests. */
+dsi_status dsi_shard_bounds(const double *cost_units, uint64_t n, int32_t parts,
+                            uint64_t *bounds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSI_SIM_H */

@@ -1,0 +1,77 @@
+// dsi_device.h -- layout shared by the host runtime (dsi_host.cpp) and the
+// sm_100a trial kernel (dsi_kernel.cu).  Internal: not part of the C ABI.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+namespace dsi {
+
+// Indicator mode of a configuration (uniform per block).
+enum : uint32_t {
+  MODE_STREAM = 0,      // Philox stream, A_p = [u < thr]
+  MODE_ALL_ACCEPT = 1,  // thr == 2^32: every draft accepted, no random numbers needed
+  MODE_ALL_REJECT = 2,  // thr == 0: every draft rejected, no random numbers needed
+};
+enum : uint32_t { CFG_NOQUEUE = 1u << 8 };  // S(b) = b*k*t_d (Eq. 1 holds or SP >= N)
+
+// One configuration in ticks, as the kernel reads it (64 bytes).
+struct alignas(16) DevCfg {
+  uint32_t thr;        // floor(a * 2^32) when mode == MODE_STREAM
+  uint32_t flags;      // mode (low byte) | CFG_NOQUEUE
+  int32_t n_tokens;    // N
+  int32_t k_eff;       // min(k, N): same ceil-divisions for every g <= N
+  int32_t sp_eff;      // min(SP, N): b <= N-1, so larger SP never queues
+  int32_t t_t;         // target latency, ticks
+  int32_t kd;          // k * t_d, ticks
+  int32_t si_cost;     // k * t_d + t_t: one SI iteration
+  uint32_t stream_id;  // Philox counter word 3
+  uint32_t m_si;       // ceil(2^32 / (k_eff+1))           : x / (k_eff+1)
+  uint32_t m_k_lo;     // ceil(2^32 / k_eff) mod 2^32       : x / k_eff
+  uint32_t m_k_hi;     //   ... and its bit 32 (k_eff == 1)
+  uint32_t m_sp_lo;    // ceil(2^32 / sp_eff) mod 2^32      : x / sp_eff
+  uint32_t m_sp_hi;
+  uint32_t si_hist_off;  // first SI-histogram bin of this config (DSI_F_HIST)
+  uint32_t pad;
+  uint64_t rec_off;      // first per-trial record of this config (DSI_F_PER_TRIAL)
+  uint64_t n_trials;
+};
+static_assert(sizeof(DevCfg) == 80, "DevCfg layout");
+
+// Per-config integer moments accumulated by the kernel (u64 each).
+enum Field : int {
+  F_M = 0,       // sum of segments m
+  F_I,           // sum of SI iterations I
+  F_I2,          // sum of I^2            (L_SI = I * si_cost)
+  F_DSI,         // sum of L_DSI
+  F_DSI2,        // sum of L_DSI^2
+  F_GT_NONSI,    // #trials with L_DSI > N t_t
+  F_GT_SI,       // #trials with L_DSI > L_SI
+  F_TRIALS,      // trials simulated (checks the partition covers every trial once)
+  NF
+};
+
+struct Keys {
+  uint32_t k0[10];  // key word 0 of rounds 0..9: seed_lo + r * 0x9E3779B9
+  uint32_t k1[10];  // key word 1 of rounds 0..9: seed_hi + r * 0xBB67AE85
+};
+
+struct LaunchParams {
+  const DevCfg *cfg;
+  const uint64_t *tile_prefix;  // n_cfg + 1: first unit of each config
+  uint32_t n_cfg;
+  uint32_t tile_trials;         // trials per unit (last unit of a config is ragged)
+  uint64_t unit_begin;          // first unit of this launch; block b runs unit_begin + b
+  unsigned long long *acc;      // n_cfg * NF
+  int32_t *rec_acc, *rec_m, *rec_iters, *rec_si, *rec_dsi;  // DSI_F_PER_TRIAL
+  unsigned long long *seg_hist;  // n_cfg * 64              (DSI_F_HIST)
+  unsigned long long *si_hist;   // sum over configs of (k_eff + 1)
+  Keys keys;
+};
+
+// Launch the trial kernel variant for (per_trial, hist, pattern) on `stream`
+// over units [p.unit_begin, p.unit_begin + n_units).  Returns a cudaError_t.
+// hist_smem: dynamic shared memory for DSI_F_HIST, (64 + max k_eff + 1) * 4 bytes.
+int launch_trial_kernel(const LaunchParams &p, uint64_t n_units, int block_threads,
+                        bool per_trial, bool hist, bool pattern, size_t hist_smem, void *stream);
+
+}  // namespace dsi

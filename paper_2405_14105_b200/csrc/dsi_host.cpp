@@ -1,0 +1,880 @@
+// dsi_host.cpp -- host runtime behind include/dsi_sim.h.
+//
+// Validation and tick conversion, Eq. 1 planner helpers, the cost-balanced
+// sharder, per-device state (streams, buffers, pinned staging of the config
+// table and results), the NCCL all-reduce of the per-config integer moments,
+// and FP64 finalisation.  All arithmetic of the method runs in dsi_kernel.cu;
+// this file only prepares inputs and combines exact integer sums.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only; libnccl is loaded with dlopen at first use
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dsi_sim.h"
+#include "dsi_device.h"
+
+using dsi::DevCfg;
+using dsi::LaunchParams;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+constexpr int kMaxTokens = 32768;  // keeps every magic division exact (x * d <= 2^32)
+constexpr uint64_t kMaxTrials = 1ull << 32;
+constexpr int kDefaultThreads = 128;
+
+// ----------------------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void *lib = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi &nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    // Reuse a libnccl already mapped into the process (e.g. torch's), else load one.
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.lib = h;
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+      api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
+               api.GroupStart && api.GroupEnd && api.GetErrorString;
+    }
+  }
+  return api;
+}
+
+// ----------------------------------------------------------------------------- helpers
+struct CfgTicks {
+  int64_t t_t, t_d, kd;
+  uint64_t thr;
+  int32_t k, sp, n;
+  uint32_t stream_id;
+  uint64_t trials;
+  double a;
+};
+
+// ceil(2^32 / d) split into low word and bit 32 (d >= 1).
+void magic(uint32_t d, uint32_t &lo, uint32_t &hi) {
+  const uint64_t m = ((1ull << 32) + d - 1) / d;
+  lo = (uint32_t)m;
+  hi = (uint32_t)(m >> 32);
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+template <class T>
+struct Pinned {  // page-locked host buffer (true async DMA for H2D/D2H)
+  T *p = nullptr;
+  size_t n = 0;
+  cudaError_t alloc(size_t count) {
+    release();
+    n = count;
+    return cudaMallocHost((void **)&p, std::max<size_t>(1, count) * sizeof(T));
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+// ----------------------------------------------------------------------------- handle
+struct DeviceState {
+  int ordinal = -1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  DevCfg *d_cfg = nullptr;
+  uint64_t *d_prefix = nullptr;
+  unsigned long long *d_acc = nullptr;
+  unsigned long long *d_red = nullptr;
+  unsigned long long *d_seg = nullptr, *d_seg_red = nullptr;
+  unsigned long long *d_si = nullptr, *d_si_red = nullptr;
+  int32_t *d_rec = nullptr;  // 5 arrays of total_trials
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ncclComm_t comm = nullptr;
+  std::vector<std::pair<uint64_t, uint64_t>> ranges;  // [begin, end) units, one per shard
+};
+
+struct dsi_sim {
+  dsi_options opt{};
+  size_t n_cfg = 0;
+  std::vector<CfgTicks> ticks;
+  Pinned<DevCfg> dev_cfg;                // staging of the device config table
+  std::vector<uint64_t> prefix;          // n_cfg + 1 units
+  uint64_t total_units = 0;
+  uint64_t total_trials = 0;
+  uint32_t tile_trials = 0;
+  int block_threads = kDefaultThreads;
+  size_t hist_smem = 0;
+  uint64_t si_bins_total = 0;
+  std::vector<DeviceState> dev;
+  Pinned<unsigned long long> host_acc, host_seg, host_si;  // D2H targets
+  bool ran = false, reduced = false;
+  int launches = 0;
+  std::string err;
+};
+
+namespace {
+
+dsi_status fail(dsi_sim *h, dsi_status s, const std::string &msg) {
+  if (h) h->err = msg; else g_create_error = msg;
+  return s;
+}
+
+dsi_status cuda_fail(dsi_sim *h, cudaError_t e, const char *what) {
+  return fail(h, e == cudaErrorMemoryAllocation ? DSI_E_NOMEM : DSI_E_DEVICE,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(h, call)                                  \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+  } while (0)
+
+dsi_status to_ticks(double x, double tick, int64_t *out) {
+  if (!std::isfinite(x) || x <= 0.0) return DSI_E_RANGE;
+  const double r = x / tick;
+  if (!(r < 9.0e18)) return DSI_E_OVERFLOW;
+  const int64_t t = std::llround(r);
+  if (t < 1 || std::fabs(r - (double)t) > 1e-9 * std::fabs(r)) return DSI_E_TICK;
+  *out = t;
+  return DSI_OK;
+}
+
+dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTicks &o,
+                   std::string &msg) {
+  char buf[256];
+  auto bad = [&](dsi_status s, const char *what) {
+    std::snprintf(buf, sizeof buf, "config %zu: %s", i, what);
+    msg = buf;
+    return s;
+  };
+  if (!(c.accept_rate >= 0.0 && c.accept_rate <= 1.0))
+    return bad(DSI_E_RANGE, "accept_rate must be in [0, 1]");
+  if (c.lookahead < 1) return bad(DSI_E_RANGE, "lookahead must be >= 1");
+  if (c.sp_degree < 1) return bad(DSI_E_RANGE, "sp_degree must be >= 1");
+  if (c.n_tokens < 1 || c.n_tokens > kMaxTokens)
+    return bad(DSI_E_RANGE, "n_tokens must be in [1, 32768]");
+  if (c.n_trials < 1 || c.n_trials > kMaxTrials)
+    return bad(DSI_E_RANGE, "n_trials must be in [1, 2^32]");
+  if ((opt.flags & DSI_F_PATTERN) && c.n_tokens > 33)
+    return bad(DSI_E_RANGE, "DSI_F_PATTERN needs n_tokens <= 33");
+  dsi_status s = to_ticks(c.t_target, opt.tick, &o.t_t);
+  if (s != DSI_OK) return bad(s, "t_target is not a positive whole number of ticks");
+  s = to_ticks(c.t_drafter, opt.tick, &o.t_d);
+  if (s != DSI_OK) return bad(s, "t_drafter is not a positive whole number of ticks");
+  if (o.t_d > o.t_t) return bad(DSI_E_RANGE, "t_drafter > t_target violates Assumption 2 (P:187-189)");
+  // every per-trial latency is <= N (k t_d + t_t) (kernel overflow bound)
+  const unsigned __int128 kd = (unsigned __int128)c.lookahead * (uint64_t)o.t_d;
+  const unsigned __int128 bound = (unsigned __int128)c.n_tokens * (kd + (uint64_t)o.t_t);
+  if (bound >= ((unsigned __int128)1 << 31))
+    return bad(DSI_E_OVERFLOW, "N*(k*t_drafter + t_target) must stay below 2^31 ticks");
+  if ((unsigned __int128)c.n_trials * bound * bound >= ((unsigned __int128)1 << 64))
+    return bad(DSI_E_OVERFLOW, "n_trials * bound^2 must stay below 2^64");
+  o.kd = (int64_t)kd;
+  if ((opt.flags & DSI_F_STRICT_EQ1) && ceil_div(o.t_t, o.kd) > c.sp_degree)
+    return bad(DSI_E_STRICT_EQ1, "Eq. 1 violated: ceil(t_t/(k t_d)) > SP");
+  o.a = c.accept_rate;
+  o.thr = (uint64_t)(c.accept_rate * 4294967296.0);  // exact: a * 2^32, then floor
+  o.k = c.lookahead;
+  o.sp = c.sp_degree;
+  o.n = c.n_tokens;
+  o.stream_id = c.stream_id;
+  o.trials = c.n_trials;
+  return DSI_OK;
+}
+
+DevCfg make_dev_cfg(const CfgTicks &t, bool pattern) {
+  DevCfg d{};
+  uint32_t mode = dsi::MODE_STREAM;
+  if (!pattern) {
+    if (t.thr >= (1ull << 32)) mode = dsi::MODE_ALL_ACCEPT;
+    else if (t.thr == 0) mode = dsi::MODE_ALL_REJECT;
+  }
+  const int32_t k_eff = std::min(t.k, t.n);
+  const int32_t sp_eff = std::min(t.sp, t.n);
+  const bool noqueue = (t.t_t <= (int64_t)sp_eff * t.kd) || sp_eff >= t.n;
+  d.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
+  d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u);
+  d.n_tokens = t.n;
+  d.k_eff = k_eff;
+  d.sp_eff = sp_eff;
+  d.t_t = (int32_t)t.t_t;
+  d.kd = (int32_t)t.kd;
+  d.si_cost = (int32_t)(t.kd + t.t_t);
+  d.stream_id = t.stream_id;
+  uint32_t hi;
+  magic((uint32_t)k_eff + 1u, d.m_si, hi);  // k_eff + 1 >= 2: hi == 0
+  magic((uint32_t)k_eff, d.m_k_lo, d.m_k_hi);
+  magic((uint32_t)sp_eff, d.m_sp_lo, d.m_sp_hi);
+  d.n_trials = t.trials;
+  return d;
+}
+
+// Relative cost of one trial-token: Philox (~10 instr) + compare (~1) + segment walk
+// (~10 instr per rejection, expected (1-a) per token), SURVEY 8(d).4.
+double unit_cost(const CfgTicks &t, uint64_t trials) {
+  return (double)trials * (double)t.n * (11.0 + 10.0 * (1.0 - t.a));
+}
+
+// Validate every config into ticks; on failure h->err names the config.
+dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n) {
+  for (size_t i = 0; i < n; ++i) {
+    std::string msg;
+    const dsi_status s = convert(h->opt, cfg[i], i, h->ticks[i], msg);
+    if (s != DSI_OK) return fail(h, s, msg);
+  }
+  return DSI_OK;
+}
+
+// Fill the pinned device-config staging table from h->ticks.
+void fill_dev_cfg(dsi_sim *h) {
+  const bool pattern = h->opt.flags & DSI_F_PATTERN;
+  uint64_t rec = 0, sib = 0;
+  for (size_t i = 0; i < h->n_cfg; ++i) {
+    DevCfg d = make_dev_cfg(h->ticks[i], pattern);
+    d.rec_off = rec;
+    rec += h->ticks[i].trials;
+    d.si_hist_off = (uint32_t)sib;
+    sib += (uint64_t)d.k_eff + 1;
+    h->dev_cfg.p[i] = d;
+  }
+}
+
+void free_device(DeviceState &d) {
+  if (d.ordinal < 0) return;
+  cudaSetDevice(d.ordinal);
+  if (d.comm && nccl().ok) nccl().CommDestroy(d.comm);
+  cudaFree(d.d_cfg);
+  cudaFree(d.d_prefix);
+  cudaFree(d.d_acc);
+  cudaFree(d.d_red);
+  cudaFree(d.d_seg);
+  cudaFree(d.d_seg_red);
+  cudaFree(d.d_si);
+  cudaFree(d.d_si_red);
+  cudaFree(d.d_rec);
+  if (d.ev0) cudaEventDestroy(d.ev0);
+  if (d.ev1) cudaEventDestroy(d.ev1);
+  if (d.own_stream && d.stream) cudaStreamDestroy(d.stream);
+  d = DeviceState{};
+}
+
+void free_handle(dsi_sim *h) {
+  for (auto &d : h->dev) free_device(d);
+  h->dev_cfg.release();
+  h->host_acc.release();
+  h->host_seg.release();
+  h->host_si.release();
+  delete h;
+}
+
+// Upload the staging table to every device (async on each device's stream).
+dsi_status upload(dsi_sim *h) {
+  for (auto &d : h->dev) {
+    CUDA_TRY(h, cudaSetDevice(d.ordinal));
+    CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg, h->dev_cfg.p, h->n_cfg * sizeof(DevCfg),
+                                cudaMemcpyHostToDevice, d.stream));
+  }
+  return DSI_OK;
+}
+
+}  // namespace
+
+// ============================================================================= C ABI
+extern "C" {
+
+uint32_t dsi_abi_version(void) { return DSI_ABI_VERSION; }
+
+const char *dsi_status_str(dsi_status s) {
+  switch (s) {
+    case DSI_OK: return "DSI_OK";
+    case DSI_E_NULL: return "DSI_E_NULL: required pointer was NULL";
+    case DSI_E_RANGE: return "DSI_E_RANGE: argument out of range";
+    case DSI_E_TICK: return "DSI_E_TICK: latency is not a whole number of ticks";
+    case DSI_E_OVERFLOW: return "DSI_E_OVERFLOW: tick sums would overflow";
+    case DSI_E_STRICT_EQ1: return "DSI_E_STRICT_EQ1: Eq. 1 violated under DSI_F_STRICT_EQ1";
+    case DSI_E_DEVICE: return "DSI_E_DEVICE: CUDA error or missing sm_100 device";
+    case DSI_E_COMM: return "DSI_E_COMM: NCCL error";
+    case DSI_E_STATE: return "DSI_E_STATE: call order violated";
+    case DSI_E_NOMEM: return "DSI_E_NOMEM: allocation failed";
+  }
+  return "unknown dsi_status";
+}
+
+const char *dsi_sim_last_error(const dsi_sim *h) { return h ? h->err.c_str() : ""; }
+const char *dsi_last_create_error(void) { return g_create_error.c_str(); }
+
+int32_t dsi_eq1_feasible(int64_t t_t, int64_t t_d, int32_t k, int32_t sp) {
+  if (t_t < 1 || t_d < 1 || k < 1 || sp < 1) return -1;
+  return ceil_div(t_t, (int64_t)k * t_d) <= sp ? 1 : 0;
+}
+
+int32_t dsi_min_lookahead(int64_t t_t, int64_t t_d, int32_t sp) {
+  if (t_t < 1 || t_d < 1 || sp < 1) return -1;
+  // smallest k with ceil(t_t/(k t_d)) <= sp  <=>  k t_d sp >= t_t
+  const int64_t k = ceil_div(t_t, t_d * (int64_t)sp);
+  return (int32_t)std::max<int64_t>(1, k);
+}
+
+int32_t dsi_required_processors(int64_t t_t, int64_t t_d, int32_t k) {
+  if (t_t < 1 || t_d < 1 || k < 1) return -1;
+  return (int32_t)(1 + ceil_div(t_t, (int64_t)k * t_d));
+}
+
+dsi_status dsi_shard_bounds(const double *cost, uint64_t n, int32_t parts, uint64_t *bounds) {
+  if (!bounds || (!cost && n)) return DSI_E_NULL;
+  if (parts < 1) return DSI_E_RANGE;
+  double total = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (!(cost[i] >= 0.0)) return DSI_E_RANGE;
+    total += cost[i];
+  }
+  bounds[0] = 0;
+  uint64_t i = 0;
+  double run = 0.0;
+  for (int32_t j = 1; j < parts; ++j) {
+    const double target = total * (double)j / (double)parts;
+    // advance while taking unit i keeps the prefix closer to the target
+    while (i < n && run + 0.5 * cost[i] <= target) run += cost[i++];
+    bounds[j] = i;
+  }
+  bounds[parts] = n;
+  return DSI_OK;
+}
+
+dsi_status dsi_nccl_unique_id(uint8_t id[128]) {
+  if (!id) return DSI_E_NULL;
+  NcclApi &api = nccl();
+  if (!api.ok) return DSI_E_COMM;
+  ncclUniqueId u;
+  if (api.GetUniqueId(&u) != ncclSuccess) return DSI_E_COMM;
+  static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, 128);
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t n_cfg,
+                          dsi_sim **out) {
+  g_create_error.clear();
+  if (!out) return fail(nullptr, DSI_E_NULL, "out is NULL");
+  *out = nullptr;
+  if (!opt || !cfg) return fail(nullptr, DSI_E_NULL, "opt or cfg is NULL");
+  if (opt->abi_version != DSI_ABI_VERSION) return fail(nullptr, DSI_E_RANGE, "abi_version mismatch");
+  if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
+  if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
+  const uint32_t known = DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_STRICT_EQ1 | DSI_F_TIMING;
+  if (opt->flags & ~known) return fail(nullptr, DSI_E_RANGE, "unknown flag");
+  if (opt->n_devices < 1 || opt->n_devices > 8) return fail(nullptr, DSI_E_RANGE, "n_devices must be 1..8");
+  if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
+    return fail(nullptr, DSI_E_RANGE, "need 0 <= rank < world");
+  if (opt->device < 0) return fail(nullptr, DSI_E_RANGE, "device must be >= 0");
+  if (opt->n_shards < 0 || opt->n_shards > 4096) return fail(nullptr, DSI_E_RANGE, "n_shards out of range");
+  if (opt->n_shards > 1 && (opt->n_devices > 1 || opt->world > 1))
+    return fail(nullptr, DSI_E_RANGE, "n_shards > 1 is single-device only");
+  if (opt->block_threads != 0 &&
+      (opt->block_threads < 32 || opt->block_threads > 256 || opt->block_threads % 32))
+    return fail(nullptr, DSI_E_RANGE, "block_threads must be a multiple of 32 in [32, 256]");
+  const int total_devices = opt->world * opt->n_devices;
+  if (total_devices > 1 && !opt->nccl_id)
+    return fail(nullptr, DSI_E_NULL, "nccl_id is required when world*n_devices > 1");
+  const bool per_trial = opt->flags & DSI_F_PER_TRIAL;
+  if (per_trial && total_devices > 1)
+    return fail(nullptr, DSI_E_RANGE, "DSI_F_PER_TRIAL needs a single device and world == 1");
+
+  dsi_sim *h = new (std::nothrow) dsi_sim;
+  if (!h) return fail(nullptr, DSI_E_NOMEM, "handle allocation");
+  auto abort_create = [&](dsi_status s) {
+    g_create_error = h->err;
+    free_handle(h);
+    return s;
+  };
+  h->opt = *opt;
+  h->opt.nccl_id = nullptr;
+  h->n_cfg = n_cfg;
+  h->block_threads = opt->block_threads ? opt->block_threads : kDefaultThreads;
+  try {
+    h->ticks.resize(n_cfg);
+    h->prefix.resize(n_cfg + 1);
+  } catch (...) {
+    h->err = "host tables";
+    return abort_create(DSI_E_NOMEM);
+  }
+
+  // ---- validation and tick conversion (before any device work)
+  dsi_status s = validate_all(h, cfg, n_cfg);
+  if (s != DSI_OK) return abort_create(s);
+  uint64_t max_keff = 0, sib = 0;
+  for (size_t i = 0; i < n_cfg; ++i) {
+    h->total_trials += h->ticks[i].trials;
+    const uint64_t ke = (uint64_t)std::min(h->ticks[i].k, h->ticks[i].n);
+    max_keff = std::max(max_keff, ke);
+    sib += ke + 1;
+  }
+  if (per_trial && h->total_trials > (1ull << 31)) {
+    h->err = "DSI_F_PER_TRIAL supports at most 2^31 trials in total";
+    return abort_create(DSI_E_RANGE);
+  }
+  if (sib >= (1ull << 32)) {
+    h->err = "too many SI histogram bins";
+    return abort_create(DSI_E_RANGE);
+  }
+  h->si_bins_total = sib;
+  h->hist_smem = (64 + max_keff + 1) * sizeof(unsigned int);
+  if ((opt->flags & DSI_F_HIST) && h->hist_smem > 200 * 1024) {
+    h->err = "DSI_F_HIST needs (64 + k + 1) * 4 bytes of shared memory <= 200 KiB";
+    return abort_create(DSI_E_RANGE);
+  }
+
+  // ---- work units: (config, tile of tile_trials trials)
+  {
+    const uint64_t threads = (uint64_t)h->block_threads;
+    const uint64_t target_blocks = 148ull * 16 * 8 * (uint64_t)total_devices;
+    uint64_t r = h->total_trials / (threads * target_blocks);
+    r = std::min<uint64_t>(32, std::max<uint64_t>(1, r));
+    h->tile_trials = (uint32_t)(threads * r);
+    h->prefix[0] = 0;
+    for (size_t i = 0; i < n_cfg; ++i)
+      h->prefix[i + 1] = h->prefix[i] + (h->ticks[i].trials + h->tile_trials - 1) / h->tile_trials;
+    h->total_units = h->prefix[n_cfg];
+  }
+
+  // ---- shards: world x n_devices x n_shards contiguous unit ranges of equal cost
+  const int shards_per_dev = std::max(1, opt->n_shards);
+  const int parts = total_devices * shards_per_dev;
+  std::vector<uint64_t> bounds(parts + 1);
+  {
+    std::vector<double> cost;
+    try {
+      cost.resize(h->total_units);
+    } catch (...) {
+      h->err = "sharder cost table";
+      return abort_create(DSI_E_NOMEM);
+    }
+    for (size_t i = 0; i < n_cfg; ++i) {
+      const uint64_t t = h->ticks[i].trials;
+      for (uint64_t u = h->prefix[i]; u < h->prefix[i + 1]; ++u) {
+        const uint64_t first = (u - h->prefix[i]) * h->tile_trials;
+        cost[u] = unit_cost(h->ticks[i], std::min<uint64_t>(h->tile_trials, t - first));
+      }
+    }
+    dsi_shard_bounds(cost.data(), h->total_units, parts, bounds.data());
+  }
+
+  // ---- devices
+  int visible = 0;
+  if (cudaGetDeviceCount(&visible) != cudaSuccess || visible < opt->device + opt->n_devices) {
+    h->err = "not enough CUDA devices visible";
+    return abort_create(DSI_E_DEVICE);
+  }
+  for (int di = 0; di < opt->n_devices; ++di) {
+    cudaDeviceProp prop;
+    const int ord = opt->device + di;
+    if (cudaGetDeviceProperties(&prop, ord) != cudaSuccess || prop.major != 10) {
+      h->err = "device " + std::to_string(ord) + " is not an sm_100 (Blackwell) GPU";
+      return abort_create(DSI_E_DEVICE);
+    }
+  }
+  if (cudaSetDevice(opt->device) != cudaSuccess) {
+    h->err = "cudaSetDevice failed";
+    return abort_create(DSI_E_DEVICE);
+  }
+  // pinned staging: config table (H2D) and results (D2H)
+  {
+    cudaError_t e = h->dev_cfg.alloc(n_cfg);
+    if (e == cudaSuccess) e = h->host_acc.alloc(n_cfg * dsi::NF);
+    if (e == cudaSuccess && (opt->flags & DSI_F_HIST)) {
+      e = h->host_seg.alloc(n_cfg * 64);
+      if (e == cudaSuccess) e = h->host_si.alloc(sib);
+    }
+    if (e != cudaSuccess) {
+      h->err = std::string("pinned host buffers: ") + cudaGetErrorString(e);
+      return abort_create(DSI_E_NOMEM);
+    }
+  }
+  fill_dev_cfg(h);
+
+  h->dev.resize(opt->n_devices);
+  for (int di = 0; di < opt->n_devices; ++di) {
+    DeviceState &d = h->dev[di];
+    d.ordinal = opt->device + di;
+    cudaError_t e = cudaSetDevice(d.ordinal);
+    const int global_dev = opt->rank * opt->n_devices + di;
+    for (int sh = 0; sh < shards_per_dev; ++sh) {
+      const int part = global_dev * shards_per_dev + sh;
+      d.ranges.emplace_back(bounds[part], bounds[part + 1]);
+    }
+    if (e == cudaSuccess) {
+      if (di == 0 && opt->stream) {
+        d.stream = (cudaStream_t)opt->stream;
+      } else {
+        e = cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking);
+        d.own_stream = true;
+      }
+    }
+    const size_t acc_bytes = n_cfg * dsi::NF * sizeof(unsigned long long);
+    if (e == cudaSuccess) e = cudaMalloc(&d.d_cfg, n_cfg * sizeof(DevCfg));
+    if (e == cudaSuccess) e = cudaMalloc(&d.d_prefix, (n_cfg + 1) * sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMalloc(&d.d_acc, acc_bytes);
+    if (e == cudaSuccess && total_devices > 1) e = cudaMalloc(&d.d_red, acc_bytes);
+    if (e == cudaSuccess && (opt->flags & DSI_F_HIST)) {
+      e = cudaMalloc(&d.d_seg, n_cfg * 64 * sizeof(unsigned long long));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_si, sib * sizeof(unsigned long long));
+      if (e == cudaSuccess && total_devices > 1) {
+        e = cudaMalloc(&d.d_seg_red, n_cfg * 64 * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMalloc(&d.d_si_red, sib * sizeof(unsigned long long));
+      }
+    }
+    if (e == cudaSuccess && per_trial) e = cudaMalloc(&d.d_rec, 5 * h->total_trials * sizeof(int32_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(d.d_prefix, h->prefix.data(), (n_cfg + 1) * sizeof(uint64_t),
+                          cudaMemcpyHostToDevice, d.stream);
+    if (e == cudaSuccess && (opt->flags & DSI_F_TIMING)) {
+      e = cudaEventCreate(&d.ev0);
+      if (e == cudaSuccess) e = cudaEventCreate(&d.ev1);
+    }
+    if (e != cudaSuccess) {
+      h->err = std::string("device setup: ") + cudaGetErrorString(e);
+      return abort_create(e == cudaErrorMemoryAllocation ? DSI_E_NOMEM : DSI_E_DEVICE);
+    }
+  }
+  s = upload(h);
+  if (s != DSI_OK) return abort_create(s);
+  for (auto &d : h->dev) {
+    cudaSetDevice(d.ordinal);
+    if (cudaStreamSynchronize(d.stream) != cudaSuccess) {
+      h->err = "device setup: stream synchronize failed";
+      return abort_create(DSI_E_DEVICE);
+    }
+  }
+
+  // ---- NCCL: one communicator per device over world * n_devices ranks
+  if (total_devices > 1) {
+    NcclApi &api = nccl();
+    if (!api.ok) {
+      h->err = "libnccl.so.2 could not be loaded";
+      return abort_create(DSI_E_COMM);
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, opt->nccl_id, sizeof(uid));
+    ncclResult_t r = api.GroupStart();
+    for (int di = 0; di < opt->n_devices && r == ncclSuccess; ++di) {
+      cudaSetDevice(h->dev[di].ordinal);
+      r = api.CommInitRank(&h->dev[di].comm, total_devices, uid, opt->rank * opt->n_devices + di);
+    }
+    const ncclResult_t r2 = api.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess) {
+      h->err = std::string("ncclCommInitRank: ") + api.GetErrorString(r != ncclSuccess ? r : r2);
+      return abort_create(DSI_E_COMM);
+    }
+  }
+  *out = h;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
+  if (!h) return DSI_E_NULL;
+  h->err.clear();
+  if (!cfg) return fail(h, DSI_E_NULL, "cfg is NULL");
+  if (n_cfg != h->n_cfg) return fail(h, DSI_E_RANGE, "n_cfg must equal the handle's");
+  std::vector<CfgTicks> old;
+  try {
+    old = h->ticks;
+  } catch (...) {
+    return fail(h, DSI_E_NOMEM, "host tables");
+  }
+  dsi_status s = validate_all(h, cfg, n_cfg);
+  if (s == DSI_OK) {
+    for (size_t i = 0; i < n_cfg; ++i) {
+      const bool same_trials = h->ticks[i].trials == old[i].trials;
+      const bool same_bins = std::min(h->ticks[i].k, h->ticks[i].n) == std::min(old[i].k, old[i].n);
+      if (!same_trials || ((h->opt.flags & DSI_F_HIST) && !same_bins)) {
+        s = fail(h, DSI_E_RANGE, "config " + std::to_string(i) +
+                                     ": n_trials (and, with DSI_F_HIST, min(k, N)) must not change");
+        break;
+      }
+    }
+  }
+  if (s != DSI_OK) {
+    const std::string msg = h->err;
+    h->ticks.swap(old);
+    h->err = msg;
+    return s;
+  }
+  // wait until no kernel of a previous run still reads the table, then restage it
+  for (auto &d : h->dev) {
+    CUDA_TRY(h, cudaSetDevice(d.ordinal));
+    CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+  }
+  fill_dev_cfg(h);
+  h->ran = h->reduced = false;
+  return upload(h);
+}
+
+dsi_status dsi_sim_run(dsi_sim *h) {
+  if (!h) return DSI_E_NULL;
+  h->err.clear();
+  const size_t n_cfg = h->n_cfg;
+  const uint64_t tt = h->total_trials;
+  h->launches = 0;
+  for (auto &d : h->dev) {
+    CUDA_TRY(h, cudaSetDevice(d.ordinal));
+    CUDA_TRY(h, cudaMemsetAsync(d.d_acc, 0, n_cfg * dsi::NF * sizeof(unsigned long long), d.stream));
+    if (d.d_seg) {
+      CUDA_TRY(h, cudaMemsetAsync(d.d_seg, 0, n_cfg * 64 * sizeof(unsigned long long), d.stream));
+      CUDA_TRY(h, cudaMemsetAsync(d.d_si, 0, h->si_bins_total * sizeof(unsigned long long), d.stream));
+    }
+    LaunchParams p{};
+    p.cfg = d.d_cfg;
+    p.tile_prefix = d.d_prefix;
+    p.n_cfg = (uint32_t)n_cfg;
+    p.tile_trials = h->tile_trials;
+    p.acc = d.d_acc;
+    if (d.d_rec) {
+      p.rec_acc = d.d_rec;
+      p.rec_m = d.d_rec + tt;
+      p.rec_iters = d.d_rec + 2 * tt;
+      p.rec_si = d.d_rec + 3 * tt;
+      p.rec_dsi = d.d_rec + 4 * tt;
+    }
+    p.seg_hist = d.d_seg;
+    p.si_hist = d.d_si;
+    const uint32_t s_lo = (uint32_t)h->opt.seed, s_hi = (uint32_t)(h->opt.seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+      p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;
+      p.keys.k1[r] = s_hi + (uint32_t)r * 0xBB67AE85u;
+    }
+    if (d.ev0) CUDA_TRY(h, cudaEventRecord(d.ev0, d.stream));
+    for (const auto &rg : d.ranges) {
+      if (rg.second <= rg.first) continue;
+      p.unit_begin = rg.first;
+      const int e = dsi::launch_trial_kernel(p, rg.second - rg.first, h->block_threads,
+                                             h->opt.flags & DSI_F_PER_TRIAL, h->opt.flags & DSI_F_HIST,
+                                             h->opt.flags & DSI_F_PATTERN, h->hist_smem, d.stream);
+      if (e) return cuda_fail(h, (cudaError_t)e, "trial kernel launch");
+      h->launches += 1;
+    }
+    if (d.ev1) CUDA_TRY(h, cudaEventRecord(d.ev1, d.stream));
+  }
+  h->ran = true;
+  h->reduced = false;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
+  if (!h) return DSI_E_NULL;
+  if (!out) return fail(h, DSI_E_NULL, "out is NULL");
+  h->err.clear();
+  const size_t n_cfg = h->n_cfg;
+  if (n != n_cfg) return fail(h, DSI_E_RANGE, "n must equal n_cfg");
+  if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_reduce before dsi_sim_run");
+  const bool hist = h->opt.flags & DSI_F_HIST;
+  const int total_devices = h->opt.world * h->opt.n_devices;
+  const size_t nacc = n_cfg * dsi::NF;
+  if (total_devices > 1) {
+    NcclApi &api = nccl();
+    ncclResult_t r = api.GroupStart();
+    for (auto &d : h->dev) {
+      if (r != ncclSuccess) break;
+      cudaSetDevice(d.ordinal);
+      r = api.AllReduce(d.d_acc, d.d_red, nacc, ncclUint64, ncclSum, d.comm, d.stream);
+      if (r == ncclSuccess && hist) {
+        r = api.AllReduce(d.d_seg, d.d_seg_red, n_cfg * 64, ncclUint64, ncclSum, d.comm, d.stream);
+        if (r == ncclSuccess)
+          r = api.AllReduce(d.d_si, d.d_si_red, h->si_bins_total, ncclUint64, ncclSum, d.comm, d.stream);
+      }
+    }
+    const ncclResult_t r2 = api.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+      return fail(h, DSI_E_COMM, std::string("ncclAllReduce: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
+  }
+  // every device now holds the global sums (or there is one device): read device 0
+  DeviceState &d0 = h->dev[0];
+  CUDA_TRY(h, cudaSetDevice(d0.ordinal));
+  const unsigned long long *src = total_devices > 1 ? d0.d_red : d0.d_acc;
+  CUDA_TRY(h, cudaMemcpyAsync(h->host_acc.p, src, nacc * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, d0.stream));
+  if (hist) {
+    CUDA_TRY(h, cudaMemcpyAsync(h->host_seg.p, total_devices > 1 ? d0.d_seg_red : d0.d_seg,
+                                n_cfg * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d0.stream));
+    CUDA_TRY(h, cudaMemcpyAsync(h->host_si.p, total_devices > 1 ? d0.d_si_red : d0.d_si,
+                                h->si_bins_total * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                d0.stream));
+  }
+  for (auto &d : h->dev) {
+    CUDA_TRY(h, cudaSetDevice(d.ordinal));
+    CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+  }
+  // check the partition: every trial simulated exactly once
+  for (size_t i = 0; i < n_cfg; ++i) {
+    if (h->host_acc.p[i * dsi::NF + dsi::F_TRIALS] != h->ticks[i].trials)
+      return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
+  }
+  const double tick = h->opt.tick;
+  for (size_t i = 0; i < n_cfg; ++i) {
+    const unsigned long long *a = &h->host_acc.p[i * dsi::NF];
+    const CfgTicks &t = h->ticks[i];
+    dsi_result &r = out[i];
+    const uint64_t T = t.trials;
+    const uint64_t si_cost = (uint64_t)(t.kd + t.t_t);
+    r.trials = T;
+    r.t_target_ticks = t.t_t;
+    r.t_drafter_ticks = t.t_d;
+    r.nonsi_ticks = (int64_t)t.n * t.t_t;
+    r.sum_si_iters = (int64_t)a[dsi::F_I];
+    r.sum_si_ticks = (int64_t)(si_cost * a[dsi::F_I]);
+    r.sumsq_si_ticks = si_cost * si_cost * a[dsi::F_I2];
+    r.sum_dsi_ticks = (int64_t)a[dsi::F_DSI];
+    r.sumsq_dsi_ticks = a[dsi::F_DSI2];
+    r.sum_segments = (int64_t)a[dsi::F_M];
+    // acc = (N-1) - (m-1) per trial
+    r.sum_accepts = (int64_t)(T * (uint64_t)t.n) - (int64_t)a[dsi::F_M];
+    r.n_dsi_gt_nonsi = (int64_t)a[dsi::F_GT_NONSI];
+    r.n_dsi_gt_si = (int64_t)a[dsi::F_GT_SI];
+    r.threshold = t.thr;
+    r.eq1_feasible = dsi_eq1_feasible(t.t_t, t.t_d, t.k, t.sp);
+    r.min_lookahead = dsi_min_lookahead(t.t_t, t.t_d, t.sp);
+    const double Td = (double)T;
+    r.mean_nonsi = (double)r.nonsi_ticks * tick;
+    r.mean_si = ((double)r.sum_si_ticks / Td) * tick;
+    r.mean_dsi = ((double)r.sum_dsi_ticks / Td) * tick;
+    auto stdev = [&](uint64_t s1, uint64_t s2) {
+      const unsigned __int128 num = (unsigned __int128)T * s2 - (unsigned __int128)s1 * s1;
+      return std::sqrt((double)num) / Td * tick;
+    };
+    r.std_si = stdev((uint64_t)r.sum_si_ticks, r.sumsq_si_ticks);
+    r.std_dsi = stdev((uint64_t)r.sum_dsi_ticks, r.sumsq_dsi_ticks);
+  }
+  h->reduced = true;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_trials(dsi_sim *h, size_t cfg, uint64_t first, uint64_t count, int32_t *acc,
+                          int32_t *m, int32_t *iters, int32_t *si_ticks, int32_t *dsi_ticks) {
+  if (!h) return DSI_E_NULL;
+  h->err.clear();
+  if (!(h->opt.flags & DSI_F_PER_TRIAL)) return fail(h, DSI_E_STATE, "needs DSI_F_PER_TRIAL");
+  if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_trials before dsi_sim_run");
+  if (cfg >= h->n_cfg) return fail(h, DSI_E_RANGE, "cfg out of range");
+  const uint64_t T = h->ticks[cfg].trials;
+  if (first > T || count > T - first) return fail(h, DSI_E_RANGE, "trial range out of bounds");
+  DeviceState &d = h->dev[0];
+  CUDA_TRY(h, cudaSetDevice(d.ordinal));
+  CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+  const uint64_t tt = h->total_trials;
+  const uint64_t off = h->dev_cfg.p[cfg].rec_off + first;
+  int32_t *dst[5] = {acc, m, iters, si_ticks, dsi_ticks};
+  for (int f = 0; f < 5; ++f) {
+    if (!dst[f] || count == 0) continue;
+    CUDA_TRY(h, cudaMemcpy(dst[f], d.d_rec + f * tt + off, count * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_hist(dsi_sim *h, size_t cfg, int64_t *seg_hist, int64_t *si_hist, size_t si_bins) {
+  if (!h) return DSI_E_NULL;
+  h->err.clear();
+  if (!(h->opt.flags & DSI_F_HIST)) return fail(h, DSI_E_STATE, "needs DSI_F_HIST");
+  if (!h->reduced) return fail(h, DSI_E_STATE, "dsi_sim_hist before dsi_sim_reduce");
+  if (cfg >= h->n_cfg) return fail(h, DSI_E_RANGE, "cfg out of range");
+  const size_t k = (size_t)h->ticks[cfg].k;
+  if (si_hist && si_bins != k + 1) return fail(h, DSI_E_RANGE, "si_bins must equal k+1");
+  if (seg_hist)
+    for (int i = 0; i < 64; ++i) seg_hist[i] = (int64_t)h->host_seg.p[cfg * 64 + i];
+  if (si_hist) {
+    const DevCfg &dc = h->dev_cfg.p[cfg];
+    for (size_t j = 0; j <= k; ++j)
+      si_hist[j] = j <= (size_t)dc.k_eff ? (int64_t)h->host_si.p[dc.si_hist_off + j] : 0;
+  }
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_stream(dsi_sim *h, int32_t i, void **stream) {
+  if (!h || !stream) return DSI_E_NULL;
+  if (i < 0 || i >= (int32_t)h->dev.size()) return fail(h, DSI_E_RANGE, "device index");
+  *stream = (void *)h->dev[i].stream;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_launches(dsi_sim *h, int32_t *launches) {
+  if (!h || !launches) return DSI_E_NULL;
+  *launches = h->launches;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_kernel_ms(dsi_sim *h, int32_t i, float *ms) {
+  if (!h || !ms) return DSI_E_NULL;
+  if (!(h->opt.flags & DSI_F_TIMING)) return fail(h, DSI_E_STATE, "needs DSI_F_TIMING");
+  if (!h->ran) return fail(h, DSI_E_STATE, "no run yet");
+  if (i < 0 || i >= (int32_t)h->dev.size()) return fail(h, DSI_E_RANGE, "device index");
+  DeviceState &d = h->dev[i];
+  CUDA_TRY(h, cudaSetDevice(d.ordinal));
+  CUDA_TRY(h, cudaEventSynchronize(d.ev1));
+  CUDA_TRY(h, cudaEventElapsedTime(ms, d.ev0, d.ev1));
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_io_bytes(dsi_sim *h, uint64_t *h2d, uint64_t *d2h) {
+  if (!h || !h2d || !d2h) return DSI_E_NULL;
+  const uint64_t n = h->n_cfg;
+  *h2d = (uint64_t)h->dev.size() * n * sizeof(DevCfg);
+  uint64_t back = n * dsi::NF * sizeof(unsigned long long);
+  if (h->opt.flags & DSI_F_HIST) back += (n * 64 + h->si_bins_total) * sizeof(unsigned long long);
+  *d2h = back;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_units(dsi_sim *h, uint64_t *first, uint64_t *count, uint64_t *total) {
+  if (!h || !first || !count || !total) return DSI_E_NULL;
+  uint64_t lo = UINT64_MAX, hi = 0;
+  for (auto &d : h->dev)
+    for (auto &r : d.ranges) {
+      lo = std::min(lo, r.first);
+      hi = std::max(hi, r.second);
+    }
+  *first = lo == UINT64_MAX ? 0 : lo;
+  *count = hi > *first ? hi - *first : 0;
+  *total = h->total_units;
+  return DSI_OK;
+}
+
+void dsi_sim_destroy(dsi_sim *h) {
+  if (!h) return;
+  free_handle(h);
+}
+
+}  // extern "C"
+
+static_assert(sizeof(dsi_config) == 48, "dsi_config ABI layout");
+static_assert(sizeof(dsi_result) == 160, "dsi_result ABI layout");
+static_assert(sizeof(dsi_options) == 64, "dsi_options ABI layout");

@@ -1,0 +1,272 @@
+"""Thin ctypes binding of include/dsi_sim.h (argument marshalling only).
+
+Every step of the simulation runs in libdsi_sim.so (sm_100a kernels + C++ host
+runtime).  There is no Python or CPU fallback: importing this module without
+the built library raises ImportError, and creating a simulator without an
+sm_100 GPU fails with DSI_E_DEVICE.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdsi_sim.so")
+
+DSI_ABI_VERSION = 1
+DSI_OK, DSI_E_NULL, DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW, DSI_E_STRICT_EQ1, DSI_E_DEVICE, \
+    DSI_E_COMM, DSI_E_STATE, DSI_E_NOMEM = range(10)
+DSI_F_PER_TRIAL, DSI_F_HIST, DSI_F_PATTERN, DSI_F_STRICT_EQ1, DSI_F_TIMING = 0x1, 0x2, 0x4, 0x8, 0x10
+
+# Structured dtypes with the exact C layouts (numpy arrays are passed by pointer).
+CONFIG_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_rate", "<f8"),
+                         ("lookahead", "<i4"), ("sp_degree", "<i4"), ("n_tokens", "<i4"),
+                         ("stream_id", "<u4"), ("n_trials", "<u8")])
+RESULT_DTYPE = np.dtype([("trials", "<u8"), ("t_target_ticks", "<i8"), ("t_drafter_ticks", "<i8"),
+                         ("nonsi_ticks", "<i8"), ("sum_si_ticks", "<i8"), ("sum_dsi_ticks", "<i8"),
+                         ("sumsq_si_ticks", "<u8"), ("sumsq_dsi_ticks", "<u8"),
+                         ("sum_si_iters", "<i8"), ("sum_accepts", "<i8"), ("sum_segments", "<i8"),
+                         ("n_dsi_gt_nonsi", "<i8"), ("n_dsi_gt_si", "<i8"), ("threshold", "<u8"),
+                         ("eq1_feasible", "<i4"), ("min_lookahead", "<i4"),
+                         ("mean_nonsi", "<f8"), ("mean_si", "<f8"), ("mean_dsi", "<f8"),
+                         ("std_si", "<f8"), ("std_dsi", "<f8")])
+assert CONFIG_DTYPE.itemsize == 48 and RESULT_DTYPE.itemsize == 160
+
+
+class dsi_options(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+                ("tick", ctypes.c_double), ("seed", ctypes.c_uint64), ("device", ctypes.c_int32),
+                ("n_devices", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p), ("n_shards", ctypes.c_int32),
+                ("block_threads", ctypes.c_int32), ("stream", ctypes.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, V = ctypes.POINTER, ctypes.c_void_p
+    u64, i32, i64, sz = ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    sigs = {
+        "dsi_sim_create": ([P(dsi_options), V, sz, P(V)], ctypes.c_int),
+        "dsi_sim_update": ([V, V, sz], ctypes.c_int),
+        "dsi_sim_run": ([V], ctypes.c_int),
+        "dsi_sim_reduce": ([V, V, sz], ctypes.c_int),
+        "dsi_sim_trials": ([V, sz, u64, u64, V, V, V, V, V], ctypes.c_int),
+        "dsi_sim_hist": ([V, sz, V, V, sz], ctypes.c_int),
+        "dsi_sim_stream": ([V, i32, P(V)], ctypes.c_int),
+        "dsi_sim_launches": ([V, P(i32)], ctypes.c_int),
+        "dsi_sim_kernel_ms": ([V, i32, P(ctypes.c_float)], ctypes.c_int),
+        "dsi_sim_units": ([V, P(u64), P(u64), P(u64)], ctypes.c_int),
+        "dsi_sim_io_bytes": ([V, P(u64), P(u64)], ctypes.c_int),
+        "dsi_sim_destroy": ([V], None),
+        "dsi_status_str": ([ctypes.c_int], ctypes.c_char_p),
+        "dsi_sim_last_error": ([V], ctypes.c_char_p),
+        "dsi_last_create_error": ([], ctypes.c_char_p),
+        "dsi_abi_version": ([], ctypes.c_uint32),
+        "dsi_nccl_unique_id": ([V], ctypes.c_int),
+        "dsi_min_lookahead": ([i64, i64, i32], i32),
+        "dsi_required_processors": ([i64, i64, i32], i32),
+        "dsi_eq1_feasible": ([i64, i64, i32, i32], i32),
+        "dsi_shard_bounds": ([V, u64, i32, V], ctypes.c_int),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+lib = _load()
+EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce", "dsi_sim_trials", "dsi_sim_hist",
+            "dsi_sim_stream", "dsi_sim_launches", "dsi_sim_kernel_ms", "dsi_sim_units", "dsi_sim_io_bytes",
+            "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
+            "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
+            "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds")
+
+
+class DsiError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        self.status = status
+        super().__init__(f"{lib.dsi_status_str(status).decode()}{': ' + msg if msg else ''}")
+
+
+def _check(status: int, handle=None, create: bool = False):
+    if status != DSI_OK:
+        if create:
+            msg = lib.dsi_last_create_error().decode()
+        else:
+            msg = lib.dsi_sim_last_error(handle).decode() if handle else ""
+        raise DsiError(status, msg)
+
+
+# ----------------------------------------------------------------------------- same names as the C ABI
+def dsi_min_lookahead(t_target_ticks: int, t_drafter_ticks: int, sp: int) -> int:
+    return lib.dsi_min_lookahead(t_target_ticks, t_drafter_ticks, sp)
+
+
+def dsi_required_processors(t_target_ticks: int, t_drafter_ticks: int, k: int) -> int:
+    return lib.dsi_required_processors(t_target_ticks, t_drafter_ticks, k)
+
+
+def dsi_eq1_feasible(t_target_ticks: int, t_drafter_ticks: int, k: int, sp: int) -> int:
+    return lib.dsi_eq1_feasible(t_target_ticks, t_drafter_ticks, k, sp)
+
+
+def dsi_shard_bounds(costs, parts: int) -> np.ndarray:
+    c = np.ascontiguousarray(costs, dtype=np.float64)
+    b = np.zeros(parts + 1, np.uint64)
+    _check(lib.dsi_shard_bounds(c.ctypes.data, c.size, parts, b.ctypes.data))
+    return b
+
+
+def dsi_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib.dsi_nccl_unique_id(ctypes.addressof(buf)))
+    return bytes(buf)
+
+
+def make_configs(n: int) -> np.ndarray:
+    return np.zeros(n, CONFIG_DTYPE)
+
+
+def dsi_sim_create(configs: np.ndarray, *, tick: float, seed: int, flags: int = 0, device: int = 0,
+                   n_devices: int = 1, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                   n_shards: int = 0, block_threads: int = 0, stream: int | None = None):
+    configs = np.ascontiguousarray(configs, dtype=CONFIG_DTYPE)
+    idbuf = None
+    if nccl_id is not None:
+        idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+    opt = dsi_options(DSI_ABI_VERSION, flags, tick, seed, device, n_devices, rank, world,
+                      ctypes.addressof(idbuf) if idbuf is not None else None, n_shards,
+                      block_threads, stream)
+    h = ctypes.c_void_p()
+    _check(lib.dsi_sim_create(ctypes.byref(opt), configs.ctypes.data, configs.size, ctypes.byref(h)),
+           create=True)
+    return h
+
+
+def dsi_sim_update(h, configs: np.ndarray) -> None:
+    configs = np.ascontiguousarray(configs, dtype=CONFIG_DTYPE)
+    _check(lib.dsi_sim_update(h, configs.ctypes.data, configs.size), h)
+
+
+def dsi_sim_run(h) -> None:
+    _check(lib.dsi_sim_run(h), h)
+
+
+def dsi_sim_reduce(h, n: int, out: np.ndarray | None = None) -> np.ndarray:
+    if out is None:
+        out = np.zeros(n, RESULT_DTYPE)
+    _check(lib.dsi_sim_reduce(h, out.ctypes.data, n), h)
+    return out
+
+
+def dsi_sim_trials(h, cfg: int, first: int, count: int) -> dict:
+    arrs = {k: np.zeros(count, np.int32) for k in ("acc", "m", "iters", "si", "dsi")}
+    _check(lib.dsi_sim_trials(h, cfg, first, count, *[arrs[k].ctypes.data for k in
+                                                      ("acc", "m", "iters", "si", "dsi")]), h)
+    return arrs
+
+
+def dsi_sim_hist(h, cfg: int, k: int) -> tuple:
+    seg = np.zeros(64, np.int64)
+    si = np.zeros(k + 1, np.int64)
+    _check(lib.dsi_sim_hist(h, cfg, seg.ctypes.data, si.ctypes.data, k + 1), h)
+    return seg, si
+
+
+def dsi_sim_stream(h, device_index: int = 0) -> int:
+    s = ctypes.c_void_p()
+    _check(lib.dsi_sim_stream(h, device_index, ctypes.byref(s)), h)
+    return s.value or 0
+
+
+def dsi_sim_launches(h) -> int:
+    n = ctypes.c_int32()
+    _check(lib.dsi_sim_launches(h, ctypes.byref(n)), h)
+    return n.value
+
+
+def dsi_sim_kernel_ms(h, device_index: int = 0) -> float:
+    ms = ctypes.c_float()
+    _check(lib.dsi_sim_kernel_ms(h, device_index, ctypes.byref(ms)), h)
+    return ms.value
+
+
+def dsi_sim_units(h) -> tuple:
+    a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.dsi_sim_units(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), h)
+    return a.value, b.value, c.value
+
+
+def dsi_sim_io_bytes(h) -> tuple:
+    a, b = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.dsi_sim_io_bytes(h, ctypes.byref(a), ctypes.byref(b)), h)
+    return a.value, b.value
+
+
+def dsi_sim_destroy(h) -> None:
+    if h:
+        lib.dsi_sim_destroy(h)
+
+
+class Simulator:
+    """RAII wrapper: create on construction, destroy on close/exit."""
+
+    def __init__(self, configs: np.ndarray, **kw):
+        self.configs = np.ascontiguousarray(configs, dtype=CONFIG_DTYPE)
+        self.n = self.configs.size
+        self.h = dsi_sim_create(self.configs, **kw)
+
+    def update(self, configs: np.ndarray) -> "Simulator":
+        configs = np.ascontiguousarray(configs, dtype=CONFIG_DTYPE)
+        dsi_sim_update(self.h, configs)
+        self.configs = configs
+        return self
+
+    def run(self) -> "Simulator":
+        dsi_sim_run(self.h)
+        return self
+
+    def reduce(self) -> np.ndarray:
+        return dsi_sim_reduce(self.h, self.n)
+
+    def trials(self, cfg: int, first: int = 0, count: int | None = None) -> dict:
+        if count is None:
+            count = int(self.configs["n_trials"][cfg]) - first
+        return dsi_sim_trials(self.h, cfg, first, count)
+
+    def hist(self, cfg: int) -> tuple:
+        return dsi_sim_hist(self.h, cfg, int(self.configs["lookahead"][cfg]))
+
+    def kernel_ms(self, device_index: int = 0) -> float:
+        return dsi_sim_kernel_ms(self.h, device_index)
+
+    def launches(self) -> int:
+        return dsi_sim_launches(self.h)
+
+    def io_bytes(self) -> tuple:
+        return dsi_sim_io_bytes(self.h)
+
+    def stream(self, device_index: int = 0) -> int:
+        return dsi_sim_stream(self.h, device_index)
+
+    def close(self) -> None:
+        if self.h:
+            dsi_sim_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

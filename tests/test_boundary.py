@@ -1,0 +1,166 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/dsi_sim.h
+declares, and its host-only logic (validation, planner, sharder) behaves.  No compute
+call is made without a GPU: on this box dsi_sim_create must stop with DSI_E_DEVICE
+after validation passes."""
+import json
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2405_14105_b200 import dsi_sim as D
+from paper_2405_14105_b200 import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dsi_sim.h")
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dsi_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_every_header_symbol_is_exported_and_bound():
+    names = header_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(D.lib, n), n            # dlsym succeeds
+        assert n in D.EXPORTED, n               # the binding declares it
+        assert hasattr(D, n) or n in ("dsi_status_str", "dsi_sim_last_error",
+                                      "dsi_last_create_error", "dsi_abi_version"), n
+
+
+def test_abi_version_and_status_strings():
+    assert D.lib.dsi_abi_version() == D.DSI_ABI_VERSION
+    for s in range(10):
+        assert D.lib.dsi_status_str(s).decode().startswith("DSI_")
+
+
+def test_planner_matches_paper_examples():
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "planner.json")))
+    for e in g["min_lookahead"]:
+        assert D.dsi_min_lookahead(e["t_target"], e["t_drafter"], e["sp"]) == e["k"], e["cite"]
+    for e in g["required_processors"]:
+        assert D.dsi_required_processors(e["t_target"], e["t_drafter"], e["k"]) == e["procs"], e["cite"]
+
+
+def test_planner_matches_definition():
+    """Eq. 1 by its plain definition (the oracle's search) on random integers."""
+    rng = random.Random(7)
+    for _ in range(2000):
+        t_t = rng.randint(1, 500)
+        t_d = rng.randint(1, t_t)
+        sp = rng.randint(1, 9)
+        k = rng.randint(1, 30)
+        assert D.dsi_min_lookahead(t_t, t_d, sp) == O.min_lookahead(t_t, t_d, sp)
+        assert D.dsi_eq1_feasible(t_t, t_d, k, sp) == int(O.eq1_feasible(t_t, t_d, k, sp))
+        assert D.dsi_required_processors(t_t, t_d, k) == O.required_processors(t_t, t_d, k)
+    assert D.dsi_min_lookahead(0, 1, 1) == -1
+
+
+def test_shard_bounds_properties():
+    rng = np.random.default_rng(0)
+    for n, parts in [(0, 1), (1, 4), (10, 3), (1000, 8), (997, 7), (50, 64)]:
+        c = rng.random(n) * 10
+        b = D.dsi_shard_bounds(c, parts)
+        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b.astype(np.int64)) >= 0)
+        if n >= parts * 10:
+            sums = [c[b[j]:b[j + 1]].sum() for j in range(parts)]
+            assert max(sums) - min(sums) <= 2 * c.max() + 1e-9
+    with pytest.raises(D.DsiError):
+        D.dsi_shard_bounds(np.array([1.0, -1.0]), 2)
+
+
+def _create(cfgs, tick=0.01, **kw):
+    return D.dsi_sim_create(cfgs, tick=tick, seed=W.SEED, **kw)
+
+
+def _one(**over):
+    cfgs, tick = W.cfg1(trials=10)
+    for k, v in over.items():
+        cfgs[k] = v
+    return cfgs
+
+
+@pytest.mark.parametrize("over,status", [
+    ({"accept_rate": 1.5}, D.DSI_E_RANGE), ({"accept_rate": -0.1}, D.DSI_E_RANGE),
+    ({"accept_rate": np.nan}, D.DSI_E_RANGE), ({"lookahead": 0}, D.DSI_E_RANGE),
+    ({"sp_degree": 0}, D.DSI_E_RANGE), ({"n_tokens": 0}, D.DSI_E_RANGE),
+    ({"n_tokens": 40000}, D.DSI_E_RANGE), ({"n_trials": 0}, D.DSI_E_RANGE),
+    ({"n_trials": (1 << 32) + 1}, D.DSI_E_RANGE), ({"t_drafter": 2.0}, D.DSI_E_RANGE),
+    ({"t_target": -1.0}, D.DSI_E_RANGE), ({"t_target": np.inf}, D.DSI_E_RANGE),
+    ({"t_drafter": 0.105}, D.DSI_E_TICK), ({"t_target": 0.001}, D.DSI_E_TICK),
+    ({"lookahead": 10**7}, D.DSI_E_OVERFLOW), ({"n_tokens": 30000, "t_target": 1000.0}, D.DSI_E_OVERFLOW),
+])
+def test_create_validation_errors(over, status):
+    with pytest.raises(D.DsiError) as e:
+        _create(_one(**over))
+    assert e.value.status == status, str(e.value)
+
+
+def test_create_option_errors():
+    cfgs = _one()
+    bad = [dict(tick=0.0), dict(tick=-1.0), dict(flags=0x100), dict(n_devices=0), dict(n_devices=9),
+           dict(world=2, rank=2), dict(world=0), dict(block_threads=48), dict(block_threads=512),
+           dict(n_shards=2, n_devices=2)]
+    for kw in bad:
+        tick = kw.pop("tick", 0.01)
+        with pytest.raises(D.DsiError) as e:
+            D.dsi_sim_create(cfgs, tick=tick, seed=1, **kw)
+        assert e.value.status in (D.DSI_E_RANGE, D.DSI_E_NULL), (kw, str(e.value))
+    with pytest.raises(D.DsiError) as e:  # multi-GPU without an NCCL id
+        D.dsi_sim_create(cfgs, tick=0.01, seed=1, world=2, rank=0)
+    assert e.value.status == D.DSI_E_NULL
+    with pytest.raises(D.DsiError) as e:  # per-trial records are single-device only
+        D.dsi_sim_create(cfgs, tick=0.01, seed=1, world=2, rank=0, nccl_id=b"\0" * 128,
+                         flags=D.DSI_F_PER_TRIAL)
+    assert e.value.status == D.DSI_E_RANGE
+
+
+def test_strict_eq1_and_pattern_limits():
+    cfgs = _one(sp_degree=1)  # ceil(100 / (5*10)) = 2 > 1
+    with pytest.raises(D.DsiError) as e:
+        _create(cfgs, flags=D.DSI_F_STRICT_EQ1)
+    assert e.value.status == D.DSI_E_STRICT_EQ1
+    with pytest.raises(D.DsiError) as e:
+        _create(_one(n_tokens=34), flags=D.DSI_F_PATTERN)
+    assert e.value.status == D.DSI_E_RANGE
+    with pytest.raises(D.DsiError):
+        D.dsi_sim_create(W.cfg1()[0][:0], tick=0.01, seed=1)  # n_cfg == 0
+
+
+@pytest.mark.skipif(D.lib is None, reason="no library")
+def test_valid_config_without_gpu_reports_device_error():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(D.DsiError) as e:
+        _create(W.cfg1()[0])
+    assert e.value.status == D.DSI_E_DEVICE
+
+
+def test_null_handles_are_rejected():
+    assert D.lib.dsi_sim_run(None) == D.DSI_E_NULL
+    assert D.lib.dsi_sim_reduce(None, None, 0) == D.DSI_E_NULL
+    D.lib.dsi_sim_destroy(None)  # NULL-safe
+
+
+def test_workloads_shapes():
+    assert W.cfg1()[0].size == 1
+    c2, t2 = W.cfg2()
+    assert c2.size == 30 and t2 == 0.1
+    c3, _ = W.cfg3(k_max=20)
+    assert c3.size == 10100 * 20
+    c4, _ = W.cfg4()
+    assert c4.size == 140
+    c5, _ = W.cfg5(D.dsi_min_lookahead)
+    assert c5.size == 10100
+    # every latency is a whole number of ticks (checked by the oracle's own converter)
+    for c, tick in (W.cfg2(), W.cfg3(k_max=2), W.cfg5(D.dsi_min_lookahead)):
+        for row in c[:: max(1, c.size // 500)]:
+            O.ticks(float(row["t_target"]), tick)
+            O.ticks(float(row["t_drafter"]), tick)

@@ -1,0 +1,226 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle.
+
+Per-trial records {acc, m, I, L_SI, L_DSI} must be bit-exact (integer ticks), the
+per-config integer sums exact, and the FP64 means within 1e-9 relative (north_star).
+Sizes span several tiles with ragged tails; the full-size bench workload is checked
+on a sample of configs the oracle recomputes one by one, plus invariants.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import exact_math as X
+from helpers import assert_result_equals_oracle, assert_trials_equal, oracle_config, oracle_sums
+
+pytestmark = pytest.mark.gpu
+
+D = pytest.importorskip("paper_2405_14105_b200.dsi_sim")
+from paper_2405_14105_b200 import workloads as W  # noqa: E402
+
+SEED = W.SEED
+ALL = D.DSI_F_PER_TRIAL | D.DSI_F_HIST
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run_sim(cfgs, tick, flags=ALL, **kw):
+    sim = D.Simulator(cfgs, tick=tick, seed=kw.pop("seed", SEED), flags=flags, **kw)
+    sim.run()
+    res = sim.reduce()
+    return sim, res
+
+
+def check_against_oracle(sim, res, cfgs, tick, per_trial=True, hist=True, pattern=False, ctx=""):
+    for i, row in enumerate(cfgs):
+        want = oracle_sums(row, tick, SEED, pattern=pattern, hist=hist, per_trial=per_trial)
+        assert_result_equals_oracle(res[i], want, tick, ctx=f"{ctx} cfg {i}")
+        if per_trial:
+            assert_trials_equal(sim.trials(i), want, ctx=f"{ctx} cfg {i}")
+        if hist:
+            seg, si = sim.hist(i)
+            assert np.array_equal(seg, want["seg_hist"]), (ctx, i, "seg_hist")
+            assert np.array_equal(si, want["si_hist"]), (ctx, i, "si_hist")
+
+
+def test_cfg1_bit_exact():
+    cfgs, tick = W.cfg1(trials=1000)
+    sim, res = run_sim(cfgs, tick)
+    check_against_oracle(sim, res, cfgs, tick, ctx="cfg1")
+    assert res[0]["eq1_feasible"] == 1 and res[0]["min_lookahead"] == 5
+    sim.close()
+
+
+def test_fuzz_bit_exact():
+    """Edge cases: SP 1..8, k 1..12 and k > N, N in {1,2,3,..}, a in {0,1,rand}, Eq. 1 violated."""
+    cfgs, tick = W.fuzz(160, seed=11, trials=300)
+    sim, res = run_sim(cfgs, tick)
+    check_against_oracle(sim, res, cfgs, tick, ctx="fuzz")
+    sim.close()
+
+
+def test_cfg2_table2_rows_subsample_bit_exact():
+    cfgs, tick = W.cfg2(trials=2000)
+    sim, res = run_sim(cfgs, tick)
+    check_against_oracle(sim, res, cfgs, tick, ctx="cfg2")
+    sim.close()
+
+
+def test_cfg4_ragged_tiles_bit_exact():
+    """N = 500 (16 Philox words), trials not a multiple of the block or the tile."""
+    cfgs, tick = W.cfg4(trials=777)
+    cfgs = cfgs[::9]
+    sim, res = run_sim(cfgs, tick)
+    check_against_oracle(sim, res, cfgs, tick, ctx="cfg4")
+    sim.close()
+
+
+def test_long_sequences_bit_exact():
+    """N up to 1000 (config 5) and N = 4097 (an odd tail of the last Philox word)."""
+    rows = [(1.0, 0.05, 0.9, 3, 7, 1000, 0, 257), (1.0, 0.3, 0.5, 2, 3, 4097, 1, 65),
+            (1.0, 1.0, 0.97, 1, 1, 1000, 2, 130)]
+    cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
+    for i, r in enumerate(rows):
+        cfgs[i] = r
+    sim, res = run_sim(cfgs, 0.01)
+    check_against_oracle(sim, res, cfgs, 0.01, ctx="long")
+    sim.close()
+
+
+@pytest.mark.parametrize("N", [1, 2, 5, 12])
+def test_pattern_mode_enumerates_every_pattern(N):
+    """Enumeration mode: trial i's indicators are the bits of i; all 2^(N-1) patterns,
+    each bit-exact against the oracle, and the weighted sum equals the exact h(g) form."""
+    rows = [(100.0, 30.0, 0.5, 2, 2, N, 0, 1 << (N - 1)), (100.0, 7.0, 0.5, 4, 3, N, 0, 1 << (N - 1)),
+            (100.0, 30.0, 0.5, 2, 1, N, 0, 1 << (N - 1))]
+    cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
+    for i, r in enumerate(rows):
+        cfgs[i] = r
+    sim, res = run_sim(cfgs, 1.0, flags=ALL | D.DSI_F_PATTERN)
+    check_against_oracle(sim, res, cfgs, 1.0, pattern=True, ctx=f"pattern N={N}")
+    from fractions import Fraction
+    for i, row in enumerate(cfgs):
+        tr = sim.trials(i)
+        a = Fraction(2, 3)
+
+        def per_pattern(A):
+            j = X.pattern_index(A)
+            return {"dsi": int(tr["dsi"][j]), "iters": int(tr["iters"][j])}
+
+        got = X.enumerate_expectations(N, a, per_pattern)
+        want = X.expectations(N, int(row["lookahead"]), int(row["t_drafter"]), int(row["t_target"]),
+                              int(row["sp_degree"]), a)
+        assert got["dsi"] == want["dsi"] and got["iters"] == want["iters"]
+    sim.close()
+
+
+def test_shard_and_block_invariance():
+    """The same seeded work split into 1..7 cost-balanced shards or run with other block
+    sizes gives bit-identical per-trial records and sums (multi-GPU contract)."""
+    cfgs, tick = W.fuzz(40, seed=3, trials=1000)
+    base_sim, base = run_sim(cfgs, tick)
+    base_tr = [base_sim.trials(i) for i in range(cfgs.size)]
+    for kw in (dict(n_shards=2), dict(n_shards=3), dict(n_shards=7), dict(block_threads=32),
+               dict(block_threads=256), dict(block_threads=96, n_shards=5)):
+        sim, res = run_sim(cfgs, tick, **kw)
+        for f in ("sum_dsi_ticks", "sum_si_ticks", "sumsq_dsi_ticks", "sum_segments", "n_dsi_gt_si"):
+            assert np.array_equal(res[f], base[f]), (kw, f)
+        for i in range(cfgs.size):
+            assert_trials_equal(sim.trials(i), base_tr[i], ctx=str(kw))
+        if kw.get("n_shards", 1) > 1:
+            assert sim.launches() == kw["n_shards"]
+        sim.close()
+    base_sim.close()
+
+
+def test_production_variant_matches_test_variant():
+    """The kernel the bench runs (no per-trial records, no histograms) gives the same sums."""
+    cfgs, tick = W.fuzz(60, seed=8, trials=900)
+    sim_a, ra = run_sim(cfgs, tick, flags=ALL)
+    sim_b, rb = run_sim(cfgs, tick, flags=0)
+    for f in ("sum_dsi_ticks", "sum_si_ticks", "sumsq_dsi_ticks", "sumsq_si_ticks", "sum_segments",
+              "sum_si_iters", "n_dsi_gt_nonsi", "n_dsi_gt_si", "mean_dsi", "std_dsi"):
+        assert np.array_equal(ra[f], rb[f]), f
+    sim_a.close()
+    sim_b.close()
+
+
+def test_seed_and_stream_change_the_draws():
+    cfgs, tick = W.cfg1(trials=500)
+    _, r1 = run_sim(cfgs, tick, flags=0)
+    _, r2 = run_sim(cfgs, tick, flags=0, seed=SEED + 1)
+    cfgs2 = cfgs.copy()
+    cfgs2["stream_id"] = 9
+    _, r3 = run_sim(cfgs2, tick, flags=0)
+    assert r1["sum_dsi_ticks"][0] != r2["sum_dsi_ticks"][0]
+    assert r1["sum_dsi_ticks"][0] != r3["sum_dsi_ticks"][0]
+
+
+def test_bench_workload_full_size_sampled():
+    """The bench's workload (cfg3 heatmap, k <= 200, T = 1e4, N = 100) in the bench's launch
+    configuration; a sample of configs is recomputed by the oracle one by one (exact sums),
+    and properties that hold at any size are checked on all 2.02 M configs."""
+    cfgs, tick = W.cfg3()
+    sim = D.Simulator(cfgs, tick=tick, seed=SEED, flags=D.DSI_F_TIMING)
+    sim.run()
+    res = sim.reduce()
+    assert np.all(res["trials"] == 10_000)
+    idx = np.unique(np.linspace(0, cfgs.size - 1, 24).round().astype(int))
+    rng = np.random.default_rng(1)
+    idx = np.unique(np.concatenate([idx, rng.integers(0, cfgs.size, 8)]))
+    for i in idx:
+        want = oracle_sums(cfgs[i], tick, SEED)
+        assert_result_equals_oracle(res[i], want, tick, ctx=f"cfg3[{i}]")
+    # Thm 1 holds per trial wherever k t_d <= t_t; Thm 2 where also Eq. 1 holds (R6)
+    kd = res["t_drafter_ticks"] * cfgs["lookahead"]
+    inside = kd <= res["t_target_ticks"]
+    assert np.all(res["n_dsi_gt_nonsi"][inside] == 0)
+    assert np.all(res["n_dsi_gt_si"][inside & (res["eq1_feasible"] == 1)] == 0)
+    # a = 0: DSI equals non-SI exactly (Thm 1 equality case); a = 1: one segment per trial
+    a0 = cfgs["accept_rate"] == 0.0
+    assert np.all(res["sum_dsi_ticks"][a0] == res["nonsi_ticks"][a0] * 10_000)
+    a1 = cfgs["accept_rate"] == 1.0
+    assert np.all(res["sum_segments"][a1] == 10_000)
+    assert sim.kernel_ms() > 0
+    sim.close()
+
+
+def test_monte_carlo_mean_vs_exact_expectation():
+    """Large-T GPU means sit within 6 sigma of the exact expectation (P11)."""
+    from fractions import Fraction
+    cfgs, tick = W.cfg1(trials=2_000_000)
+    sim, res = run_sim(cfgs, tick, flags=0)
+    r = res[0]
+    p = Fraction(int(r["threshold"]), 2 ** 32)
+    e = X.expectations(50, 5, 10, 100, 2, p)
+    T = int(r["trials"])
+    for mean, std, ex in ((r["mean_dsi"] / tick, r["std_dsi"] / tick, e["dsi"]),
+                          (r["mean_si"] / tick, r["std_si"] / tick, e["si"])):
+        assert abs(mean - float(ex)) < 6 * std / math.sqrt(T)
+    sim.close()
+
+
+def test_api_state_errors():
+    cfgs, tick = W.cfg1(trials=10)
+    sim = D.Simulator(cfgs, tick=tick, seed=SEED, flags=0)
+    with pytest.raises(D.DsiError) as e:
+        sim.reduce()
+    assert e.value.status == D.DSI_E_STATE
+    sim.run()
+    with pytest.raises(D.DsiError) as e:
+        sim.trials(0)
+    assert e.value.status == D.DSI_E_STATE
+    with pytest.raises(D.DsiError) as e:
+        sim.hist(0)
+    assert e.value.status == D.DSI_E_STATE
+    with pytest.raises(D.DsiError) as e:
+        sim.kernel_ms()
+    assert e.value.status == D.DSI_E_STATE
+    sim.reduce()
+    sim.close()
