@@ -65,13 +65,17 @@ struct LaunchParams {
   int32_t *rec_acc, *rec_m, *rec_iters, *rec_si, *rec_dsi;  // DSI_F_PER_TRIAL
   unsigned long long *seg_hist;  // n_cfg * 64              (DSI_F_HIST)
   unsigned long long *si_hist;   // sum over configs of (k_eff + 1)
+  int32_t max_n;                 // largest N over all configs (shared-memory sizing)
+  int32_t max_keff;              // largest min(k, N) over all configs
   Keys keys;
 };
 
+// Dynamic shared memory of the variant chosen for (max_n, max_keff, hist).
+size_t trial_kernel_smem(int max_n, int max_keff, bool hist);
+
 // Launch the trial kernel variant for (per_trial, hist, pattern) on `stream`
 // over units [p.unit_begin, p.unit_begin + n_units).  Returns a cudaError_t.
-// hist_smem: dynamic shared memory for DSI_F_HIST, (64 + max k_eff + 1) * 4 bytes.
 int launch_trial_kernel(const LaunchParams &p, uint64_t n_units, int block_threads,
-                        bool per_trial, bool hist, bool pattern, size_t hist_smem, void *stream);
+                        bool per_trial, bool hist, bool pattern, void *stream);
 
 }  // namespace dsi

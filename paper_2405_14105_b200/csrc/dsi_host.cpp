@@ -134,7 +134,7 @@ struct dsi_sim {
   uint64_t total_trials = 0;
   uint32_t tile_trials = 0;
   int block_threads = kDefaultThreads;
-  size_t hist_smem = 0;
+  int32_t max_n = 1, max_keff = 1;
   uint64_t si_bins_total = 0;
   std::vector<DeviceState> dev;
   Pinned<unsigned long long> host_acc, host_seg, host_si;  // D2H targets
@@ -450,8 +450,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     return abort_create(DSI_E_RANGE);
   }
   h->si_bins_total = sib;
-  h->hist_smem = (64 + max_keff + 1) * sizeof(unsigned int);
-  if ((opt->flags & DSI_F_HIST) && h->hist_smem > 200 * 1024) {
+  for (size_t i = 0; i < n_cfg; ++i) h->max_n = std::max(h->max_n, h->ticks[i].n);
+  h->max_keff = (int32_t)max_keff;
+  if (dsi::trial_kernel_smem(h->max_n, h->max_keff, opt->flags & DSI_F_HIST) > 200 * 1024) {
     h->err = "DSI_F_HIST needs (64 + k + 1) * 4 bytes of shared memory <= 200 KiB";
     return abort_create(DSI_E_RANGE);
   }
@@ -669,6 +670,8 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     }
     p.seg_hist = d.d_seg;
     p.si_hist = d.d_si;
+    p.max_n = h->max_n;
+    p.max_keff = h->max_keff;
     const uint32_t s_lo = (uint32_t)h->opt.seed, s_hi = (uint32_t)(h->opt.seed >> 32);
     for (int r = 0; r < 10; ++r) {
       p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;
@@ -680,7 +683,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       p.unit_begin = rg.first;
       const int e = dsi::launch_trial_kernel(p, rg.second - rg.first, h->block_threads,
                                              h->opt.flags & DSI_F_PER_TRIAL, h->opt.flags & DSI_F_HIST,
-                                             h->opt.flags & DSI_F_PATTERN, h->hist_smem, d.stream);
+                                             h->opt.flags & DSI_F_PATTERN, d.stream);
       if (e) return cuda_fail(h, (cudaError_t)e, "trial kernel launch");
       h->launches += 1;
     }

@@ -3,18 +3,31 @@
 // One thread simulates one trial at a time.  A block owns one work unit
 // (configuration c, tile of up to tile_trials consecutive trials); its threads
 // stride over the tile.  Per trial:
-//   1. Philox4x32-10 in registers, 8 calls per 32 positions (4 words per call);
-//      A_p = [u < thr] for p = 1..N-1 is packed as a rejection mask (bit = A_p == 0).
+//   1. Philox4x32-10 in registers, 8 calls per 32 positions; A_p = [u < thr] for
+//      p = 1..N-1 is packed as a rejection mask (bit i of word w = position 32w+i+1,
+//      set when A_p = 0) with a carry chain (add.cc/addc: 2 instructions per bit).
 //   2. The zeros of the mask cut the trial into segments g_1..g_m (sum g = N).
 //      Every segment starts with all servers free (a rejection terminates every
 //      thread, Alg. 1 lines 8/10), so its costs depend on g only:
 //        SI: ceil(g/(k+1)) iterations of k t_d + t_t
 //        DSI (Alg. 1 P:112-142 + App. D): C(g) = t_t + S(ceil((g-1)/k)),
 //            S(b) = max(b k t_d, (b mod SP) k t_d + floor(b/SP) t_t)  (FIFO, R7)
+//      A segment of length 1 costs exactly (1 SI iteration, t_t), so
+//        I = m + sum_{g>=2} (ceil(g/(k+1)) - 1),  L_DSI = m t_t + sum_{g>=2} S(b(g)),
+//      and only segments with g >= 2 are walked: they end at a zero whose
+//      predecessor is an accepted draft (mask E = R & ~(R << 1 | carry)).
 //   3. Integer moments are reduced with warp shuffles and added to the
 //      per-config accumulators with 64-bit integer atomics (exact, order-free).
-// Nothing here is a contraction: the kernel is bound by the SM issue rate
-// (Philox is ~10 integer instructions per trial-token), not by HBM or tensor cores.
+//
+// Where the time goes (ncu): Philox's 32x32->64 multiplies (IMAD.WIDE,
+// ~4 cycles of the fmaheavy pipe each) bound the kernel.  So
+//   - rounds 0 and 1 carry no multiply that depends on both the trial and the
+//     counter q: the trial half is hoisted per trial, the q half (uniform across
+//     the warp) is precomputed per block into shared memory (U table);
+//   - the per-segment divisions become a shared-memory table T[g] = (ceil(g/(k+1))-1,
+//     S(ceil((g-1)/k))) read with LDS, keeping the walk off the fmaheavy pipe.
+// Nothing here is a contraction: no tensor cores, and HBM traffic is only the
+// per-config result write-back.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,33 +38,71 @@ namespace {
 
 constexpr uint32_t PHILOX_M0 = 0xD2511F53u;
 constexpr uint32_t PHILOX_M1 = 0xCD9E8D57u;
+constexpr int TABLE_MAX_N = 4096;  // larger N: arithmetic segment costs, per-call rounds 0-1
 
 struct Word4 {
   uint32_t x, y, z, w;
 };
 
-// Philox4x32-10 for counter (q, 0, trial, stream).  Round 0 depends on q only
-// through M0*q; its trial half (M1*trial) is hoisted per trial by the caller:
-//   r0_c0 = hi(M1*trial) ^ 0 ^ k0[0],  r0_c1 = lo(M1*trial),  sk1 = stream ^ k1[0].
-__device__ __forceinline__ Word4 philox_q(uint32_t q, uint32_t r0_c0, uint32_t r0_c1, uint32_t sk1,
-                                          const Keys &K) {
-  uint64_t p0 = (uint64_t)PHILOX_M0 * q;
-  uint32_t c0 = r0_c0;
-  uint32_t c1 = r0_c1;
-  uint32_t c2 = (uint32_t)(p0 >> 32) ^ sk1;
-  uint32_t c3 = (uint32_t)p0;
+// Philox rounds 2..9 from the round-1 output (c0, c1, c2, c3).
+__device__ __forceinline__ Word4 philox_rounds_2_9(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                   const Keys &K) {
 #pragma unroll
-  for (int r = 1; r < 10; ++r) {
-    uint64_t a = (uint64_t)PHILOX_M0 * c0;
-    uint64_t b = (uint64_t)PHILOX_M1 * c2;
-    uint32_t n0 = (uint32_t)(b >> 32) ^ c1 ^ K.k0[r];
-    uint32_t n2 = (uint32_t)(a >> 32) ^ c3 ^ K.k1[r];
+  for (int r = 2; r < 10; ++r) {
+    const uint64_t a = (uint64_t)PHILOX_M0 * c0;
+    const uint64_t b = (uint64_t)PHILOX_M1 * c2;
+    const uint32_t n0 = (uint32_t)(b >> 32) ^ c1 ^ K.k0[r];
+    const uint32_t n2 = (uint32_t)(a >> 32) ^ c3 ^ K.k1[r];
     c1 = (uint32_t)b;
     c3 = (uint32_t)a;
     c0 = n0;
     c2 = n2;
   }
   return Word4{c0, c1, c2, c3};
+}
+
+// Per-q half of rounds 0-1 for counter (q, 0, trial, stream):
+//   round 0: n2 = hi(M0 q) ^ stream ^ k1[0], n3 = lo(M0 q)
+//   round 1: (hi(M1 n2) ^ k0[1], lo(M1 n2), n3 ^ k1[1])
+__device__ __forceinline__ uint4 philox_q_half(uint32_t q, uint32_t stream, const Keys &K) {
+  const uint64_t p = (uint64_t)PHILOX_M0 * q;
+  const uint32_t n2 = (uint32_t)(p >> 32) ^ stream ^ K.k1[0];
+  const uint64_t b = (uint64_t)PHILOX_M1 * n2;
+  return make_uint4((uint32_t)(b >> 32) ^ K.k0[1], (uint32_t)b, (uint32_t)p ^ K.k1[1], 0u);
+}
+
+// Per-trial half of rounds 0-1: n0 = hi(M1 trial) ^ k0[0], n1 = lo(M1 trial),
+// then a = M0 n0 gives (hi(a), lo(a)).
+struct TrialHalf {
+  uint32_t n1, ha, la;
+};
+__device__ __forceinline__ TrialHalf philox_trial_half(uint32_t trial, const Keys &K) {
+  const uint64_t p = (uint64_t)PHILOX_M1 * trial;
+  const uint32_t n0 = (uint32_t)(p >> 32) ^ K.k0[0];
+  const uint64_t a = (uint64_t)PHILOX_M0 * n0;
+  return TrialHalf{(uint32_t)p, (uint32_t)(a >> 32), (uint32_t)a};
+}
+
+// Full Philox4x32-10 output for (q, 0, trial, stream) from the two halves.
+__device__ __forceinline__ Word4 philox_call(const uint4 &u, const TrialHalf &t, const Keys &K) {
+  return philox_rounds_2_9(u.x ^ t.n1, u.y, t.ha ^ u.z, t.la, K);
+}
+
+// rej = (rej << 4) | [w >= thr] << 3 | [z >= thr] << 2 | [y >= thr] << 1 | [x >= thr]
+// from the carries of u + (2^32 - thr) (thr >= 1): 2 ALU instructions per bit.
+__device__ __forceinline__ uint32_t pack4(uint32_t rej, const Word4 &u, uint32_t nthr) {
+  uint32_t t;
+  asm("add.cc.u32 %1, %2, %6;\n\t"
+      "addc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %1, %3, %6;\n\t"
+      "addc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %1, %4, %6;\n\t"
+      "addc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %1, %5, %6;\n\t"
+      "addc.u32 %0, %0, %0;"
+      : "+r"(rej), "=&r"(t)
+      : "r"(u.w), "r"(u.z), "r"(u.y), "r"(u.x), "r"(nthr));
+  return rej;
 }
 
 // floor(x / d) for x * d <= 2^32 with M = ceil(2^32 / d) = lo + hi * 2^32.
@@ -68,40 +119,39 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 struct SegCtx {
   uint32_t k_eff, m_si, m_k_lo, m_k_hi, m_sp_lo, m_sp_hi;
   int32_t sp_eff, kd, t_t, n_tokens;
-  bool noqueue;
 };
 
-template <bool HIST>
-__device__ __forceinline__ void segment(int g, int seg_start, const SegCtx &s, int &iters,
-                                        int &sum_b, int &sum_s, unsigned int *sh_seg,
-                                        unsigned int *sh_si) {
-  // SI iterations in this segment: ceil(g / (k+1)) = floor((g + k) / (k+1))
-  uint32_t M = magic_div((uint32_t)g + s.k_eff, s.m_si, 0u);
-  iters += (int)M;
-  // DSI: the last position of the segment is settled by thread b = ceil((g-1)/k)
-  uint32_t b = magic_div((uint32_t)g + s.k_eff - 2u, s.m_k_lo, s.m_k_hi);
-  if (s.noqueue) {
-    sum_b += (int)b;  // S(b) = b k t_d
-  } else {
-    uint32_t qq = magic_div(b, s.m_sp_lo, s.m_sp_hi);
-    int rr = (int)b - (int)qq * s.sp_eff;
-    sum_s += max((int)b * s.kd, rr * s.kd + (int)qq * s.t_t);
-  }
-  if (HIST) {
-    atomicAdd(&sh_seg[g < 63 ? g : 63], 1u);
-    // the first M-1 SI iterations of a segment accept k drafts each; the last
-    // accepts r-1 and is counted only if its k-draft window ends before N
-    int kk = (int)s.k_eff;
-    if (M > 1) atomicAdd(&sh_si[kk], M - 1u);
-    int last_start = seg_start + ((int)M - 1) * (kk + 1);
-    int r = g - ((int)M - 1) * (kk + 1);
-    if (last_start + kk + 1 <= s.n_tokens) atomicAdd(&sh_si[r - 1], 1u);
-  }
+// Segment costs beyond those of a length-1 segment: (ceil(g/(k+1)) - 1, S(ceil((g-1)/k))).
+__device__ __forceinline__ uint2 seg_extra(int g, const SegCtx &s) {
+  const uint32_t M = magic_div((uint32_t)g + s.k_eff, s.m_si, 0u);              // ceil(g/(k+1))
+  const uint32_t b = magic_div((uint32_t)g + s.k_eff - 2u, s.m_k_lo, s.m_k_hi);  // ceil((g-1)/k)
+  const uint32_t qq = magic_div(b, s.m_sp_lo, s.m_sp_hi);
+  const int rr = (int)b - (int)qq * s.sp_eff;
+  const int S = max((int)b * s.kd, rr * s.kd + (int)qq * s.t_t);
+  return make_uint2(M - 1u, (uint32_t)S);
 }
 
-template <bool PER_TRIAL, bool HIST, bool PATTERN>
+// Test-mode (DSI_F_HIST) accounting of one segment into the block histograms.
+__device__ __forceinline__ void seg_hist(int g, int seg_start, const SegCtx &s, unsigned int *sh_seg,
+                                         unsigned int *sh_si) {
+  atomicAdd(&sh_seg[g < 63 ? g : 63], 1u);
+  // the first M-1 SI iterations of a segment accept k drafts each; the last
+  // accepts r-1 and is counted only if its k-draft window ends before N
+  const int kk = (int)s.k_eff;
+  const int M = (int)magic_div((uint32_t)g + s.k_eff, s.m_si, 0u);
+  if (M > 1) atomicAdd(&sh_si[kk], (unsigned)(M - 1));
+  const int last_start = seg_start + (M - 1) * (kk + 1);
+  const int r = g - (M - 1) * (kk + 1);
+  if (last_start + kk + 1 <= s.n_tokens) atomicAdd(&sh_si[r - 1], 1u);
+}
+
+// Shared-memory layout of the TABLE variant for a config with N tokens.
+__host__ __device__ __forceinline__ size_t t_table_bytes(int n) { return (size_t)((n + 2) & ~1) * 8; }
+__host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t)((n - 1 + 3) / 4 + 1) * 16; }
+
+template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE>
 __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
-  extern __shared__ unsigned int sh_hist[];  // HIST only: 64 segment bins + k_eff+1 SI bins
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t s_cfg;
 
   const uint64_t unit = P.unit_begin + blockIdx.x;
@@ -109,7 +159,7 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
     // config owning this unit: largest c with tile_prefix[c] <= unit
     uint32_t lo = 0, hi = P.n_cfg;  // invariant: prefix[lo] <= unit < prefix[hi]
     while (hi - lo > 1) {
-      uint32_t mid = (lo + hi) >> 1;
+      const uint32_t mid = (lo + hi) >> 1;
       if (__ldg(&P.tile_prefix[mid]) <= unit) lo = mid; else hi = mid;
     }
     s_cfg = lo;
@@ -125,6 +175,7 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   const int N = cfg.n_tokens;
   const int npos = N - 1;  // positions carrying an indicator
   const int nwords = (npos + 31) >> 5;
+  const int nq = (npos + 3) >> 2;
   SegCtx s;
   s.k_eff = (uint32_t)cfg.k_eff;
   s.m_si = cfg.m_si;
@@ -136,68 +187,104 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   s.kd = cfg.kd;
   s.t_t = cfg.t_t;
   s.n_tokens = N;
-  s.noqueue = (cfg.flags & CFG_NOQUEUE) != 0;
-  const uint32_t thr = cfg.thr;
-  const uint32_t sk1 = cfg.stream_id ^ P.keys.k1[0];
-  const int64_t nonsi = (int64_t)N * cfg.t_t;
+  const uint32_t nthr = 0u - cfg.thr;  // carry of u + nthr <=> u >= thr (thr >= 1 in stream mode)
+  const bool stream = !PATTERN && mode == MODE_STREAM;
 
-  unsigned int *sh_seg = sh_hist;
-  unsigned int *sh_si = sh_hist + 64;
-  if (HIST) {
-    for (int i = threadIdx.x; i < 64 + cfg.k_eff + 1; i += blockDim.x) sh_hist[i] = 0u;
-    __syncthreads();
+  // shared memory: TABLE -> T[g] (g = 0..N) then U[q] (q < nq); HIST -> histograms
+  uint2 *T = reinterpret_cast<uint2 *>(smem);
+  uint4 *U = reinterpret_cast<uint4 *>(smem + t_table_bytes(N));
+  unsigned int *sh_seg = reinterpret_cast<unsigned int *>(smem);
+  unsigned int *sh_si = sh_seg + 64;
+  if (TABLE) {
+    for (int g = threadIdx.x; g <= N; g += blockDim.x) T[g] = g >= 1 ? seg_extra(g, s) : make_uint2(0u, 0u);
+    if (stream)
+      for (int q = threadIdx.x; q < nq; q += blockDim.x) U[q] = philox_q_half((uint32_t)q, cfg.stream_id, P.keys);
   }
+  if (HIST)
+    for (int i = threadIdx.x; i < 64 + cfg.k_eff + 1; i += blockDim.x) sh_seg[i] = 0u;
+  if (TABLE || HIST) __syncthreads();
 
   unsigned long long a_m = 0, a_i = 0, a_i2 = 0, a_dsi = 0, a_dsi2 = 0, a_gtn = 0, a_gts = 0,
                      a_trials = 0;
+  const int64_t nonsi = (int64_t)N * cfg.t_t;
 
   for (uint64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     const uint32_t trial = (uint32_t)t;
-    const uint64_t pt = (uint64_t)PHILOX_M1 * trial;
-    const uint32_t r0_c0 = (uint32_t)(pt >> 32) ^ P.keys.k0[0];
-    const uint32_t r0_c1 = (uint32_t)pt;
+    const TrialHalf th = philox_trial_half(trial, P.keys);
 
-    int prev = 0, nz = 0, iters = 0, sum_b = 0, sum_s = 0;
+    int nz = 0;        // zeros (rejections) among positions 1..N-1
+    int lastz = 0;     // position of the last zero so far (0 = sentinel before position 1)
+    uint32_t cin = 1;  // position 32w is a zero (the sentinel for w = 0)
+    uint32_t ai = 0, ay = 0;  // sums of T[g].x, T[g].y over segments with g >= 2
     for (int w = 0; w < nwords; ++w) {
-      uint32_t rej;
+      uint32_t R;
       if (PATTERN) {
-        rej = ~trial;  // N <= 33: one word, A_p = bit p-1 of the trial index
+        R = ~trial;  // N <= 33: one word, A_p = bit p-1 of the trial index
       } else if (mode == MODE_STREAM) {
-        rej = 0u;
-        const int ncalls = min(8, (npos - 32 * w + 3) >> 2);
+        R = 0u;
+        const int ncalls = min(8, nq - 8 * w);
         if (ncalls == 8) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            Word4 u = philox_q((uint32_t)(8 * w + j), r0_c0, r0_c1, sk1, P.keys);
-            rej |= ((uint32_t)(u.x >= thr) | ((uint32_t)(u.y >= thr) << 1) |
-                    ((uint32_t)(u.z >= thr) << 2) | ((uint32_t)(u.w >= thr) << 3))
-                   << (4 * j);
+          for (int j = 7; j >= 0; --j) {
+            const uint4 u = TABLE ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), cfg.stream_id, P.keys);
+            R = pack4(R, philox_call(u, th, P.keys), nthr);
           }
         } else {
-          for (int j = 0; j < ncalls; ++j) {
-            Word4 u = philox_q((uint32_t)(8 * w + j), r0_c0, r0_c1, sk1, P.keys);
-            rej |= ((uint32_t)(u.x >= thr) | ((uint32_t)(u.y >= thr) << 1) |
-                    ((uint32_t)(u.z >= thr) << 2) | ((uint32_t)(u.w >= thr) << 3))
-                   << (4 * j);
+          for (int j = ncalls - 1; j >= 0; --j) {
+            const uint4 u = TABLE ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), cfg.stream_id, P.keys);
+            R = pack4(R, philox_call(u, th, P.keys), nthr);
           }
         }
       } else {
-        rej = (mode == MODE_ALL_REJECT) ? 0xffffffffu : 0u;
+        R = (mode == MODE_ALL_REJECT) ? 0xffffffffu : 0u;
       }
-      const int rem = npos - 32 * w;  // positions 32w+1 .. 32w+32 map to bits 0..31
-      if (rem < 32) rej &= (1u << rem) - 1u;
-      nz += __popc(rej);
-      while (rej) {
-        const int z = 32 * w + __ffs(rej);  // position of the next rejection
-        rej &= rej - 1u;
-        segment<HIST>(z - prev, prev, s, iters, sum_b, sum_s, sh_seg, sh_si);
-        prev = z;
+      const int base = 32 * w + 1;  // position of bit 0
+      const int rem = npos - 32 * w;
+      if (rem < 32) R &= (1u << rem) - 1u;
+      nz += __popc(R);
+      if (HIST) {
+        // test mode: walk every zero (all segments, with histograms)
+        uint32_t Z = R;
+        while (Z) {
+          const int z = base + __ffs(Z) - 1;
+          Z &= Z - 1u;
+          const int g = z - lastz;
+          seg_hist(g, lastz, s, sh_seg, sh_si);
+          if (g >= 2) {
+            const uint2 e = TABLE ? T[g] : seg_extra(g, s);
+            ai += e.x;
+            ay += e.y;
+          }
+          lastz = z;
+        }
+      } else {
+        // ends of segments with g >= 2: a zero whose predecessor position is a one
+        uint32_t E = R & ~((R << 1) | cin);
+        while (E) {
+          const int zb = 31 - __clz(E);
+          E ^= 1u << zb;
+          const uint32_t below = R & ((1u << zb) - 1u);
+          const int prev = below ? base + 31 - __clz(below) : lastz;
+          const int g = base + zb - prev;
+          const uint2 e = TABLE ? T[g] : seg_extra(g, s);
+          ai += e.x;
+          ay += e.y;
+        }
+        if (R) lastz = base + 31 - __clz(R);
       }
+      cin = R >> 31;
     }
-    segment<HIST>(N - prev, prev, s, iters, sum_b, sum_s, sh_seg, sh_si);  // final segment ends at N
+    const int gl = N - lastz;  // the final segment ends at N
+    if (HIST) seg_hist(gl, lastz, s, sh_seg, sh_si);
+    if (gl >= 2) {
+      const uint2 e = TABLE ? T[gl] : seg_extra(gl, s);
+      ai += e.x;
+      ay += e.y;
+    }
 
     const int m = nz + 1;
-    const int64_t dsi = (int64_t)m * cfg.t_t + (s.noqueue ? (int64_t)sum_b * cfg.kd : (int64_t)sum_s);
+    const int iters = m + (int)ai;
+    const int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)ay;
     const int64_t si = (int64_t)iters * cfg.si_cost;
     a_m += (unsigned)m;
     a_i += (unsigned)iters;
@@ -246,15 +333,19 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   }
 }
 
-template <bool A, bool B, bool C>
-int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t smem,
-                   cudaStream_t st) {
+template <bool A, bool B, bool C, bool D>
+int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(dsi_trial_kernel<A, B, C, D>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
   const uint64_t max_grid = 0x7fffffffull;
   LaunchParams q = p;
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_trial_kernel<A, B, C><<<(unsigned)n, threads, smem, st>>>(q);
+    dsi_trial_kernel<A, B, C, D><<<(unsigned)n, threads, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
@@ -264,32 +355,40 @@ int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t 
 
 }  // namespace
 
+size_t trial_kernel_smem(int max_n, int max_keff, bool hist) {
+  if (hist) return (size_t)(64 + max_keff + 1) * sizeof(unsigned int);
+  if (max_n > TABLE_MAX_N) return 0;
+  return t_table_bytes(max_n) + u_table_bytes(max_n);
+}
+
 int launch_trial_kernel(const LaunchParams &p, uint64_t n_units, int block_threads, bool per_trial,
-                        bool hist, bool pattern, size_t hist_smem, void *stream) {
+                        bool hist, bool pattern, void *stream) {
   if (n_units == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = hist ? hist_smem : 0;
-  if (hist && smem > 48 * 1024) {
-    // the attribute is per device; setting it before every launch is cheap
-    cudaFuncSetAttribute(dsi_trial_kernel<false, true, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(dsi_trial_kernel<true, true, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(dsi_trial_kernel<false, true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(dsi_trial_kernel<true, true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = trial_kernel_smem(p.max_n, p.max_keff, hist);
+  const int code = (per_trial ? 2 : 0) | (pattern ? 1 : 0);
+  if (hist) {
+    // histograms occupy shared memory: segment costs come from arithmetic
+    switch (code) {
+      case 0: return launch_variant<false, true, false, false>(p, n_units, block_threads, smem, st);
+      case 1: return launch_variant<false, true, true, false>(p, n_units, block_threads, smem, st);
+      case 2: return launch_variant<true, true, false, false>(p, n_units, block_threads, smem, st);
+      default: return launch_variant<true, true, true, false>(p, n_units, block_threads, smem, st);
+    }
   }
-  const int code = (per_trial ? 4 : 0) | (hist ? 2 : 0) | (pattern ? 1 : 0);
+  if (p.max_n <= TABLE_MAX_N) {
+    switch (code) {
+      case 0: return launch_variant<false, false, false, true>(p, n_units, block_threads, smem, st);
+      case 1: return launch_variant<false, false, true, true>(p, n_units, block_threads, smem, st);
+      case 2: return launch_variant<true, false, false, true>(p, n_units, block_threads, smem, st);
+      default: return launch_variant<true, false, true, true>(p, n_units, block_threads, smem, st);
+    }
+  }
   switch (code) {
-    case 0: return launch_variant<false, false, false>(p, n_units, block_threads, smem, st);
-    case 1: return launch_variant<false, false, true>(p, n_units, block_threads, smem, st);
-    case 2: return launch_variant<false, true, false>(p, n_units, block_threads, smem, st);
-    case 3: return launch_variant<false, true, true>(p, n_units, block_threads, smem, st);
-    case 4: return launch_variant<true, false, false>(p, n_units, block_threads, smem, st);
-    case 5: return launch_variant<true, false, true>(p, n_units, block_threads, smem, st);
-    case 6: return launch_variant<true, true, false>(p, n_units, block_threads, smem, st);
-    default: return launch_variant<true, true, true>(p, n_units, block_threads, smem, st);
+    case 0: return launch_variant<false, false, false, false>(p, n_units, block_threads, 0, st);
+    case 1: return launch_variant<false, false, true, false>(p, n_units, block_threads, 0, st);
+    case 2: return launch_variant<true, false, false, false>(p, n_units, block_threads, 0, st);
+    default: return launch_variant<true, false, true, false>(p, n_units, block_threads, 0, st);
   }
 }
 
