@@ -31,7 +31,7 @@ struct alignas(16) DevCfg {
   uint32_t m_sp_lo;    // ceil(2^32 / sp_eff) mod 2^32      : x / sp_eff
   uint32_t m_sp_hi;
   uint32_t si_hist_off;  // first SI-histogram bin of this config (DSI_F_HIST)
-  uint32_t pad;
+  int32_t s1;            // S(1): DSI cost of any segment with 2 <= g <= k+1 beyond t_t
   uint64_t rec_off;      // first per-trial record of this config (DSI_F_PER_TRIAL)
   uint64_t n_trials;
 };

@@ -232,6 +232,8 @@ DevCfg make_dev_cfg(const CfgTicks &t, bool pattern) {
   d.t_t = (int32_t)t.t_t;
   d.kd = (int32_t)t.kd;
   d.si_cost = (int32_t)(t.kd + t.t_t);
+  // S(1) = max(k t_d, (1 mod SP) k t_d + floor(1/SP) t_t): k t_d, or max(k t_d, t_t) if SP = 1
+  d.s1 = (int32_t)(t.sp >= 2 ? t.kd : std::max(t.kd, t.t_t));
   d.stream_id = t.stream_id;
   uint32_t hi;
   magic((uint32_t)k_eff + 1u, d.m_si, hi);  // k_eff + 1 >= 2: hi == 0

@@ -118,7 +118,7 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 
 struct SegCtx {
   uint32_t k_eff, m_si, m_k_lo, m_k_hi, m_sp_lo, m_sp_hi;
-  int32_t sp_eff, kd, t_t, n_tokens;
+  int32_t sp_eff, kd, t_t, n_tokens, s1;
 };
 
 // Segment costs beyond those of a length-1 segment: (ceil(g/(k+1)) - 1, S(ceil((g-1)/k))).
@@ -129,6 +129,26 @@ __device__ __forceinline__ uint2 seg_extra(int g, const SegCtx &s) {
   const int rr = (int)b - (int)qq * s.sp_eff;
   const int S = max((int)b * s.kd, rr * s.kd + (int)qq * s.t_t);
   return make_uint2(M - 1u, (uint32_t)S);
+}
+
+// Costs of a long segment (g >= k+2) beyond those of a short one (2 <= g <= k+1,
+// which always costs (0 extra SI iterations, S(1))): seg_extra(g) - (0, S(1)).
+__device__ __forceinline__ uint2 seg_long(int g, const SegCtx &s) {
+  const uint2 e = seg_extra(g, s);
+  return make_uint2(e.x, e.y - (uint32_t)s.s1);
+}
+
+// Bits i of x such that bits i-n+1 .. i are all ones (runs of at least n ones),
+// by log-doubling: y_s marks runs >= s, then y_s & (y_s << (n - s)) for s <= n < 2s.
+__device__ __forceinline__ uint32_t runs_at_least(uint32_t x, int n) {
+  uint32_t y = x;
+  int sh = 1;
+  while (2 * sh <= n) {
+    y &= y << sh;
+    sh <<= 1;
+  }
+  if (sh < n) y &= y << (n - sh);
+  return y;
 }
 
 // Test-mode (DSI_F_HIST) accounting of one segment into the block histograms.
@@ -187,6 +207,8 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   s.kd = cfg.kd;
   s.t_t = cfg.t_t;
   s.n_tokens = N;
+  s.s1 = cfg.s1;
+  const int Lk = cfg.k_eff + 1;  // a run of >= k+1 accepted drafts makes a long segment
   const uint32_t nthr = 0u - cfg.thr;  // carry of u + nthr <=> u >= thr (thr >= 1 in stream mode)
   const bool stream = !PATTERN && mode == MODE_STREAM;
 
@@ -196,7 +218,7 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   unsigned int *sh_seg = reinterpret_cast<unsigned int *>(smem);
   unsigned int *sh_si = sh_seg + 64;
   if (TABLE) {
-    for (int g = threadIdx.x; g <= N; g += blockDim.x) T[g] = g >= 1 ? seg_extra(g, s) : make_uint2(0u, 0u);
+    for (int g = threadIdx.x; g <= N; g += blockDim.x) T[g] = g >= 2 ? (HIST ? seg_extra(g, s) : seg_long(g, s)) : make_uint2(0u, 0u);
     if (stream)
       for (int q = threadIdx.x; q < nq; q += blockDim.x) U[q] = philox_q_half((uint32_t)q, cfg.stream_id, P.keys);
   }
@@ -213,9 +235,12 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
     const TrialHalf th = philox_trial_half(trial, P.keys);
 
     int nz = 0;        // zeros (rejections) among positions 1..N-1
-    int lastz = 0;     // position of the last zero so far (0 = sentinel before position 1)
-    uint32_t cin = 1;  // position 32w is a zero (the sentinel for w = 0)
-    uint32_t ai = 0, ay = 0;  // sums of T[g].x, T[g].y over segments with g >= 2
+    int n2 = 0;        // segments with g >= 2 (production walk)
+    int run = 0;       // accepted drafts since the last zero (production walk)
+    int lastz = 0;     // HIST walk: position of the last zero (0 = sentinel before position 1)
+    uint32_t cin = 1;  // HIST walk: position 32w is a zero (the sentinel for w = 0)
+    uint32_t ai = 0, ay = 0;  // summed extra costs (HIST: seg_extra of every g >= 2 segment;
+                              // production: seg_long of every segment with g >= k+2)
     for (int w = 0; w < nwords; ++w) {
       uint32_t R;
       if (PATTERN) {
@@ -258,33 +283,61 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
           lastz = z;
         }
       } else {
-        // ends of segments with g >= 2: a zero whose predecessor position is a one
-        uint32_t E = R & ~((R << 1) | cin);
-        while (E) {
-          const int zb = 31 - __clz(E);
-          E ^= 1u << zb;
-          const uint32_t below = R & ((1u << zb) - 1u);
-          const int prev = below ? base + 31 - __clz(below) : lastz;
-          const int g = base + zb - prev;
-          const uint2 e = TABLE ? T[g] : seg_extra(g, s);
-          ai += e.x;
-          ay += e.y;
+        // Segments with g >= 2 end at a zero whose predecessor is a one (mask E);
+        // each costs (0, S(1)) unless its run of ones is long (L = g-1 >= k+1).
+        const int nv = min(rem, 32);  // valid positions in this word
+        if (R == 0) {
+          run += nv;  // the run of accepted drafts continues through the word
+        } else {
+          const uint32_t E = R & ~((R << 1) | (run == 0 ? 1u : 0u));
+          n2 += __popc(E);
+          const int z0 = __ffs(R) - 1;  // the first zero closes the run carried in
+          if (run + z0 >= Lk) {
+            const uint2 e = TABLE ? T[run + z0 + 1] : seg_long(run + z0 + 1, s);
+            ai += e.x;
+            ay += e.y;
+          }
+          if (Lk <= 30) {
+            // runs of >= Lk ones strictly inside the word (between two zeros)
+            const uint32_t V = rem >= 32 ? 0xffffffffu : (1u << rem) - 1u;
+            const uint32_t y = runs_at_least(~R & V & ~((2u << z0) - 1u), Lk);
+            uint32_t El = R & (y << 1);
+            while (El) {
+              const int zb = 31 - __clz(El);
+              El ^= 1u << zb;
+              const int g = zb - (31 - __clz(R & ((1u << zb) - 1u)));
+              const uint2 e = TABLE ? T[g] : seg_long(g, s);
+              ai += e.x;
+              ay += e.y;
+            }
+          }
+          run = nv - 1 - (31 - __clz(R));  // ones above the last zero
         }
-        if (R) lastz = base + 31 - __clz(R);
       }
-      cin = R >> 31;
+      if (HIST) cin = R >> 31;
     }
-    const int gl = N - lastz;  // the final segment ends at N
-    if (HIST) seg_hist(gl, lastz, s, sh_seg, sh_si);
-    if (gl >= 2) {
-      const uint2 e = TABLE ? T[gl] : seg_extra(gl, s);
-      ai += e.x;
-      ay += e.y;
+    int gl;
+    if (HIST) {
+      gl = N - lastz;  // the final segment ends at N
+      seg_hist(gl, lastz, s, sh_seg, sh_si);
+      if (gl >= 2) {
+        const uint2 e = TABLE ? T[gl] : seg_extra(gl, s);
+        ai += e.x;
+        ay += e.y;
+      }
+    } else {
+      gl = run + 1;  // the final segment: the trailing run of ones, then position N
+      n2 += gl >= 2;
+      if (run >= Lk) {
+        const uint2 e = TABLE ? T[gl] : seg_long(gl, s);
+        ai += e.x;
+        ay += e.y;
+      }
     }
 
     const int m = nz + 1;
     const int iters = m + (int)ai;
-    const int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)ay;
+    const int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)n2 * cfg.s1 + (int64_t)ay;
     const int64_t si = (int64_t)iters * cfg.si_cost;
     a_m += (unsigned)m;
     a_i += (unsigned)iters;

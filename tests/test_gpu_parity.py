@@ -65,6 +65,24 @@ def test_fuzz_bit_exact():
     sim.close()
 
 
+def test_fuzz_long_runs_bit_exact():
+    """Long runs of accepted drafts crossing 32-position words: a in [0.85, 0.999], N up to
+    300, k in 1..40 (runs of >= k+1 ones inside a word, across words and at the end), SP 1..8."""
+    rng = np.random.default_rng(21)
+    rows = []
+    for _ in range(60):
+        t_t = int(rng.integers(2, 101))
+        t_d = int(rng.integers(1, t_t + 1))
+        rows.append((float(t_t), float(t_d), float(rng.uniform(0.85, 0.999)), int(rng.integers(1, 41)),
+                     int(rng.integers(1, 9)), int(rng.integers(33, 301)), int(rng.integers(0, 3)), 200))
+    cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
+    for i, r in enumerate(rows):
+        cfgs[i] = r
+    sim, res = run_sim(cfgs, 1.0)
+    check_against_oracle(sim, res, cfgs, 1.0, ctx="longruns")
+    sim.close()
+
+
 def test_cfg2_table2_rows_subsample_bit_exact():
     cfgs, tick = W.cfg2(trials=2000)
     sim, res = run_sim(cfgs, tick)
