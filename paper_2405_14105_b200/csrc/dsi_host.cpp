@@ -133,6 +133,7 @@ struct dsi_sim {
   uint64_t total_units = 0;
   uint64_t total_trials = 0;
   uint32_t tile_trials = 0;
+  uint64_t tiles_per_cfg = 0;  // nonzero when every config has the same number of units
   int block_threads = kDefaultThreads;
   int32_t max_n = 1, max_keff = 1;
   uint64_t si_bins_total = 0;
@@ -467,9 +468,14 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     r = std::min<uint64_t>(32, std::max<uint64_t>(1, r));
     h->tile_trials = (uint32_t)(threads * r);
     h->prefix[0] = 0;
-    for (size_t i = 0; i < n_cfg; ++i)
-      h->prefix[i + 1] = h->prefix[i] + (h->ticks[i].trials + h->tile_trials - 1) / h->tile_trials;
+    bool uniform = true;
+    for (size_t i = 0; i < n_cfg; ++i) {
+      const uint64_t nt = (h->ticks[i].trials + h->tile_trials - 1) / h->tile_trials;
+      h->prefix[i + 1] = h->prefix[i] + nt;
+      uniform = uniform && nt == h->prefix[1];
+    }
     h->total_units = h->prefix[n_cfg];
+    h->tiles_per_cfg = uniform ? h->prefix[1] : 0;
   }
 
   // ---- shards: world x n_devices x n_shards contiguous unit ranges of equal cost
@@ -486,9 +492,10 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     }
     for (size_t i = 0; i < n_cfg; ++i) {
       const uint64_t t = h->ticks[i].trials;
+      const uint64_t nt = h->prefix[i + 1] - h->prefix[i];
       for (uint64_t u = h->prefix[i]; u < h->prefix[i + 1]; ++u) {
-        const uint64_t first = (u - h->prefix[i]) * h->tile_trials;
-        cost[u] = unit_cost(h->ticks[i], std::min<uint64_t>(h->tile_trials, t - first));
+        const uint64_t j = u - h->prefix[i];  // same balanced split as the kernel
+        cost[u] = unit_cost(h->ticks[i], (j + 1) * t / nt - j * t / nt);
       }
     }
     dsi_shard_bounds(cost.data(), h->total_units, parts, bounds.data());
@@ -662,6 +669,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     p.tile_prefix = d.d_prefix;
     p.n_cfg = (uint32_t)n_cfg;
     p.tile_trials = h->tile_trials;
+    p.tiles_per_cfg = h->tiles_per_cfg;
     p.acc = d.d_acc;
     if (d.d_rec) {
       p.rec_acc = d.d_rec;

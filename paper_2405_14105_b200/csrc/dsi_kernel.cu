@@ -91,6 +91,12 @@ __device__ __forceinline__ Word4 philox_call(const uint4 &u, const TrialHalf &t,
 // rej = (rej << 4) | [w >= thr] << 3 | [z >= thr] << 2 | [y >= thr] << 1 | [x >= thr]
 // from the carries of u + (2^32 - thr) (thr >= 1): 2 ALU instructions per bit.
 __device__ __forceinline__ uint32_t pack4(uint32_t rej, const Word4 &u, uint32_t nthr) {
+#ifdef DSI_PACK_SELECT
+  // alternative kept for A/B measurement: compare + select (ALU pipe only)
+  const uint32_t thr = 0u - nthr;
+  return (rej << 4) | ((uint32_t)(u.w >= thr) << 3) | ((uint32_t)(u.z >= thr) << 2) |
+         ((uint32_t)(u.y >= thr) << 1) | (uint32_t)(u.x >= thr);
+#endif
   uint32_t t;
   asm("add.cc.u32 %1, %2, %6;\n\t"
       "addc.u32 %0, %0, %0;\n\t"
@@ -175,21 +181,33 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   __shared__ uint32_t s_cfg;
 
   const uint64_t unit = P.unit_begin + blockIdx.x;
-  if (threadIdx.x == 0) {
-    // config owning this unit: largest c with tile_prefix[c] <= unit
-    uint32_t lo = 0, hi = P.n_cfg;  // invariant: prefix[lo] <= unit < prefix[hi]
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(&P.tile_prefix[mid]) <= unit) lo = mid; else hi = mid;
+  uint32_t c;
+  uint64_t tile, n_tiles;
+  if (P.tiles_per_cfg) {
+    // every config has the same number of tiles: direct mapping
+    c = (uint32_t)(unit / P.tiles_per_cfg);
+    tile = unit - (uint64_t)c * P.tiles_per_cfg;
+    n_tiles = P.tiles_per_cfg;
+  } else {
+    if (threadIdx.x == 0) {
+      // config owning this unit: largest c with tile_prefix[c] <= unit
+      uint32_t lo = 0, hi = P.n_cfg;  // invariant: prefix[lo] <= unit < prefix[hi]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(&P.tile_prefix[mid]) <= unit) lo = mid; else hi = mid;
+      }
+      s_cfg = lo;
     }
-    s_cfg = lo;
+    __syncthreads();
+    c = s_cfg;
+    const uint64_t first = __ldg(&P.tile_prefix[c]);
+    tile = unit - first;
+    n_tiles = __ldg(&P.tile_prefix[c + 1]) - first;
   }
-  __syncthreads();
-  const uint32_t c = s_cfg;
   const DevCfg cfg = P.cfg[c];
-  const uint64_t tile = unit - __ldg(&P.tile_prefix[c]);
-  const uint64_t t0 = tile * P.tile_trials;
-  const uint64_t t1 = min(t0 + P.tile_trials, cfg.n_trials);
+  // balanced tiles: tile i of n covers trials [floor(i T / n), floor((i+1) T / n))
+  const uint64_t t0 = tile * cfg.n_trials / n_tiles;
+  const uint64_t t1 = (tile + 1) * cfg.n_trials / n_tiles;
 
   const uint32_t mode = cfg.flags & 0xffu;
   const int N = cfg.n_tokens;

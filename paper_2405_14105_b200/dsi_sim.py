@@ -14,6 +14,8 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libdsi_sim.so")
+# developer A/B runs only: load an alternative in-tree build of the same library
+LIB_PATH = os.environ.get("DSI_SIM_LIB", LIB_PATH)
 
 DSI_ABI_VERSION = 1
 DSI_OK, DSI_E_NULL, DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW, DSI_E_STRICT_EQ1, DSI_E_DEVICE, \
