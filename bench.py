@@ -77,6 +77,13 @@ def alg_instructions(cfgs) -> float:
     return float(np.sum(tt * (11.0 + 10.0 * (1.0 - cfgs["accept_rate"]))))
 
 
+def _imad_ceiling(sm_mhz: float) -> float:
+    """Trial-tokens/s if the fmaheavy pipe did nothing but Philox multiplies: 148 SMs x 4 SMSPs,
+    one warp IMAD.WIDE per 4 cycles, 16 per Philox call of 4 tokens (rounds 2-9)."""
+    wide_per_s = SM_COUNT * 4 * 32 / 4.0 * sm_mhz * 1e6
+    return wide_per_s / 4.0
+
+
 def measured_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -338,7 +345,13 @@ def ours(args):
                                         "(MEASURED_PEAKS.json) = issue slots; algorithmic "
                                         "instructions per trial-token 11 + 10(1-a)",
                          "frac_at_measured_clock": (achieved / (peak_instr * clk["sm_mhz"] / sm_max)
-                                                    if clk.get("sm_mhz") else None)},
+                                                    if clk.get("sm_mhz") else None),
+                         # the unit that binds in ncu: Philox's 32x32->64 multiplies (IMAD.WIDE,
+                         # 4 fmaheavy cycles per warp instruction, profiles/r01_philox_ceiling.txt);
+                         # 16 of them per 4 trial-tokens after hoisting rounds 0-1
+                         "pipe_bound": {"pipe": "fmaheavy (IMAD.WIDE.U32)",
+                                        "ceiling_trial_tokens_per_s": _imad_ceiling(sm_max),
+                                        "frac": (tt / world / (kern_ms / 1000.0)) / _imad_ceiling(sm_max)}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches,

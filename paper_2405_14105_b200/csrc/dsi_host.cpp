@@ -14,7 +14,9 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dsi_sim.h"
@@ -250,27 +252,61 @@ double unit_cost(const CfgTicks &t, uint64_t trials) {
   return (double)trials * (double)t.n * (11.0 + 10.0 * (1.0 - t.a));
 }
 
-// Validate every config into ticks; on failure h->err names the config.
-dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n) {
-  for (size_t i = 0; i < n; ++i) {
-    std::string msg;
-    const dsi_status s = convert(h->opt, cfg[i], i, h->ticks[i], msg);
-    if (s != DSI_OK) return fail(h, s, msg);
+// Run fn(begin, end) over [0, n) on up to hardware_concurrency host threads
+// (large grids only: the per-config host work is O(1) and independent).
+template <class Fn>
+void parallel_for(size_t n, Fn fn) {
+  size_t nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 1;
+  nt = std::min<size_t>(nt, 16);
+  if (n < (1u << 16) || nt == 1) {
+    fn((size_t)0, n);
+    return;
   }
+  std::vector<std::thread> pool;
+  const size_t chunk = (n + nt - 1) / nt;
+  for (size_t b = 0; b < n; b += chunk) pool.emplace_back(fn, b, std::min(n, b + chunk));
+  for (auto &t : pool) t.join();
+}
+
+// Validate every config into ticks; on failure h->err names the first bad config.
+dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n) {
+  std::mutex mu;
+  size_t bad = n;
+  dsi_status bad_s = DSI_OK;
+  std::string bad_msg;
+  parallel_for(n, [&](size_t b, size_t e) {
+    for (size_t i = b; i < e; ++i) {
+      std::string msg;
+      const dsi_status s = convert(h->opt, cfg[i], i, h->ticks[i], msg);
+      if (s != DSI_OK) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (i < bad) {
+          bad = i;
+          bad_s = s;
+          bad_msg = msg;
+        }
+        return;
+      }
+    }
+  });
+  if (bad < n) return fail(h, bad_s, bad_msg);
   return DSI_OK;
 }
 
 // Fill the pinned device-config staging table from h->ticks.
 void fill_dev_cfg(dsi_sim *h) {
   const bool pattern = h->opt.flags & DSI_F_PATTERN;
-  uint64_t rec = 0, sib = 0;
+  parallel_for(h->n_cfg, [&](size_t b, size_t e) {
+    for (size_t i = b; i < e; ++i) h->dev_cfg.p[i] = make_dev_cfg(h->ticks[i], pattern);
+  });
+  uint64_t rec = 0, sib = 0;  // prefix offsets: per-trial records and SI-histogram bins
   for (size_t i = 0; i < h->n_cfg; ++i) {
-    DevCfg d = make_dev_cfg(h->ticks[i], pattern);
+    DevCfg &d = h->dev_cfg.p[i];
     d.rec_off = rec;
     rec += h->ticks[i].trials;
     d.si_hist_off = (uint32_t)sib;
     sib += (uint64_t)d.k_eff + 1;
-    h->dev_cfg.p[i] = d;
   }
 }
 
@@ -754,7 +790,8 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
       return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
   }
   const double tick = h->opt.tick;
-  for (size_t i = 0; i < n_cfg; ++i) {
+  parallel_for(n_cfg, [&](size_t b, size_t e) {
+  for (size_t i = b; i < e; ++i) {
     const unsigned long long *a = &h->host_acc.p[i * dsi::NF];
     const CfgTicks &t = h->ticks[i];
     dsi_result &r = out[i];
@@ -788,6 +825,7 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
     r.std_si = stdev((uint64_t)r.sum_si_ticks, r.sumsq_si_ticks);
     r.std_dsi = stdev((uint64_t)r.sum_dsi_ticks, r.sumsq_dsi_ticks);
   }
+  });
   h->reduced = true;
   return DSI_OK;
 }
