@@ -289,6 +289,20 @@ def ours(args):
     tt = trial_tokens(cfgs)
     value = tt * args.steps / (total_ms / 1000.0)
 
+    # the heatmap product over the last step's results (Fig. 3): per-cell argmin over k + panels
+    heat = None
+    if rank == 0:
+        t0 = time.perf_counter()
+        cells = D.dsi_heatmap(cfgs, res)
+        heat_s = time.perf_counter() - t0
+        i = int(np.nanargmax(cells["r_min_dsi"]))
+        heat = {"cells": int(cells.size), "product_s": heat_s,
+                "grid_time_s": total_ms / args.steps / 1000.0 + heat_s,
+                "max_r_min_dsi": float(cells["r_min_dsi"][i]),
+                "at": {"t_drafter": float(cells["t_drafter"][i]), "accept_rate": float(cells["accept_rate"][i]),
+                       "si_lookahead": int(cells["si_lookahead"][i]),
+                       "dsi_lookahead": int(cells["dsi_lookahead"][i])}}
+
     # e2e through the public API with host buffers: update (validate + pinned H2D of the
     # config table) + run + reduce (all-reduce + D2H of the moments + FP64 finalise)
     h2d, d2h = sim.io_bytes()
@@ -355,6 +369,7 @@ def ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches,
+            "heatmap": heat,
             "clocks": clk,
             "create_s": create_s,
             "wall_s_timed": wall,

@@ -189,6 +189,36 @@ int32_t dsi_min_lookahead(int64_t t_target_ticks, int64_t t_drafter_ticks, int32
 int32_t dsi_required_processors(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k);
 int32_t dsi_eq1_feasible(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k, int32_t sp);
 
+/* ---- Heatmap product (Fig. 3 / Fig. 5) ----------------
+ * A cell is a maximal run of consecutive configs with equal (t_target, t_drafter,
+ * accept_rate, sp_degree, n_tokens): the lookahead grid of one (drafter latency,
+ * acceptance rate) point.  Per cell: SI = the minimal mean SI latency over the cell's
+ * lookaheads ("the minimal average latency among all the lookahead values"),
+ * DSI = the minimal mean DSI latency over the lookaheads satisfying Eq. 1 at the
+ * config's SP, ties to the smallest k.  Panel "X/Y" is the run time of X divided
+ * by the run time of Y: r_nonsi_si = nonSI/SI, r_si_dsi = SI/DSI,
+ * r_nonsi_dsi = nonSI/DSI, r_min_dsi = min(SI, nonSI)/DSI (Fig. 3(a)-(d));
+ * a ratio above 1 is a speedup of Y.  Cells with no feasible
+ * DSI lookahead get dsi_lookahead = -1 and NaN DSI fields. */
+typedef struct {
+  double t_target, t_drafter, accept_rate; /* user units, copied from the configs */
+  int32_t sp_degree, n_tokens;
+  int32_t si_lookahead;   /* argmin k of mean SI                                    */
+  int32_t dsi_lookahead;  /* argmin Eq.-1-feasible k of mean DSI, or -1             */
+  double nonsi, si, dsi;  /* mean latencies, user units                             */
+  double r_nonsi_si, r_si_dsi, r_nonsi_dsi, r_min_dsi;
+  uint64_t first_cfg;     /* index of the cell's first config                       */
+  uint64_t n_cfg;         /* number of configs (lookaheads) in the cell             */
+} dsi_heatmap_cell;       /* 112 bytes */
+
+/* Host-only.  cells may be NULL to count: *n_cells receives the number of cells;
+ * otherwise at most cap cells are written (DSI_E_RANGE if cap is too small). */
+dsi_status dsi_heatmap(const dsi_config *cfg, const dsi_result *res, size_t n,
+                       dsi_heatmap_cell *cells, size_t cap, size_t *n_cells);
+
+/* CSV of cells (SPEC S:450-458 columns; fixed formatting, %.6f; rows in input order). */
+dsi_status dsi_heatmap_csv(const dsi_heatmap_cell *cells, size_t n, const char *path);
+
 /* Pure sharder (host only, no device): split per-unit costs into `parts`
  * contiguous ranges of near-equal total cost.  cost_units[i] >= 0.
  * bounds must hold parts+1 entries; bounds[0] = 0, bounds[parts] = n.

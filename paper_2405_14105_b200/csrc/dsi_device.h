@@ -59,9 +59,7 @@ struct LaunchParams {
   const DevCfg *cfg;
   const uint64_t *tile_prefix;  // n_cfg + 1: first unit of each config
   uint32_t n_cfg;
-  uint32_t tile_trials;         // at most this many trials per unit; a config of T trials has
-                                // n = ceil(T / tile_trials) units, unit i = [iT/n, (i+1)T/n)
-  uint64_t tiles_per_cfg;       // n when every config has the same n (direct mapping), else 0
+  uint32_t tile_trials;         // trials per unit (the last unit of a config is ragged)
   uint64_t unit_begin;          // first unit of this launch; block b runs unit_begin + b
   unsigned long long *acc;      // n_cfg * NF
   int32_t *rec_acc, *rec_m, *rec_iters, *rec_si, *rec_dsi;  // DSI_F_PER_TRIAL

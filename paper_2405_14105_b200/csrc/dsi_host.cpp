@@ -135,7 +135,6 @@ struct dsi_sim {
   uint64_t total_units = 0;
   uint64_t total_trials = 0;
   uint32_t tile_trials = 0;
-  uint64_t tiles_per_cfg = 0;  // nonzero when every config has the same number of units
   int block_threads = kDefaultThreads;
   int32_t max_n = 1, max_keff = 1;
   uint64_t si_bins_total = 0;
@@ -504,14 +503,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     r = std::min<uint64_t>(32, std::max<uint64_t>(1, r));
     h->tile_trials = (uint32_t)(threads * r);
     h->prefix[0] = 0;
-    bool uniform = true;
-    for (size_t i = 0; i < n_cfg; ++i) {
-      const uint64_t nt = (h->ticks[i].trials + h->tile_trials - 1) / h->tile_trials;
-      h->prefix[i + 1] = h->prefix[i] + nt;
-      uniform = uniform && nt == h->prefix[1];
-    }
+    for (size_t i = 0; i < n_cfg; ++i)
+      h->prefix[i + 1] = h->prefix[i] + (h->ticks[i].trials + h->tile_trials - 1) / h->tile_trials;
     h->total_units = h->prefix[n_cfg];
-    h->tiles_per_cfg = uniform ? h->prefix[1] : 0;
   }
 
   // ---- shards: world x n_devices x n_shards contiguous unit ranges of equal cost
@@ -528,10 +522,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     }
     for (size_t i = 0; i < n_cfg; ++i) {
       const uint64_t t = h->ticks[i].trials;
-      const uint64_t nt = h->prefix[i + 1] - h->prefix[i];
       for (uint64_t u = h->prefix[i]; u < h->prefix[i + 1]; ++u) {
-        const uint64_t j = u - h->prefix[i];  // same balanced split as the kernel
-        cost[u] = unit_cost(h->ticks[i], (j + 1) * t / nt - j * t / nt);
+        const uint64_t first = (u - h->prefix[i]) * h->tile_trials;  // the last tile is ragged
+        cost[u] = unit_cost(h->ticks[i], std::min<uint64_t>(h->tile_trials, t - first));
       }
     }
     dsi_shard_bounds(cost.data(), h->total_units, parts, bounds.data());
@@ -591,6 +584,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     const size_t acc_bytes = n_cfg * dsi::NF * sizeof(unsigned long long);
     if (e == cudaSuccess) e = cudaMalloc(&d.d_cfg, n_cfg * sizeof(DevCfg));
     if (e == cudaSuccess) e = cudaMalloc(&d.d_prefix, (n_cfg + 1) * sizeof(uint64_t));
+
     if (e == cudaSuccess) e = cudaMalloc(&d.d_acc, acc_bytes);
     if (e == cudaSuccess && total_devices > 1) e = cudaMalloc(&d.d_red, acc_bytes);
     if (e == cudaSuccess && (opt->flags & DSI_F_HIST)) {
@@ -705,7 +699,6 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     p.tile_prefix = d.d_prefix;
     p.n_cfg = (uint32_t)n_cfg;
     p.tile_trials = h->tile_trials;
-    p.tiles_per_cfg = h->tiles_per_cfg;
     p.acc = d.d_acc;
     if (d.d_rec) {
       p.rec_acc = d.d_rec;

@@ -91,12 +91,7 @@ __device__ __forceinline__ Word4 philox_call(const uint4 &u, const TrialHalf &t,
 // rej = (rej << 4) | [w >= thr] << 3 | [z >= thr] << 2 | [y >= thr] << 1 | [x >= thr]
 // from the carries of u + (2^32 - thr) (thr >= 1): 2 ALU instructions per bit.
 __device__ __forceinline__ uint32_t pack4(uint32_t rej, const Word4 &u, uint32_t nthr) {
-#ifdef DSI_PACK_SELECT
-  // alternative kept for A/B measurement: compare + select (ALU pipe only)
-  const uint32_t thr = 0u - nthr;
-  return (rej << 4) | ((uint32_t)(u.w >= thr) << 3) | ((uint32_t)(u.z >= thr) << 2) |
-         ((uint32_t)(u.y >= thr) << 1) | (uint32_t)(u.x >= thr);
-#endif
+  // (measured: compare + select packing, all on the ALU pipe, was 6% slower)
   uint32_t t;
   asm("add.cc.u32 %1, %2, %6;\n\t"
       "addc.u32 %0, %0, %0;\n\t"
@@ -171,6 +166,42 @@ __device__ __forceinline__ void seg_hist(int g, int seg_start, const SegCtx &s, 
   if (last_start + kk + 1 <= s.n_tokens) atomicAdd(&sh_si[r - 1], 1u);
 }
 
+// Production accounting of one word of the rejection mask R (bit i = position
+// base+i, nv valid bits, bits >= nv are zero).  Segments with g >= 2 end at a zero
+// whose predecessor is a one (mask E) and each costs (0, S(1)) unless its run of
+// ones is long (L = g-1 >= Lk = k+1); long segments add T[g] = seg_long(g).
+template <bool TABLE>
+__device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint2 *T, const SegCtx &s,
+                                          int &run, int &n2, uint32_t &ai, uint32_t &ay) {
+  if (R == 0) {
+    run += nv;  // the run of accepted drafts continues through the word
+    return;
+  }
+  const uint32_t E = R & ~((R << 1) | (run == 0 ? 1u : 0u));
+  n2 += __popc(E);
+  const int z0 = __ffs(R) - 1;  // the first zero closes the run carried in
+  if (run + z0 >= Lk) {
+    const uint2 e = TABLE ? T[run + z0 + 1] : seg_long(run + z0 + 1, s);
+    ai += e.x;
+    ay += e.y;
+  }
+  if (Lk <= 30) {
+    // runs of >= Lk ones strictly inside the word (between two zeros)
+    const uint32_t V = nv >= 32 ? 0xffffffffu : (1u << nv) - 1u;
+    const uint32_t y = runs_at_least(~R & V & ~((2u << z0) - 1u), Lk);
+    uint32_t El = R & (y << 1);
+    while (El) {
+      const int zb = 31 - __clz(El);
+      El ^= 1u << zb;
+      const int g = zb - (31 - __clz(R & ((1u << zb) - 1u)));
+      const uint2 e = TABLE ? T[g] : seg_long(g, s);
+      ai += e.x;
+      ay += e.y;
+    }
+  }
+  run = nv - 1 - (31 - __clz(R));  // ones above the last zero
+}
+
 // Shared-memory layout of the TABLE variant for a config with N tokens.
 __host__ __device__ __forceinline__ size_t t_table_bytes(int n) { return (size_t)((n + 2) & ~1) * 8; }
 __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t)((n - 1 + 3) / 4 + 1) * 16; }
@@ -178,36 +209,25 @@ __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t
 template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE>
 __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ uint32_t s_cfg;
 
+  __shared__ uint32_t s_cfg;
   const uint64_t unit = P.unit_begin + blockIdx.x;
-  uint32_t c;
-  uint64_t tile, n_tiles;
-  if (P.tiles_per_cfg) {
-    // every config has the same number of tiles: direct mapping
-    c = (uint32_t)(unit / P.tiles_per_cfg);
-    tile = unit - (uint64_t)c * P.tiles_per_cfg;
-    n_tiles = P.tiles_per_cfg;
-  } else {
-    if (threadIdx.x == 0) {
-      // config owning this unit: largest c with tile_prefix[c] <= unit
-      uint32_t lo = 0, hi = P.n_cfg;  // invariant: prefix[lo] <= unit < prefix[hi]
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(&P.tile_prefix[mid]) <= unit) lo = mid; else hi = mid;
-      }
-      s_cfg = lo;
+  if (threadIdx.x == 0) {
+    // config owning this unit: largest c with tile_prefix[c] <= unit
+    uint32_t lo = 0, hi = P.n_cfg;  // invariant: prefix[lo] <= unit < prefix[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(&P.tile_prefix[mid]) <= unit) lo = mid; else hi = mid;
     }
-    __syncthreads();
-    c = s_cfg;
-    const uint64_t first = __ldg(&P.tile_prefix[c]);
-    tile = unit - first;
-    n_tiles = __ldg(&P.tile_prefix[c + 1]) - first;
+    s_cfg = lo;
   }
+  __syncthreads();
+  // (A/B measured, profiles/r01_ab.jsonl: balanced tiles, a direct unit -> config
+  //  division and a host-built unit -> config map were each 1-5% slower than this)
+  const uint32_t c = s_cfg;
   const DevCfg cfg = P.cfg[c];
-  // balanced tiles: tile i of n covers trials [floor(i T / n), floor((i+1) T / n))
-  const uint64_t t0 = tile * cfg.n_trials / n_tiles;
-  const uint64_t t1 = (tile + 1) * cfg.n_trials / n_tiles;
+  const uint64_t t0 = (unit - __ldg(&P.tile_prefix[c])) * P.tile_trials;
+  const uint64_t t1 = min(t0 + P.tile_trials, cfg.n_trials);
 
   const uint32_t mode = cfg.flags & 0xffu;
   const int N = cfg.n_tokens;
@@ -301,36 +321,7 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
           lastz = z;
         }
       } else {
-        // Segments with g >= 2 end at a zero whose predecessor is a one (mask E);
-        // each costs (0, S(1)) unless its run of ones is long (L = g-1 >= k+1).
-        const int nv = min(rem, 32);  // valid positions in this word
-        if (R == 0) {
-          run += nv;  // the run of accepted drafts continues through the word
-        } else {
-          const uint32_t E = R & ~((R << 1) | (run == 0 ? 1u : 0u));
-          n2 += __popc(E);
-          const int z0 = __ffs(R) - 1;  // the first zero closes the run carried in
-          if (run + z0 >= Lk) {
-            const uint2 e = TABLE ? T[run + z0 + 1] : seg_long(run + z0 + 1, s);
-            ai += e.x;
-            ay += e.y;
-          }
-          if (Lk <= 30) {
-            // runs of >= Lk ones strictly inside the word (between two zeros)
-            const uint32_t V = rem >= 32 ? 0xffffffffu : (1u << rem) - 1u;
-            const uint32_t y = runs_at_least(~R & V & ~((2u << z0) - 1u), Lk);
-            uint32_t El = R & (y << 1);
-            while (El) {
-              const int zb = 31 - __clz(El);
-              El ^= 1u << zb;
-              const int g = zb - (31 - __clz(R & ((1u << zb) - 1u)));
-              const uint2 e = TABLE ? T[g] : seg_long(g, s);
-              ai += e.x;
-              ay += e.y;
-            }
-          }
-          run = nv - 1 - (31 - __clz(R));  // ones above the last zero
-        }
+        walk_word<TABLE>(R, rem >= 32 ? 32 : rem, Lk, T, s, run, n2, ai, ay);
       }
       if (HIST) cin = R >> 31;
     }

@@ -34,7 +34,12 @@ RESULT_DTYPE = np.dtype([("trials", "<u8"), ("t_target_ticks", "<i8"), ("t_draft
                          ("eq1_feasible", "<i4"), ("min_lookahead", "<i4"),
                          ("mean_nonsi", "<f8"), ("mean_si", "<f8"), ("mean_dsi", "<f8"),
                          ("std_si", "<f8"), ("std_dsi", "<f8")])
-assert CONFIG_DTYPE.itemsize == 48 and RESULT_DTYPE.itemsize == 160
+HEATMAP_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_rate", "<f8"),
+                          ("sp_degree", "<i4"), ("n_tokens", "<i4"), ("si_lookahead", "<i4"),
+                          ("dsi_lookahead", "<i4"), ("nonsi", "<f8"), ("si", "<f8"), ("dsi", "<f8"),
+                          ("r_nonsi_si", "<f8"), ("r_si_dsi", "<f8"), ("r_nonsi_dsi", "<f8"),
+                          ("r_min_dsi", "<f8"), ("first_cfg", "<u8"), ("n_cfg", "<u8")])
+assert CONFIG_DTYPE.itemsize == 48 and RESULT_DTYPE.itemsize == 160 and HEATMAP_DTYPE.itemsize == 112
 
 
 class dsi_options(ctypes.Structure):
@@ -73,8 +78,12 @@ def _load():
         "dsi_required_processors": ([i64, i64, i32], i32),
         "dsi_eq1_feasible": ([i64, i64, i32, i32], i32),
         "dsi_shard_bounds": ([V, u64, i32, V], ctypes.c_int),
+        "dsi_heatmap": ([V, V, sz, V, sz, P(sz)], ctypes.c_int),
+        "dsi_heatmap_csv": ([V, sz, ctypes.c_char_p], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
+        if "DSI_SIM_LIB" in os.environ and not hasattr(lib, name):
+            continue  # an older build under A/B test may lack newer entry points
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
@@ -86,7 +95,8 @@ EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce",
             "dsi_sim_stream", "dsi_sim_launches", "dsi_sim_kernel_ms", "dsi_sim_units", "dsi_sim_io_bytes",
             "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
             "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
-            "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds")
+            "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
+            "dsi_heatmap_csv")
 
 
 class DsiError(RuntimeError):
@@ -128,6 +138,25 @@ def dsi_nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     _check(lib.dsi_nccl_unique_id(ctypes.addressof(buf)))
     return bytes(buf)
+
+
+def dsi_heatmap(configs: np.ndarray, results: np.ndarray) -> np.ndarray:
+    """Per-cell argmin over lookaheads and the four ratio panels (Fig. 3 / Fig. 5)."""
+    configs = np.ascontiguousarray(configs, dtype=CONFIG_DTYPE)
+    results = np.ascontiguousarray(results, dtype=RESULT_DTYPE)
+    if configs.size != results.size:
+        raise ValueError("configs and results differ in length")
+    n = ctypes.c_size_t()
+    _check(lib.dsi_heatmap(configs.ctypes.data, results.ctypes.data, configs.size, None, 0, ctypes.byref(n)))
+    cells = np.zeros(n.value, HEATMAP_DTYPE)
+    _check(lib.dsi_heatmap(configs.ctypes.data, results.ctypes.data, configs.size, cells.ctypes.data,
+                           cells.size, ctypes.byref(n)))
+    return cells
+
+
+def dsi_heatmap_csv(cells: np.ndarray, path: str) -> None:
+    cells = np.ascontiguousarray(cells, dtype=HEATMAP_DTYPE)
+    _check(lib.dsi_heatmap_csv(cells.ctypes.data, cells.size, os.fsencode(path)))
 
 
 def make_configs(n: int) -> np.ndarray:

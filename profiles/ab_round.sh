@@ -1,7 +1,13 @@
+# A/B timing of kernel builds (developer tool): writes gpurun_out/ab.jsonl
 mkdir -p gpurun_out
-timeout 700 python -m pytest tests -m gpu -q --maxfail=5 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? > gpurun_out/status6.txt
-for t in 128 64 256; do timeout 120 python profiles/ab.py --threads $t >> gpurun_out/ab.jsonl 2>&1; done
-DSI_SIM_LIB=build/libdsi_sim_packsel.so timeout 120 python profiles/ab.py --threads 128 >> gpurun_out/ab.jsonl 2>&1
-timeout 120 python profiles/ab.py --workload cfg5 --stride 10 >> gpurun_out/ab.jsonl 2>&1
-timeout 120 python profiles/ab.py --workload cfg4 >> gpurun_out/ab.jsonl 2>&1
-timeout 120 python profiles/ab.py --workload cfg2 >> gpurun_out/ab.jsonl 2>&1
+timeout 900 python -m pytest tests -m gpu -q --maxfail=5 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/ab.jsonl
+for rep in 1 2; do
+for lib in build/libdsi_sim_v3.so paper_2405_14105_b200/libdsi_sim.so; do
+  DSI_SIM_LIB=$lib timeout 200 python profiles/ab.py --stride 5 --runs 3 >> gpurun_out/ab.jsonl 2>&1
+done
+done
+for w in cfg5 cfg4; do
+for lib in build/libdsi_sim_v3.so paper_2405_14105_b200/libdsi_sim.so; do
+  DSI_SIM_LIB=$lib timeout 200 python profiles/ab.py --workload $w --stride 10 --runs 3 >> gpurun_out/ab.jsonl 2>&1
+done
+done

@@ -1,0 +1,92 @@
+"""Summarise the ncu captures of profiles/profile_round.sh into profiles/<round>_ncu_summary.json
+and profiles/latest_ncu_summary.json (read by bench.py for roofline.traffic).
+
+    python profiles/summarize_ncu.py r01      # reads gpurun_out/{launches,dram,prof}_r01*
+"""
+import collections
+import csv
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+R = sys.argv[1] if len(sys.argv) > 1 else "r01"
+
+
+def read_csv(path):
+    with open(path) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    return list(csv.reader(io.StringIO("".join(lines))))
+
+
+def launches():
+    rows = read_csv(os.path.join(OUT, f"launches_{R}.csv"))
+    hdr = rows[0]
+    iK, iV = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    per = collections.defaultdict(list)
+    for r in rows[1:]:
+        per[r[iK]].append(float(r[iV]))
+    total = sum(sum(v) for v in per.values())
+    return {k: {"launches": len(v), "mean_ms": sum(v) / len(v) / 1e6, "share": sum(v) / total}
+            for k, v in per.items()}
+
+
+def dram():
+    rows = read_csv(os.path.join(OUT, f"dram_{R}.csv"))
+    hdr = rows[0]
+    iM, iU, iV = hdr.index("Metric Name"), hdr.index("Metric Unit"), hdr.index("Metric Value")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}
+    d = {r[iM]: float(r[iV].replace(",", "")) * scale.get(r[iU], 1) for r in rows[1:]}
+    return d
+
+
+def full():
+    rep = os.path.join(OUT, f"prof_{R}.ncu-rep")
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    d = {h: (u, v) for h, u, v in zip(rows[0], rows[1], rows[2])}
+    keys = ["gpu__time_duration.sum", "smsp__inst_executed.sum",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "launch__grid_size", "launch__block_size", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "sm__cycles_elapsed.avg.per_second"]
+    keys += [k for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    srows = list(csv.reader(io.StringIO(src)))
+    hdr = srows[1]
+    iS, iE = hdr.index("Source"), hdr.index("Instructions Executed")
+    ops = collections.Counter()
+    for r in srows[2:]:
+        if len(r) > iE and r[iE]:
+            m = re.match(r"(@!?U?P\w+\s+)?([A-Z0-9_.]+)", r[iS].strip())
+            ops[m.group(2)] += int(r[iE])
+    tot = sum(ops.values())
+    return {k: d[k] for k in keys if k in d}, {k: [v, round(v / tot, 4)] for k, v in ops.most_common(20)}
+
+
+out = {"round": R, "workload": "cfg3"}
+try:
+    out["launch_list"] = launches()
+except OSError as e:
+    out["launch_list_error"] = str(e)
+try:
+    dd = dram()
+    out["full_bench_launch"] = dd
+    out["dram_bytes_per_launch"] = dd.get("dram__bytes_read.sum", 0) + dd.get("dram__bytes_write.sum", 0)
+except OSError as e:
+    out["dram_error"] = str(e)
+try:
+    out["set_full_stride20"], out["instruction_mix_stride20"] = full()
+except (OSError, ValueError, IndexError) as e:
+    out["full_error"] = str(e)
+for name in (f"{R}_ncu_summary.json", "latest_ncu_summary.json"):
+    with open(os.path.join(ROOT, "profiles", name), "w") as f:
+        json.dump(out, f, indent=1)
+print(json.dumps({k: out.get(k) for k in ("dram_bytes_per_launch", "launch_list")}, indent=1))

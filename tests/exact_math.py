@@ -88,6 +88,31 @@ def pattern_index(A):
     return sum(int(v) << i for i, v in enumerate(A))
 
 
+def expectations_grid_f64(N, t_t, t_ds, ks, sp, ps):
+    """Exact E[L_SI], E[L_DSI] (float64) for every (p, t_d, k) of a grid: the same h(g)
+    and C(g) formulas as above, vectorised with numpy.  Shapes (len(ps), len(t_ds), len(ks))."""
+    import numpy as np
+    g = np.arange(1, N + 1, dtype=np.float64)
+    ps = np.asarray(ps, dtype=np.float64)
+    H = np.empty((ps.size, N))
+    for i, p in enumerate(ps):
+        h = (1 - p) * p ** (g - 1) * (2 + (1 - p) * (N - 1 - g))
+        h[-1] = p ** (N - 1)
+        H[i] = h
+    ks = np.asarray(ks, dtype=np.int64)
+    t_ds = np.asarray(t_ds, dtype=np.int64)
+    gi = np.arange(1, N + 1, dtype=np.int64)
+    b = -(-(gi[None, :] - 1) // ks[:, None])                    # (k, g)
+    iters = -(-gi[None, :] // (ks[:, None] + 1))                # (k, g)
+    KD = ks[None, :, None] * t_ds[:, None, None]                # (t_d, k, 1)
+    S = np.maximum(b[None] * KD, (b[None] % sp) * KD + (b[None] // sp) * t_t)
+    C = (t_t + S).astype(np.float64)                            # (t_d, k, g)
+    e_dsi = np.einsum("pg,dkg->pdk", H, C)
+    e_i = np.einsum("pg,kg->pk", H, iters.astype(np.float64))   # (p, k)
+    e_si = e_i[:, None, :] * (KD[None, :, :, 0] + t_t)
+    return e_si, e_dsi
+
+
 def si_tokens_per_iteration(a, k):
     """E[n+1] = (1 - a^(k+1)) / (1 - a): truncated geometric."""
     a = Fraction(a)

@@ -208,6 +208,23 @@ def test_bench_workload_full_size_sampled():
     assert sim.kernel_ms() > 0
     sim.close()
 
+    # every one of the 2.02 M Monte Carlo means sits within 6 sigma of its exact expectation
+    from test_heatmap import exact_results
+    ex = exact_results(cfgs, tick)
+    T = 10_000.0
+    for f, s in (("mean_si", "std_si"), ("mean_dsi", "std_dsi")):
+        dev = np.abs(res[f] - ex[f])
+        lim = 6.0 * res[s] / np.sqrt(T) + 1e-9 * ex[f]
+        assert np.all(dev <= lim), (f, int(np.sum(dev > lim)))
+    # the heatmap product of the GPU run against the exact one (Fig. 3 claims)
+    cells = D.dsi_heatmap(cfgs, res)
+    exact_cells = D.dsi_heatmap(cfgs, ex)
+    assert cells.size == 10100
+    assert np.all(cells["r_nonsi_dsi"] >= 1.0 - 1e-12)
+    assert abs(cells["r_min_dsi"].max() - exact_cells["r_min_dsi"].max()) < 0.01
+    clear = np.abs(cells["accept_rate"] - cells["t_drafter"]) > 0.05  # away from the a = t_d line
+    assert np.array_equal((cells["r_nonsi_si"] > 1)[clear], (exact_cells["r_nonsi_si"] > 1)[clear])
+
 
 def test_monte_carlo_mean_vs_exact_expectation():
     """Large-T GPU means sit within 6 sigma of the exact expectation (P11)."""
