@@ -69,6 +69,11 @@ typedef enum {
 #define DSI_F_PATTERN 0x4u    /* enumeration mode: A_p = bit (p-1) of the trial index; N <= 33 */
 #define DSI_F_STRICT_EQ1 0x8u /* reject configs violating Eq. 1                               */
 #define DSI_F_TIMING 0x10u    /* record CUDA events around the trial kernels of each run      */
+#define DSI_F_SHARED_STREAMS 0x20u /* configs with equal (stream_id, floor(a 2^32), N, n_trials)
+                                 draw identical indicators (the RNG contract): generate each
+                                 trial's stream once per group and evaluate every config of the
+                                 group on it.  Results are bit-identical to the default mode.
+                                 Not with PER_TRIAL, HIST or PATTERN; N <= 4096.             */
 
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {

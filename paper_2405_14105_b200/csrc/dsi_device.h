@@ -70,6 +70,35 @@ struct LaunchParams {
   Keys keys;
 };
 
+// ---- shared-stream mode (DSI_F_SHARED_STREAMS, dsi_crn.cu)
+struct CrnGroup {      // configs drawing identical indicators: equal (stream, threshold, N, T)
+  uint32_t first;      // first position in perm
+  uint32_t count;      // configs in the group
+  int32_t n_tokens;
+  uint32_t stream_id;
+  uint32_t thr;        // threshold low word (mode says whether the stream is used)
+  uint32_t mode;       // MODE_*
+  uint64_t n_trials;
+};
+struct CrnUnit {       // one block: a slice of one group's configs
+  uint32_t group;
+  uint32_t begin;      // position in perm
+  uint32_t count;      // <= cfg_per_block
+  uint32_t pad;
+};
+struct CrnParams {
+  const DevCfg *cfg;
+  const uint32_t *perm;  // processing order of the configs (grouped, lookahead-major)
+  const CrnGroup *groups;
+  const CrnUnit *units;
+  uint64_t unit_begin;
+  unsigned long long *acc;  // n_cfg * NF, written with plain stores (a config has one owner)
+  int32_t max_n, max_nq, max_runs, cfg_per_block;
+  Keys keys;
+};
+size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs);
+int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream);
+
 // Dynamic shared memory of the variant chosen for (max_n, max_keff, hist).
 size_t trial_kernel_smem(int max_n, int max_keff, bool hist);
 

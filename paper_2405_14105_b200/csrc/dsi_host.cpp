@@ -32,6 +32,8 @@ thread_local std::string g_create_error;
 constexpr int kMaxTokens = 32768;  // keeps every magic division exact (x * d <= 2^32)
 constexpr uint64_t kMaxTrials = 1ull << 32;
 constexpr int kDefaultThreads = 128;
+constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size (launch bounds)
+constexpr int kCrnMaxN = 4096;     // shared-stream mode: per-trial run lists in shared memory
 
 // ----------------------------------------------------------------------------- NCCL (dlopen)
 struct NcclApi {
@@ -121,6 +123,9 @@ struct DeviceState {
   unsigned long long *d_seg = nullptr, *d_seg_red = nullptr;
   unsigned long long *d_si = nullptr, *d_si_red = nullptr;
   int32_t *d_rec = nullptr;  // 5 arrays of total_trials
+  uint32_t *d_perm = nullptr;            // shared-stream mode: processing order
+  dsi::CrnGroup *d_groups = nullptr;     //   groups of configs sharing a stream
+  dsi::CrnUnit *d_crn_units = nullptr;   //   one block per unit
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<std::pair<uint64_t, uint64_t>> ranges;  // [begin, end) units, one per shard
@@ -138,6 +143,11 @@ struct dsi_sim {
   int block_threads = kDefaultThreads;
   int32_t max_n = 1, max_keff = 1;
   uint64_t si_bins_total = 0;
+  bool shared = false;                    // DSI_F_SHARED_STREAMS
+  std::vector<uint32_t> perm;
+  std::vector<dsi::CrnGroup> groups;
+  std::vector<dsi::CrnUnit> crn_units;
+  int32_t cfg_per_block = 0, max_runs = 0;
   std::vector<DeviceState> dev;
   Pinned<unsigned long long> host_acc, host_seg, host_si;  // D2H targets
   bool ran = false, reduced = false;
@@ -322,6 +332,9 @@ void free_device(DeviceState &d) {
   cudaFree(d.d_si);
   cudaFree(d.d_si_red);
   cudaFree(d.d_rec);
+  cudaFree(d.d_perm);
+  cudaFree(d.d_groups);
+  cudaFree(d.d_crn_units);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
   if (d.own_stream && d.stream) cudaStreamDestroy(d.stream);
@@ -343,7 +356,83 @@ dsi_status upload(dsi_sim *h) {
     CUDA_TRY(h, cudaSetDevice(d.ordinal));
     CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg, h->dev_cfg.p, h->n_cfg * sizeof(DevCfg),
                                 cudaMemcpyHostToDevice, d.stream));
+    if (h->shared) {
+      CUDA_TRY(h, cudaMemcpyAsync(d.d_perm, h->perm.data(), h->perm.size() * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, d.stream));
+      CUDA_TRY(h, cudaMemcpyAsync(d.d_groups, h->groups.data(), h->groups.size() * sizeof(dsi::CrnGroup),
+                                  cudaMemcpyHostToDevice, d.stream));
+      CUDA_TRY(h, cudaMemcpyAsync(d.d_crn_units, h->crn_units.data(),
+                                  h->crn_units.size() * sizeof(dsi::CrnUnit), cudaMemcpyHostToDevice,
+                                  d.stream));
+      CUDA_TRY(h, cudaStreamSynchronize(d.stream));  // the host vectors are pageable and may change
+    }
   }
+  return DSI_OK;
+}
+
+// Shared-stream plan: group configs by (stream_id, threshold, N, n_trials) -- equal keys
+// draw identical indicators -- ordered lookahead-major inside a group (so the lanes of a
+// warp mostly share k), then cut each group into slices of cfg_per_block configs.
+dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
+  const size_t n = h->n_cfg;
+  try {
+    h->perm.resize(n);
+    for (size_t i = 0; i < n; ++i) h->perm[i] = (uint32_t)i;
+    const auto &t = h->ticks;
+    std::stable_sort(h->perm.begin(), h->perm.end(), [&](uint32_t a, uint32_t b) {
+      const CfgTicks &x = t[a], &y = t[b];
+      if (x.stream_id != y.stream_id) return x.stream_id < y.stream_id;
+      if (x.thr != y.thr) return x.thr < y.thr;
+      if (x.n != y.n) return x.n < y.n;
+      if (x.trials != y.trials) return x.trials < y.trials;
+      if (x.k != y.k) return x.k < y.k;
+      if (x.t_t != y.t_t) return x.t_t < y.t_t;
+      if (x.t_d != y.t_d) return x.t_d < y.t_d;
+      return x.sp < y.sp;
+    });
+    h->max_runs = h->max_n / 3 + 2;  // runs of >= 2 accepted drafts in one trial
+    h->cfg_per_block = kCrnThreads;
+    for (int cpb : {4 * kCrnThreads, 2 * kCrnThreads}) {
+      if (dsi::crn_kernel_smem(h->max_n, kCrnThreads, cpb, h->max_runs) <= 100 * 1024) {
+        h->cfg_per_block = cpb;
+        break;
+      }
+    }
+    h->groups.clear();
+    h->crn_units.clear();
+    cost.clear();
+    for (size_t i = 0; i < n;) {
+      const CfgTicks &k0 = t[h->perm[i]];
+      size_t j = i + 1;
+      while (j < n) {
+        const CfgTicks &kj = t[h->perm[j]];
+        if (kj.stream_id != k0.stream_id || kj.thr != k0.thr || kj.n != k0.n || kj.trials != k0.trials) break;
+        ++j;
+      }
+      dsi::CrnGroup g{};
+      g.first = (uint32_t)i;
+      g.count = (uint32_t)(j - i);
+      g.n_tokens = k0.n;
+      g.stream_id = k0.stream_id;
+      g.thr = (uint32_t)std::min<uint64_t>(k0.thr, 0xffffffffull);
+      g.mode = k0.thr >= (1ull << 32) ? dsi::MODE_ALL_ACCEPT : (k0.thr == 0 ? dsi::MODE_ALL_REJECT : dsi::MODE_STREAM);
+      g.n_trials = k0.trials;
+      for (size_t b = i; b < j; b += (size_t)h->cfg_per_block) {
+        dsi::CrnUnit u{};
+        u.group = (uint32_t)h->groups.size();
+        u.begin = (uint32_t)b;
+        u.count = (uint32_t)std::min<size_t>((size_t)h->cfg_per_block, j - b);
+        h->crn_units.push_back(u);
+        // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
+        cost.push_back((double)k0.trials * ((double)k0.n * 12.0 + (double)u.count * 25.0));
+      }
+      h->groups.push_back(g);
+      i = j;
+    }
+  } catch (...) {
+    return fail(h, DSI_E_NOMEM, "shared-stream plan");
+  }
+  h->total_units = h->crn_units.size();
   return DSI_OK;
 }
 
@@ -431,7 +520,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (opt->abi_version != DSI_ABI_VERSION) return fail(nullptr, DSI_E_RANGE, "abi_version mismatch");
   if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
-  const uint32_t known = DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_STRICT_EQ1 | DSI_F_TIMING;
+  const uint32_t known = DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_STRICT_EQ1 | DSI_F_TIMING |
+                         DSI_F_SHARED_STREAMS;
   if (opt->flags & ~known) return fail(nullptr, DSI_E_RANGE, "unknown flag");
   if (opt->n_devices < 1 || opt->n_devices > 8) return fail(nullptr, DSI_E_RANGE, "n_devices must be 1..8");
   if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
@@ -449,6 +539,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   const bool per_trial = opt->flags & DSI_F_PER_TRIAL;
   if (per_trial && total_devices > 1)
     return fail(nullptr, DSI_E_RANGE, "DSI_F_PER_TRIAL needs a single device and world == 1");
+  const bool shared = opt->flags & DSI_F_SHARED_STREAMS;
+  if (shared && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN)))
+    return fail(nullptr, DSI_E_RANGE, "DSI_F_SHARED_STREAMS excludes PER_TRIAL, HIST and PATTERN");
 
   dsi_sim *h = new (std::nothrow) dsi_sim;
   if (!h) return fail(nullptr, DSI_E_NOMEM, "handle allocation");
@@ -460,7 +553,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   h->opt = *opt;
   h->opt.nccl_id = nullptr;
   h->n_cfg = n_cfg;
-  h->block_threads = opt->block_threads ? opt->block_threads : kDefaultThreads;
+  h->shared = shared;
+  h->block_threads = shared ? kCrnThreads : (opt->block_threads ? opt->block_threads : kDefaultThreads);
   try {
     h->ticks.resize(n_cfg);
     h->prefix.resize(n_cfg + 1);
@@ -495,8 +589,17 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     return abort_create(DSI_E_RANGE);
   }
 
-  // ---- work units: (config, tile of tile_trials trials)
-  {
+  if (shared && h->max_n > kCrnMaxN) {
+    h->err = "DSI_F_SHARED_STREAMS supports n_tokens <= 4096";
+    return abort_create(DSI_E_RANGE);
+  }
+
+  // ---- work units: (config, tile of tile_trials trials), or shared-stream (group, config slice)
+  std::vector<double> crn_cost;
+  if (shared) {
+    s = plan_shared(h, crn_cost);
+    if (s != DSI_OK) return abort_create(s);
+  } else {
     const uint64_t threads = (uint64_t)h->block_threads;
     const uint64_t target_blocks = 148ull * 16 * 8 * (uint64_t)total_devices;
     uint64_t r = h->total_trials / (threads * target_blocks);
@@ -520,11 +623,15 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       h->err = "sharder cost table";
       return abort_create(DSI_E_NOMEM);
     }
-    for (size_t i = 0; i < n_cfg; ++i) {
-      const uint64_t t = h->ticks[i].trials;
-      for (uint64_t u = h->prefix[i]; u < h->prefix[i + 1]; ++u) {
-        const uint64_t first = (u - h->prefix[i]) * h->tile_trials;  // the last tile is ragged
-        cost[u] = unit_cost(h->ticks[i], std::min<uint64_t>(h->tile_trials, t - first));
+    if (shared) {
+      cost.swap(crn_cost);
+    } else {
+      for (size_t i = 0; i < n_cfg; ++i) {
+        const uint64_t t = h->ticks[i].trials;
+        for (uint64_t u = h->prefix[i]; u < h->prefix[i + 1]; ++u) {
+          const uint64_t first = (u - h->prefix[i]) * h->tile_trials;  // the last tile is ragged
+          cost[u] = unit_cost(h->ticks[i], std::min<uint64_t>(h->tile_trials, t - first));
+        }
       }
     }
     dsi_shard_bounds(cost.data(), h->total_units, parts, bounds.data());
@@ -596,6 +703,11 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       }
     }
     if (e == cudaSuccess && per_trial) e = cudaMalloc(&d.d_rec, 5 * h->total_trials * sizeof(int32_t));
+    if (e == cudaSuccess && shared) {
+      e = cudaMalloc(&d.d_perm, n_cfg * sizeof(uint32_t));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_groups, h->groups.size() * sizeof(dsi::CrnGroup));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_crn_units, h->crn_units.size() * sizeof(dsi::CrnUnit));
+    }
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(d.d_prefix, h->prefix.data(), (n_cfg + 1) * sizeof(uint64_t),
                           cudaMemcpyHostToDevice, d.stream);
@@ -677,6 +789,14 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     CUDA_TRY(h, cudaStreamSynchronize(d.stream));
   }
   fill_dev_cfg(h);
+  if (h->shared) {
+    const size_t ng = h->groups.size(), nu = h->crn_units.size();
+    std::vector<double> cost;
+    s = plan_shared(h, cost);
+    if (s == DSI_OK && (h->groups.size() != ng || h->crn_units.size() != nu))
+      s = fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS: the stream grouping changed; create a new handle");
+    if (s != DSI_OK) return s;
+  }
   h->ran = h->reduced = false;
   return upload(h);
 }
@@ -717,7 +837,28 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       p.keys.k1[r] = s_hi + (uint32_t)r * 0xBB67AE85u;
     }
     if (d.ev0) CUDA_TRY(h, cudaEventRecord(d.ev0, d.stream));
+    if (h->shared) {
+      dsi::CrnParams q{};
+      q.cfg = d.d_cfg;
+      q.perm = d.d_perm;
+      q.groups = d.d_groups;
+      q.units = d.d_crn_units;
+      q.acc = d.d_acc;
+      q.max_n = h->max_n;
+      q.max_nq = (h->max_n - 1 + 3) / 4 + 1;
+      q.max_runs = h->max_runs;
+      q.cfg_per_block = h->cfg_per_block;
+      q.keys = p.keys;
+      for (const auto &rg : d.ranges) {
+        if (rg.second <= rg.first) continue;
+        q.unit_begin = rg.first;
+        const int e = dsi::launch_crn_kernel(q, rg.second - rg.first, kCrnThreads, d.stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
+        h->launches += 1;
+      }
+    }
     for (const auto &rg : d.ranges) {
+      if (h->shared) break;
       if (rg.second <= rg.first) continue;
       p.unit_begin = rg.first;
       const int e = dsi::launch_trial_kernel(p, rg.second - rg.first, h->block_threads,

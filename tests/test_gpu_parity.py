@@ -169,6 +169,56 @@ def test_production_variant_matches_test_variant():
     sim_b.close()
 
 
+MOMENTS = ("sum_dsi_ticks", "sum_si_ticks", "sumsq_dsi_ticks", "sumsq_si_ticks", "sum_segments",
+           "sum_si_iters", "sum_accepts", "n_dsi_gt_nonsi", "n_dsi_gt_si", "trials", "mean_dsi", "std_dsi")
+
+
+@pytest.mark.parametrize("name", ["fuzz", "cfg2", "cfg3", "cfg4", "cfg5", "ragged"])
+def test_shared_streams_bit_identical_to_default(name):
+    """DSI_F_SHARED_STREAMS: one Philox pass per trial per group of configs
+    with equal (stream, threshold, N, T); every per-config moment must equal the default
+    mode's bit for bit (and so the oracle's, which the default mode matches)."""
+    if name == "fuzz":
+        cfgs, tick = W.fuzz(300, seed=31, trials=400)
+    elif name == "cfg2":
+        cfgs, tick = W.cfg2(trials=3000)
+    elif name == "cfg3":
+        cfgs, tick = W.cfg3(trials=1500, k_max=200, cells=slice(0, 10100, 37))
+    elif name == "cfg4":
+        cfgs, tick = W.cfg4(trials=2000)
+    elif name == "cfg5":
+        cfgs, tick = W.cfg5(D.dsi_min_lookahead, trials=300)
+        cfgs = cfgs[::13]
+    else:  # groups with trials not a multiple of the 128-trial tile, and a = 0 / a = 1 groups
+        rows = [(1.0, 0.25, a, k, sp, 77, 0, 129 + 7 * k) for a in (0.0, 0.5, 1.0) for k in (1, 3, 9)
+                for sp in (1, 7)]
+        cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
+        for i, r in enumerate(rows):
+            cfgs[i] = r
+        tick = 0.01
+    _, base = run_sim(cfgs, tick, flags=0)
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    for f in MOMENTS:
+        assert np.array_equal(res[f], base[f]), (name, f)
+    sim.close()
+
+
+def test_shared_streams_against_oracle_sample():
+    cfgs, tick = W.cfg3(trials=700, k_max=200, cells=slice(5, 10100, 1001))
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    for i in range(0, cfgs.size, 97):
+        assert_result_equals_oracle(res[i], oracle_sums(cfgs[i], tick, SEED), tick, ctx=f"crn {i}")
+    sim.close()
+
+
+def test_shared_streams_options_are_validated():
+    cfgs, tick = W.cfg1(trials=10)
+    for bad in (D.DSI_F_PER_TRIAL, D.DSI_F_HIST, D.DSI_F_PATTERN):
+        with pytest.raises(D.DsiError) as e:
+            D.Simulator(cfgs, tick=tick, seed=SEED, flags=D.DSI_F_SHARED_STREAMS | bad)
+        assert e.value.status == D.DSI_E_RANGE
+
+
 def test_seed_and_stream_change_the_draws():
     cfgs, tick = W.cfg1(trials=500)
     _, r1 = run_sim(cfgs, tick, flags=0)
