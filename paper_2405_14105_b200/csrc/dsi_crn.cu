@@ -4,17 +4,20 @@
 // N, n_trials) draw identical indicators for every trial index.  A group of such
 // configurations (e.g. the 20 000 (t_d, k) points of one acceptance rate of the
 // heatmap) therefore needs ONE Philox pass per trial.  This kernel:
-//   block = (group, slice of <= cfg_per_block configs of the group), loops over the
+//   block = (group, slice of <= CPT * blockDim configs of the group), loops over the
 //   group's trials in tiles of blockDim:
 //   phase 1 (one trial per thread): Philox + Bernoulli mask exactly as dsi_kernel.cu,
 //     then the trial's summary m = #zeros + 1, n2 = #segments with g >= 2 and the list
 //     of run lengths L >= 2 of accepted drafts (a segment of length g has L = g - 1),
 //     sorted in decreasing order, into shared memory;
-//   phase 2 (configs across threads, trials in lockstep): for each config,
-//     I = m + sum_{L >= k+1} floor(L/(k+1)),  L_DSI = m t_t + n2 S(1) + sum_{L >= k+1} (S(ceil(L/k)) - S(1))
+//   phase 2 (each thread owns CPT configs, the tile's trials in lockstep):
+//     I = m + sum_{L >= k+1} floor(L/(k+1)),
+//     L_DSI = m t_t + n2 S(1) + sum_{L >= k+1} (S(ceil(L/k)) - S(1))
 //     -- the closed form of DESIGN.md section 2 with short segments (2 <= g <= k+1)
-//     costing (0, S(1)) -- then the per-config integer moments.
+//     costing (0, S(1)) -- then the per-config integer moments, in registers.
 // Per-trial latencies, and so every sum, are bit-identical to the per-config kernel.
+// Bounds used for 32-bit arithmetic: L_DSI, L_SI < 2^31 (create validates
+// N (k t_d + t_t) < 2^31), I <= N <= 4096 so I^2 * 128 trials < 2^32.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -24,30 +27,45 @@
 namespace dsi {
 namespace {
 
-struct CfgLite {  // what phase 2 needs of a config (shared memory)
+constexpr int CRN_THREADS = 128;
+
+struct CfgLite {  // what phase 2 needs of a config (shared memory, 48 B)
   int32_t t_t, s1, si_cost, k_eff;
   uint32_t m_si, m_k_lo, m_k_hi, m_sp_lo;
   uint32_t m_sp_hi;
-  int32_t kd, sp_eff, pad;
+  int32_t kd, sp_eff, nonsi;
 };
 
-__device__ __forceinline__ void insert_desc(uint16_t *runs, int stride, int &nr, int L) {
+__device__ __forceinline__ void insert_desc(uint16_t *runs, int &nr, int L) {
   // insertion into runs[0..nr) kept in decreasing order (slot-interleaved layout)
   int i = nr++;
   while (i > 0) {
-    const int prev = runs[(i - 1) * stride];
+    const int prev = runs[(i - 1) * CRN_THREADS];
     if (prev >= L) break;
-    runs[i * stride] = (uint16_t)prev;
+    runs[i * CRN_THREADS] = (uint16_t)prev;
     --i;
   }
-  runs[i * stride] = (uint16_t)L;
+  runs[i * CRN_THREADS] = (uint16_t)L;
 }
 
-__global__ void __launch_bounds__(128) dsi_crn_kernel(const CrnParams P) {
+// Extra costs of a segment with L = g - 1 >= k + 1 accepted drafts (seg_long of the
+// per-config kernel): x = floor(L/(k+1)) SI iterations, y = S(ceil(L/k)) - S(1).
+__device__ __forceinline__ void long_run(int L, const CfgLite &l, int &ai, int &ay) {
+  const uint32_t x = magic_div((uint32_t)L, l.m_si, 0u);
+  const uint32_t b = magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
+  const uint32_t qq = magic_div(b, l.m_sp_lo, l.m_sp_hi);
+  const int rr = (int)b - (int)qq * l.sp_eff;
+  const int S = max((int)b * l.kd, rr * l.kd + (int)qq * l.t_t);
+  ai += (int)x;
+  ay += S - l.s1;
+}
+
+template <int CPT>
+__global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long s_msum;
   const CrnUnit un = P.units[P.unit_begin + blockIdx.x];
   const CrnGroup G = P.groups[un.group];
-  const int TT = blockDim.x;  // trials per tile (one per thread in phase 1)
   const int N = G.n_tokens;
   const int npos = N - 1;
   const int nwords = (npos + 31) >> 5;
@@ -59,38 +77,47 @@ __global__ void __launch_bounds__(128) dsi_crn_kernel(const CrnParams P) {
   unsigned char *sp = smem;
   uint4 *U = reinterpret_cast<uint4 *>(sp);
   sp += (size_t)P.max_nq * sizeof(uint4);
-  unsigned long long *acc = reinterpret_cast<unsigned long long *>(sp);  // [cfg][NF]
-  sp += (size_t)P.cfg_per_block * NF * sizeof(unsigned long long);
   CfgLite *cl = reinterpret_cast<CfgLite *>(sp);
-  sp += (size_t)P.cfg_per_block * sizeof(CfgLite);
-  uint2 *summ = reinterpret_cast<uint2 *>(sp);  // per trial slot: (m | n2 << 16, nruns)
-  sp += (size_t)TT * sizeof(uint2);
-  uint16_t *runs = reinterpret_cast<uint16_t *>(sp);  // runs[i * TT + slot]
+  sp += (size_t)CPT * CRN_THREADS * sizeof(CfgLite);
+  uint2 *summ = reinterpret_cast<uint2 *>(sp);  // per trial slot: (m | n2 << 16, nruns | maxL << 16)
+  sp += (size_t)CRN_THREADS * sizeof(uint2);
+  uint16_t *runs = reinterpret_cast<uint16_t *>(sp);  // runs[i * CRN_THREADS + slot]
 
+  if (threadIdx.x == 0) s_msum = 0ull;
   if (mode == MODE_STREAM)
-    for (int q = threadIdx.x; q < nq; q += TT) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
-  for (int j = threadIdx.x; j < (int)un.count; j += TT) {
-    const DevCfg c = P.cfg[P.perm[un.begin + j]];
-    CfgLite l;
-    l.t_t = c.t_t;
-    l.s1 = c.s1;
-    l.si_cost = c.si_cost;
-    l.k_eff = c.k_eff;
-    l.m_si = c.m_si;
-    l.m_k_lo = c.m_k_lo;
-    l.m_k_hi = c.m_k_hi;
-    l.m_sp_lo = c.m_sp_lo;
-    l.m_sp_hi = c.m_sp_hi;
-    l.kd = c.kd;
-    l.sp_eff = c.sp_eff;
-    l.pad = 0;
+    for (int q = threadIdx.x; q < nq; q += CRN_THREADS) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
+  for (int j = threadIdx.x; j < CPT * CRN_THREADS; j += CRN_THREADS) {
+    CfgLite l{};
+    if (j < (int)un.count) {
+      const DevCfg c = P.cfg[P.perm[un.begin + j]];
+      l.t_t = c.t_t;
+      l.s1 = c.s1;
+      l.si_cost = c.si_cost;
+      l.k_eff = c.k_eff;
+      l.m_si = c.m_si;
+      l.m_k_lo = c.m_k_lo;
+      l.m_k_hi = c.m_k_hi;
+      l.m_sp_lo = c.m_sp_lo;
+      l.m_sp_hi = c.m_sp_hi;
+      l.kd = c.kd;
+      l.sp_eff = c.sp_eff;
+      l.nonsi = N * c.t_t;
+    } else {
+      l.k_eff = 1 << 20;  // an empty slot: no run is ever long
+      l.m_sp_lo = 1u;
+    }
     cl[j] = l;
-    for (int f = 0; f < NF; ++f) acc[j * NF + f] = 0ull;
   }
   __syncthreads();
 
-  const uint64_t T = G.n_trials;
-  for (uint64_t tile0 = 0; tile0 < T; tile0 += TT) {
+  // per owned config: moments in registers for the whole group
+  unsigned long long a_i[CPT], a_i2[CPT], a_dsi[CPT], a_dsi2[CPT], a_gtn[CPT], a_gts[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) a_i[c] = a_i2[c] = a_dsi[c] = a_dsi2[c] = a_gtn[c] = a_gts[c] = 0ull;
+  unsigned long long my_m = 0ull;  // sum of m over this thread's phase-1 trials (config-independent)
+
+  const uint64_t T = un.t1;  // this unit's trials: [un.t0, un.t1)
+  for (uint64_t tile0 = un.t0; tile0 < T; tile0 += CRN_THREADS) {
     // ---------------- phase 1: one trial per thread -> summary + sorted long-run list
     const uint64_t t = tile0 + threadIdx.x;
     if (t < T) {
@@ -129,86 +156,88 @@ __global__ void __launch_bounds__(128) dsi_crn_kernel(const CrnParams P) {
           const uint32_t below = Rw & ((1u << zb) - 1u);
           const int prev = below ? base + 31 - __clz(below) : lastz;
           const int L = base + zb - prev - 1;  // accepted drafts in this segment
-          if (L >= 2) insert_desc(myruns, TT, nr, L);
+          if (L >= 2) insert_desc(myruns, nr, L);
         }
         lastz = base + 31 - __clz(Rw);
         run = nv - 1 - (31 - __clz(Rw));
       }
       n2 += run >= 1;  // the final segment (the trailing run, then position N)
-      if (run >= 2) insert_desc(myruns, TT, nr, run);
-      summ[threadIdx.x] = make_uint2((uint32_t)(nz + 1) | ((uint32_t)n2 << 16), (uint32_t)nr);
+      if (run >= 2) insert_desc(myruns, nr, run);
+      const uint32_t maxL = nr ? myruns[0] : 0u;
+      summ[threadIdx.x] = make_uint2((uint32_t)(nz + 1) | ((uint32_t)n2 << 16), (uint32_t)nr | (maxL << 16));
+      my_m += (unsigned)(nz + 1);
     }
     __syncthreads();
-    // ---------------- phase 2: configs across threads, this tile's trials in lockstep
-    const int ntr = (int)min((uint64_t)TT, T - tile0);
-    for (int j = threadIdx.x; j < (int)un.count; j += TT) {
-      const CfgLite l = cl[j];
-      const int Lk = l.k_eff + 1;
-      const int64_t nonsi = (int64_t)N * l.t_t;
-      unsigned long long a_i = 0, a_i2 = 0, a_dsi = 0, a_dsi2 = 0, a_gtn = 0, a_gts = 0, a_m = 0;
-      for (int s = 0; s < ntr; ++s) {
-        const uint2 sm = summ[s];
-        const int m = (int)(sm.x & 0xffffu), n2 = (int)(sm.x >> 16), nr = (int)sm.y;
+    // ---------------- phase 2: CPT configs per thread, the tile's trials in lockstep
+    const int ntr = (int)min((uint64_t)CRN_THREADS, T - tile0);
+    CfgLite l[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) l[c] = cl[threadIdx.x + c * CRN_THREADS];
+    uint32_t p_i[CPT], p_i2[CPT], p_gtn[CPT], p_gts[CPT];  // per-tile 32-bit partial sums
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) p_i[c] = p_i2[c] = p_gtn[c] = p_gts[c] = 0u;
+    for (int s = 0; s < ntr; ++s) {
+      const uint2 sm = summ[s];
+      const int m = (int)(sm.x & 0xffffu), n2 = (int)(sm.x >> 16);
+      const int nr = (int)(sm.y & 0xffffu), maxL = (int)(sm.y >> 16);
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
         int ai = 0, ay = 0;
-        for (int r = 0; r < nr; ++r) {
-          const int L = runs[r * TT + s];
-          if (L < Lk) break;
-          // a segment of g = L + 1: ceil(g/(k+1)) - 1 = floor(L/(k+1)) extra SI iterations,
-          // thread b = ceil((g-1)/k) = ceil(L/k) settles its last position
-          const uint32_t x = magic_div((uint32_t)L, l.m_si, 0u);
-          const uint32_t b = magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
-          const uint32_t qq = magic_div(b, l.m_sp_lo, l.m_sp_hi);
-          const int rr = (int)b - (int)qq * l.sp_eff;
-          const int S = max((int)b * l.kd, rr * l.kd + (int)qq * l.t_t);
-          ai += (int)x;
-          ay += S - l.s1;
+        if (maxL > l[c].k_eff) {  // some run is long for this config
+          for (int r = 0; r < nr; ++r) {
+            const int L = runs[r * CRN_THREADS + s];
+            if (L <= l[c].k_eff) break;
+            long_run(L, l[c], ai, ay);
+          }
         }
-        const int iters = m + ai;
-        const int64_t dsi = (int64_t)m * l.t_t + (int64_t)n2 * l.s1 + ay;
-        const int64_t si = (int64_t)iters * l.si_cost;
-        a_m += (unsigned)m;
-        a_i += (unsigned)iters;
-        a_i2 += (unsigned long long)iters * (unsigned long long)iters;
-        a_dsi += (unsigned long long)dsi;
-        a_dsi2 += (unsigned long long)dsi * (unsigned long long)dsi;
-        a_gtn += dsi > nonsi;
-        a_gts += dsi > si;
+        const uint32_t iters = (uint32_t)(m + ai);
+        const uint32_t dsi = (uint32_t)(m * l[c].t_t + n2 * l[c].s1 + ay);
+        const uint32_t si = iters * (uint32_t)l[c].si_cost;
+        p_i[c] += iters;
+        p_i2[c] += iters * iters;
+        a_dsi[c] += dsi;
+        a_dsi2[c] += (unsigned long long)dsi * dsi;
+        p_gtn[c] += dsi > (uint32_t)l[c].nonsi;
+        p_gts[c] += dsi > si;
       }
-      unsigned long long *a = acc + (size_t)j * NF;
-      a[F_M] += a_m;
-      a[F_I] += a_i;
-      a[F_I2] += a_i2;
-      a[F_DSI] += a_dsi;
-      a[F_DSI2] += a_dsi2;
-      a[F_GT_NONSI] += a_gtn;
-      a[F_GT_SI] += a_gts;
-      a[F_TRIALS] += (unsigned long long)ntr;
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      a_i[c] += p_i[c];
+      a_i2[c] += p_i2[c];
+      a_gtn[c] += p_gtn[c];
+      a_gts[c] += p_gts[c];
     }
     __syncthreads();
   }
-  // every config of the slice is owned by this block: plain stores of its moments
-  for (int j = threadIdx.x; j < (int)un.count; j += TT) {
-    unsigned long long *dst = P.acc + (size_t)P.perm[un.begin + j] * NF;
-    for (int f = 0; f < NF; ++f) dst[f] = acc[j * NF + f];
+  // the sum of m over this unit's trials (identical for all its configs), then one
+  // 64-bit integer atomic per field and config (exact and order-free)
+  for (int o = 16; o > 0; o >>= 1) my_m += __shfl_xor_sync(0xffffffffu, my_m, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_msum, my_m);
+  __syncthreads();
+  const unsigned long long msum = s_msum;
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int j = threadIdx.x + c * CRN_THREADS;
+    if (j < (int)un.count) {
+      unsigned long long *dst = P.acc + (size_t)P.perm[un.begin + j] * NF;
+      atomicAdd(dst + F_M, msum);
+      atomicAdd(dst + F_I, a_i[c]);
+      atomicAdd(dst + F_I2, a_i2[c]);
+      atomicAdd(dst + F_DSI, a_dsi[c]);
+      atomicAdd(dst + F_DSI2, a_dsi2[c]);
+      if (a_gtn[c]) atomicAdd(dst + F_GT_NONSI, a_gtn[c]);
+      if (a_gts[c]) atomicAdd(dst + F_GT_SI, a_gts[c]);
+      atomicAdd(dst + F_TRIALS, (unsigned long long)(un.t1 - un.t0));
+    }
   }
 }
 
-}  // namespace
-
-size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs) {
-  const int max_nq = (max_n - 1 + 3) / 4 + 1;
-  return (size_t)max_nq * sizeof(uint4) + (size_t)cfg_per_block * NF * sizeof(unsigned long long) +
-         (size_t)cfg_per_block * sizeof(CfgLite) + (size_t)block_threads * sizeof(uint2) +
-         (size_t)block_threads * max_runs * sizeof(uint16_t);
-}
-
-int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream) {
-  if (n_units == 0) return 0;
-  cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = crn_kernel_smem(p.max_n, block_threads, p.cfg_per_block, p.max_runs);
+template <int CPT>
+int launch_cpt(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
     const cudaError_t e =
-        cudaFuncSetAttribute(dsi_crn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(dsi_crn_kernel<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
   const uint64_t max_grid = 0x7fffffffull;
@@ -216,12 +245,33 @@ int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, v
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_crn_kernel<<<(unsigned)n, block_threads, smem, st>>>(q);
+    dsi_crn_kernel<CPT><<<(unsigned)n, CRN_THREADS, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
   }
   return 0;
+}
+
+}  // namespace
+
+size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs) {
+  const int max_nq = (max_n - 1 + 3) / 4 + 1;
+  return (size_t)max_nq * sizeof(uint4) + (size_t)cfg_per_block * sizeof(CfgLite) +
+         (size_t)block_threads * sizeof(uint2) + (size_t)block_threads * max_runs * sizeof(uint16_t);
+}
+
+int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream) {
+  if (n_units == 0) return 0;
+  if (block_threads != CRN_THREADS) return (int)cudaErrorInvalidValue;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t smem = crn_kernel_smem(p.max_n, CRN_THREADS, p.cfg_per_block, p.max_runs);
+  switch (p.cfg_per_block / CRN_THREADS) {
+    case 1: return launch_cpt<1>(p, n_units, smem, st);
+    case 2: return launch_cpt<2>(p, n_units, smem, st);
+    case 4: return launch_cpt<4>(p, n_units, smem, st);
+    default: return (int)cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace dsi

@@ -80,11 +80,12 @@ struct CrnGroup {      // configs drawing identical indicators: equal (stream, t
   uint32_t mode;       // MODE_*
   uint64_t n_trials;
 };
-struct CrnUnit {       // one block: a slice of one group's configs
+struct CrnUnit {       // one block: a slice of one group's configs over a range of its trials
   uint32_t group;
   uint32_t begin;      // position in perm
   uint32_t count;      // <= cfg_per_block
   uint32_t pad;
+  uint64_t t0, t1;     // trials [t0, t1)
 };
 struct CrnParams {
   const DevCfg *cfg;
@@ -92,7 +93,7 @@ struct CrnParams {
   const CrnGroup *groups;
   const CrnUnit *units;
   uint64_t unit_begin;
-  unsigned long long *acc;  // n_cfg * NF, written with plain stores (a config has one owner)
+  unsigned long long *acc;  // n_cfg * NF, integer atomics (a config may span trial ranges)
   int32_t max_n, max_nq, max_runs, cfg_per_block;
   Keys keys;
 };

@@ -391,16 +391,8 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
       return x.sp < y.sp;
     });
     h->max_runs = h->max_n / 3 + 2;  // runs of >= 2 accepted drafts in one trial
-    h->cfg_per_block = kCrnThreads;
-    for (int cpb : {4 * kCrnThreads, 2 * kCrnThreads}) {
-      if (dsi::crn_kernel_smem(h->max_n, kCrnThreads, cpb, h->max_runs) <= 100 * 1024) {
-        h->cfg_per_block = cpb;
-        break;
-      }
-    }
+    // groups first, then the block shape: configs per block follow the typical group size
     h->groups.clear();
-    h->crn_units.clear();
-    cost.clear();
     for (size_t i = 0; i < n;) {
       const CfgTicks &k0 = t[h->perm[i]];
       size_t j = i + 1;
@@ -417,17 +409,48 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
       g.thr = (uint32_t)std::min<uint64_t>(k0.thr, 0xffffffffull);
       g.mode = k0.thr >= (1ull << 32) ? dsi::MODE_ALL_ACCEPT : (k0.thr == 0 ? dsi::MODE_ALL_REJECT : dsi::MODE_STREAM);
       g.n_trials = k0.trials;
-      for (size_t b = i; b < j; b += (size_t)h->cfg_per_block) {
-        dsi::CrnUnit u{};
-        u.group = (uint32_t)h->groups.size();
-        u.begin = (uint32_t)b;
-        u.count = (uint32_t)std::min<size_t>((size_t)h->cfg_per_block, j - b);
-        h->crn_units.push_back(u);
-        // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
-        cost.push_back((double)k0.trials * ((double)k0.n * 12.0 + (double)u.count * 25.0));
-      }
       h->groups.push_back(g);
       i = j;
+    }
+    std::vector<uint32_t> sizes;
+    for (const auto &g : h->groups) sizes.push_back(g.count);
+    std::nth_element(sizes.begin(), sizes.begin() + sizes.size() / 2, sizes.end());
+    const uint32_t median = sizes[sizes.size() / 2];
+    h->cfg_per_block = kCrnThreads;
+    for (int cpb : {4 * kCrnThreads, 2 * kCrnThreads}) {
+      if (median >= (uint32_t)cpb &&
+          dsi::crn_kernel_smem(h->max_n, kCrnThreads, cpb, h->max_runs) <= 96 * 1024) {
+        h->cfg_per_block = cpb;
+        break;
+      }
+    }
+    // units: (group, slice of cfg_per_block configs, range of trials); trials are split
+    // until there are enough blocks to fill every SM of every device a few times
+    size_t slices = 0;
+    for (const auto &g : h->groups) slices += (g.count + h->cfg_per_block - 1) / h->cfg_per_block;
+    const int total_devices = h->opt.world * h->opt.n_devices;
+    const uint64_t target = 148ull * 4 * 4 * (uint64_t)total_devices;
+    const uint64_t split = std::max<uint64_t>(1, (target + slices - 1) / slices);
+    h->crn_units.clear();
+    cost.clear();
+    for (uint32_t gi = 0; gi < h->groups.size(); ++gi) {
+      const dsi::CrnGroup &g = h->groups[gi];
+      const uint64_t tiles = (g.n_trials + kCrnThreads - 1) / kCrnThreads;
+      const uint64_t nchunks = std::min<uint64_t>(split, tiles);
+      for (uint32_t b = g.first; b < g.first + g.count; b += (uint32_t)h->cfg_per_block) {
+        const uint32_t cnt = std::min<uint32_t>((uint32_t)h->cfg_per_block, g.first + g.count - b);
+        for (uint64_t c = 0; c < nchunks; ++c) {
+          dsi::CrnUnit u{};
+          u.group = gi;
+          u.begin = b;
+          u.count = cnt;
+          u.t0 = (tiles * c / nchunks) * kCrnThreads;
+          u.t1 = std::min<uint64_t>((tiles * (c + 1) / nchunks) * kCrnThreads, g.n_trials);
+          h->crn_units.push_back(u);
+          // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
+          cost.push_back((double)(u.t1 - u.t0) * ((double)g.n_tokens * 12.0 + (double)cnt * 25.0));
+        }
+      }
     }
   } catch (...) {
     return fail(h, DSI_E_NOMEM, "shared-stream plan");

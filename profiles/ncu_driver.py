@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg3")
 ap.add_argument("--stride", type=int, default=10)
 ap.add_argument("--runs", type=int, default=1)
+ap.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
 args = ap.parse_args()
 if args.workload == "cfg3":
     cfgs, tick = W.cfg3(cells=slice(None, None, args.stride))
@@ -27,7 +28,7 @@ elif args.workload == "cfg5":
     cfgs = cfgs[:: args.stride]
 else:
     raise SystemExit("workload")
-with D.Simulator(cfgs, tick=tick, seed=W.SEED) as sim:
+with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_SHARED_STREAMS if args.shared else 0) as sim:
     for _ in range(args.runs):
         sim.run()
         sim.reduce()
