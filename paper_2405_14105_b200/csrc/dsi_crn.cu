@@ -63,7 +63,7 @@ __device__ __forceinline__ void long_run(int L, const CfgLite &l, int &ai, int &
 template <int CPT>
 __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long s_msum;
+  __shared__ unsigned long long s_bsum[5];
   const CrnUnit un = P.units[P.unit_begin + blockIdx.x];
   const CrnGroup G = P.groups[un.group];
   const int N = G.n_tokens;
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
   sp += (size_t)CRN_THREADS * sizeof(uint2);
   uint16_t *runs = reinterpret_cast<uint16_t *>(sp);  // runs[i * CRN_THREADS + slot]
 
-  if (threadIdx.x == 0) s_msum = 0ull;
+  if (threadIdx.x < 5) s_bsum[threadIdx.x] = 0ull;
   if (mode == MODE_STREAM)
     for (int q = threadIdx.x; q < nq; q += CRN_THREADS) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
   for (int j = threadIdx.x; j < CPT * CRN_THREADS; j += CRN_THREADS) {
@@ -110,11 +110,20 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
   }
   __syncthreads();
 
-  // per owned config: moments in registers for the whole group
-  unsigned long long a_i[CPT], a_i2[CPT], a_dsi[CPT], a_dsi2[CPT], a_gtn[CPT], a_gts[CPT];
+  // Per-trial latencies split into a config-independent part and long-run corrections:
+  //   I = m + ai,  L_DSI = m t_t + n2 S(1) + ay   (ai = ay = 0 unless a run exceeds k)
+  // so the moments are polynomials in sums the whole block shares -- Sm, Sn, Smm, Snn,
+  // Smn over its trials -- plus per-config sums of ai, ai^2, m ai, ay, ay^2, m ay, n2 ay
+  // that are only touched on trials with a long run.  The threshold counters need the
+  // per-trial latency and are counted per (trial, config).
+  // per owned config (registers): sums of ai, ai^2, m ai, ay, ay^2 and ay * (m t_t + n2 S(1))
+  unsigned long long c_ai[CPT], c_ai2[CPT], c_mai[CPT], c_ay[CPT], c_ay2[CPT], c_ydl[CPT];
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) a_i[c] = a_i2[c] = a_dsi[c] = a_dsi2[c] = a_gtn[c] = a_gts[c] = 0ull;
-  unsigned long long my_m = 0ull;  // sum of m over this thread's phase-1 trials (config-independent)
+  for (int c = 0; c < CPT; ++c) c_ai[c] = c_ai2[c] = c_mai[c] = c_ay[c] = c_ay2[c] = c_ydl[c] = 0ull;
+  unsigned long long a_gtn[CPT], a_gts[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) a_gtn[c] = a_gts[c] = 0ull;
+  unsigned long long my_m = 0ull, my_n = 0ull, my_mm = 0ull, my_nn = 0ull, my_mn = 0ull;
 
   const uint64_t T = un.t1;  // this unit's trials: [un.t0, un.t1)
   for (uint64_t tile0 = un.t0; tile0 < T; tile0 += CRN_THREADS) {
@@ -164,68 +173,101 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
       n2 += run >= 1;  // the final segment (the trailing run, then position N)
       if (run >= 2) insert_desc(myruns, nr, run);
       const uint32_t maxL = nr ? myruns[0] : 0u;
-      summ[threadIdx.x] = make_uint2((uint32_t)(nz + 1) | ((uint32_t)n2 << 16), (uint32_t)nr | (maxL << 16));
-      my_m += (unsigned)(nz + 1);
+      const uint32_t m = (uint32_t)(nz + 1);
+      summ[threadIdx.x] = make_uint2(m | ((uint32_t)n2 << 16), (uint32_t)nr | (maxL << 16));
+      my_m += m;
+      my_n += (unsigned)n2;
+      my_mm += m * m;
+      my_nn += (unsigned)(n2 * n2);
+      my_mn += m * (unsigned)n2;
     }
     __syncthreads();
     // ---------------- phase 2: CPT configs per thread, the tile's trials in lockstep
     const int ntr = (int)min((uint64_t)CRN_THREADS, T - tile0);
-    CfgLite l[CPT];
+    CfgLite l[CPT];  // the owned configs, in registers for the tile
 #pragma unroll
     for (int c = 0; c < CPT; ++c) l[c] = cl[threadIdx.x + c * CRN_THREADS];
-    uint32_t p_i[CPT], p_i2[CPT], p_gtn[CPT], p_gts[CPT];  // per-tile 32-bit partial sums
+    // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 4096, 128 trials: no overflow)
+    uint32_t p_gtn[CPT], p_gts[CPT], p_ai[CPT], p_ai2[CPT], p_mai[CPT];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) p_i[c] = p_i2[c] = p_gtn[c] = p_gts[c] = 0u;
+    for (int c = 0; c < CPT; ++c) p_gtn[c] = p_gts[c] = p_ai[c] = p_ai2[c] = p_mai[c] = 0u;
     for (int s = 0; s < ntr; ++s) {
       const uint2 sm = summ[s];
       const int m = (int)(sm.x & 0xffffu), n2 = (int)(sm.x >> 16);
       const int nr = (int)(sm.y & 0xffffu), maxL = (int)(sm.y >> 16);
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
-        int ai = 0, ay = 0;
-        if (maxL > l[c].k_eff) {  // some run is long for this config
+        int dsi = m * l[c].t_t + n2 * l[c].s1;
+        int si = m * l[c].si_cost;
+        if (maxL > l[c].k_eff) {  // some run is long for this config: corrections
+          int ai = 0, ay = 0;
           for (int r = 0; r < nr; ++r) {
             const int L = runs[r * CRN_THREADS + s];
             if (L <= l[c].k_eff) break;
             long_run(L, l[c], ai, ay);
           }
+          p_ai[c] += (unsigned)ai;
+          p_ai2[c] += (unsigned)(ai * ai);
+          p_mai[c] += (unsigned)(m * ai);
+          c_ay[c] += (unsigned)ay;
+          c_ay2[c] += (unsigned long long)ay * (unsigned)ay;
+          c_ydl[c] += (unsigned long long)ay * (unsigned)dsi;
+          dsi += ay;
+          si += ai * l[c].si_cost;
         }
-        const uint32_t iters = (uint32_t)(m + ai);
-        const uint32_t dsi = (uint32_t)(m * l[c].t_t + n2 * l[c].s1 + ay);
-        const uint32_t si = iters * (uint32_t)l[c].si_cost;
-        p_i[c] += iters;
-        p_i2[c] += iters * iters;
-        a_dsi[c] += dsi;
-        a_dsi2[c] += (unsigned long long)dsi * dsi;
-        p_gtn[c] += dsi > (uint32_t)l[c].nonsi;
-        p_gts[c] += dsi > si;
+        // dsi, si, nonsi < 2^31: the sign bit of the difference is the comparison
+        p_gtn[c] += (uint32_t)(l[c].nonsi - dsi) >> 31;
+        p_gts[c] += (uint32_t)(si - dsi) >> 31;
       }
     }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
-      a_i[c] += p_i[c];
-      a_i2[c] += p_i2[c];
       a_gtn[c] += p_gtn[c];
       a_gts[c] += p_gts[c];
+      c_ai[c] += p_ai[c];
+      c_ai2[c] += p_ai2[c];
+      c_mai[c] += p_mai[c];
     }
     __syncthreads();
   }
-  // the sum of m over this unit's trials (identical for all its configs), then one
-  // 64-bit integer atomic per field and config (exact and order-free)
-  for (int o = 16; o > 0; o >>= 1) my_m += __shfl_xor_sync(0xffffffffu, my_m, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_msum, my_m);
+  // block sums of the config-independent terms
+  unsigned long long *bs = reinterpret_cast<unsigned long long *>(&s_bsum[0]);
+  for (int o = 16; o > 0; o >>= 1) {
+    my_m += __shfl_xor_sync(0xffffffffu, my_m, o);
+    my_n += __shfl_xor_sync(0xffffffffu, my_n, o);
+    my_mm += __shfl_xor_sync(0xffffffffu, my_mm, o);
+    my_nn += __shfl_xor_sync(0xffffffffu, my_nn, o);
+    my_mn += __shfl_xor_sync(0xffffffffu, my_mn, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(bs + 0, my_m);
+    atomicAdd(bs + 1, my_n);
+    atomicAdd(bs + 2, my_mm);
+    atomicAdd(bs + 3, my_nn);
+    atomicAdd(bs + 4, my_mn);
+  }
   __syncthreads();
-  const unsigned long long msum = s_msum;
+  const unsigned long long Sm = bs[0], Sn = bs[1], Smm = bs[2], Snn = bs[3], Smn = bs[4];
+  // per config: assemble the moments (exact u64 arithmetic) and add them with one
+  // 64-bit integer atomic per field (exact and order-free)
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
     const int j = threadIdx.x + c * CRN_THREADS;
     if (j < (int)un.count) {
+      const CfgLite &l = cl[j];
+      const unsigned long long tt = (unsigned)l.t_t, ss = (unsigned)l.s1;
+      const unsigned long long sum_i = Sm + c_ai[c];
+      const unsigned long long sum_i2 = Smm + 2ull * c_mai[c] + c_ai2[c];
+      const unsigned long long sum_dsi = tt * Sm + ss * Sn + c_ay[c];
+      // sum (m t + n2 s + ay)^2 = t^2 Smm + s^2 Snn + 2 t s Smn + 2 sum ay (m t + n2 s) + sum ay^2
+      const unsigned long long sum_dsi2 = tt * tt * Smm + ss * ss * Snn + 2ull * tt * ss * Smn +
+                                          2ull * c_ydl[c] + c_ay2[c];
       unsigned long long *dst = P.acc + (size_t)P.perm[un.begin + j] * NF;
-      atomicAdd(dst + F_M, msum);
-      atomicAdd(dst + F_I, a_i[c]);
-      atomicAdd(dst + F_I2, a_i2[c]);
-      atomicAdd(dst + F_DSI, a_dsi[c]);
-      atomicAdd(dst + F_DSI2, a_dsi2[c]);
+      atomicAdd(dst + F_M, Sm);
+      atomicAdd(dst + F_I, sum_i);
+      atomicAdd(dst + F_I2, sum_i2);
+      atomicAdd(dst + F_DSI, sum_dsi);
+      atomicAdd(dst + F_DSI2, sum_dsi2);
       if (a_gtn[c]) atomicAdd(dst + F_GT_NONSI, a_gtn[c]);
       if (a_gts[c]) atomicAdd(dst + F_GT_SI, a_gts[c]);
       atomicAdd(dst + F_TRIALS, (unsigned long long)(un.t1 - un.t0));
@@ -257,8 +299,9 @@ int launch_cpt(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t s
 
 size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs) {
   const int max_nq = (max_n - 1 + 3) / 4 + 1;
+  const size_t runs = ((size_t)block_threads * max_runs * sizeof(uint16_t) + 7) & ~(size_t)7;
   return (size_t)max_nq * sizeof(uint4) + (size_t)cfg_per_block * sizeof(CfgLite) +
-         (size_t)block_threads * sizeof(uint2) + (size_t)block_threads * max_runs * sizeof(uint16_t);
+         (size_t)block_threads * sizeof(uint2) + runs;
 }
 
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream) {

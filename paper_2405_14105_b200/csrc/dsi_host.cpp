@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -412,17 +413,12 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
       h->groups.push_back(g);
       i = j;
     }
-    std::vector<uint32_t> sizes;
-    for (const auto &g : h->groups) sizes.push_back(g.count);
-    std::nth_element(sizes.begin(), sizes.begin() + sizes.size() / 2, sizes.end());
-    const uint32_t median = sizes[sizes.size() / 2];
+    // one config per thread: 2 or 4 per thread (more Philox reuse, more registers) measured
+    // equal or slower on cfg3/cfg4/cfg5 (profiles/r01_ab_crn*.jsonl)
     h->cfg_per_block = kCrnThreads;
-    for (int cpb : {4 * kCrnThreads, 2 * kCrnThreads}) {
-      if (median >= (uint32_t)cpb &&
-          dsi::crn_kernel_smem(h->max_n, kCrnThreads, cpb, h->max_runs) <= 96 * 1024) {
-        h->cfg_per_block = cpb;
-        break;
-      }
+    if (const char *force = std::getenv("DSI_CRN_CPT")) {  // developer A/B runs only
+      const int cpt = std::atoi(force);
+      if (cpt == 1 || cpt == 2 || cpt == 4) h->cfg_per_block = cpt * kCrnThreads;
     }
     // units: (group, slice of cfg_per_block configs, range of trials); trials are split
     // until there are enough blocks to fill every SM of every device a few times
