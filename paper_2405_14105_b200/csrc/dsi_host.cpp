@@ -10,6 +10,7 @@
 #include <nccl.h>  // types and enums only; libnccl is loaded with dlopen at first use
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -268,7 +269,7 @@ template <class Fn>
 void parallel_for(size_t n, Fn fn) {
   size_t nt = std::thread::hardware_concurrency();
   if (nt == 0) nt = 1;
-  nt = std::min<size_t>(nt, 16);
+  nt = std::min<size_t>(nt, 32);
   if (n < (1u << 16) || nt == 1) {
     fn((size_t)0, n);
     return;
@@ -937,11 +938,13 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
     CUDA_TRY(h, cudaSetDevice(d.ordinal));
     CUDA_TRY(h, cudaStreamSynchronize(d.stream));
   }
-  // check the partition: every trial simulated exactly once
-  for (size_t i = 0; i < n_cfg; ++i) {
-    if (h->host_acc.p[i * dsi::NF + dsi::F_TRIALS] != h->ticks[i].trials)
-      return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
-  }
+  // check the partition (every trial simulated exactly once) before writing any output
+  std::atomic<bool> bad_trials{false};
+  parallel_for(n_cfg, [&](size_t b, size_t e) {
+    for (size_t i = b; i < e; ++i)
+      if (h->host_acc.p[i * dsi::NF + dsi::F_TRIALS] != h->ticks[i].trials) bad_trials = true;
+  });
+  if (bad_trials) return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
   const double tick = h->opt.tick;
   parallel_for(n_cfg, [&](size_t b, size_t e) {
   for (size_t i = b; i < e; ++i) {

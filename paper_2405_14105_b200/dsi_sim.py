@@ -263,8 +263,9 @@ class Simulator:
         dsi_sim_run(self.h)
         return self
 
-    def reduce(self) -> np.ndarray:
-        return dsi_sim_reduce(self.h, self.n)
+    def reduce(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Per-config results; pass a preallocated RESULT_DTYPE array to reuse its pages."""
+        return dsi_sim_reduce(self.h, self.n, out)
 
     def trials(self, cfg: int, first: int = 0, count: int | None = None) -> dict:
         if count is None:
