@@ -1,0 +1,113 @@
+"""Command-line front end of the simulator (every number comes from libdsi_sim.so).
+
+    python -m paper_2405_14105_b200 plan --t-target 1.0 --t-drafter 0.05 --sp 4
+    python -m paper_2405_14105_b200 simulate --t-target 20.6 --t-drafter 6.8 --accept 0.93 \
+        --lookahead 5 --sp 7 --n-tokens 50 --trials 100000 --tick 0.1
+    python -m paper_2405_14105_b200 table2 [--trials 100000] [--sp 8] [--n-tokens 100]
+    python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200] [--csv out.csv] [--shared]
+
+`plan` is Eq. 1; `table2` evaluates the Table 2 (target, drafter, acceptance)
+rows offline with lookahead in {1, 5, 10}, SI over all of them and DSI over the
+Eq.-1-feasible ones (the protocol of P:273); `heatmap` is Fig. 3.
+Exit codes: 0 success, 2 invalid arguments (DSI_E_RANGE / DSI_E_TICK / ...), 3 device error.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+
+import numpy as np
+
+from . import dsi_sim as D
+from . import workloads as W
+
+
+def _ticks(x: float, tick: float) -> int:
+    return int(round(x / tick))
+
+
+def cmd_plan(a) -> dict:
+    tt, td = _ticks(a.t_target, a.tick), _ticks(a.t_drafter, a.tick)
+    k = D.dsi_min_lookahead(tt, td, a.sp)
+    return {"min_lookahead": k, "processors": D.dsi_required_processors(tt, td, k),
+            "max_useful_sp": -(-tt // td), "eq1_feasible_at_k": bool(D.dsi_eq1_feasible(tt, td, k, a.sp))}
+
+
+def cmd_simulate(a) -> dict:
+    cfg = np.zeros(1, D.CONFIG_DTYPE)
+    cfg[0] = (a.t_target, a.t_drafter, a.accept, a.lookahead, a.sp, a.n_tokens, a.stream, a.trials)
+    with D.Simulator(cfg, tick=a.tick, seed=a.seed) as sim:
+        r = sim.run().reduce()[0]
+    return {k: (float(r[k]) if r.dtype[k].kind == "f" else int(r[k])) for k in r.dtype.names}
+
+
+def table2(trials: int, sp: int, n_tokens: int, seed: int = W.SEED, device: int = 0) -> list:
+    cfgs, tick = W.cfg2(trials=trials, sp=sp, n_tokens=n_tokens)
+    with D.Simulator(cfgs, tick=tick, seed=seed, device=device) as sim:
+        res = sim.run().reduce()
+    cells = D.dsi_heatmap(cfgs, res)
+    rows = []
+    for (name, *_), c in zip(W.TABLE2_ROWS, cells):
+        rows.append({"pair": name, "si_ms": float(c["si"]), "si_lookahead": int(c["si_lookahead"]),
+                     "dsi_ms": float(c["dsi"]), "dsi_lookahead": int(c["dsi_lookahead"]),
+                     "nonsi_ms": float(c["nonsi"]), "speedup_dsi_vs_si": float(c["r_si_dsi"])})
+    return rows
+
+
+def cmd_table2(a) -> list:
+    return table2(a.trials, a.sp, a.n_tokens, a.seed)
+
+
+def cmd_heatmap(a) -> dict:
+    cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
+    flags = D.DSI_F_SHARED_STREAMS if a.shared else 0
+    with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags) as sim:
+        res = sim.run().reduce()
+    cells = D.dsi_heatmap(cfgs, res)
+    if a.csv:
+        D.dsi_heatmap_csv(cells, a.csv)
+    i = int(np.nanargmax(cells["r_min_dsi"]))
+    return {"cells": int(cells.size), "csv": a.csv,
+            "max_min_si_nonsi_over_dsi": float(cells["r_min_dsi"][i]),
+            "at": {"t_drafter": float(cells["t_drafter"][i]), "accept_rate": float(cells["accept_rate"][i])},
+            "si_slower_than_nonsi_cells": int(np.sum(cells["r_nonsi_si"] < 1.0)),
+            "dsi_slower_than_si_cells": int(np.sum(cells["r_si_dsi"] < 1.0))}
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="python -m paper_2405_14105_b200")
+    ap.add_argument("--seed", type=int, default=W.SEED)
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    p = sub.add_parser("plan", help="Eq. 1: minimal lookahead and processors")
+    p.add_argument("--t-target", type=float, required=True)
+    p.add_argument("--t-drafter", type=float, required=True)
+    p.add_argument("--sp", type=int, required=True)
+    p.add_argument("--tick", type=float, default=0.01)
+    p = sub.add_parser("simulate", help="one configuration")
+    for f in ("--t-target", "--t-drafter", "--accept"):
+        p.add_argument(f, type=float, required=True)
+    for f in ("--lookahead", "--sp", "--n-tokens"):
+        p.add_argument(f, type=int, required=True)
+    p.add_argument("--trials", type=int, default=100_000)
+    p.add_argument("--tick", type=float, default=0.01)
+    p.add_argument("--stream", type=int, default=0)
+    p = sub.add_parser("table2", help="Table 2 pairs offline, lookahead in {1, 5, 10}")
+    p.add_argument("--trials", type=int, default=100_000)
+    p.add_argument("--sp", type=int, default=8)
+    p.add_argument("--n-tokens", type=int, default=100)
+    p = sub.add_parser("heatmap", help="Fig. 3 grid; optional CSV")
+    p.add_argument("--trials", type=int, default=10_000)
+    p.add_argument("--k-max", type=int, default=200)
+    p.add_argument("--sp", type=int, default=7)
+    p.add_argument("--n-tokens", type=int, default=100)
+    p.add_argument("--csv", default=None)
+    p.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
+    a = ap.parse_args(argv)
+    try:
+        out = {"plan": cmd_plan, "simulate": cmd_simulate, "table2": cmd_table2, "heatmap": cmd_heatmap}[a.cmd](a)
+    except D.DsiError as e:
+        print(str(e), file=sys.stderr)
+        return 3 if e.status in (D.DSI_E_DEVICE, D.DSI_E_COMM, D.DSI_E_NOMEM) else 2
+    print(json.dumps(out, indent=1))
+    return 0
