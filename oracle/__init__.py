@@ -45,7 +45,8 @@ class _Config(ctypes.Structure):
     _fields_ = [("t_target", ctypes.c_int64), ("t_drafter", ctypes.c_int64),
                 ("accept_rate", ctypes.c_double), ("lookahead", ctypes.c_int32),
                 ("sp_degree", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
-                ("stream_id", ctypes.c_uint32)]
+                ("stream_id", ctypes.c_uint32), ("t_target_first", ctypes.c_int64),
+                ("t_drafter_first", ctypes.c_int64)]
 
 
 class _TrialOut(ctypes.Structure):
@@ -95,11 +96,13 @@ class Config:
     sp_degree: int
     n_tokens: int
     stream_id: int = 0
+    t_target_first: int = 0   # TTFT variant: 0 = same as t_target
+    t_drafter_first: int = 0  # TTFT variant: 0 = same as t_drafter
 
     def _c(self) -> _Config:
         return _Config(int(self.t_target), int(self.t_drafter), float(self.accept_rate),
                        int(self.lookahead), int(self.sp_degree), int(self.n_tokens),
-                       int(self.stream_id))
+                       int(self.stream_id), int(self.t_target_first), int(self.t_drafter_first))
 
 
 def ticks(x: float, tick: float) -> int:
@@ -162,7 +165,7 @@ def run(cfg: Config, seed: int, first: int = 0, count: int = 1, pattern: bool = 
     if rc:
         raise ValueError(f"oracle_run failed for {cfg}")
     out = {f: int(getattr(sums, f)) for f, _ in _Sums._fields_}
-    out["nonsi"] = cfg.n_tokens * cfg.t_target
+    out["nonsi"] = (cfg.t_target_first or cfg.t_target) + (cfg.n_tokens - 1) * cfg.t_target
     out.update(arrs)
     if hist:
         out["si_hist"], out["seg_hist"] = si_hist, seg_hist

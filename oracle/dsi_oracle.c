@@ -92,8 +92,11 @@ static int indicator(const indicator_stream *s, int64_t p) {
 /* position N-1 may be read; the result does not depend on them (any read    */
 /* of A(p), p >= N, ends the loop whatever its value).                       */
 /* ------------------------------------------------------------------------ */
+/* TTFT variant: the first iteration's first draft costs t_d1 and its target   */
+/* forward t_t1 (each model's first forward).                          */
 static void si_literal(const indicator_stream *s, int32_t N, int32_t k, int64_t t_t, int64_t t_d,
-                       int32_t *iters_out, int64_t *cost_out, int64_t *si_hist) {
+                       int64_t t_t1, int64_t t_d1, int32_t *iters_out, int64_t *cost_out,
+                       int64_t *si_hist) {
   int64_t total_toks = 0;
   int64_t total_cost = 0;
   int32_t iters = 0;
@@ -102,7 +105,10 @@ static void si_literal(const indicator_stream *s, int32_t N, int32_t k, int64_t 
     int64_t start = total_toks;
     while (n < k && indicator(s, total_toks + n + 1) == 1) n += 1;
     total_toks += n + 1;
-    total_cost += (int64_t)k * t_d + t_t;
+    if (iters == 0)
+      total_cost += t_d1 + (int64_t)(k - 1) * t_d + t_t1;
+    else
+      total_cost += (int64_t)k * t_d + t_t;
     iters += 1;
     /* unbiased accepted-drafts histogram: only iterations whose whole k-draft
        window lies in positions 1..N-1 (north_star's SI pin) */
@@ -214,10 +220,36 @@ static int fifo_push(fifo *q, int64_t b) {
   return 0;
 }
 
+/* TTFT variant: in the first segment the drafter's first draft takes t_d1  */
+/* (draft c+j is done at t_d1 + (j-1) t_d) and thread 0 -- the target pool's */
+/* first-ever forward -- takes t_t1; everything later costs the TPOTs.       */
+typedef struct {
+  unsigned char *v;
+  size_t cap;
+} flagset;
+
+static int flags_set(flagset *f, int64_t i) { /* 0 on success */
+  if ((size_t)i >= f->cap) {
+    size_t nc = f->cap ? 2 * f->cap : 64;
+    unsigned char *nv;
+    while (nc <= (size_t)i) nc *= 2;
+    nv = (unsigned char *)realloc(f->v, nc);
+    if (!nv) return -1;
+    memset(nv + f->cap, 0, nc - f->cap);
+    f->v = nv;
+    f->cap = nc;
+  }
+  f->v[i] = 1;
+  return 0;
+}
+
+static int flag_get(const flagset *f, int64_t i) { return (size_t)i < f->cap && f->v[i]; }
+
 static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_t SP, int64_t t_t,
-                         int64_t t_d, oracle_trial_out *out) {
+                         int64_t t_d, int64_t t_t1, int64_t t_d1, oracle_trial_out *out) {
   heap h = {0, 0, 0};
   fifo q = {0, 0, 0, 0};
+  flagset fin = {0, 0}; /* threads of the current segment that have finished */
   int64_t T = 0;   /* segment start time */
   int64_t c = 0;   /* committed tokens */
   int64_t epoch = 0;
@@ -226,13 +258,16 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
 
   for (;;) { /* one iteration per segment */
     int64_t r = c + 1;          /* next unresolved position */
-    int64_t next_done = 0;      /* threads must complete in index order */
+    int64_t next_done = 0;      /* the next thread whose tokens are settled (the verifier) */
     int32_t busy = 0;
     int64_t b;
     int restarted = 0;
     epoch += 1;
     segments += 1;
+    /* time at which the draft of position c+j is done: T + lag + j*t_d */
+    const int64_t lag = segments == 1 ? t_d1 - t_d : 0;
     q.head = q.tail = 0;        /* cancelled tasks leave the queue */
+    if (fin.v) memset(fin.v, 0, fin.cap);
 
     h.n = 0; /* cancellation: every pending thread, task and draft is dropped */
     if (heap_push(&h, (event){T, EV_REQUEST, 0, epoch})) goto done;
@@ -247,12 +282,13 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
            are done, while its first draft position c+b*k+1 is <= N-1 */
         b = e.b + 1;
         if (c + (b - 1) * (int64_t)k + 1 <= (int64_t)N - 1)
-          if (heap_push(&h, (event){T + b * (int64_t)k * t_d, EV_REQUEST, b, epoch})) goto done;
+          if (heap_push(&h, (event){T + lag + b * (int64_t)k * t_d, EV_REQUEST, b, epoch})) goto done;
         if (busy < SP) {
           busy += 1;
           forwards += 1;
           if (busy > peak_busy) peak_busy = busy;
-          if (heap_push(&h, (event){e.time + t_t, EV_TARGET_DONE, e.b, epoch})) goto done;
+          const int64_t service = (segments == 1 && e.b == 0) ? t_t1 : t_t;
+          if (heap_push(&h, (event){e.time + service, EV_TARGET_DONE, e.b, epoch})) goto done;
         } else {
           if (fifo_push(&q, e.b)) goto done;
           if ((int32_t)(q.tail - q.head) > max_queue) max_queue = (int32_t)(q.tail - q.head);
@@ -267,25 +303,31 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
           if (busy > peak_busy) peak_busy = busy;
           if (heap_push(&h, (event){e.time + t_t, EV_TARGET_DONE, nb, epoch})) goto done;
         }
-        if (e.b != next_done) goto done; /* assertion: completion in index order */
-        next_done += 1;
-        hi = (e.b == 0) ? c + 1 : c + e.b * (int64_t)k + 1;
-        for (p = r; p <= hi; p++) {
-          if (p == N) { /* the N-th token is committed: L_DSI */
-            out->dsi = e.time;
-            rc = 0;
-            goto done;
+        /* Positions are settled in order.  A thread that finishes before an
+           earlier one (possible only when the first forward is slower, TTFT)
+           waits: its tokens are read when the verifier reaches it (Alg. 1
+           lines 133-134, "if C has already finished, go back"). */
+        if (flags_set(&fin, e.b)) goto done;
+        while (!restarted && flag_get(&fin, next_done)) {
+          const int64_t bb = next_done++;
+          hi = (bb == 0) ? c + 1 : c + bb * (int64_t)k + 1;
+          for (p = r; p <= hi; p++) {
+            if (p == N) { /* the N-th token is committed: L_DSI */
+              out->dsi = e.time;
+              rc = 0;
+              goto done;
+            }
+            /* assertion: the draft of position p exists by now (t_d <= t_t, t_d1 <= t_t1) */
+            if (T + lag + (p - c) * t_d > e.time) goto done;
+            if (indicator(s, p) == 0) { /* rejection: restart from the target's token */
+              T = e.time;
+              c = p;
+              restarted = 1;
+              break;
+            }
           }
-          /* assertion: the draft of position p exists by now (t_d <= t_t) */
-          if (T + (p - c) * t_d > e.time) goto done;
-          if (indicator(s, p) == 0) { /* rejection: restart from the target's token */
-            T = e.time;
-            c = p;
-            restarted = 1;
-            break;
-          }
+          if (!restarted) r = hi + 1;
         }
-        if (!restarted) r = hi + 1;
       }
     }
   }
@@ -296,6 +338,7 @@ done:
   out->dsi_forwards = forwards;
   free(h.v);
   free(q.v);
+  free(fin.v);
   return rc;
 }
 
@@ -303,6 +346,12 @@ static int valid(const oracle_config *cfg) {
   if (!cfg) return 0;
   if (cfg->n_tokens < 1 || cfg->lookahead < 1 || cfg->sp_degree < 1) return 0;
   if (cfg->t_drafter < 1 || cfg->t_target < cfg->t_drafter) return 0; /* Assumption 2 */
+  if (cfg->t_target_first < 0 || cfg->t_drafter_first < 0) return 0;
+  {
+    const int64_t tt1 = cfg->t_target_first ? cfg->t_target_first : cfg->t_target;
+    const int64_t td1 = cfg->t_drafter_first ? cfg->t_drafter_first : cfg->t_drafter;
+    if (td1 > tt1) return 0; /* Assumption 2 for the first forwards */
+  }
   if (!(cfg->accept_rate >= 0.0 && cfg->accept_rate <= 1.0)) return 0;
   return 1;
 }
@@ -336,10 +385,15 @@ int oracle_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pa
   }
   if (seg_hist) seg_hist[(N - last_zero) < 63 ? (N - last_zero) : 63] += 1;
 
-  out->nonsi = (int64_t)N * cfg->t_target; /* P:537 */
-  si_literal(&s, N, cfg->lookahead, cfg->t_target, cfg->t_drafter, &out->iters, &out->si, si_hist);
-  if (dsi_event_sim(&s, N, cfg->lookahead, cfg->sp_degree, cfg->t_target, cfg->t_drafter, out))
-    return -1;
+  {
+    const int64_t tt1 = cfg->t_target_first ? cfg->t_target_first : cfg->t_target;
+    const int64_t td1 = cfg->t_drafter_first ? cfg->t_drafter_first : cfg->t_drafter;
+    out->nonsi = tt1 + (int64_t)(N - 1) * cfg->t_target; /* P:537; TTFT first */
+    si_literal(&s, N, cfg->lookahead, cfg->t_target, cfg->t_drafter, tt1, td1, &out->iters, &out->si,
+               si_hist);
+    if (dsi_event_sim(&s, N, cfg->lookahead, cfg->sp_degree, cfg->t_target, cfg->t_drafter, tt1, td1, out))
+      return -1;
+  }
   if (out->dsi_segments != out->m) return -1;
   return 0;
 }

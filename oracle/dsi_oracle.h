@@ -35,6 +35,11 @@ typedef struct {
   int32_t  sp_degree;    /* SP >= 1 target servers                              */
   int32_t  n_tokens;     /* N >= 1                                              */
   uint32_t stream_id;    /* Philox counter word 3                               */
+  /* TTFT variant: the first forward of each model costs
+     its time-to-first-token -- the drafter's first draft and the target pool's
+     first-ever forward (thread 0 of the first segment); 0 = same as the TPOT. */
+  int64_t  t_target_first;
+  int64_t  t_drafter_first;
 } oracle_config;
 
 typedef struct {

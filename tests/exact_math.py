@@ -113,6 +113,45 @@ def expectations_grid_f64(N, t_t, t_ds, ks, sp, ps):
     return e_si, e_dsi
 
 
+def first_segment_costs(N, k, t_d, t_t, sp, t_t1, t_d1):
+    """TTFT variant: cost C1(g) of a FIRST segment of length g, by a plain FIFO
+    multi-server schedule written independently of the oracle: thread 0 (the target's
+    first forward) is requested at 0 and serves t_t1; thread b >= 1 is requested when
+    its k drafts are done, at t_d1 + (b k - 1) t_d, and serves t_t; positions settle in
+    order, so the segment ends at max(f_0..f_b(g)), b(g) = ceil((g-1)/k)."""
+    import heapq
+    B = -(-(N - 1) // k) if N > 1 else 0
+    free = [0] * sp
+    heapq.heapify(free)
+    f = []
+    for b in range(B + 1):
+        r = 0 if b == 0 else t_d1 + (b * k - 1) * t_d
+        start = max(r, heapq.heappop(free))
+        end = start + (t_t1 if b == 0 else t_t)
+        heapq.heappush(free, end)
+        f.append(end)
+    out = {}
+    for g in range(1, N + 1):
+        b = -(-(g - 1) // k)
+        out[g] = max(f[: b + 1])
+    return out
+
+
+def expectations_ttft(N, k, t_d, t_t, sp, a, t_t1, t_d1):
+    """Exact E[L_DSI], E[L_SI], L_non with first-forward costs: later segments keep C(g);
+    the first segment (length g with probability a^(g-1)(1-a), or a^(N-1) for g = N)
+    costs C1(g); SI's first iteration pays (t_d1 - t_d) + (t_t1 - t_t) more."""
+    a = Fraction(a)
+    base = expectations(N, k, t_d, t_t, sp, a)
+    c1 = first_segment_costs(N, k, t_d, t_t, sp, t_t1, t_d1)
+    extra = Fraction(0)
+    for g in range(1, N + 1):
+        pg = a ** (N - 1) if g == N else a ** (g - 1) * (1 - a)
+        extra += pg * (c1[g] - C(g, k, t_d, t_t, sp))
+    return {"dsi": base["dsi"] + extra, "si": base["si"] + (t_d1 - t_d) + (t_t1 - t_t),
+            "nonsi": Fraction(t_t1 + (N - 1) * t_t), "iters": base["iters"]}
+
+
 def si_tokens_per_iteration(a, k):
     """E[n+1] = (1 - a^(k+1)) / (1 - a): truncated geometric."""
     a = Fraction(a)
