@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define DSI_ABI_VERSION 1u
+#define DSI_ABI_VERSION 2u
 
 typedef enum {
   DSI_OK = 0,
@@ -73,7 +73,7 @@ typedef enum {
                                  draw identical indicators (the RNG contract): generate each
                                  trial's stream once per group and evaluate every config of the
                                  group on it.  Results are bit-identical to the default mode.
-                                 Not with PER_TRIAL, HIST or PATTERN; N <= 4096.             */
+                                 Not with PER_TRIAL, HIST or PATTERN; N <= 4096; no TTFT.    */
 
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {
@@ -85,7 +85,12 @@ typedef struct {
   int32_t n_tokens;   /* N in [1, 32768]: tokens to generate                               */
   uint32_t stream_id; /* Philox counter word 3; equal ids => common random numbers         */
   uint64_t n_trials;  /* T in [1, 2^32]                                                    */
-} dsi_config;         /* 48 bytes */
+  double ttft_target; /* TTFT variant: the target pool's first-ever forward
+                         (thread 0 of the first segment; non-SI's and SI's first target
+                         forward) costs this; 0 = same as t_target                         */
+  double ttft_drafter;/* the drafter's first forward costs this; 0 = same as t_drafter;
+                         ttft_drafter <= ttft_target (Assumption 2 for first forwards)     */
+} dsi_config;         /* 64 bytes */
 
 typedef struct {
   uint32_t abi_version;   /* must equal DSI_ABI_VERSION                                     */

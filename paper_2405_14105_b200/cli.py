@@ -36,14 +36,20 @@ def cmd_plan(a) -> dict:
 
 def cmd_simulate(a) -> dict:
     cfg = np.zeros(1, D.CONFIG_DTYPE)
-    cfg[0] = (a.t_target, a.t_drafter, a.accept, a.lookahead, a.sp, a.n_tokens, a.stream, a.trials)
+    cfg[0] = (a.t_target, a.t_drafter, a.accept, a.lookahead, a.sp, a.n_tokens, a.stream, a.trials,
+              a.ttft_target, a.ttft_drafter)
     with D.Simulator(cfg, tick=a.tick, seed=a.seed) as sim:
         r = sim.run().reduce()[0]
     return {k: (float(r[k]) if r.dtype[k].kind == "f" else int(r[k])) for k in r.dtype.names}
 
 
-def table2(trials: int, sp: int, n_tokens: int, seed: int = W.SEED, device: int = 0) -> list:
-    cfgs, tick = W.cfg2(trials=trials, sp=sp, n_tokens=n_tokens)
+def table2(trials: int, sp: int, n_tokens: int, seed: int = W.SEED, device: int = 0,
+           prefill: bool = False) -> list:
+    """prefill: first forwards cost TTFT = Table-3 ratio x TPOT (P:273 'including prefilling')."""
+    if prefill:
+        cfgs, tick = W.cfg2_ttft(trials=trials, sp=sp, n_tokens=n_tokens)
+    else:
+        cfgs, tick = W.cfg2(trials=trials, sp=sp, n_tokens=n_tokens)
     with D.Simulator(cfgs, tick=tick, seed=seed, device=device) as sim:
         res = sim.run().reduce()
     cells = D.dsi_heatmap(cfgs, res)
@@ -56,7 +62,7 @@ def table2(trials: int, sp: int, n_tokens: int, seed: int = W.SEED, device: int 
 
 
 def cmd_table2(a) -> list:
-    return table2(a.trials, a.sp, a.n_tokens, a.seed)
+    return table2(a.trials, a.sp, a.n_tokens, a.seed, prefill=a.prefill)
 
 
 def cmd_heatmap(a) -> dict:
@@ -92,10 +98,14 @@ def main(argv=None) -> int:
     p.add_argument("--trials", type=int, default=100_000)
     p.add_argument("--tick", type=float, default=0.01)
     p.add_argument("--stream", type=int, default=0)
+    p.add_argument("--ttft-target", type=float, default=0.0, help="first target forward (0 = TPOT)")
+    p.add_argument("--ttft-drafter", type=float, default=0.0, help="first drafter forward (0 = TPOT)")
     p = sub.add_parser("table2", help="Table 2 pairs offline, lookahead in {1, 5, 10}")
     p.add_argument("--trials", type=int, default=100_000)
     p.add_argument("--sp", type=int, default=8)
     p.add_argument("--n-tokens", type=int, default=100)
+    p.add_argument("--prefill", action="store_true",
+                   help="TTFT = Table-3 ratio x TPOT for each model's first forward (use --trials <= 1e4)")
     p = sub.add_parser("heatmap", help="Fig. 3 grid; optional CSV")
     p.add_argument("--trials", type=int, default=10_000)
     p.add_argument("--k-max", type=int, default=200)

@@ -12,9 +12,12 @@ enum : uint32_t {
   MODE_ALL_ACCEPT = 1,  // thr == 2^32: every draft accepted, no random numbers needed
   MODE_ALL_REJECT = 2,  // thr == 0: every draft rejected, no random numbers needed
 };
-enum : uint32_t { CFG_NOQUEUE = 1u << 8 };  // S(b) = b*k*t_d (Eq. 1 holds or SP >= N)
+enum : uint32_t {
+  CFG_NOQUEUE = 1u << 8,  // S(b) = b*k*t_d (Eq. 1 holds or SP >= N)
+  CFG_TTFT = 1u << 9,     // first forwards cost TTFT: first-segment correction table
+};
 
-// One configuration in ticks, as the kernel reads it (64 bytes).
+// One configuration in ticks, as the kernel reads it (96 bytes).
 struct alignas(16) DevCfg {
   uint32_t thr;        // floor(a * 2^32) when mode == MODE_STREAM
   uint32_t flags;      // mode (low byte) | CFG_NOQUEUE
@@ -34,8 +37,12 @@ struct alignas(16) DevCfg {
   int32_t s1;            // S(1): DSI cost of any segment with 2 <= g <= k+1 beyond t_t
   uint64_t rec_off;      // first per-trial record of this config (DSI_F_PER_TRIAL)
   uint64_t n_trials;
+  int32_t nonsi;         // t_t1 + (N-1) t_t: non-SI latency (first forward TTFT)
+  int32_t e_si;          // (t_d1 - t_d) + (t_t1 - t_t): SI's first-iteration surcharge
+  int32_t t_t1;          // the target's first-forward latency (TTFT variant), ticks
+  int32_t ttft_shift;    // t_d1 - t_d: first-segment drafts are late by this (TTFT variant)
 };
-static_assert(sizeof(DevCfg) == 80, "DevCfg layout");
+static_assert(sizeof(DevCfg) == 96, "DevCfg layout");
 
 // Per-config integer moments accumulated by the kernel (u64 each).
 enum Field : int {
@@ -67,6 +74,7 @@ struct LaunchParams {
   unsigned long long *si_hist;   // sum over configs of (k_eff + 1)
   int32_t max_n;                 // largest N over all configs (shared-memory sizing)
   int32_t max_keff;              // largest min(k, N) over all configs
+  int32_t any_ttft;              // some config uses the TTFT variant (first-segment tables)
   Keys keys;
 };
 
@@ -101,7 +109,7 @@ size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream);
 
 // Dynamic shared memory of the variant chosen for (max_n, max_keff, hist).
-size_t trial_kernel_smem(int max_n, int max_keff, bool hist);
+size_t trial_kernel_smem(int max_n, int max_keff, bool hist, bool ttft);
 
 // Launch the trial kernel variant for (per_trial, hist, pattern) on `stream`
 // over units [p.unit_begin, p.unit_begin + n_units).  Returns a cudaError_t.

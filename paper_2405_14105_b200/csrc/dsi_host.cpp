@@ -79,6 +79,7 @@ NcclApi &nccl() {
 // ----------------------------------------------------------------------------- helpers
 struct CfgTicks {
   int64_t t_t, t_d, kd;
+  int64_t t_t1, t_d1;  // first-forward latencies (TTFT variant; equal to t_t, t_d when off)
   uint64_t thr;
   int32_t k, sp, n;
   uint32_t stream_id;
@@ -144,6 +145,7 @@ struct dsi_sim {
   uint32_t tile_trials = 0;
   int block_threads = kDefaultThreads;
   int32_t max_n = 1, max_keff = 1;
+  bool any_ttft = false;
   uint64_t si_bins_total = 0;
   bool shared = false;                    // DSI_F_SHARED_STREAMS
   std::vector<uint32_t> perm;
@@ -208,9 +210,25 @@ dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTic
   s = to_ticks(c.t_drafter, opt.tick, &o.t_d);
   if (s != DSI_OK) return bad(s, "t_drafter is not a positive whole number of ticks");
   if (o.t_d > o.t_t) return bad(DSI_E_RANGE, "t_drafter > t_target violates Assumption 2 (P:187-189)");
-  // every per-trial latency is <= N (k t_d + t_t) (kernel overflow bound)
+  o.t_t1 = o.t_t;
+  o.t_d1 = o.t_d;
+  if (c.ttft_target != 0.0) {
+    s = to_ticks(c.ttft_target, opt.tick, &o.t_t1);
+    if (s != DSI_OK) return bad(s, "ttft_target is not 0 or a positive whole number of ticks");
+  }
+  if (c.ttft_drafter != 0.0) {
+    s = to_ticks(c.ttft_drafter, opt.tick, &o.t_d1);
+    if (s != DSI_OK) return bad(s, "ttft_drafter is not 0 or a positive whole number of ticks");
+  }
+  if (o.t_d1 > o.t_t1) return bad(DSI_E_RANGE, "ttft_drafter > ttft_target violates Assumption 2");
+  if ((opt.flags & DSI_F_SHARED_STREAMS) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d))
+    return bad(DSI_E_RANGE, "DSI_F_SHARED_STREAMS does not support the TTFT variant");
+  // every per-trial latency is <= N (k t_d + t_t) plus the first-forward surcharges
+  // (kernel overflow bound)
   const unsigned __int128 kd = (unsigned __int128)c.lookahead * (uint64_t)o.t_d;
-  const unsigned __int128 bound = (unsigned __int128)c.n_tokens * (kd + (uint64_t)o.t_t);
+  const unsigned __int128 bound = (unsigned __int128)c.n_tokens * (kd + (uint64_t)o.t_t) +
+                                  (uint64_t)std::max<int64_t>(0, o.t_t1 - o.t_t) +
+                                  (uint64_t)std::max<int64_t>(0, o.t_d1 - o.t_d);
   if (bound >= ((unsigned __int128)1 << 31))
     return bad(DSI_E_OVERFLOW, "N*(k*t_drafter + t_target) must stay below 2^31 ticks");
   if ((unsigned __int128)c.n_trials * bound * bound >= ((unsigned __int128)1 << 64))
@@ -239,7 +257,12 @@ DevCfg make_dev_cfg(const CfgTicks &t, bool pattern) {
   const int32_t sp_eff = std::min(t.sp, t.n);
   const bool noqueue = (t.t_t <= (int64_t)sp_eff * t.kd) || sp_eff >= t.n;
   d.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
-  d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u);
+  const bool ttft = t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+  d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u) | (ttft ? dsi::CFG_TTFT : 0u);
+  d.nonsi = (int32_t)(t.t_t1 + (int64_t)(t.n - 1) * t.t_t);
+  d.e_si = (int32_t)((t.t_d1 - t.t_d) + (t.t_t1 - t.t_t));
+  d.t_t1 = (int32_t)t.t_t1;
+  d.ttft_shift = (int32_t)(t.t_d1 - t.t_d);
   d.n_tokens = t.n;
   d.k_eff = k_eff;
   d.sp_eff = sp_eff;
@@ -604,7 +627,13 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   h->si_bins_total = sib;
   for (size_t i = 0; i < n_cfg; ++i) h->max_n = std::max(h->max_n, h->ticks[i].n);
   h->max_keff = (int32_t)max_keff;
-  if (dsi::trial_kernel_smem(h->max_n, h->max_keff, opt->flags & DSI_F_HIST) > 200 * 1024) {
+  for (size_t i = 0; i < n_cfg; ++i)
+    h->any_ttft = h->any_ttft || h->ticks[i].t_t1 != h->ticks[i].t_t || h->ticks[i].t_d1 != h->ticks[i].t_d;
+  if (h->any_ttft && h->max_n > 4096) {
+    h->err = "the TTFT variant supports n_tokens <= 4096";
+    return abort_create(DSI_E_RANGE);
+  }
+  if (dsi::trial_kernel_smem(h->max_n, h->max_keff, opt->flags & DSI_F_HIST, h->any_ttft) > 200 * 1024) {
     h->err = "DSI_F_HIST needs (64 + k + 1) * 4 bytes of shared memory <= 200 KiB";
     return abort_create(DSI_E_RANGE);
   }
@@ -851,6 +880,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     p.si_hist = d.d_si;
     p.max_n = h->max_n;
     p.max_keff = h->max_keff;
+    p.any_ttft = h->any_ttft ? 1 : 0;
     const uint32_t s_lo = (uint32_t)h->opt.seed, s_hi = (uint32_t)(h->opt.seed >> 32);
     for (int r = 0; r < 10; ++r) {
       p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;
@@ -953,13 +983,16 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
     dsi_result &r = out[i];
     const uint64_t T = t.trials;
     const uint64_t si_cost = (uint64_t)(t.kd + t.t_t);
+    // L_SI = I (k t_d + t_t) + e, e = SI's first-iteration surcharge (TTFT variant, else 0)
+    const __int128 e = (__int128)(t.t_d1 - t.t_d) + (__int128)(t.t_t1 - t.t_t);
     r.trials = T;
     r.t_target_ticks = t.t_t;
     r.t_drafter_ticks = t.t_d;
-    r.nonsi_ticks = (int64_t)t.n * t.t_t;
+    r.nonsi_ticks = t.t_t1 + (int64_t)(t.n - 1) * t.t_t;
     r.sum_si_iters = (int64_t)a[dsi::F_I];
-    r.sum_si_ticks = (int64_t)(si_cost * a[dsi::F_I]);
-    r.sumsq_si_ticks = si_cost * si_cost * a[dsi::F_I2];
+    r.sum_si_ticks = (int64_t)((__int128)si_cost * a[dsi::F_I] + (__int128)T * e);
+    r.sumsq_si_ticks = (uint64_t)((__int128)si_cost * si_cost * a[dsi::F_I2] +
+                                  2 * (__int128)si_cost * e * a[dsi::F_I] + (__int128)T * e * e);
     r.sum_dsi_ticks = (int64_t)a[dsi::F_DSI];
     r.sumsq_dsi_ticks = a[dsi::F_DSI2];
     r.sum_segments = (int64_t)a[dsi::F_M];
@@ -1082,6 +1115,6 @@ void dsi_sim_destroy(dsi_sim *h) {
 
 }  // extern "C"
 
-static_assert(sizeof(dsi_config) == 48, "dsi_config ABI layout");
+static_assert(sizeof(dsi_config) == 64, "dsi_config ABI layout");
 static_assert(sizeof(dsi_result) == 160, "dsi_result ABI layout");
 static_assert(sizeof(dsi_options) == 64, "dsi_options ABI layout");

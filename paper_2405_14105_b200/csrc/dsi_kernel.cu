@@ -149,17 +149,62 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   }
   if (HIST)
     for (int i = threadIdx.x; i < 64 + cfg.k_eff + 1; i += blockDim.x) sh_seg[i] = 0u;
-  if (TABLE || HIST) __syncthreads();
+  // TTFT variant: first-segment correction D1[g] = C1(g) - C(g) (R23).  Thread 0
+  // runs the FIFO schedule of the first segment in O(B): thread 0 (the target's first
+  // forward, t_t1) holds one server; threads b >= 1 arrive at t_d1 + (b k - 1) t_d with
+  // service t_t and take the earliest free server -- a never-used one (free at 0), thread
+  // 0's server (free at t_t1) or the one of the earliest earlier thread still holding one
+  // (finish times of threads b >= 1 are nondecreasing, so they form a FIFO queue: F[h]).
+  const bool ttft = (cfg.flags & CFG_TTFT) != 0;
+  int *F = reinterpret_cast<int *>(smem + (HIST ? (size_t)(64 + P.max_keff + 1) * 4
+                                                : t_table_bytes(N) + u_table_bytes(N)));
+  int *D1 = F + (N + 2);
+  if (ttft) {
+    if (TABLE || HIST) __syncthreads();
+    if (threadIdx.x == 0) {
+      const int B = N > 1 ? (N - 2) / cfg.k_eff + 1 : 0;  // ceil((N-1)/k)
+      int zero_servers = cfg.sp_eff - 1, h = 1;
+      bool first_unused = true;
+      F[0] = cfg.t_t1;
+      for (int b = 1; b <= B; ++b) {
+        const int r = cfg.ttft_shift + b * cfg.kd;  // t_d1 + (b k - 1) t_d
+        int free_at;
+        if (zero_servers > 0) {
+          free_at = 0;
+          --zero_servers;
+        } else if (first_unused && (h >= b || cfg.t_t1 <= F[h])) {
+          free_at = cfg.t_t1;
+          first_unused = false;
+        } else {
+          free_at = F[h++];
+        }
+        F[b] = max(r, free_at) + cfg.t_t;
+      }
+      for (int b = 1; b <= B; ++b) F[b] = max(F[b], F[b - 1]);  // positions settle in order
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g <= N; g += blockDim.x) {
+      if (g == 0) {
+        D1[0] = 0;
+        continue;
+      }
+      const uint32_t b = magic_div((uint32_t)g + s.k_eff - 2u, s.m_k_lo, s.m_k_hi);  // ceil((g-1)/k)
+      const int S = (int)seg_extra(g, s).y;  // S(b) of the closed form (0 for g = 1)
+      D1[g] = F[b] - (cfg.t_t + (g >= 2 ? S : 0));
+    }
+  }
+  if (TABLE || HIST || ttft) __syncthreads();
 
   unsigned long long a_m = 0, a_i = 0, a_i2 = 0, a_dsi = 0, a_dsi2 = 0, a_gtn = 0, a_gts = 0,
                      a_trials = 0;
-  const int64_t nonsi = (int64_t)N * cfg.t_t;
+  const int64_t nonsi = cfg.nonsi;  // t_t1 + (N-1) t_t
 
   for (uint64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     const uint32_t trial = (uint32_t)t;
     const TrialHalf th = philox_trial_half(trial, P.keys);
 
     int nz = 0;        // zeros (rejections) among positions 1..N-1
+    int g1 = 0;        // TTFT variant: length of the first segment (position of the first zero)
     int n2 = 0;        // segments with g >= 2 (production walk)
     int run = 0;       // accepted drafts since the last zero (production walk)
     int lastz = 0;     // HIST walk: position of the last zero (0 = sentinel before position 1)
@@ -192,6 +237,7 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
       const int rem = npos - 32 * w;
       if (rem < 32) R &= (1u << rem) - 1u;
       nz += __popc(R);
+      if (ttft && g1 == 0 && R) g1 = 32 * w + __ffs(R);
       if (HIST) {
         // test mode: walk every zero (all segments, with histograms)
         uint32_t Z = R;
@@ -233,8 +279,12 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
 
     const int m = nz + 1;
     const int iters = m + (int)ai;
-    const int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)n2 * cfg.s1 + (int64_t)ay;
-    const int64_t si = (int64_t)iters * cfg.si_cost;
+    int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)n2 * cfg.s1 + (int64_t)ay;
+    int64_t si = (int64_t)iters * cfg.si_cost;
+    if (ttft) {  // first forwards: SI's first iteration and DSI's first segment
+      dsi += D1[g1 ? g1 : N];
+      si += cfg.e_si;
+    }
     a_m += (unsigned)m;
     a_i += (unsigned)iters;
     a_i2 += (unsigned long long)iters * (unsigned long long)iters;
@@ -304,17 +354,18 @@ int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t 
 
 }  // namespace
 
-size_t trial_kernel_smem(int max_n, int max_keff, bool hist) {
-  if (hist) return (size_t)(64 + max_keff + 1) * sizeof(unsigned int);
-  if (max_n > TABLE_MAX_N) return 0;
-  return t_table_bytes(max_n) + u_table_bytes(max_n);
+size_t trial_kernel_smem(int max_n, int max_keff, bool hist, bool ttft) {
+  const size_t first = ttft ? (size_t)2 * (max_n + 2) * sizeof(int) : 0;  // F and D1
+  if (hist) return (size_t)(64 + max_keff + 1) * sizeof(unsigned int) + first;
+  if (max_n > TABLE_MAX_N) return first;
+  return t_table_bytes(max_n) + u_table_bytes(max_n) + first;
 }
 
 int launch_trial_kernel(const LaunchParams &p, uint64_t n_units, int block_threads, bool per_trial,
                         bool hist, bool pattern, void *stream) {
   if (n_units == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = trial_kernel_smem(p.max_n, p.max_keff, hist);
+  const size_t smem = trial_kernel_smem(p.max_n, p.max_keff, hist, p.any_ttft != 0);
   const int code = (per_trial ? 2 : 0) | (pattern ? 1 : 0);
   if (hist) {
     // histograms occupy shared memory: segment costs come from arithmetic
@@ -334,10 +385,10 @@ int launch_trial_kernel(const LaunchParams &p, uint64_t n_units, int block_threa
     }
   }
   switch (code) {
-    case 0: return launch_variant<false, false, false, false>(p, n_units, block_threads, 0, st);
-    case 1: return launch_variant<false, false, true, false>(p, n_units, block_threads, 0, st);
-    case 2: return launch_variant<true, false, false, false>(p, n_units, block_threads, 0, st);
-    default: return launch_variant<true, false, true, false>(p, n_units, block_threads, 0, st);
+    case 0: return launch_variant<false, false, false, false>(p, n_units, block_threads, smem, st);
+    case 1: return launch_variant<false, false, true, false>(p, n_units, block_threads, smem, st);
+    case 2: return launch_variant<true, false, false, false>(p, n_units, block_threads, smem, st);
+    default: return launch_variant<true, false, true, false>(p, n_units, block_threads, smem, st);
   }
 }
 

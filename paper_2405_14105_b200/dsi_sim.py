@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_PKG, "libdsi_sim.so")
 # developer A/B runs only: load an alternative in-tree build of the same library
 LIB_PATH = os.environ.get("DSI_SIM_LIB", LIB_PATH)
 
-DSI_ABI_VERSION = 1
+DSI_ABI_VERSION = 2
 DSI_OK, DSI_E_NULL, DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW, DSI_E_STRICT_EQ1, DSI_E_DEVICE, \
     DSI_E_COMM, DSI_E_STATE, DSI_E_NOMEM = range(10)
 DSI_F_PER_TRIAL, DSI_F_HIST, DSI_F_PATTERN, DSI_F_STRICT_EQ1, DSI_F_TIMING = 0x1, 0x2, 0x4, 0x8, 0x10
@@ -26,7 +26,8 @@ DSI_F_SHARED_STREAMS = 0x20
 # Structured dtypes with the exact C layouts (numpy arrays are passed by pointer).
 CONFIG_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_rate", "<f8"),
                          ("lookahead", "<i4"), ("sp_degree", "<i4"), ("n_tokens", "<i4"),
-                         ("stream_id", "<u4"), ("n_trials", "<u8")])
+                         ("stream_id", "<u4"), ("n_trials", "<u8"), ("ttft_target", "<f8"),
+                         ("ttft_drafter", "<f8")])
 RESULT_DTYPE = np.dtype([("trials", "<u8"), ("t_target_ticks", "<i8"), ("t_drafter_ticks", "<i8"),
                          ("nonsi_ticks", "<i8"), ("sum_si_ticks", "<i8"), ("sum_dsi_ticks", "<i8"),
                          ("sumsq_si_ticks", "<u8"), ("sumsq_dsi_ticks", "<u8"),
@@ -40,7 +41,7 @@ HEATMAP_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_ra
                           ("dsi_lookahead", "<i4"), ("nonsi", "<f8"), ("si", "<f8"), ("dsi", "<f8"),
                           ("r_nonsi_si", "<f8"), ("r_si_dsi", "<f8"), ("r_nonsi_dsi", "<f8"),
                           ("r_min_dsi", "<f8"), ("first_cfg", "<u8"), ("n_cfg", "<u8")])
-assert CONFIG_DTYPE.itemsize == 48 and RESULT_DTYPE.itemsize == 160 and HEATMAP_DTYPE.itemsize == 112
+assert CONFIG_DTYPE.itemsize == 64 and RESULT_DTYPE.itemsize == 160 and HEATMAP_DTYPE.itemsize == 112
 
 
 class dsi_options(ctypes.Structure):

@@ -26,7 +26,8 @@ SEED = 2405141050
 
 CONFIG_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_rate", "<f8"),
                          ("lookahead", "<i4"), ("sp_degree", "<i4"), ("n_tokens", "<i4"),
-                         ("stream_id", "<u4"), ("n_trials", "<u8")])
+                         ("stream_id", "<u4"), ("n_trials", "<u8"), ("ttft_target", "<f8"),
+                         ("ttft_drafter", "<f8")])
 
 # Table 2: target latency ms, drafter latency ms, acceptance rate.
 TABLE2_ROWS = [
@@ -43,11 +44,21 @@ TABLE2_ROWS = [
 ]
 
 
+# Table 3: TTFT/TPOT ratios of (target, drafter) per Table-2 row; the Phi-3
+# Alpaca row has no Table-3 entry and keeps TTFT = TPOT (ratio 1).
+TABLE3_TTFT_RATIOS = [(1.35, 1.19), (1.54, 1.20), (1.0, 1.0), (1.29, 1.23), (4.77, 3.88),
+                      (1.43, 1.27), (5.36, 1.04), (1.15, 1.05), (4.53, 1.06), (1.19, 1.06)]
+
+
 def _grid(rows) -> np.ndarray:
+    """Rows (t_target, t_drafter, a, k, SP, N, stream_id, T[, ttft_target, ttft_drafter])."""
     out = np.zeros(len(rows), CONFIG_DTYPE)
     for i, r in enumerate(rows):
-        out[i] = r
+        out[i] = tuple(r) + (0.0, 0.0)[: 10 - len(r)]
     return out
+
+
+rows = _grid  # public name for tests and tools
 
 
 def cfg1(trials: int = 1000):
@@ -59,6 +70,17 @@ def cfg2(trials: int = 100_000, sp: int = 8, n_tokens: int = 100, ks=(1, 5, 10))
     """BASELINE configs[1]: Table-2 (target, drafter, task) pairs; tick 0.1 ms."""
     rows = [(tt, td, a, k, sp, n_tokens, 0, trials) for _, tt, td, a in TABLE2_ROWS for k in ks]
     return _grid(rows), 0.1
+
+
+def cfg2_ttft(trials: int = 10_000, sp: int = 7, n_tokens: int = 50, ks=(1, 5, 10)):
+    """The Table-2 protocol with prefill (50 tokens, "including prefilling", up to 8
+    GPUs -> SP 7, k in {1,5,10}): first forwards cost TTFT = Table-3 ratio x TPOT (SURVEY
+    8(f) N2).  tick 0.001 ms makes every ratio x TPOT a whole number of ticks."""
+    rows = []
+    for (_, tt, td, a), (rt, rd) in zip(TABLE2_ROWS, TABLE3_TTFT_RATIOS):
+        for k in ks:
+            rows.append((tt, td, a, k, sp, n_tokens, 0, trials, rt * tt, rd * td))
+    return _grid(rows), 0.001
 
 
 def heatmap_axes():
@@ -131,5 +153,5 @@ def fuzz(n: int, seed: int = 5, n_max: int = 60, trials: int = 64):
         if i % 17 == 0:
             k = N + int(rng.integers(1, 5))  # lookahead beyond N
         out[i] = (float(t_t), float(t_d), a, k, int(rng.integers(1, 9)), N,
-                  int(rng.integers(0, 4)), trials)
+                  int(rng.integers(0, 4)), trials, 0.0, 0.0)
     return out, 1.0

@@ -123,6 +123,22 @@ def test_create_option_errors():
     assert e.value.status == D.DSI_E_RANGE
 
 
+def test_ttft_validation():
+    cfgs = _one(ttft_target=1.5, ttft_drafter=2.0)  # drafter's first forward slower than target's
+    with pytest.raises(D.DsiError) as e:
+        _create(cfgs)
+    assert e.value.status == D.DSI_E_RANGE
+    with pytest.raises(D.DsiError) as e:
+        _create(_one(ttft_target=1.505))
+    assert e.value.status == D.DSI_E_TICK
+    with pytest.raises(D.DsiError) as e:
+        _create(_one(ttft_target=2.0), flags=D.DSI_F_SHARED_STREAMS)
+    assert e.value.status == D.DSI_E_RANGE
+    with pytest.raises(D.DsiError) as e:
+        _create(_one(ttft_target=2.0, n_tokens=5000))
+    assert e.value.status == D.DSI_E_RANGE
+
+
 def test_strict_eq1_and_pattern_limits():
     cfgs = _one(sp_degree=1)  # ceil(100 / (5*10)) = 2 > 1
     with pytest.raises(D.DsiError) as e:

@@ -75,9 +75,7 @@ def test_fuzz_long_runs_bit_exact():
         t_d = int(rng.integers(1, t_t + 1))
         rows.append((float(t_t), float(t_d), float(rng.uniform(0.85, 0.999)), int(rng.integers(1, 41)),
                      int(rng.integers(1, 9)), int(rng.integers(33, 301)), int(rng.integers(0, 3)), 200))
-    cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
-    for i, r in enumerate(rows):
-        cfgs[i] = r
+    cfgs = W.rows(rows)
     sim, res = run_sim(cfgs, 1.0)
     check_against_oracle(sim, res, cfgs, 1.0, ctx="longruns")
     sim.close()
@@ -103,9 +101,7 @@ def test_long_sequences_bit_exact():
     """N up to 1000 (config 5) and N = 4097 (an odd tail of the last Philox word)."""
     rows = [(1.0, 0.05, 0.9, 3, 7, 1000, 0, 257), (1.0, 0.3, 0.5, 2, 3, 4097, 1, 65),
             (1.0, 1.0, 0.97, 1, 1, 1000, 2, 130)]
-    cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
-    for i, r in enumerate(rows):
-        cfgs[i] = r
+    cfgs = W.rows(rows)
     sim, res = run_sim(cfgs, 0.01)
     check_against_oracle(sim, res, cfgs, 0.01, ctx="long")
     sim.close()
@@ -117,9 +113,7 @@ def test_pattern_mode_enumerates_every_pattern(N):
     each bit-exact against the oracle, and the weighted sum equals the exact h(g) form."""
     rows = [(100.0, 30.0, 0.5, 2, 2, N, 0, 1 << (N - 1)), (100.0, 7.0, 0.5, 4, 3, N, 0, 1 << (N - 1)),
             (100.0, 30.0, 0.5, 2, 1, N, 0, 1 << (N - 1))]
-    cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
-    for i, r in enumerate(rows):
-        cfgs[i] = r
+    cfgs = W.rows(rows)
     sim, res = run_sim(cfgs, 1.0, flags=ALL | D.DSI_F_PATTERN)
     check_against_oracle(sim, res, cfgs, 1.0, pattern=True, ctx=f"pattern N={N}")
     from fractions import Fraction
@@ -169,6 +163,56 @@ def test_production_variant_matches_test_variant():
     sim_b.close()
 
 
+def ttft_fuzz(n, seed, trials):
+    rng = np.random.default_rng(seed)
+    base, _ = W.fuzz(n, seed=seed, trials=trials)
+    for r in base:
+        t_t, t_d = float(r["t_target"]), float(r["t_drafter"])
+        t_t1 = float(rng.choice([t_t, rng.integers(1, 4 * t_t + 2), rng.integers(t_t, 12 * t_t + 2)]))
+        t_d1 = float(rng.integers(1, int(min(t_t1, 5 * t_d + 3)) + 1))
+        r["ttft_target"], r["ttft_drafter"] = t_t1, t_d1
+    return base, 1.0
+
+
+@pytest.mark.parametrize("flags", [0, ALL])
+def test_ttft_fuzz_bit_exact(flags):
+    """TTFT variant (N2): first forwards cost TTFT, incl. a first target forward much slower
+    than later ones (threads finishing before thread 0) and TTFT below TPOT."""
+    cfgs, tick = ttft_fuzz(150, seed=44, trials=250)
+    sim, res = run_sim(cfgs, tick, flags=flags | D.DSI_F_PER_TRIAL)
+    check_against_oracle(sim, res, cfgs, tick, hist=bool(flags & D.DSI_F_HIST), ctx=f"ttft {flags}")
+    sim.close()
+
+
+def test_ttft_table2_protocol_bit_exact():
+    """Table 2's protocol with prefill: N = 50, SP 7, k in {1,5,10}, TTFT = Table-3
+    ratio x TPOT, tick 0.001 ms."""
+    cfgs, tick = W.cfg2_ttft(trials=1500)
+    sim, res = run_sim(cfgs, tick, flags=0)
+    check_against_oracle(sim, res, cfgs, tick, per_trial=False, hist=False, ctx="cfg2_ttft")
+    sim.close()
+
+
+def test_ttft_pattern_enumeration_exact():
+    from fractions import Fraction
+    N = 10
+    rows = [(100.0, 14.0, 0.5, 1, 2, N, 0, 1 << (N - 1), 536.0, 15.0),
+            (50.0, 7.0, 0.5, 2, 3, N, 0, 1 << (N - 1), 62.0, 9.0),
+            (30.0, 10.0, 0.5, 3, 1, N, 0, 1 << (N - 1), 300.0, 12.0)]
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 1.0, flags=D.DSI_F_PATTERN | D.DSI_F_PER_TRIAL)
+    check_against_oracle(sim, res, cfgs, 1.0, pattern=True, hist=False, ctx="ttft pattern")
+    for i, row in enumerate(cfgs):
+        tr = sim.trials(i)
+        per = lambda A: {"dsi": int(tr["dsi"][X.pattern_index(A)]), "si": int(tr["si"][X.pattern_index(A)])}
+        got = X.enumerate_expectations(N, Fraction(3, 4), per)
+        want = X.expectations_ttft(N, int(row["lookahead"]), int(row["t_drafter"]), int(row["t_target"]),
+                                   int(row["sp_degree"]), Fraction(3, 4), int(row["ttft_target"]),
+                                   int(row["ttft_drafter"]))
+        assert got["dsi"] == want["dsi"] and got["si"] == want["si"]
+    sim.close()
+
+
 MOMENTS = ("sum_dsi_ticks", "sum_si_ticks", "sumsq_dsi_ticks", "sumsq_si_ticks", "sum_segments",
            "sum_si_iters", "sum_accepts", "n_dsi_gt_nonsi", "n_dsi_gt_si", "trials", "mean_dsi", "std_dsi")
 
@@ -192,9 +236,7 @@ def test_shared_streams_bit_identical_to_default(name):
     else:  # groups with trials not a multiple of the 128-trial tile, and a = 0 / a = 1 groups
         rows = [(1.0, 0.25, a, k, sp, 77, 0, 129 + 7 * k) for a in (0.0, 0.5, 1.0) for k in (1, 3, 9)
                 for sp in (1, 7)]
-        cfgs = np.zeros(len(rows), W.CONFIG_DTYPE)
-        for i, r in enumerate(rows):
-            cfgs[i] = r
+        cfgs = W.rows(rows)
         tick = 0.01
     _, base = run_sim(cfgs, tick, flags=0)
     sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
