@@ -100,9 +100,11 @@ typedef struct {
   int32_t device;         /* first CUDA device ordinal of this process (e.g. LOCAL_RANK)    */
   int32_t n_devices;      /* 1..8 devices [device, device+n) driven by this process         */
   int32_t rank, world;    /* multi-process mode: this process is rank of world (world >= 1) */
-  const uint8_t *nccl_id; /* 128-byte ncclUniqueId shared by all ranks when the total device
-                             count world*n_devices > 1; NULL otherwise.  Obtain it with
-                             dsi_nccl_unique_id on one rank and broadcast it.              */
+  const uint8_t *nccl_id; /* 128-byte ncclUniqueId shared by all ranks; required when the
+                             total device count world*n_devices > 1.  With one device, a
+                             non-NULL id still routes the reduction through a one-rank NCCL
+                             communicator.  Obtain it with dsi_nccl_unique_id on one rank
+                             and broadcast it.                                              */
   int32_t n_shards;       /* 0 or 1: normal.  > 1 (test only, single device): split the work
                              into n_shards cost-balanced shards run back to back on one
                              device, exercising the same partition code as multi-GPU.     */

@@ -148,6 +148,7 @@ struct dsi_sim {
   bool any_ttft = false;
   uint64_t si_bins_total = 0;
   bool shared = false;                    // DSI_F_SHARED_STREAMS
+  bool use_nccl = false;                  // per-config moments summed with ncclAllReduce
   std::vector<uint32_t> perm;
   std::vector<dsi::CrnGroup> groups;
   std::vector<dsi::CrnUnit> crn_units;
@@ -579,6 +580,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   const int total_devices = opt->world * opt->n_devices;
   if (total_devices > 1 && !opt->nccl_id)
     return fail(nullptr, DSI_E_NULL, "nccl_id is required when world*n_devices > 1");
+  // NCCL whenever several devices take part, or when the caller passes an id for a
+  // one-rank communicator (exercises the collective path on one GPU)
+  const bool use_nccl = total_devices > 1 || opt->nccl_id != nullptr;
   const bool per_trial = opt->flags & DSI_F_PER_TRIAL;
   if (per_trial && total_devices > 1)
     return fail(nullptr, DSI_E_RANGE, "DSI_F_PER_TRIAL needs a single device and world == 1");
@@ -597,6 +601,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   h->opt.nccl_id = nullptr;
   h->n_cfg = n_cfg;
   h->shared = shared;
+  h->use_nccl = use_nccl;
   h->block_threads = shared ? kCrnThreads : (opt->block_threads ? opt->block_threads : kDefaultThreads);
   try {
     h->ticks.resize(n_cfg);
@@ -742,11 +747,11 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     if (e == cudaSuccess) e = cudaMalloc(&d.d_prefix, (n_cfg + 1) * sizeof(uint64_t));
 
     if (e == cudaSuccess) e = cudaMalloc(&d.d_acc, acc_bytes);
-    if (e == cudaSuccess && total_devices > 1) e = cudaMalloc(&d.d_red, acc_bytes);
+    if (e == cudaSuccess && use_nccl) e = cudaMalloc(&d.d_red, acc_bytes);
     if (e == cudaSuccess && (opt->flags & DSI_F_HIST)) {
       e = cudaMalloc(&d.d_seg, n_cfg * 64 * sizeof(unsigned long long));
       if (e == cudaSuccess) e = cudaMalloc(&d.d_si, sib * sizeof(unsigned long long));
-      if (e == cudaSuccess && total_devices > 1) {
+      if (e == cudaSuccess && use_nccl) {
         e = cudaMalloc(&d.d_seg_red, n_cfg * 64 * sizeof(unsigned long long));
         if (e == cudaSuccess) e = cudaMalloc(&d.d_si_red, sib * sizeof(unsigned long long));
       }
@@ -780,7 +785,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   }
 
   // ---- NCCL: one communicator per device over world * n_devices ranks
-  if (total_devices > 1) {
+  if (use_nccl) {
     NcclApi &api = nccl();
     if (!api.ok) {
       h->err = "libnccl.so.2 could not be loaded";
@@ -934,7 +939,7 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   const bool hist = h->opt.flags & DSI_F_HIST;
   const int total_devices = h->opt.world * h->opt.n_devices;
   const size_t nacc = n_cfg * dsi::NF;
-  if (total_devices > 1) {
+  if (h->use_nccl) {
     NcclApi &api = nccl();
     ncclResult_t r = api.GroupStart();
     for (auto &d : h->dev) {
@@ -954,13 +959,13 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   // every device now holds the global sums (or there is one device): read device 0
   DeviceState &d0 = h->dev[0];
   CUDA_TRY(h, cudaSetDevice(d0.ordinal));
-  const unsigned long long *src = total_devices > 1 ? d0.d_red : d0.d_acc;
+  const unsigned long long *src = h->use_nccl ? d0.d_red : d0.d_acc;
   CUDA_TRY(h, cudaMemcpyAsync(h->host_acc.p, src, nacc * sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, d0.stream));
   if (hist) {
-    CUDA_TRY(h, cudaMemcpyAsync(h->host_seg.p, total_devices > 1 ? d0.d_seg_red : d0.d_seg,
+    CUDA_TRY(h, cudaMemcpyAsync(h->host_seg.p, h->use_nccl ? d0.d_seg_red : d0.d_seg,
                                 n_cfg * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d0.stream));
-    CUDA_TRY(h, cudaMemcpyAsync(h->host_si.p, total_devices > 1 ? d0.d_si_red : d0.d_si,
+    CUDA_TRY(h, cudaMemcpyAsync(h->host_si.p, h->use_nccl ? d0.d_si_red : d0.d_si,
                                 h->si_bins_total * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                 d0.stream));
   }

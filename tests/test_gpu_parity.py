@@ -261,6 +261,24 @@ def test_shared_streams_options_are_validated():
         assert e.value.status == D.DSI_E_RANGE
 
 
+@pytest.mark.parametrize("flags", [0, D.DSI_F_HIST, D.DSI_F_SHARED_STREAMS])
+def test_nccl_one_rank_reduction_matches(flags):
+    """The NCCL path of dsi_sim_reduce (dlopen'ed libnccl, ncclCommInitRank, ncclAllReduce
+    of the u64 moments and histograms) on a one-rank communicator reproduces the local sums."""
+    cfgs, tick = W.fuzz(30, seed=12, trials=500)
+    _, base = run_sim(cfgs, tick, flags=flags)
+    sim, res = run_sim(cfgs, tick, flags=flags, nccl_id=D.dsi_nccl_unique_id())
+    for f in MOMENTS:
+        assert np.array_equal(res[f], base[f]), f
+    if flags & D.DSI_F_HIST:
+        base_sim, _ = run_sim(cfgs, tick, flags=flags)
+        for i in range(cfgs.size):
+            a, b = sim.hist(i), base_sim.hist(i)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        base_sim.close()
+    sim.close()
+
+
 def test_seed_and_stream_change_the_draws():
     cfgs, tick = W.cfg1(trials=500)
     _, r1 = run_sim(cfgs, tick, flags=0)
