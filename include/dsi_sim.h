@@ -73,7 +73,7 @@ typedef enum {
                                  draw identical indicators (the RNG contract): generate each
                                  trial's stream once per group and evaluate every config of the
                                  group on it.  Results are bit-identical to the default mode.
-                                 Not with PER_TRIAL, HIST or PATTERN; N <= 4096; no TTFT.    */
+                                 Not with PER_TRIAL, HIST or PATTERN; N <= 2048; no TTFT.      */
 
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {

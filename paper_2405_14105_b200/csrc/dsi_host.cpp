@@ -35,7 +35,8 @@ constexpr int kMaxTokens = 32768;  // keeps every magic division exact (x * d <=
 constexpr uint64_t kMaxTrials = 1ull << 32;
 constexpr int kDefaultThreads = 128;
 constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size (launch bounds)
-constexpr int kCrnMaxN = 4096;     // shared-stream mode: per-trial run lists in shared memory
+constexpr int kCrnMaxN = 2048;     // shared-stream mode: 128 per-trial run lists of <= N/3+2
+                                   // u16 entries fit shared memory (209 KB at N 2048)
 
 // ----------------------------------------------------------------------------- NCCL (dlopen)
 struct NcclApi {
@@ -399,6 +400,28 @@ dsi_status upload(dsi_sim *h) {
 // Shared-stream plan: group configs by (stream_id, threshold, N, n_trials) -- equal keys
 // draw identical indicators -- ordered lookahead-major inside a group (so the lanes of a
 // warp mostly share k), then cut each group into slices of cfg_per_block configs.
+// Launch-shape limits that follow from the configs (max N, max min(k, N), TTFT present),
+// and the shared-memory bounds they imply.  Called by create and again by update, whose
+// new configs may change them (the kernels size shared memory from these values).
+dsi_status derive_limits(dsi_sim *h) {
+  int32_t max_n = 1, max_keff = 1;
+  bool any_ttft = false;
+  for (const CfgTicks &t : h->ticks) {
+    max_n = std::max(max_n, t.n);
+    max_keff = std::max(max_keff, std::min(t.k, t.n));
+    any_ttft = any_ttft || t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+  }
+  if (any_ttft && max_n > 4096) return fail(h, DSI_E_RANGE, "the TTFT variant supports n_tokens <= 4096");
+  if (dsi::trial_kernel_smem(max_n, max_keff, h->opt.flags & DSI_F_HIST, any_ttft) > 200 * 1024)
+    return fail(h, DSI_E_RANGE, "DSI_F_HIST needs (64 + k + 1) * 4 bytes of shared memory <= 200 KiB");
+  if (h->shared && max_n > kCrnMaxN)
+    return fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS supports n_tokens <= " + std::to_string(kCrnMaxN));
+  h->max_n = max_n;
+  h->max_keff = max_keff;
+  h->any_ttft = any_ttft;
+  return DSI_OK;
+}
+
 dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
   const size_t n = h->n_cfg;
   try {
@@ -614,12 +637,10 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   // ---- validation and tick conversion (before any device work)
   dsi_status s = validate_all(h, cfg, n_cfg);
   if (s != DSI_OK) return abort_create(s);
-  uint64_t max_keff = 0, sib = 0;
+  uint64_t sib = 0;
   for (size_t i = 0; i < n_cfg; ++i) {
     h->total_trials += h->ticks[i].trials;
-    const uint64_t ke = (uint64_t)std::min(h->ticks[i].k, h->ticks[i].n);
-    max_keff = std::max(max_keff, ke);
-    sib += ke + 1;
+    sib += (uint64_t)std::min(h->ticks[i].k, h->ticks[i].n) + 1;
   }
   if (per_trial && h->total_trials > (1ull << 31)) {
     h->err = "DSI_F_PER_TRIAL supports at most 2^31 trials in total";
@@ -630,23 +651,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     return abort_create(DSI_E_RANGE);
   }
   h->si_bins_total = sib;
-  for (size_t i = 0; i < n_cfg; ++i) h->max_n = std::max(h->max_n, h->ticks[i].n);
-  h->max_keff = (int32_t)max_keff;
-  for (size_t i = 0; i < n_cfg; ++i)
-    h->any_ttft = h->any_ttft || h->ticks[i].t_t1 != h->ticks[i].t_t || h->ticks[i].t_d1 != h->ticks[i].t_d;
-  if (h->any_ttft && h->max_n > 4096) {
-    h->err = "the TTFT variant supports n_tokens <= 4096";
-    return abort_create(DSI_E_RANGE);
-  }
-  if (dsi::trial_kernel_smem(h->max_n, h->max_keff, opt->flags & DSI_F_HIST, h->any_ttft) > 200 * 1024) {
-    h->err = "DSI_F_HIST needs (64 + k + 1) * 4 bytes of shared memory <= 200 KiB";
-    return abort_create(DSI_E_RANGE);
-  }
-
-  if (shared && h->max_n > kCrnMaxN) {
-    h->err = "DSI_F_SHARED_STREAMS supports n_tokens <= 4096";
-    return abort_create(DSI_E_RANGE);
-  }
+  s = derive_limits(h);
+  if (s != DSI_OK) return abort_create(s);
 
   // ---- work units: (config, tile of tile_trials trials), or shared-stream (group, config slice)
   std::vector<double> crn_cost;
@@ -831,9 +837,39 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
       }
     }
   }
-  if (s != DSI_OK) {
+  const int32_t old_n = h->max_n, old_keff = h->max_keff, old_cpb = h->cfg_per_block, old_runs = h->max_runs;
+  const bool old_ttft = h->any_ttft;
+  std::vector<uint32_t> old_perm;
+  std::vector<dsi::CrnGroup> old_groups;
+  std::vector<dsi::CrnUnit> old_units;
+  if (s == DSI_OK) s = derive_limits(h);  // the new configs may need a larger launch shape
+  if (s == DSI_OK && h->shared) {
+    // re-plan on the host first: the unit table's size is fixed at create
+    try {
+      old_perm = h->perm;
+      old_groups = h->groups;
+      old_units = h->crn_units;
+      std::vector<double> cost;
+      s = plan_shared(h, cost);
+    } catch (...) {
+      s = fail(h, DSI_E_NOMEM, "host tables");
+    }
+    if (s == DSI_OK && (h->groups.size() != old_groups.size() || h->crn_units.size() != old_units.size()))
+      s = fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS: the stream grouping changed; create a new handle");
+    if (s != DSI_OK && !old_groups.empty()) {
+      h->perm.swap(old_perm);
+      h->groups.swap(old_groups);
+      h->crn_units.swap(old_units);
+      h->cfg_per_block = old_cpb;
+      h->max_runs = old_runs;
+    }
+  }
+  if (s != DSI_OK) {  // the handle keeps its previous configs
     const std::string msg = h->err;
     h->ticks.swap(old);
+    h->max_n = old_n;
+    h->max_keff = old_keff;
+    h->any_ttft = old_ttft;
     h->err = msg;
     return s;
   }
@@ -843,14 +879,6 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     CUDA_TRY(h, cudaStreamSynchronize(d.stream));
   }
   fill_dev_cfg(h);
-  if (h->shared) {
-    const size_t ng = h->groups.size(), nu = h->crn_units.size();
-    std::vector<double> cost;
-    s = plan_shared(h, cost);
-    if (s == DSI_OK && (h->groups.size() != ng || h->crn_units.size() != nu))
-      s = fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS: the stream grouping changed; create a new handle");
-    if (s != DSI_OK) return s;
-  }
   h->ran = h->reduced = false;
   return upload(h);
 }

@@ -93,7 +93,7 @@ __device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint
 __host__ __device__ __forceinline__ size_t t_table_bytes(int n) { return (size_t)((n + 2) & ~1) * 8; }
 __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t)((n - 1 + 3) / 4 + 1) * 16; }
 
-template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE>
+template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, bool TTFT>
 __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
 
@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   // service t_t and take the earliest free server -- a never-used one (free at 0), thread
   // 0's server (free at t_t1) or the one of the earliest earlier thread still holding one
   // (finish times of threads b >= 1 are nondecreasing, so they form a FIFO queue: F[h]).
-  const bool ttft = (cfg.flags & CFG_TTFT) != 0;
+  // (a template parameter: launches without a TTFT config compile the variant out)
+  const bool ttft = TTFT && (cfg.flags & CFG_TTFT) != 0;
   int *F = reinterpret_cast<int *>(smem + (HIST ? (size_t)(64 + P.max_keff + 1) * 4
                                                 : t_table_bytes(N) + u_table_bytes(N)));
   int *D1 = F + (N + 2);
@@ -332,10 +333,10 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   }
 }
 
-template <bool A, bool B, bool C, bool D>
-int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
+template <bool A, bool B, bool C, bool D, bool E>
+int launch_variant_t(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(dsi_trial_kernel<A, B, C, D>,
+    const cudaError_t e = cudaFuncSetAttribute(dsi_trial_kernel<A, B, C, D, E>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
@@ -344,12 +345,18 @@ int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t 
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_trial_kernel<A, B, C, D><<<(unsigned)n, threads, smem, st>>>(q);
+    dsi_trial_kernel<A, B, C, D, E><<<(unsigned)n, threads, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
   }
   return 0;
+}
+
+template <bool A, bool B, bool C, bool D>
+int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
+  return p.any_ttft ? launch_variant_t<A, B, C, D, true>(p, n_units, threads, smem, st)
+                    : launch_variant_t<A, B, C, D, false>(p, n_units, threads, smem, st);
 }
 
 }  // namespace

@@ -139,6 +139,12 @@ def test_ttft_validation():
     assert e.value.status == D.DSI_E_RANGE
 
 
+def test_shared_streams_n_limit():
+    with pytest.raises(D.DsiError) as e:  # 128 run lists of N/3 + 2 u16 must fit shared memory
+        _create(_one(n_tokens=2049), flags=D.DSI_F_SHARED_STREAMS)
+    assert e.value.status == D.DSI_E_RANGE
+
+
 def test_strict_eq1_and_pattern_limits():
     cfgs = _one(sp_degree=1)  # ceil(100 / (5*10)) = 2 > 1
     with pytest.raises(D.DsiError) as e:

@@ -369,3 +369,83 @@ def test_api_state_errors():
     assert e.value.status == D.DSI_E_STATE
     sim.reduce()
     sim.close()
+
+
+def _changed(cfgs, dn=0, ttft=False):
+    """Same trials per config; new acceptance, lookahead, N + dn (and TTFT).  a -> 1 - a and
+    N -> N + dn are one-to-one, so the shared-stream grouping keeps its shape."""
+    new = cfgs.copy()
+    new["accept_rate"] = 1.0 - cfgs["accept_rate"]
+    new["lookahead"] = cfgs["lookahead"] % 7 + 1
+    new["n_tokens"] = cfgs["n_tokens"] + dn
+    if ttft:
+        new["ttft_target"] = new["t_target"] * 3
+        new["ttft_drafter"] = new["t_drafter"] * 2
+    return new
+
+
+@pytest.mark.parametrize("flags,dn,ttft", [(0, 300, True), (ALL, 30, True), (0, 5000, False),
+                                           (D.DSI_F_SHARED_STREAMS, 900, False)])
+def test_update_matches_a_fresh_handle(flags, dn, ttft):
+    """dsi_sim_update may grow N past the create-time maximum (shared-memory tables are
+    sized per launch) and switch the TTFT variant on; results equal a fresh handle's."""
+    cfgs, tick = W.fuzz(40, seed=77, trials=300)
+    if flags & D.DSI_F_HIST:  # HIST fixes min(k, N) per config
+        cfgs["lookahead"] = cfgs["lookahead"] % 7 + 1
+        cfgs["n_tokens"] = np.maximum(cfgs["n_tokens"], 8)
+    new = _changed(cfgs, dn, ttft)
+    if flags & D.DSI_F_HIST:
+        new["lookahead"] = cfgs["lookahead"]
+    sim, _ = run_sim(cfgs, tick, flags=flags)
+    sim.update(new).run()
+    got = sim.reduce()
+    _, want = run_sim(new, tick, flags=flags)
+    for f in MOMENTS:
+        assert np.array_equal(got[f], want[f]), f
+    if flags & D.DSI_F_PER_TRIAL:
+        for i in range(0, new.size, 9):
+            assert_result_equals_oracle(got[i], oracle_sums(new[i], tick, SEED), tick, ctx=f"upd {i}")
+    sim.close()
+
+
+def test_failed_update_keeps_previous_configs():
+    cfgs, tick = W.fuzz(20, seed=3, trials=200)
+    sim, before = run_sim(cfgs, tick, flags=0)
+    bad = cfgs.copy()
+    bad["accept_rate"][4] = 1.5
+    with pytest.raises(D.DsiError) as e:
+        sim.update(bad)
+    assert e.value.status == D.DSI_E_RANGE
+    after = sim.run().reduce()
+    for f in MOMENTS:
+        assert np.array_equal(after[f], before[f]), f
+    sim.close()
+    # shared streams: an update that changes the grouping is refused, the plan kept
+    sim, before = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    regroup = cfgs.copy()
+    regroup["stream_id"], regroup["accept_rate"], regroup["n_tokens"] = 0, 0.5, 50  # one group
+    with pytest.raises(D.DsiError) as e:
+        sim.update(regroup)
+    assert e.value.status == D.DSI_E_RANGE
+    after = sim.run().reduce()
+    for f in MOMENTS:
+        assert np.array_equal(after[f], before[f]), f
+    # growing N past the shared-stream limit is refused too
+    big = cfgs.copy()
+    big["n_tokens"] = 2049
+    with pytest.raises(D.DsiError) as e:
+        sim.update(big)
+    assert e.value.status == D.DSI_E_RANGE
+    sim.close()
+
+
+def test_shared_streams_at_max_n():
+    """N = 2048 (the shared-stream limit: 128 run lists of N/3 + 2 entries in shared memory)."""
+    rows = [(1.0, td, a, k, 7, 2048, 0, 256) for td in (0.05, 0.5) for a in (0.5, 0.9, 0.99)
+            for k in (1, 4, 30)]
+    cfgs, tick = W.rows(rows), 0.01
+    _, base = run_sim(cfgs, tick, flags=0)
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    for f in MOMENTS:
+        assert np.array_equal(res[f], base[f]), f
+    sim.close()
