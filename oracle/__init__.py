@@ -46,7 +46,8 @@ class _Config(ctypes.Structure):
                 ("accept_rate", ctypes.c_double), ("lookahead", ctypes.c_int32),
                 ("sp_degree", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
                 ("stream_id", ctypes.c_uint32), ("t_target_first", ctypes.c_int64),
-                ("t_drafter_first", ctypes.c_int64)]
+                ("t_drafter_first", ctypes.c_int64), ("fresh_verifier", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class _TrialOut(ctypes.Structure):
@@ -98,11 +99,13 @@ class Config:
     stream_id: int = 0
     t_target_first: int = 0   # TTFT variant: 0 = same as t_target
     t_drafter_first: int = 0  # TTFT variant: 0 = same as t_drafter
+    fresh_verifier: bool = False  # N4 variant (R24)
 
     def _c(self) -> _Config:
         return _Config(int(self.t_target), int(self.t_drafter), float(self.accept_rate),
                        int(self.lookahead), int(self.sp_degree), int(self.n_tokens),
-                       int(self.stream_id), int(self.t_target_first), int(self.t_drafter_first))
+                       int(self.stream_id), int(self.t_target_first), int(self.t_drafter_first),
+                       int(bool(self.fresh_verifier)), 0)
 
 
 def ticks(x: float, tick: float) -> int:

@@ -140,7 +140,10 @@ static void si_literal(const indicator_stream *s, int32_t N, int32_t k, int64_t 
 /* Events at equal times: server release (TARGET_DONE) before claims         */
 /* (REQUEST); R8.                                                   */
 /* ------------------------------------------------------------------------ */
-enum { EV_TARGET_DONE = 0, EV_REQUEST = 1 };
+/* Fresh-verifier variant only: EV_FRESH_DONE completes a fresh forward (a     */
+/* completion, like EV_TARGET_DONE) and EV_CHECK -- the decision whether to   */
+/* start one -- runs after every other event of its time stamp.               */
+enum { EV_TARGET_DONE = 0, EV_FRESH_DONE = 1, EV_REQUEST = 2, EV_CHECK = 3 };
 
 typedef struct {
   int64_t time;
@@ -245,14 +248,52 @@ static int flags_set(flagset *f, int64_t i) { /* 0 on success */
 
 static int flag_get(const flagset *f, int64_t i) { return (size_t)i < f->cap && f->v[i]; }
 
+/* Fresh-verifier variant: completion time of each started thread of the segment */
+/* (0 = not started).                                                           */
+typedef struct {
+  int64_t *v;
+  size_t cap;
+} timeset;
+
+static int time_set(timeset *f, int64_t i, int64_t t) { /* 0 on success */
+  if ((size_t)i >= f->cap) {
+    size_t nc = f->cap ? 2 * f->cap : 64;
+    int64_t *nv;
+    while (nc <= (size_t)i) nc *= 2;
+    nv = (int64_t *)realloc(f->v, nc * sizeof(int64_t));
+    if (!nv) return -1;
+    memset(nv + f->cap, 0, (nc - f->cap) * sizeof(int64_t));
+    f->v = nv;
+    f->cap = nc;
+  }
+  f->v[i] = t;
+  return 0;
+}
+
+static int64_t time_get(const timeset *f, int64_t i) { return (size_t)i < f->cap ? f->v[i] : 0; }
+
+/* Fresh-verifier variant (R24).  Thm 2's proof     */
+/* (P:445): when the verifier accepts and commits x_{k+1}, "DSI either invokes */
+/* a new current verifier thread or labels an existing thread as the current  */
+/* verifier".  Read as: each time the committed prefix grows to position p at */
+/* time tau (after every other event at tau), unless a started target thread */
+/* covering p+1 completes by tau + t_t, a fresh target forward starts at tau  */
+/* on one extra server (outside the SP pool): its prefix is the committed     */
+/* tokens plus the drafts done by tau, at most k of them (the lookahead,      */
+/* P:143), so it yields the target's tokens for p+1 .. min(d, p+k)+1 (d = the */
+/* last draft done by tau) at tau + t_t.  A newer fresh forward supersedes an */
+/* older one (which no longer covers p+1); a rejection cancels it like every  */
+/* other thread.                                                              */
 static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_t SP, int64_t t_t,
-                         int64_t t_d, int64_t t_t1, int64_t t_d1, oracle_trial_out *out) {
+                         int64_t t_d, int64_t t_t1, int64_t t_d1, int fresh, oracle_trial_out *out) {
   heap h = {0, 0, 0};
   fifo q = {0, 0, 0, 0};
   flagset fin = {0, 0}; /* threads of the current segment that have finished */
+  timeset ends = {0, 0}; /* fresh variant: completion time of started threads */
   int64_t T = 0;   /* segment start time */
   int64_t c = 0;   /* committed tokens */
   int64_t epoch = 0;
+  int64_t fresh_id = 0;
   int32_t segments = 0, peak_busy = 0, max_queue = 0, forwards = 0;
   int rc = -1;
 
@@ -262,21 +303,27 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
     int32_t busy = 0;
     int64_t b;
     int restarted = 0;
+    /* fresh variant: the live fresh forward covers [f_lo, f_hi], completes at f_end */
+    int f_live = 0, f_done = 0;
+    int64_t f_lo = 0, f_hi = 0, f_end = 0;
     epoch += 1;
     segments += 1;
     /* time at which the draft of position c+j is done: T + lag + j*t_d */
     const int64_t lag = segments == 1 ? t_d1 - t_d : 0;
     q.head = q.tail = 0;        /* cancelled tasks leave the queue */
     if (fin.v) memset(fin.v, 0, fin.cap);
+    if (ends.v) memset(ends.v, 0, ends.cap * sizeof(int64_t));
 
     h.n = 0; /* cancellation: every pending thread, task and draft is dropped */
     if (heap_push(&h, (event){T, EV_REQUEST, 0, epoch})) goto done;
 
     while (!restarted) {
       event e;
+      int64_t r_before;
       if (h.n == 0) goto done; /* cannot happen: position N is always settled */
       e = heap_pop(&h);
       if (e.epoch != epoch) continue; /* cancelled thread / task */
+      r_before = r;
       if (e.cls == EV_REQUEST) {
         /* the drafter keeps drafting: task b+1 is requested once its k drafts
            are done, while its first draft position c+b*k+1 is <= N-1 */
@@ -289,12 +336,34 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
           if (busy > peak_busy) peak_busy = busy;
           const int64_t service = (segments == 1 && e.b == 0) ? t_t1 : t_t;
           if (heap_push(&h, (event){e.time + service, EV_TARGET_DONE, e.b, epoch})) goto done;
+          if (fresh && time_set(&ends, e.b, e.time + service)) goto done;
         } else {
           if (fifo_push(&q, e.b)) goto done;
           if ((int32_t)(q.tail - q.head) > max_queue) max_queue = (int32_t)(q.tail - q.head);
         }
+        continue;
+      }
+      if (e.cls == EV_CHECK) { /* fresh variant: start a fresh forward for position r? */
+        int64_t j = r - c, bb, d;
+        if (e.b != r) continue; /* the prefix has grown since: a later check decides */
+        bb = (j == 1) ? 0 : (j - 1 + k - 1) / k; /* the regular thread covering r */
+        if (time_get(&ends, bb) && time_get(&ends, bb) <= e.time + t_t) continue;
+        if (f_live && !f_done && f_lo <= r && r <= f_hi && f_end <= e.time + t_t) continue;
+        d = c + (e.time - T) / t_d; /* the last draft done by now */
+        f_live = 1;
+        f_done = 0;
+        f_lo = r;
+        f_hi = (d < r - 1 + k ? d : r - 1 + k) + 1;
+        f_end = e.time + t_t;
+        fresh_id += 1;
+        forwards += 1;
+        if (heap_push(&h, (event){f_end, EV_FRESH_DONE, fresh_id, epoch})) goto done;
+        continue;
+      }
+      if (e.cls == EV_FRESH_DONE) {
+        if (e.b != fresh_id) continue; /* superseded */
+        f_done = 1;
       } else { /* EV_TARGET_DONE */
-        int64_t hi, p;
         busy -= 1;
         if (q.head < q.tail) { /* FIFO: the head of the queue starts now */
           int64_t nb = q.v[q.head++];
@@ -302,12 +371,16 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
           forwards += 1;
           if (busy > peak_busy) peak_busy = busy;
           if (heap_push(&h, (event){e.time + t_t, EV_TARGET_DONE, nb, epoch})) goto done;
+          if (fresh && time_set(&ends, nb, e.time + t_t)) goto done;
         }
+        if (flags_set(&fin, e.b)) goto done;
+      }
+      if (!fresh) {
+        int64_t hi, p;
         /* Positions are settled in order.  A thread that finishes before an
            earlier one (possible only when the first forward is slower, TTFT)
            waits: its tokens are read when the verifier reaches it (Alg. 1
            lines 133-134, "if C has already finished, go back"). */
-        if (flags_set(&fin, e.b)) goto done;
         while (!restarted && flag_get(&fin, next_done)) {
           const int64_t bb = next_done++;
           hi = (bb == 0) ? c + 1 : c + bb * (int64_t)k + 1;
@@ -328,6 +401,30 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
           }
           if (!restarted) r = hi + 1;
         }
+      } else {
+        /* fresh variant: position r is settled once a finished thread covers it
+           (regular thread 0 covers c+1, thread b >= 1 covers c+(b-1)k+2 ..
+           c+bk+1, the fresh forward [f_lo, f_hi]); in order, as above */
+        for (;;) {
+          const int64_t j = r - c;
+          const int64_t bb = (j == 1) ? 0 : (j - 1 + k - 1) / k;
+          if (!flag_get(&fin, bb) && !(f_live && f_done && f_lo <= r && r <= f_hi)) break;
+          if (r == N) {
+            out->dsi = e.time;
+            rc = 0;
+            goto done;
+          }
+          if (T + (r - c) * t_d > e.time) goto done; /* the draft exists (t_d <= t_t) */
+          if (indicator(s, r) == 0) {
+            T = e.time;
+            c = r;
+            restarted = 1;
+            break;
+          }
+          r += 1;
+        }
+        if (!restarted && r != r_before)
+          if (heap_push(&h, (event){e.time, EV_CHECK, r, epoch})) goto done;
       }
     }
   }
@@ -339,6 +436,7 @@ done:
   free(h.v);
   free(q.v);
   free(fin.v);
+  free(ends.v);
   return rc;
 }
 
@@ -351,6 +449,7 @@ static int valid(const oracle_config *cfg) {
     const int64_t tt1 = cfg->t_target_first ? cfg->t_target_first : cfg->t_target;
     const int64_t td1 = cfg->t_drafter_first ? cfg->t_drafter_first : cfg->t_drafter;
     if (td1 > tt1) return 0; /* Assumption 2 for the first forwards */
+    if (cfg->fresh_verifier && (tt1 != cfg->t_target || td1 != cfg->t_drafter)) return 0;
   }
   if (!(cfg->accept_rate >= 0.0 && cfg->accept_rate <= 1.0)) return 0;
   return 1;
@@ -391,7 +490,8 @@ int oracle_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pa
     out->nonsi = tt1 + (int64_t)(N - 1) * cfg->t_target; /* P:537; TTFT first */
     si_literal(&s, N, cfg->lookahead, cfg->t_target, cfg->t_drafter, tt1, td1, &out->iters, &out->si,
                si_hist);
-    if (dsi_event_sim(&s, N, cfg->lookahead, cfg->sp_degree, cfg->t_target, cfg->t_drafter, tt1, td1, out))
+    if (dsi_event_sim(&s, N, cfg->lookahead, cfg->sp_degree, cfg->t_target, cfg->t_drafter, tt1, td1,
+                      cfg->fresh_verifier != 0, out))
       return -1;
   }
   if (out->dsi_segments != out->m) return -1;

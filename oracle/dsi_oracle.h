@@ -40,6 +40,11 @@ typedef struct {
      first-ever forward (thread 0 of the first segment); 0 = same as the TPOT. */
   int64_t  t_target_first;
   int64_t  t_drafter_first;
+  /* Fresh-verifier variant (R24; Thm 2's proof P:445:
+     "DSI either invokes a new current verifier thread or labels an existing thread
+     as the current verifier"): non-zero enables it.  Not with the TTFT variant. */
+  int32_t  fresh_verifier;
+  int32_t  reserved;     /* 0 */
 } oracle_config;
 
 typedef struct {

@@ -158,3 +158,33 @@ def si_tokens_per_iteration(a, k):
     if a == 1:
         return Fraction(k + 1)
     return (1 - a ** (k + 1)) / (1 - a)
+
+
+def C_fresh(g, k, t_d, t_t, sp):
+    """Fresh-verifier variant (R24), derived by hand from the
+    reading, not from the oracle.  If k t_d <= t_t a fresh forward never finishes sooner
+    than the regular thread (S(b+1) - S(b) <= max(k t_d, t_t) = t_t), so C_fresh = C.
+    Otherwise no task ever queues (requests are k t_d > t_t apart) and thread b ends at
+    F_b = b k t_d + t_t; inside block b (offsets j = 1..k after position (b-1)k + 1,
+    reached at F_{b-1}) fresh forward i >= 0 starts at F_{b-1} + i t_t while
+    (i+1) t_t < k t_d and settles offsets up to floor((i+1) t_t / t_d), so offset j
+    settles at F_{b-1} + min(k t_d, t_t ceil(j t_d / t_t))."""
+    kd = k * t_d
+    if g == 1 or kd <= t_t:
+        return C(g, k, t_d, t_t, sp)
+    b = -(-(g - 1) // k)
+    j = g - 1 - (b - 1) * k
+    return t_t + (b - 1) * kd + min(kd, t_t * (-(-(j * t_d) // t_t)))
+
+
+def closed_form_fresh(A, N, k, t_d, t_t, sp):
+    out = closed_form(A, N, k, t_d, t_t, sp)
+    out["dsi"] = sum(C_fresh(g, k, t_d, t_t, sp) for g in segments(A, N))
+    return out
+
+
+def expectations_fresh(N, k, t_d, t_t, sp, a):
+    a = Fraction(a)
+    out = expectations(N, k, t_d, t_t, sp, a)
+    out["dsi"] = sum(h(g, N, a) * C_fresh(g, k, t_d, t_t, sp) for g in range(1, N + 1))
+    return out
