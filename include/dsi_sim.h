@@ -74,6 +74,15 @@ typedef enum {
                                  trial's stream once per group and evaluate every config of the
                                  group on it.  Results are bit-identical to the default mode.
                                  Not with PER_TRIAL, HIST or PATTERN; N <= 2048; no TTFT.      */
+#define DSI_F_FRESH_VERIFIER 0x40u /* fresh-verifier DSI variant (R24; Thm 2's proof
+                                 P:445, "DSI either invokes a new current verifier thread or
+                                 labels an existing thread"): whenever the committed prefix
+                                 grows to p at time tau and no started target thread settles
+                                 p+1 by tau + t_t, a fresh target forward starts at tau on an
+                                 extra server, on the committed prefix plus the drafts done by
+                                 tau (at most k).  Identical to the default when k t_d <= t_t;
+                                 otherwise L_DSI <= N t_t on every trial (Thm 1).
+                                 Not with SHARED_STREAMS or TTFT configs.                       */
 
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {

@@ -4,7 +4,7 @@
     python -m paper_2405_14105_b200 simulate --t-target 20.6 --t-drafter 6.8 --accept 0.93 \
         --lookahead 5 --sp 7 --n-tokens 50 --trials 100000 --tick 0.1
     python -m paper_2405_14105_b200 table2 [--trials 100000] [--sp 8] [--n-tokens 100]
-    python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200] [--csv out.csv] [--shared]
+    python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200] [--csv out.csv] [--shared|--fresh]
 
 `plan` is Eq. 1; `table2` evaluates the Table 2 (target, drafter, acceptance)
 rows offline with lookahead in {1, 5, 10}, SI over all of them and DSI over the
@@ -38,7 +38,8 @@ def cmd_simulate(a) -> dict:
     cfg = np.zeros(1, D.CONFIG_DTYPE)
     cfg[0] = (a.t_target, a.t_drafter, a.accept, a.lookahead, a.sp, a.n_tokens, a.stream, a.trials,
               a.ttft_target, a.ttft_drafter)
-    with D.Simulator(cfg, tick=a.tick, seed=a.seed) as sim:
+    flags = D.DSI_F_FRESH_VERIFIER if a.fresh else 0
+    with D.Simulator(cfg, tick=a.tick, seed=a.seed, flags=flags) as sim:
         r = sim.run().reduce()[0]
     return {k: (float(r[k]) if r.dtype[k].kind == "f" else int(r[k])) for k in r.dtype.names}
 
@@ -67,7 +68,7 @@ def cmd_table2(a) -> list:
 
 def cmd_heatmap(a) -> dict:
     cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
-    flags = D.DSI_F_SHARED_STREAMS if a.shared else 0
+    flags = (D.DSI_F_SHARED_STREAMS if a.shared else 0) | (D.DSI_F_FRESH_VERIFIER if a.fresh else 0)
     with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags) as sim:
         res = sim.run().reduce()
     cells = D.dsi_heatmap(cfgs, res)
@@ -100,6 +101,7 @@ def main(argv=None) -> int:
     p.add_argument("--stream", type=int, default=0)
     p.add_argument("--ttft-target", type=float, default=0.0, help="first target forward (0 = TPOT)")
     p.add_argument("--ttft-drafter", type=float, default=0.0, help="first drafter forward (0 = TPOT)")
+    p.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER (DESIGN.md R24)")
     p = sub.add_parser("table2", help="Table 2 pairs offline, lookahead in {1, 5, 10}")
     p.add_argument("--trials", type=int, default=100_000)
     p.add_argument("--sp", type=int, default=8)
@@ -113,6 +115,7 @@ def main(argv=None) -> int:
     p.add_argument("--n-tokens", type=int, default=100)
     p.add_argument("--csv", default=None)
     p.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
+    p.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER (DESIGN.md R24)")
     a = ap.parse_args(argv)
     try:
         out = {"plan": cmd_plan, "simulate": cmd_simulate, "table2": cmd_table2, "heatmap": cmd_heatmap}[a.cmd](a)

@@ -113,6 +113,18 @@ __device__ __forceinline__ uint2 seg_long(int g, const SegCtx &s) {
   return make_uint2(e.x, e.y - (uint32_t)s.s1);
 }
 
+// Fresh-verifier variant (R24) with k t_d > t_t, where no task ever queues
+// (S(b) = b k t_d): a segment of length g >= 2 ends at offset j = g-1-(b-1)k of block
+// b = ceil((g-1)/k), which the chain of fresh forwards started at F_{b-1}, F_{b-1} + t_t,
+// ... settles at F_{b-1} + min(k t_d, t_t ceil(j t_d / t_t)) instead of F_b = F_{b-1} + k t_d.
+// Returns the saving k t_d - min(k t_d, t_t ceil(j t_d / t_t)) (< 2^31: j t_d <= k t_d).
+__device__ __forceinline__ uint32_t fresh_saving(int g, const SegCtx &s, int t_d) {
+  const uint32_t b = magic_div((uint32_t)g + s.k_eff - 2u, s.m_k_lo, s.m_k_hi);  // ceil((g-1)/k)
+  const int j = g - 1 - ((int)b - 1) * (int)s.k_eff;
+  const int v = s.t_t * ((j * t_d + s.t_t - 1) / s.t_t);
+  return (uint32_t)max(0, s.kd - v);
+}
+
 // Bits i of x such that bits i-n+1 .. i are all ones (runs of at least n ones),
 // by log-doubling: y_s marks runs >= s, then y_s & (y_s << (n - s)) for s <= n < 2s.
 __device__ __forceinline__ uint32_t runs_at_least(uint32_t x, int n) {

@@ -15,9 +15,10 @@ enum : uint32_t {
 enum : uint32_t {
   CFG_NOQUEUE = 1u << 8,  // S(b) = b*k*t_d (Eq. 1 holds or SP >= N)
   CFG_TTFT = 1u << 9,     // first forwards cost TTFT: first-segment correction table
+  CFG_FRESH = 1u << 10,   // fresh-verifier variant and k t_d > t_t (else it equals the default)
 };
 
-// One configuration in ticks, as the kernel reads it (96 bytes).
+// One configuration in ticks, as the kernel reads it (112 bytes).
 struct alignas(16) DevCfg {
   uint32_t thr;        // floor(a * 2^32) when mode == MODE_STREAM
   uint32_t flags;      // mode (low byte) | CFG_NOQUEUE
@@ -41,8 +42,10 @@ struct alignas(16) DevCfg {
   int32_t e_si;          // (t_d1 - t_d) + (t_t1 - t_t): SI's first-iteration surcharge
   int32_t t_t1;          // the target's first-forward latency (TTFT variant), ticks
   int32_t ttft_shift;    // t_d1 - t_d: first-segment drafts are late by this (TTFT variant)
+  int32_t t_d;           // drafter latency, ticks (fresh-verifier variant)
+  int32_t reserved[3];
 };
-static_assert(sizeof(DevCfg) == 96, "DevCfg layout");
+static_assert(sizeof(DevCfg) == 112, "DevCfg layout");
 
 // Per-config integer moments accumulated by the kernel (u64 each).
 enum Field : int {
@@ -75,6 +78,7 @@ struct LaunchParams {
   int32_t max_n;                 // largest N over all configs (shared-memory sizing)
   int32_t max_keff;              // largest min(k, N) over all configs
   int32_t any_ttft;              // some config uses the TTFT variant (first-segment tables)
+  int32_t any_fresh;             // some config has CFG_FRESH (every segment walked)
   Keys keys;
 };
 

@@ -147,6 +147,7 @@ struct dsi_sim {
   int block_threads = kDefaultThreads;
   int32_t max_n = 1, max_keff = 1;
   bool any_ttft = false;
+  bool any_fresh = false;                 // DSI_F_FRESH_VERIFIER and some k t_d > t_t
   uint64_t si_bins_total = 0;
   bool shared = false;                    // DSI_F_SHARED_STREAMS
   bool use_nccl = false;                  // per-config moments summed with ncclAllReduce
@@ -225,6 +226,8 @@ dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTic
   if (o.t_d1 > o.t_t1) return bad(DSI_E_RANGE, "ttft_drafter > ttft_target violates Assumption 2");
   if ((opt.flags & DSI_F_SHARED_STREAMS) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d))
     return bad(DSI_E_RANGE, "DSI_F_SHARED_STREAMS does not support the TTFT variant");
+  if ((opt.flags & DSI_F_FRESH_VERIFIER) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d))
+    return bad(DSI_E_RANGE, "DSI_F_FRESH_VERIFIER does not support the TTFT variant");
   // every per-trial latency is <= N (k t_d + t_t) plus the first-forward surcharges
   // (kernel overflow bound)
   const unsigned __int128 kd = (unsigned __int128)c.lookahead * (uint64_t)o.t_d;
@@ -248,7 +251,7 @@ dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTic
   return DSI_OK;
 }
 
-DevCfg make_dev_cfg(const CfgTicks &t, bool pattern) {
+DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
   DevCfg d{};
   uint32_t mode = dsi::MODE_STREAM;
   if (!pattern) {
@@ -260,7 +263,12 @@ DevCfg make_dev_cfg(const CfgTicks &t, bool pattern) {
   const bool noqueue = (t.t_t <= (int64_t)sp_eff * t.kd) || sp_eff >= t.n;
   d.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
   const bool ttft = t.t_t1 != t.t_t || t.t_d1 != t.t_d;
-  d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u) | (ttft ? dsi::CFG_TTFT : 0u);
+  // fresh-verifier variant: with k t_d <= t_t a fresh forward never finishes sooner than
+  // the regular thread (R24), so only k t_d > t_t configs take its cost table
+  const bool fresh_cfg = fresh && t.kd > t.t_t;
+  d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u) | (ttft ? dsi::CFG_TTFT : 0u) |
+            (fresh_cfg ? dsi::CFG_FRESH : 0u);
+  d.t_d = (int32_t)t.t_d;
   d.nonsi = (int32_t)(t.t_t1 + (int64_t)(t.n - 1) * t.t_t);
   d.e_si = (int32_t)((t.t_d1 - t.t_d) + (t.t_t1 - t.t_t));
   d.t_t1 = (int32_t)t.t_t1;
@@ -333,8 +341,9 @@ dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n) {
 // Fill the pinned device-config staging table from h->ticks.
 void fill_dev_cfg(dsi_sim *h) {
   const bool pattern = h->opt.flags & DSI_F_PATTERN;
+  const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
   parallel_for(h->n_cfg, [&](size_t b, size_t e) {
-    for (size_t i = b; i < e; ++i) h->dev_cfg.p[i] = make_dev_cfg(h->ticks[i], pattern);
+    for (size_t i = b; i < e; ++i) h->dev_cfg.p[i] = make_dev_cfg(h->ticks[i], pattern, fresh);
   });
   uint64_t rec = 0, sib = 0;  // prefix offsets: per-trial records and SI-histogram bins
   for (size_t i = 0; i < h->n_cfg; ++i) {
@@ -405,11 +414,13 @@ dsi_status upload(dsi_sim *h) {
 // new configs may change them (the kernels size shared memory from these values).
 dsi_status derive_limits(dsi_sim *h) {
   int32_t max_n = 1, max_keff = 1;
-  bool any_ttft = false;
+  bool any_ttft = false, any_fresh = false;
+  const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
   for (const CfgTicks &t : h->ticks) {
     max_n = std::max(max_n, t.n);
     max_keff = std::max(max_keff, std::min(t.k, t.n));
     any_ttft = any_ttft || t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+    any_fresh = any_fresh || (fresh && t.kd > t.t_t);
   }
   if (any_ttft && max_n > 4096) return fail(h, DSI_E_RANGE, "the TTFT variant supports n_tokens <= 4096");
   if (dsi::trial_kernel_smem(max_n, max_keff, h->opt.flags & DSI_F_HIST, any_ttft) > 200 * 1024)
@@ -419,6 +430,7 @@ dsi_status derive_limits(dsi_sim *h) {
   h->max_n = max_n;
   h->max_keff = max_keff;
   h->any_ttft = any_ttft;
+  h->any_fresh = any_fresh;
   return DSI_OK;
 }
 
@@ -588,7 +600,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
   const uint32_t known = DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_STRICT_EQ1 | DSI_F_TIMING |
-                         DSI_F_SHARED_STREAMS;
+                         DSI_F_SHARED_STREAMS | DSI_F_FRESH_VERIFIER;
   if (opt->flags & ~known) return fail(nullptr, DSI_E_RANGE, "unknown flag");
   if (opt->n_devices < 1 || opt->n_devices > 8) return fail(nullptr, DSI_E_RANGE, "n_devices must be 1..8");
   if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
@@ -610,8 +622,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (per_trial && total_devices > 1)
     return fail(nullptr, DSI_E_RANGE, "DSI_F_PER_TRIAL needs a single device and world == 1");
   const bool shared = opt->flags & DSI_F_SHARED_STREAMS;
-  if (shared && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN)))
-    return fail(nullptr, DSI_E_RANGE, "DSI_F_SHARED_STREAMS excludes PER_TRIAL, HIST and PATTERN");
+  if (shared && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_FRESH_VERIFIER)))
+    return fail(nullptr, DSI_E_RANGE,
+                "DSI_F_SHARED_STREAMS excludes PER_TRIAL, HIST, PATTERN and FRESH_VERIFIER");
 
   dsi_sim *h = new (std::nothrow) dsi_sim;
   if (!h) return fail(nullptr, DSI_E_NOMEM, "handle allocation");
@@ -838,7 +851,7 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     }
   }
   const int32_t old_n = h->max_n, old_keff = h->max_keff, old_cpb = h->cfg_per_block, old_runs = h->max_runs;
-  const bool old_ttft = h->any_ttft;
+  const bool old_ttft = h->any_ttft, old_fresh = h->any_fresh;
   std::vector<uint32_t> old_perm;
   std::vector<dsi::CrnGroup> old_groups;
   std::vector<dsi::CrnUnit> old_units;
@@ -870,6 +883,7 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     h->max_n = old_n;
     h->max_keff = old_keff;
     h->any_ttft = old_ttft;
+    h->any_fresh = old_fresh;
     h->err = msg;
     return s;
   }
@@ -914,6 +928,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     p.max_n = h->max_n;
     p.max_keff = h->max_keff;
     p.any_ttft = h->any_ttft ? 1 : 0;
+    p.any_fresh = h->any_fresh ? 1 : 0;
     const uint32_t s_lo = (uint32_t)h->opt.seed, s_hi = (uint32_t)(h->opt.seed >> 32);
     for (int r = 0; r < 10; ++r) {
       p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;

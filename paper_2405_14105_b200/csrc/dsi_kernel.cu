@@ -93,7 +93,8 @@ __device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint
 __host__ __device__ __forceinline__ size_t t_table_bytes(int n) { return (size_t)((n + 2) & ~1) * 8; }
 __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t)((n - 1 + 3) / 4 + 1) * 16; }
 
-template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, bool TTFT>
+// VAR: 0 = default model, 1 = TTFT variant present, 2 = fresh-verifier variant present
+template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, int VAR>
 __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
 
@@ -136,6 +137,11 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   const int Lk = cfg.k_eff + 1;  // a run of >= k+1 accepted drafts makes a long segment
   const uint32_t nthr = 0u - cfg.thr;  // carry of u + nthr <=> u >= thr (thr >= 1 in stream mode)
   const bool stream = !PATTERN && mode == MODE_STREAM;
+  // fresh-verifier variant (k t_d > t_t): every segment's cost differs from C(g), so
+  // every zero is walked, as in the HIST walk (R24)
+  const bool fresh = VAR == 2 && (cfg.flags & CFG_FRESH) != 0;
+  const bool walk_all = HIST || fresh;
+  const int t_d = cfg.t_d;
 
   // shared memory: TABLE -> T[g] (g = 0..N) then U[q] (q < nq); HIST -> histograms
   uint2 *T = reinterpret_cast<uint2 *>(smem);
@@ -143,7 +149,18 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   unsigned int *sh_seg = reinterpret_cast<unsigned int *>(smem);
   unsigned int *sh_si = sh_seg + 64;
   if (TABLE) {
-    for (int g = threadIdx.x; g <= N; g += blockDim.x) T[g] = g >= 2 ? (HIST ? seg_extra(g, s) : seg_long(g, s)) : make_uint2(0u, 0u);
+    for (int g = threadIdx.x; g <= N; g += blockDim.x) {
+      uint2 e = make_uint2(0u, 0u);
+      if (g >= 2) {
+        if (HIST || fresh) {
+          e = seg_extra(g, s);
+          if (fresh) e.y -= fresh_saving(g, s, t_d);
+        } else {
+          e = seg_long(g, s);
+        }
+      }
+      T[g] = e;
+    }
     if (stream)
       for (int q = threadIdx.x; q < nq; q += blockDim.x) U[q] = philox_q_half((uint32_t)q, cfg.stream_id, P.keys);
   }
@@ -156,7 +173,7 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   // 0's server (free at t_t1) or the one of the earliest earlier thread still holding one
   // (finish times of threads b >= 1 are nondecreasing, so they form a FIFO queue: F[h]).
   // (a template parameter: launches without a TTFT config compile the variant out)
-  const bool ttft = TTFT && (cfg.flags & CFG_TTFT) != 0;
+  const bool ttft = VAR == 1 && (cfg.flags & CFG_TTFT) != 0;
   int *F = reinterpret_cast<int *>(smem + (HIST ? (size_t)(64 + P.max_keff + 1) * 4
                                                 : t_table_bytes(N) + u_table_bytes(N)));
   int *D1 = F + (N + 2);
@@ -239,16 +256,17 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
       if (rem < 32) R &= (1u << rem) - 1u;
       nz += __popc(R);
       if (ttft && g1 == 0 && R) g1 = 32 * w + __ffs(R);
-      if (HIST) {
-        // test mode: walk every zero (all segments, with histograms)
+      if (walk_all) {
+        // test mode (HIST) and the fresh-verifier variant: walk every zero
         uint32_t Z = R;
         while (Z) {
           const int z = base + __ffs(Z) - 1;
           Z &= Z - 1u;
           const int g = z - lastz;
-          seg_hist(g, lastz, s, sh_seg, sh_si);
+          if (HIST) seg_hist(g, lastz, s, sh_seg, sh_si);
           if (g >= 2) {
-            const uint2 e = TABLE ? T[g] : seg_extra(g, s);
+            uint2 e = TABLE ? T[g] : seg_extra(g, s);
+            if (!TABLE && VAR == 2 && fresh) e.y -= fresh_saving(g, s, t_d);
             ai += e.x;
             ay += e.y;
           }
@@ -260,11 +278,12 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
       if (HIST) cin = R >> 31;
     }
     int gl;
-    if (HIST) {
+    if (walk_all) {
       gl = N - lastz;  // the final segment ends at N
-      seg_hist(gl, lastz, s, sh_seg, sh_si);
+      if (HIST) seg_hist(gl, lastz, s, sh_seg, sh_si);
       if (gl >= 2) {
-        const uint2 e = TABLE ? T[gl] : seg_extra(gl, s);
+        uint2 e = TABLE ? T[gl] : seg_extra(gl, s);
+        if (!TABLE && VAR == 2 && fresh) e.y -= fresh_saving(gl, s, t_d);
         ai += e.x;
         ay += e.y;
       }
@@ -333,7 +352,7 @@ __global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
   }
 }
 
-template <bool A, bool B, bool C, bool D, bool E>
+template <bool A, bool B, bool C, bool D, int E>
 int launch_variant_t(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(dsi_trial_kernel<A, B, C, D, E>,
@@ -355,8 +374,9 @@ int launch_variant_t(const LaunchParams &p, uint64_t n_units, int threads, size_
 
 template <bool A, bool B, bool C, bool D>
 int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
-  return p.any_ttft ? launch_variant_t<A, B, C, D, true>(p, n_units, threads, smem, st)
-                    : launch_variant_t<A, B, C, D, false>(p, n_units, threads, smem, st);
+  if (p.any_fresh) return launch_variant_t<A, B, C, D, 2>(p, n_units, threads, smem, st);
+  if (p.any_ttft) return launch_variant_t<A, B, C, D, 1>(p, n_units, threads, smem, st);
+  return launch_variant_t<A, B, C, D, 0>(p, n_units, threads, smem, st);
 }
 
 }  // namespace

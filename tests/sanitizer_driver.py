@@ -9,8 +9,14 @@ from paper_2405_14105_b200 import dsi_sim as D  # noqa: E402
 from paper_2405_14105_b200 import workloads as W  # noqa: E402
 
 cfgs, tick = W.fuzz(12, seed=9, trials=150)
-for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST, D.DSI_F_SHARED_STREAMS):
+FRESH = D.DSI_F_FRESH_VERIFIER
+for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST, D.DSI_F_SHARED_STREAMS, FRESH,
+              FRESH | D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
     with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
+        sim.run().reduce()
+ttft, ttick = W.cfg2_ttft(trials=50)  # the TTFT variant (first-segment tables)
+for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
+    with D.Simulator(ttft[:6], tick=ttick, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
 pat, _ = W.fuzz(4, seed=2, trials=64)
 pat["n_tokens"] = 9
@@ -18,8 +24,9 @@ pat["n_trials"] = 256
 pat["lookahead"] = 3
 with D.Simulator(pat, tick=1.0, seed=W.SEED, flags=D.DSI_F_PATTERN | D.DSI_F_PER_TRIAL) as sim:
     sim.run().reduce()
-long_n, _ = W.cfg1(trials=40)
-long_n["n_tokens"] = 5000  # the arithmetic (non-table) variant
-with D.Simulator(long_n, tick=0.01, seed=W.SEED) as sim:
-    sim.run().reduce()
+# the arithmetic (non-table) variant; k t_d > t_t in the second row (fresh-verifier costs)
+long_n = W.rows([(1.0, 0.1, 0.8, 5, 2, 5000, 0, 40), (1.0, 0.1, 0.8, 20, 2, 5000, 0, 40)])
+for flags in (0, FRESH):
+    with D.Simulator(long_n, tick=0.01, seed=W.SEED, flags=flags) as sim:
+        sim.run().reduce()
 print("sanitizer driver ok")

@@ -139,6 +139,15 @@ def test_ttft_validation():
     assert e.value.status == D.DSI_E_RANGE
 
 
+def test_fresh_verifier_validation():
+    with pytest.raises(D.DsiError) as e:
+        _create(_one(ttft_target=2.0), flags=D.DSI_F_FRESH_VERIFIER)
+    assert e.value.status == D.DSI_E_RANGE
+    with pytest.raises(D.DsiError) as e:
+        _create(_one(), flags=D.DSI_F_FRESH_VERIFIER | D.DSI_F_SHARED_STREAMS)
+    assert e.value.status == D.DSI_E_RANGE
+
+
 def test_shared_streams_n_limit():
     with pytest.raises(D.DsiError) as e:  # 128 run lists of N/3 + 2 u16 must fit shared memory
         _create(_one(n_tokens=2049), flags=D.DSI_F_SHARED_STREAMS)

@@ -81,3 +81,20 @@ def test_heatmap_cli_writes_csv(tmp_path):
     assert d["cells"] == 10100
     lines = path.read_text().splitlines()
     assert len(lines) == 2 + 10100
+
+
+@pytest.mark.gpu
+def test_simulate_fresh_verifier_cli():
+    """k t_d > t_t: the default model can lose to non-SI; the fresh-verifier variant cannot
+    (Thm 1 per trial, R24)."""
+    args = ["simulate", "--t-target", "1.0", "--t-drafter", "1.0", "--accept", "0.48", "--lookahead", "20",
+            "--sp", "7", "--n-tokens", "100", "--trials", "20000"]
+    rc, out, err = run_cli(*args)
+    assert rc == 0, err
+    base = json.loads(out)
+    rc, out, err = run_cli(*args, "--fresh")
+    assert rc == 0, err
+    fresh = json.loads(out)
+    assert base["mean_dsi"] > base["mean_nonsi"]          # R5: E[non-SI]/E[DSI] = 0.18
+    assert fresh["n_dsi_gt_nonsi"] == 0 and fresh["mean_dsi"] <= fresh["mean_nonsi"]
+    assert fresh["sum_si_ticks"] == base["sum_si_ticks"]   # SI is unchanged

@@ -37,9 +37,10 @@ def run_sim(cfgs, tick, flags=ALL, **kw):
     return sim, res
 
 
-def check_against_oracle(sim, res, cfgs, tick, per_trial=True, hist=True, pattern=False, ctx=""):
+def check_against_oracle(sim, res, cfgs, tick, per_trial=True, hist=True, pattern=False, ctx="",
+                         fresh=False):
     for i, row in enumerate(cfgs):
-        want = oracle_sums(row, tick, SEED, pattern=pattern, hist=hist, per_trial=per_trial)
+        want = oracle_sums(row, tick, SEED, pattern=pattern, hist=hist, per_trial=per_trial, fresh=fresh)
         assert_result_equals_oracle(res[i], want, tick, ctx=f"{ctx} cfg {i}")
         if per_trial:
             assert_trials_equal(sim.trials(i), want, ctx=f"{ctx} cfg {i}")
@@ -449,3 +450,69 @@ def test_shared_streams_at_max_n():
     for f in MOMENTS:
         assert np.array_equal(res[f], base[f]), f
     sim.close()
+
+
+FRESH = D.DSI_F_FRESH_VERIFIER
+
+
+@pytest.mark.parametrize("flags", [0, ALL])
+def test_fresh_verifier_fuzz_bit_exact(flags):
+    """the fresh-verifier variant through the C ABI against
+    the oracle's event simulation, per trial (flags ALL) and in the production walk."""
+    cfgs, tick = W.fuzz(160, seed=41, trials=192)
+    assert np.sum(cfgs["lookahead"] * cfgs["t_drafter"] > cfgs["t_target"]) > 40
+    sim, res = run_sim(cfgs, tick, flags=flags | FRESH)
+    check_against_oracle(sim, res, cfgs, tick, per_trial=bool(flags), hist=bool(flags), ctx="fresh",
+                         fresh=True)
+    assert np.all(res["n_dsi_gt_nonsi"] == 0)  # Thm 1 per trial (P:199-201)
+    sim.close()
+
+
+def test_fresh_verifier_pattern_enumeration():
+    """Every pattern of N <= 12 against the hand-derived closed form (exact_math.C_fresh)."""
+    rows = [(10.0, 4.0, 0.5, 5, 1, 12, 0, 1 << 11), (100.0, 14.0, 0.5, 20, 7, 12, 0, 1 << 11),
+            (40.0, 30.0, 0.5, 3, 2, 11, 0, 1 << 10), (12.0, 11.0, 0.5, 2, 3, 10, 0, 1 << 9),
+            (9.0, 2.0, 0.5, 7, 1, 12, 0, 1 << 11)]
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 1.0, flags=D.DSI_F_PATTERN | D.DSI_F_PER_TRIAL | FRESH)
+    for i, r in enumerate(rows):
+        t_t, t_d, _, k, sp, N, _, T = r
+        got = sim.trials(i)
+        for idx in range(T):
+            A = [(idx >> p) & 1 for p in range(N - 1)]
+            want = X.closed_form_fresh(A, N, k, int(t_d), int(t_t), sp)
+            assert int(got["dsi"][idx]) == want["dsi"], (r, A)
+            assert int(got["si"][idx]) == want["si"], (r, A)
+    sim.close()
+
+
+def test_fresh_verifier_cfg4_sweep():
+    """Config 4 (k = 1..20 x SP 2..8, t_d = t_t/10): k > 10 is where the variant acts."""
+    cfgs, tick = W.cfg4(trials=3000)
+    _, base = run_sim(cfgs, tick, flags=0)
+    sim, res = run_sim(cfgs, tick, flags=FRESH)
+    act = cfgs["lookahead"] * cfgs["t_drafter"] > cfgs["t_target"] + 1e-12
+    for f in MOMENTS:
+        assert np.array_equal(res[f][~act], base[f][~act]), f
+    assert np.all(res["sum_dsi_ticks"][act] < base["sum_dsi_ticks"][act])
+    assert np.all(res["n_dsi_gt_nonsi"] == 0)
+    for i in np.nonzero(act)[0][::9]:
+        want = oracle_sums(cfgs[i], tick, SEED, count=3000, fresh=True)
+        assert_result_equals_oracle(res[i], want, tick, ctx=f"cfg4 fresh {i}")
+    sim.close()
+
+
+def test_fresh_verifier_long_sequences_arithmetic_path():
+    """N > 4096 (no shared-memory tables: segment costs by arithmetic)."""
+    cfgs = W.rows([(100.0, 30.0, a, k, sp, 5000, 0, 64) for a, k, sp in
+                   ((0.9, 7, 1), (0.99, 40, 3), (0.5, 4, 2))])
+    sim, res = run_sim(cfgs, 1.0, flags=FRESH | D.DSI_F_PER_TRIAL)
+    check_against_oracle(sim, res, cfgs, 1.0, hist=False, ctx="fresh N5000", fresh=True)
+    sim.close()
+
+
+def test_fresh_verifier_options():
+    cfgs, tick = W.cfg1(trials=10)
+    with pytest.raises(D.DsiError) as e:
+        D.Simulator(cfgs, tick=tick, seed=SEED, flags=FRESH | D.DSI_F_SHARED_STREAMS)
+    assert e.value.status == D.DSI_E_RANGE
