@@ -65,6 +65,33 @@ WORKLOAD_DESC = {
 }
 
 
+def heatmap_grid_times(sim, flush, steps):
+    """Wall time of run + on-device heatmap product per step (L2 flushed before each)."""
+    import torch
+    out, times = None, []
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sim.run()
+        out = sim.heatmap(out)
+        times.append(time.perf_counter() - t0)
+    return times, out
+
+
+def cells_equal(a, b) -> bool:
+    if a.size != b.size:
+        return False
+    for f in b.dtype.names:
+        x, y = a[f], b[f]
+        if x.dtype.kind == "f":
+            if not np.array_equal(x, y, equal_nan=True):
+                return False
+        elif not np.array_equal(x, y):
+            return False
+    return True
+
+
 def trial_tokens(cfgs) -> int:
     return int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"].astype(np.int64)))
 
@@ -329,22 +356,36 @@ def ours(args):
                "launches_per_step": simc.launches(), "bit_identical_to_value_run": bool(same),
                "note": "DSI_F_SHARED_STREAMS: configs with equal (stream_id, floor(a 2^32), N, T) share "
                        "one Philox pass per trial; per-config results identical to the default mode"}
+        heat_shared_s, cells_shared = heatmap_grid_times(simc, flush, args.steps)
         simc.close()
 
-    # the heatmap product over the last step's results (Fig. 3): per-cell argmin over k + panels
+    # "heatmap grid time" (BASELINE metric): run + all-reduce + on-device
+    # per-cell argmin over k + the four ratio panels + D2H of the cells, end to end on the
+    # host clock (dsi_sim_heatmap), in both modes; the cells must equal the
+    # host product (dsi_heatmap) over the default run's reduced results
+    heat_s, cells = heatmap_grid_times(sim, flush, args.steps)
+    grid_s = max_over_ranks(statistics.median(heat_s))
+    grid_shared_s = max_over_ranks(statistics.median(heat_shared_s)) if crn is not None else None
     heat = None
     if rank == 0:
         t0 = time.perf_counter()
-        cells = D.dsi_heatmap(cfgs, res)
-        heat_s = time.perf_counter() - t0
+        host_cells = D.dsi_heatmap(cfgs, res)
+        host_product_s = time.perf_counter() - t0
+        same_cells = cells_equal(cells, host_cells)
+        if crn is not None:
+            same_cells = same_cells and cells_equal(cells_shared, host_cells)
         i = int(np.nanargmax(cells["r_min_dsi"]))
-        heat = {"cells": int(cells.size), "product_s": heat_s,
-                "grid_time_s": total_ms / args.steps / 1000.0 + heat_s,
+        heat = {"cells": int(cells.size),
+                "grid_time_s": grid_s,
+                "grid_time_shared_streams_s": grid_shared_s,
+                "host_product_s": host_product_s,
+                "device_cells_equal_host_product": bool(same_cells),
                 "max_r_min_dsi": float(cells["r_min_dsi"][i]),
                 "at": {"t_drafter": float(cells["t_drafter"][i]), "accept_rate": float(cells["accept_rate"][i]),
                        "si_lookahead": int(cells["si_lookahead"][i]),
-                       "dsi_lookahead": int(cells["dsi_lookahead"][i])}}
-
+                       "dsi_lookahead": int(cells["dsi_lookahead"][i])},
+                "note": "grid time = dsi_sim_run + dsi_sim_heatmap (all-reduce, one warp per cell on "
+                        "the device, D2H of 10100 cells), host wall clock, median of the timed steps"}
     # e2e through the public API with host buffers: update (validate + pinned H2D of the
     # config table) + run + reduce (all-reduce + D2H of the moments + FP64 finalise)
     h2d, d2h = sim.io_bytes()

@@ -237,6 +237,15 @@ typedef struct {
 dsi_status dsi_heatmap(const dsi_config *cfg, const dsi_result *res, size_t n,
                        dsi_heatmap_cell *cells, size_t cap, size_t *n_cells);
 
+/* On-device form: after dsi_sim_run, sums the moments across devices and
+ * ranks (the all-reduce of dsi_sim_reduce; every rank must call it), evaluates every cell on
+ * device 0 -- one warp per cell -- and copies only the cells back (64 B each instead of
+ * 64 B per config).  Cells group consecutive configs with equal (t_target, t_drafter,
+ * accept_rate, sp_degree, n_tokens) as given to create/update; the values are bit-identical
+ * to dsi_heatmap over dsi_sim_reduce's results.  cells == NULL: *n_cells receives the
+ * count (no device work).  DSI_E_RANGE if cap is too small, DSI_E_STATE before a run. */
+dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size_t *n_cells);
+
 /* CSV of cells (SPEC S:450-458 columns; fixed formatting, %.6f; rows in input order). */
 dsi_status dsi_heatmap_csv(const dsi_heatmap_cell *cells, size_t n, const char *path);
 

@@ -52,8 +52,7 @@ def table2(trials: int, sp: int, n_tokens: int, seed: int = W.SEED, device: int 
     else:
         cfgs, tick = W.cfg2(trials=trials, sp=sp, n_tokens=n_tokens)
     with D.Simulator(cfgs, tick=tick, seed=seed, device=device) as sim:
-        res = sim.run().reduce()
-    cells = D.dsi_heatmap(cfgs, res)
+        cells = sim.run().heatmap()  # on-device argmin over k (dsi_sim_heatmap)
     rows = []
     for (name, *_), c in zip(W.TABLE2_ROWS, cells):
         rows.append({"pair": name, "si_ms": float(c["si"]), "si_lookahead": int(c["si_lookahead"]),
@@ -70,8 +69,7 @@ def cmd_heatmap(a) -> dict:
     cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
     flags = (D.DSI_F_SHARED_STREAMS if a.shared else 0) | (D.DSI_F_FRESH_VERIFIER if a.fresh else 0)
     with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags) as sim:
-        res = sim.run().reduce()
-    cells = D.dsi_heatmap(cfgs, res)
+        cells = sim.run().heatmap()
     if a.csv:
         D.dsi_heatmap_csv(cells, a.csv)
     i = int(np.nanargmax(cells["r_min_dsi"]))

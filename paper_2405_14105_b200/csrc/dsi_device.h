@@ -16,6 +16,7 @@ enum : uint32_t {
   CFG_NOQUEUE = 1u << 8,  // S(b) = b*k*t_d (Eq. 1 holds or SP >= N)
   CFG_TTFT = 1u << 9,     // first forwards cost TTFT: first-segment correction table
   CFG_FRESH = 1u << 10,   // fresh-verifier variant and k t_d > t_t (else it equals the default)
+  CFG_EQ1 = 1u << 11,     // Eq. 1 holds: ceil(t_t / (k t_d)) <= SP (heatmap DSI argmin)
 };
 
 // One configuration in ticks, as the kernel reads it (112 bytes).
@@ -43,7 +44,8 @@ struct alignas(16) DevCfg {
   int32_t t_t1;          // the target's first-forward latency (TTFT variant), ticks
   int32_t ttft_shift;    // t_d1 - t_d: first-segment drafts are late by this (TTFT variant)
   int32_t t_d;           // drafter latency, ticks (fresh-verifier variant)
-  int32_t reserved[3];
+  int32_t k;             // the lookahead as given (heatmap argmin reports it)
+  int32_t reserved[2];
 };
 static_assert(sizeof(DevCfg) == 112, "DevCfg layout");
 
@@ -109,6 +111,28 @@ struct CrnParams {
   int32_t max_n, max_nq, max_runs, cfg_per_block;
   Keys keys;
 };
+// On-device heatmap product: one warp per cell, a cell being a run of
+// consecutive configs (the lookahead grid of one (t_d, a) point).
+struct HeatCell {
+  uint64_t first;
+  uint32_t count;
+  uint32_t pad;
+};
+struct HeatOut {  // 64 bytes: the computed part of dsi_heatmap_cell
+  double nonsi, si, dsi, r_nonsi_si, r_si_dsi, r_nonsi_dsi, r_min_dsi;
+  int32_t si_k, dsi_k;  // argmin lookaheads (-1: no Eq.-1-feasible lookahead)
+};
+struct HeatParams {
+  const DevCfg *cfg;
+  const unsigned long long *acc;  // n_cfg * NF global sums
+  const HeatCell *cells;
+  uint32_t n_cells;
+  double tick;
+  HeatOut *out;
+  unsigned int *bad;  // set when a config's trial count differs from n_trials
+};
+int launch_heatmap_kernel(const HeatParams &p, void *stream);
+
 size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs);
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream);
 

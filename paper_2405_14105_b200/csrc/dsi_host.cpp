@@ -86,6 +86,7 @@ struct CfgTicks {
   uint32_t stream_id;
   uint64_t trials;
   double a;
+  double ut, ud;  // t_target, t_drafter as given (heatmap cells group on the user values)
 };
 
 // ceil(2^32 / d) split into low word and bit 32 (d >= 1).
@@ -130,6 +131,9 @@ struct DeviceState {
   uint32_t *d_perm = nullptr;            // shared-stream mode: processing order
   dsi::CrnGroup *d_groups = nullptr;     //   groups of configs sharing a stream
   dsi::CrnUnit *d_crn_units = nullptr;   //   one block per unit
+  dsi::HeatCell *d_heat_cells = nullptr; // on-device heatmap product (device 0 only)
+  dsi::HeatOut *d_heat_out = nullptr;
+  unsigned int *d_heat_bad = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<std::pair<uint64_t, uint64_t>> ranges;  // [begin, end) units, one per shard
@@ -158,6 +162,9 @@ struct dsi_sim {
   std::vector<DeviceState> dev;
   Pinned<unsigned long long> host_acc, host_seg, host_si;  // D2H targets
   bool ran = false, reduced = false;
+  std::vector<dsi::HeatCell> heat_cells;  // heatmap cells (planned on first use, reset by update)
+  bool heat_planned = false, heat_uploaded = false;
+  Pinned<dsi::HeatOut> heat_out;
   int launches = 0;
   std::string err;
 };
@@ -242,6 +249,8 @@ dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTic
   if ((opt.flags & DSI_F_STRICT_EQ1) && ceil_div(o.t_t, o.kd) > c.sp_degree)
     return bad(DSI_E_STRICT_EQ1, "Eq. 1 violated: ceil(t_t/(k t_d)) > SP");
   o.a = c.accept_rate;
+  o.ut = c.t_target;
+  o.ud = c.t_drafter;
   o.thr = (uint64_t)(c.accept_rate * 4294967296.0);  // exact: a * 2^32, then floor
   o.k = c.lookahead;
   o.sp = c.sp_degree;
@@ -269,6 +278,8 @@ DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
   d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u) | (ttft ? dsi::CFG_TTFT : 0u) |
             (fresh_cfg ? dsi::CFG_FRESH : 0u);
   d.t_d = (int32_t)t.t_d;
+  d.k = t.k;
+  if (dsi_eq1_feasible(t.t_t, t.t_d, t.k, t.sp) == 1) d.flags |= dsi::CFG_EQ1;
   d.nonsi = (int32_t)(t.t_t1 + (int64_t)(t.n - 1) * t.t_t);
   d.e_si = (int32_t)((t.t_d1 - t.t_d) + (t.t_t1 - t.t_t));
   d.t_t1 = (int32_t)t.t_t1;
@@ -371,6 +382,9 @@ void free_device(DeviceState &d) {
   cudaFree(d.d_perm);
   cudaFree(d.d_groups);
   cudaFree(d.d_crn_units);
+  cudaFree(d.d_heat_cells);
+  cudaFree(d.d_heat_out);
+  cudaFree(d.d_heat_bad);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
   if (d.own_stream && d.stream) cudaStreamDestroy(d.stream);
@@ -383,6 +397,7 @@ void free_handle(dsi_sim *h) {
   h->host_acc.release();
   h->host_seg.release();
   h->host_si.release();
+  h->heat_out.release();
   delete h;
 }
 
@@ -431,6 +446,29 @@ dsi_status derive_limits(dsi_sim *h) {
   h->max_keff = max_keff;
   h->any_ttft = any_ttft;
   h->any_fresh = any_fresh;
+  return DSI_OK;
+}
+
+// Sum the per-config moments (and, with hist, the histograms) over every device of
+// every rank: one grouped ncclAllReduce into the *_red buffers.  No-op on one device.
+dsi_status sum_across(dsi_sim *h, bool hist) {
+  if (!h->use_nccl) return DSI_OK;
+  const size_t n_cfg = h->n_cfg;
+  NcclApi &api = nccl();
+  ncclResult_t r = api.GroupStart();
+  for (auto &d : h->dev) {
+    if (r != ncclSuccess) break;
+    cudaSetDevice(d.ordinal);
+    r = api.AllReduce(d.d_acc, d.d_red, n_cfg * dsi::NF, ncclUint64, ncclSum, d.comm, d.stream);
+    if (r == ncclSuccess && hist) {
+      r = api.AllReduce(d.d_seg, d.d_seg_red, n_cfg * 64, ncclUint64, ncclSum, d.comm, d.stream);
+      if (r == ncclSuccess)
+        r = api.AllReduce(d.d_si, d.d_si_red, h->si_bins_total, ncclUint64, ncclSum, d.comm, d.stream);
+    }
+  }
+  const ncclResult_t r2 = api.GroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess)
+    return fail(h, DSI_E_COMM, std::string("ncclAllReduce: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
   return DSI_OK;
 }
 
@@ -894,6 +932,7 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   }
   fill_dev_cfg(h);
   h->ran = h->reduced = false;
+  h->heat_planned = h->heat_uploaded = false;
   return upload(h);
 }
 
@@ -980,25 +1019,9 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   if (n != n_cfg) return fail(h, DSI_E_RANGE, "n must equal n_cfg");
   if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_reduce before dsi_sim_run");
   const bool hist = h->opt.flags & DSI_F_HIST;
-  const int total_devices = h->opt.world * h->opt.n_devices;
   const size_t nacc = n_cfg * dsi::NF;
-  if (h->use_nccl) {
-    NcclApi &api = nccl();
-    ncclResult_t r = api.GroupStart();
-    for (auto &d : h->dev) {
-      if (r != ncclSuccess) break;
-      cudaSetDevice(d.ordinal);
-      r = api.AllReduce(d.d_acc, d.d_red, nacc, ncclUint64, ncclSum, d.comm, d.stream);
-      if (r == ncclSuccess && hist) {
-        r = api.AllReduce(d.d_seg, d.d_seg_red, n_cfg * 64, ncclUint64, ncclSum, d.comm, d.stream);
-        if (r == ncclSuccess)
-          r = api.AllReduce(d.d_si, d.d_si_red, h->si_bins_total, ncclUint64, ncclSum, d.comm, d.stream);
-      }
-    }
-    const ncclResult_t r2 = api.GroupEnd();
-    if (r != ncclSuccess || r2 != ncclSuccess)
-      return fail(h, DSI_E_COMM, std::string("ncclAllReduce: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
-  }
+  dsi_status st = sum_across(h, hist);
+  if (st != DSI_OK) return st;
   // every device now holds the global sums (or there is one device): read device 0
   DeviceState &d0 = h->dev[0];
   CUDA_TRY(h, cudaSetDevice(d0.ordinal));
@@ -1064,6 +1087,98 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   }
   });
   h->reduced = true;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size_t *n_cells) {
+  if (!h) return DSI_E_NULL;
+  h->err.clear();
+  if (!n_cells) return fail(h, DSI_E_NULL, "n_cells is NULL");
+  if (!h->heat_planned) {  // cells: maximal runs of equal (t_target, t_drafter, a, SP, N)
+    try {
+      h->heat_cells.clear();
+      const auto &t = h->ticks;
+      for (size_t i = 0; i < h->n_cfg;) {
+        size_t j = i + 1;
+        while (j < h->n_cfg && t[j].ut == t[i].ut && t[j].ud == t[i].ud && t[j].a == t[i].a &&
+               t[j].sp == t[i].sp && t[j].n == t[i].n)
+          ++j;
+        h->heat_cells.push_back(dsi::HeatCell{(uint64_t)i, (uint32_t)(j - i), 0u});
+        i = j;
+      }
+    } catch (...) {
+      return fail(h, DSI_E_NOMEM, "host tables");
+    }
+    h->heat_planned = true;
+    h->heat_uploaded = false;
+  }
+  const size_t nc = h->heat_cells.size();
+  *n_cells = nc;
+  if (!cells) return DSI_OK;
+  if (cap < nc) return fail(h, DSI_E_RANGE, "cap is smaller than the number of cells");
+  if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_heatmap before dsi_sim_run");
+  dsi_status st = sum_across(h, false);
+  if (st != DSI_OK) return st;
+  DeviceState &d0 = h->dev[0];
+  CUDA_TRY(h, cudaSetDevice(d0.ordinal));
+  if (!h->heat_uploaded) {
+    if (h->heat_out.n < nc) {
+      cudaFree(d0.d_heat_cells);
+      cudaFree(d0.d_heat_out);
+      d0.d_heat_cells = nullptr;
+      d0.d_heat_out = nullptr;
+      CUDA_TRY(h, cudaMalloc((void **)&d0.d_heat_cells, std::max<size_t>(1, nc) * sizeof(dsi::HeatCell)));
+      CUDA_TRY(h, cudaMalloc((void **)&d0.d_heat_out, std::max<size_t>(1, nc) * sizeof(dsi::HeatOut)));
+      CUDA_TRY(h, h->heat_out.alloc(nc));
+    }
+    if (!d0.d_heat_bad) CUDA_TRY(h, cudaMalloc((void **)&d0.d_heat_bad, sizeof(unsigned int)));
+    CUDA_TRY(h, cudaMemcpyAsync(d0.d_heat_cells, h->heat_cells.data(), nc * sizeof(dsi::HeatCell),
+                                cudaMemcpyHostToDevice, d0.stream));
+    CUDA_TRY(h, cudaStreamSynchronize(d0.stream));  // the vector is pageable
+    h->heat_uploaded = true;
+  }
+  CUDA_TRY(h, cudaMemsetAsync(d0.d_heat_bad, 0, sizeof(unsigned int), d0.stream));
+  dsi::HeatParams p{};
+  p.cfg = d0.d_cfg;
+  p.acc = h->use_nccl ? d0.d_red : d0.d_acc;
+  p.cells = d0.d_heat_cells;
+  p.n_cells = (uint32_t)nc;
+  p.tick = h->opt.tick;
+  p.out = d0.d_heat_out;
+  p.bad = d0.d_heat_bad;
+  const int e = dsi::launch_heatmap_kernel(p, d0.stream);
+  if (e) return cuda_fail(h, (cudaError_t)e, "heatmap kernel launch");
+  unsigned int bad = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(h->heat_out.p, d0.d_heat_out, nc * sizeof(dsi::HeatOut), cudaMemcpyDeviceToHost,
+                              d0.stream));
+  CUDA_TRY(h, cudaMemcpyAsync(&bad, d0.d_heat_bad, sizeof(unsigned int), cudaMemcpyDeviceToHost, d0.stream));
+  for (auto &d : h->dev) {  // the all-reduce ran on every device's stream
+    CUDA_TRY(h, cudaSetDevice(d.ordinal));
+    CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+  }
+  if (bad) return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
+  for (size_t i = 0; i < nc; ++i) {
+    const dsi::HeatCell &hc = h->heat_cells[i];
+    const dsi::HeatOut &o = h->heat_out.p[i];
+    const CfgTicks &t = h->ticks[hc.first];
+    dsi_heatmap_cell &c = cells[i];
+    c.t_target = t.ut;
+    c.t_drafter = t.ud;
+    c.accept_rate = t.a;
+    c.sp_degree = t.sp;
+    c.n_tokens = t.n;
+    c.si_lookahead = o.si_k;
+    c.dsi_lookahead = o.dsi_k;
+    c.nonsi = o.nonsi;
+    c.si = o.si;
+    c.dsi = o.dsi;
+    c.r_nonsi_si = o.r_nonsi_si;
+    c.r_si_dsi = o.r_si_dsi;
+    c.r_nonsi_dsi = o.r_nonsi_dsi;
+    c.r_min_dsi = o.r_min_dsi;
+    c.first_cfg = hc.first;
+    c.n_cfg = hc.count;
+  }
   return DSI_OK;
 }
 

@@ -82,6 +82,7 @@ def _load():
         "dsi_eq1_feasible": ([i64, i64, i32, i32], i32),
         "dsi_shard_bounds": ([V, u64, i32, V], ctypes.c_int),
         "dsi_heatmap": ([V, V, sz, V, sz, P(sz)], ctypes.c_int),
+        "dsi_sim_heatmap": ([V, V, sz, P(sz)], ctypes.c_int),
         "dsi_heatmap_csv": ([V, sz, ctypes.c_char_p], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
@@ -99,7 +100,7 @@ EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce",
             "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
             "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
             "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
-            "dsi_heatmap_csv")
+            "dsi_heatmap_csv", "dsi_sim_heatmap")
 
 
 class DsiError(RuntimeError):
@@ -198,6 +199,16 @@ def dsi_sim_reduce(h, n: int, out: np.ndarray | None = None) -> np.ndarray:
     return out
 
 
+def dsi_sim_heatmap(h, out: np.ndarray | None = None) -> np.ndarray:
+    """On-device heatmap product after a run (every rank must call it)."""
+    n = ctypes.c_size_t()
+    _check(lib.dsi_sim_heatmap(h, None, 0, ctypes.byref(n)), h)
+    if out is None or out.size != n.value:
+        out = np.zeros(n.value, HEATMAP_DTYPE)
+    _check(lib.dsi_sim_heatmap(h, out.ctypes.data, out.size, ctypes.byref(n)), h)
+    return out
+
+
 def dsi_sim_trials(h, cfg: int, first: int, count: int) -> dict:
     arrs = {k: np.zeros(count, np.int32) for k in ("acc", "m", "iters", "si", "dsi")}
     _check(lib.dsi_sim_trials(h, cfg, first, count, *[arrs[k].ctypes.data for k in
@@ -273,6 +284,10 @@ class Simulator:
         if count is None:
             count = int(self.configs["n_trials"][cfg]) - first
         return dsi_sim_trials(self.h, cfg, first, count)
+
+    def heatmap(self, out: np.ndarray | None = None) -> np.ndarray:
+        """Per-cell argmins and ratio panels computed on the device."""
+        return dsi_sim_heatmap(self.h, out)
 
     def hist(self, cfg: int) -> tuple:
         return dsi_sim_hist(self.h, cfg, int(self.configs["lookahead"][cfg]))

@@ -516,3 +516,59 @@ def test_fresh_verifier_options():
     with pytest.raises(D.DsiError) as e:
         D.Simulator(cfgs, tick=tick, seed=SEED, flags=FRESH | D.DSI_F_SHARED_STREAMS)
     assert e.value.status == D.DSI_E_RANGE
+
+
+def _assert_cells_equal(got, want, ctx=""):
+    assert got.size == want.size, ctx
+    for f in want.dtype.names:
+        np.testing.assert_array_equal(got[f], want[f], err_msg=f"{ctx} {f}")
+
+
+@pytest.mark.parametrize("mode", ["default", "shared", "fresh", "ttft", "nccl"])
+def test_device_heatmap_equals_host_heatmap(mode):
+    """dsi_sim_heatmap (argmin over k on the device) == dsi_heatmap over
+    dsi_sim_reduce's results, every field bit for bit (NaN where no k satisfies Eq. 1)."""
+    flags, kw = 0, {}
+    if mode == "ttft":
+        cfgs, tick = W.cfg2_ttft(trials=2000)
+    elif mode == "default":  # k <= 10: the t_d = 0.01 cells have no Eq.-1-feasible k (need k >= 15)
+        cfgs, tick = W.cfg3(trials=400, k_max=10, cells=slice(0, 10100, 29))
+    else:
+        cfgs, tick = W.cfg3(trials=400, k_max=200, cells=slice(3, 10100, 53))
+    if mode == "shared":
+        flags = D.DSI_F_SHARED_STREAMS
+    elif mode == "fresh":
+        flags = FRESH
+    elif mode == "nccl":
+        kw["nccl_id"] = D.dsi_nccl_unique_id()
+    sim, res = run_sim(cfgs, tick, flags=flags, **kw)
+    want = D.dsi_heatmap(cfgs, res)
+    got = sim.heatmap()
+    _assert_cells_equal(got, want, mode)
+    assert np.any(got["dsi_lookahead"] == -1) == (mode == "default")
+    assert np.isnan(got["dsi"]).sum() == np.sum(got["dsi_lookahead"] == -1)
+    sim.close()
+
+
+def test_device_heatmap_after_update_and_state():
+    cfgs, tick = W.cfg3(trials=200, k_max=20, cells=slice(0, 10100, 97))
+    sim = D.Simulator(cfgs, tick=tick, seed=SEED)
+    n = ctypes_count(sim)
+    assert n == cfgs.size // 20
+    with pytest.raises(D.DsiError) as e:
+        sim.heatmap()
+    assert e.value.status == D.DSI_E_STATE
+    new = cfgs.copy()
+    new["accept_rate"] = np.round(1.0 - cfgs["accept_rate"], 2)
+    sim.update(new).run()
+    got = sim.heatmap()
+    _, res = run_sim(new, tick, flags=0)
+    _assert_cells_equal(got, D.dsi_heatmap(new, res), "update")
+    sim.close()
+
+
+def ctypes_count(sim):
+    import ctypes
+    n = ctypes.c_size_t()
+    assert D.lib.dsi_sim_heatmap(sim.h, None, 0, ctypes.byref(n)) == 0
+    return n.value
