@@ -64,7 +64,9 @@ __device__ __forceinline__ Word4 philox_call(const uint4 &u, const TrialHalf &t,
 // rej = (rej << 4) | [w >= thr] << 3 | [z >= thr] << 2 | [y >= thr] << 1 | [x >= thr]
 // from the carries of u + (2^32 - thr) (thr >= 1): 2 ALU instructions per bit.
 __device__ __forceinline__ uint32_t pack4(uint32_t rej, const Word4 &u, uint32_t nthr) {
-  // (measured: compare + select packing, all on the ALU pipe, was 6% slower)
+  // (measured, profiles/r01_ab_pack.jsonl: compare + select packing was 6% slower; the
+  //  carry as the majority bit of (u, n, u + n) funnel-shifted in, all on the ALU pipe, 16%
+  //  slower for 4 bits and 8% for 2 of the 4: the IMAD.X half of addc is the cheaper pipe)
   uint32_t t;
   asm("add.cc.u32 %1, %2, %6;\n\t"
       "addc.u32 %0, %0, %0;\n\t"

@@ -8,8 +8,8 @@
 //   group's trials in tiles of blockDim:
 //   phase 1 (one trial per thread): Philox + Bernoulli mask exactly as dsi_kernel.cu,
 //     then the trial's summary m = #zeros + 1, n2 = #segments with g >= 2 and the list
-//     of run lengths L >= 2 of accepted drafts (a segment of length g has L = g - 1),
-//     sorted in decreasing order, into shared memory;
+//     of run lengths L of accepted drafts (a segment of length g has L = g - 1) that are
+//     long for at least one of the block's configs (L > min k_eff), into shared memory;
 //   phase 2 (each thread owns CPT configs, the tile's trials in lockstep):
 //     I = m + sum_{L >= k+1} floor(L/(k+1)),
 //     L_DSI = m t_t + n2 S(1) + sum_{L >= k+1} (S(ceil(L/k)) - S(1))
@@ -35,18 +35,6 @@ struct CfgLite {  // what phase 2 needs of a config (shared memory, 48 B)
   uint32_t m_sp_hi;
   int32_t kd, sp_eff, nonsi;
 };
-
-__device__ __forceinline__ void insert_desc(uint16_t *runs, int &nr, int L) {
-  // insertion into runs[0..nr) kept in decreasing order (slot-interleaved layout)
-  int i = nr++;
-  while (i > 0) {
-    const int prev = runs[(i - 1) * CRN_THREADS];
-    if (prev >= L) break;
-    runs[i * CRN_THREADS] = (uint16_t)prev;
-    --i;
-  }
-  runs[i * CRN_THREADS] = (uint16_t)L;
-}
 
 // Extra costs of a segment with L = g - 1 >= k + 1 accepted drafts (seg_long of the
 // per-config kernel): x = floor(L/(k+1)) SI iterations, y = S(ceil(L/k)) - S(1).
@@ -83,7 +71,10 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
   sp += (size_t)CRN_THREADS * sizeof(uint2);
   uint16_t *runs = reinterpret_cast<uint16_t *>(sp);  // runs[i * CRN_THREADS + slot]
 
+  __shared__ int s_kmin;
   if (threadIdx.x < 5) s_bsum[threadIdx.x] = 0ull;
+  if (threadIdx.x == 0) s_kmin = 1 << 30;
+  __syncthreads();
   if (mode == MODE_STREAM)
     for (int q = threadIdx.x; q < nq; q += CRN_THREADS) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
   for (int j = threadIdx.x; j < CPT * CRN_THREADS; j += CRN_THREADS) {
@@ -107,8 +98,12 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
       l.m_sp_lo = 1u;
     }
     cl[j] = l;
+    if (j < (int)un.count) atomicMin(&s_kmin, l.k_eff);
   }
   __syncthreads();
+  // a run of L accepted drafts is long for a config iff L > k_eff: runs of at most the
+  // block's smallest k_eff are long for none of its configs and are not stored
+  const int kmin = s_kmin;
 
   // Per-trial latencies split into a config-independent part and long-run corrections:
   //   I = m + ai,  L_DSI = m t_t + n2 S(1) + ay   (ai = ay = 0 unless a run exceeds k)
@@ -133,7 +128,7 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
       const uint32_t trial = (uint32_t)t;
       const TrialHalf th = philox_trial_half(trial, P.keys);
       uint16_t *myruns = runs + threadIdx.x;
-      int nz = 0, n2 = 0, run = 0, lastz = 0, nr = 0;
+      int nz = 0, n2 = 0, run = 0, lastz = 0, nr = 0, maxL = 0;
       for (int w = 0; w < nwords; ++w) {
         uint32_t Rw;
         if (mode == MODE_STREAM) {
@@ -165,16 +160,21 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
           const uint32_t below = Rw & ((1u << zb) - 1u);
           const int prev = below ? base + 31 - __clz(below) : lastz;
           const int L = base + zb - prev - 1;  // accepted drafts in this segment
-          if (L >= 2) insert_desc(myruns, nr, L);
+          if (L > kmin) {
+            myruns[nr++ * CRN_THREADS] = (uint16_t)L;
+            maxL = max(maxL, L);
+          }
         }
         lastz = base + 31 - __clz(Rw);
         run = nv - 1 - (31 - __clz(Rw));
       }
       n2 += run >= 1;  // the final segment (the trailing run, then position N)
-      if (run >= 2) insert_desc(myruns, nr, run);
-      const uint32_t maxL = nr ? myruns[0] : 0u;
+      if (run > kmin) {
+        myruns[nr++ * CRN_THREADS] = (uint16_t)run;
+        maxL = max(maxL, run);
+      }
       const uint32_t m = (uint32_t)(nz + 1);
-      summ[threadIdx.x] = make_uint2(m | ((uint32_t)n2 << 16), (uint32_t)nr | (maxL << 16));
+      summ[threadIdx.x] = make_uint2(m | ((uint32_t)n2 << 16), (uint32_t)nr | ((uint32_t)maxL << 16));
       my_m += m;
       my_n += (unsigned)n2;
       my_mm += m * m;
@@ -201,10 +201,9 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
         int si = m * l[c].si_cost;
         if (maxL > l[c].k_eff) {  // some run is long for this config: corrections
           int ai = 0, ay = 0;
-          for (int r = 0; r < nr; ++r) {
+          for (int r = 0; r < nr; ++r) {  // the stored runs, in trial order
             const int L = runs[r * CRN_THREADS + s];
-            if (L <= l[c].k_eff) break;
-            long_run(L, l[c], ai, ay);
+            if (L > l[c].k_eff) long_run(L, l[c], ai, ay);
           }
           p_ai[c] += (unsigned)ai;
           p_ai2[c] += (unsigned)(ai * ai);
