@@ -33,7 +33,8 @@ struct CfgLite {  // what phase 2 needs of a config (shared memory, 48 B)
   int32_t t_t, s1, si_cost, k_eff;
   uint32_t m_si, m_k_lo, m_k_hi, m_sp_lo;
   uint32_t m_sp_hi;
-  int32_t kd, sp_eff, nonsi;
+  int32_t kd, nonsi;
+  int16_t sp_eff, noqueue;  // noqueue: S(b) = b k t_d (CFG_NOQUEUE)
 };
 
 // Extra costs of a segment with L = g - 1 >= k + 1 accepted drafts (seg_long of the
@@ -67,13 +68,18 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
   sp += (size_t)P.max_nq * sizeof(uint4);
   CfgLite *cl = reinterpret_cast<CfgLite *>(sp);
   sp += (size_t)CPT * CRN_THREADS * sizeof(CfgLite);
-  uint2 *summ = reinterpret_cast<uint2 *>(sp);  // per trial slot: (m | n2 << 16, nruns | maxL << 16)
-  sp += (size_t)CRN_THREADS * sizeof(uint2);
+  // per trial slot: (m, n2, max stored L, nr | sum ceil(L/kmin) << 10 | sum floor(L/(kmin+1)) << 21)
+  // (nr <= N/3 + 2 < 2^10, both sums <= N - 1 < 2^11: N <= 2048)
+  uint4 *summ = reinterpret_cast<uint4 *>(sp);
+  sp += (size_t)CRN_THREADS * sizeof(uint4);
   uint16_t *runs = reinterpret_cast<uint16_t *>(sp);  // runs[i * CRN_THREADS + slot]
 
-  __shared__ int s_kmin;
+  __shared__ int s_kmin, s_nfast;
   if (threadIdx.x < 5) s_bsum[threadIdx.x] = 0ull;
-  if (threadIdx.x == 0) s_kmin = 1 << 30;
+  if (threadIdx.x == 0) {
+    s_kmin = 1 << 30;
+    s_nfast = 0;
+  }
   __syncthreads();
   if (mode == MODE_STREAM)
     for (int q = threadIdx.x; q < nq; q += CRN_THREADS) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
@@ -91,7 +97,8 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
       l.m_sp_lo = c.m_sp_lo;
       l.m_sp_hi = c.m_sp_hi;
       l.kd = c.kd;
-      l.sp_eff = c.sp_eff;
+      l.sp_eff = (int16_t)c.sp_eff;
+      l.noqueue = (c.flags & CFG_NOQUEUE) ? 1 : 0;
       l.nonsi = N * c.t_t;
     } else {
       l.k_eff = 1 << 20;  // an empty slot: no run is ever long
@@ -102,8 +109,20 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
   }
   __syncthreads();
   // a run of L accepted drafts is long for a config iff L > k_eff: runs of at most the
-  // block's smallest k_eff are long for none of its configs and are not stored
+  // block's smallest k_eff are long for none of its configs and are not stored.  Configs
+  // with k_eff == kmin (most of a block: configs are sorted by k) and no queueing take
+  // every stored run, and their corrections are linear in per-trial sums over the runs:
+  //   ai = sum floor(L/(k+1)),  ay = sum (S(ceil(L/k)) - S(1)) = kd sum ceil(L/k) - nr S(1)
   const int kmin = s_kmin;
+  for (int j = threadIdx.x; j < (int)un.count; j += CRN_THREADS)
+    if (cl[j].noqueue && cl[j].k_eff == kmin) atomicAdd(&s_nfast, 1);
+  __syncthreads();
+  // the per-trial sums cost two divisions per stored run in phase 1: worth it only when
+  // enough of the block's configs use them
+  const bool sums = s_nfast * 8 >= (int)un.count;
+  const uint32_t mk_lo = (uint32_t)((0x100000000ull + (unsigned)kmin - 1) / (unsigned)kmin);
+  const uint32_t mk_hi = kmin == 1 ? 1u : 0u;  // ceil(2^32 / kmin) = lo + hi 2^32
+  const uint32_t mk1 = (uint32_t)((0x100000000ull + (unsigned)kmin) / (unsigned)(kmin + 1));
 
   // Per-trial latencies split into a config-independent part and long-run corrections:
   //   I = m + ai,  L_DSI = m t_t + n2 S(1) + ay   (ai = ay = 0 unless a run exceeds k)
@@ -129,6 +148,7 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
       const TrialHalf th = philox_trial_half(trial, P.keys);
       uint16_t *myruns = runs + threadIdx.x;
       int nz = 0, n2 = 0, run = 0, lastz = 0, nr = 0, maxL = 0;
+      uint32_t sumb = 0, sumx = 0;  // sum ceil(L/kmin), sum floor(L/(kmin+1)) over stored runs
       for (int w = 0; w < nwords; ++w) {
         uint32_t Rw;
         if (mode == MODE_STREAM) {
@@ -163,6 +183,10 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
           if (L > kmin) {
             myruns[nr++ * CRN_THREADS] = (uint16_t)L;
             maxL = max(maxL, L);
+            if (sums) {
+              sumb += magic_div((uint32_t)(L + kmin - 1), mk_lo, mk_hi);
+              sumx += magic_div((uint32_t)L, mk1, 0u);
+            }
           }
         }
         lastz = base + 31 - __clz(Rw);
@@ -172,9 +196,14 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
       if (run > kmin) {
         myruns[nr++ * CRN_THREADS] = (uint16_t)run;
         maxL = max(maxL, run);
+        if (sums) {
+          sumb += magic_div((uint32_t)(run + kmin - 1), mk_lo, mk_hi);
+          sumx += magic_div((uint32_t)run, mk1, 0u);
+        }
       }
+
       const uint32_t m = (uint32_t)(nz + 1);
-      summ[threadIdx.x] = make_uint2(m | ((uint32_t)n2 << 16), (uint32_t)nr | ((uint32_t)maxL << 16));
+      summ[threadIdx.x] = make_uint4(m, (uint32_t)n2, (uint32_t)maxL, (uint32_t)nr | (sumb << 10) | (sumx << 21));
       my_m += m;
       my_n += (unsigned)n2;
       my_mm += m * m;
@@ -191,19 +220,23 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
     uint32_t p_gtn[CPT], p_gts[CPT], p_ai[CPT], p_ai2[CPT], p_mai[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) p_gtn[c] = p_gts[c] = p_ai[c] = p_ai2[c] = p_mai[c] = 0u;
-    for (int s = 0; s < ntr; ++s) {
-      const uint2 sm = summ[s];
-      const int m = (int)(sm.x & 0xffffu), n2 = (int)(sm.x >> 16);
-      const int nr = (int)(sm.y & 0xffffu), maxL = (int)(sm.y >> 16);
+    auto visit = [&](const uint4 v, const int s) {
+      const int m = (int)v.x, n2 = (int)v.y, maxL = (int)v.z;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         int dsi = m * l[c].t_t + n2 * l[c].s1;
         int si = m * l[c].si_cost;
         if (maxL > l[c].k_eff) {  // some run is long for this config: corrections
+          const int nr = (int)(v.w & 0x3ffu);
           int ai = 0, ay = 0;
-          for (int r = 0; r < nr; ++r) {  // the stored runs, in trial order
-            const int L = runs[r * CRN_THREADS + s];
-            if (L > l[c].k_eff) long_run(L, l[c], ai, ay);
+          if (sums && l[c].noqueue && l[c].k_eff == kmin) {  // every stored run, S linear in b
+            ai = (int)(v.w >> 21);
+            ay = (int)((v.w >> 10) & 0x7ffu) * l[c].kd - nr * l[c].s1;
+          } else {
+            for (int r = 0; r < nr; ++r) {  // the stored runs, in trial order
+              const int L = runs[r * CRN_THREADS + s];
+              if (L > l[c].k_eff) long_run(L, l[c], ai, ay);
+            }
           }
           p_ai[c] += (unsigned)ai;
           p_ai2[c] += (unsigned)(ai * ai);
@@ -218,7 +251,14 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
         p_gtn[c] += (uint32_t)(l[c].nonsi - dsi) >> 31;
         p_gts[c] += (uint32_t)(si - dsi) >> 31;
       }
+    };
+    int s = 0;
+    for (; s + 1 < ntr; s += 2) {  // two trials per iteration: half the loop overhead
+      const uint4 v0 = summ[s], v1 = summ[s + 1];
+      visit(v0, s);
+      visit(v1, s + 1);
     }
+    if (s < ntr) visit(summ[s], s);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       a_gtn[c] += p_gtn[c];
@@ -300,7 +340,7 @@ size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_
   const int max_nq = (max_n - 1 + 3) / 4 + 1;
   const size_t runs = ((size_t)block_threads * max_runs * sizeof(uint16_t) + 7) & ~(size_t)7;
   return (size_t)max_nq * sizeof(uint4) + (size_t)cfg_per_block * sizeof(CfgLite) +
-         (size_t)block_threads * sizeof(uint2) + runs;
+         (size_t)block_threads * sizeof(uint4) + runs;
 }
 
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream) {
