@@ -132,6 +132,9 @@ struct HeatParams {
   unsigned int *bad;  // set when a config's trial count differs from n_trials
 };
 int launch_heatmap_kernel(const HeatParams &p, void *stream);
+// *bad |= 1 if some config's F_TRIALS differs from its n_trials
+int launch_check_trials(const DevCfg *cfg, const unsigned long long *acc, uint64_t n, unsigned int *bad,
+                        void *stream);
 
 size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs);
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream);

@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -35,6 +37,7 @@ constexpr int kMaxTokens = 32768;  // keeps every magic division exact (x * d <=
 constexpr uint64_t kMaxTrials = 1ull << 32;
 constexpr int kDefaultThreads = 128;
 constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size (launch bounds)
+constexpr size_t kReduceChunks = 8;  // dsi_sim_reduce: D2H chunks overlapped with the finalize
 constexpr int kCrnMaxN = 2048;     // shared-stream mode: 128 per-trial run lists of <= N/3+2
                                    // u16 entries fit shared memory (209 KB at N 2048)
 
@@ -87,6 +90,7 @@ struct CfgTicks {
   uint64_t trials;
   double a;
   double ut, ud;  // t_target, t_drafter as given (heatmap cells group on the user values)
+  int32_t eq1, min_k;  // Eq. 1 holds at (k, SP); the minimal lookahead at SP
 };
 
 // ceil(2^32 / d) split into low word and bit 32 (d >= 1).
@@ -165,6 +169,8 @@ struct dsi_sim {
   std::vector<dsi::HeatCell> heat_cells;  // heatmap cells (planned on first use, reset by update)
   bool heat_planned = false, heat_uploaded = false;
   Pinned<dsi::HeatOut> heat_out;
+  Pinned<unsigned int> host_bad;         // partition-check flag (D2H)
+  cudaEvent_t chunk_ev[8] = {};          // reduce: one event per D2H chunk
   int launches = 0;
   std::string err;
 };
@@ -251,6 +257,8 @@ dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTic
   o.a = c.accept_rate;
   o.ut = c.t_target;
   o.ud = c.t_drafter;
+  o.eq1 = dsi_eq1_feasible(o.t_t, o.t_d, c.lookahead, c.sp_degree);
+  o.min_k = dsi_min_lookahead(o.t_t, o.t_d, c.sp_degree);
   o.thr = (uint64_t)(c.accept_rate * 4294967296.0);  // exact: a * 2^32, then floor
   o.k = c.lookahead;
   o.sp = c.sp_degree;
@@ -279,7 +287,7 @@ DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
             (fresh_cfg ? dsi::CFG_FRESH : 0u);
   d.t_d = (int32_t)t.t_d;
   d.k = t.k;
-  if (dsi_eq1_feasible(t.t_t, t.t_d, t.k, t.sp) == 1) d.flags |= dsi::CFG_EQ1;
+  if (t.eq1 == 1) d.flags |= dsi::CFG_EQ1;
   d.nonsi = (int32_t)(t.t_t1 + (int64_t)(t.n - 1) * t.t_t);
   d.e_si = (int32_t)((t.t_d1 - t.t_d) + (t.t_t1 - t.t_t));
   d.t_t1 = (int32_t)t.t_t1;
@@ -307,21 +315,84 @@ double unit_cost(const CfgTicks &t, uint64_t trials) {
   return (double)trials * (double)t.n * (11.0 + 10.0 * (1.0 - t.a));
 }
 
-// Run fn(begin, end) over [0, n) on up to hardware_concurrency host threads
-// (large grids only: the per-config host work is O(1) and independent).
+// Process-wide pool of host worker threads (created on first use, kept for the life of
+// the process): the O(n_cfg) host passes -- validation, staging, finalize -- run on it
+// without spawning threads per call.  One job at a time; the calling thread helps.
+class WorkerPool {
+ public:
+  static WorkerPool &get() {
+    static WorkerPool *pool = new WorkerPool();  // never destroyed: workers idle at exit
+    return *pool;
+  }
+  size_t threads() const { return workers_.size() + 1; }
+  void run(uint32_t n_chunks, const std::function<void(size_t)> &job) {
+    std::lock_guard<std::mutex> one_job(submit_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      ++gen_;
+      job_.store(&job);
+      // tickets are (generation << 32 | chunk): a worker holding a ticket of an older job
+      // sees a different generation in info_ and drops it, so no chunk runs twice
+      info_.store(gen_ << 32 | n_chunks);
+      pending_.store(n_chunks);
+      next_.store(gen_ << 32);
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_.load() == 0; });
+  }
+
+ private:
+  WorkerPool() {
+    size_t nt = std::thread::hardware_concurrency();
+    nt = std::min<size_t>(std::max<size_t>(nt, 1), 32);
+    for (size_t i = 1; i < nt; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  void work() {
+    for (;;) {
+      const uint64_t t = next_.fetch_add(1);
+      const uint64_t info = info_.load();
+      if ((t >> 32) != (info >> 32) || (t & 0xffffffffu) >= (info & 0xffffffffu)) return;
+      (*job_.load())((size_t)(t & 0xffffffffu));  // a valid ticket: its job is still running
+      if (pending_.fetch_sub(1) == 1) {
+        std::lock_guard<std::mutex> lk(mu_);
+        done_cv_.notify_all();
+      }
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex submit_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::atomic<const std::function<void(size_t)> *> job_{nullptr};
+  std::atomic<uint64_t> info_{0}, next_{0};
+  std::atomic<uint32_t> pending_{0};
+  uint64_t gen_ = 0;  // guarded by mu_
+};
+
+// Run fn(begin, end) over [0, n) on the worker pool (large grids only: the per-config
+// host work is O(1) and independent).
 template <class Fn>
 void parallel_for(size_t n, Fn fn) {
-  size_t nt = std::thread::hardware_concurrency();
-  if (nt == 0) nt = 1;
-  nt = std::min<size_t>(nt, 32);
-  if (n < (1u << 16) || nt == 1) {
+  WorkerPool &pool = WorkerPool::get();
+  if (n < (1u << 15) || pool.threads() == 1) {
     fn((size_t)0, n);
     return;
   }
-  std::vector<std::thread> pool;
-  const size_t chunk = (n + nt - 1) / nt;
-  for (size_t b = 0; b < n; b += chunk) pool.emplace_back(fn, b, std::min(n, b + chunk));
-  for (auto &t : pool) t.join();
+  const size_t chunks = std::min(n, pool.threads() * 4);
+  const std::function<void(size_t)> job = [&](size_t c) { fn(n * c / chunks, n * (c + 1) / chunks); };
+  pool.run((uint32_t)chunks, job);
 }
 
 // Validate every config into ticks; on failure h->err names the first bad config.
@@ -398,6 +469,9 @@ void free_handle(dsi_sim *h) {
   h->host_seg.release();
   h->host_si.release();
   h->heat_out.release();
+  h->host_bad.release();
+  for (auto &ev : h->chunk_ev)
+    if (ev) cudaEventDestroy(ev);
   delete h;
 }
 
@@ -770,6 +844,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   {
     cudaError_t e = h->dev_cfg.alloc(n_cfg);
     if (e == cudaSuccess) e = h->host_acc.alloc(n_cfg * dsi::NF);
+    if (e == cudaSuccess) e = h->host_bad.alloc(1);
     if (e == cudaSuccess && (opt->flags & DSI_F_HIST)) {
       e = h->host_seg.alloc(n_cfg * 64);
       if (e == cudaSuccess) e = h->host_si.alloc(sib);
@@ -1022,12 +1097,23 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   const size_t nacc = n_cfg * dsi::NF;
   dsi_status st = sum_across(h, hist);
   if (st != DSI_OK) return st;
-  // every device now holds the global sums (or there is one device): read device 0
+  // every device now holds the global sums (or there is one device): read device 0.
+  // The partition check (every trial simulated exactly once) runs on the device before the
+  // copies; the moments come back in chunks so the host finalizes chunk i while chunk i+1
+  // is in flight.
   DeviceState &d0 = h->dev[0];
   CUDA_TRY(h, cudaSetDevice(d0.ordinal));
   const unsigned long long *src = h->use_nccl ? d0.d_red : d0.d_acc;
-  CUDA_TRY(h, cudaMemcpyAsync(h->host_acc.p, src, nacc * sizeof(unsigned long long),
-                              cudaMemcpyDeviceToHost, d0.stream));
+  if (!d0.d_heat_bad) CUDA_TRY(h, cudaMalloc((void **)&d0.d_heat_bad, sizeof(unsigned int)));
+  if (!h->chunk_ev[0])
+    for (auto &ev : h->chunk_ev) CUDA_TRY(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaMemsetAsync(d0.d_heat_bad, 0, sizeof(unsigned int), d0.stream));
+  {
+    const int e = dsi::launch_check_trials(d0.d_cfg, src, n_cfg, d0.d_heat_bad, d0.stream);
+    if (e) return cuda_fail(h, (cudaError_t)e, "partition check launch");
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(h->host_bad.p, d0.d_heat_bad, sizeof(unsigned int), cudaMemcpyDeviceToHost,
+                              d0.stream));
   if (hist) {
     CUDA_TRY(h, cudaMemcpyAsync(h->host_seg.p, h->use_nccl ? d0.d_seg_red : d0.d_seg,
                                 n_cfg * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d0.stream));
@@ -1035,20 +1121,31 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
                                 h->si_bins_total * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                 d0.stream));
   }
-  for (auto &d : h->dev) {
+  const size_t n_chunks = n_cfg < (1u << 16) ? 1 : kReduceChunks;
+  for (size_t c = 0; c < n_chunks; ++c) {
+    const size_t b = n_cfg * c / n_chunks, e = n_cfg * (c + 1) / n_chunks;
+    CUDA_TRY(h, cudaMemcpyAsync(h->host_acc.p + b * dsi::NF, src + b * dsi::NF,
+                                (e - b) * dsi::NF * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                d0.stream));
+    CUDA_TRY(h, cudaEventRecord(h->chunk_ev[c], d0.stream));
+  }
+  for (auto &d : h->dev) {  // the all-reduce ran on every device's stream
+    if (d.ordinal == d0.ordinal) continue;
     CUDA_TRY(h, cudaSetDevice(d.ordinal));
     CUDA_TRY(h, cudaStreamSynchronize(d.stream));
   }
-  // check the partition (every trial simulated exactly once) before writing any output
-  std::atomic<bool> bad_trials{false};
-  parallel_for(n_cfg, [&](size_t b, size_t e) {
-    for (size_t i = b; i < e; ++i)
-      if (h->host_acc.p[i * dsi::NF + dsi::F_TRIALS] != h->ticks[i].trials) bad_trials = true;
-  });
-  if (bad_trials) return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
+  CUDA_TRY(h, cudaSetDevice(d0.ordinal));
+  CUDA_TRY(h, cudaEventSynchronize(h->chunk_ev[0]));  // the flag precedes chunk 0
+  if (*h->host_bad.p) {
+    CUDA_TRY(h, cudaStreamSynchronize(d0.stream));
+    return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
+  }
   const double tick = h->opt.tick;
-  parallel_for(n_cfg, [&](size_t b, size_t e) {
-  for (size_t i = b; i < e; ++i) {
+  for (size_t c = 0; c < n_chunks; ++c) {
+  const size_t cb = n_cfg * c / n_chunks, ce = n_cfg * (c + 1) / n_chunks;
+  if (c) CUDA_TRY(h, cudaEventSynchronize(h->chunk_ev[c]));
+  parallel_for(ce - cb, [&](size_t b, size_t e) {
+  for (size_t i = cb + b; i < cb + e; ++i) {
     const unsigned long long *a = &h->host_acc.p[i * dsi::NF];
     const CfgTicks &t = h->ticks[i];
     dsi_result &r = out[i];
@@ -1072,8 +1169,8 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
     r.n_dsi_gt_nonsi = (int64_t)a[dsi::F_GT_NONSI];
     r.n_dsi_gt_si = (int64_t)a[dsi::F_GT_SI];
     r.threshold = t.thr;
-    r.eq1_feasible = dsi_eq1_feasible(t.t_t, t.t_d, t.k, t.sp);
-    r.min_lookahead = dsi_min_lookahead(t.t_t, t.t_d, t.sp);
+    r.eq1_feasible = t.eq1;
+    r.min_lookahead = t.min_k;
     const double Td = (double)T;
     r.mean_nonsi = (double)r.nonsi_ticks * tick;
     r.mean_si = ((double)r.sum_si_ticks / Td) * tick;
@@ -1086,6 +1183,8 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
     r.std_dsi = stdev((uint64_t)r.sum_dsi_ticks, r.sumsq_dsi_ticks);
   }
   });
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(d0.stream));  // the histogram copies (HIST), if any
   h->reduced = true;
   return DSI_OK;
 }

@@ -1,4 +1,5 @@
-// dsi_heatmap_dev.cu -- on-device heatmap product (Fig. 3 / Fig. 5 of the
+// dsi_reduce_dev.cu -- device side of dsi_sim_reduce (the partition check) and the
+// on-device heatmap product (Fig. 3 / Fig. 5 of the
 // paper): per (drafter latency, acceptance) cell, the argmin over
 // the lookaheads of the mean SI latency, and over the Eq.-1-feasible lookaheads of the
 // mean DSI latency (ties to the smallest k), plus the four ratio panels.
@@ -12,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+
+#include <algorithm>
 
 #include "dsi_device.h"
 
@@ -85,7 +88,26 @@ __global__ void __launch_bounds__(256) dsi_heatmap_kernel(const HeatParams P) {
   P.out[cell] = o;
 }
 
+// dsi_sim_reduce's partition check: every config's trial counter equals n_trials (each
+// trial simulated exactly once), read on the device so the host never scans the sums.
+__global__ void __launch_bounds__(256) dsi_check_trials_kernel(const DevCfg *cfg,
+                                                               const unsigned long long *acc, uint64_t n,
+                                                               unsigned int *bad) {
+  bool b = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    b |= acc[i * NF + F_TRIALS] != cfg[i].n_trials;
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
 }  // namespace
+
+int launch_check_trials(const DevCfg *cfg, const unsigned long long *acc, uint64_t n, unsigned int *bad,
+                        void *stream) {
+  if (n == 0) return 0;
+  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, 148ull * 8);
+  dsi_check_trials_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(cfg, acc, n, bad);
+  return (int)cudaGetLastError();
+}
 
 int launch_heatmap_kernel(const HeatParams &p, void *stream) {
   if (p.n_cells == 0) return 0;
