@@ -15,6 +15,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 R = sys.argv[1] if len(sys.argv) > 1 else "r01"
+if R.startswith("-"):
+    sys.exit(__doc__)
 
 
 def read_csv(path):
@@ -44,8 +46,27 @@ def dram():
     return d
 
 
-def full():
-    rep = os.path.join(OUT, f"prof_{R}.ncu-rep")
+def hotspots(rep, top=15):
+    """Source lines by share of executed warp instructions and of stall samples."""
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+                         capture_output=True, text=True).stdout
+    cur, hdr, out = None, None, []
+    for r in csv.reader(io.StringIO(src)):
+        if r and r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+        elif r and r[0] == "Line No":
+            hdr = r
+        elif hdr and r and r[0] and len(r) > 5 and r[2] == "-":
+            out.append((int(r[hdr.index("Instructions Executed")] or 0),
+                        int(r[hdr.index("Warp Stall Sampling (All Samples)")] or 0), f"{cur}:{r[0]}", r[1].strip()[:80]))
+    ti = sum(o[0] for o in out) or 1
+    ts = sum(o[1] for o in out) or 1
+    return [{"line": w, "instr_share": round(i / ti, 4), "stall_share": round(st / ts, 4), "source": src_}
+            for i, st, w, src_ in sorted(out, reverse=True)[:top]]
+
+
+def full(name=None):
+    rep = os.path.join(OUT, f"{name or 'prof_' + R}.ncu-rep")
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     d = {h: (u, v) for h, u, v in zip(rows[0], rows[1], rows[2])}
@@ -84,8 +105,14 @@ except OSError as e:
     out["dram_error"] = str(e)
 try:
     out["set_full_stride20"], out["instruction_mix_stride20"] = full()
+    out["source_hotspots_stride20"] = hotspots(os.path.join(OUT, f"prof_{R}.ncu-rep"))
 except (OSError, ValueError, IndexError) as e:
     out["full_error"] = str(e)
+try:  # the shared-stream kernel on the full cfg3 grid (profiles/profile_round.sh)
+    out["set_full_crn"], out["instruction_mix_crn"] = full(f"prof_crn_{R}")
+    out["source_hotspots_crn"] = hotspots(os.path.join(OUT, f"prof_crn_{R}.ncu-rep"))
+except (OSError, ValueError, IndexError) as e:
+    out["crn_error"] = str(e)
 for name in (f"{R}_ncu_summary.json", "latest_ncu_summary.json"):
     with open(os.path.join(ROOT, "profiles", name), "w") as f:
         json.dump(out, f, indent=1)
