@@ -147,6 +147,7 @@ struct dsi_sim {
   dsi_options opt{};
   size_t n_cfg = 0;
   std::vector<CfgTicks> ticks;
+  std::vector<CfgTicks> ticks_next;      // dsi_sim_update validates into this, then swaps
   Pinned<DevCfg> dev_cfg;                // staging of the device config table
   std::vector<uint64_t> prefix;          // n_cfg + 1 units
   uint64_t total_units = 0;
@@ -384,9 +385,9 @@ class WorkerPool {
 // Run fn(begin, end) over [0, n) on the worker pool (large grids only: the per-config
 // host work is O(1) and independent).
 template <class Fn>
-void parallel_for(size_t n, Fn fn) {
+void parallel_for(size_t n, Fn fn, size_t min_parallel = (1u << 15)) {
   WorkerPool &pool = WorkerPool::get();
-  if (n < (1u << 15) || pool.threads() == 1) {
+  if (n < min_parallel || n < 2 || pool.threads() == 1) {
     fn((size_t)0, n);
     return;
   }
@@ -396,15 +397,27 @@ void parallel_for(size_t n, Fn fn) {
 }
 
 // Validate every config into ticks; on failure h->err names the first bad config.
-dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n) {
+// Validate every config into `out`; on failure h->err names the first bad config.  With
+// `prev` (dsi_sim_update), also checks what an update must keep: n_trials, and with
+// DSI_F_HIST min(k, N) (the histogram layout).
+dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n, std::vector<CfgTicks> &out,
+                        const std::vector<CfgTicks> *prev = nullptr) {
   std::mutex mu;
   size_t bad = n;
   dsi_status bad_s = DSI_OK;
   std::string bad_msg;
+  const bool hist = h->opt.flags & DSI_F_HIST;
   parallel_for(n, [&](size_t b, size_t e) {
     for (size_t i = b; i < e; ++i) {
       std::string msg;
-      const dsi_status s = convert(h->opt, cfg[i], i, h->ticks[i], msg);
+      dsi_status s = convert(h->opt, cfg[i], i, out[i], msg);
+      if (s == DSI_OK && prev) {
+        const CfgTicks &o = (*prev)[i], &t = out[i];
+        if (t.trials != o.trials || (hist && std::min(t.k, t.n) != std::min(o.k, o.n))) {
+          s = DSI_E_RANGE;
+          msg = "config " + std::to_string(i) + ": n_trials (and, with DSI_F_HIST, min(k, N)) must not change";
+        }
+      }
       if (s != DSI_OK) {
         std::lock_guard<std::mutex> lock(mu);
         if (i < bad) {
@@ -424,17 +437,34 @@ dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n) {
 void fill_dev_cfg(dsi_sim *h) {
   const bool pattern = h->opt.flags & DSI_F_PATTERN;
   const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
-  parallel_for(h->n_cfg, [&](size_t b, size_t e) {
-    for (size_t i = b; i < e; ++i) h->dev_cfg.p[i] = make_dev_cfg(h->ticks[i], pattern, fresh);
-  });
-  uint64_t rec = 0, sib = 0;  // prefix offsets: per-trial records and SI-histogram bins
-  for (size_t i = 0; i < h->n_cfg; ++i) {
-    DevCfg &d = h->dev_cfg.p[i];
-    d.rec_off = rec;
-    rec += h->ticks[i].trials;
-    d.si_hist_off = (uint32_t)sib;
-    sib += (uint64_t)d.k_eff + 1;
+  const size_t n = h->n_cfg;
+  // prefix offsets (per-trial records, SI-histogram bins) in two passes over fixed chunks
+  constexpr size_t K = 64;
+  uint64_t rec[K + 1] = {}, sib[K + 1] = {};
+  parallel_for(K, [&](size_t b, size_t e) {
+    for (size_t c = b; c < e; ++c)
+      for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) {
+        rec[c + 1] += h->ticks[i].trials;
+        sib[c + 1] += (uint64_t)std::min(h->ticks[i].k, h->ticks[i].n) + 1;
+      }
+  }, 1);
+  for (size_t c = 0; c < K; ++c) {
+    rec[c + 1] += rec[c];
+    sib[c + 1] += sib[c];
   }
+  parallel_for(K, [&](size_t b, size_t e) {
+    for (size_t c = b; c < e; ++c) {
+      uint64_t r = rec[c], q = sib[c];
+      for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) {
+        DevCfg &d = h->dev_cfg.p[i];
+        d = make_dev_cfg(h->ticks[i], pattern, fresh);
+        d.rec_off = r;
+        r += h->ticks[i].trials;
+        d.si_hist_off = (uint32_t)q;
+        q += (uint64_t)d.k_eff + 1;
+      }
+    }
+  }, 1);
 }
 
 void free_device(DeviceState &d) {
@@ -476,12 +506,12 @@ void free_handle(dsi_sim *h) {
 }
 
 // Upload the staging table to every device (async on each device's stream).
-dsi_status upload(dsi_sim *h) {
+dsi_status upload(dsi_sim *h, bool plan = true) {
   for (auto &d : h->dev) {
     CUDA_TRY(h, cudaSetDevice(d.ordinal));
     CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg, h->dev_cfg.p, h->n_cfg * sizeof(DevCfg),
                                 cudaMemcpyHostToDevice, d.stream));
-    if (h->shared) {
+    if (h->shared && plan) {  // the shared-stream plan (unchanged by an update that keeps its keys)
       CUDA_TRY(h, cudaMemcpyAsync(d.d_perm, h->perm.data(), h->perm.size() * sizeof(uint32_t),
                                   cudaMemcpyHostToDevice, d.stream));
       CUDA_TRY(h, cudaMemcpyAsync(d.d_groups, h->groups.data(), h->groups.size() * sizeof(dsi::CrnGroup),
@@ -501,26 +531,53 @@ dsi_status upload(dsi_sim *h) {
 // Launch-shape limits that follow from the configs (max N, max min(k, N), TTFT present),
 // and the shared-memory bounds they imply.  Called by create and again by update, whose
 // new configs may change them (the kernels size shared memory from these values).
-dsi_status derive_limits(dsi_sim *h) {
-  int32_t max_n = 1, max_keff = 1;
-  bool any_ttft = false, any_fresh = false;
+dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks) {
+  struct Lim {
+    int32_t max_n = 1, max_keff = 1;
+    bool ttft = false, fresh = false;
+  } lim;
+  std::mutex mu;
   const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
-  for (const CfgTicks &t : h->ticks) {
-    max_n = std::max(max_n, t.n);
-    max_keff = std::max(max_keff, std::min(t.k, t.n));
-    any_ttft = any_ttft || t.t_t1 != t.t_t || t.t_d1 != t.t_d;
-    any_fresh = any_fresh || (fresh && t.kd > t.t_t);
-  }
-  if (any_ttft && max_n > 4096) return fail(h, DSI_E_RANGE, "the TTFT variant supports n_tokens <= 4096");
-  if (dsi::trial_kernel_smem(max_n, max_keff, h->opt.flags & DSI_F_HIST, any_ttft) > 200 * 1024)
+  parallel_for(ticks.size(), [&](size_t b, size_t e) {
+    Lim l;
+    for (size_t i = b; i < e; ++i) {
+      const CfgTicks &t = ticks[i];
+      l.max_n = std::max(l.max_n, t.n);
+      l.max_keff = std::max(l.max_keff, std::min(t.k, t.n));
+      l.ttft = l.ttft || t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+      l.fresh = l.fresh || (fresh && t.kd > t.t_t);
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    lim.max_n = std::max(lim.max_n, l.max_n);
+    lim.max_keff = std::max(lim.max_keff, l.max_keff);
+    lim.ttft = lim.ttft || l.ttft;
+    lim.fresh = lim.fresh || l.fresh;
+  });
+  if (lim.ttft && lim.max_n > 4096) return fail(h, DSI_E_RANGE, "the TTFT variant supports n_tokens <= 4096");
+  if (dsi::trial_kernel_smem(lim.max_n, lim.max_keff, h->opt.flags & DSI_F_HIST, lim.ttft) > 200 * 1024)
     return fail(h, DSI_E_RANGE, "DSI_F_HIST needs (64 + k + 1) * 4 bytes of shared memory <= 200 KiB");
-  if (h->shared && max_n > kCrnMaxN)
+  if (h->shared && lim.max_n > kCrnMaxN)
     return fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS supports n_tokens <= " + std::to_string(kCrnMaxN));
-  h->max_n = max_n;
-  h->max_keff = max_keff;
-  h->any_ttft = any_ttft;
-  h->any_fresh = any_fresh;
+  h->max_n = lim.max_n;
+  h->max_keff = lim.max_keff;
+  h->any_ttft = lim.ttft;
+  h->any_fresh = lim.fresh;
   return DSI_OK;
+}
+
+// The shared-stream plan orders configs by these fields (plan_shared): an update that
+// keeps all of them keeps the plan.
+bool same_plan_keys(const std::vector<CfgTicks> &a, const std::vector<CfgTicks> &b) {
+  std::atomic<bool> same{true};
+  parallel_for(a.size(), [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi && same.load(std::memory_order_relaxed); ++i) {
+      const CfgTicks &x = a[i], &y = b[i];
+      if (x.stream_id != y.stream_id || x.thr != y.thr || x.n != y.n || x.trials != y.trials || x.k != y.k ||
+          x.t_t != y.t_t || x.t_d != y.t_d || x.sp != y.sp)
+        same = false;
+    }
+  });
+  return same;
 }
 
 // Sum the per-config moments (and, with hist, the histograms) over every device of
@@ -760,7 +817,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   }
 
   // ---- validation and tick conversion (before any device work)
-  dsi_status s = validate_all(h, cfg, n_cfg);
+  dsi_status s = validate_all(h, cfg, n_cfg, h->ticks);
   if (s != DSI_OK) return abort_create(s);
   uint64_t sib = 0;
   for (size_t i = 0; i < n_cfg; ++i) {
@@ -776,7 +833,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     return abort_create(DSI_E_RANGE);
   }
   h->si_bins_total = sib;
-  s = derive_limits(h);
+  s = derive_limits(h, h->ticks);
   if (s != DSI_OK) return abort_create(s);
 
   // ---- work units: (config, tile of tile_trials trials), or shared-stream (group, config slice)
@@ -945,32 +1002,25 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   h->err.clear();
   if (!cfg) return fail(h, DSI_E_NULL, "cfg is NULL");
   if (n_cfg != h->n_cfg) return fail(h, DSI_E_RANGE, "n_cfg must equal the handle's");
-  std::vector<CfgTicks> old;
+  // validate into the spare table; h->ticks (and the whole handle) stay as they are on failure
   try {
-    old = h->ticks;
+    h->ticks_next.resize(n_cfg);
   } catch (...) {
     return fail(h, DSI_E_NOMEM, "host tables");
   }
-  dsi_status s = validate_all(h, cfg, n_cfg);
-  if (s == DSI_OK) {
-    for (size_t i = 0; i < n_cfg; ++i) {
-      const bool same_trials = h->ticks[i].trials == old[i].trials;
-      const bool same_bins = std::min(h->ticks[i].k, h->ticks[i].n) == std::min(old[i].k, old[i].n);
-      if (!same_trials || ((h->opt.flags & DSI_F_HIST) && !same_bins)) {
-        s = fail(h, DSI_E_RANGE, "config " + std::to_string(i) +
-                                     ": n_trials (and, with DSI_F_HIST, min(k, N)) must not change");
-        break;
-      }
-    }
-  }
-  const int32_t old_n = h->max_n, old_keff = h->max_keff, old_cpb = h->cfg_per_block, old_runs = h->max_runs;
+  const int32_t old_n = h->max_n, old_keff = h->max_keff;
   const bool old_ttft = h->any_ttft, old_fresh = h->any_fresh;
-  std::vector<uint32_t> old_perm;
-  std::vector<dsi::CrnGroup> old_groups;
-  std::vector<dsi::CrnUnit> old_units;
-  if (s == DSI_OK) s = derive_limits(h);  // the new configs may need a larger launch shape
-  if (s == DSI_OK && h->shared) {
+  dsi_status s = validate_all(h, cfg, n_cfg, h->ticks_next, &h->ticks);
+  if (s == DSI_OK) s = derive_limits(h, h->ticks_next);  // the new configs may need a larger launch shape
+  if (s != DSI_OK) return s;                              // derive_limits only commits on success
+  const bool replan = h->shared && !same_plan_keys(h->ticks, h->ticks_next);
+  if (replan) {
     // re-plan on the host first: the unit table's size is fixed at create
+    const int32_t old_cpb = h->cfg_per_block, old_runs = h->max_runs;
+    std::vector<uint32_t> old_perm;
+    std::vector<dsi::CrnGroup> old_groups;
+    std::vector<dsi::CrnUnit> old_units;
+    h->ticks.swap(h->ticks_next);
     try {
       old_perm = h->perm;
       old_groups = h->groups;
@@ -982,23 +1032,23 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     }
     if (s == DSI_OK && (h->groups.size() != old_groups.size() || h->crn_units.size() != old_units.size()))
       s = fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS: the stream grouping changed; create a new handle");
-    if (s != DSI_OK && !old_groups.empty()) {
-      h->perm.swap(old_perm);
-      h->groups.swap(old_groups);
-      h->crn_units.swap(old_units);
+    if (s != DSI_OK) {  // the handle keeps its previous configs and plan
+      if (!old_groups.empty()) {
+        h->perm.swap(old_perm);
+        h->groups.swap(old_groups);
+        h->crn_units.swap(old_units);
+      }
       h->cfg_per_block = old_cpb;
       h->max_runs = old_runs;
+      h->ticks.swap(h->ticks_next);
+      h->max_n = old_n;
+      h->max_keff = old_keff;
+      h->any_ttft = old_ttft;
+      h->any_fresh = old_fresh;
+      return s;
     }
-  }
-  if (s != DSI_OK) {  // the handle keeps its previous configs
-    const std::string msg = h->err;
-    h->ticks.swap(old);
-    h->max_n = old_n;
-    h->max_keff = old_keff;
-    h->any_ttft = old_ttft;
-    h->any_fresh = old_fresh;
-    h->err = msg;
-    return s;
+  } else {
+    h->ticks.swap(h->ticks_next);
   }
   // wait until no kernel of a previous run still reads the table, then restage it
   for (auto &d : h->dev) {
@@ -1008,7 +1058,7 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   fill_dev_cfg(h);
   h->ran = h->reduced = false;
   h->heat_planned = h->heat_uploaded = false;
-  return upload(h);
+  return upload(h, replan);
 }
 
 dsi_status dsi_sim_run(dsi_sim *h) {
