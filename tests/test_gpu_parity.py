@@ -572,3 +572,22 @@ def ctypes_count(sim):
     n = ctypes.c_size_t()
     assert D.lib.dsi_sim_heatmap(sim.h, None, 0, ctypes.byref(n)) == 0
     return n.value
+
+
+def test_shared_streams_update_with_same_keys_keeps_plan():
+    """An update that keeps every plan key (stream, threshold, N, T, k, t_t, t_d, SP) reuses
+    the shared-stream plan; results equal a fresh handle's, also after a re-planning update."""
+    cfgs, tick = W.cfg3(trials=300, k_max=30, cells=slice(0, 10100, 211))
+    sim, first = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    sim.update(cfgs.copy()).run()
+    again = sim.reduce()
+    for f in MOMENTS:
+        assert np.array_equal(again[f], first[f]), f
+    new = cfgs.copy()
+    new["lookahead"] = 31 - cfgs["lookahead"]  # same grouping, new order inside groups
+    sim.update(new).run()
+    got = sim.reduce()
+    _, want = run_sim(new, tick, flags=D.DSI_F_SHARED_STREAMS)
+    for f in MOMENTS:
+        assert np.array_equal(got[f], want[f]), f
+    sim.close()
