@@ -104,6 +104,22 @@ def alg_instructions(cfgs) -> float:
     return float(np.sum(tt * (11.0 + 10.0 * (1.0 - cfgs["accept_rate"]))))
 
 
+def alg_multiplies(cfgs) -> float:
+    """Algorithmic 32x32->64 multiplies of one pass: Philox4x32-10 takes 10 rounds x 2 per
+    call of 4 indicators, ceil((N-1)/4) calls per trial; configs with a = 0
+    or a = 1 need no random numbers (thresholds 0 and 2^32)."""
+    thr = np.floor(cfgs["accept_rate"] * 4294967296.0)
+    rnd = (thr > 0) & (thr < 4294967296.0)
+    calls = cfgs["n_trials"].astype(np.float64) * np.ceil((cfgs["n_tokens"].astype(np.float64) - 1) / 4)
+    return float(np.sum(calls[rnd]) * 20.0)
+
+
+def mul_peak(sm_mhz: float) -> float:
+    """The fmaheavy pipe's multiply rate: 148 SMs x 4 SMSPs x 8 lanes per clock (one warp
+    IMAD.WIDE.U32 per 4 cycles, profiles/r01_philox_ceiling.txt, B300_MICROARCH IMAD rate / 2)."""
+    return SM_COUNT * 4 * 8 * sm_mhz * 1e6
+
+
 def _imad_ceiling(sm_mhz: float) -> float:
     """Trial-tokens/s if the fmaheavy pipe did nothing but Philox multiplies: 148 SMs x 4 SMSPs,
     one warp IMAD.WIDE per 4 cycles, 16 per Philox call of 4 tokens (rounds 2-9)."""
@@ -410,6 +426,7 @@ def ours(args):
     peak_instr = SM_COUNT * LANES_PER_SM_CLK * sm_max * 1e6  # thread-instr/s per GPU
     # dominant kernel = the trial kernel; algorithmic instructions of this rank's share
     achieved = alg_instructions(cfgs) / world / (kern_ms / 1000.0)
+    mults = alg_multiplies(cfgs) / world  # this rank's share
     clk = clocks.summary()
     prof = {}
     try:
@@ -434,21 +451,32 @@ def ours(args):
                        "configs": int(cfgs.size), "trials": int(cfgs["n_trials"].sum()),
                        "trial_tokens_per_step": tt, "tick": tick, "seed": W.SEED,
                        "l2": "flushed between timed steps (256 MiB memset)", "parallelism": f"dp{world}"},
-            "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_instr / 1e9,
-                         "unit": "Ginstr/s", "frac": achieved / peak_instr, "traffic": traffic,
+            # the unit that binds in ncu is the fmaheavy pipe (89.9% busy, profiles/*_ncu_summary.json),
+            # where Philox's 32x32->64 multiplies (IMAD.WIDE.U32) take 4 cycles per warp instruction;
+            # algorithmic work = the multiplies Philox4x32-10 defines (20 per 4 indicators; the kernel
+            # executes 16 of them per call after hoisting rounds 0-1)
+            "roofline": {"bound": "alu", "achieved": mults / (kern_ms / 1000.0) / 1e9,
+                         "peak": mul_peak(sm_max) / 1e9, "unit": "Gmul/s",
+                         "frac": mults / (kern_ms / 1000.0) / mul_peak(sm_max), "traffic": traffic,
                          "kernel": "dsi_trial_kernel", "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / (total_ms / args.steps),
-                         "peak_source": f"148 SM x 4 SMSP x 32 lanes x sm_max_mhz {sm_max:.0f} "
-                                        "(MEASURED_PEAKS.json) = issue slots; algorithmic "
-                                        "instructions per trial-token 11 + 10(1-a)",
-                         "frac_at_measured_clock": (achieved / (peak_instr * clk["sm_mhz"] / sm_max)
+                         "peak_source": f"fmaheavy pipe: 148 SM x 4 SMSP x 8 lanes/clk (one warp IMAD.WIDE "
+                                        f"per 4 cycles, measured, profiles/r01_philox_ceiling.txt) x sm_max_mhz "
+                                        f"{sm_max:.0f} (MEASURED_PEAKS.json)",
+                         "work": "Philox4x32-10: 20 multiplies per call of 4 indicators, ceil((N-1)/4) calls "
+                                 "per trial, configs with 0 < a < 1",
+                         "frac_at_measured_clock": (mults / (kern_ms / 1000.0) /
+                                                    (mul_peak(sm_max) * clk["sm_mhz"] / sm_max)
                                                     if clk.get("sm_mhz") else None),
-                         # the unit that binds in ncu: Philox's 32x32->64 multiplies (IMAD.WIDE,
-                         # 4 fmaheavy cycles per warp instruction, profiles/r01_philox_ceiling.txt);
-                         # 16 of them per 4 trial-tokens after hoisting rounds 0-1
-                         "pipe_bound": {"pipe": "fmaheavy (IMAD.WIDE.U32)",
-                                        "ceiling_trial_tokens_per_s": _imad_ceiling(sm_max),
-                                        "frac": (tt / world / (kern_ms / 1000.0)) / _imad_ceiling(sm_max)}},
+                         "issue_slots": {"achieved": achieved / 1e9, "peak": peak_instr / 1e9,
+                                         "unit": "Ginstr/s", "frac": achieved / peak_instr,
+                                         "work": "11 + 10(1-a) thread-instructions per trial-token "
+                                                 "(SURVEY 8(d).4)",
+                                         "peak_source": "148 SM x 4 SMSP x 32 lanes x sm_max_mhz"},
+                         "trial_tokens_ceiling": {
+                             "pipe": "fmaheavy, 16 IMAD.WIDE per call executed",
+                             "ceiling_trial_tokens_per_s": _imad_ceiling(sm_max),
+                             "frac": (tt / world / (kern_ms / 1000.0)) / _imad_ceiling(sm_max)}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches,
