@@ -193,29 +193,69 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle baseline
-def run_oracle_sample(cfgs, tick, seconds: float):
+def _oracle_sample_configs(cfgs, tick):
     import oracle as O
 
     sub = W.subsample(cfgs, 100)
     ocfgs = [O.Config(O.ticks(float(r["t_target"]), tick), O.ticks(float(r["t_drafter"]), tick),
                       float(r["accept_rate"]), int(r["lookahead"]), int(r["sp_degree"]),
                       int(r["n_tokens"]), int(r["stream_id"])) for r in sub]
-    # calibrate: 2 trials of each sampled config
-    t0 = time.perf_counter()
+    return sub, ocfgs
+
+
+def _oracle_worker(job):
+    """One host process of the multi-process oracle timing: trials [first, first + S) of every
+    sampled config, started at a common wall-clock instant."""
+    import oracle as O
+
+    ocfgs, S, first, start_at = job
+    O.run(ocfgs[0], W.SEED, first, 1, per_trial=False)  # load the library before the start
+    while time.time() < start_at:
+        time.sleep(0.001)
+    t0 = time.time()
+    tt = 0
+    for c in ocfgs:
+        O.run(c, W.SEED, first, S, per_trial=False)
+        tt += S * c.n_tokens
+    return tt, t0, time.time()
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_oracle_sample(cfgs, tick, seconds: float, processes: int = 1):
+    """The oracle as it stands (single-threaded C) on a bounded sample of the workload: the
+    first S trials of 100 evenly spaced configs, S sized to ~`seconds` of work per process.
+    processes > 1: that many independent host processes, each on its own trial range of the
+    same configs, started together; value = all their trial-tokens / the common wall time."""
+    import oracle as O
+
+    sub, ocfgs = _oracle_sample_configs(cfgs, tick)
+    t0 = time.perf_counter()  # calibrate: 2 trials of each sampled config
     for c in ocfgs:
         O.run(c, W.SEED, 0, 2, per_trial=False)
     per_trial = (time.perf_counter() - t0) / (2 * len(ocfgs))
-    S = int(max(1, min(min(int(r["n_trials"]) for r in sub), seconds / (per_trial * len(ocfgs)))))
-    t0 = time.perf_counter()
-    tt = 0
-    for c, r in zip(ocfgs, sub):
-        O.run(c, W.SEED, 0, S, per_trial=False)
-        tt += S * int(r["n_tokens"])
-    dt = time.perf_counter() - t0
-    return {"value": tt / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {S} trials of {len(ocfgs)} evenly spaced configs of the workload "
-                      f"({tt} trial-tokens, {dt:.1f} s, single-threaded C oracle: literal SI loop + "
-                      f"DSI event simulation)"}
+    S = int(max(1, min(min(int(r["n_trials"]) for r in sub) // max(1, processes),
+                       seconds / (per_trial * len(ocfgs)))))
+    if processes <= 1:
+        tt, a, b = _oracle_worker((ocfgs, S, 0, 0.0))
+        dt = b - a
+    else:
+        import multiprocessing as mp
+
+        start_at = time.time() + 2.0 + 0.05 * processes
+        with mp.get_context("spawn").Pool(processes) as pool:
+            res = pool.map(_oracle_worker, [(ocfgs, S, w * S, start_at) for w in range(processes)])
+        tt = sum(r[0] for r in res)
+        dt = max(r[2] for r in res) - min(r[1] for r in res)
+    return {"value": tt / dt, "unit": UNIT, "cores": processes, "kind": "oracle",
+            "sample": f"first {S} trials of {len(ocfgs)} evenly spaced configs of the workload per process, "
+                      f"{processes} process(es) on distinct trial ranges ({tt} trial-tokens, {dt:.1f} s; "
+                      f"single-threaded C oracle: literal SI loop + DSI event simulation)"}
 
 
 def reference_arm(args):
@@ -226,13 +266,14 @@ def reference_arm(args):
     O.build()
     cfgs, tick = workload(args.workload, _min_lookahead_plain)
     per_step = max(1.0, args.reference_seconds / max(1, args.steps + args.warmup))
+    procs = host_cores()
     for _ in range(args.warmup):
-        run_oracle_sample(cfgs, tick, per_step / 4)
+        run_oracle_sample(cfgs, tick, per_step / 4, procs)
     vals = []
     t0 = time.perf_counter()
     last = None
     for _ in range(args.steps):
-        last = run_oracle_sample(cfgs, tick, per_step)
+        last = run_oracle_sample(cfgs, tick, per_step, procs)
         vals.append(last["value"])
     wall = time.perf_counter() - t0
     value = statistics.mean(vals)
@@ -240,7 +281,7 @@ def reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * wall / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/int64",
             "data": "synthetic", "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload]},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle",
                              "sample": last["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -440,7 +481,9 @@ def ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O
         O.build()
-        cpu = run_oracle_sample(cfgs, tick, args.cpu_seconds)
+        cpu = run_oracle_sample(cfgs, tick, args.cpu_seconds / 2, host_cores())
+        one = run_oracle_sample(cfgs, tick, args.cpu_seconds / 2, 1)
+        cpu["single_core"] = {"value": one["value"], "cores": 1, "sample": one["sample"]}
 
     if rank == 0:
         line = {
