@@ -14,6 +14,7 @@ for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST, D.DSI_F_SHARED_STREAMS, FRESH
               FRESH | D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
     with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
+        sim.heatmap()  # the on-device heatmap product
 ttft, ttick = W.cfg2_ttft(trials=50)  # the TTFT variant (first-segment tables)
 for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
     with D.Simulator(ttft[:6], tick=ttick, seed=W.SEED, flags=flags) as sim:
