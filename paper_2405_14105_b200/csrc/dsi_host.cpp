@@ -1161,6 +1161,7 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   {
     const int e = dsi::launch_check_trials(d0.d_cfg, src, n_cfg, d0.d_heat_bad, d0.stream);
     if (e) return cuda_fail(h, (cudaError_t)e, "partition check launch");
+    h->launches += 1;
   }
   CUDA_TRY(h, cudaMemcpyAsync(h->host_bad.p, d0.d_heat_bad, sizeof(unsigned int), cudaMemcpyDeviceToHost,
                               d0.stream));
@@ -1297,6 +1298,7 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
   p.bad = d0.d_heat_bad;
   const int e = dsi::launch_heatmap_kernel(p, d0.stream);
   if (e) return cuda_fail(h, (cudaError_t)e, "heatmap kernel launch");
+  h->launches += 1;
   unsigned int bad = 0;
   CUDA_TRY(h, cudaMemcpyAsync(h->heat_out.p, d0.d_heat_out, nc * sizeof(dsi::HeatOut), cudaMemcpyDeviceToHost,
                               d0.stream));

@@ -147,7 +147,7 @@ def test_shard_and_block_invariance():
         for i in range(cfgs.size):
             assert_trials_equal(sim.trials(i), base_tr[i], ctx=str(kw))
         if kw.get("n_shards", 1) > 1:
-            assert sim.launches() == kw["n_shards"]
+            assert sim.launches() == kw["n_shards"] + 1  # + the reduce's partition check
         sim.close()
     base_sim.close()
 
