@@ -4,7 +4,7 @@
     python -m paper_2405_14105_b200 simulate --t-target 20.6 --t-drafter 6.8 --accept 0.93 \
         --lookahead 5 --sp 7 --n-tokens 50 --trials 100000 --tick 0.1
     python -m paper_2405_14105_b200 table2 [--trials 100000] [--sp 8] [--n-tokens 100]
-    python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200] [--csv out.csv] [--shared|--fresh]
+    python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200 | --k 5] [--csv out.csv] [--shared|--fresh]
 
 `plan` is Eq. 1; `table2` evaluates the Table 2 (target, drafter, acceptance)
 rows offline with lookahead in {1, 5, 10}, SI over all of them and DSI over the
@@ -66,7 +66,10 @@ def cmd_table2(a) -> list:
 
 
 def cmd_heatmap(a) -> dict:
-    cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
+    if a.k:  # one lookahead for SI and DSI: the static panels of Fig. 5
+        cfgs, tick = W.cfg3(trials=a.trials, k_min=a.k, k_max=a.k, sp=a.sp, n_tokens=a.n_tokens)
+    else:
+        cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
     flags = (D.DSI_F_SHARED_STREAMS if a.shared else 0) | (D.DSI_F_FRESH_VERIFIER if a.fresh else 0)
     with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags) as sim:
         cells = sim.run().heatmap()
@@ -109,6 +112,7 @@ def main(argv=None) -> int:
     p = sub.add_parser("heatmap", help="Fig. 3 grid; optional CSV")
     p.add_argument("--trials", type=int, default=10_000)
     p.add_argument("--k-max", type=int, default=200)
+    p.add_argument("--k", type=int, default=0, help="a single lookahead (Fig. 5 uses 5; with --fresh)")
     p.add_argument("--sp", type=int, default=7)
     p.add_argument("--n-tokens", type=int, default=100)
     p.add_argument("--csv", default=None)

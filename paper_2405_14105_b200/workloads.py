@@ -91,11 +91,12 @@ def heatmap_axes():
 
 
 def cfg3(trials: int = 10_000, k_max: int = 200, sp: int = 7, n_tokens: int = 100,
-         cells: slice | None = None):
-    """BASELINE configs[2]: the heatmap, every (t_d, a, k) point; order t_d-major, then a, then k."""
+         cells: slice | None = None, k_min: int = 1):
+    """BASELINE configs[2]: the heatmap, every (t_d, a, k) point; order t_d-major, then a, then k.
+    k_min = k_max = 5 gives the static-lookahead panels of Fig. 5."""
     t_d, acc = heatmap_axes()
     n_cells = t_d.size * acc.size
-    ks = np.arange(1, k_max + 1, dtype=np.int32)
+    ks = np.arange(k_min, k_max + 1, dtype=np.int32)
     cell_idx = np.arange(n_cells)
     if cells is not None:
         cell_idx = cell_idx[cells]

@@ -88,9 +88,10 @@ def pattern_index(A):
     return sum(int(v) << i for i, v in enumerate(A))
 
 
-def expectations_grid_f64(N, t_t, t_ds, ks, sp, ps):
+def expectations_grid_f64(N, t_t, t_ds, ks, sp, ps, fresh=False):
     """Exact E[L_SI], E[L_DSI] (float64) for every (p, t_d, k) of a grid: the same h(g)
-    and C(g) formulas as above, vectorised with numpy.  Shapes (len(ps), len(t_ds), len(ks))."""
+    and C(g) (or, fresh=True, C_fresh(g)) formulas as above, vectorised with numpy.
+    Shapes (len(ps), len(t_ds), len(ks))."""
     import numpy as np
     g = np.arange(1, N + 1, dtype=np.float64)
     ps = np.asarray(ps, dtype=np.float64)
@@ -107,6 +108,12 @@ def expectations_grid_f64(N, t_t, t_ds, ks, sp, ps):
     KD = ks[None, :, None] * t_ds[:, None, None]                # (t_d, k, 1)
     S = np.maximum(b[None] * KD, (b[None] % sp) * KD + (b[None] // sp) * t_t)
     C = (t_t + S).astype(np.float64)                            # (t_d, k, g)
+    if fresh:  # C_fresh where k t_d > t_t (block b, offset j; see C_fresh)
+        j = gi[None, :] - 1 - (b - 1) * ks[:, None]             # (k, g)
+        TD = t_ds[:, None, None]
+        Cf = t_t + (b[None] - 1) * KD + np.minimum(KD, t_t * (-(-(j[None] * TD) // t_t)))
+        act = (KD > t_t) & (gi[None, None, :] >= 2)
+        C = np.where(act, Cf, C).astype(np.float64)
     e_dsi = np.einsum("pg,dkg->pdk", H, C)
     e_i = np.einsum("pg,kg->pk", H, iters.astype(np.float64))   # (p, k)
     e_si = e_i[:, None, :] * (KD[None, :, :, 0] + t_t)

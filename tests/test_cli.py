@@ -98,3 +98,20 @@ def test_simulate_fresh_verifier_cli():
     assert base["mean_dsi"] > base["mean_nonsi"]          # R5: E[non-SI]/E[DSI] = 0.18
     assert fresh["n_dsi_gt_nonsi"] == 0 and fresh["mean_dsi"] <= fresh["mean_nonsi"]
     assert fresh["sum_si_ticks"] == base["sum_si_ticks"]   # SI is unchanged
+
+
+@pytest.mark.gpu
+def test_fig5_static_lookahead_monte_carlo(tmp_path):
+    """Fig. 5 by Monte Carlo through the CLI: lookahead 5, fresh-verifier DSI.
+    DSI is never slower than non-SI (per trial, so exactly in the means) and not slower than
+    SI beyond Monte Carlo noise; SI is slower than non-SI on about 7266 cells (exact count)."""
+    path = tmp_path / "fig5.csv"
+    rc, out, err = run_cli("heatmap", "--trials", "4000", "--k", "5", "--fresh", "--csv", str(path))
+    assert rc == 0, err
+    rows = np.genfromtxt(path, delimiter=",", skip_header=2)
+    r_nonsi_si, r_si_dsi, r_nonsi_dsi = rows[:, 7], rows[:, 8], rows[:, 9]
+    ok = ~np.isnan(r_nonsi_dsi)  # t_d in {0.01, 0.02}: Eq. 1 fails at k = 5, SP = 7 (no DSI value)
+    assert ok.sum() == 10100 - 2 * 101
+    assert np.all(r_nonsi_dsi[ok] >= 1.0)
+    assert np.all(r_si_dsi[ok] >= 0.99)
+    assert abs(int(np.sum(r_nonsi_si < 1.0)) - 7266) < 150

@@ -111,3 +111,34 @@ def test_fig3bcd_dsi_never_slower(full_grid):
     assert abs(cells["r_min_dsi"][i] - 1.528) < 0.001
     assert np.isclose(cells["t_drafter"][i], 0.15) and np.isclose(cells["accept_rate"][i], 0.91)
     assert cells["si_lookahead"][i] == 8 and cells["dsi_lookahead"][i] == 1
+
+
+def test_fresh_grid_matches_scalar_closed_form():
+    e_si, e_dsi = X.expectations_grid_f64(40, 100, [7, 30, 100], [1, 5, 20], 3, [0.0, 0.6, 1.0], fresh=True)
+    for ip, p in enumerate([0, Fraction(3, 5), 1]):
+        for idd, td in enumerate([7, 30, 100]):
+            for ik, k in enumerate([1, 5, 20]):
+                e = X.expectations_fresh(40, k, td, 100, 3, p)
+                assert abs(e_dsi[ip, idd, ik] - float(e["dsi"])) < 1e-9 * float(e["dsi"])
+
+
+def test_fig5_static_lookahead_needs_the_fresh_verifier():
+    """App. F.5 / Fig. 5: with SI and DSI at lookahead 5 (N = 100, SP = 7),
+    "SI is slower than non-SI when the drafter is either slow or inaccurate enough" and
+    "DSI is never slower than either SI or non-SI".  Exact expectations on all 10 100 cells:
+    the fresh-verifier variant (R24) meets both claims everywhere; the default
+    model (R5) is slower than non-SI on 5497 cells, all with k t_d > t_t."""
+    t_d = np.arange(1, 101)
+    ps = np.arange(0, 101) / 100
+    non = 100 * 100.0
+    for fresh in (False, True):
+        e_si, e_dsi = X.expectations_grid_f64(100, 100, t_d, [5], 7, ps, fresh=fresh)
+        e_si, e_dsi = e_si[:, :, 0], e_dsi[:, :, 0]
+        assert int(np.sum(e_si > non * (1 + 1e-12))) == 7266            # Fig. 5(a) pink cells
+        assert np.all(e_dsi <= e_si * (1 + 1e-12))                       # Fig. 5(b)
+        slower = e_dsi > non * (1 + 1e-12)                               # Fig. 5(c)
+        if fresh:
+            assert not slower.any()
+        else:
+            assert int(slower.sum()) == 5497
+            assert np.all(5 * t_d[np.nonzero(slower)[1]] > 100)
