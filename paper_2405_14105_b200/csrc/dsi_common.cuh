@@ -62,23 +62,24 @@ __device__ __forceinline__ Word4 philox_call(const uint4 &u, const TrialHalf &t,
 }
 
 // rej = (rej << 4) | [w >= thr] << 3 | [z >= thr] << 2 | [y >= thr] << 1 | [x >= thr]
-// from the carries of u + (2^32 - thr) (thr >= 1): 2 ALU instructions per bit.
+// from the carries of u + (2^32 - thr) (thr >= 1): 2 instructions per bit (IADD3 + IMAD.X).
 __device__ __forceinline__ uint32_t pack4(uint32_t rej, const Word4 &u, uint32_t nthr) {
   // (measured, profiles/r01_ab_pack.jsonl: compare + select packing was 6% slower; the
   //  carry as the majority bit of (u, n, u + n) funnel-shifted in, all on the ALU pipe, 16%
   //  slower for 4 bits and 8% for 2 of the 4: the IMAD.X half of addc is the cheaper pipe)
-  uint32_t t;
-  asm("add.cc.u32 %1, %2, %6;\n\t"
+  asm("{\n\t"
+      ".reg .u32 t;\n\t"
+      "add.cc.u32 t, %1, %5;\n\t"
       "addc.u32 %0, %0, %0;\n\t"
-      "add.cc.u32 %1, %3, %6;\n\t"
+      "add.cc.u32 t, %2, %5;\n\t"
       "addc.u32 %0, %0, %0;\n\t"
-      "add.cc.u32 %1, %4, %6;\n\t"
+      "add.cc.u32 t, %3, %5;\n\t"
       "addc.u32 %0, %0, %0;\n\t"
-      "add.cc.u32 %1, %5, %6;\n\t"
-      "addc.u32 %0, %0, %0;"
-      : "+r"(rej), "=&r"(t)
+      "add.cc.u32 t, %4, %5;\n\t"
+      "addc.u32 %0, %0, %0;\n\t"
+      "}"
+      : "+r"(rej)
       : "r"(u.w), "r"(u.z), "r"(u.y), "r"(u.x), "r"(nthr));
-  (void)t;
   return rej;
 }
 
