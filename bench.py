@@ -193,10 +193,10 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle baseline
-def _oracle_sample_configs(cfgs, tick):
+def _oracle_sample_configs(cfgs, tick, n=100):
     import oracle as O
 
-    sub = W.subsample(cfgs, 100)
+    sub = W.subsample(cfgs, n)
     ocfgs = [O.Config(O.ticks(float(r["t_target"]), tick), O.ticks(float(r["t_drafter"]), tick),
                       float(r["accept_rate"]), int(r["lookahead"]), int(r["sp_degree"]),
                       int(r["n_tokens"]), int(r["stream_id"])) for r in sub]
@@ -229,18 +229,19 @@ def host_cores() -> int:
 
 def run_oracle_sample(cfgs, tick, seconds: float, processes: int = 1):
     """The oracle as it stands (single-threaded C) on a bounded sample of the workload: the
-    first S trials of 100 evenly spaced configs, S sized to ~`seconds` of work per process.
-    processes > 1: that many independent host processes, each on its own trial range of the
-    same configs, started together; value = all their trial-tokens / the common wall time."""
+    first S trials of 100 evenly spaced configs per process, S sized to ~`seconds` of work.
+    processes > 1: that many independent host processes on disjoint interleaved subsets of
+    100 x processes evenly spaced configs, started together; value = all their trial-tokens
+    / the common wall time."""
     import oracle as O
 
-    sub, ocfgs = _oracle_sample_configs(cfgs, tick)
-    t0 = time.perf_counter()  # calibrate: 2 trials of each sampled config
-    for c in ocfgs:
+    sub, ocfgs = _oracle_sample_configs(cfgs, tick, 100 * processes)
+    probe = ocfgs[::processes]
+    t0 = time.perf_counter()  # calibrate: 2 trials of each config of one process's share
+    for c in probe:
         O.run(c, W.SEED, 0, 2, per_trial=False)
-    per_trial = (time.perf_counter() - t0) / (2 * len(ocfgs))
-    S = int(max(1, min(min(int(r["n_trials"]) for r in sub) // max(1, processes),
-                       seconds / (per_trial * len(ocfgs)))))
+    per_trial = (time.perf_counter() - t0) / (2 * len(probe))
+    S = int(max(1, min(int(sub["n_trials"].min()), seconds / (per_trial * len(probe)))))
     if processes <= 1:
         tt, a, b = _oracle_worker((ocfgs, S, 0, 0.0))
         dt = b - a
@@ -249,13 +250,13 @@ def run_oracle_sample(cfgs, tick, seconds: float, processes: int = 1):
 
         start_at = time.time() + 2.0 + 0.05 * processes
         with mp.get_context("spawn").Pool(processes) as pool:
-            res = pool.map(_oracle_worker, [(ocfgs, S, w * S, start_at) for w in range(processes)])
+            res = pool.map(_oracle_worker, [(ocfgs[w::processes], S, 0, start_at) for w in range(processes)])
         tt = sum(r[0] for r in res)
         dt = max(r[2] for r in res) - min(r[1] for r in res)
     return {"value": tt / dt, "unit": UNIT, "cores": processes, "kind": "oracle",
-            "sample": f"first {S} trials of {len(ocfgs)} evenly spaced configs of the workload per process, "
-                      f"{processes} process(es) on distinct trial ranges ({tt} trial-tokens, {dt:.1f} s; "
-                      f"single-threaded C oracle: literal SI loop + DSI event simulation)"}
+            "sample": f"first {S} trials of {len(ocfgs)} evenly spaced configs of the workload, "
+                      f"{processes} process(es) on disjoint config subsets ({tt} trial-tokens, {dt:.1f} s "
+                      f"wall; single-threaded C oracle: literal SI loop + DSI event simulation)"}
 
 
 def reference_arm(args):
