@@ -27,8 +27,6 @@
 namespace dsi {
 namespace {
 
-constexpr int CRN_THREADS = 128;
-
 struct CfgLite {  // what phase 2 needs of a config (shared memory, 48 B)
   int32_t t_t, s1, si_cost, k_eff;
   uint32_t m_si, m_k_lo, m_k_hi, m_sp_lo;
@@ -49,8 +47,11 @@ __device__ __forceinline__ void long_run(int L, const CfgLite &l, int &ai, int &
   ay += S - l.s1;
 }
 
-template <int CPT>
-__global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P) {
+// TH threads per block = trials per tile = configs per block (CPT = 1: 2 or 4 configs per
+// thread measured slower, profiles/r01_ab_crn_cpt_unroll.jsonl)
+template <int TH, int CPT>
+__global__ void __launch_bounds__(TH) dsi_crn_kernel(const CrnParams P) {
+  constexpr int CRN_THREADS = TH;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_bsum[5];
   const CrnUnit un = P.units[P.unit_begin + blockIdx.x];
@@ -314,11 +315,11 @@ __global__ void __launch_bounds__(CRN_THREADS) dsi_crn_kernel(const CrnParams P)
   }
 }
 
-template <int CPT>
-int launch_cpt(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st) {
+template <int TH>
+int launch_th(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
     const cudaError_t e =
-        cudaFuncSetAttribute(dsi_crn_kernel<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(dsi_crn_kernel<TH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
   const uint64_t max_grid = 0x7fffffffull;
@@ -326,7 +327,7 @@ int launch_cpt(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t s
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_crn_kernel<CPT><<<(unsigned)n, CRN_THREADS, smem, st>>>(q);
+    dsi_crn_kernel<TH, 1><<<(unsigned)n, TH, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
@@ -345,13 +346,12 @@ size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_
 
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream) {
   if (n_units == 0) return 0;
-  if (block_threads != CRN_THREADS) return (int)cudaErrorInvalidValue;
+  if (p.cfg_per_block != block_threads) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = crn_kernel_smem(p.max_n, CRN_THREADS, p.cfg_per_block, p.max_runs);
-  switch (p.cfg_per_block / CRN_THREADS) {
-    case 1: return launch_cpt<1>(p, n_units, smem, st);
-    case 2: return launch_cpt<2>(p, n_units, smem, st);
-    case 4: return launch_cpt<4>(p, n_units, smem, st);
+  const size_t smem = crn_kernel_smem(p.max_n, block_threads, p.cfg_per_block, p.max_runs);
+  switch (block_threads) {
+    case 128: return launch_th<128>(p, n_units, smem, st);
+    case 256: return launch_th<256>(p, n_units, smem, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }

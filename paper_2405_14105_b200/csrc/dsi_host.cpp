@@ -36,7 +36,7 @@ thread_local std::string g_create_error;
 constexpr int kMaxTokens = 32768;  // keeps every magic division exact (x * d <= 2^32)
 constexpr uint64_t kMaxTrials = 1ull << 32;
 constexpr int kDefaultThreads = 128;
-constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size (launch bounds)
+constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size when 256 does not fit (see plan_shared)
 constexpr size_t kReduceChunks = 8;  // dsi_sim_reduce: D2H chunks overlapped with the finalize
 constexpr int kCrnMaxN = 2048;     // shared-stream mode: 128 per-trial run lists of <= N/3+2
                                    // u16 entries fit shared memory (209 KB at N 2048)
@@ -642,13 +642,20 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
       h->groups.push_back(g);
       i = j;
     }
-    // one config per thread: 2 or 4 per thread (more Philox reuse, more registers) measured
-    // equal or slower on cfg3/cfg4/cfg5 (profiles/r01_ab_crn*.jsonl)
-    h->cfg_per_block = kCrnThreads;
-    if (const char *force = std::getenv("DSI_CRN_CPT")) {  // developer A/B runs only
-      const int cpt = std::atoi(force);
-      if (cpt == 1 || cpt == 2 || cpt == 4) h->cfg_per_block = cpt * kCrnThreads;
+    // one config per thread, one trial per thread per tile; 256-thread blocks halve the
+    // phase-1 (Philox) passes per trial of a group -- worth it when groups are large (>= 256
+    // configs on average) and the shared memory still leaves room for 4 blocks per SM; else
+    // 128 (profiles/r01_ab_crn_th.jsonl: cfg3 30.5 -> 26.0 ms; forced on cfg2/cfg4/cfg5, whose
+    // groups hold 3 / 140 / 100 configs, 1.8-1.9x slower; 2 or 4 configs per thread were
+    // slower too, profiles/r01_ab_crn*.jsonl)
+    const bool big_groups = n >= 256 * h->groups.size();
+    int th = (big_groups && dsi::crn_kernel_smem(h->max_n, 256, 256, h->max_runs) <= 48 * 1024) ? 256 : kCrnThreads;
+    if (const char *force = std::getenv("DSI_CRN_THREADS")) {  // developer A/B runs only
+      const int f = std::atoi(force);
+      if (f == 128 || f == 256) th = f;
     }
+    h->cfg_per_block = th;
+    h->block_threads = th;
     // units: (group, slice of cfg_per_block configs, range of trials); trials are split
     // until there are enough blocks to fill every SM of every device a few times
     size_t slices = 0;
@@ -660,7 +667,7 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
     cost.clear();
     for (uint32_t gi = 0; gi < h->groups.size(); ++gi) {
       const dsi::CrnGroup &g = h->groups[gi];
-      const uint64_t tiles = (g.n_trials + kCrnThreads - 1) / kCrnThreads;
+      const uint64_t tiles = (g.n_trials + th - 1) / th;
       const uint64_t nchunks = std::min<uint64_t>(split, tiles);
       for (uint32_t b = g.first; b < g.first + g.count; b += (uint32_t)h->cfg_per_block) {
         const uint32_t cnt = std::min<uint32_t>((uint32_t)h->cfg_per_block, g.first + g.count - b);
@@ -669,8 +676,8 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
           u.group = gi;
           u.begin = b;
           u.count = cnt;
-          u.t0 = (tiles * c / nchunks) * kCrnThreads;
-          u.t1 = std::min<uint64_t>((tiles * (c + 1) / nchunks) * kCrnThreads, g.n_trials);
+          u.t0 = (tiles * c / nchunks) * th;
+          u.t1 = std::min<uint64_t>((tiles * (c + 1) / nchunks) * th, g.n_trials);
           h->crn_units.push_back(u);
           // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
           cost.push_back((double)(u.t1 - u.t0) * ((double)g.n_tokens * 12.0 + (double)cnt * 25.0));
@@ -1120,7 +1127,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       for (const auto &rg : d.ranges) {
         if (rg.second <= rg.first) continue;
         q.unit_begin = rg.first;
-        const int e = dsi::launch_crn_kernel(q, rg.second - rg.first, kCrnThreads, d.stream);
+        const int e = dsi::launch_crn_kernel(q, rg.second - rg.first, h->cfg_per_block, d.stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
         h->launches += 1;
       }
