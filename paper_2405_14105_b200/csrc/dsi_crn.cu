@@ -22,30 +22,11 @@
 #include <stdint.h>
 
 #include "dsi_common.cuh"
+#include "dsi_crn_common.cuh"
 #include "dsi_device.h"
 
 namespace dsi {
 namespace {
-
-struct CfgLite {  // what phase 2 needs of a config (shared memory, 48 B)
-  int32_t t_t, s1, si_cost, k_eff;
-  uint32_t m_si, m_k_lo, m_k_hi, m_sp_lo;
-  uint32_t m_sp_hi;
-  int32_t kd, nonsi;
-  int16_t sp_eff, noqueue;  // noqueue: S(b) = b k t_d (CFG_NOQUEUE)
-};
-
-// Extra costs of a segment with L = g - 1 >= k + 1 accepted drafts (seg_long of the
-// per-config kernel): x = floor(L/(k+1)) SI iterations, y = S(ceil(L/k)) - S(1).
-__device__ __forceinline__ void long_run(int L, const CfgLite &l, int &ai, int &ay) {
-  const uint32_t x = magic_div((uint32_t)L, l.m_si, 0u);
-  const uint32_t b = magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
-  const uint32_t qq = magic_div(b, l.m_sp_lo, l.m_sp_hi);
-  const int rr = (int)b - (int)qq * l.sp_eff;
-  const int S = max((int)b * l.kd, rr * l.kd + (int)qq * l.t_t);
-  ai += (int)x;
-  ay += S - l.s1;
-}
 
 // TH threads per block = trials per tile = configs per block (CPT = 1: 2 or 4 configs per
 // thread measured slower, profiles/r01_ab_crn_cpt_unroll.jsonl)
@@ -85,26 +66,7 @@ __global__ void __launch_bounds__(TH) dsi_crn_kernel(const CrnParams P) {
   if (mode == MODE_STREAM)
     for (int q = threadIdx.x; q < nq; q += CRN_THREADS) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
   for (int j = threadIdx.x; j < CPT * CRN_THREADS; j += CRN_THREADS) {
-    CfgLite l{};
-    if (j < (int)un.count) {
-      const DevCfg c = P.cfg[P.perm[un.begin + j]];
-      l.t_t = c.t_t;
-      l.s1 = c.s1;
-      l.si_cost = c.si_cost;
-      l.k_eff = c.k_eff;
-      l.m_si = c.m_si;
-      l.m_k_lo = c.m_k_lo;
-      l.m_k_hi = c.m_k_hi;
-      l.m_sp_lo = c.m_sp_lo;
-      l.m_sp_hi = c.m_sp_hi;
-      l.kd = c.kd;
-      l.sp_eff = (int16_t)c.sp_eff;
-      l.noqueue = (c.flags & CFG_NOQUEUE) ? 1 : 0;
-      l.nonsi = N * c.t_t;
-    } else {
-      l.k_eff = 1 << 20;  // an empty slot: no run is ever long
-      l.m_sp_lo = 1u;
-    }
+    const CfgLite l = load_cfglite(P.cfg, P.perm, un, j, N);
     cl[j] = l;
     if (j < (int)un.count) atomicMin(&s_kmin, l.k_eff);
   }

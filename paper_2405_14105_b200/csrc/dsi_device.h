@@ -101,6 +101,10 @@ struct CrnUnit {       // one block: a slice of one group's configs over a range
   uint32_t pad;
   uint64_t t0, t1;     // trials [t0, t1)
 };
+struct CrnTile {       // two-pass mode, pass 1: one block per (group, tile of trials)
+  uint32_t group;
+  uint32_t tile;
+};
 struct CrnParams {
   const DevCfg *cfg;
   const uint32_t *perm;  // processing order of the configs (grouped, lookahead-major)
@@ -109,6 +113,12 @@ struct CrnParams {
   uint64_t unit_begin;
   unsigned long long *acc;  // n_cfg * NF, integer atomics (a config may span trial ranges)
   int32_t max_n, max_nq, max_runs, cfg_per_block;
+  // two-pass mode (dsi_crn2.cu): trial records written by pass 1, streamed by pass 2
+  unsigned char *records;      // record of (group g, tile t) at (group_tile0[g] + t) * rec_bytes
+  const uint64_t *group_tile0;
+  const CrnTile *tiles;        // pass-1 work list of this device
+  uint64_t tile_begin;
+  uint32_t rec_bytes;
   Keys keys;
 };
 // On-device heatmap product: one warp per cell, a cell being a run of
@@ -137,6 +147,10 @@ int launch_check_trials(const DevCfg *cfg, const unsigned long long *acc, uint64
                         void *stream);
 
 size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs);
+size_t crn_record_bytes(int max_runs, int threads);
+size_t crn_eval_smem(int max_runs, int threads);
+// pass 1 over n_tiles records (p.tiles from p.tile_begin), then pass 2 over n_units units
+int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, int threads, void *stream);
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream);
 
 // Dynamic shared memory of the variant chosen for (max_n, max_keff, hist).

@@ -135,6 +135,11 @@ struct DeviceState {
   uint32_t *d_perm = nullptr;            // shared-stream mode: processing order
   dsi::CrnGroup *d_groups = nullptr;     //   groups of configs sharing a stream
   dsi::CrnUnit *d_crn_units = nullptr;   //   one block per unit
+  unsigned char *d_records = nullptr;    //   two-pass mode: trial records (pass 1 -> pass 2)
+  uint64_t *d_group_tile0 = nullptr;
+  dsi::CrnTile *d_tiles = nullptr;       //   pass-1 work list of this device
+  size_t tiles_cap = 0, records_cap = 0;
+  std::vector<dsi::CrnTile> tiles;
   dsi::HeatCell *d_heat_cells = nullptr; // on-device heatmap product (device 0 only)
   dsi::HeatOut *d_heat_out = nullptr;
   unsigned int *d_heat_bad = nullptr;
@@ -164,6 +169,10 @@ struct dsi_sim {
   std::vector<dsi::CrnGroup> groups;
   std::vector<dsi::CrnUnit> crn_units;
   int32_t cfg_per_block = 0, max_runs = 0;
+  bool two_pass = false;                  // shared-stream mode in two passes (dsi_crn2.cu)
+  uint32_t rec_bytes = 0;
+  uint64_t total_records = 0;
+  std::vector<uint64_t> group_tile0;
   std::vector<DeviceState> dev;
   Pinned<unsigned long long> host_acc, host_seg, host_si;  // D2H targets
   bool ran = false, reduced = false;
@@ -483,6 +492,9 @@ void free_device(DeviceState &d) {
   cudaFree(d.d_perm);
   cudaFree(d.d_groups);
   cudaFree(d.d_crn_units);
+  cudaFree(d.d_records);
+  cudaFree(d.d_group_tile0);
+  cudaFree(d.d_tiles);
   cudaFree(d.d_heat_cells);
   cudaFree(d.d_heat_out);
   cudaFree(d.d_heat_bad);
@@ -519,6 +531,13 @@ dsi_status upload(dsi_sim *h, bool plan = true) {
       CUDA_TRY(h, cudaMemcpyAsync(d.d_crn_units, h->crn_units.data(),
                                   h->crn_units.size() * sizeof(dsi::CrnUnit), cudaMemcpyHostToDevice,
                                   d.stream));
+      if (h->two_pass) {
+        CUDA_TRY(h, cudaMemcpyAsync(d.d_group_tile0, h->group_tile0.data(), h->group_tile0.size() * sizeof(uint64_t),
+                                    cudaMemcpyHostToDevice, d.stream));
+        if (!d.tiles.empty())
+          CUDA_TRY(h, cudaMemcpyAsync(d.d_tiles, d.tiles.data(), d.tiles.size() * sizeof(dsi::CrnTile),
+                                      cudaMemcpyHostToDevice, d.stream));
+      }
       CUDA_TRY(h, cudaStreamSynchronize(d.stream));  // the host vectors are pageable and may change
     }
   }
@@ -600,6 +619,66 @@ dsi_status sum_across(dsi_sim *h, bool hist) {
   const ncclResult_t r2 = api.GroupEnd();
   if (r != ncclSuccess || r2 != ncclSuccess)
     return fail(h, DSI_E_COMM, std::string("ncclAllReduce: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
+  return DSI_OK;
+}
+
+// Two-pass shared-stream mode (dsi_crn2.cu): records of (group, tile of TH trials), and
+// for every device the tiles its units read (pass 1 writes exactly those).  Requires
+// h->crn_units and the devices' unit ranges.
+dsi_status plan_two_pass(dsi_sim *h) {
+  const int th = h->cfg_per_block;
+  h->two_pass = th == 256 && dsi::crn_eval_smem(h->max_runs, th) <= 76 * 1024;
+  if (const char *force = std::getenv("DSI_CRN_TWO_PASS"))  // developer A/B runs only
+    h->two_pass = h->two_pass && std::atoi(force) != 0;
+  if (!h->two_pass) return DSI_OK;
+  try {
+    h->rec_bytes = (uint32_t)dsi::crn_record_bytes(h->max_runs, th);
+    h->group_tile0.assign(h->groups.size() + 1, 0);
+    for (size_t g = 0; g < h->groups.size(); ++g)
+      h->group_tile0[g + 1] = h->group_tile0[g] + (h->groups[g].n_trials + th - 1) / th;
+    h->total_records = h->group_tile0.back();
+    for (auto &d : h->dev) {
+      std::vector<char> seen(h->total_records, 0);
+      d.tiles.clear();
+      for (const auto &rg : d.ranges)
+        for (uint64_t u = rg.first; u < rg.second; ++u) {
+          const dsi::CrnUnit &un = h->crn_units[u];
+          for (uint64_t t = un.t0 / th; t * th < un.t1; ++t) {
+            const uint64_t r = h->group_tile0[un.group] + t;
+            if (!seen[r]) {
+              seen[r] = 1;
+              d.tiles.push_back(dsi::CrnTile{un.group, (uint32_t)t});
+            }
+          }
+        }
+    }
+  } catch (...) {
+    return fail(h, DSI_E_NOMEM, "two-pass plan");
+  }
+  return DSI_OK;
+}
+
+// Device buffers of the two-pass mode (sized by plan_two_pass; grown if an update needs more).
+dsi_status alloc_two_pass(dsi_sim *h) {
+  if (!h->two_pass) return DSI_OK;
+  for (auto &d : h->dev) {
+    CUDA_TRY(h, cudaSetDevice(d.ordinal));
+    if (h->total_records > d.records_cap || !d.d_records) {
+      cudaFree(d.d_records);
+      cudaFree(d.d_group_tile0);
+      d.d_records = nullptr;
+      d.d_group_tile0 = nullptr;
+      CUDA_TRY(h, cudaMalloc((void **)&d.d_records, std::max<uint64_t>(1, h->total_records) * h->rec_bytes));
+      CUDA_TRY(h, cudaMalloc((void **)&d.d_group_tile0, h->group_tile0.size() * sizeof(uint64_t)));
+      d.records_cap = h->total_records;
+    }
+    if (d.tiles.size() > d.tiles_cap) {
+      cudaFree(d.d_tiles);
+      d.d_tiles = nullptr;
+      CUDA_TRY(h, cudaMalloc((void **)&d.d_tiles, d.tiles.size() * sizeof(dsi::CrnTile)));
+      d.tiles_cap = d.tiles.size();
+    }
+  }
   return DSI_OK;
 }
 
@@ -976,6 +1055,11 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       return abort_create(e == cudaErrorMemoryAllocation ? DSI_E_NOMEM : DSI_E_DEVICE);
     }
   }
+  if (shared) {
+    s = plan_two_pass(h);
+    if (s == DSI_OK) s = alloc_two_pass(h);
+    if (s != DSI_OK) return abort_create(s);
+  }
   s = upload(h);
   if (s != DSI_OK) return abort_create(s);
   for (auto &d : h->dev) {
@@ -1045,6 +1129,14 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     }
     if (s == DSI_OK && (h->groups.size() != old_groups.size() || h->crn_units.size() != old_units.size()))
       s = fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS: the stream grouping changed; create a new handle");
+    if (s == DSI_OK) s = plan_two_pass(h);
+    if (s == DSI_OK) {  // the buffers may grow: wait for any run still reading them
+      for (auto &d : h->dev) {
+        CUDA_TRY(h, cudaSetDevice(d.ordinal));
+        CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+      }
+      s = alloc_two_pass(h);
+    }
     if (s != DSI_OK) {  // the handle keeps its previous configs and plan
       if (!old_groups.empty()) {
         h->perm.swap(old_perm);
@@ -1053,7 +1145,11 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
       }
       h->cfg_per_block = old_cpb;
       h->max_runs = old_runs;
+      h->block_threads = old_cpb;
       h->ticks.swap(h->ticks_next);
+      const std::string msg = h->err;
+      plan_two_pass(h);  // the old plan's pass-1 lists (the buffers only ever grow)
+      h->err = msg;
       h->max_n = old_n;
       h->max_keff = old_keff;
       h->any_ttft = old_ttft;
@@ -1124,10 +1220,23 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       q.max_runs = h->max_runs;
       q.cfg_per_block = h->cfg_per_block;
       q.keys = p.keys;
+      if (h->two_pass) {
+        q.records = d.d_records;
+        q.group_tile0 = d.d_group_tile0;
+        q.tiles = d.d_tiles;
+        q.tile_begin = 0;
+        q.rec_bytes = h->rec_bytes;
+        if (!d.tiles.empty()) {  // pass 1: every record this device's units read
+          const int e = dsi::launch_crn_two_pass(q, d.tiles.size(), 0, h->cfg_per_block, d.stream);
+          if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream pass-1 launch");
+          h->launches += 1;
+        }
+      }
       for (const auto &rg : d.ranges) {
         if (rg.second <= rg.first) continue;
         q.unit_begin = rg.first;
-        const int e = dsi::launch_crn_kernel(q, rg.second - rg.first, h->cfg_per_block, d.stream);
+        const int e = h->two_pass ? dsi::launch_crn_two_pass(q, 0, rg.second - rg.first, h->cfg_per_block, d.stream)
+                                  : dsi::launch_crn_kernel(q, rg.second - rg.first, h->cfg_per_block, d.stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
         h->launches += 1;
       }
