@@ -164,6 +164,9 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
 
   const CfgLite l = cl[threadIdx.x];
   const bool fast = l.noqueue && l.k_eff == 1;  // every run is long; S(b) = b k t_d
+  // the lanes of a warp share k (lookahead-major order) and differ in t_d: where none of
+  // them queues, the long-run loop needs no SP division (warp-uniform, so no divergence)
+  const bool warp_noqueue = __all_sync(0xffffffffu, l.noqueue != 0);
   unsigned long long c_ai = 0, c_ai2 = 0, c_mai = 0, c_ay = 0, c_ay2 = 0, c_ydl = 0, a_gtn = 0, a_gts = 0;
   unsigned long long my_m = 0, my_n = 0, my_mm = 0, my_nn = 0, my_mn = 0;
   for (uint64_t ti = tile_a; ti < tile_b; ++ti) {
@@ -198,8 +201,18 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
         if (fast) {  // k = 1: ai = sum floor(L/2), ay = k t_d sum L - nr S(1)
           ai = (int)(v.w >> 21);
           ay = (int)((v.w >> 10) & 0x7ffu) * l.kd - nr * l.s1;
-        } else {
+        } else if (warp_noqueue) {  // S(b) = b k t_d: ay = k t_d sum ceil(L/k) - n S(1)
+          int sb = 0, cnt = 0;
           for (int r = 0; r < nr; ++r) {  // runs in decreasing order: stop at the first short one
+            const int L = runs[r * TH + s];
+            if (L <= l.k_eff) break;
+            ai += (int)magic_div((uint32_t)L, l.m_si, 0u);
+            sb += (int)magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
+            ++cnt;
+          }
+          ay = sb * l.kd - cnt * l.s1;
+        } else {
+          for (int r = 0; r < nr; ++r) {
             const int L = runs[r * TH + s];
             if (L <= l.k_eff) break;
             long_run(L, l, ai, ay);
