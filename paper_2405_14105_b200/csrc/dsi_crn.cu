@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(TH) dsi_crn_kernel(const CrnParams P) {
     __syncthreads();
   }
   // block sums of the config-independent terms
-  unsigned long long *bs = reinterpret_cast<unsigned long long *>(&s_bsum[0]);
   for (int o = 16; o > 0; o >>= 1) {
     my_m += __shfl_xor_sync(0xffffffffu, my_m, o);
     my_n += __shfl_xor_sync(0xffffffffu, my_n, o);
@@ -242,14 +241,14 @@ __global__ void __launch_bounds__(TH) dsi_crn_kernel(const CrnParams P) {
     my_mn += __shfl_xor_sync(0xffffffffu, my_mn, o);
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicAdd(bs + 0, my_m);
-    atomicAdd(bs + 1, my_n);
-    atomicAdd(bs + 2, my_mm);
-    atomicAdd(bs + 3, my_nn);
-    atomicAdd(bs + 4, my_mn);
+    atomicAdd(&s_bsum[0], my_m);
+    atomicAdd(&s_bsum[1], my_n);
+    atomicAdd(&s_bsum[2], my_mm);
+    atomicAdd(&s_bsum[3], my_nn);
+    atomicAdd(&s_bsum[4], my_mn);
   }
   __syncthreads();
-  const unsigned long long Sm = bs[0], Sn = bs[1], Smm = bs[2], Snn = bs[3], Smn = bs[4];
+  const unsigned long long Sm = s_bsum[0], Sn = s_bsum[1], Smm = s_bsum[2], Snn = s_bsum[3], Smn = s_bsum[4];
   // per config: assemble the moments (exact u64 arithmetic) and add them with one
   // 64-bit integer atomic per field (exact and order-free)
 #pragma unroll

@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
   const CrnUnit un = P.units[P.unit_begin + blockIdx.x];
   const CrnGroup G = P.groups[un.group];
   const int N = G.n_tokens;
-  unsigned char *buf[2] = {smem, smem + P.rec_bytes};
+  // buffer b of the two tile buffers is smem + b * rec_bytes (computed from the shared array
+  // itself, so the loads stay shared-memory loads)
   CfgLite *cl = reinterpret_cast<CfgLite *>(smem + 2 * (size_t)P.rec_bytes);
   if (threadIdx.x < 5) s_bsum[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) {
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
 
   const uint64_t tile_a = un.t0 / TH, tile_b = (un.t1 + TH - 1) / TH;  // un.t0 is tile-aligned
   const unsigned char *rec0 = P.records + (P.group_tile0[un.group] + tile_a) * (uint64_t)P.rec_bytes;
-  if (threadIdx.x == 0) bulk_load(buf[0], rec0, P.rec_bytes, &bar[0]);
+  if (threadIdx.x == 0) bulk_load(smem, rec0, P.rec_bytes, &bar[0]);
 
   const CfgLite l = cl[threadIdx.x];
   const bool fast = l.noqueue && l.k_eff == 1;  // every run is long; S(b) = b k t_d
@@ -174,11 +175,13 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
     if (threadIdx.x == 0 && ti + 1 < tile_b) {
       // the other buffer was last read in the previous iteration (ended by __syncthreads)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bulk_load(buf[cur ^ 1], rec0 + (ti + 1 - tile_a) * (uint64_t)P.rec_bytes, P.rec_bytes, &bar[cur ^ 1]);
+      bulk_load(smem + (size_t)(cur ^ 1) * P.rec_bytes, rec0 + (ti + 1 - tile_a) * (uint64_t)P.rec_bytes,
+                P.rec_bytes, &bar[cur ^ 1]);
     }
     mbar_wait(&bar[cur], (uint32_t)(((ti - tile_a) >> 1) & 1));
-    const uint4 *summ = reinterpret_cast<const uint4 *>(buf[cur]);
-    const uint16_t *runs = reinterpret_cast<const uint16_t *>(buf[cur] + (size_t)TH * sizeof(uint4));
+    const unsigned char *bufc = smem + (size_t)cur * P.rec_bytes;
+    const uint4 *summ = reinterpret_cast<const uint4 *>(bufc);
+    const uint16_t *runs = reinterpret_cast<const uint16_t *>(bufc + (size_t)TH * sizeof(uint4));
     const uint64_t tile0 = ti * TH;
     const int ntr = (int)(min(un.t1, tile0 + TH) - tile0);
     if ((int)threadIdx.x < ntr) {  // the config-independent block sums, one trial per thread
