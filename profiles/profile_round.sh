@@ -15,7 +15,7 @@ timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsi_trial_kernel -c 1 \
   -o gpurun_out/prof_${R} python profiles/ncu_driver.py --workload cfg3 --stride 20 \
   > gpurun_out/ncu_full_${R}.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsi_crn_kernel -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsi_crn -c 2 \
   -o gpurun_out/prof_crn_${R} python profiles/ncu_driver.py --workload cfg3 --stride 1 --shared \
   > gpurun_out/ncu_full_crn_${R}.log 2>&1
 echo done

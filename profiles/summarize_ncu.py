@@ -46,10 +46,13 @@ def dram():
     return d
 
 
-def hotspots(rep, top=15):
-    """Source lines by share of executed warp instructions and of stall samples."""
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
-                         capture_output=True, text=True).stdout
+def hotspots(rep, top=15, kernel=None):
+    """Source lines by share of executed warp instructions and of stall samples (of the
+    kernels matching `kernel`, an ncu -k filter, when given)."""
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"]
+    if kernel:
+        cmd[3:3] = ["-k", kernel]
+    src = subprocess.run(cmd, capture_output=True, text=True).stdout
     cur, hdr, out = None, None, []
     for r in csv.reader(io.StringIO(src)):
         if r and r[0] == "File Path":
@@ -69,14 +72,18 @@ def full(name=None):
     rep = os.path.join(OUT, f"{name or 'prof_' + R}.ncu-rep")
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    d = {h: (u, v) for h, u, v in zip(rows[0], rows[1], rows[2])}
+    # the longest kernel of the capture (the shared-stream capture holds pass 1 and pass 2)
+    it = rows[0].index("gpu__time_duration.sum")
+    main = max(rows[2:], key=lambda r: float(r[it].replace(",", "") or 0))
+    d = {h: (u, v) for h, u, v in zip(rows[0], rows[1], main)}
+    d["kernel"] = ("", main[rows[0].index("Kernel Name")]) if "Kernel Name" in rows[0] else ("", "")
     keys = ["gpu__time_duration.sum", "smsp__inst_executed.sum",
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__grid_size", "launch__block_size", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "sm__cycles_elapsed.avg.per_second"]
+            "sm__cycles_elapsed.avg.per_second", "kernel"]
     keys += [k for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
@@ -110,7 +117,9 @@ except (OSError, ValueError, IndexError) as e:
     out["full_error"] = str(e)
 try:  # the shared-stream kernel on the full cfg3 grid (profiles/profile_round.sh)
     out["set_full_crn"], out["instruction_mix_crn"] = full(f"prof_crn_{R}")
-    out["source_hotspots_crn"] = hotspots(os.path.join(OUT, f"prof_crn_{R}.ncu-rep"))
+    name = out["set_full_crn"].get("kernel", ("", ""))[1]
+    out["source_hotspots_crn"] = hotspots(os.path.join(OUT, f"prof_crn_{R}.ncu-rep"),
+                                          kernel="regex:eval" if "eval" in name else None)
 except (OSError, ValueError, IndexError) as e:
     out["crn_error"] = str(e)
 for name in (f"{R}_ncu_summary.json", "latest_ncu_summary.json"):
