@@ -85,16 +85,20 @@ def full(name=None):
             "launch__grid_size", "launch__block_size", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "sm__cycles_elapsed.avg.per_second", "kernel"]
     keys += [k for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    kname = d["kernel"][1]
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+    if "eval" in kname:
+        cmd[3:3] = ["-k", "regex:eval"]
+    src = subprocess.run(cmd, capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))
-    hdr = srows[1]
+    hdr = next(r for r in srows if "Instructions Executed" in r)
     iS, iE = hdr.index("Source"), hdr.index("Instructions Executed")
     ops = collections.Counter()
-    for r in srows[2:]:
-        if len(r) > iE and r[iE]:
+    for r in srows:
+        if len(r) > iE and r[iE] and r[iE].isdigit():
             m = re.match(r"(@!?U?P\w+\s+)?([A-Z0-9_.]+)", r[iS].strip())
-            ops[m.group(2)] += int(r[iE])
+            if m:
+                ops[m.group(2)] += int(r[iE])
     tot = sum(ops.values())
     return {k: d[k] for k in keys if k in d}, {k: [v, round(v / tot, 4)] for k, v in ops.most_common(20)}
 
