@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "dsi_common.cuh"
 #include "dsi_crn_common.cuh"
 #include "dsi_device.h"
@@ -168,6 +170,10 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
   // the lanes of a warp share k (lookahead-major order) and differ in t_d: where none of
   // them queues, the long-run loop needs no SP division (warp-uniform, so no divergence)
   const bool warp_noqueue = __all_sync(0xffffffffu, l.noqueue != 0);
+  // without a long run L_DSI - L_SI = n2 S(1) - m k t_d <= m (S(1) - k t_d) (n2 <= m): where no
+  // lane of the warp has S(1) > k t_d (SP >= 2 always), the L_DSI > L_SI counter can only move
+  // on trials with a long run -- the short path skips it (a warp-uniform choice of loop)
+  const bool warp_gts_long_only = __all_sync(0xffffffffu, l.s1 <= l.kd);
   unsigned long long c_ai = 0, c_ai2 = 0, c_mai = 0, c_ay = 0, c_ay2 = 0, c_ydl = 0, a_gtn = 0, a_gts = 0;
   unsigned long long my_m = 0, my_n = 0, my_mm = 0, my_nn = 0, my_mn = 0;
   for (uint64_t ti = tile_a; ti < tile_b; ++ti) {
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
     }
     // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 2048, 256 trials: no overflow)
     uint32_t p_gtn = 0, p_gts = 0, p_ai = 0, p_ai2 = 0, p_mai = 0;
-    auto visit = [&](const uint4 v, const int s) {
+    auto visit = [&](const uint4 v, const int s, auto gts_long_only) {
       const int m = (int)v.x, n2 = (int)v.y, maxL = (int)v.z;
       int dsi = m * l.t_t + n2 * l.s1;
       int si = m * l.si_cost;
@@ -229,18 +235,23 @@ __global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
         c_ydl += (unsigned long long)ay * (unsigned)dsi;
         dsi += ay;
         si += ai * l.si_cost;
+        if (decltype(gts_long_only)::value) p_gts += (uint32_t)(si - dsi) >> 31;
       }
       // dsi, si, nonsi < 2^31: the sign bit of the difference is the comparison
       p_gtn += (uint32_t)(l.nonsi - dsi) >> 31;
-      p_gts += (uint32_t)(si - dsi) >> 31;
+      if (!decltype(gts_long_only)::value) p_gts += (uint32_t)(si - dsi) >> 31;
     };
-    int s = 0;
-    for (; s + 1 < ntr; s += 2) {
-      const uint4 v0 = summ[s], v1 = summ[s + 1];
-      visit(v0, s);
-      visit(v1, s + 1);
-    }
-    if (s < ntr) visit(summ[s], s);
+    auto trials = [&](auto gts_long_only) {
+      int s = 0;
+      for (; s + 1 < ntr; s += 2) {
+        const uint4 v0 = summ[s], v1 = summ[s + 1];
+        visit(v0, s, gts_long_only);
+        visit(v1, s + 1, gts_long_only);
+      }
+      if (s < ntr) visit(summ[s], s, gts_long_only);
+    };
+    if (warp_gts_long_only) trials(std::true_type{});
+    else trials(std::false_type{});
     a_gtn += p_gtn;
     a_gts += p_gts;
     c_ai += p_ai;
