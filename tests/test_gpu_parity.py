@@ -591,3 +591,21 @@ def test_shared_streams_update_with_same_keys_keeps_plan():
     for f in MOMENTS:
         assert np.array_equal(got[f], want[f]), f
     sim.close()
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(n_shards=3), dict(n_shards=7)])
+def test_two_pass_shared_streams_ragged_and_sharded(kw):
+    """The two-pass shared-stream form (groups >= 256 configs: pass 1 writes each trial's
+    record once, pass 2 streams tile records with bulk copies) with trial counts that are not
+    multiples of the 256-trial tile and several shards per device (each shard's pass-1 tile
+    list): bit-identical to the default mode."""
+    cfgs, tick = W.cfg3(trials=1000, k_max=40)
+    a100 = np.rint(cfgs["accept_rate"] * 100).astype(np.int64)
+    cfgs = cfgs[np.isin(a100, [0, 45, 70, 93, 100])].copy()  # 5 groups of 4000 configs (t_d x k)
+    a100 = np.rint(cfgs["accept_rate"] * 100).astype(np.int64)
+    cfgs["n_trials"] = 700 + 13 * (a100 % 7)  # ragged: not multiples of the 256-trial tile
+    _, base = run_sim(cfgs, tick, flags=0)
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS, **kw)
+    for f in MOMENTS:
+        assert np.array_equal(res[f], base[f]), (kw, f)
+    sim.close()
