@@ -15,6 +15,13 @@ for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST, D.DSI_F_SHARED_STREAMS, FRESH
     with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
         sim.heatmap()  # the on-device heatmap product
+# the two-pass shared-stream form (groups of >= 256 configs): bulk copies on mbarriers
+big, btick = W.cfg3(trials=300, k_max=8)
+a100 = (big["accept_rate"] * 100).round().astype(int)
+big = big[(a100 == 50) | (a100 == 90)].copy()
+big["n_trials"] = 300 + 7 * (a100[(a100 == 50) | (a100 == 90)] == 90)
+with D.Simulator(big, tick=btick, seed=W.SEED, flags=D.DSI_F_SHARED_STREAMS) as sim:
+    sim.run().reduce()
 ttft, ttick = W.cfg2_ttft(trials=50)  # the TTFT variant (first-segment tables)
 for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
     with D.Simulator(ttft[:6], tick=ttick, seed=W.SEED, flags=flags) as sim:
