@@ -117,7 +117,7 @@ typedef struct {
   int32_t n_shards;       /* 0 or 1: normal.  > 1 (test only, single device): split the work
                              into n_shards cost-balanced shards run back to back on one
                              device, exercising the same partition code as multi-GPU.     */
-  int32_t block_threads;  /* 0 = default (128); else 32..256, multiple of 32               */
+  int32_t block_threads;  /* 0 = default (128); else 32..128, multiple of 32 (trial kernel)  */
   void *stream;           /* cudaStream_t for the first device, or NULL (library-owned)    */
 } dsi_options;
 

@@ -865,8 +865,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (opt->n_shards > 1 && (opt->n_devices > 1 || opt->world > 1))
     return fail(nullptr, DSI_E_RANGE, "n_shards > 1 is single-device only");
   if (opt->block_threads != 0 &&
-      (opt->block_threads < 32 || opt->block_threads > 256 || opt->block_threads % 32))
-    return fail(nullptr, DSI_E_RANGE, "block_threads must be a multiple of 32 in [32, 256]");
+      (opt->block_threads < 32 || opt->block_threads > 128 || opt->block_threads % 32))
+    return fail(nullptr, DSI_E_RANGE, "block_threads must be a multiple of 32 in [32, 128]");
   const int total_devices = opt->world * opt->n_devices;
   if (total_devices > 1 && !opt->nccl_id)
     return fail(nullptr, DSI_E_NULL, "nccl_id is required when world*n_devices > 1");

@@ -37,7 +37,18 @@
 namespace dsi {
 namespace {
 
-constexpr int TABLE_MAX_N = 4096;  // larger N: arithmetic segment costs, per-call rounds 0-1
+constexpr int TABLE_MAX_N = 4096;
+// Launch bounds: blocks of at most 128 threads, at least 5 per SM -- a register budget of
+// ~100 per thread, of which ptxas takes 78.  Measured (profiles/r01_ab_lb.jsonl, cfg3): 78
+// registers 244.1 ms, 84 (bounds (256, 1)) 246.0 ms, 58 (bounds (256), no minimum) 251.3 ms,
+// 70 / 64 / 48 registers 248.5 / 250.0 / 257.5 ms: more registers than the occupancy
+// heuristic picks keep more independent Philox calls in flight.
+#ifndef DSI_TRIAL_MINB
+#define DSI_TRIAL_MINB 5
+#endif
+#ifndef DSI_TRIAL_MAXT
+#define DSI_TRIAL_MAXT 128
+#endif  // larger N: arithmetic segment costs, per-call rounds 0-1
 
 // Test-mode (DSI_F_HIST) accounting of one segment into the block histograms.
 __device__ __forceinline__ void seg_hist(int g, int seg_start, const SegCtx &s, unsigned int *sh_seg,
@@ -95,7 +106,7 @@ __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t
 
 // VAR: 0 = default model, 1 = TTFT variant present, 2 = fresh-verifier variant present
 template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, int VAR>
-__global__ void __launch_bounds__(256) dsi_trial_kernel(const LaunchParams P) {
+__global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kernel(const LaunchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
 
   __shared__ uint32_t s_cfg;

@@ -140,7 +140,7 @@ def test_shard_and_block_invariance():
     base_sim, base = run_sim(cfgs, tick)
     base_tr = [base_sim.trials(i) for i in range(cfgs.size)]
     for kw in (dict(n_shards=2), dict(n_shards=3), dict(n_shards=7), dict(block_threads=32),
-               dict(block_threads=256), dict(block_threads=96, n_shards=5)):
+               dict(block_threads=64), dict(block_threads=96, n_shards=5)):
         sim, res = run_sim(cfgs, tick, **kw)
         for f in ("sum_dsi_ticks", "sum_si_ticks", "sumsq_dsi_ticks", "sum_segments", "n_dsi_gt_si"):
             assert np.array_equal(res[f], base[f]), (kw, f)
