@@ -28,10 +28,17 @@
 namespace dsi {
 namespace {
 
+// An explicit minimum of 1 block per SM lets ptxas use 96 registers (80 with plain
+// __launch_bounds__(TH)): cfg5 142.5 -> 136.0 ms, cfg4 1.15 -> 1.11 ms, cfg2 0.94 -> 1.10 ms
+// (profiles/r01_ab_crn_regs.jsonl).
+#ifndef DSI_CRN_MINB
+#define DSI_CRN_MINB 1
+#endif
+
 // TH threads per block = trials per tile = configs per block (CPT = 1: 2 or 4 configs per
 // thread measured slower, profiles/r01_ab_crn_cpt_unroll.jsonl)
 template <int TH, int CPT>
-__global__ void __launch_bounds__(TH) dsi_crn_kernel(const CrnParams P) {
+__global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnParams P) {
   constexpr int CRN_THREADS = TH;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_bsum[5];

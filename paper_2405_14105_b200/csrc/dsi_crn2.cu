@@ -28,6 +28,11 @@
 namespace dsi {
 namespace {
 
+// (an explicit minimum of 1 block per SM: 72 registers instead of 64, cfg3 unchanged)
+#ifndef DSI_EVAL_MINB
+#define DSI_EVAL_MINB 1
+#endif
+
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -142,7 +147,7 @@ __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
 }
 
 template <int TH>
-__global__ void __launch_bounds__(TH) dsi_crn_eval_kernel(const CrnParams P) {
+__global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const CrnParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_bsum[5];
   __shared__ __align__(8) uint64_t bar[2];
