@@ -197,3 +197,16 @@ def test_workloads_shapes():
         for row in c[:: max(1, c.size // 500)]:
             O.ticks(float(row["t_target"]), tick)
             O.ticks(float(row["t_drafter"]), tick)
+
+
+def test_parallel_validation_reports_the_first_bad_config():
+    """Large grids are validated on the host worker pool; the error names the lowest bad index
+    whatever the thread interleaving (two bad rows, the later one first in memory order)."""
+    cfgs, _ = W.cfg3(k_max=20)  # 202 000 configs
+    cfgs["accept_rate"][150_001] = 2.0
+    cfgs["lookahead"][70_003] = 0
+    for _ in range(3):
+        with pytest.raises(D.DsiError) as e:
+            _create(cfgs)
+        assert e.value.status == D.DSI_E_RANGE
+        assert "config 70003" in str(e.value), str(e.value)
