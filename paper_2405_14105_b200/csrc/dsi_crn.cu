@@ -37,7 +37,9 @@ namespace {
 
 // TH threads per block = trials per tile = configs per block (CPT = 1: 2 or 4 configs per
 // thread measured slower, profiles/r01_ab_crn_cpt_unroll.jsonl)
-template <int TH, int CPT>
+// SUMS: a sums-only unit (CrnUnit::kind 1, every config k_eff = 1 without queueing): no
+// run lists -- the corrections come from the per-trial sums alone (plan_shared)
+template <int TH, int CPT, bool SUMS>
 __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnParams P) {
   constexpr int CRN_THREADS = TH;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -151,7 +153,8 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
           const int prev = below ? base + 31 - __clz(below) : lastz;
           const int L = base + zb - prev - 1;  // accepted drafts in this segment
           if (L > kmin) {
-            myruns[nr++ * CRN_THREADS] = (uint16_t)L;
+            if (!SUMS) myruns[nr * CRN_THREADS] = (uint16_t)L;
+            ++nr;
             maxL = max(maxL, L);
             if (sums) {
               sumb += magic_div((uint32_t)(L + kmin - 1), mk_lo, mk_hi);
@@ -164,7 +167,8 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
       }
       n2 += run >= 1;  // the final segment (the trailing run, then position N)
       if (run > kmin) {
-        myruns[nr++ * CRN_THREADS] = (uint16_t)run;
+        if (!SUMS) myruns[nr * CRN_THREADS] = (uint16_t)run;
+        ++nr;
         maxL = max(maxL, run);
         if (sums) {
           sumb += magic_div((uint32_t)(run + kmin - 1), mk_lo, mk_hi);
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
         if (maxL > l[c].k_eff) {  // some run is long for this config: corrections
           const int nr = (int)(v.w & 0x3ffu);
           int ai = 0, ay = 0;
-          if (sums && l[c].noqueue && l[c].k_eff == kmin) {  // every stored run, S linear in b
+          if (SUMS || (sums && l[c].noqueue && l[c].k_eff == kmin)) {  // every stored run, S linear in b
             ai = (int)(v.w >> 21);
             ay = (int)((v.w >> 10) & 0x7ffu) * l[c].kd - nr * l[c].s1;
           } else {
@@ -283,11 +287,11 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   }
 }
 
-template <int TH>
+template <int TH, bool SUMS>
 int launch_th(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
     const cudaError_t e =
-        cudaFuncSetAttribute(dsi_crn_kernel<TH, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(dsi_crn_kernel<TH, 1, SUMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
   const uint64_t max_grid = 0x7fffffffull;
@@ -295,7 +299,7 @@ int launch_th(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_crn_kernel<TH, 1><<<(unsigned)n, TH, smem, st>>>(q);
+    dsi_crn_kernel<TH, 1, SUMS><<<(unsigned)n, TH, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
@@ -312,14 +316,14 @@ size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_
          (size_t)block_threads * sizeof(uint4) + runs;
 }
 
-int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream) {
+int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream, bool sums_only) {
   if (n_units == 0) return 0;
   if (p.cfg_per_block != block_threads) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = crn_kernel_smem(p.max_n, block_threads, p.cfg_per_block, p.max_runs);
+  const size_t smem = crn_kernel_smem(p.max_n, block_threads, p.cfg_per_block, sums_only ? 0 : p.max_runs);
   switch (block_threads) {
-    case 128: return launch_th<128>(p, n_units, smem, st);
-    case 256: return launch_th<256>(p, n_units, smem, st);
+    case 128: return sums_only ? launch_th<128, true>(p, n_units, smem, st) : launch_th<128, false>(p, n_units, smem, st);
+    case 256: return sums_only ? launch_th<256, true>(p, n_units, smem, st) : launch_th<256, false>(p, n_units, smem, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }

@@ -98,7 +98,7 @@ struct CrnUnit {       // one block: a slice of one group's configs over a range
   uint32_t group;
   uint32_t begin;      // position in perm
   uint32_t count;      // <= cfg_per_block
-  uint32_t pad;
+  uint32_t kind;       // 1: every config has k_eff = 1 and no queueing (no run lists needed)
   uint64_t t0, t1;     // trials [t0, t1)
 };
 struct CrnTile {       // two-pass mode, pass 1: one block per (group, tile of trials)
@@ -151,7 +151,8 @@ size_t crn_record_bytes(int max_runs, int threads);
 size_t crn_eval_smem(int max_runs, int threads);
 // pass 1 over n_tiles records (p.tiles from p.tile_begin), then pass 2 over n_units units
 int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, int threads, void *stream);
-int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream);
+int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream,
+                      bool sums_only = false);
 
 // Dynamic shared memory of the variant chosen for (max_n, max_keff, hist).
 size_t trial_kernel_smem(int max_n, int max_keff, bool hist, bool ttft);

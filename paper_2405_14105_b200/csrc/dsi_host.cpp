@@ -170,6 +170,7 @@ struct dsi_sim {
   std::vector<dsi::CrnUnit> crn_units;
   int32_t cfg_per_block = 0, max_runs = 0;
   bool two_pass = false;                  // shared-stream mode in two passes (dsi_crn2.cu)
+  uint64_t n_sums_units = 0;              // the first units need no run lists (plan_shared)
   uint32_t rec_bytes = 0;
   uint64_t total_records = 0;
   std::vector<uint64_t> group_tile0;
@@ -278,6 +279,12 @@ dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTic
   return DSI_OK;
 }
 
+// S(b) = b k t_d for every b: Eq. 1 holds at min(SP, N), or SP >= N (no thread ever waits).
+bool config_noqueue(const CfgTicks &t) {
+  const int32_t sp_eff = std::min(t.sp, t.n);
+  return (t.t_t <= (int64_t)sp_eff * t.kd) || sp_eff >= t.n;
+}
+
 DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
   DevCfg d{};
   uint32_t mode = dsi::MODE_STREAM;
@@ -287,7 +294,7 @@ DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
   }
   const int32_t k_eff = std::min(t.k, t.n);
   const int32_t sp_eff = std::min(t.sp, t.n);
-  const bool noqueue = (t.t_t <= (int64_t)sp_eff * t.kd) || sp_eff >= t.n;
+  const bool noqueue = config_noqueue(t);
   d.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
   const bool ttft = t.t_t1 != t.t_t || t.t_d1 != t.t_d;
   // fresh-verifier variant: with k t_d <= t_t a fresh forward never finishes sooner than
@@ -736,30 +743,57 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
     h->cfg_per_block = th;
     h->block_threads = th;
     // units: (group, slice of cfg_per_block configs, range of trials); trials are split
-    // until there are enough blocks to fill every SM of every device a few times
-    size_t slices = 0;
-    for (const auto &g : h->groups) slices += (g.count + h->cfg_per_block - 1) / h->cfg_per_block;
+    // until there are enough blocks to fill every SM of every device a few times.  With
+    // 128-thread blocks a group's configs are first cut into maximal runs of "sums-only"
+    // configs (k_eff = 1 and no queueing: every run of >= 2 accepted drafts is long and
+    // the corrections are linear in per-trial sums, no run list needed) and the others;
+    // sums-only units go first and run a kernel variant without run lists in shared memory
+    // (so many more blocks fit an SM; large N, e.g. config 5, gains most).
+    const bool split_sums = th == kCrnThreads && !std::getenv("DSI_CRN_NO_SUMS_SPLIT");
+    auto sums_only = [&](uint32_t pos) {
+      const CfgTicks &c = t[h->perm[pos]];
+      return split_sums && std::min(c.k, c.n) == 1 && config_noqueue(c);
+    };
+    struct Slice {
+      uint32_t group, begin, count;
+      bool sums;
+    };
+    std::vector<Slice> slices_v;
+    for (uint32_t gi = 0; gi < h->groups.size(); ++gi) {
+      const dsi::CrnGroup &g = h->groups[gi];
+      for (uint32_t b = g.first; b < g.first + g.count;) {
+        const bool kind = sums_only(b);
+        uint32_t e = b + 1;
+        while (e < g.first + g.count && e - b < (uint32_t)th && sums_only(e) == kind) ++e;
+        slices_v.push_back(Slice{gi, b, e - b, kind});
+        b = e;
+      }
+    }
+    const size_t slices = slices_v.size();
     const int total_devices = h->opt.world * h->opt.n_devices;
     const uint64_t target = 148ull * 4 * 4 * (uint64_t)total_devices;
     const uint64_t split = std::max<uint64_t>(1, (target + slices - 1) / slices);
     h->crn_units.clear();
     cost.clear();
-    for (uint32_t gi = 0; gi < h->groups.size(); ++gi) {
-      const dsi::CrnGroup &g = h->groups[gi];
-      const uint64_t tiles = (g.n_trials + th - 1) / th;
-      const uint64_t nchunks = std::min<uint64_t>(split, tiles);
-      for (uint32_t b = g.first; b < g.first + g.count; b += (uint32_t)h->cfg_per_block) {
-        const uint32_t cnt = std::min<uint32_t>((uint32_t)h->cfg_per_block, g.first + g.count - b);
+    h->n_sums_units = 0;
+    for (int pass = 0; pass < 2; ++pass) {  // sums-only units first
+      for (const Slice &sl : slices_v) {
+        if (sl.sums != (pass == 0)) continue;
+        const dsi::CrnGroup &g = h->groups[sl.group];
+        const uint64_t tiles = (g.n_trials + th - 1) / th;
+        const uint64_t nchunks = std::min<uint64_t>(split, tiles);
         for (uint64_t c = 0; c < nchunks; ++c) {
           dsi::CrnUnit u{};
-          u.group = gi;
-          u.begin = b;
-          u.count = cnt;
+          u.group = sl.group;
+          u.begin = sl.begin;
+          u.count = sl.count;
+          u.kind = sl.sums ? 1u : 0u;
           u.t0 = (tiles * c / nchunks) * th;
           u.t1 = std::min<uint64_t>((tiles * (c + 1) / nchunks) * th, g.n_trials);
           h->crn_units.push_back(u);
+          if (sl.sums) ++h->n_sums_units;
           // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
-          cost.push_back((double)(u.t1 - u.t0) * ((double)g.n_tokens * 12.0 + (double)cnt * 25.0));
+          cost.push_back((double)(u.t1 - u.t0) * ((double)g.n_tokens * 12.0 + (double)sl.count * 25.0));
         }
       }
     }
@@ -1234,11 +1268,23 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       }
       for (const auto &rg : d.ranges) {
         if (rg.second <= rg.first) continue;
-        q.unit_begin = rg.first;
-        const int e = h->two_pass ? dsi::launch_crn_two_pass(q, 0, rg.second - rg.first, h->cfg_per_block, d.stream)
-                                  : dsi::launch_crn_kernel(q, rg.second - rg.first, h->cfg_per_block, d.stream);
-        if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
-        h->launches += 1;
+        if (h->two_pass) {
+          q.unit_begin = rg.first;
+          const int e = dsi::launch_crn_two_pass(q, 0, rg.second - rg.first, h->cfg_per_block, d.stream);
+          if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
+          h->launches += 1;
+          continue;
+        }
+        // units [0, n_sums_units) are sums-only (no run lists), the rest are not
+        const uint64_t mid = std::min(std::max(rg.first, h->n_sums_units), rg.second);
+        for (int part = 0; part < 2; ++part) {
+          const uint64_t b = part ? mid : rg.first, e_ = part ? rg.second : mid;
+          if (e_ <= b) continue;
+          q.unit_begin = b;
+          const int e = dsi::launch_crn_kernel(q, e_ - b, h->cfg_per_block, d.stream, part == 0);
+          if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
+          h->launches += 1;
+        }
       }
     }
     for (const auto &rg : d.ranges) {
