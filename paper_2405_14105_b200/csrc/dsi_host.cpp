@@ -171,6 +171,7 @@ struct dsi_sim {
   int32_t cfg_per_block = 0, max_runs = 0;
   bool two_pass = false;                  // shared-stream mode in two passes (dsi_crn2.cu)
   uint64_t n_sums_units = 0;              // the first units need no run lists (plan_shared)
+  int32_t max_runs_normal = 0;            // run-list slots the other units need
   uint32_t rec_bytes = 0;
   uint64_t total_records = 0;
   std::vector<uint64_t> group_tile0;
@@ -776,6 +777,7 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
     h->crn_units.clear();
     cost.clear();
     h->n_sums_units = 0;
+    h->max_runs_normal = 1;
     for (int pass = 0; pass < 2; ++pass) {  // sums-only units first
       for (const Slice &sl : slices_v) {
         if (sl.sums != (pass == 0)) continue;
@@ -792,6 +794,12 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
           u.t1 = std::min<uint64_t>((tiles * (c + 1) / nchunks) * th, g.n_trials);
           h->crn_units.push_back(u);
           if (sl.sums) ++h->n_sums_units;
+          else {  // stored runs have L > the slice's smallest k_eff: each takes >= kmin + 2 positions
+            int32_t kmin = 1 << 30;
+            for (uint32_t q = sl.begin; q < sl.begin + sl.count; ++q)
+              kmin = std::min(kmin, std::min(t[h->perm[q]].k, t[h->perm[q]].n));
+            h->max_runs_normal = std::max<int32_t>(h->max_runs_normal, (g.n_tokens - 1) / (kmin + 2) + 1);
+          }
           // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
           cost.push_back((double)(u.t1 - u.t0) * ((double)g.n_tokens * 12.0 + (double)sl.count * 25.0));
         }
@@ -1281,6 +1289,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
           const uint64_t b = part ? mid : rg.first, e_ = part ? rg.second : mid;
           if (e_ <= b) continue;
           q.unit_begin = b;
+          q.max_runs = part == 0 ? h->max_runs : std::min(h->max_runs, h->max_runs_normal);
           const int e = dsi::launch_crn_kernel(q, e_ - b, h->cfg_per_block, d.stream, part == 0);
           if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
           h->launches += 1;
