@@ -83,7 +83,11 @@ def full(name=None):
             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__grid_size", "launch__block_size", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "sm__cycles_elapsed.avg.per_second", "kernel"]
+            "sm__cycles_elapsed.avg.per_second", "kernel",
+            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+            "TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+            "dram__bytes_write.sum.per_second"]
     keys += [k for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
     kname = d["kernel"][1]
     cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
