@@ -210,3 +210,37 @@ def test_parallel_validation_reports_the_first_bad_config():
             _create(cfgs)
         assert e.value.status == D.DSI_E_RANGE
         assert "config 70003" in str(e.value), str(e.value)
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    exe = tmp_path / "c_abi_example"
+    lib_dir = os.path.join(ROOT, "paper_2405_14105_b200")
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "c_abi_example.c"), "-L" + lib_dir, "-ldsi_sim",
+                        "-Wl,-rpath," + lib_dir, "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_abi_example_compiles_and_runs_without_gpu(tmp_path):
+    """The README's C example builds against include/dsi_sim.h with a plain C compiler and,
+    without an sm_100 device, stops at create with DSI_E_DEVICE after validating."""
+    import subprocess
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present (tests/test_gpu_parity.py runs it)")
+    r = subprocess.run([str(_build_c_example(tmp_path))], capture_output=True, text=True)
+    assert r.returncode == 3, r.stdout + r.stderr
+    assert "no device" in r.stdout
+
+
+@pytest.mark.gpu
+def test_c_abi_example_on_gpu(tmp_path):
+    import subprocess
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([str(_build_c_example(tmp_path))], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "mean non-SI 50.000000 SI 21.231000 DSI 16.941000 over 1000 trials" in r.stdout, r.stdout
