@@ -178,6 +178,9 @@ dsi_status dsi_sim_hist(dsi_sim *h, size_t cfg, int64_t *seg_hist, int64_t *si_h
 /* CUDA stream of the i-th device of this handle (cudaStream_t as void*). */
 dsi_status dsi_sim_stream(dsi_sim *h, int32_t device_index, void **stream);
 
+/* Environment: DSI_TRACE=1 makes create / update / run / reduce / heatmap print their host-side
+ * phases (wall clock, ms) to stderr on return. */
+
 /* Kernel launches enqueued on this process since the last dsi_sim_run began: its trial
  * kernels, plus the partition check of dsi_sim_reduce and the heatmap kernel of
  * dsi_sim_heatmap when those were called. */

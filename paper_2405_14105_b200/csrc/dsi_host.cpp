@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <functional>
@@ -95,7 +96,14 @@ struct CfgTicks {
 
 // ceil(2^32 / d) split into low word and bit 32 (d >= 1).
 void magic(uint32_t d, uint32_t &lo, uint32_t &hi) {
-  const uint64_t m = ((1ull << 32) + d - 1) / d;
+  // divisors below 2^16 (every lookahead, SP and N the planner sees in practice) come from a
+  // table built once: make_dev_cfg needs three per config, millions of times per update
+  static const std::vector<uint64_t> table = [] {
+    std::vector<uint64_t> t(1u << 16, 0);
+    for (uint32_t x = 1; x < (1u << 16); ++x) t[x] = ((1ull << 32) + x - 1) / x;
+    return t;
+  }();
+  const uint64_t m = d < (1u << 16) ? table[d] : ((1ull << 32) + d - 1) / d;
   lo = (uint32_t)m;
   hi = (uint32_t)(m >> 32);
 }
@@ -333,6 +341,42 @@ double unit_cost(const CfgTicks &t, uint64_t trials) {
   return (double)trials * (double)t.n * (11.0 + 10.0 * (1.0 - t.a));
 }
 
+// DSI_TRACE=1 in the environment: each API call prints its phases (host wall clock, ms)
+// to stderr on return -- e.g. where dsi_sim_update's time goes.
+class Trace {
+ public:
+  explicit Trace(const char *call) : call_(call), on_(enabled()) {
+    if (on_) t0_ = last_ = std::chrono::steady_clock::now();
+  }
+  void mark(const char *phase) {
+    if (!on_) return;
+    const auto t = std::chrono::steady_clock::now();
+    char b[96];
+    std::snprintf(b, sizeof b, " %s=%.3f", phase, std::chrono::duration<double, std::milli>(t - last_).count());
+    phases_ += b;
+    last_ = t;
+  }
+  ~Trace() {
+    if (!on_) return;
+    const double total =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+    std::fprintf(stderr, "[dsi] %s %.3f ms:%s\n", call_, total, phases_.c_str());
+  }
+
+ private:
+  static bool enabled() {
+    static const bool e = [] {
+      const char *v = std::getenv("DSI_TRACE");
+      return v && std::atoi(v) != 0;
+    }();
+    return e;
+  }
+  const char *call_;
+  bool on_;
+  std::chrono::steady_clock::time_point t0_, last_;
+  std::string phases_;
+};
+
 // Process-wide pool of host worker threads (created on first use, kept for the life of
 // the process): the O(n_cfg) host passes -- validation, staging, finalize -- run on it
 // without spawning threads per call.  One job at a time; the calling thread helps.
@@ -459,11 +503,15 @@ void fill_dev_cfg(dsi_sim *h) {
   constexpr size_t K = 64;
   uint64_t rec[K + 1] = {}, sib[K + 1] = {};
   parallel_for(K, [&](size_t b, size_t e) {
-    for (size_t c = b; c < e; ++c)
+    for (size_t c = b; c < e; ++c) {
+      uint64_t r = 0, q = 0;  // in registers: the neighbouring chunks' sums share cache lines
       for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) {
-        rec[c + 1] += h->ticks[i].trials;
-        sib[c + 1] += (uint64_t)std::min(h->ticks[i].k, h->ticks[i].n) + 1;
+        r += h->ticks[i].trials;
+        q += (uint64_t)std::min(h->ticks[i].k, h->ticks[i].n) + 1;
       }
+      rec[c + 1] = r;
+      sib[c + 1] = q;
+    }
   }, 1);
   for (size_t c = 0; c < K; ++c) {
     rec[c + 1] += rec[c];
@@ -889,6 +937,7 @@ dsi_status dsi_nccl_unique_id(uint8_t id[128]) {
 
 dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t n_cfg,
                           dsi_sim **out) {
+  Trace tr("dsi_sim_create");
   g_create_error.clear();
   if (!out) return fail(nullptr, DSI_E_NULL, "out is NULL");
   *out = nullptr;
@@ -963,6 +1012,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   h->si_bins_total = sib;
   s = derive_limits(h, h->ticks);
   if (s != DSI_OK) return abort_create(s);
+  tr.mark("validate+limits");
 
   // ---- work units: (config, tile of tile_trials trials), or shared-stream (group, config slice)
   std::vector<double> crn_cost;
@@ -1012,6 +1062,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     }
     dsi_shard_bounds(cost.data(), h->total_units, parts, bounds.data());
   }
+  tr.mark("plan+shard");
 
   // ---- devices
   int visible = 0;
@@ -1097,6 +1148,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       return abort_create(e == cudaErrorMemoryAllocation ? DSI_E_NOMEM : DSI_E_DEVICE);
     }
   }
+  tr.mark("devices");
   if (shared) {
     s = plan_two_pass(h);
     if (s == DSI_OK) s = alloc_two_pass(h);
@@ -1112,6 +1164,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     }
   }
 
+  tr.mark("upload");
   // ---- NCCL: one communicator per device over world * n_devices ranks
   if (use_nccl) {
     NcclApi &api = nccl();
@@ -1138,6 +1191,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
 
 dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   if (!h) return DSI_E_NULL;
+  Trace tr("dsi_sim_update");
   h->err.clear();
   if (!cfg) return fail(h, DSI_E_NULL, "cfg is NULL");
   if (n_cfg != h->n_cfg) return fail(h, DSI_E_RANGE, "n_cfg must equal the handle's");
@@ -1150,9 +1204,11 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   const int32_t old_n = h->max_n, old_keff = h->max_keff;
   const bool old_ttft = h->any_ttft, old_fresh = h->any_fresh;
   dsi_status s = validate_all(h, cfg, n_cfg, h->ticks_next, &h->ticks);
+  tr.mark("validate");
   if (s == DSI_OK) s = derive_limits(h, h->ticks_next);  // the new configs may need a larger launch shape
   if (s != DSI_OK) return s;                              // derive_limits only commits on success
   const bool replan = h->shared && !same_plan_keys(h->ticks, h->ticks_next);
+  tr.mark("limits");
   if (replan) {
     // re-plan on the host first: the unit table's size is fixed at create
     const int32_t old_cpb = h->cfg_per_block, old_runs = h->max_runs;
@@ -1206,14 +1262,19 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     CUDA_TRY(h, cudaSetDevice(d.ordinal));
     CUDA_TRY(h, cudaStreamSynchronize(d.stream));
   }
+  tr.mark(replan ? "replan+sync" : "sync");
   fill_dev_cfg(h);
+  tr.mark("fill");
   h->ran = h->reduced = false;
   h->heat_planned = h->heat_uploaded = false;
-  return upload(h, replan);
+  const dsi_status su = upload(h, replan);
+  tr.mark("upload");
+  return su;
 }
 
 dsi_status dsi_sim_run(dsi_sim *h) {
   if (!h) return DSI_E_NULL;
+  Trace tr("dsi_sim_run (enqueue)");
   h->err.clear();
   const size_t n_cfg = h->n_cfg;
   const uint64_t tt = h->total_trials;
@@ -1315,6 +1376,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
 
 dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   if (!h) return DSI_E_NULL;
+  Trace tr("dsi_sim_reduce");
   if (!out) return fail(h, DSI_E_NULL, "out is NULL");
   h->err.clear();
   const size_t n_cfg = h->n_cfg;
@@ -1324,6 +1386,7 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   const size_t nacc = n_cfg * dsi::NF;
   dsi_status st = sum_across(h, hist);
   if (st != DSI_OK) return st;
+  tr.mark("allreduce-enqueue");
   // every device now holds the global sums (or there is one device): read device 0.
   // The partition check (every trial simulated exactly once) runs on the device before the
   // copies; the moments come back in chunks so the host finalizes chunk i while chunk i+1
@@ -1364,6 +1427,7 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   }
   CUDA_TRY(h, cudaSetDevice(d0.ordinal));
   CUDA_TRY(h, cudaEventSynchronize(h->chunk_ev[0]));  // the flag precedes chunk 0
+  tr.mark("wait-run+check+chunk0");
   if (*h->host_bad.p) {
     CUDA_TRY(h, cudaStreamSynchronize(d0.stream));
     return fail(h, DSI_E_DEVICE, "trial count mismatch after reduce (partition error)");
@@ -1413,12 +1477,14 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   });
   }
   CUDA_TRY(h, cudaStreamSynchronize(d0.stream));  // the histogram copies (HIST), if any
+  tr.mark("finalize");
   h->reduced = true;
   return DSI_OK;
 }
 
 dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size_t *n_cells) {
   if (!h) return DSI_E_NULL;
+  Trace tr("dsi_sim_heatmap");
   h->err.clear();
   if (!n_cells) return fail(h, DSI_E_NULL, "n_cells is NULL");
   if (!h->heat_planned) {  // cells: maximal runs of equal (t_target, t_drafter, a, SP, N)
