@@ -415,6 +415,18 @@ def ours(args):
                "note": "DSI_F_SHARED_STREAMS: configs with equal (stream_id, floor(a 2^32), N, T) share "
                        "one Philox pass per trial; per-config results identical to the default mode"}
         heat_shared_s, cells_shared = heatmap_grid_times(simc, flush, args.steps)
+        # end to end through the public API with host buffers, as the top-level e2e
+        h2d_c, d2h_c = simc.io_bytes()
+        barrier()
+        e2e_c = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            simc.update(cfgs)
+            simc.run()
+            simc.reduce(resc)
+            e2e_c.append(time.perf_counter() - t0)
+        crn["e2e"] = {"value": tt * args.steps / max_over_ranks(sum(e2e_c)), "unit": UNIT,
+                      "h2d_bytes_per_step": int(h2d_c), "d2h_bytes_per_step": int(d2h_c)}
         simc.close()
 
     # "heatmap grid time" (BASELINE metric): run + all-reduce + on-device
