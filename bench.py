@@ -514,6 +514,9 @@ def ours(args):
             "roofline": {"bound": "alu", "achieved": mults / (kern_ms / 1000.0) / 1e9,
                          "peak": mul_peak(sm_max) / 1e9, "unit": "Gmul/s",
                          "frac": mults / (kern_ms / 1000.0) / mul_peak(sm_max), "traffic": traffic,
+                         # what a launch must move: the config table (112 B), the unit prefix (8 B) and
+                         # the moment accumulators read and written by the L2 atomics (2 x 64 B)
+                         "algorithmic_bytes": int(cfgs.size) * (112 + 8 + 2 * 64),
                          "kernel": "dsi_trial_kernel", "kernel_ms": kern_ms,
                          "kernel_share_of_step": kern_ms / (total_ms / args.steps),
                          "peak_source": f"fmaheavy pipe: 148 SM x 4 SMSP x 8 lanes/clk (one warp IMAD.WIDE "
