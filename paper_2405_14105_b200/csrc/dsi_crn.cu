@@ -4,8 +4,9 @@
 // N, n_trials) draw identical indicators for every trial index.  A group of such
 // configurations (e.g. the 20 000 (t_d, k) points of one acceptance rate of the
 // heatmap) therefore needs ONE Philox pass per trial.  This kernel:
-//   block = (group, slice of <= CPT * blockDim configs of the group), loops over the
-//   group's trials in tiles of blockDim:
+//   block = (group, slice of <= TH configs of the group), loops over the group's
+//   trials in tiles of TH (128, or 256 for large groups -- which the two-pass form in
+//   dsi_crn2.cu usually takes instead):
 //   phase 1 (one trial per thread): Philox + Bernoulli mask exactly as dsi_kernel.cu,
 //     then the trial's summary m = #zeros + 1, n2 = #segments with g >= 2 and the list
 //     of run lengths L of accepted drafts (a segment of length g has L = g - 1) that are
@@ -15,9 +16,11 @@
 //     L_DSI = m t_t + n2 S(1) + sum_{L >= k+1} (S(ceil(L/k)) - S(1))
 //     -- the closed form of DESIGN.md section 2 with short segments (2 <= g <= k+1)
 //     costing (0, S(1)) -- then the per-config integer moments, in registers.
+//   SUMS variant (sums-only units, every config k_eff = 1 without queueing): no run lists
+//   at all, the corrections come from per-trial sums (see plan_shared).
 // Per-trial latencies, and so every sum, are bit-identical to the per-config kernel.
 // Bounds used for 32-bit arithmetic: L_DSI, L_SI < 2^31 (create validates
-// N (k t_d + t_t) < 2^31), I <= N <= 4096 so I^2 * 128 trials < 2^32.
+// N (k t_d + t_t) < 2^31), I <= N <= 2048 so I^2 * 256 trials < 2^32.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -12,10 +12,13 @@
 //        SI: ceil(g/(k+1)) iterations of k t_d + t_t
 //        DSI (Alg. 1 P:112-142 + App. D): C(g) = t_t + S(ceil((g-1)/k)),
 //            S(b) = max(b k t_d, (b mod SP) k t_d + floor(b/SP) t_t)  (FIFO, R7)
-//      A segment of length 1 costs exactly (1 SI iteration, t_t), so
-//        I = m + sum_{g>=2} (ceil(g/(k+1)) - 1),  L_DSI = m t_t + sum_{g>=2} S(b(g)),
-//      and only segments with g >= 2 are walked: they end at a zero whose
-//      predecessor is an accepted draft (mask E = R & ~(R << 1 | carry)).
+//      A segment of length 1 costs exactly (1 SI iteration, t_t), one with
+//      2 <= g <= k+1 exactly (1, t_t + S(1)), so
+//        I = m + sum_long x(g),  L_DSI = m t_t + n2 S(1) + sum_long y(g),
+//      with n2 = popc(zeros preceded by an accepted draft, E = R & ~(R << 1 | carry))
+//      and only the "long" segments (runs of >= k+1 accepted drafts) walked, found by
+//      a log-doubling run detector (walk_word).  HIST and the fresh-verifier variant
+//      walk every zero instead.
 //   3. Integer moments are reduced with warp shuffles and added to the
 //      per-config accumulators with 64-bit integer atomics (exact, order-free).
 //
@@ -26,8 +29,8 @@
 //     the warp) is precomputed per block into shared memory (U table);
 //   - the per-segment divisions become a shared-memory table T[g] = (ceil(g/(k+1))-1,
 //     S(ceil((g-1)/k))) read with LDS, keeping the walk off the fmaheavy pipe.
-// Nothing here is a contraction: no tensor cores, and HBM traffic is only the
-// per-config result write-back.
+// Nothing here is a contraction: no tensor cores, and HBM traffic is the config table
+// and the per-config moment accumulators.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
