@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
     CfgLite l[CPT];  // the owned configs, in registers for the tile
 #pragma unroll
     for (int c = 0; c < CPT; ++c) l[c] = cl[threadIdx.x + c * CRN_THREADS];
-    // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 4096, 128 trials: no overflow)
+    // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 2048, <= 256 trials: no overflow)
     uint32_t p_gtn[CPT], p_gts[CPT], p_ai[CPT], p_ai2[CPT], p_mai[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) p_gtn[c] = p_gts[c] = p_ai[c] = p_ai2[c] = p_mai[c] = 0u;
