@@ -114,6 +114,11 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   for (int c = 0; c < CPT; ++c) a_gtn[c] = a_gts[c] = 0ull;
   unsigned long long my_m = 0ull, my_n = 0ull, my_mm = 0ull, my_nn = 0ull, my_mn = 0ull;
 
+  static_assert(CPT == 1, "one config per thread (replicas cover short slices)");
+  const int C = (int)un.count;
+  const int R = C >= CRN_THREADS ? 1 : CRN_THREADS / C;
+  const int my_c = (int)threadIdx.x % C, my_r = (int)threadIdx.x / C;
+  const bool active = (int)threadIdx.x < C * R;
   const uint64_t T = un.t1;  // this unit's trials: [un.t0, un.t1)
   for (uint64_t tile0 = un.t0; tile0 < T; tile0 += CRN_THREADS) {
     // ---------------- phase 1: one trial per thread -> summary + sorted long-run list
@@ -188,61 +193,55 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
       my_mn += m * (unsigned)n2;
     }
     __syncthreads();
-    // ---------------- phase 2: CPT configs per thread, the tile's trials in lockstep
+    // ---------------- phase 2: R replicas of each of the unit's C configs (R = TH / C when
+    // the slice is short: a group of 3 configs, or the k >= 2 remainder of a sums-only
+    // split, still keeps every warp busy); replica r takes the tile's trials r, r+R, ...
     const int ntr = (int)min((uint64_t)CRN_THREADS, T - tile0);
-    CfgLite l[CPT];  // the owned configs, in registers for the tile
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) l[c] = cl[threadIdx.x + c * CRN_THREADS];
-    // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 2048, <= 256 trials: no overflow)
-    uint32_t p_gtn[CPT], p_gts[CPT], p_ai[CPT], p_ai2[CPT], p_mai[CPT];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) p_gtn[c] = p_gts[c] = p_ai[c] = p_ai2[c] = p_mai[c] = 0u;
-    auto visit = [&](const uint4 v, const int s) {
-      const int m = (int)v.x, n2 = (int)v.y, maxL = (int)v.z;
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        int dsi = m * l[c].t_t + n2 * l[c].s1;
-        int si = m * l[c].si_cost;
-        if (maxL > l[c].k_eff) {  // some run is long for this config: corrections
+    if (active) {
+      const CfgLite l = cl[my_c];
+      // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 2048, <= 256 trials: no overflow)
+      uint32_t p_gtn = 0, p_gts = 0, p_ai = 0, p_ai2 = 0, p_mai = 0;
+      auto visit = [&](const uint4 v, const int s) {
+        const int m = (int)v.x, n2 = (int)v.y, maxL = (int)v.z;
+        int dsi = m * l.t_t + n2 * l.s1;
+        int si = m * l.si_cost;
+        if (maxL > l.k_eff) {  // some run is long for this config: corrections
           const int nr = (int)(v.w & 0x3ffu);
           int ai = 0, ay = 0;
-          if (SUMS || (sums && l[c].noqueue && l[c].k_eff == kmin)) {  // every stored run, S linear in b
+          if (SUMS || (sums && l.noqueue && l.k_eff == kmin)) {  // every stored run, S linear in b
             ai = (int)(v.w >> 21);
-            ay = (int)((v.w >> 10) & 0x7ffu) * l[c].kd - nr * l[c].s1;
+            ay = (int)((v.w >> 10) & 0x7ffu) * l.kd - nr * l.s1;
           } else {
             for (int r = 0; r < nr; ++r) {  // the stored runs, in trial order
               const int L = runs[r * CRN_THREADS + s];
-              if (L > l[c].k_eff) long_run(L, l[c], ai, ay);
+              if (L > l.k_eff) long_run(L, l, ai, ay);
             }
           }
-          p_ai[c] += (unsigned)ai;
-          p_ai2[c] += (unsigned)(ai * ai);
-          p_mai[c] += (unsigned)(m * ai);
-          c_ay[c] += (unsigned)ay;
-          c_ay2[c] += (unsigned long long)ay * (unsigned)ay;
-          c_ydl[c] += (unsigned long long)ay * (unsigned)dsi;
+          p_ai += (unsigned)ai;
+          p_ai2 += (unsigned)(ai * ai);
+          p_mai += (unsigned)(m * ai);
+          c_ay[0] += (unsigned)ay;
+          c_ay2[0] += (unsigned long long)ay * (unsigned)ay;
+          c_ydl[0] += (unsigned long long)ay * (unsigned)dsi;
           dsi += ay;
-          si += ai * l[c].si_cost;
+          si += ai * l.si_cost;
         }
         // dsi, si, nonsi < 2^31: the sign bit of the difference is the comparison
-        p_gtn[c] += (uint32_t)(l[c].nonsi - dsi) >> 31;
-        p_gts[c] += (uint32_t)(si - dsi) >> 31;
+        p_gtn += (uint32_t)(l.nonsi - dsi) >> 31;
+        p_gts += (uint32_t)(si - dsi) >> 31;
+      };
+      int s = my_r;
+      for (; s + R < ntr; s += 2 * R) {  // two trials per iteration: half the loop overhead
+        const uint4 v0 = summ[s], v1 = summ[s + R];
+        visit(v0, s);
+        visit(v1, s + R);
       }
-    };
-    int s = 0;
-    for (; s + 1 < ntr; s += 2) {  // two trials per iteration: half the loop overhead
-      const uint4 v0 = summ[s], v1 = summ[s + 1];
-      visit(v0, s);
-      visit(v1, s + 1);
-    }
-    if (s < ntr) visit(summ[s], s);
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      a_gtn[c] += p_gtn[c];
-      a_gts[c] += p_gts[c];
-      c_ai[c] += p_ai[c];
-      c_ai2[c] += p_ai2[c];
-      c_mai[c] += p_mai[c];
+      if (s < ntr) visit(summ[s], s);
+      a_gtn[0] += p_gtn;
+      a_gts[0] += p_gts;
+      c_ai[0] += p_ai;
+      c_ai2[0] += p_ai2;
+      c_mai[0] += p_mai;
     }
     __syncthreads();
   }
@@ -263,31 +262,30 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   }
   __syncthreads();
   const unsigned long long Sm = s_bsum[0], Sn = s_bsum[1], Smm = s_bsum[2], Snn = s_bsum[3], Smn = s_bsum[4];
-  // per config: assemble the moments (exact u64 arithmetic) and add them with one
-  // 64-bit integer atomic per field (exact and order-free)
-#pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int j = threadIdx.x + c * CRN_THREADS;
-    if (j < (int)un.count) {
-      const CfgLite &l = cl[j];
-      const unsigned long long tt = (unsigned)l.t_t, ss = (unsigned)l.s1;
-      const unsigned long long sum_i = Sm + c_ai[c];
-      const unsigned long long sum_i2 = Smm + 2ull * c_mai[c] + c_ai2[c];
-      const unsigned long long sum_dsi = tt * Sm + ss * Sn + c_ay[c];
-      // sum (m t + n2 s + ay)^2 = t^2 Smm + s^2 Snn + 2 t s Smn + 2 sum ay (m t + n2 s) + sum ay^2
-      const unsigned long long sum_dsi2 = tt * tt * Smm + ss * ss * Snn + 2ull * tt * ss * Smn +
-                                          2ull * c_ydl[c] + c_ay2[c];
-      unsigned long long *dst = P.acc + (size_t)P.perm[un.begin + j] * NF;
-      atomicAdd(dst + F_M, Sm);
-      atomicAdd(dst + F_I, sum_i);
-      atomicAdd(dst + F_I2, sum_i2);
-      atomicAdd(dst + F_DSI, sum_dsi);
-      atomicAdd(dst + F_DSI2, sum_dsi2);
-      if (a_gtn[c]) atomicAdd(dst + F_GT_NONSI, a_gtn[c]);
-      if (a_gts[c]) atomicAdd(dst + F_GT_SI, a_gts[c]);
-      atomicAdd(dst + F_TRIALS, (unsigned long long)(un.t1 - un.t0));
-    }
+  // per config: assemble the moments (exact u64 arithmetic) and add them with 64-bit
+  // integer atomics (exact and order-free); replica 0 adds the block-sum terms, every
+  // replica its own trials' corrections and counters
+  if (!active) return;
+  const CfgLite &l = cl[my_c];
+  const unsigned long long tt = (unsigned)l.t_t, ss = (unsigned)l.s1;
+  const bool first = my_r == 0;
+  unsigned long long *dst = P.acc + (size_t)P.perm[un.begin + my_c] * NF;
+  const unsigned long long sum_i = (first ? Sm : 0ull) + c_ai[0];
+  const unsigned long long sum_i2 = (first ? Smm : 0ull) + 2ull * c_mai[0] + c_ai2[0];
+  const unsigned long long sum_dsi = (first ? tt * Sm + ss * Sn : 0ull) + c_ay[0];
+  // sum (m t + n2 s + ay)^2 = t^2 Smm + s^2 Snn + 2 t s Smn + 2 sum ay (m t + n2 s) + sum ay^2
+  const unsigned long long sum_dsi2 =
+      (first ? tt * tt * Smm + ss * ss * Snn + 2ull * tt * ss * Smn : 0ull) + 2ull * c_ydl[0] + c_ay2[0];
+  if (first) {
+    atomicAdd(dst + F_M, Sm);
+    atomicAdd(dst + F_TRIALS, (unsigned long long)(un.t1 - un.t0));
   }
+  if (sum_i) atomicAdd(dst + F_I, sum_i);
+  if (sum_i2) atomicAdd(dst + F_I2, sum_i2);
+  if (sum_dsi) atomicAdd(dst + F_DSI, sum_dsi);
+  if (sum_dsi2) atomicAdd(dst + F_DSI2, sum_dsi2);
+  if (a_gtn[0]) atomicAdd(dst + F_GT_NONSI, a_gtn[0]);
+  if (a_gts[0]) atomicAdd(dst + F_GT_SI, a_gts[0]);
 }
 
 template <int TH, bool SUMS>
