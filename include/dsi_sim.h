@@ -125,7 +125,7 @@ typedef struct {
 typedef struct {
   uint64_t trials;
   int64_t t_target_ticks, t_drafter_ticks;
-  int64_t nonsi_ticks;              /* N * t_t (per trial, constant)                       */
+  int64_t nonsi_ticks;              /* ttft_t + (N-1) t_t per trial (N t_t without TTFT)   */
   int64_t sum_si_ticks, sum_dsi_ticks;
   uint64_t sumsq_si_ticks, sumsq_dsi_ticks;
   int64_t sum_si_iters;             /* sum of I = SI target forwards                       */
@@ -152,15 +152,21 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
 /* Replace the configuration values of an existing handle (same n_cfg, same
  * n_trials per config; with DSI_F_HIST also the same min(k, N)).  Validates like
  * create, waits for any previous run, then copies the table host -> device from
- * pinned staging.  On error the handle keeps its previous configs. */
+ * pinned staging.  N may grow (shared-memory tables are sized per launch).  With
+ * DSI_F_SHARED_STREAMS the plan is kept when (stream_id, threshold, N, n_trials, k,
+ * t_target, t_drafter, SP) are unchanged, else rebuilt; an update that changes the
+ * number of groups or units returns DSI_E_RANGE ("create a new handle").  On error
+ * the handle keeps its previous configs. */
 dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg);
 
 /* Enqueue one full simulation on every device of this process (asynchronous). */
 dsi_status dsi_sim_run(dsi_sim *h);
 
 /* Wait for the run, sum the per-config integer moments across devices and ranks
- * (one NCCL all-reduce), copy them to the host and derive FP64 means/std.
- * n must equal n_cfg.  Blocking.  Every rank must call it. */
+ * (one NCCL all-reduce), check on the device that every trial was simulated exactly
+ * once (DSI_E_DEVICE otherwise, nothing written), copy the moments to the host in
+ * chunks and derive FP64 means/std (overlapped).  n must equal n_cfg.  Blocking.
+ * Every rank must call it. */
 dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n);
 
 /* Per-trial records of trials [first, first+count) of config cfg (needs
