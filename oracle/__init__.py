@@ -27,6 +27,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "dsi_oracle.c")
+_SRC_MULTI = os.path.join(_HERE, "dsi_oracle_multi.c")
 _HDR = os.path.join(_HERE, "dsi_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
@@ -34,10 +35,10 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (-O2, no intrinsics)."""
     stale = (not os.path.exists(_LIB)) or any(
-        os.path.getmtime(s) > os.path.getmtime(_LIB) for s in (_SRC, _HDR))
+        os.path.getmtime(s) > os.path.getmtime(_LIB) for s in (_SRC, _SRC_MULTI, _HDR))
     if force or stale:
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", "-shared", "-fPIC",
-                               "-o", _LIB, _SRC])
+                               "-o", _LIB, _SRC, _SRC_MULTI])
     return _LIB
 
 
@@ -199,3 +200,131 @@ def min_lookahead(t_target: int, t_drafter: int, sp: int) -> int:
 def required_processors(t_target: int, t_drafter: int, k: int) -> int:
     """1 + ceil(t_t / (k t_d)): one drafter GPU plus the target servers."""
     return 1 + -(-t_target // (k * t_drafter))
+
+
+# ---- multi-drafter DSI (SURVEY 8(f) N4; dsi_oracle_multi.c) ------------------------------
+MAX_MODELS = 8
+
+
+class _MultiConfig(ctypes.Structure):
+    _fields_ = [("t_target", ctypes.c_int64), ("t_drafter", ctypes.c_int64 * (MAX_MODELS - 1)),
+                ("accept_rate", ctypes.c_double * (MAX_MODELS - 1)),
+                ("n_drafters", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
+                ("stream_id", ctypes.c_uint32), ("reserved", ctypes.c_int32)]
+
+
+class _MultiOut(ctypes.Structure):
+    _fields_ = [("nonsi", ctypes.c_int64), ("dsi", ctypes.c_int64),
+                ("settled", ctypes.c_int32 * MAX_MODELS), ("threads", ctypes.c_int64)]
+
+
+class _MultiSums(ctypes.Structure):
+    _fields_ = [("trials", ctypes.c_uint64), ("sum_dsi", ctypes.c_int64),
+                ("sumsq_dsi", ctypes.c_uint64), ("sum_settled", ctypes.c_int64 * MAX_MODELS),
+                ("n_dsi_gt_nonsi", ctypes.c_int64)]
+
+
+_multi_ready = False
+
+
+def _load_multi():
+    global _multi_ready
+    lib = _load()
+    if not _multi_ready:
+        P = ctypes.POINTER
+        lib.oracle_multi_indicator.argtypes = [P(_MultiConfig), ctypes.c_uint64, ctypes.c_uint64,
+                                               ctypes.c_int, ctypes.c_int32, ctypes.c_int32]
+        lib.oracle_multi_indicator.restype = ctypes.c_int
+        lib.oracle_multi_tree.argtypes = [P(_MultiConfig), ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.c_int, ctypes.c_int64, P(_MultiOut)]
+        lib.oracle_multi_tree.restype = ctypes.c_int
+        lib.oracle_multi_chain.argtypes = [P(_MultiConfig), ctypes.c_uint64, ctypes.c_uint64,
+                                           ctypes.c_int, P(_MultiOut)]
+        lib.oracle_multi_chain.restype = ctypes.c_int
+        lib.oracle_multi_run.argtypes = [P(_MultiConfig), ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.c_uint64, ctypes.c_int, P(_MultiSums),
+                                         ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_multi_run.restype = ctypes.c_int
+        _multi_ready = True
+    return lib
+
+
+@dataclass(frozen=True)
+class MultiConfig:
+    """Algorithm 1 with m = len(t_drafters) + 1 models, lookahead 1, integer ticks.
+    Drafters are ordered by latency, t_drafters[0] <= ... <= t_target (R25)."""
+    t_target: int
+    t_drafters: tuple
+    accept_rates: tuple
+    n_tokens: int
+    stream_id: int = 0
+
+    @property
+    def m(self) -> int:
+        return len(self.t_drafters) + 1
+
+    def _c(self) -> _MultiConfig:
+        c = _MultiConfig()
+        c.t_target = int(self.t_target)
+        for j, (t, a) in enumerate(zip(self.t_drafters, self.accept_rates)):
+            c.t_drafter[j] = int(t)
+            c.accept_rate[j] = float(a)
+        c.n_drafters = len(self.t_drafters)
+        c.n_tokens = int(self.n_tokens)
+        c.stream_id = int(self.stream_id)
+        return c
+
+
+def multi_indicator(cfg: MultiConfig, seed: int, trial: int, j: int, p: int,
+                    pattern: bool = False) -> int:
+    r = _load_multi().oracle_multi_indicator(ctypes.byref(cfg._c()), seed, trial, int(pattern), j, p)
+    if r < 0:
+        raise ValueError("oracle_multi_indicator: bad input")
+    return int(r)
+
+
+def _multi_out(o: _MultiOut, m: int) -> dict:
+    return {"nonsi": int(o.nonsi), "dsi": int(o.dsi),
+            "settled": [int(o.settled[j]) for j in range(m)], "threads": int(o.threads)}
+
+
+def multi_tree(cfg: MultiConfig, seed: int, trial: int, pattern: bool = False,
+               max_threads: int = 1 << 22) -> dict:
+    """Literal thread-tree simulation of Algorithm 1 (small N only)."""
+    o = _MultiOut()
+    rc = _load_multi().oracle_multi_tree(ctypes.byref(cfg._c()), seed, trial, int(pattern),
+                                         max_threads, ctypes.byref(o))
+    if rc == -2:
+        raise OverflowError("oracle_multi_tree: thread budget exceeded")
+    if rc:
+        raise ValueError(f"oracle_multi_tree failed for {cfg}")
+    return _multi_out(o, cfg.m)
+
+
+def multi_chain(cfg: MultiConfig, seed: int, trial: int, pattern: bool = False) -> dict:
+    o = _MultiOut()
+    if _load_multi().oracle_multi_chain(ctypes.byref(cfg._c()), seed, trial, int(pattern),
+                                        ctypes.byref(o)):
+        raise ValueError(f"oracle_multi_chain failed for {cfg}")
+    return _multi_out(o, cfg.m)
+
+
+def multi_run(cfg: MultiConfig, seed: int, first: int = 0, count: int = 1,
+              pattern: bool = False, per_trial: bool = True) -> dict:
+    """Trials first..first+count-1 (chain simulation) -> exact sums (+ per-trial arrays)."""
+    sums = _MultiSums()
+    dsi = np.zeros(count, np.int64) if per_trial else None
+    settled = np.zeros((count, cfg.m), np.int32) if per_trial else None
+    rc = _load_multi().oracle_multi_run(ctypes.byref(cfg._c()), seed, first, count, int(pattern),
+                                        ctypes.byref(sums),
+                                        dsi.ctypes.data if per_trial else None,
+                                        settled.ctypes.data if per_trial else None)
+    if rc:
+        raise ValueError(f"oracle_multi_run failed for {cfg}")
+    out = {"trials": int(sums.trials), "sum_dsi": int(sums.sum_dsi),
+           "sumsq_dsi": int(sums.sumsq_dsi),
+           "sum_settled": [int(sums.sum_settled[j]) for j in range(cfg.m)],
+           "n_dsi_gt_nonsi": int(sums.n_dsi_gt_nonsi), "nonsi": cfg.n_tokens * cfg.t_target}
+    if per_trial:
+        out["dsi"], out["settled"] = dsi, settled
+    return out

@@ -91,6 +91,73 @@ int oracle_run(const oracle_config *cfg, uint64_t seed, uint64_t first, uint64_t
                int32_t *acc, int32_t *m, int32_t *iters, int64_t *si, int64_t *dsi,
                int64_t *si_hist, int64_t *seg_hist);
 
+/* ------------------------------------------------------------------------ */
+/* Multi-drafter DSI (dsi_oracle_multi.c).  Algorithm 1 as    */
+/* stated: m models f_1..f_m, f_m the target, lookahead 1 (P:150 */
+/* "set to 1 for simplicity"), every finished thread spawns m children, no   */
+/* bound on concurrent threads.  Readings (R25):                   */
+/*   - latencies t_1 <= t_2 <= ... <= t_{m-1} <= t_m (Assumption 2;   */
+/*     j* = the smallest agreeing index is then the fastest agreeing model); */
+/*   - on the verified prefix, drafter j's token at position p equals the    */
+/*     target's with probability a_j, independently over j and p:            */
+/*     A_{j,p} = [u < floor(a_j 2^32)], u = word (p-1)&3 of Philox at counter */
+/*     (q = (p-1)>>2, j-1, trial, stream_id) -- drafter 1 draws exactly the   */
+/*     single-drafter stream;                                                */
+/*   - pattern mode: trial index i holds j*(p) - 1 as base-m digit p-1, and   */
+/*     A_{j,p} = [j >= j*(p)];                                               */
+/*   - equal finish ticks: drafters before targets, lower levels first;      */
+/*   - RETURN (line 17) is taken by the current verifier at level N (a target */
+/*     thread on an unverified prefix is never returned).                    */
+/* ------------------------------------------------------------------------ */
+#define ORACLE_MAX_MODELS 8
+
+typedef struct {
+  int64_t  t_target;                          /* t_m, ticks >= 1                     */
+  int64_t  t_drafter[ORACLE_MAX_MODELS - 1];  /* t_1..t_{m-1}: 1 <= t_1 <= ... <= t_m  */
+  double   accept_rate[ORACLE_MAX_MODELS - 1];/* a_j in [0,1]                         */
+  int32_t  n_drafters;                        /* m - 1 in 1..7                        */
+  int32_t  n_tokens;                          /* N >= 1                               */
+  uint32_t stream_id;
+  int32_t  reserved;                          /* 0                                    */
+} oracle_multi_config;
+
+typedef struct {
+  int64_t nonsi;                       /* N t_m                                         */
+  int64_t dsi;                         /* return time of Algorithm 1                    */
+  int32_t settled[ORACLE_MAX_MODELS];  /* settled[j-1] = #{p in 1..N-1 : j*(p) = j}      */
+  int64_t threads;                     /* tree simulation: threads started (0 in chain)  */
+} oracle_multi_out;
+
+typedef struct {
+  uint64_t trials;
+  int64_t  sum_dsi;
+  uint64_t sumsq_dsi;
+  int64_t  sum_settled[ORACLE_MAX_MODELS];
+  int64_t  n_dsi_gt_nonsi;
+} oracle_multi_sums;
+
+/* A_{j,p} for drafter j in 1..m-1 and position p in 1..N-1 (0/1), -1 on bad input. */
+int oracle_multi_indicator(const oracle_multi_config *cfg, uint64_t seed, uint64_t trial,
+                           int pattern, int32_t j, int32_t p);
+
+/* Literal thread-tree event simulation of Algorithm 1 (exponential in N; for pins).
+ * Returns 0, -1 on invalid input / internal assertion, -2 if more than max_threads
+ * threads would be started. */
+int oracle_multi_tree(const oracle_multi_config *cfg, uint64_t seed, uint64_t trial, int pattern,
+                      int64_t max_threads, oracle_multi_out *out);
+
+/* The same schedule followed only along the verified prefix: threads on a rejected
+ * prefix never change the verified chain's times when threads are unbounded, so the
+ * chain is simulated level by level (spawn m siblings, the target sibling verifies,
+ * j* = first agreeing model, its target child becomes the verifier).  Linear in N. */
+int oracle_multi_chain(const oracle_multi_config *cfg, uint64_t seed, uint64_t trial, int pattern,
+                       oracle_multi_out *out);
+
+/* Trials first..first+count-1 with the chain simulation; optional per-trial arrays
+ * (dsi[count], settled[count * m], m = n_drafters + 1); sums accumulated into *sums. */
+int oracle_multi_run(const oracle_multi_config *cfg, uint64_t seed, uint64_t first, uint64_t count,
+                     int pattern, oracle_multi_sums *sums, int64_t *dsi, int32_t *settled);
+
 #ifdef __cplusplus
 }
 #endif
