@@ -260,6 +260,67 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
 /* CSV of cells (SPEC S:450-458 columns; fixed formatting, %.6f; rows in input order). */
 dsi_status dsi_heatmap_csv(const dsi_heatmap_cell *cells, size_t n, const char *path);
 
+/* ---- Multi-drafter DSI: Algorithm 1 with m > 2 models ------------------
+ * Algorithm 1 as stated: models f_1..f_m, f_m the target, lookahead 1 ("set to 1
+ * for simplicity"), every finished thread initiates m threads (line 6), no bound on
+ * concurrent threads (the abstract form).  The verifier at position p (a target
+ * thread) keeps the sibling with the smallest index j* whose token equals the target's
+ * (lines 8-11), so position p costs t_{j*(p)} and the run takes
+ *     L_DSI = t_m + sum_{p=1}^{N-1} t_{j*(p)}       (P:418 with j_N = m),
+ * non-SI N t_m.  Readings (R25):
+ *   - drafters are ordered by latency, t_1 <= ... <= t_{m-1} <= t_m (Assumption 2);
+ *   - drafter j's token at position p equals the target's with probability a_j,
+ *     independently over j and p: A_{j,p} = [u < floor(a_j 2^32)], u = word (p-1) & 3 of
+ *     Philox4x32-10 at counter ((p-1) >> 2, j-1, trial, stream_id) -- drafter 1 draws
+ *     exactly the single-drafter stream of this library;
+ *   - equal finish ticks: a drafter's token is compared before the target's (tie rule only
+ *     affects which j is credited, never L_DSI);
+ *   - DSI_F_PATTERN: trial i enumerates outcomes, digit p-1 of i in base m is j*(p) - 1
+ *     (A_{j,p} = [j >= j*(p)]); run m^(N-1) trials for all of them.
+ * The paper never measures m > 2; App. D's lookahead > 1 form for m > 2 and a
+ * bounded SP are not modelled. */
+#define DSI_MAX_DRAFTERS 7
+
+typedef struct {
+  double t_target;                      /* t_m: target forward latency, user units > 0      */
+  double t_drafter[DSI_MAX_DRAFTERS];   /* t_1..t_{m-1}: 0 < t_1 <= ... <= t_{m-1} <= t_m    */
+  double accept_rate[DSI_MAX_DRAFTERS]; /* a_j in [0,1]                                      */
+  int32_t n_drafters;                   /* m - 1 in 1..7; entries beyond it are ignored      */
+  int32_t n_tokens;                     /* N in [1, 32768]                                   */
+  uint32_t stream_id;                   /* Philox counter word 3                             */
+  uint32_t reserved;                    /* must be 0                                         */
+  uint64_t n_trials;                    /* T in [1, 2^32]                                    */
+} dsi_multi_config;                     /* 144 bytes */
+
+typedef struct {
+  uint64_t trials;
+  int64_t t_target_ticks;
+  int64_t nonsi_ticks;                           /* N t_m per trial                      */
+  int64_t sum_dsi_ticks;
+  uint64_t sumsq_dsi_ticks;
+  int64_t sum_settled[DSI_MAX_DRAFTERS + 1];     /* [j-1]: sum over trials of
+                                                    #{p in 1..N-1 : j*(p) = j}, j = 1..m;
+                                                    entries >= m are 0                  */
+  int64_t n_dsi_gt_nonsi;                        /* trials with L_DSI > N t_m (Thm 1: 0) */
+  double mean_nonsi, mean_dsi;                   /* ((double)sum / (double)T) * tick     */
+  double std_dsi;                                /* population std from exact integers   */
+} dsi_multi_result;                              /* 136 bytes */
+
+/* Simulate every config on one device (opt->device; n_devices = world = 1), blocking.
+ * Options used: abi_version, tick, seed, device, stream, flags (DSI_F_PER_TRIAL,
+ * DSI_F_PATTERN, DSI_F_TIMING only); other fields must be 0/1 defaults.  out[n_cfg] is
+ * written on success.  With DSI_F_PER_TRIAL (else both must be NULL): trial_dsi[i] and
+ * trial_settled[8 i + j-1] for i = the trial's position in config-major order (config c's
+ * trials follow those of configs < c), either pointer may be NULL.  Validation as
+ * dsi_sim_create (DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW when N t_m >= 2^31 ticks or
+ * T (N t_m)^2 >= 2^64); the message is in dsi_last_create_error(). */
+dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cfg, size_t n_cfg,
+                              dsi_multi_result *out, int32_t *trial_dsi, int32_t *trial_settled);
+
+/* With DSI_F_TIMING: device time (ms) of the kernel of the last dsi_multi_simulate on this
+ * host thread (CUDA events on the launching stream); launches of it in *launches. */
+dsi_status dsi_multi_last_kernel(float *ms, int32_t *launches);
+
 /* Pure sharder (host only, no device): split per-unit costs into `parts`
  * contiguous ranges of near-equal total cost.  cost_units[i] >= 0.
  * bounds must hold parts+1 entries; bounds[0] = 0, bounds[parts] = n.

@@ -154,6 +154,38 @@ int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, 
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream,
                       bool sums_only = false);
 
+// ---- multi-drafter DSI (dsi_multi.cu)
+struct alignas(16) MultiCfg {  // 112 bytes
+  uint32_t thr[7];      // floor(a_j 2^32) when mode[j] == MODE_STREAM
+  uint8_t mode[8];      // MODE_* per drafter
+  int32_t t_d[7];       // drafter latencies, ticks (nondecreasing)
+  int32_t t_t;          // target latency, ticks
+  int32_t n_drafters;   // m - 1
+  int32_t n_tokens;     // N
+  uint32_t stream_id;
+  uint64_t n_trials;
+  uint64_t rec_off;     // first per-trial record of this config (DSI_F_PER_TRIAL)
+  uint8_t width[8];     // drafter j >= 2 is called per group of width[j] quads (4, 2 or 1)
+                        // when any of them is open: wide when quads are rarely all settled
+  uint32_t pad[2];
+};
+static_assert(sizeof(MultiCfg) == 112, "MultiCfg layout");
+enum MField : int { MF_DSI = 0, MF_DSI2, MF_GT_NONSI, MF_TRIALS, MF_SETTLED, MF = MF_SETTLED + 7 };
+struct MultiParams {
+  const MultiCfg *cfg;
+  const uint64_t *tile_prefix;  // n_cfg + 1
+  uint32_t n_cfg;
+  uint32_t tile_trials;
+  uint64_t unit_begin;
+  unsigned long long *acc;      // n_cfg * MF
+  int32_t *rec_dsi;             // per trial (or NULL)
+  int32_t *rec_settled;         // 8 per trial (or NULL)
+  int32_t max_n;
+  int32_t max_drafters;
+  Keys keys;
+};
+int launch_multi_kernel(const MultiParams &p, uint64_t n_units, bool pattern, void *stream);
+
 // Dynamic shared memory of the variant chosen for (max_n, max_keff, hist).
 size_t trial_kernel_smem(int max_n, int max_keff, bool hist, bool ttft);
 

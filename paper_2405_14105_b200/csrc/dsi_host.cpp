@@ -1670,7 +1670,229 @@ void dsi_sim_destroy(dsi_sim *h) {
   free_handle(h);
 }
 
+// ---- multi-drafter DSI: one-shot, one device -------------------------------
+#ifndef DSI_MULTI_TILE
+#define DSI_MULTI_TILE 2048  // trials per block (1024..8192 within 3%, profiles/r01_ab_multi.txt)
+#endif
+namespace {
+thread_local float g_multi_ms = 0.0f;
+thread_local int32_t g_multi_launches = 0;
+
+struct DevBuf {  // device allocation freed on scope exit
+  void *p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+};
+}  // namespace
+
+dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cfg, size_t n_cfg,
+                              dsi_multi_result *out, int32_t *trial_dsi, int32_t *trial_settled) {
+  Trace tr("dsi_multi_simulate");
+  g_create_error.clear();
+  g_multi_ms = 0.0f;
+  g_multi_launches = 0;
+  if (!opt || !cfg || !out) return fail(nullptr, DSI_E_NULL, "opt, cfg or out is NULL");
+  if (opt->abi_version != DSI_ABI_VERSION) return fail(nullptr, DSI_E_RANGE, "abi_version mismatch");
+  if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
+  if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
+  if (opt->flags & ~(DSI_F_PER_TRIAL | DSI_F_PATTERN | DSI_F_TIMING))
+    return fail(nullptr, DSI_E_RANGE, "multi-drafter mode takes PER_TRIAL, PATTERN and TIMING only");
+  if (opt->n_devices != 1 || opt->world != 1 || opt->rank != 0 || opt->n_shards > 1 || opt->device < 0)
+    return fail(nullptr, DSI_E_RANGE, "multi-drafter mode runs on one device (n_devices = world = 1)");
+  const bool per_trial = opt->flags & DSI_F_PER_TRIAL;
+  if (!per_trial && (trial_dsi || trial_settled))
+    return fail(nullptr, DSI_E_STATE, "per-trial outputs need DSI_F_PER_TRIAL");
+
+  std::vector<dsi::MultiCfg> dc(n_cfg);
+  std::vector<uint64_t> prefix(n_cfg + 1, 0);
+  std::vector<int64_t> tt(n_cfg);
+  uint64_t rec = 0;
+  int32_t max_n = 1, max_d = 1;
+  const uint32_t tile = DSI_MULTI_TILE;  // trials per block
+  for (size_t i = 0; i < n_cfg; ++i) {
+    const dsi_multi_config &c = cfg[i];
+    char buf[160];
+    auto bad = [&](dsi_status st, const char *what) {
+      std::snprintf(buf, sizeof buf, "config %zu: %s", i, what);
+      return fail(nullptr, st, buf);
+    };
+    if (c.n_drafters < 1 || c.n_drafters > DSI_MAX_DRAFTERS) return bad(DSI_E_RANGE, "n_drafters must be 1..7");
+    if (c.reserved != 0) return bad(DSI_E_RANGE, "reserved must be 0");
+    if (c.n_tokens < 1 || c.n_tokens > kMaxTokens) return bad(DSI_E_RANGE, "n_tokens out of [1, 32768]");
+    if (c.n_trials < 1 || c.n_trials > kMaxTrials) return bad(DSI_E_RANGE, "n_trials out of [1, 2^32]");
+    int64_t t_t = 0;
+    dsi_status st = to_ticks(c.t_target, opt->tick, &t_t);
+    if (st != DSI_OK) return bad(st, "t_target is not a positive whole number of ticks");
+    dsi::MultiCfg &d = dc[i];
+    std::memset(&d, 0, sizeof d);
+    int64_t prev = 1;
+    for (int j = 0; j < c.n_drafters; ++j) {
+      int64_t t_d = 0;
+      st = to_ticks(c.t_drafter[j], opt->tick, &t_d);
+      if (st != DSI_OK) return bad(st, "t_drafter is not a positive whole number of ticks");
+      if (t_d > t_t) return bad(DSI_E_RANGE, "t_drafter > t_target (Assumption 2, P:109)");
+      if (t_d < prev) return bad(DSI_E_RANGE, "drafters must be ordered by latency (R25)");
+      prev = t_d;
+      const double a = c.accept_rate[j];
+      if (!(a >= 0.0 && a <= 1.0)) return bad(DSI_E_RANGE, "accept_rate not in [0, 1]");
+      const uint64_t thr = (uint64_t)(a * 4294967296.0);  // exact scaling, then floor
+      d.thr[j] = (uint32_t)std::min<uint64_t>(thr, 0xffffffffull);
+      d.mode[j] = thr >= (1ull << 32) ? dsi::MODE_ALL_ACCEPT : (thr == 0 ? dsi::MODE_ALL_REJECT : dsi::MODE_STREAM);
+      d.t_d[j] = (int32_t)t_d;
+    }
+    const unsigned __int128 bound = (unsigned __int128)c.n_tokens * (uint64_t)t_t;
+    if (bound >= ((unsigned __int128)1 << 31)) return bad(DSI_E_OVERFLOW, "N * t_target >= 2^31 ticks");
+    if ((unsigned __int128)c.n_trials * bound * bound >= ((unsigned __int128)1 << 64))
+      return bad(DSI_E_OVERFLOW, "n_trials * (N t_target)^2 >= 2^64");
+    d.t_t = (int32_t)t_t;
+    {
+      // P(a quad still has an open position when drafter j is reached) = 1 - (1 - r)^4,
+      // r = prod_{i<j} (1 - a_i) the chance a position is open: call 4 quads together when
+      // that is >= 0.9 (<= ~10% extra calls), pairs when >= 0.6, else quad by quad
+      double r = 1.0;
+      for (int j = 0; j < c.n_drafters; ++j) {
+        const double open = 1.0 - std::pow(1.0 - r, 4.0);
+        d.width[j] = open >= 0.9 ? 4 : (open >= 0.6 ? 2 : 1);
+        r *= d.mode[j] == dsi::MODE_ALL_ACCEPT ? 0.0 : 1.0 - (double)d.thr[j] / 4294967296.0;
+      }
+    }
+    d.n_drafters = c.n_drafters;
+    d.n_tokens = c.n_tokens;
+    d.stream_id = c.stream_id;
+    d.n_trials = c.n_trials;
+    d.rec_off = rec;
+    rec += c.n_trials;
+    tt[i] = t_t;
+    prefix[i + 1] = prefix[i] + (c.n_trials + tile - 1) / tile;
+    max_n = std::max(max_n, c.n_tokens);
+    max_d = std::max(max_d, c.n_drafters);
+  }
+  tr.mark("validate");
+
+  int visible = 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceCount(&visible) != cudaSuccess || visible <= opt->device)
+    return fail(nullptr, DSI_E_DEVICE, "not enough CUDA devices visible");
+  if (cudaGetDeviceProperties(&prop, opt->device) != cudaSuccess || prop.major != 10)
+    return fail(nullptr, DSI_E_DEVICE, "device is not an sm_100 (Blackwell) GPU");
+  if (cudaSetDevice(opt->device) != cudaSuccess) return fail(nullptr, DSI_E_DEVICE, "cudaSetDevice failed");
+#define MULTI_TRY(call)                                    \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail(nullptr, e_, #call); \
+  } while (0)
+  cudaStream_t stream = (cudaStream_t)opt->stream;
+  struct OwnedStream {
+    cudaStream_t s = nullptr;
+    ~OwnedStream() { if (s) cudaStreamDestroy(s); }
+  } owned;
+  if (!stream) {
+    MULTI_TRY(cudaStreamCreateWithFlags(&owned.s, cudaStreamNonBlocking));
+    stream = owned.s;
+  }
+  DevBuf b_cfg, b_prefix, b_acc, b_dsi, b_set;
+  const size_t acc_bytes = n_cfg * dsi::MF * sizeof(unsigned long long);
+  MULTI_TRY(cudaMalloc(&b_cfg.p, n_cfg * sizeof(dsi::MultiCfg)));
+  MULTI_TRY(cudaMalloc(&b_prefix.p, (n_cfg + 1) * sizeof(uint64_t)));
+  MULTI_TRY(cudaMalloc(&b_acc.p, acc_bytes));
+  if (trial_dsi) MULTI_TRY(cudaMalloc(&b_dsi.p, rec * sizeof(int32_t)));
+  if (trial_settled) MULTI_TRY(cudaMalloc(&b_set.p, rec * 8 * sizeof(int32_t)));
+  MULTI_TRY(cudaMemcpyAsync(b_cfg.p, dc.data(), n_cfg * sizeof(dsi::MultiCfg), cudaMemcpyHostToDevice, stream));
+  MULTI_TRY(cudaMemcpyAsync(b_prefix.p, prefix.data(), (n_cfg + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                            stream));
+  MULTI_TRY(cudaMemsetAsync(b_acc.p, 0, acc_bytes, stream));
+  tr.mark("alloc+h2d");
+
+  dsi::MultiParams p{};
+  p.cfg = (const dsi::MultiCfg *)b_cfg.p;
+  p.tile_prefix = (const uint64_t *)b_prefix.p;
+  p.n_cfg = (uint32_t)n_cfg;
+  p.tile_trials = tile;
+  p.unit_begin = 0;
+  p.acc = (unsigned long long *)b_acc.p;
+  p.rec_dsi = (int32_t *)b_dsi.p;
+  p.rec_settled = (int32_t *)b_set.p;
+  p.max_n = max_n;
+  p.max_drafters = max_d;
+  const uint32_t s_lo = (uint32_t)opt->seed, s_hi = (uint32_t)(opt->seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;
+    p.keys.k1[r] = s_hi + (uint32_t)r * 0xBB67AE85u;
+  }
+  const bool timing = opt->flags & DSI_F_TIMING;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (timing) {
+    MULTI_TRY(cudaEventCreate(&ev0));
+    MULTI_TRY(cudaEventCreate(&ev1));
+    MULTI_TRY(cudaEventRecord(ev0, stream));
+  }
+  const int le = dsi::launch_multi_kernel(p, prefix[n_cfg], (opt->flags & DSI_F_PATTERN) != 0, stream);
+  if (le) {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    return cuda_fail(nullptr, (cudaError_t)le, "dsi_multi_kernel launch");
+  }
+  g_multi_launches = (int32_t)((prefix[n_cfg] + 0x7ffffffeull) / 0x7fffffffull);
+  if (timing) MULTI_TRY(cudaEventRecord(ev1, stream));
+  std::vector<unsigned long long> acc(n_cfg * dsi::MF);
+  MULTI_TRY(cudaMemcpyAsync(acc.data(), b_acc.p, acc_bytes, cudaMemcpyDeviceToHost, stream));
+  if (trial_dsi) MULTI_TRY(cudaMemcpyAsync(trial_dsi, b_dsi.p, rec * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+  if (trial_settled)
+    MULTI_TRY(cudaMemcpyAsync(trial_settled, b_set.p, rec * 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+  const cudaError_t se = cudaStreamSynchronize(stream);
+  if (timing) {
+    if (se == cudaSuccess) cudaEventElapsedTime(&g_multi_ms, ev0, ev1);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
+  if (se != cudaSuccess) return cuda_fail(nullptr, se, "dsi_multi_simulate");
+  tr.mark("kernel+d2h");
+#undef MULTI_TRY
+
+  // every trial simulated exactly once, then the FP64 derivations of the exact sums
+  for (size_t i = 0; i < n_cfg; ++i)
+    if (acc[i * dsi::MF + dsi::MF_TRIALS] != cfg[i].n_trials)
+      return fail(nullptr, DSI_E_DEVICE, "trial count mismatch after the kernel");
+  const double tick = opt->tick;
+  for (size_t i = 0; i < n_cfg; ++i) {
+    const unsigned long long *a = &acc[i * dsi::MF];
+    dsi_multi_result &r = out[i];
+    std::memset(&r, 0, sizeof r);
+    const uint64_t T = cfg[i].n_trials;
+    const int m = cfg[i].n_drafters + 1;
+    r.trials = T;
+    r.t_target_ticks = tt[i];
+    r.nonsi_ticks = (int64_t)cfg[i].n_tokens * tt[i];
+    r.sum_dsi_ticks = (int64_t)a[dsi::MF_DSI];
+    r.sumsq_dsi_ticks = a[dsi::MF_DSI2];
+    r.n_dsi_gt_nonsi = (int64_t)a[dsi::MF_GT_NONSI];
+    int64_t by_drafters = 0;
+    for (int j = 0; j < m - 1; ++j) {
+      r.sum_settled[j] = (int64_t)a[dsi::MF_SETTLED + j];
+      by_drafters += r.sum_settled[j];
+    }
+    r.sum_settled[m - 1] = (int64_t)T * (cfg[i].n_tokens - 1) - by_drafters;
+    const double Td = (double)T;
+    r.mean_nonsi = (double)r.nonsi_ticks * tick;
+    r.mean_dsi = ((double)r.sum_dsi_ticks / Td) * tick;
+    const unsigned __int128 num = (unsigned __int128)T * r.sumsq_dsi_ticks -
+                                  (unsigned __int128)(uint64_t)r.sum_dsi_ticks * (uint64_t)r.sum_dsi_ticks;
+    r.std_dsi = std::sqrt((double)num) / Td * tick;
+  }
+  tr.mark("finalize");
+  return DSI_OK;
+}
+
+dsi_status dsi_multi_last_kernel(float *ms, int32_t *launches) {
+  if (!ms || !launches) return DSI_E_NULL;
+  *ms = g_multi_ms;
+  *launches = g_multi_launches;
+  return DSI_OK;
+}
+
 }  // extern "C"
+
+static_assert(sizeof(dsi_multi_config) == 144, "dsi_multi_config ABI layout");
+static_assert(sizeof(dsi_multi_result) == 136, "dsi_multi_result ABI layout");
 
 static_assert(sizeof(dsi_config) == 64, "dsi_config ABI layout");
 static_assert(sizeof(dsi_result) == 160, "dsi_result ABI layout");

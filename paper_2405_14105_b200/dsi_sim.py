@@ -43,6 +43,17 @@ HEATMAP_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_ra
                           ("r_nonsi_si", "<f8"), ("r_si_dsi", "<f8"), ("r_nonsi_dsi", "<f8"),
                           ("r_min_dsi", "<f8"), ("first_cfg", "<u8"), ("n_cfg", "<u8")])
 assert CONFIG_DTYPE.itemsize == 64 and RESULT_DTYPE.itemsize == 160 and HEATMAP_DTYPE.itemsize == 112
+DSI_MAX_DRAFTERS = 7
+MULTI_CONFIG_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8", (DSI_MAX_DRAFTERS,)),
+                               ("accept_rate", "<f8", (DSI_MAX_DRAFTERS,)), ("n_drafters", "<i4"),
+                               ("n_tokens", "<i4"), ("stream_id", "<u4"), ("reserved", "<u4"),
+                               ("n_trials", "<u8")])
+MULTI_RESULT_DTYPE = np.dtype([("trials", "<u8"), ("t_target_ticks", "<i8"), ("nonsi_ticks", "<i8"),
+                               ("sum_dsi_ticks", "<i8"), ("sumsq_dsi_ticks", "<u8"),
+                               ("sum_settled", "<i8", (DSI_MAX_DRAFTERS + 1,)),
+                               ("n_dsi_gt_nonsi", "<i8"), ("mean_nonsi", "<f8"), ("mean_dsi", "<f8"),
+                               ("std_dsi", "<f8")])
+assert MULTI_CONFIG_DTYPE.itemsize == 144 and MULTI_RESULT_DTYPE.itemsize == 136
 
 
 class dsi_options(ctypes.Structure):
@@ -84,6 +95,8 @@ def _load():
         "dsi_heatmap": ([V, V, sz, V, sz, P(sz)], ctypes.c_int),
         "dsi_sim_heatmap": ([V, V, sz, P(sz)], ctypes.c_int),
         "dsi_heatmap_csv": ([V, sz, ctypes.c_char_p], ctypes.c_int),
+        "dsi_multi_simulate": ([P(dsi_options), V, sz, V, V, V], ctypes.c_int),
+        "dsi_multi_last_kernel": ([P(ctypes.c_float), P(i32)], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         if "DSI_SIM_LIB" in os.environ and not hasattr(lib, name):
@@ -100,7 +113,7 @@ EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce",
             "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
             "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
             "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
-            "dsi_heatmap_csv", "dsi_sim_heatmap")
+            "dsi_heatmap_csv", "dsi_sim_heatmap", "dsi_multi_simulate", "dsi_multi_last_kernel")
 
 
 class DsiError(RuntimeError):
@@ -165,6 +178,38 @@ def dsi_heatmap_csv(cells: np.ndarray, path: str) -> None:
 
 def make_configs(n: int) -> np.ndarray:
     return np.zeros(n, CONFIG_DTYPE)
+
+
+def make_multi_configs(n: int) -> np.ndarray:
+    return np.zeros(n, MULTI_CONFIG_DTYPE)
+
+
+def dsi_multi_simulate(configs: np.ndarray, *, tick: float, seed: int, flags: int = 0, device: int = 0,
+                       stream: int | None = None, per_trial: bool = False) -> tuple:
+    """Multi-drafter DSI (Algorithm 1 with m models, lookahead 1) on one device.  Returns
+    (results, trial_dsi, trial_settled); the per-trial arrays (config-major, settled with 8
+    columns) are None unless per_trial (which adds DSI_F_PER_TRIAL)."""
+    configs = np.ascontiguousarray(configs, dtype=MULTI_CONFIG_DTYPE)
+    if per_trial:
+        flags |= DSI_F_PER_TRIAL
+    opt = dsi_options(DSI_ABI_VERSION, flags, tick, seed, device, 1, 0, 1, None, 0, 0, stream)
+    out = np.zeros(configs.size, MULTI_RESULT_DTYPE)
+    dsi = settled = None
+    if flags & DSI_F_PER_TRIAL:
+        total = int(configs["n_trials"].sum())
+        dsi = np.zeros(total, np.int32)
+        settled = np.zeros((total, 8), np.int32)
+    _check(lib.dsi_multi_simulate(ctypes.byref(opt), configs.ctypes.data, configs.size, out.ctypes.data,
+                                  dsi.ctypes.data if dsi is not None else None,
+                                  settled.ctypes.data if settled is not None else None), create=True)
+    return out, dsi, settled
+
+
+def dsi_multi_last_kernel() -> tuple:
+    """(kernel ms of the last dsi_multi_simulate with DSI_F_TIMING, its launches)."""
+    ms, n = ctypes.c_float(), ctypes.c_int32()
+    _check(lib.dsi_multi_last_kernel(ctypes.byref(ms), ctypes.byref(n)))
+    return float(ms.value), int(n.value)
 
 
 def dsi_sim_create(configs: np.ndarray, *, tick: float, seed: int, flags: int = 0, device: int = 0,

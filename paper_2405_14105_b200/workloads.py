@@ -156,3 +156,59 @@ def fuzz(n: int, seed: int = 5, n_max: int = 60, trials: int = 64):
         out[i] = (float(t_t), float(t_d), a, k, int(rng.integers(1, 9)), N,
                   int(rng.integers(0, 4)), trials, 0.0, 0.0)
     return out, 1.0
+
+
+# ---- multi-drafter DSI: Algorithm 1 with m models, lookahead 1 ----------
+MAX_DRAFTERS = 7
+MULTI_CONFIG_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8", (MAX_DRAFTERS,)),
+                               ("accept_rate", "<f8", (MAX_DRAFTERS,)), ("n_drafters", "<i4"),
+                               ("n_tokens", "<i4"), ("stream_id", "<u4"), ("reserved", "<u4"),
+                               ("n_trials", "<u8")])
+
+
+def multi_rows(rows, trials: int, n_tokens: int, stream_id: int = 0) -> np.ndarray:
+    """rows: (t_target, (t_1, ..., t_{m-1}), (a_1, ..., a_{m-1})) in user units."""
+    out = np.zeros(len(rows), MULTI_CONFIG_DTYPE)
+    for i, (tt, tds, rates) in enumerate(rows):
+        out[i]["t_target"] = tt
+        out[i]["t_drafter"][:len(tds)] = tds
+        out[i]["accept_rate"][:len(rates)] = rates
+        out[i]["n_drafters"] = len(tds)
+    out["n_tokens"] = n_tokens
+    out["n_trials"] = trials
+    out["stream_id"] = stream_id
+    return out
+
+
+def multi_heatmap(trials: int = 10_000, n_tokens: int = 100, t_fast: float = 0.01, a_fast: float = 0.5):
+    """cfg3's (drafter latency, acceptance) grid as drafter f_2 of m = 3 models, with a
+    fast drafter f_1 (t_fast <= every t_d, acceptance a_fast) in front: 10 100 configs, tick 0.01."""
+    t_ds, rates = heatmap_axes()
+    rows = [(1.0, (t_fast, float(td)), (a_fast, float(a))) for td in t_ds for a in rates]
+    return multi_rows(rows, trials, n_tokens), 0.01
+
+
+def multi_fuzz(n: int, seed: int = 9, n_max: int = 60, trials: int = 64):
+    """Random m in 2..8, latencies on a 1-tick grid (tick 1), ordered drafters, a in [0, 1]
+    with exact 0 and 1 mixed in, ragged N and trial counts."""
+    rng = np.random.default_rng(seed)
+    rows, Ns, Ts = [], [], []
+    for _ in range(n):
+        m = int(rng.integers(2, 9))
+        tt = int(rng.integers(1, 120))
+        tds = sorted(int(x) for x in rng.integers(1, tt + 1, size=m - 1))
+        rates = [float(x) for x in rng.random(m - 1)]
+        for j in range(m - 1):
+            u = rng.random()
+            if u < 0.1:
+                rates[j] = 0.0
+            elif u < 0.2:
+                rates[j] = 1.0
+        rows.append((float(tt), tuple(float(x) for x in tds), tuple(rates)))
+        Ns.append(int(rng.integers(1, n_max + 1)))
+        Ts.append(int(rng.integers(1, trials + 1)))
+    out = multi_rows(rows, 1, 1)
+    out["n_tokens"] = Ns
+    out["n_trials"] = Ts
+    out["stream_id"] = rng.integers(0, 1 << 32, size=n, dtype=np.uint64).astype(np.uint32)
+    return out, 1.0
