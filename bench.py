@@ -114,6 +114,57 @@ def alg_multiplies(cfgs) -> float:
     return float(np.sum(calls[rnd]) * 20.0)
 
 
+def multi_alg_multiplies(cfgs) -> float:
+    """Expected algorithmic multiplies of one multi-drafter pass (dsi_multi_simulate): the RNG
+    contract gives drafter j's indicators of a quad from one Philox call (20 multiplies), and
+    the call is needed only if the quad still has a position no earlier drafter settled:
+    P = 1 - (1 - prod_{i<j}(1 - a_i))^r for a quad of r positions; a_j in {0, 1} needs none."""
+    total = 0.0
+    for c in cfgs:
+        npos = int(c["n_tokens"]) - 1
+        full, rem = divmod(npos, 4)
+        open_p = 1.0
+        calls = 0.0
+        for j in range(int(c["n_drafters"])):
+            thr = np.floor(c["accept_rate"][j] * 4294967296.0)
+            a = thr / 4294967296.0
+            if 0 < thr < 4294967296.0:
+                calls += full * (1.0 - (1.0 - open_p) ** 4)
+                if rem:
+                    calls += 1.0 - (1.0 - open_p) ** rem
+            open_p *= 1.0 - a
+        total += float(c["n_trials"]) * calls * 20.0
+    return total
+
+
+def multi_drafter_block(steps: int, sm_max: float) -> dict:
+    """Multi-drafter DSI on W.multi_heatmap: kernel time by CUDA events
+    (DSI_F_TIMING) and the one-call host wall clock (config H2D + kernel + moments D2H)."""
+    cfgs, tick = W.multi_heatmap()
+    tt = int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"]))
+    D.dsi_multi_simulate(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING)  # warm-up
+    ks, ws = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        D.dsi_multi_simulate(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING)
+        ws.append(time.perf_counter() - t0)
+        ks.append(D.dsi_multi_last_kernel()[0])
+    k_ms = statistics.median(ks)
+    mults = multi_alg_multiplies(cfgs)
+    return {"workload": "W.multi_heatmap: m = 3, f_1 (t 0.01, a 0.5) ahead of cfg3's 10100 (t_d, a) "
+                        "points as f_2, t_m 1.0, N 100, 1e4 trials, lookahead 1 (Alg. 1 as stated)",
+            "value": tt / (k_ms / 1000.0), "unit": UNIT, "kernel_ms": k_ms,
+            "trial_tokens_per_step": tt, "gpu_launches": D.dsi_multi_last_kernel()[1],
+            "e2e": {"value": tt / statistics.median(ws), "unit": UNIT,
+                    "h2d_bytes_per_step": int(cfgs.size * 112 + (cfgs.size + 1) * 8),
+                    "d2h_bytes_per_step": int(cfgs.size * 11 * 8)},
+            "roofline": {"bound": "alu", "achieved": mults / (k_ms / 1000.0) / 1e9,
+                         "peak": mul_peak(sm_max) / 1e9, "unit": "Gmul/s",
+                         "frac": mults / (k_ms / 1000.0) / mul_peak(sm_max), "kernel": "dsi_multi_kernel",
+                         "work": "20 multiplies per Philox call a drafter must make (quads with an "
+                                 "unsettled position), expected over the configs"}}
+
+
 def mul_peak(sm_mhz: float) -> float:
     """The fmaheavy pipe's multiply rate: 148 SMs x 4 SMSPs x 8 lanes per clock (one warp
     IMAD.WIDE.U32 per 4 cycles, profiles/r01_philox_ceiling.txt, B300_MICROARCH IMAD rate / 2)."""
@@ -490,6 +541,11 @@ def ours(args):
         pass
     traffic = prof.get("dram_bytes_per_launch") if prof.get("workload") == args.workload else None
 
+    multi = None
+    if rank == 0 and not args.no_multi:
+        multi = multi_drafter_block(args.steps, sm_max)
+    barrier()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O
@@ -541,6 +597,7 @@ def ours(args):
             "gpu_launches": launches,
             "heatmap": heat,
             "shared_streams": crn,
+            "multi_drafter": multi,
             "clocks": clk,
             "create_s": create_s,
             "wall_s_timed": wall,
@@ -564,6 +621,7 @@ def main():
     ap.add_argument("--reference-seconds", type=float, default=90.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shared-streams", action="store_true")
+    ap.add_argument("--no-multi", action="store_true", help="skip the multi-drafter block")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)

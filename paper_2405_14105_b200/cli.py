@@ -5,10 +5,13 @@
         --lookahead 5 --sp 7 --n-tokens 50 --trials 100000 --tick 0.1
     python -m paper_2405_14105_b200 table2 [--trials 100000] [--sp 8] [--n-tokens 100]
     python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200 | --k 5] [--csv out.csv] [--shared|--fresh]
+    python -m paper_2405_14105_b200 multi --t-target 1.0 --drafter 0.02:0.5 --drafter 0.1:0.8 \
+        --n-tokens 100 [--trials 100000]
 
 `plan` is Eq. 1; `table2` evaluates the Table 2 (target, drafter, acceptance)
 rows offline with lookahead in {1, 5, 10}, SI over all of them and DSI over the
-Eq.-1-feasible ones (the protocol of P:273); `heatmap` is Fig. 3.
+Eq.-1-feasible ones (the protocol of P:273); `heatmap` is Fig. 3 (P:290-311, P:525-535);
+`multi` is Algorithm 1 with several drafters (latency:acceptance, fastest first), lookahead 1.
 Exit codes: 0 success, 2 invalid arguments (DSI_E_RANGE / DSI_E_TICK / ...), 3 device error.
 """
 from __future__ import annotations
@@ -83,6 +86,21 @@ def cmd_heatmap(a) -> dict:
             "dsi_slower_than_si_cells": int(np.sum(cells["r_si_dsi"] < 1.0))}
 
 
+def cmd_multi(a) -> dict:
+    ds = []
+    for d in a.drafter:
+        t, _, acc = d.partition(":")
+        ds.append((float(t), float(acc)))
+    cfg = W.multi_rows([(a.t_target, tuple(t for t, _ in ds), tuple(x for _, x in ds))], a.trials, a.n_tokens,
+                       a.stream)
+    r = D.dsi_multi_simulate(cfg, tick=a.tick, seed=a.seed)[0][0]
+    m = len(ds) + 1
+    return {"models": m, "mean_dsi": float(r["mean_dsi"]), "std_dsi": float(r["std_dsi"]),
+            "mean_nonsi": float(r["mean_nonsi"]), "speedup_vs_nonsi": float(r["mean_nonsi"] / r["mean_dsi"]),
+            "settled_share": [float(x) / (int(r["trials"]) * max(a.n_tokens - 1, 1)) for x in r["sum_settled"][:m]],
+            "n_dsi_gt_nonsi": int(r["n_dsi_gt_nonsi"]), "trials": int(r["trials"])}
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="python -m paper_2405_14105_b200")
     ap.add_argument("--seed", type=int, default=W.SEED)
@@ -118,9 +136,17 @@ def main(argv=None) -> int:
     p.add_argument("--csv", default=None)
     p.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
     p.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER (DESIGN.md R24)")
+    p = sub.add_parser("multi", help="Alg. 1 with several drafters (lookahead 1, unbounded threads)")
+    p.add_argument("--t-target", type=float, required=True)
+    p.add_argument("--drafter", action="append", required=True, help="latency:acceptance, fastest first")
+    p.add_argument("--n-tokens", type=int, required=True)
+    p.add_argument("--trials", type=int, default=100_000)
+    p.add_argument("--tick", type=float, default=0.01)
+    p.add_argument("--stream", type=int, default=0)
     a = ap.parse_args(argv)
     try:
-        out = {"plan": cmd_plan, "simulate": cmd_simulate, "table2": cmd_table2, "heatmap": cmd_heatmap}[a.cmd](a)
+        out = {"plan": cmd_plan, "simulate": cmd_simulate, "table2": cmd_table2, "heatmap": cmd_heatmap,
+               "multi": cmd_multi}[a.cmd](a)
     except D.DsiError as e:
         print(str(e), file=sys.stderr)
         return 3 if e.status in (D.DSI_E_DEVICE, D.DSI_E_COMM, D.DSI_E_NOMEM) else 2

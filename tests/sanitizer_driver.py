@@ -37,4 +37,14 @@ long_n = W.rows([(1.0, 0.1, 0.8, 5, 2, 5000, 0, 40), (1.0, 0.1, 0.8, 20, 2, 5000
 for flags in (0, FRESH):
     with D.Simulator(long_n, tick=0.01, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
+# multi-drafter kernel (dsi_multi.cu): D = 1, 2, 4, 7 variants, table and per-call q halves,
+# pattern mode and per-trial records, ragged tiles
+mf, mtick = W.multi_fuzz(20, seed=4, n_max=40, trials=70)
+for flags in (0, D.DSI_F_PER_TRIAL, D.DSI_F_TIMING):
+    D.dsi_multi_simulate(mf, tick=mtick, seed=W.SEED, flags=flags)
+for m in (2, 3, 5, 8):
+    rows = [(10.0, tuple(float(j + 1) for j in range(m - 1)), (0.5,) * (m - 1))]
+    D.dsi_multi_simulate(W.multi_rows(rows, m ** 3, 4), tick=1.0, seed=W.SEED,
+                         flags=D.DSI_F_PATTERN | D.DSI_F_PER_TRIAL)
+D.dsi_multi_simulate(W.multi_rows([(1.0, (0.1, 0.3), (0.6, 0.8))], 2100, 5000), tick=0.01, seed=W.SEED)
 print("sanitizer driver ok")

@@ -115,3 +115,26 @@ def test_fig5_static_lookahead_monte_carlo(tmp_path):
     assert np.all(r_nonsi_dsi[ok] >= 1.0)
     assert np.all(r_si_dsi[ok] >= 0.99)
     assert abs(int(np.sum(r_nonsi_si < 1.0)) - 7266) < 150
+
+
+def test_multi_cli_rejects_unordered_drafters():
+    rc, out, err = run_cli("multi", "--t-target", "1.0", "--drafter", "0.2:0.5", "--drafter", "0.1:0.5",
+                           "--n-tokens", "10", "--trials", "10")
+    assert rc == 2 and "ordered by latency" in err
+
+
+@pytest.mark.gpu
+def test_multi_cli_expectation():
+    """Two drafters, lookahead 1: E[L] = t_m + (N-1) sum_j t_j pi_j, pi = (a_1,
+    (1-a_1) a_2, (1-a_1)(1-a_2)); 1e5 trials within 6 sigma (sigma from the per-position law)."""
+    rc, out, err = run_cli("multi", "--t-target", "1.0", "--drafter", "0.02:0.5", "--drafter", "0.1:0.8",
+                           "--n-tokens", "100", "--trials", "100000")
+    assert rc == 0, err
+    r = json.loads(out)
+    pi = [0.5, 0.5 * 0.8, 0.5 * 0.2]
+    lat = [0.02, 0.1, 1.0]
+    e1 = sum(p * t for p, t in zip(pi, lat))
+    e2 = sum(p * t * t for p, t in zip(pi, lat))
+    mean, sd = 1.0 + 99 * e1, (99 * (e2 - e1 * e1)) ** 0.5
+    assert abs(r["mean_dsi"] - mean) <= 6 * sd / 100000 ** 0.5
+    assert r["n_dsi_gt_nonsi"] == 0 and r["models"] == 3
