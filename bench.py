@@ -140,6 +140,7 @@ def multi_alg_multiplies(cfgs) -> float:
 def multi_drafter_block(steps: int, sm_max: float) -> dict:
     """Multi-drafter DSI on W.multi_heatmap: kernel time by CUDA events
     (DSI_F_TIMING) and the one-call host wall clock (config H2D + kernel + moments D2H)."""
+    from paper_2405_14105_b200 import dsi_sim as D
     cfgs, tick = W.multi_heatmap()
     tt = int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"]))
     D.dsi_multi_simulate(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING)  # warm-up
