@@ -130,6 +130,11 @@ try:  # the shared-stream kernel on the full cfg3 grid (profiles/profile_round.s
                                           kernel="regex:eval" if "eval" in name else None)
 except (OSError, ValueError, IndexError) as e:
     out["crn_error"] = str(e)
+try:  # the multi-drafter kernel on W.multi_heatmap (profiles/profile_round.sh)
+    out["set_full_multi"], out["instruction_mix_multi"] = full(f"prof_multi_{R}")
+    out["source_hotspots_multi"] = hotspots(os.path.join(OUT, f"prof_multi_{R}.ncu-rep"))
+except (OSError, ValueError, IndexError) as e:
+    out["multi_error"] = str(e)
 for name in (f"{R}_ncu_summary.json", "latest_ncu_summary.json"):
     with open(os.path.join(ROOT, "profiles", name), "w") as f:
         json.dump(out, f, indent=1)
