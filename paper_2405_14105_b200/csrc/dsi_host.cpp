@@ -1071,9 +1071,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     return abort_create(DSI_E_DEVICE);
   }
   for (int di = 0; di < opt->n_devices; ++di) {
-    cudaDeviceProp prop;
+    int major = 0;
     const int ord = opt->device + di;
-    if (cudaGetDeviceProperties(&prop, ord) != cudaSuccess || prop.major != 10) {
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, ord) != cudaSuccess || major != 10) {
       h->err = "device " + std::to_string(ord) + " is not an sm_100 (Blackwell) GPU";
       return abort_create(DSI_E_DEVICE);
     }
@@ -1678,9 +1678,15 @@ namespace {
 thread_local float g_multi_ms = 0.0f;
 thread_local int32_t g_multi_launches = 0;
 
-struct DevBuf {  // device allocation freed on scope exit
+struct DevBuf {  // stream-ordered device allocation (the device's default pool keeps the memory
+                 // between calls, so repeated calls do not pay cudaMalloc / cudaFree), freed on exit
   void *p = nullptr;
-  ~DevBuf() { if (p) cudaFree(p); }
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t bytes, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync(&p, bytes, st);
+  }
+  ~DevBuf() { if (p) cudaFreeAsync(p, s); }
 };
 }  // namespace
 
@@ -1768,11 +1774,11 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   }
   tr.mark("validate");
 
-  int visible = 0;
-  cudaDeviceProp prop;
+  int visible = 0, major = 0;  // (an attribute query: cudaGetDeviceProperties costs ~10 ms)
   if (cudaGetDeviceCount(&visible) != cudaSuccess || visible <= opt->device)
     return fail(nullptr, DSI_E_DEVICE, "not enough CUDA devices visible");
-  if (cudaGetDeviceProperties(&prop, opt->device) != cudaSuccess || prop.major != 10)
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, opt->device) != cudaSuccess ||
+      major != 10)
     return fail(nullptr, DSI_E_DEVICE, "device is not an sm_100 (Blackwell) GPU");
   if (cudaSetDevice(opt->device) != cudaSuccess) return fail(nullptr, DSI_E_DEVICE, "cudaSetDevice failed");
 #define MULTI_TRY(call)                                    \
@@ -1789,18 +1795,29 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     MULTI_TRY(cudaStreamCreateWithFlags(&owned.s, cudaStreamNonBlocking));
     stream = owned.s;
   }
+  tr.mark("stream");
+  {
+    // keep freed blocks in the device's default pool between calls (release threshold 0
+    // would hand them back to the driver at every synchronisation)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, opt->device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   DevBuf b_cfg, b_prefix, b_acc, b_dsi, b_set;
   const size_t acc_bytes = n_cfg * dsi::MF * sizeof(unsigned long long);
-  MULTI_TRY(cudaMalloc(&b_cfg.p, n_cfg * sizeof(dsi::MultiCfg)));
-  MULTI_TRY(cudaMalloc(&b_prefix.p, (n_cfg + 1) * sizeof(uint64_t)));
-  MULTI_TRY(cudaMalloc(&b_acc.p, acc_bytes));
-  if (trial_dsi) MULTI_TRY(cudaMalloc(&b_dsi.p, rec * sizeof(int32_t)));
-  if (trial_settled) MULTI_TRY(cudaMalloc(&b_set.p, rec * 8 * sizeof(int32_t)));
+  MULTI_TRY(b_cfg.alloc(n_cfg * sizeof(dsi::MultiCfg), stream));
+  MULTI_TRY(b_prefix.alloc((n_cfg + 1) * sizeof(uint64_t), stream));
+  MULTI_TRY(b_acc.alloc(acc_bytes, stream));
+  if (trial_dsi) MULTI_TRY(b_dsi.alloc(rec * sizeof(int32_t), stream));
+  if (trial_settled) MULTI_TRY(b_set.alloc(rec * 8 * sizeof(int32_t), stream));
+  tr.mark("alloc");
   MULTI_TRY(cudaMemcpyAsync(b_cfg.p, dc.data(), n_cfg * sizeof(dsi::MultiCfg), cudaMemcpyHostToDevice, stream));
   MULTI_TRY(cudaMemcpyAsync(b_prefix.p, prefix.data(), (n_cfg + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                             stream));
   MULTI_TRY(cudaMemsetAsync(b_acc.p, 0, acc_bytes, stream));
-  tr.mark("alloc+h2d");
+  tr.mark("h2d");
 
   dsi::MultiParams p{};
   p.cfg = (const dsi::MultiCfg *)b_cfg.p;
