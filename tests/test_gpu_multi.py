@@ -159,3 +159,14 @@ def test_invalid_configs_rejected_before_device_work():
     with pytest.raises(D.DsiError) as e:
         D.dsi_multi_simulate(W.multi_rows([(1e7, (1.0,), (0.5,))], 10, 1000), tick=0.01, seed=SEED)
     assert e.value.status == D.DSI_E_OVERFLOW
+
+
+def test_max_n_and_single_token():
+    """N = 32768 (the ABI's maximum) and N = 1 (no drafts: L = t_m)."""
+    big = W.multi_rows([(1.0, (0.01, 0.1, 0.4), (0.3, 0.6, 0.9))], 40, 32768, stream_id=3)
+    res, dsi, settled = D.dsi_multi_simulate(big, tick=0.01, seed=SEED, per_trial=True)
+    check(big, 0.01, res, dsi, settled)
+    one = W.multi_rows([(1.0, (0.1,), (0.5,)), (1.0, (0.1, 0.2), (0.9, 0.9))], 1000, 1)
+    res, dsi, settled = D.dsi_multi_simulate(one, tick=0.01, seed=SEED, per_trial=True)
+    assert (dsi == 100).all() and not settled.any()
+    check(one, 0.01, res, dsi, settled)

@@ -609,3 +609,39 @@ def test_two_pass_shared_streams_ragged_and_sharded(kw):
     for f in MOMENTS:
         assert np.array_equal(res[f], base[f]), (kw, f)
     sim.close()
+
+
+def test_max_n_bit_exact():
+    """N = 32768, the largest the ABI accepts (arithmetic segment costs, 8192 Philox calls per
+    trial), with and without queueing, and the fresh-verifier variant (k t_d > t_t)."""
+    rows = [(1.0, 0.1, 0.9, 4, 3, 32768, 0, 40), (1.0, 0.5, 0.6, 1, 1, 32768, 5, 33)]
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 0.01, flags=D.DSI_F_PER_TRIAL)
+    check_against_oracle(sim, res, cfgs, 0.01, hist=False, ctx="maxN")
+    sim.close()
+    fr = W.rows([(1.0, 0.5, 0.7, 3, 2, 32768, 1, 20)])
+    sim, res = run_sim(fr, 0.01, flags=D.DSI_F_PER_TRIAL | D.DSI_F_FRESH_VERIFIER)
+    check_against_oracle(sim, res, fr, 0.01, hist=False, fresh=True, ctx="maxN fresh")
+    sim.close()
+
+
+def test_max_trials_every_trial_counted_once():
+    """n_trials = 2^32, the largest the ABI accepts (the 32-bit trial counter word takes every
+    value): the on-device partition check passes, N = 1 sums are exact (L = t_t, no draws), and
+    at N = 2 the one indicator per trial is Binomial(2^32, thr/2^32) within 6 sigma with L_DSI,
+    L_SI determined by it (A_1 = 1: one segment of 2; A_1 = 0: two of 1)."""
+    T = 1 << 32
+    cfgs = W.rows([(1.0, 0.2, 0.7, 3, 2, 1, 0, T), (1.0, 0.2, 0.7, 3, 2, 2, 0, T)])
+    sim, res = run_sim(cfgs, 0.01, flags=0)
+    r1, r2 = res[0], res[1]
+    assert int(r1["trials"]) == T and int(r1["sum_dsi_ticks"]) == 100 * T and int(r1["sum_si_ticks"]) == 160 * T
+    assert int(r1["sum_accepts"]) == 0 and int(r1["sum_segments"]) == T
+    acc = int(r2["sum_accepts"])
+    p = int(r2["threshold"]) / 2 ** 32
+    assert abs(acc - T * p) <= 6 * math.sqrt(T * p * (1 - p))
+    # g = 2 costs t_t + S(1) = 100 + 60; two segments of 1 cost 2 t_t; SI: 1 iteration (k+1 >= 2)
+    # for A_1 = 1, 2 iterations for A_1 = 0, each k t_d + t_t = 160
+    assert int(r2["sum_dsi_ticks"]) == acc * 160 + (T - acc) * 200
+    assert int(r2["sum_si_ticks"]) == acc * 160 + (T - acc) * 320
+    assert int(r2["trials"]) == T
+    sim.close()
