@@ -306,10 +306,16 @@ typedef struct {
   double std_dsi;                                /* population std from exact integers   */
 } dsi_multi_result;                              /* 136 bytes */
 
-/* Simulate every config on one device (opt->device; n_devices = world = 1), blocking.
- * Options used: abi_version, tick, seed, device, stream, flags (DSI_F_PER_TRIAL,
- * DSI_F_PATTERN, DSI_F_TIMING only); other fields must be 0/1 defaults.  out[n_cfg] is
- * written on success.  With DSI_F_PER_TRIAL (else both must be NULL): trial_dsi[i] and
+/* Simulate every config, blocking.  One device per process (opt->device, n_devices = 1).
+ * Multi-GPU: with world > 1 each rank runs a contiguous, cost-balanced share of the units
+ * (config, tile of trials) and the per-config integer moments are summed with one NCCL
+ * all-reduce over a communicator created for the call from opt->nccl_id (a fresh id per
+ * call: an NCCL id serves one communicator; every rank must call it with the same configs;
+ * results are bit-identical for any world).  A non-NULL
+ * nccl_id with world == 1 runs the same path on a one-rank communicator; n_shards > 1
+ * (world == 1, tests) runs the partition's shards back to back.  Options used: abi_version,
+ * tick, seed, device, rank, world, nccl_id, n_shards, stream, flags (DSI_F_PER_TRIAL (world
+ * == 1), DSI_F_PATTERN, DSI_F_TIMING only).  out[n_cfg] is written on success.  With DSI_F_PER_TRIAL (else both must be NULL): trial_dsi[i] and
  * trial_settled[8 i + j-1] for i = the trial's position in config-major order (config c's
  * trials follow those of configs < c), either pointer may be NULL.  Validation as
  * dsi_sim_create (DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW when N t_m >= 2^31 ticks or

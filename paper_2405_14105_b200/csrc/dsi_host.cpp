@@ -1702,9 +1702,18 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
   if (opt->flags & ~(DSI_F_PER_TRIAL | DSI_F_PATTERN | DSI_F_TIMING))
     return fail(nullptr, DSI_E_RANGE, "multi-drafter mode takes PER_TRIAL, PATTERN and TIMING only");
-  if (opt->n_devices != 1 || opt->world != 1 || opt->rank != 0 || opt->n_shards > 1 || opt->device < 0)
-    return fail(nullptr, DSI_E_RANGE, "multi-drafter mode runs on one device (n_devices = world = 1)");
+  if (opt->n_devices != 1 || opt->device < 0)
+    return fail(nullptr, DSI_E_RANGE, "multi-drafter mode drives one device per process (n_devices = 1)");
+  if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
+    return fail(nullptr, DSI_E_RANGE, "need 0 <= rank < world");
+  if (opt->n_shards < 0 || opt->n_shards > 4096 || (opt->n_shards > 1 && opt->world > 1))
+    return fail(nullptr, DSI_E_RANGE, "n_shards must be 0..4096 and > 1 only with world == 1");
+  if (opt->world > 1 && !opt->nccl_id)
+    return fail(nullptr, DSI_E_NULL, "nccl_id is required when world > 1");
+  const bool use_nccl = opt->world > 1 || opt->nccl_id != nullptr;
   const bool per_trial = opt->flags & DSI_F_PER_TRIAL;
+  if (per_trial && opt->world > 1)
+    return fail(nullptr, DSI_E_RANGE, "DSI_F_PER_TRIAL needs world == 1");
   if (!per_trial && (trial_dsi || trial_settled))
     return fail(nullptr, DSI_E_STATE, "per-trial outputs need DSI_F_PER_TRIAL");
 
@@ -1771,6 +1780,31 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     prefix[i + 1] = prefix[i] + (c.n_trials + tile - 1) / tile;
     max_n = std::max(max_n, c.n_tokens);
     max_d = std::max(max_d, c.n_drafters);
+  }
+  // units (config, tile of trials) split into world x shards contiguous ranges of equal expected
+  // cost (trials x Philox calls a drafter must make, as bench.py's multi_alg_multiplies); this
+  // rank runs its ranges, the per-config moments are summed with one NCCL all-reduce
+  const uint64_t n_units = prefix[n_cfg];
+  const int shards = std::max(1, opt->n_shards);
+  const int parts = opt->world * shards;
+  std::vector<uint64_t> bounds(parts + 1, 0);
+  {
+    std::vector<double> cost(n_units);
+    for (size_t i = 0; i < n_cfg; ++i) {
+      const dsi::MultiCfg &d = dc[i];
+      const int npos = d.n_tokens - 1;
+      double open = 1.0, calls = 0.0;
+      for (int j = 0; j < d.n_drafters; ++j) {
+        if (d.mode[j] == dsi::MODE_STREAM) calls += (double)((npos + 3) / 4) * (1.0 - std::pow(1.0 - open, 4.0));
+        open *= d.mode[j] == dsi::MODE_ALL_ACCEPT ? 0.0 : 1.0 - (double)d.thr[j] / 4294967296.0;
+      }
+      const double per_trial_cost = 1.0 + (double)npos * 0.05 + calls;  // + per-trial and per-position work
+      for (uint64_t u = prefix[i]; u < prefix[i + 1]; ++u) {
+        const uint64_t t0 = (u - prefix[i]) * tile;
+        cost[u] = per_trial_cost * (double)std::min<uint64_t>(tile, d.n_trials - t0);
+      }
+    }
+    dsi_shard_bounds(cost.data(), n_units, parts, bounds.data());
   }
   tr.mark("validate");
 
@@ -1842,14 +1876,36 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     MULTI_TRY(cudaEventCreate(&ev1));
     MULTI_TRY(cudaEventRecord(ev0, stream));
   }
-  const int le = dsi::launch_multi_kernel(p, prefix[n_cfg], (opt->flags & DSI_F_PATTERN) != 0, stream);
-  if (le) {
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    return cuda_fail(nullptr, (cudaError_t)le, "dsi_multi_kernel launch");
+  int32_t launches = 0;
+  for (int sh = 0; sh < shards; ++sh) {
+    const int part = opt->rank * shards + sh;
+    p.unit_begin = bounds[part];
+    const uint64_t nu = bounds[part + 1] - bounds[part];
+    const int le = dsi::launch_multi_kernel(p, nu, (opt->flags & DSI_F_PATTERN) != 0, stream);
+    if (le) {
+      if (ev0) cudaEventDestroy(ev0);
+      if (ev1) cudaEventDestroy(ev1);
+      return cuda_fail(nullptr, (cudaError_t)le, "dsi_multi_kernel launch");
+    }
+    launches += (int32_t)((nu + 0x7ffffffeull) / 0x7fffffffull);
   }
-  g_multi_launches = (int32_t)((prefix[n_cfg] + 0x7ffffffeull) / 0x7fffffffull);
+  g_multi_launches = launches;
   if (timing) MULTI_TRY(cudaEventRecord(ev1, stream));
+  if (use_nccl) {
+    // one communicator for this call (ranks of the world, one device each), one all-reduce
+    NcclApi &api = nccl();
+    if (!api.ok) return fail(nullptr, DSI_E_COMM, "libnccl.so.2 could not be loaded");
+    ncclUniqueId uid;
+    std::memcpy(&uid, opt->nccl_id, sizeof(uid));
+    ncclComm_t comm = nullptr;
+    ncclResult_t r = api.CommInitRank(&comm, opt->world, uid, opt->rank);
+    if (r == ncclSuccess)
+      r = api.AllReduce(b_acc.p, b_acc.p, n_cfg * dsi::MF, ncclUint64, ncclSum, comm, stream);
+    if (r == ncclSuccess && cudaStreamSynchronize(stream) != cudaSuccess) r = ncclUnhandledCudaError;
+    if (comm) api.CommDestroy(comm);
+    if (r != ncclSuccess) return fail(nullptr, DSI_E_COMM, std::string("multi-drafter all-reduce: ") +
+                                                           api.GetErrorString(r));
+  }
   std::vector<unsigned long long> acc(n_cfg * dsi::MF);
   MULTI_TRY(cudaMemcpyAsync(acc.data(), b_acc.p, acc_bytes, cudaMemcpyDeviceToHost, stream));
   if (trial_dsi) MULTI_TRY(cudaMemcpyAsync(trial_dsi, b_dsi.p, rec * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));

@@ -185,14 +185,17 @@ def make_multi_configs(n: int) -> np.ndarray:
 
 
 def dsi_multi_simulate(configs: np.ndarray, *, tick: float, seed: int, flags: int = 0, device: int = 0,
-                       stream: int | None = None, per_trial: bool = False) -> tuple:
+                       stream: int | None = None, per_trial: bool = False, rank: int = 0, world: int = 1,
+                       nccl_id: bytes | None = None, n_shards: int = 0) -> tuple:
     """Multi-drafter DSI (Algorithm 1 with m models, lookahead 1) on one device.  Returns
     (results, trial_dsi, trial_settled); the per-trial arrays (config-major, settled with 8
     columns) are None unless per_trial (which adds DSI_F_PER_TRIAL)."""
     configs = np.ascontiguousarray(configs, dtype=MULTI_CONFIG_DTYPE)
     if per_trial:
         flags |= DSI_F_PER_TRIAL
-    opt = dsi_options(DSI_ABI_VERSION, flags, tick, seed, device, 1, 0, 1, None, 0, 0, stream)
+    idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+    opt = dsi_options(DSI_ABI_VERSION, flags, tick, seed, device, 1, rank, world,
+                      ctypes.addressof(idbuf) if idbuf is not None else None, n_shards, 0, stream)
     out = np.zeros(configs.size, MULTI_RESULT_DTYPE)
     dsi = settled = None
     if flags & DSI_F_PER_TRIAL:

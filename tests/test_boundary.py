@@ -244,3 +244,17 @@ def test_c_abi_example_on_gpu(tmp_path):
     r = subprocess.run([str(_build_c_example(tmp_path))], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "mean non-SI 50.000000 SI 21.231000 DSI 16.941000 over 1000 trials" in r.stdout, r.stdout
+
+
+def test_multi_drafter_options_validated_before_device_work():
+    """dsi_multi_simulate rejects bad option combinations before touching a device (CPU)."""
+    cfgs = W.multi_rows([(1.0, (0.1,), (0.5,))], 10, 10)
+    cases = [(dict(world=2), D.DSI_E_NULL),                       # world > 1 needs an NCCL id
+             (dict(world=2, rank=2, nccl_id=bytes(128)), D.DSI_E_RANGE),
+             (dict(world=2, nccl_id=bytes(128), per_trial=True), D.DSI_E_RANGE),
+             (dict(n_shards=2, world=2, nccl_id=bytes(128)), D.DSI_E_RANGE),
+             (dict(flags=D.DSI_F_SHARED_STREAMS), D.DSI_E_RANGE)]
+    for kw, status in cases:
+        with pytest.raises(D.DsiError) as e:
+            D.dsi_multi_simulate(cfgs, tick=0.01, seed=1, **kw)
+        assert e.value.status == status, kw

@@ -170,3 +170,17 @@ def test_max_n_and_single_token():
     res, dsi, settled = D.dsi_multi_simulate(one, tick=0.01, seed=SEED, per_trial=True)
     assert (dsi == 100).all() and not settled.any()
     check(one, 0.01, res, dsi, settled)
+
+
+@pytest.mark.parametrize("kw", [{"n_shards": 2}, {"n_shards": 7}, {"nccl": True}])
+def test_partition_and_one_rank_nccl_bit_identical(kw):
+    """The multi-GPU path on one device: the cost-balanced partition run as 2 or 7 shards back
+    to back, and the NCCL all-reduce on a one-rank communicator, give the same integers."""
+    cfgs, tick = W.multi_fuzz(40, seed=12, n_max=90, trials=5000)
+    ref, _, _ = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED)
+    if kw.get("nccl"):
+        got, _, _ = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED, nccl_id=D.dsi_nccl_unique_id())
+    else:
+        got, _, _ = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED, **kw)
+    for f in ("trials", "sum_dsi_ticks", "sumsq_dsi_ticks", "sum_settled", "n_dsi_gt_nonsi", "mean_dsi", "std_dsi"):
+        assert np.array_equal(got[f], ref[f]), f

@@ -107,3 +107,70 @@ def test_sharder_balances_cost():
         b = D.dsi_shard_bounds(cost, parts)
         shares = np.array([cost[b[j]:b[j + 1]].sum() for j in range(parts)])
         assert shares.max() / shares.mean() < 1.01
+
+
+# ---- multi-drafter DSI (dsi_multi_simulate's world > 1 path): the same exchange --------------
+MULTI_BLOCK = 29
+
+
+def _multi_units(cfgs):
+    units = []
+    for c, row in enumerate(cfgs):
+        for f in range(0, int(row["n_trials"]), MULTI_BLOCK):
+            units.append((c, f, min(MULTI_BLOCK, int(row["n_trials"]) - f)))
+    cost = np.array([n * (1.0 + int(cfgs[c]["n_tokens"])) for c, _, n in units], dtype=np.float64)
+    return units, cost
+
+
+def _multi_simulate(cfgs, tick, units):
+    acc = np.zeros((cfgs.size, 3 + O.MAX_MODELS), np.int64)
+    for c, first, n in units:
+        row = cfgs[c]
+        nd = int(row["n_drafters"])
+        oc = O.MultiConfig(O.ticks(float(row["t_target"]), tick),
+                           tuple(O.ticks(float(x), tick) for x in row["t_drafter"][:nd]),
+                           tuple(float(x) for x in row["accept_rate"][:nd]), int(row["n_tokens"]),
+                           int(row["stream_id"]))
+        r = O.multi_run(oc, W.SEED, first, n, per_trial=False)
+        acc[c, 0] += r["trials"]
+        acc[c, 1] += r["sum_dsi"]
+        acc[c, 2] += np.uint64(r["sumsq_dsi"]).astype(np.int64)
+        acc[c, 3:3 + len(r["sum_settled"])] += r["sum_settled"]
+    return acc
+
+
+def _multi_worker(rank, world, port, parts, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfgs, tick = W.multi_fuzz(10, seed=31, n_max=50, trials=120)
+    units, cost = _multi_units(cfgs)
+    bounds = D.dsi_shard_bounds(cost, parts)
+    per = parts // world  # contiguous parts per rank, as dsi_multi_simulate assigns them
+    mine = []
+    for p in range(rank * per, (rank + 1) * per):
+        mine += units[int(bounds[p]):int(bounds[p + 1])]
+    acc = torch.from_numpy(_multi_simulate(cfgs, tick, mine))
+    dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        out.put(acc.numpy().tobytes())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("parts", [2, 6])
+def test_two_rank_multi_drafter_partition_allreduce_is_bit_identical(parts):
+    cfgs, tick = W.multi_fuzz(10, seed=31, n_max=50, trials=120)
+    units, _ = _multi_units(cfgs)
+    want = _multi_simulate(cfgs, tick, units)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_multi_worker, args=(r, 2, port, parts, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = np.frombuffer(q.get(timeout=300), dtype=np.int64).reshape(want.shape)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert np.array_equal(got, want)
