@@ -84,6 +84,18 @@ typedef enum {
                                  otherwise L_DSI <= N t_t on every trial (Thm 1).
                                  Not with SHARED_STREAMS or TTFT configs.                       */
 
+#define DSI_F_MEANS_ONLY 0x80u /* means only ("aggregate H[g]"): per group of
+                                 configs drawing identical indicators (as SHARED_STREAMS), one
+                                 pass builds the histogram H[g] of segment lengths over all
+                                 trials, and each config's sums follow by linearity over
+                                 segments: sum L_DSI = sum_g H[g] C(g), sum I = sum_g H[g]
+                                 ceil(g/(k+1)), sum m = sum_g H[g] -- the same integers as the
+                                 default mode, so sums, means and dsi_sim_heatmap are
+                                 bit-identical.  Second moments and per-trial counters are not
+                                 produced: sumsq_* = 0, std_* = NaN, n_dsi_gt_* = -1.  Not with
+                                 PER_TRIAL, HIST, PATTERN, SHARED_STREAMS or TTFT; N <= 8192;
+                                 dsi_sim_update keeps (stream_id, a, N, n_trials) per config.    */
+
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {
   double t_target;    /* target forward latency (t_2, "Target Latency"), user units > 0   */

@@ -12,7 +12,7 @@ LIB = os.path.join(PKG, "libdsi_sim.so")
 SOURCES = [os.path.join(CSRC, "dsi_host.cpp"), os.path.join(CSRC, "dsi_heatmap.cpp"),
            os.path.join(CSRC, "dsi_kernel.cu"), os.path.join(CSRC, "dsi_crn.cu"),
            os.path.join(CSRC, "dsi_reduce_dev.cu"), os.path.join(CSRC, "dsi_crn2.cu"),
-           os.path.join(CSRC, "dsi_multi.cu")]
+           os.path.join(CSRC, "dsi_multi.cu"), os.path.join(CSRC, "dsi_seg.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "dsi_device.h"), os.path.join(CSRC, "dsi_common.cuh"),
                   os.path.join(CSRC, "dsi_crn_common.cuh"),
                   os.path.join(ROOT, "include", "dsi_sim.h")]

@@ -154,6 +154,33 @@ int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, 
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream,
                       bool sums_only = false);
 
+// ---- means-only mode (dsi_seg.cu, DSI_F_MEANS_ONLY): segment-length histograms per group
+struct SegGroup {      // configs drawing identical indicators: equal (stream, threshold, N, T)
+  uint64_t n_trials;
+  uint64_t hist_off;   // H of this group: hist[hist_off .. hist_off + N]
+  int32_t n_tokens;
+  uint32_t stream_id;
+  uint32_t thr;
+  uint32_t mode;       // MODE_*
+};
+struct SegParams {
+  const DevCfg *cfg;
+  const SegGroup *groups;
+  const uint64_t *unit_prefix;  // n_groups + 1: first hist unit of each group
+  const uint32_t *cfg_group;    // group of each config
+  uint32_t n_groups;
+  uint32_t tile_trials;
+  uint64_t unit_begin;          // pass 1: first unit of this launch
+  uint64_t cfg_begin, cfg_end;  // pass 2: configs evaluated by this launch
+  unsigned long long *hist;     // sum over groups of (N + 1) bins; bin 0 = trials
+  unsigned long long *acc;      // n_cfg * NF
+  int32_t max_n;
+  Keys keys;
+};
+size_t seg_hist_smem(int max_n);
+int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream);
+int launch_seg_eval(const SegParams &p, void *stream);
+
 // ---- multi-drafter DSI (dsi_multi.cu)
 struct alignas(16) MultiCfg {  // 112 bytes
   uint32_t thr[7];      // floor(a_j 2^32) when mode[j] == MODE_STREAM

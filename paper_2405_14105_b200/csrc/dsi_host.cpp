@@ -39,6 +39,7 @@ constexpr uint64_t kMaxTrials = 1ull << 32;
 constexpr int kDefaultThreads = 128;
 constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size when 256 does not fit (see plan_shared)
 constexpr size_t kReduceChunks = 8;  // dsi_sim_reduce: D2H chunks overlapped with the finalize
+constexpr int kMeansMaxN = 8192;   // means-only mode: a block's histogram and q halves in smem
 constexpr int kCrnMaxN = 2048;     // shared-stream mode: 128 per-trial run lists of <= N/3+2
                                    // u16 entries fit shared memory (209 KB at N 2048)
 
@@ -154,6 +155,11 @@ struct DeviceState {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<std::pair<uint64_t, uint64_t>> ranges;  // [begin, end) units, one per shard
+  dsi::SegGroup *d_seg_groups = nullptr;  // means-only mode: groups, unit prefix, config -> group,
+  uint64_t *d_seg_prefix = nullptr;       //   segment-length histograms (bin 0 = trials)
+  uint32_t *d_cfg_group = nullptr;
+  unsigned long long *d_hist = nullptr;
+  std::vector<std::pair<uint64_t, uint64_t>> cfg_ranges;  // means-only: configs evaluated here
 };
 
 struct dsi_sim {
@@ -172,6 +178,11 @@ struct dsi_sim {
   bool any_fresh = false;                 // DSI_F_FRESH_VERIFIER and some k t_d > t_t
   uint64_t si_bins_total = 0;
   bool shared = false;                    // DSI_F_SHARED_STREAMS
+  bool means_only = false;                // DSI_F_MEANS_ONLY (dsi_seg.cu)
+  std::vector<dsi::SegGroup> seg_groups;
+  std::vector<uint64_t> seg_prefix;       // groups + 1 histogram units
+  std::vector<uint32_t> cfg_group;
+  uint64_t hist_len = 0;
   bool use_nccl = false;                  // per-config moments summed with ncclAllReduce
   std::vector<uint32_t> perm;
   std::vector<dsi::CrnGroup> groups;
@@ -554,6 +565,10 @@ void free_device(DeviceState &d) {
   cudaFree(d.d_heat_cells);
   cudaFree(d.d_heat_out);
   cudaFree(d.d_heat_bad);
+  cudaFree(d.d_seg_groups);
+  cudaFree(d.d_seg_prefix);
+  cudaFree(d.d_cfg_group);
+  cudaFree(d.d_hist);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
   if (d.own_stream && d.stream) cudaStreamDestroy(d.stream);
@@ -579,6 +594,15 @@ dsi_status upload(dsi_sim *h, bool plan = true) {
     CUDA_TRY(h, cudaSetDevice(d.ordinal));
     CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg, h->dev_cfg.p, h->n_cfg * sizeof(DevCfg),
                                 cudaMemcpyHostToDevice, d.stream));
+    if (h->means_only && plan) {
+      CUDA_TRY(h, cudaMemcpyAsync(d.d_seg_groups, h->seg_groups.data(), h->seg_groups.size() * sizeof(dsi::SegGroup),
+                                  cudaMemcpyHostToDevice, d.stream));
+      CUDA_TRY(h, cudaMemcpyAsync(d.d_seg_prefix, h->seg_prefix.data(), h->seg_prefix.size() * sizeof(uint64_t),
+                                  cudaMemcpyHostToDevice, d.stream));
+      CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg_group, h->cfg_group.data(), h->cfg_group.size() * sizeof(uint32_t),
+                                  cudaMemcpyHostToDevice, d.stream));
+      CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+    }
     if (h->shared && plan) {  // the shared-stream plan (unchanged by an update that keeps its keys)
       CUDA_TRY(h, cudaMemcpyAsync(d.d_perm, h->perm.data(), h->perm.size() * sizeof(uint32_t),
                                   cudaMemcpyHostToDevice, d.stream));
@@ -606,6 +630,60 @@ dsi_status upload(dsi_sim *h, bool plan = true) {
 // Launch-shape limits that follow from the configs (max N, max min(k, N), TTFT present),
 // and the shared-memory bounds they imply.  Called by create and again by update, whose
 // new configs may change them (the kernels size shared memory from these values).
+// Means-only plan: groups of configs with equal (stream_id, threshold, N, n_trials) -- they
+// draw identical indicators -- each with its segment-length histogram; histogram units are
+// (group, tile of tile_trials trials).  cost[u] feeds the sharder.
+dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_units) {
+  const size_t n = h->n_cfg;
+  std::vector<uint32_t> order(n);
+  for (size_t i = 0; i < n; ++i) order[i] = (uint32_t)i;
+  auto key = [&](uint32_t i) {
+    const CfgTicks &t = h->ticks[i];
+    return std::make_tuple(t.stream_id, t.thr, t.n, t.trials);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
+  h->seg_groups.clear();
+  h->cfg_group.assign(n, 0u);
+  uint64_t off = 0, trials = 0;
+  for (size_t i = 0; i < n;) {
+    size_t j = i + 1;
+    while (j < n && key(order[j]) == key(order[i])) ++j;
+    const CfgTicks &t = h->ticks[order[i]];
+    dsi::SegGroup g{};
+    g.n_trials = t.trials;
+    g.hist_off = off;
+    g.n_tokens = t.n;
+    g.stream_id = t.stream_id;
+    g.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
+    g.mode = t.thr >= (1ull << 32) ? dsi::MODE_ALL_ACCEPT : (t.thr == 0 ? dsi::MODE_ALL_REJECT : dsi::MODE_STREAM);
+    for (size_t q = i; q < j; ++q) h->cfg_group[order[q]] = (uint32_t)h->seg_groups.size();
+    h->seg_groups.push_back(g);
+    off += (uint64_t)t.n + 1;
+    trials += t.trials;
+    i = j;
+  }
+  h->hist_len = off;
+  // tiles: multiples of 128 trials, enough units to fill the devices
+  uint64_t r = trials / (128ull * std::max<uint64_t>(1, target_units));
+  r = std::min<uint64_t>(128, std::max<uint64_t>(1, r));
+  h->tile_trials = (uint32_t)(128 * r);
+  h->seg_prefix.assign(h->seg_groups.size() + 1, 0);
+  for (size_t gi = 0; gi < h->seg_groups.size(); ++gi)
+    h->seg_prefix[gi + 1] = h->seg_prefix[gi] + (h->seg_groups[gi].n_trials + h->tile_trials - 1) / h->tile_trials;
+  h->total_units = h->seg_prefix.back();
+  cost.assign(h->total_units, 0.0);
+  for (size_t gi = 0; gi < h->seg_groups.size(); ++gi) {
+    const dsi::SegGroup &g = h->seg_groups[gi];
+    const double a = (double)g.thr / 4294967296.0;
+    for (uint64_t u = h->seg_prefix[gi]; u < h->seg_prefix[gi + 1]; ++u) {
+      const uint64_t t0 = (u - h->seg_prefix[gi]) * h->tile_trials;
+      const double tr = (double)std::min<uint64_t>(h->tile_trials, g.n_trials - t0);
+      cost[u] = tr * (double)g.n_tokens * (g.mode == dsi::MODE_STREAM ? 11.0 + 10.0 * (1.0 - a) : 1.0);
+    }
+  }
+  return DSI_OK;
+}
+
 dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks) {
   struct Lim {
     int32_t max_n = 1, max_keff = 1;
@@ -946,7 +1024,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
   const uint32_t known = DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_STRICT_EQ1 | DSI_F_TIMING |
-                         DSI_F_SHARED_STREAMS | DSI_F_FRESH_VERIFIER;
+                         DSI_F_SHARED_STREAMS | DSI_F_FRESH_VERIFIER | DSI_F_MEANS_ONLY;
   if (opt->flags & ~known) return fail(nullptr, DSI_E_RANGE, "unknown flag");
   if (opt->n_devices < 1 || opt->n_devices > 8) return fail(nullptr, DSI_E_RANGE, "n_devices must be 1..8");
   if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
@@ -972,6 +1050,10 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     return fail(nullptr, DSI_E_RANGE,
                 "DSI_F_SHARED_STREAMS excludes PER_TRIAL, HIST, PATTERN and FRESH_VERIFIER");
 
+  const bool means_only = opt->flags & DSI_F_MEANS_ONLY;
+  if (means_only && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_SHARED_STREAMS)))
+    return fail(nullptr, DSI_E_RANGE, "DSI_F_MEANS_ONLY excludes PER_TRIAL, HIST, PATTERN and SHARED_STREAMS");
+
   dsi_sim *h = new (std::nothrow) dsi_sim;
   if (!h) return fail(nullptr, DSI_E_NOMEM, "handle allocation");
   auto abort_create = [&](dsi_status s) {
@@ -983,6 +1065,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   h->opt.nccl_id = nullptr;
   h->n_cfg = n_cfg;
   h->shared = shared;
+  h->means_only = means_only;
   h->use_nccl = use_nccl;
   h->block_threads = shared ? kCrnThreads : (opt->block_threads ? opt->block_threads : kDefaultThreads);
   try {
@@ -1016,7 +1099,14 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
 
   // ---- work units: (config, tile of tile_trials trials), or shared-stream (group, config slice)
   std::vector<double> crn_cost;
-  if (shared) {
+  if (means_only) {
+    if (h->any_ttft || h->max_n > kMeansMaxN) {
+      h->err = "DSI_F_MEANS_ONLY: no TTFT configs, N <= 8192";
+      return abort_create(DSI_E_RANGE);
+    }
+    s = plan_means(h, crn_cost, 148ull * 16 * (uint64_t)total_devices);
+    if (s != DSI_OK) return abort_create(s);
+  } else if (shared) {
     s = plan_shared(h, crn_cost);
     if (s != DSI_OK) return abort_create(s);
   } else {
@@ -1049,7 +1139,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       h->err = "sharder cost table";
       return abort_create(DSI_E_NOMEM);
     }
-    if (shared) {
+    if (shared || means_only) {
       cost.swap(crn_cost);
     } else {
       for (size_t i = 0; i < n_cfg; ++i) {
@@ -1107,6 +1197,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     for (int sh = 0; sh < shards_per_dev; ++sh) {
       const int part = global_dev * shards_per_dev + sh;
       d.ranges.emplace_back(bounds[part], bounds[part + 1]);
+      // means-only: part p also evaluates configs [p n / parts, (p+1) n / parts)
+      d.cfg_ranges.emplace_back((uint64_t)n_cfg * part / parts, (uint64_t)n_cfg * (part + 1) / parts);
     }
     if (e == cudaSuccess) {
       if (di == 0 && opt->stream) {
@@ -1131,6 +1223,12 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       }
     }
     if (e == cudaSuccess && per_trial) e = cudaMalloc(&d.d_rec, 5 * h->total_trials * sizeof(int32_t));
+    if (e == cudaSuccess && means_only) {
+      e = cudaMalloc(&d.d_seg_groups, h->seg_groups.size() * sizeof(dsi::SegGroup));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_seg_prefix, h->seg_prefix.size() * sizeof(uint64_t));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_cfg_group, n_cfg * sizeof(uint32_t));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_hist, h->hist_len * sizeof(unsigned long long));
+    }
     if (e == cudaSuccess && shared) {
       e = cudaMalloc(&d.d_perm, n_cfg * sizeof(uint32_t));
       if (e == cudaSuccess) e = cudaMalloc(&d.d_groups, h->groups.size() * sizeof(dsi::CrnGroup));
@@ -1207,6 +1305,21 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   tr.mark("validate");
   if (s == DSI_OK) s = derive_limits(h, h->ticks_next);  // the new configs may need a larger launch shape
   if (s != DSI_OK) return s;                              // derive_limits only commits on success
+  if (h->means_only) {  // the histogram groups are fixed at create: their keys must not change
+    bool same = !h->any_ttft && h->max_n <= kMeansMaxN;
+    for (size_t i = 0; same && i < n_cfg; ++i) {
+      const CfgTicks &a = h->ticks[i], &b = h->ticks_next[i];
+      same = a.stream_id == b.stream_id && a.thr == b.thr && a.n == b.n && a.trials == b.trials;
+    }
+    if (!same) {
+      h->max_n = old_n;
+      h->max_keff = old_keff;
+      h->any_ttft = old_ttft;
+      h->any_fresh = old_fresh;
+      return fail(h, DSI_E_RANGE,
+                  "DSI_F_MEANS_ONLY: (stream_id, accept_rate, N, n_trials) changed or TTFT; create a new handle");
+    }
+  }
   const bool replan = h->shared && !same_plan_keys(h->ticks, h->ticks_next);
   tr.mark("limits");
   if (replan) {
@@ -1272,6 +1385,21 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   return su;
 }
 
+static dsi::SegParams seg_params(dsi_sim *h, DeviceState &d, const dsi::Keys &keys) {
+  dsi::SegParams q{};
+  q.cfg = d.d_cfg;
+  q.groups = d.d_seg_groups;
+  q.unit_prefix = d.d_seg_prefix;
+  q.cfg_group = d.d_cfg_group;
+  q.n_groups = (uint32_t)h->seg_groups.size();
+  q.tile_trials = h->tile_trials;
+  q.hist = d.d_hist;
+  q.acc = d.d_acc;
+  q.max_n = h->max_n;
+  q.keys = keys;
+  return q;
+}
+
 dsi_status dsi_sim_run(dsi_sim *h) {
   if (!h) return DSI_E_NULL;
   Trace tr("dsi_sim_run (enqueue)");
@@ -1311,6 +1439,18 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       p.keys.k1[r] = s_hi + (uint32_t)r * 0xBB67AE85u;
     }
     if (d.ev0) CUDA_TRY(h, cudaEventRecord(d.ev0, d.stream));
+    if (h->means_only) {  // pass 1 here; the histogram all-reduce and pass 2 after the loop
+      CUDA_TRY(h, cudaMemsetAsync(d.d_hist, 0, h->hist_len * sizeof(unsigned long long), d.stream));
+      dsi::SegParams q = seg_params(h, d, p.keys);
+      for (const auto &rg : d.ranges) {
+        if (rg.second <= rg.first) continue;
+        q.unit_begin = rg.first;
+        const int e = dsi::launch_seg_hist(q, rg.second - rg.first, d.stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "segment histogram launch");
+        h->launches += 1;
+      }
+      continue;
+    }
     if (h->shared) {
       dsi::CrnParams q{};
       q.cfg = d.d_cfg;
@@ -1368,6 +1508,34 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       h->launches += 1;
     }
     if (d.ev1) CUDA_TRY(h, cudaEventRecord(d.ev1, d.stream));
+  }
+  if (h->means_only) {
+    // every device needs every group's full histogram: one (grouped) all-reduce, in place
+    if (h->use_nccl) {
+      NcclApi &api = nccl();
+      ncclResult_t r = api.GroupStart();
+      for (auto &d : h->dev) {
+        if (r != ncclSuccess) break;
+        cudaSetDevice(d.ordinal);
+        r = api.AllReduce(d.d_hist, d.d_hist, h->hist_len, ncclUint64, ncclSum, d.comm, d.stream);
+      }
+      const ncclResult_t r2 = api.GroupEnd();
+      if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(h, DSI_E_COMM, std::string("histogram all-reduce: ") +
+                                       api.GetErrorString(r != ncclSuccess ? r : r2));
+    }
+    for (auto &d : h->dev) {
+      CUDA_TRY(h, cudaSetDevice(d.ordinal));
+      dsi::SegParams q = seg_params(h, d, dsi::Keys{});
+      for (const auto &cr : d.cfg_ranges) {
+        q.cfg_begin = cr.first;
+        q.cfg_end = cr.second;
+        const int e = dsi::launch_seg_eval(q, d.stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "segment evaluation launch");
+        h->launches += cr.second > cr.first;
+      }
+      if (d.ev1) CUDA_TRY(h, cudaEventRecord(d.ev1, d.stream));
+    }
   }
   h->ran = true;
   h->reduced = false;
@@ -1471,8 +1639,14 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
       const unsigned __int128 num = (unsigned __int128)T * s2 - (unsigned __int128)s1 * s1;
       return std::sqrt((double)num) / Td * tick;
     };
-    r.std_si = stdev((uint64_t)r.sum_si_ticks, r.sumsq_si_ticks);
-    r.std_dsi = stdev((uint64_t)r.sum_dsi_ticks, r.sumsq_dsi_ticks);
+    if (h->means_only) {  // no per-trial values: no second moments, no per-trial counters
+      r.sumsq_si_ticks = r.sumsq_dsi_ticks = 0;
+      r.n_dsi_gt_nonsi = r.n_dsi_gt_si = -1;
+      r.std_si = r.std_dsi = std::nan("");
+    } else {
+      r.std_si = stdev((uint64_t)r.sum_si_ticks, r.sumsq_si_ticks);
+      r.std_dsi = stdev((uint64_t)r.sum_dsi_ticks, r.sumsq_dsi_ticks);
+    }
   }
   });
   }

@@ -1,0 +1,172 @@
+// dsi_seg.cu -- means-only mode (DSI_F_MEANS_ONLY, SURVEY 8(f) N3's "aggregate H[g]"):
+// per group of configs drawing identical indicators (equal stream_id, floor(a 2^32), N, T),
+// one pass over the group's trials builds the histogram H[g] of segment lengths g = 1..N
+// (H[0] counts the trials); then every config's sums follow by linearity over segments,
+//   sum_trials L_DSI = sum_g H[g] C(g),  sum_trials I = sum_g H[g] ceil(g/(k+1)),
+//   sum_trials m = sum_g H[g],
+// the same integers the per-trial kernels add up (L_DSI and I are sums over segments,
+// DESIGN.md section 2), so means are bit-identical to the default mode.  Second moments and
+// the per-trial counters need per-trial values and are not produced.
+//
+// Pass 1 (dsi_seg_hist_kernel): one block per unit (group, tile of trials); per trial the
+// Philox stream and rejection mask exactly as dsi_kernel.cu, then its segments: g = 1
+// segments (a zero preceded by a zero, or position 1) are counted with bit operations in a
+// register, longer ones with shared-memory atomics into the block's H, flushed to the
+// group's H with 64-bit atomics.  Pass 2 (dsi_seg_eval_kernel): one thread per config,
+// an O(N) dot product of H with the config's segment costs (H read by every lane of a
+// warp at once: a broadcast).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dsi_common.cuh"
+#include "dsi_device.h"
+
+namespace dsi {
+namespace {
+
+__global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ uint32_t s_grp;
+  const uint64_t unit = P.unit_begin + blockIdx.x;
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = P.n_groups;  // prefix[lo] <= unit < prefix[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(&P.unit_prefix[mid]) <= unit) lo = mid; else hi = mid;
+    }
+    s_grp = lo;
+  }
+  __syncthreads();
+  const uint32_t gi = s_grp;
+  const SegGroup G = P.groups[gi];
+  const uint64_t t0 = (unit - __ldg(&P.unit_prefix[gi])) * P.tile_trials;
+  const uint64_t t1 = min(t0 + P.tile_trials, G.n_trials);
+  const int N = G.n_tokens;
+  const int npos = N - 1;
+  const int nwords = (npos + 31) >> 5;
+  const int nq = (npos + 3) >> 2;
+  const uint32_t nthr = 0u - G.thr;
+
+  uint32_t *H = reinterpret_cast<uint32_t *>(smem);           // N + 1 bins
+  uint4 *U = reinterpret_cast<uint4 *>(smem + (((size_t)(N + 1) * 4 + 15) & ~(size_t)15));
+  for (int g = threadIdx.x; g <= N; g += blockDim.x) H[g] = 0u;
+  if (G.mode == MODE_STREAM)
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
+  __syncthreads();
+
+  uint32_t ones = 0;  // segments of length 1 counted by this thread
+  for (uint64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+    if (G.mode != MODE_STREAM) {  // a = 0: N segments of 1; a = 1: one segment of N
+      if (G.mode == MODE_ALL_REJECT) ones += (uint32_t)N;
+      else if (N == 1) ones += 1u;
+      else atomicAdd(&H[N], 1u);
+      continue;
+    }
+    const TrialHalf th = philox_trial_half((uint32_t)t, P.keys);
+    int lastz = 0;     // position of the last zero (0: the sentinel before position 1)
+    uint32_t cin = 1;  // position 32w is a zero (the sentinel for w = 0)
+    for (int w = 0; w < nwords; ++w) {
+      uint32_t R = 0u;
+      const int ncalls = min(8, nq - 8 * w);
+      if (ncalls == 8) {
+#pragma unroll
+        for (int j = 7; j >= 0; --j) R = pack4(R, philox_call(U[8 * w + j], th, P.keys), nthr);
+      } else {
+        for (int j = ncalls - 1; j >= 0; --j) R = pack4(R, philox_call(U[8 * w + j], th, P.keys), nthr);
+      }
+      const int rem = npos - 32 * w;
+      if (rem < 32) R &= (1u << rem) - 1u;
+      // a zero whose predecessor is a zero ends a segment of length 1
+      const uint32_t single = R & ((R << 1) | cin);
+      ones += __popc(single);
+      uint32_t Z = R & ~single;  // zeros ending a segment of length >= 2
+      while (Z) {
+        const int b = __ffs(Z) - 1;  // bit b is position 32w + b + 1
+        Z &= Z - 1u;
+        const uint32_t below = R & ((1u << b) - 1u);
+        const int prev = below ? 32 * w + 32 - __clz(below) : lastz;  // the previous zero
+        atomicAdd(&H[32 * w + b + 1 - prev], 1u);
+      }
+      if (R) lastz = 32 * w + 32 - __clz(R);
+      cin = R >> 31;
+    }
+    const int gl = N - lastz;  // the final segment ends at N
+    if (gl == 1) ones += 1u;
+    else atomicAdd(&H[gl], 1u);
+  }
+  // the g = 1 count: warp sums, one shared atomic per warp
+  unsigned long long o = warp_sum((unsigned long long)ones);
+  if ((threadIdx.x & 31) == 0 && o) atomicAdd(&H[1], (uint32_t)o);
+  __syncthreads();
+  unsigned long long *out = P.hist + G.hist_off;
+  for (int g = threadIdx.x; g <= N; g += blockDim.x) {
+    const uint32_t v = g == 0 ? (uint32_t)(t1 - t0) : H[g];
+    if (v) atomicAdd(out + g, (unsigned long long)v);
+  }
+}
+
+__global__ void __launch_bounds__(128) dsi_seg_eval_kernel(const SegParams P) {
+  const uint64_t c = P.cfg_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P.cfg_end) return;
+  const DevCfg cfg = P.cfg[c];
+  const SegGroup G = P.groups[P.cfg_group[c]];
+  const unsigned long long *H = P.hist + G.hist_off;
+  const SegCtx s = make_segctx(cfg);
+  const bool fresh = (cfg.flags & CFG_FRESH) != 0;
+  const int N = cfg.n_tokens;
+  unsigned long long sm = 0, si = 0, sd = 0;
+  for (int g = 1; g <= N; ++g) {
+    const unsigned long long h = __ldg(H + g);
+    if (!h) continue;
+    uint32_t M = 1u, S = 0u;  // SI iterations ceil(g/(k+1)) and S(ceil((g-1)/k)) of C(g)
+    if (g >= 2) {
+      const uint2 e = seg_extra(g, s);
+      M = e.x + 1u;
+      S = e.y;
+      if (fresh) S -= fresh_saving(g, s, cfg.t_d);
+    }
+    sm += h;
+    si += h * M;
+    sd += h * (unsigned long long)((uint32_t)cfg.t_t + S);
+  }
+  unsigned long long *acc = P.acc + c * NF;
+  acc[F_M] = sm;
+  acc[F_I] = si;
+  acc[F_DSI] = sd;
+  acc[F_TRIALS] = __ldg(H);
+}
+
+}  // namespace
+
+size_t seg_hist_smem(int max_n) {
+  return (((size_t)(max_n + 1) * 4 + 15) & ~(size_t)15) + (size_t)((max_n - 1 + 3) / 4 + 1) * sizeof(uint4);
+}
+
+int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream) {
+  if (n_units == 0) return 0;
+  const size_t smem = seg_hist_smem(p.max_n);
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(dsi_seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  SegParams q = p;
+  for (uint64_t done = 0; done < n_units;) {
+    const uint64_t n = (n_units - done) < 0x7fffffffull ? (n_units - done) : 0x7fffffffull;
+    q.unit_begin = p.unit_begin + done;
+    dsi_seg_hist_kernel<<<(unsigned)n, 128, smem, (cudaStream_t)stream>>>(q);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+    done += n;
+  }
+  return 0;
+}
+
+int launch_seg_eval(const SegParams &p, void *stream) {
+  if (p.cfg_end <= p.cfg_begin) return 0;
+  const uint64_t blocks = (p.cfg_end - p.cfg_begin + 127) / 128;
+  dsi_seg_eval_kernel<<<(unsigned)blocks, 128, 0, (cudaStream_t)stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace dsi

@@ -37,6 +37,14 @@ long_n = W.rows([(1.0, 0.1, 0.8, 5, 2, 5000, 0, 40), (1.0, 0.1, 0.8, 20, 2, 5000
 for flags in (0, FRESH):
     with D.Simulator(long_n, tick=0.01, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
+# means-only mode (dsi_seg.cu): histogram and evaluation passes, smem above 48 KB at N 8192
+for flags in (D.DSI_F_MEANS_ONLY, D.DSI_F_MEANS_ONLY | FRESH):
+    with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
+        sim.run().reduce()
+        sim.heatmap()
+with D.Simulator(W.rows([(1.0, 0.1, 0.97, 5, 2, 8192, 2, 40), (1.0, 0.1, 0.5, 1, 2, 300, 0, 1000)]),
+                 tick=0.01, seed=W.SEED, flags=D.DSI_F_MEANS_ONLY, n_shards=3) as sim:
+    sim.run().reduce()
 # multi-drafter kernel (dsi_multi.cu): D = 1, 2, 4, 7 variants, table and per-call q halves,
 # pattern mode and per-trial records, ragged tiles
 mf, mtick = W.multi_fuzz(20, seed=4, n_max=40, trials=70)

@@ -1,0 +1,132 @@
+"""GPU tests of the means-only mode (DSI_F_MEANS_ONLY, SURVEY 8(f) N3 "aggregate H[g]").
+
+Per group of configs that draw identical indicators, one pass builds the segment-length
+histogram H[g]; every config's sums follow by linearity over segments.  Those are the same
+integers the per-trial kernels add, so every sum (and hence every mean and every heatmap
+cell) must be bit-identical to the default mode, which is itself bit-exact against the
+oracle (tests/test_gpu_parity.py); a sample is also checked against the oracle directly."""
+import numpy as np
+import pytest
+
+from helpers import oracle_sums
+
+pytestmark = pytest.mark.gpu
+
+D = pytest.importorskip("paper_2405_14105_b200.dsi_sim")
+from paper_2405_14105_b200 import workloads as W  # noqa: E402
+
+SEED = W.SEED
+MEANS = D.DSI_F_MEANS_ONLY
+EXACT = ("trials", "nonsi_ticks", "sum_si_ticks", "sum_dsi_ticks", "sum_si_iters", "sum_accepts",
+         "sum_segments", "threshold", "eq1_feasible", "min_lookahead", "mean_nonsi", "mean_si", "mean_dsi")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def results(cfgs, tick, flags=0, **kw):
+    with D.Simulator(cfgs, tick=tick, seed=SEED, flags=flags, **kw) as sim:
+        return sim.run().reduce(), sim.run().heatmap()
+
+
+def assert_same_sums(got, want, ctx=""):
+    for f in EXACT:
+        assert np.array_equal(got[f], want[f]), (ctx, f)
+    assert (got["sumsq_si_ticks"] == 0).all() and (got["sumsq_dsi_ticks"] == 0).all()
+    assert np.isnan(got["std_si"]).all() and np.isnan(got["std_dsi"]).all()
+    assert (got["n_dsi_gt_nonsi"] == -1).all() and (got["n_dsi_gt_si"] == -1).all()
+
+
+def assert_cells_equal(a, b, ctx=""):
+    for f in a.dtype.names:
+        x, y = a[f], b[f]
+        if x.dtype.kind == "f":
+            assert np.array_equal(np.isnan(x), np.isnan(y)) and np.array_equal(x[~np.isnan(x)], y[~np.isnan(y)]), (ctx, f)
+        else:
+            assert np.array_equal(x, y), (ctx, f)
+
+
+@pytest.mark.parametrize("name", ["fuzz", "cfg2", "cfg3", "cfg4", "long", "fresh"])
+def test_sums_and_heatmap_bit_identical_to_default(name):
+    flags = 0
+    if name == "fuzz":
+        cfgs, tick = W.fuzz(160, seed=11, trials=300)
+    elif name == "cfg2":
+        cfgs, tick = W.cfg2(trials=3000)
+    elif name == "cfg3":
+        cfgs, tick = W.cfg3(trials=500, k_max=200, cells=slice(1, 10100, 41))
+    elif name == "cfg4":
+        cfgs, tick = W.cfg4(trials=777)
+    elif name == "long":  # N up to 8192 (the mode's limit): multi-word walks, 64 KB of smem
+        cfgs = W.rows([(1.0, 0.05, 0.9, 3, 7, 1000, 0, 257), (1.0, 0.3, 0.5, 2, 3, 4097, 1, 65),
+                       (1.0, 0.1, 0.97, 5, 2, 8192, 2, 40), (1.0, 1.0, 0.0, 1, 1, 8192, 0, 9),
+                       (1.0, 0.2, 1.0, 4, 2, 8192, 0, 9)])
+        tick = 0.01
+    else:
+        cfgs, tick = W.cfg4(trials=500)
+        flags = D.DSI_F_FRESH_VERIFIER
+    want, want_cells = results(cfgs, tick, flags)
+    got, got_cells = results(cfgs, tick, flags | MEANS)
+    assert_same_sums(got, want, name)
+    assert_cells_equal(got_cells, want_cells, name)
+
+
+def test_sample_against_oracle():
+    cfgs, tick = W.cfg3(trials=300, k_max=20, cells=slice(5, 10100, 401))
+    got, _ = results(cfgs, tick, MEANS)
+    for i in range(0, cfgs.size, 7):
+        want = oracle_sums(cfgs[i], tick, SEED)
+        assert int(got[i]["sum_dsi_ticks"]) == want["sum_dsi"] and int(got[i]["sum_si_ticks"]) == want["sum_si"]
+        assert int(got[i]["sum_segments"]) == want["sum_m"] and int(got[i]["sum_accepts"]) == want["sum_acc"]
+
+
+@pytest.mark.parametrize("kw", [{"n_shards": 3}, {"n_shards": 11}, {"nccl": True}])
+def test_partition_and_one_rank_nccl(kw):
+    cfgs, tick = W.cfg3(trials=700, k_max=20, cells=slice(2, 10100, 97))
+    want, want_cells = results(cfgs, tick, MEANS)
+    extra = {"nccl_id": D.dsi_nccl_unique_id()} if kw.get("nccl") else kw
+    got, got_cells = results(cfgs, tick, MEANS, **extra)
+    for f in EXACT:
+        assert np.array_equal(got[f], want[f]), f
+    assert_cells_equal(got_cells, want_cells)
+
+
+def test_update_keeps_groups_or_refuses():
+    cfgs, tick = W.cfg3(trials=400, k_max=10, cells=slice(0, 10100, 211))
+    other = cfgs.copy()
+    other["lookahead"] = np.maximum(1, 11 - other["lookahead"])  # same indicator groups
+    other["t_drafter"] = np.round(np.minimum(1.0, other["t_drafter"] * 2), 2)
+    with D.Simulator(cfgs, tick=tick, seed=SEED, flags=MEANS) as sim:
+        sim.run().reduce()
+        got = sim.update(other).run().reduce()
+        want, _ = results(other, tick, 0)
+        for f in EXACT:
+            assert np.array_equal(got[f], want[f]), f
+        bad = other.copy()
+        bad["accept_rate"][0] = 0.333  # a new indicator group
+        with pytest.raises(D.DsiError) as e:
+            sim.update(bad)
+        assert e.value.status == D.DSI_E_RANGE
+        again = sim.run().reduce()  # the handle keeps `other`
+        for f in EXACT:
+            assert np.array_equal(again[f], want[f]), f
+
+
+def test_options_validated():
+    cfgs, tick = W.fuzz(8, seed=3, trials=20)
+    for flags in (D.DSI_F_PER_TRIAL, D.DSI_F_HIST, D.DSI_F_PATTERN, D.DSI_F_SHARED_STREAMS):
+        with pytest.raises(D.DsiError) as e:
+            D.Simulator(cfgs, tick=tick, seed=SEED, flags=MEANS | flags)
+        assert e.value.status == D.DSI_E_RANGE
+    ttft, ttick = W.cfg2_ttft(trials=10)
+    with pytest.raises(D.DsiError) as e:
+        D.Simulator(ttft, tick=ttick, seed=SEED, flags=MEANS)
+    assert e.value.status == D.DSI_E_RANGE
+    big = W.rows([(1.0, 0.1, 0.5, 2, 2, 8193, 0, 4)])
+    with pytest.raises(D.DsiError) as e:
+        D.Simulator(big, tick=0.01, seed=SEED, flags=MEANS)
+    assert e.value.status == D.DSI_E_RANGE
