@@ -481,6 +481,47 @@ def ours(args):
                       "h2d_bytes_per_step": int(h2d_c), "d2h_bytes_per_step": int(d2h_c)}
         simc.close()
 
+    # means-only mode (DSI_F_MEANS_ONLY): segment-length histograms per indicator group,
+    # per-config sums by linearity -- sums, means and heatmap cells identical to the value run
+    means = None
+    heat_means_s = None
+    if not args.no_means:
+        resm = np.zeros(cfgs.size, D.RESULT_DTYPE)
+        simm = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_MEANS_ONLY, **kw)
+        streamm = torch.cuda.ExternalStream(simm.stream(), device=torch.device("cuda", local))
+        for _ in range(args.warmup):
+            simm.run()
+            simm.reduce(resm)
+        barrier()
+        torch.cuda.synchronize()
+        m_ms, m_kern = [], []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(streamm)
+            simm.run()
+            simm.reduce(resm)
+            ev1.record(streamm)
+            ev1.synchronize()
+            m_ms.append(ev0.elapsed_time(ev1))
+            m_kern.append(simm.kernel_ms())
+        barrier()
+        m_total = max_over_ranks(sum(m_ms))
+        same = all(np.array_equal(resm[f], res[f]) for f in
+                   ("sum_si_ticks", "sum_dsi_ticks", "sum_segments", "sum_si_iters", "trials",
+                    "mean_si", "mean_dsi"))
+        heat_means_s, cells_means = heatmap_grid_times(simm, flush, args.steps)
+        means = {"value": tt * args.steps / (m_total / 1000.0), "unit": UNIT,
+                 "ms_per_step": m_total / args.steps, "kernel_ms": max_over_ranks(statistics.mean(m_kern)),
+                 "launches_per_step": simm.launches(), "sums_and_means_identical_to_value_run": bool(same),
+                 "note": "DSI_F_MEANS_ONLY: one pass per indicator group builds the segment-length "
+                         "histogram H[g]; each config's sums = sum_g H[g] x segment cost (linearity over "
+                         "segments), identical integers to the value run; no second moments or per-trial "
+                         "counters. ms_per_step includes dsi_sim_reduce of all configs (D2H + finalize)."}
+        simm.close()
+
     # "heatmap grid time" (BASELINE metric): run + all-reduce + on-device
     # per-cell argmin over k + the four ratio panels + D2H of the cells, end to end on the
     # host clock (dsi_sim_heatmap), in both modes; the cells must equal the
@@ -496,10 +537,14 @@ def ours(args):
         same_cells = cells_equal(cells, host_cells)
         if crn is not None:
             same_cells = same_cells and cells_equal(cells_shared, host_cells)
+        if means is not None:
+            same_cells = same_cells and cells_equal(cells_means, host_cells)
         i = int(np.nanargmax(cells["r_min_dsi"]))
         heat = {"cells": int(cells.size),
                 "grid_time_s": grid_s,
                 "grid_time_shared_streams_s": grid_shared_s,
+                "grid_time_means_only_s": (max_over_ranks(statistics.median(heat_means_s))
+                                           if heat_means_s else None),
                 "host_product_s": host_product_s,
                 "device_cells_equal_host_product": bool(same_cells),
                 "max_r_min_dsi": float(cells["r_min_dsi"][i]),
@@ -507,7 +552,9 @@ def ours(args):
                        "si_lookahead": int(cells["si_lookahead"][i]),
                        "dsi_lookahead": int(cells["dsi_lookahead"][i])},
                 "note": "grid time = dsi_sim_run + dsi_sim_heatmap (all-reduce, one warp per cell on "
-                        "the device, D2H of 10100 cells), host wall clock, median of the timed steps"}
+                        "the device, D2H of 10100 cells), host wall clock, median of the timed steps; "
+                        "per-config, shared-stream and means-only modes, cells compared with the host "
+                        "product of the value run"}
     # e2e through the public API with host buffers: update (validate + pinned H2D of the
     # config table) + run + reduce (all-reduce + D2H of the moments + FP64 finalise)
     h2d, d2h = sim.io_bytes()
@@ -598,6 +645,7 @@ def ours(args):
             "gpu_launches": launches,
             "heatmap": heat,
             "shared_streams": crn,
+            "means_only": means,
             "multi_drafter": multi,
             "clocks": clk,
             "create_s": create_s,
@@ -623,6 +671,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-shared-streams", action="store_true")
     ap.add_argument("--no-multi", action="store_true", help="skip the multi-drafter block")
+    ap.add_argument("--no-means", action="store_true", help="skip the means-only block")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
