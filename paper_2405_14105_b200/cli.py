@@ -4,7 +4,7 @@
     python -m paper_2405_14105_b200 simulate --t-target 20.6 --t-drafter 6.8 --accept 0.93 \
         --lookahead 5 --sp 7 --n-tokens 50 --trials 100000 --tick 0.1
     python -m paper_2405_14105_b200 table2 [--trials 100000] [--sp 8] [--n-tokens 100]
-    python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200 | --k 5] [--csv out.csv] [--shared|--fresh]
+    python -m paper_2405_14105_b200 heatmap [--trials 10000] [--k-max 200 | --k 5] [--csv out.csv] [--shared|--means] [--fresh]
     python -m paper_2405_14105_b200 multi --t-target 1.0 --drafter 0.02:0.5 --drafter 0.1:0.8 \
         --n-tokens 100 [--trials 100000]
 
@@ -73,7 +73,8 @@ def cmd_heatmap(a) -> dict:
         cfgs, tick = W.cfg3(trials=a.trials, k_min=a.k, k_max=a.k, sp=a.sp, n_tokens=a.n_tokens)
     else:
         cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
-    flags = (D.DSI_F_SHARED_STREAMS if a.shared else 0) | (D.DSI_F_FRESH_VERIFIER if a.fresh else 0)
+    flags = ((D.DSI_F_SHARED_STREAMS if a.shared else 0) | (D.DSI_F_FRESH_VERIFIER if a.fresh else 0) |
+             (D.DSI_F_MEANS_ONLY if a.means else 0))
     with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags) as sim:
         cells = sim.run().heatmap()
     if a.csv:
@@ -135,6 +136,7 @@ def main(argv=None) -> int:
     p.add_argument("--n-tokens", type=int, default=100)
     p.add_argument("--csv", default=None)
     p.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
+    p.add_argument("--means", action="store_true", help="DSI_F_MEANS_ONLY (segment histograms; no std)")
     p.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER (DESIGN.md R24)")
     p = sub.add_parser("multi", help="Alg. 1 with several drafters (lookahead 1, unbounded threads)")
     p.add_argument("--t-target", type=float, required=True)

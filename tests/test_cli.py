@@ -138,3 +138,13 @@ def test_multi_cli_expectation():
     mean, sd = 1.0 + 99 * e1, (99 * (e2 - e1 * e1)) ** 0.5
     assert abs(r["mean_dsi"] - mean) <= 6 * sd / 100000 ** 0.5
     assert r["n_dsi_gt_nonsi"] == 0 and r["models"] == 3
+
+
+@pytest.mark.gpu
+def test_heatmap_cli_means_only_matches_shared(tmp_path):
+    """--means (segment histograms) writes the same CSV as --shared (per-trial evaluation)."""
+    a, b = tmp_path / "means.csv", tmp_path / "shared.csv"
+    for path, flag in ((a, "--means"), (b, "--shared")):
+        rc, out, err = run_cli("heatmap", "--trials", "400", "--k-max", "20", "--csv", str(path), flag)
+        assert rc == 0, err
+    assert a.read_text() == b.read_text()
