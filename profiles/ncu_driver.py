@@ -20,6 +20,7 @@ ap.add_argument("--workload", default="cfg3")
 ap.add_argument("--stride", type=int, default=10)
 ap.add_argument("--runs", type=int, default=1)
 ap.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
+ap.add_argument("--means", action="store_true", help="DSI_F_MEANS_ONLY")
 args = ap.parse_args()
 if args.workload == "cfg3":
     cfgs, tick = W.cfg3(cells=slice(None, None, args.stride))
@@ -28,7 +29,8 @@ elif args.workload == "cfg5":
     cfgs = cfgs[:: args.stride]
 else:
     raise SystemExit("workload")
-with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_SHARED_STREAMS if args.shared else 0) as sim:
+flags = (D.DSI_F_SHARED_STREAMS if args.shared else 0) | (D.DSI_F_MEANS_ONLY if args.means else 0)
+with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
     for _ in range(args.runs):
         sim.run()
         sim.reduce()

@@ -2,7 +2,7 @@
 #   1. launch list of the bench command (every launch with its device time);
 #   2. DRAM bytes of one full bench launch (cfg3, 6.06 M blocks) -> roofline.traffic;
 #   3. --set full on the same kernel over 1/20 of the heatmap (same per-config mix);
-#   4. --set full on the shared-stream kernel and on the multi-drafter kernel.
+#   4. --set full on the shared-stream kernel, the multi-drafter kernel and the means-only kernels.
 # Then profiles/summarize_ncu.py turns them into profiles/latest_ncu_summary.json.
 set -u
 R=${1:-r01}
@@ -22,4 +22,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsi_
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsi_multi -c 1 \
   -o gpurun_out/prof_multi_${R} python profiles/ncu_multi_driver.py 0.5 \
   > gpurun_out/ncu_full_multi_${R}.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsi_seg -c 2 \
+  -o gpurun_out/prof_means_${R} python profiles/ncu_driver.py --workload cfg3 --stride 1 --means \
+  > gpurun_out/ncu_full_means_${R}.log 2>&1
 echo done

@@ -135,6 +135,10 @@ try:  # the multi-drafter kernel on W.multi_heatmap (profiles/profile_round.sh)
     out["source_hotspots_multi"] = hotspots(os.path.join(OUT, f"prof_multi_{R}.ncu-rep"))
 except (OSError, ValueError, IndexError) as e:
     out["multi_error"] = str(e)
+try:  # the means-only passes on the full cfg3 grid (the longer of the two is summarised)
+    out["set_full_means"], out["instruction_mix_means"] = full(f"prof_means_{R}")
+except (OSError, ValueError, IndexError) as e:
+    out["means_error"] = str(e)
 for name in (f"{R}_ncu_summary.json", "latest_ncu_summary.json"):
     with open(os.path.join(ROOT, "profiles", name), "w") as f:
         json.dump(out, f, indent=1)
