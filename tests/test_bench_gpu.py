@@ -1,0 +1,33 @@
+"""bench.py end to end on a small workload (the driver runs it at round end): one JSON line
+with the contract's keys, every sub-block present and consistent."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_bench_json_line_small_workload():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "cfg2", "--steps", "2",
+                        "--warmup", "3", "--cpu-seconds", "2"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks",
+              "cpu_baseline", "heatmap", "shared_streams", "means_only", "multi_drafter"):
+        assert k in d, k
+    assert d["value"] > 0 and d["gpu_launches"] > 0 and d["steps"] == 2 and d["warmup"] == 3
+    assert 0 < d["roofline"]["frac"] <= 1.0
+    assert d["heatmap"]["device_cells_equal_host_product"] is True
+    assert d["shared_streams"]["bit_identical_to_value_run"] is True
+    assert d["means_only"]["sums_and_means_identical_to_value_run"] is True
+    assert d["multi_drafter"]["value"] > 0 and 0 < d["multi_drafter"]["roofline"]["frac"] <= 1.0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
