@@ -381,12 +381,17 @@ def ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return int(t.item())
 
-    nccl_id = None
-    if world > 1:
+    def fresh_nccl_id():
+        """A new NCCL unique id for each handle (an id serves one communicator): made on rank 0,
+        broadcast to all ranks (every rank calls this in the same order)."""
+        if world == 1:
+            return None
         obj = [D.dsi_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    kw = dict(tick=tick, seed=W.SEED, device=local, rank=rank, world=world, nccl_id=nccl_id)
+        return obj[0]
+
+    base_kw = dict(tick=tick, seed=W.SEED, device=local, rank=rank, world=world)
+    kw = dict(base_kw, nccl_id=fresh_nccl_id())
 
     t_create = time.perf_counter()
     sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING, **kw)
@@ -436,7 +441,7 @@ def ours(args):
     # because it changes what a simulated trial-token costs.  Its sums must be bit-identical.
     crn = None
     if not args.no_shared_streams:
-        simc = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_SHARED_STREAMS, **kw)
+        simc = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_SHARED_STREAMS, nccl_id=fresh_nccl_id(), **base_kw)
         streamc = torch.cuda.ExternalStream(simc.stream(), device=torch.device("cuda", local))
         for _ in range(args.warmup):
             simc.run()
@@ -487,7 +492,7 @@ def ours(args):
     heat_means_s = None
     if not args.no_means:
         resm = np.zeros(cfgs.size, D.RESULT_DTYPE)
-        simm = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_MEANS_ONLY, **kw)
+        simm = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_MEANS_ONLY, nccl_id=fresh_nccl_id(), **base_kw)
         streamm = torch.cuda.ExternalStream(simm.stream(), device=torch.device("cuda", local))
         for _ in range(args.warmup):
             simm.run()

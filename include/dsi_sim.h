@@ -125,7 +125,9 @@ typedef struct {
                              total device count world*n_devices > 1.  With one device, a
                              non-NULL id still routes the reduction through a one-rank NCCL
                              communicator.  Obtain it with dsi_nccl_unique_id on one rank
-                             and broadcast it.                                              */
+                             and broadcast it; use a fresh id for every handle (an id serves
+                             one communicator: a second init with it fails with DSI_E_COMM,
+                             profiles/nccl_id_reuse.py).                                    */
   int32_t n_shards;       /* 0 or 1: normal.  > 1 (test only, single device): split the work
                              into n_shards cost-balanced shards run back to back on one
                              device, exercising the same partition code as multi-GPU.     */
@@ -224,7 +226,8 @@ const char *dsi_last_create_error(void);          /* thread-local message of the
                                                      dsi_sim_create                          */
 uint32_t dsi_abi_version(void);
 
-/* 128-byte NCCL unique id for multi-GPU runs (call on one rank, broadcast). */
+/* 128-byte NCCL unique id for multi-GPU runs (call on one rank, broadcast); one per handle
+ * (or per dsi_multi_simulate call). */
 dsi_status dsi_nccl_unique_id(uint8_t id[128]);
 
 /* Pure planner helpers of Eq. 1, exact integers.
