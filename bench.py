@@ -534,6 +534,7 @@ def ours(args):
     heat_s, cells = heatmap_grid_times(sim, flush, args.steps)
     grid_s = max_over_ranks(statistics.median(heat_s))
     grid_shared_s = max_over_ranks(statistics.median(heat_shared_s)) if crn is not None else None
+    grid_means_s = max_over_ranks(statistics.median(heat_means_s)) if heat_means_s else None  # (collective)
     heat = None
     if rank == 0:
         t0 = time.perf_counter()
@@ -548,8 +549,7 @@ def ours(args):
         heat = {"cells": int(cells.size),
                 "grid_time_s": grid_s,
                 "grid_time_shared_streams_s": grid_shared_s,
-                "grid_time_means_only_s": (max_over_ranks(statistics.median(heat_means_s))
-                                           if heat_means_s else None),
+                "grid_time_means_only_s": grid_means_s,
                 "host_product_s": host_product_s,
                 "device_cells_equal_host_product": bool(same_cells),
                 "max_r_min_dsi": float(cells["r_min_dsi"][i]),
