@@ -93,7 +93,7 @@ typedef enum {
                                  default mode, so sums, means and dsi_sim_heatmap are
                                  bit-identical.  Second moments and per-trial counters are not
                                  produced: sumsq_* = 0, std_* = NaN, n_dsi_gt_* = -1.  Not with
-                                 PER_TRIAL, HIST, PATTERN, SHARED_STREAMS or TTFT; N <= 8192;
+                                 PER_TRIAL, HIST, PATTERN, SHARED_STREAMS or TTFT;
                                  dsi_sim_update keeps (stream_id, a, N, n_trials) per config.    */
 
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */

@@ -39,7 +39,7 @@ constexpr uint64_t kMaxTrials = 1ull << 32;
 constexpr int kDefaultThreads = 128;
 constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size when 256 does not fit (see plan_shared)
 constexpr size_t kReduceChunks = 8;  // dsi_sim_reduce: D2H chunks overlapped with the finalize
-constexpr int kMeansMaxN = 8192;   // means-only mode: a block's histogram and q halves in smem
+constexpr int kMeansMaxN = kMaxTokens;  // means-only mode (smem histograms up to N 8192, global above)
 constexpr int kCrnMaxN = 2048;     // shared-stream mode: 128 per-trial run lists of <= N/3+2
                                    // u16 entries fit shared memory (209 KB at N 2048)
 
@@ -1101,7 +1101,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   std::vector<double> crn_cost;
   if (means_only) {
     if (h->any_ttft || h->max_n > kMeansMaxN) {
-      h->err = "DSI_F_MEANS_ONLY: no TTFT configs, N <= 8192";
+      h->err = "DSI_F_MEANS_ONLY: no TTFT configs";
       return abort_create(DSI_E_RANGE);
     }
     s = plan_means(h, crn_cost, 148ull * 16 * (uint64_t)total_devices);

@@ -24,6 +24,11 @@
 namespace dsi {
 namespace {
 
+constexpr int SEG_SMEM_MAX_N = 8192;  // 4(N+1) + 16 N/4 bytes = 64 KB of shared memory
+
+// SMEM: the block's histogram and q halves in shared memory (N <= 8192); else segments go to
+// the group's histogram in global memory with 64-bit atomics and the q halves are per call.
+template <bool SMEM>
 __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t s_grp;
@@ -49,17 +54,24 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
 
   uint32_t *H = reinterpret_cast<uint32_t *>(smem);           // N + 1 bins
   uint4 *U = reinterpret_cast<uint4 *>(smem + (((size_t)(N + 1) * 4 + 15) & ~(size_t)15));
-  for (int g = threadIdx.x; g <= N; g += blockDim.x) H[g] = 0u;
-  if (G.mode == MODE_STREAM)
-    for (int q = threadIdx.x; q < nq; q += blockDim.x) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
-  __syncthreads();
+  unsigned long long *out = P.hist + G.hist_off;
+  auto add = [&](int g) {
+    if (SMEM) atomicAdd(&H[g], 1u);
+    else atomicAdd(out + g, 1ull);
+  };
+  if (SMEM) {
+    for (int g = threadIdx.x; g <= N; g += blockDim.x) H[g] = 0u;
+    if (G.mode == MODE_STREAM)
+      for (int q = threadIdx.x; q < nq; q += blockDim.x) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
+    __syncthreads();
+  }
 
   uint32_t ones = 0;  // segments of length 1 counted by this thread
   for (uint64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
     if (G.mode != MODE_STREAM) {  // a = 0: N segments of 1; a = 1: one segment of N
       if (G.mode == MODE_ALL_REJECT) ones += (uint32_t)N;
       else if (N == 1) ones += 1u;
-      else atomicAdd(&H[N], 1u);
+      else add(N);
       continue;
     }
     const TrialHalf th = philox_trial_half((uint32_t)t, P.keys);
@@ -70,9 +82,15 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
       const int ncalls = min(8, nq - 8 * w);
       if (ncalls == 8) {
 #pragma unroll
-        for (int j = 7; j >= 0; --j) R = pack4(R, philox_call(U[8 * w + j], th, P.keys), nthr);
+        for (int j = 7; j >= 0; --j) {
+          const uint4 u = SMEM ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), G.stream_id, P.keys);
+          R = pack4(R, philox_call(u, th, P.keys), nthr);
+        }
       } else {
-        for (int j = ncalls - 1; j >= 0; --j) R = pack4(R, philox_call(U[8 * w + j], th, P.keys), nthr);
+        for (int j = ncalls - 1; j >= 0; --j) {
+          const uint4 u = SMEM ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), G.stream_id, P.keys);
+          R = pack4(R, philox_call(u, th, P.keys), nthr);
+        }
       }
       const int rem = npos - 32 * w;
       if (rem < 32) R &= (1u << rem) - 1u;
@@ -85,20 +103,24 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
         Z &= Z - 1u;
         const uint32_t below = R & ((1u << b) - 1u);
         const int prev = below ? 32 * w + 32 - __clz(below) : lastz;  // the previous zero
-        atomicAdd(&H[32 * w + b + 1 - prev], 1u);
+        add(32 * w + b + 1 - prev);
       }
       if (R) lastz = 32 * w + 32 - __clz(R);
       cin = R >> 31;
     }
     const int gl = N - lastz;  // the final segment ends at N
     if (gl == 1) ones += 1u;
-    else atomicAdd(&H[gl], 1u);
+    else add(gl);
   }
   // the g = 1 count: warp sums, one shared atomic per warp
   unsigned long long o = warp_sum((unsigned long long)ones);
+  if (!SMEM) {
+    if ((threadIdx.x & 31) == 0 && o) atomicAdd(out + 1, o);
+    if (threadIdx.x == 0) atomicAdd(out, (unsigned long long)(t1 - t0));
+    return;
+  }
   if ((threadIdx.x & 31) == 0 && o) atomicAdd(&H[1], (uint32_t)o);
   __syncthreads();
-  unsigned long long *out = P.hist + G.hist_off;
   for (int g = threadIdx.x; g <= N; g += blockDim.x) {
     const uint32_t v = g == 0 ? (uint32_t)(t1 - t0) : H[g];
     if (v) atomicAdd(out + g, (unsigned long long)v);
@@ -144,17 +166,21 @@ size_t seg_hist_smem(int max_n) {
 
 int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream) {
   if (n_units == 0) return 0;
-  const size_t smem = seg_hist_smem(p.max_n);
+  const bool use_smem = p.max_n <= SEG_SMEM_MAX_N;
+  const size_t smem = use_smem ? seg_hist_smem(p.max_n) : 0;
   if (smem > 48 * 1024) {
     const cudaError_t e =
-        cudaFuncSetAttribute(dsi_seg_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(dsi_seg_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
   SegParams q = p;
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < 0x7fffffffull ? (n_units - done) : 0x7fffffffull;
     q.unit_begin = p.unit_begin + done;
-    dsi_seg_hist_kernel<<<(unsigned)n, 128, smem, (cudaStream_t)stream>>>(q);
+    if (use_smem)
+      dsi_seg_hist_kernel<true><<<(unsigned)n, 128, smem, (cudaStream_t)stream>>>(q);
+    else
+      dsi_seg_hist_kernel<false><<<(unsigned)n, 128, 0, (cudaStream_t)stream>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;

@@ -50,7 +50,7 @@ def assert_cells_equal(a, b, ctx=""):
             assert np.array_equal(x, y), (ctx, f)
 
 
-@pytest.mark.parametrize("name", ["fuzz", "cfg2", "cfg3", "cfg4", "long", "fresh"])
+@pytest.mark.parametrize("name", ["fuzz", "cfg2", "cfg3", "cfg4", "long", "maxn", "fresh"])
 def test_sums_and_heatmap_bit_identical_to_default(name):
     flags = 0
     if name == "fuzz":
@@ -61,10 +61,14 @@ def test_sums_and_heatmap_bit_identical_to_default(name):
         cfgs, tick = W.cfg3(trials=500, k_max=200, cells=slice(1, 10100, 41))
     elif name == "cfg4":
         cfgs, tick = W.cfg4(trials=777)
-    elif name == "long":  # N up to 8192 (the mode's limit): multi-word walks, 64 KB of smem
+    elif name == "long":  # N up to 8192 (shared-memory histograms, 64 KB)
         cfgs = W.rows([(1.0, 0.05, 0.9, 3, 7, 1000, 0, 257), (1.0, 0.3, 0.5, 2, 3, 4097, 1, 65),
                        (1.0, 0.1, 0.97, 5, 2, 8192, 2, 40), (1.0, 1.0, 0.0, 1, 1, 8192, 0, 9),
                        (1.0, 0.2, 1.0, 4, 2, 8192, 0, 9)])
+        tick = 0.01
+    elif name == "maxn":  # N above 8192 up to the ABI's 32768: global-memory histograms
+        cfgs = W.rows([(1.0, 0.1, 0.9, 4, 3, 32768, 0, 40), (1.0, 0.5, 0.6, 1, 1, 20000, 5, 33),
+                       (1.0, 0.05, 0.3, 2, 7, 8193, 1, 70), (1.0, 0.2, 0.0, 1, 2, 32768, 0, 3)])
         tick = 0.01
     else:
         cfgs, tick = W.cfg4(trials=500)
@@ -125,8 +129,4 @@ def test_options_validated():
     ttft, ttick = W.cfg2_ttft(trials=10)
     with pytest.raises(D.DsiError) as e:
         D.Simulator(ttft, tick=ttick, seed=SEED, flags=MEANS)
-    assert e.value.status == D.DSI_E_RANGE
-    big = W.rows([(1.0, 0.1, 0.5, 2, 2, 8193, 0, 4)])
-    with pytest.raises(D.DsiError) as e:
-        D.Simulator(big, tick=0.01, seed=SEED, flags=MEANS)
     assert e.value.status == D.DSI_E_RANGE
