@@ -130,3 +130,25 @@ def test_options_validated():
     with pytest.raises(D.DsiError) as e:
         D.Simulator(ttft, tick=ttick, seed=SEED, flags=MEANS)
     assert e.value.status == D.DSI_E_RANGE
+
+
+def test_exact_expectation_at_2_pow_32_trials():
+    """n_trials = 2^32 per config (every value of the trial counter word) is cheap in this mode:
+    the means sit within 6 sigma / sqrt(T) of the exact expectations (P11; tests/exact_math.py),
+    sigma taken from a 2e6-trial default run -- a relative resolution of ~1e-5."""
+    import math
+    from fractions import Fraction
+
+    import exact_math as X
+    T = 1 << 32
+    rows = [(1.0, 0.1, 0.8, 5, 2, 50, 0, T), (1.0, 0.3, 0.5, 3, 7, 100, 0, T)]
+    got, _ = results(W.rows(rows), 0.01, MEANS)
+    small = W.rows([r[:7] + (2_000_000,) for r in rows])
+    ref, _ = results(small, 0.01, 0)
+    for i, (tt, td, a, k, sp, N, _, _) in enumerate(rows):
+        p = Fraction(int(got[i]["threshold"]), 2 ** 32)
+        e = X.expectations(N, k, round(td * 100), round(tt * 100), sp, p)
+        assert int(got[i]["trials"]) == T
+        for mean, std, ex in ((got[i]["mean_dsi"], ref[i]["std_dsi"], e["dsi"]),
+                              (got[i]["mean_si"], ref[i]["std_si"], e["si"])):
+            assert abs(float(mean) / 0.01 - float(ex)) < 6 * (float(std) / 0.01) / math.sqrt(T), (i, mean, ex)
