@@ -2044,11 +2044,17 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     p.keys.k1[r] = s_hi + (uint32_t)r * 0xBB67AE85u;
   }
   const bool timing = opt->flags & DSI_F_TIMING;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  struct Events {  // destroyed on every exit path
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ~Events() {
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+    }
+  } ev;
   if (timing) {
-    MULTI_TRY(cudaEventCreate(&ev0));
-    MULTI_TRY(cudaEventCreate(&ev1));
-    MULTI_TRY(cudaEventRecord(ev0, stream));
+    MULTI_TRY(cudaEventCreate(&ev.e0));
+    MULTI_TRY(cudaEventCreate(&ev.e1));
+    MULTI_TRY(cudaEventRecord(ev.e0, stream));
   }
   int32_t launches = 0;
   for (int sh = 0; sh < shards; ++sh) {
@@ -2056,15 +2062,11 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     p.unit_begin = bounds[part];
     const uint64_t nu = bounds[part + 1] - bounds[part];
     const int le = dsi::launch_multi_kernel(p, nu, (opt->flags & DSI_F_PATTERN) != 0, stream);
-    if (le) {
-      if (ev0) cudaEventDestroy(ev0);
-      if (ev1) cudaEventDestroy(ev1);
-      return cuda_fail(nullptr, (cudaError_t)le, "dsi_multi_kernel launch");
-    }
+    if (le) return cuda_fail(nullptr, (cudaError_t)le, "dsi_multi_kernel launch");
     launches += (int32_t)((nu + 0x7ffffffeull) / 0x7fffffffull);
   }
   g_multi_launches = launches;
-  if (timing) MULTI_TRY(cudaEventRecord(ev1, stream));
+  if (timing) MULTI_TRY(cudaEventRecord(ev.e1, stream));
   if (use_nccl) {
     // one communicator for this call (ranks of the world, one device each), one all-reduce
     NcclApi &api = nccl();
@@ -2086,11 +2088,7 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   if (trial_settled)
     MULTI_TRY(cudaMemcpyAsync(trial_settled, b_set.p, rec * 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
   const cudaError_t se = cudaStreamSynchronize(stream);
-  if (timing) {
-    if (se == cudaSuccess) cudaEventElapsedTime(&g_multi_ms, ev0, ev1);
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-  }
+  if (timing && se == cudaSuccess) cudaEventElapsedTime(&g_multi_ms, ev.e0, ev.e1);
   if (se != cudaSuccess) return cuda_fail(nullptr, se, "dsi_multi_simulate");
   tr.mark("kernel+d2h");
 #undef MULTI_TRY
