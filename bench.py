@@ -151,11 +151,20 @@ def multi_drafter_block(steps: int, sm_max: float) -> dict:
         ws.append(time.perf_counter() - t0)
         ks.append(D.dsi_multi_last_kernel()[0])
     k_ms = statistics.median(ks)
+    # means-only: configs differing only in latencies share one pass (101 acceptance groups here)
+    ms_means = []
+    for _ in range(steps):
+        D.dsi_multi_simulate(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING | D.DSI_F_MEANS_ONLY)
+        ms_means.append(D.dsi_multi_last_kernel()[0])
     mults = multi_alg_multiplies(cfgs)
     return {"workload": "W.multi_heatmap: m = 3, f_1 (t 0.01, a 0.5) ahead of cfg3's 10100 (t_d, a) "
                         "points as f_2, t_m 1.0, N 100, 1e4 trials, lookahead 1 (Alg. 1 as stated)",
             "value": tt / (k_ms / 1000.0), "unit": UNIT, "kernel_ms": k_ms,
             "trial_tokens_per_step": tt, "gpu_launches": D.dsi_multi_last_kernel()[1],
+            "means_only": {"value": tt / (statistics.median(ms_means) / 1000.0), "unit": UNIT,
+                           "kernel_ms": statistics.median(ms_means),
+                           "note": "DSI_F_MEANS_ONLY: one pass per acceptance group, sums for every "
+                                   "latency by linearity; same sums and means, no std"},
             "e2e": {"value": tt / statistics.median(ws), "unit": UNIT,
                     "h2d_bytes_per_step": int(cfgs.size * 112 + (cfgs.size + 1) * 8),
                     "d2h_bytes_per_step": int(cfgs.size * 11 * 8)},

@@ -330,7 +330,11 @@ typedef struct {
  * nccl_id with world == 1 runs the same path on a one-rank communicator; n_shards > 1
  * (world == 1, tests) runs the partition's shards back to back.  Options used: abi_version,
  * tick, seed, device, rank, world, nccl_id, n_shards, stream, flags (DSI_F_PER_TRIAL (world
- * == 1), DSI_F_PATTERN, DSI_F_TIMING only).  out[n_cfg] is written on success.  With DSI_F_PER_TRIAL (else both must be NULL): trial_dsi[i] and
+ * == 1), DSI_F_PATTERN, DSI_F_TIMING, DSI_F_MEANS_ONLY only).  out[n_cfg] is written on success.
+ * DSI_F_MEANS_ONLY: j*(p) depends on the indicators only, so configs with equal (stream_id, N,
+ * n_trials, thresholds) share one kernel pass and every config's sum_dsi_ticks = t_m (T +
+ * sum_settled[m-1]) + sum_j t_j sum_settled[j] exactly (bit-identical sums and means, e.g. for a
+ * latency grid); sumsq_dsi_ticks = 0 and std_dsi = NaN (n_dsi_gt_nonsi stays exact: 0).  With DSI_F_PER_TRIAL (else both must be NULL): trial_dsi[i] and
  * trial_settled[8 i + j-1] for i = the trial's position in config-major order (config c's
  * trials follow those of configs < c), either pointer may be NULL.  Validation as
  * dsi_sim_create (DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW when N t_m >= 2^31 ticks or

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -1874,8 +1875,11 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   if (opt->abi_version != DSI_ABI_VERSION) return fail(nullptr, DSI_E_RANGE, "abi_version mismatch");
   if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
-  if (opt->flags & ~(DSI_F_PER_TRIAL | DSI_F_PATTERN | DSI_F_TIMING))
-    return fail(nullptr, DSI_E_RANGE, "multi-drafter mode takes PER_TRIAL, PATTERN and TIMING only");
+  if (opt->flags & ~(DSI_F_PER_TRIAL | DSI_F_PATTERN | DSI_F_TIMING | DSI_F_MEANS_ONLY))
+    return fail(nullptr, DSI_E_RANGE, "multi-drafter mode takes PER_TRIAL, PATTERN, TIMING and MEANS_ONLY only");
+  const bool means = opt->flags & DSI_F_MEANS_ONLY;
+  if (means && (opt->flags & DSI_F_PER_TRIAL))
+    return fail(nullptr, DSI_E_RANGE, "DSI_F_MEANS_ONLY excludes DSI_F_PER_TRIAL");
   if (opt->n_devices != 1 || opt->device < 0)
     return fail(nullptr, DSI_E_RANGE, "multi-drafter mode drives one device per process (n_devices = 1)");
   if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
@@ -1955,16 +1959,45 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     max_n = std::max(max_n, c.n_tokens);
     max_d = std::max(max_d, c.n_drafters);
   }
+  // Means-only: j*(p) depends on the indicators only, never on the latencies, so configs with
+  // equal (stream_id, N, T, thresholds) have equal settled-by counts per trial.  The kernel runs
+  // one representative per such group; every config's sum of L = t_m (T + sum S_m) +
+  // sum_j t_j sum S_j follows from the representative's exact sums (no second moments).
+  std::vector<uint32_t> rep_of(n_cfg);
+  for (size_t i = 0; i < n_cfg; ++i) rep_of[i] = (uint32_t)i;
+  size_t nk = n_cfg;  // configs the kernel runs
+  std::vector<dsi::MultiCfg> orig;  // means-only: every config's latencies (dc then holds the representatives)
+  if (means) {
+    std::map<std::vector<uint64_t>, uint32_t> seen;
+    std::vector<dsi::MultiCfg> kc;
+    std::vector<uint64_t> kprefix(1, 0);
+    for (size_t i = 0; i < n_cfg; ++i) {
+      const dsi::MultiCfg &d = dc[i];
+      std::vector<uint64_t> key = {d.stream_id, (uint64_t)d.n_tokens, d.n_trials, (uint64_t)d.n_drafters};
+      for (int j = 0; j < d.n_drafters; ++j) key.push_back(((uint64_t)d.mode[j] << 32) | d.thr[j]);
+      auto it = seen.find(key);
+      if (it == seen.end()) {
+        it = seen.emplace(key, (uint32_t)kc.size()).first;
+        kc.push_back(d);
+        kprefix.push_back(kprefix.back() + (d.n_trials + tile - 1) / tile);
+      }
+      rep_of[i] = it->second;
+    }
+    nk = kc.size();
+    orig.swap(dc);
+    dc.swap(kc);
+    prefix.swap(kprefix);
+  }
   // units (config, tile of trials) split into world x shards contiguous ranges of equal expected
   // cost (trials x Philox calls a drafter must make, as bench.py's multi_alg_multiplies); this
   // rank runs its ranges, the per-config moments are summed with one NCCL all-reduce
-  const uint64_t n_units = prefix[n_cfg];
+  const uint64_t n_units = prefix[nk];
   const int shards = std::max(1, opt->n_shards);
   const int parts = opt->world * shards;
   std::vector<uint64_t> bounds(parts + 1, 0);
   {
     std::vector<double> cost(n_units);
-    for (size_t i = 0; i < n_cfg; ++i) {
+    for (size_t i = 0; i < nk; ++i) {
       const dsi::MultiCfg &d = dc[i];
       const int npos = d.n_tokens - 1;
       double open = 1.0, calls = 0.0;
@@ -2014,15 +2047,15 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     }
   }
   DevBuf b_cfg, b_prefix, b_acc, b_dsi, b_set;
-  const size_t acc_bytes = n_cfg * dsi::MF * sizeof(unsigned long long);
-  MULTI_TRY(b_cfg.alloc(n_cfg * sizeof(dsi::MultiCfg), stream));
-  MULTI_TRY(b_prefix.alloc((n_cfg + 1) * sizeof(uint64_t), stream));
+  const size_t acc_bytes = nk * dsi::MF * sizeof(unsigned long long);
+  MULTI_TRY(b_cfg.alloc(nk * sizeof(dsi::MultiCfg), stream));
+  MULTI_TRY(b_prefix.alloc((nk + 1) * sizeof(uint64_t), stream));
   MULTI_TRY(b_acc.alloc(acc_bytes, stream));
   if (trial_dsi) MULTI_TRY(b_dsi.alloc(rec * sizeof(int32_t), stream));
   if (trial_settled) MULTI_TRY(b_set.alloc(rec * 8 * sizeof(int32_t), stream));
   tr.mark("alloc");
-  MULTI_TRY(cudaMemcpyAsync(b_cfg.p, dc.data(), n_cfg * sizeof(dsi::MultiCfg), cudaMemcpyHostToDevice, stream));
-  MULTI_TRY(cudaMemcpyAsync(b_prefix.p, prefix.data(), (n_cfg + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+  MULTI_TRY(cudaMemcpyAsync(b_cfg.p, dc.data(), nk * sizeof(dsi::MultiCfg), cudaMemcpyHostToDevice, stream));
+  MULTI_TRY(cudaMemcpyAsync(b_prefix.p, prefix.data(), (nk + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
                             stream));
   MULTI_TRY(cudaMemsetAsync(b_acc.p, 0, acc_bytes, stream));
   tr.mark("h2d");
@@ -2030,7 +2063,7 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   dsi::MultiParams p{};
   p.cfg = (const dsi::MultiCfg *)b_cfg.p;
   p.tile_prefix = (const uint64_t *)b_prefix.p;
-  p.n_cfg = (uint32_t)n_cfg;
+  p.n_cfg = (uint32_t)nk;
   p.tile_trials = tile;
   p.unit_begin = 0;
   p.acc = (unsigned long long *)b_acc.p;
@@ -2076,13 +2109,13 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     ncclComm_t comm = nullptr;
     ncclResult_t r = api.CommInitRank(&comm, opt->world, uid, opt->rank);
     if (r == ncclSuccess)
-      r = api.AllReduce(b_acc.p, b_acc.p, n_cfg * dsi::MF, ncclUint64, ncclSum, comm, stream);
+      r = api.AllReduce(b_acc.p, b_acc.p, nk * dsi::MF, ncclUint64, ncclSum, comm, stream);
     if (r == ncclSuccess && cudaStreamSynchronize(stream) != cudaSuccess) r = ncclUnhandledCudaError;
     if (comm) api.CommDestroy(comm);
     if (r != ncclSuccess) return fail(nullptr, DSI_E_COMM, std::string("multi-drafter all-reduce: ") +
                                                            api.GetErrorString(r));
   }
-  std::vector<unsigned long long> acc(n_cfg * dsi::MF);
+  std::vector<unsigned long long> acc(nk * dsi::MF);
   MULTI_TRY(cudaMemcpyAsync(acc.data(), b_acc.p, acc_bytes, cudaMemcpyDeviceToHost, stream));
   if (trial_dsi) MULTI_TRY(cudaMemcpyAsync(trial_dsi, b_dsi.p, rec * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
   if (trial_settled)
@@ -2094,12 +2127,12 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
 #undef MULTI_TRY
 
   // every trial simulated exactly once, then the FP64 derivations of the exact sums
-  for (size_t i = 0; i < n_cfg; ++i)
-    if (acc[i * dsi::MF + dsi::MF_TRIALS] != cfg[i].n_trials)
+  for (size_t i = 0; i < nk; ++i)
+    if (acc[i * dsi::MF + dsi::MF_TRIALS] != dc[i].n_trials)
       return fail(nullptr, DSI_E_DEVICE, "trial count mismatch after the kernel");
   const double tick = opt->tick;
   for (size_t i = 0; i < n_cfg; ++i) {
-    const unsigned long long *a = &acc[i * dsi::MF];
+    const unsigned long long *a = &acc[(size_t)rep_of[i] * dsi::MF];
     dsi_multi_result &r = out[i];
     std::memset(&r, 0, sizeof r);
     const uint64_t T = cfg[i].n_trials;
@@ -2117,11 +2150,21 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     }
     r.sum_settled[m - 1] = (int64_t)T * (cfg[i].n_tokens - 1) - by_drafters;
     const double Td = (double)T;
+    if (means) {
+      // L = t_m (1 + S_m) + sum_{j<m} t_j S_j per trial, summed with this config's latencies;
+      // L <= N t_m on every trial (t_j <= t_m), so the Thm 1 counter is exactly 0
+      const dsi::MultiCfg &d = orig[i];
+      __int128 sum = (__int128)d.t_t * ((__int128)T + r.sum_settled[m - 1]);
+      for (int j = 0; j < m - 1; ++j) sum += (__int128)d.t_d[j] * r.sum_settled[j];
+      r.sum_dsi_ticks = (int64_t)sum;
+      r.sumsq_dsi_ticks = 0;
+      r.n_dsi_gt_nonsi = 0;
+    }
     r.mean_nonsi = (double)r.nonsi_ticks * tick;
     r.mean_dsi = ((double)r.sum_dsi_ticks / Td) * tick;
     const unsigned __int128 num = (unsigned __int128)T * r.sumsq_dsi_ticks -
                                   (unsigned __int128)(uint64_t)r.sum_dsi_ticks * (uint64_t)r.sum_dsi_ticks;
-    r.std_dsi = std::sqrt((double)num) / Td * tick;
+    r.std_dsi = means ? std::nan("") : std::sqrt((double)num) / Td * tick;
   }
   tr.mark("finalize");
   return DSI_OK;

@@ -184,3 +184,29 @@ def test_partition_and_one_rank_nccl_bit_identical(kw):
         got, _, _ = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED, **kw)
     for f in ("trials", "sum_dsi_ticks", "sumsq_dsi_ticks", "sum_settled", "n_dsi_gt_nonsi", "mean_dsi", "std_dsi"):
         assert np.array_equal(got[f], ref[f]), f
+
+
+@pytest.mark.parametrize("name", ["heatmap", "fuzz"])
+def test_means_only_shares_passes_across_latencies(name):
+    """DSI_F_MEANS_ONLY: configs differing only in latencies share one kernel pass (j* depends on
+    the indicators alone); sums, settled counts and means equal the default run bit for bit."""
+    if name == "heatmap":
+        cfgs, tick = W.multi_heatmap(trials=3000)
+    else:
+        base, tick = W.multi_fuzz(12, seed=21, n_max=80, trials=900)
+        rows = []
+        for b in base:  # each fuzz config again with every latency scaled: same indicator groups
+            rows.append(b)
+            c = b.copy()
+            nd = int(c["n_drafters"])
+            c["t_target"] = 2 * c["t_target"]
+            c["t_drafter"][:nd] = c["t_drafter"][:nd] + 1
+            rows.append(c)
+        cfgs = np.array(rows, dtype=base.dtype)
+    want, _, _ = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED)
+    got, _, _ = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED, flags=D.DSI_F_MEANS_ONLY)
+    for f in ("trials", "nonsi_ticks", "sum_dsi_ticks", "sum_settled", "n_dsi_gt_nonsi", "mean_dsi", "mean_nonsi"):
+        assert np.array_equal(got[f], want[f]), f
+    assert (got["sumsq_dsi_ticks"] == 0).all() and np.isnan(got["std_dsi"]).all()
+    with pytest.raises(D.DsiError):
+        D.dsi_multi_simulate(cfgs[:2], tick=tick, seed=SEED, flags=D.DSI_F_MEANS_ONLY, per_trial=True)
