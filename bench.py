@@ -527,9 +527,21 @@ def ours(args):
                    ("sum_si_ticks", "sum_dsi_ticks", "sum_segments", "sum_si_iters", "trials",
                     "mean_si", "mean_dsi"))
         heat_means_s, cells_means = heatmap_grid_times(simm, flush, args.steps)
+        h2d_m, d2h_m = simm.io_bytes()
+        barrier()
+        e2e_m = []
+        for _ in range(args.steps):  # update (validate + H2D) + run + reduce, host wall clock
+            t0 = time.perf_counter()
+            simm.update(cfgs)
+            simm.run()
+            simm.reduce(resm)
+            e2e_m.append(time.perf_counter() - t0)
+        e2e_m_total = max_over_ranks(sum(e2e_m))
         means = {"value": tt * args.steps / (m_total / 1000.0), "unit": UNIT,
                  "ms_per_step": m_total / args.steps, "kernel_ms": max_over_ranks(statistics.mean(m_kern)),
                  "launches_per_step": simm.launches(), "sums_and_means_identical_to_value_run": bool(same),
+                 "e2e": {"value": tt * args.steps / e2e_m_total, "unit": UNIT,
+                         "h2d_bytes_per_step": int(h2d_m), "d2h_bytes_per_step": int(d2h_m)},
                  "note": "DSI_F_MEANS_ONLY: one pass per indicator group builds the segment-length "
                          "histogram H[g]; each config's sums = sum_g H[g] x segment cost (linearity over "
                          "segments), identical integers to the value run; no second moments or per-trial "
