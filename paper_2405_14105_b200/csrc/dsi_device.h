@@ -173,6 +173,7 @@ struct SegParams {
   uint64_t unit_begin;          // pass 1: first unit of this launch
   uint64_t cfg_begin, cfg_end;  // pass 2: configs evaluated by this launch
   unsigned long long *hist;     // sum over groups of (N + 1) bins; bin 0 = trials
+  unsigned long long *pre;      // prefix sums of hist (same offsets), for the bucketed evaluation
   unsigned long long *acc;      // n_cfg * NF
   int32_t max_n;
   Keys keys;
@@ -180,6 +181,7 @@ struct SegParams {
 size_t seg_hist_smem(int max_n);
 int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream);
 int launch_seg_eval(const SegParams &p, void *stream);
+int launch_seg_prefix(const SegParams &p, void *stream);
 
 // ---- multi-drafter DSI (dsi_multi.cu)
 struct alignas(16) MultiCfg {  // 112 bytes

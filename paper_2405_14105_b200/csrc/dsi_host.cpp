@@ -1228,7 +1228,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       e = cudaMalloc(&d.d_seg_groups, h->seg_groups.size() * sizeof(dsi::SegGroup));
       if (e == cudaSuccess) e = cudaMalloc(&d.d_seg_prefix, h->seg_prefix.size() * sizeof(uint64_t));
       if (e == cudaSuccess) e = cudaMalloc(&d.d_cfg_group, n_cfg * sizeof(uint32_t));
-      if (e == cudaSuccess) e = cudaMalloc(&d.d_hist, h->hist_len * sizeof(unsigned long long));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_hist, 2 * h->hist_len * sizeof(unsigned long long));
     }
     if (e == cudaSuccess && shared) {
       e = cudaMalloc(&d.d_perm, n_cfg * sizeof(uint32_t));
@@ -1395,6 +1395,7 @@ static dsi::SegParams seg_params(dsi_sim *h, DeviceState &d, const dsi::Keys &ke
   q.n_groups = (uint32_t)h->seg_groups.size();
   q.tile_trials = h->tile_trials;
   q.hist = d.d_hist;
+  q.pre = d.d_hist + h->hist_len;
   q.acc = d.d_acc;
   q.max_n = h->max_n;
   q.keys = keys;
@@ -1528,6 +1529,11 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     for (auto &d : h->dev) {
       CUDA_TRY(h, cudaSetDevice(d.ordinal));
       dsi::SegParams q = seg_params(h, d, dsi::Keys{});
+      {
+        const int e = dsi::launch_seg_prefix(q, d.stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "segment prefix launch");
+        h->launches += 1;
+      }
       for (const auto &cr : d.cfg_ranges) {
         q.cfg_begin = cr.first;
         q.cfg_end = cr.second;

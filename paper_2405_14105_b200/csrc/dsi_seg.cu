@@ -127,6 +127,28 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
   }
 }
 
+// P[g] = H[1] + ... + H[g] (P[0] = 0) per group, for the bucketed evaluation below.
+__global__ void dsi_seg_prefix_kernel(const SegParams P) {
+  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gi >= P.n_groups) return;
+  const SegGroup G = P.groups[gi];
+  const unsigned long long *H = P.hist + G.hist_off;
+  unsigned long long *pre = P.pre + G.hist_off;
+  unsigned long long run = 0;
+  pre[0] = 0;
+  for (int g = 1; g <= G.n_tokens; ++g) {
+    run += H[g];
+    pre[g] = run;
+  }
+}
+
+// S(b) of the closed form (FIFO start of thread b), as seg_extra computes it.
+__device__ __forceinline__ uint32_t seg_S(uint32_t b, const SegCtx &s) {
+  const uint32_t qq = magic_div(b, s.m_sp_lo, s.m_sp_hi);
+  const int rr = (int)b - (int)qq * s.sp_eff;
+  return (uint32_t)max((int)b * s.kd, rr * s.kd + (int)qq * s.t_t);
+}
+
 __global__ void __launch_bounds__(128) dsi_seg_eval_kernel(const SegParams P) {
   const uint64_t c = P.cfg_begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= P.cfg_end) return;
@@ -137,6 +159,22 @@ __global__ void __launch_bounds__(128) dsi_seg_eval_kernel(const SegParams P) {
   const bool fresh = (cfg.flags & CFG_FRESH) != 0;
   const int N = cfg.n_tokens;
   unsigned long long sm = 0, si = 0, sd = 0;
+  const int k = cfg.k_eff;
+  if (k >= 2 && !fresh) {
+    // bucketed: ceil(g/(k+1)) and ceil((g-1)/k) are constant on runs of g, so each run costs one
+    // difference of the prefix sums P (O(N/k) per config instead of O(N))
+    const unsigned long long *pre = P.pre + G.hist_off;
+    sm = pre[N];
+    for (int lo = 0, M = 1; lo < N; lo += k + 1, ++M) {  // g in (lo, lo + k + 1]: M iterations
+      const int hi = min(lo + k + 1, N);
+      si += (unsigned long long)M * (pre[hi] - pre[lo]);
+    }
+    sd = (unsigned long long)(uint32_t)cfg.t_t * sm;  // every segment pays t_t; g >= 2 adds S(b)
+    for (int b = 1, lo = 2; lo <= N; ++b, lo += k) {     // g in [(b-1)k + 2, bk + 1]: thread b
+      const int hi = min(lo + k - 1, N);
+      sd += (unsigned long long)seg_S((uint32_t)b, s) * (pre[hi] - pre[lo - 1]);
+    }
+  } else
   for (int g = 1; g <= N; ++g) {
     const unsigned long long h = __ldg(H + g);
     if (!h) continue;
@@ -186,6 +224,11 @@ int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream) {
     done += n;
   }
   return 0;
+}
+
+int launch_seg_prefix(const SegParams &p, void *stream) {
+  dsi_seg_prefix_kernel<<<(p.n_groups + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
+  return (int)cudaGetLastError();
 }
 
 int launch_seg_eval(const SegParams &p, void *stream) {
