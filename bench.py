@@ -401,9 +401,12 @@ def ours(args):
 
     base_kw = dict(tick=tick, seed=W.SEED, device=local, rank=rank, world=world)
     kw = dict(base_kw, nccl_id=fresh_nccl_id())
+    # one process per GPU: the results are gathered on rank 0 (DSI_F_REDUCE_TO_ROOT), so the
+    # other ranks do not each copy back and finalize all n_cfg results on the shared host cores
+    root = D.DSI_F_REDUCE_TO_ROOT if world > 1 else 0
 
     t_create = time.perf_counter()
-    sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING, **kw)
+    sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING | root, **kw)
     create_s = time.perf_counter() - t_create
     stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local))
     # result buffers allocated (and their pages touched) once, outside the timed region
@@ -450,7 +453,8 @@ def ours(args):
     # because it changes what a simulated trial-token costs.  Its sums must be bit-identical.
     crn = None
     if not args.no_shared_streams:
-        simc = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_SHARED_STREAMS, nccl_id=fresh_nccl_id(), **base_kw)
+        simc = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_SHARED_STREAMS | root, nccl_id=fresh_nccl_id(),
+                           **base_kw)
         streamc = torch.cuda.ExternalStream(simc.stream(), device=torch.device("cuda", local))
         for _ in range(args.warmup):
             simc.run()
@@ -501,7 +505,8 @@ def ours(args):
     heat_means_s = None
     if not args.no_means:
         resm = np.zeros(cfgs.size, D.RESULT_DTYPE)
-        simm = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_MEANS_ONLY, nccl_id=fresh_nccl_id(), **base_kw)
+        simm = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_MEANS_ONLY | root, nccl_id=fresh_nccl_id(),
+                           **base_kw)
         streamm = torch.cuda.ExternalStream(simm.stream(), device=torch.device("cuda", local))
         for _ in range(args.warmup):
             simm.run()

@@ -96,6 +96,11 @@ typedef enum {
                                  PER_TRIAL, HIST, PATTERN, SHARED_STREAMS or TTFT;
                                  dsi_sim_update keeps (stream_id, a, N, n_trials) per config.    */
 
+#define DSI_F_REDUCE_TO_ROOT 0x100u /* multi-process: dsi_sim_reduce returns the results on rank 0
+                                 only; the other ranks contribute to the all-reduce and return
+                                 without the device-to-host copy and FP64 finalize (out may be
+                                 NULL there).  Without it every rank gets every result.       */
+
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {
   double t_target;    /* target forward latency (t_2, "Target Latency"), user units > 0   */

@@ -1025,7 +1025,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
   const uint32_t known = DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_STRICT_EQ1 | DSI_F_TIMING |
-                         DSI_F_SHARED_STREAMS | DSI_F_FRESH_VERIFIER | DSI_F_MEANS_ONLY;
+                         DSI_F_SHARED_STREAMS | DSI_F_FRESH_VERIFIER | DSI_F_MEANS_ONLY |
+                         DSI_F_REDUCE_TO_ROOT;
   if (opt->flags & ~known) return fail(nullptr, DSI_E_RANGE, "unknown flag");
   if (opt->n_devices < 1 || opt->n_devices > 8) return fail(nullptr, DSI_E_RANGE, "n_devices must be 1..8");
   if (opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world)
@@ -1552,8 +1553,9 @@ dsi_status dsi_sim_run(dsi_sim *h) {
 dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   if (!h) return DSI_E_NULL;
   Trace tr("dsi_sim_reduce");
-  if (!out) return fail(h, DSI_E_NULL, "out is NULL");
   h->err.clear();
+  const bool root_only = (h->opt.flags & DSI_F_REDUCE_TO_ROOT) && h->opt.rank != 0;
+  if (!out && !root_only) return fail(h, DSI_E_NULL, "out is NULL");
   const size_t n_cfg = h->n_cfg;
   if (n != n_cfg) return fail(h, DSI_E_RANGE, "n must equal n_cfg");
   if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_reduce before dsi_sim_run");
@@ -1562,6 +1564,14 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   dsi_status st = sum_across(h, hist);
   if (st != DSI_OK) return st;
   tr.mark("allreduce-enqueue");
+  if (root_only) {  // DSI_F_REDUCE_TO_ROOT: this rank contributed its sums; rank 0 checks and finalizes
+    for (auto &d : h->dev) {
+      CUDA_TRY(h, cudaSetDevice(d.ordinal));
+      CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+    }
+    h->reduced = true;
+    return DSI_OK;
+  }
   // every device now holds the global sums (or there is one device): read device 0.
   // The partition check (every trial simulated exactly once) runs on the device before the
   // copies; the moments come back in chunks so the host finalizes chunk i while chunk i+1

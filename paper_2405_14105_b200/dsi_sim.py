@@ -24,6 +24,7 @@ DSI_F_PER_TRIAL, DSI_F_HIST, DSI_F_PATTERN, DSI_F_STRICT_EQ1, DSI_F_TIMING = 0x1
 DSI_F_SHARED_STREAMS = 0x20
 DSI_F_FRESH_VERIFIER = 0x40
 DSI_F_MEANS_ONLY = 0x80
+DSI_F_REDUCE_TO_ROOT = 0x100
 
 # Structured dtypes with the exact C layouts (numpy arrays are passed by pointer).
 CONFIG_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_rate", "<f8"),

@@ -645,3 +645,14 @@ def test_max_trials_every_trial_counted_once():
     assert int(r2["sum_si_ticks"]) == acc * 160 + (T - acc) * 320
     assert int(r2["trials"]) == T
     sim.close()
+
+
+def test_reduce_to_root_flag_on_rank_zero():
+    """DSI_F_REDUCE_TO_ROOT: rank 0 (here the only rank, through a one-rank NCCL communicator)
+    gets exactly the results of the default reduce."""
+    cfgs, tick = W.fuzz(40, seed=8, trials=500)
+    _, want = run_sim(cfgs, tick, flags=0)
+    sim, got = run_sim(cfgs, tick, flags=D.DSI_F_REDUCE_TO_ROOT, nccl_id=D.dsi_nccl_unique_id())
+    for f in want.dtype.names:
+        assert np.array_equal(got[f], want[f]) or np.allclose(got[f], want[f], equal_nan=True), f
+    sim.close()
