@@ -92,9 +92,11 @@ typedef enum {
                                  ceil(g/(k+1)), sum m = sum_g H[g] -- the same integers as the
                                  default mode, so sums, means and dsi_sim_heatmap are
                                  bit-identical.  Second moments and per-trial counters are not
-                                 produced: sumsq_* = 0, std_* = NaN, n_dsi_gt_* = -1.  Not with
-                                 PER_TRIAL, HIST, PATTERN, SHARED_STREAMS or TTFT;
-                                 dsi_sim_update keeps (stream_id, a, N, n_trials) per config.    */
+                                 produced: sumsq_* = 0, std_* = NaN, n_dsi_gt_* = -1.  TTFT
+                                 configs add sum_g H1[g] D1(g), H1 the first-segment lengths.
+                                 Not with PER_TRIAL, HIST, PATTERN or SHARED_STREAMS;
+                                 dsi_sim_update keeps (stream_id, a, N, n_trials) and which
+                                 configs use TTFT.                                              */
 
 #define DSI_F_REDUCE_TO_ROOT 0x100u /* multi-process: dsi_sim_reduce returns the results on rank 0
                                  only; the other ranks contribute to the all-reduce and return

@@ -174,6 +174,8 @@ struct SegParams {
   uint64_t cfg_begin, cfg_end;  // pass 2: configs evaluated by this launch
   unsigned long long *hist;     // sum over groups of (N + 1) bins; bin 0 = trials
   unsigned long long *pre;      // prefix sums of hist (same offsets), for the bucketed evaluation
+  unsigned long long *hist1;    // TTFT: first-segment lengths per group (same offsets; or NULL)
+  const uint32_t *ttft_cfgs;    // TTFT: sorted indices of the TTFT configs of this launch
   unsigned long long *acc;      // n_cfg * NF
   int32_t max_n;
   Keys keys;
@@ -182,6 +184,8 @@ size_t seg_hist_smem(int max_n);
 int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream);
 int launch_seg_eval(const SegParams &p, void *stream);
 int launch_seg_prefix(const SegParams &p, void *stream);
+// TTFT correction of the configs ttft_cfgs[begin, end): F_DSI += sum_g H1[g] D1(g)
+int launch_seg_ttft(const SegParams &p, uint64_t begin, uint64_t end, void *stream);
 
 // ---- multi-drafter DSI (dsi_multi.cu)
 struct alignas(16) MultiCfg {  // 112 bytes

@@ -159,7 +159,8 @@ struct DeviceState {
   dsi::SegGroup *d_seg_groups = nullptr;  // means-only mode: groups, unit prefix, config -> group,
   uint64_t *d_seg_prefix = nullptr;       //   segment-length histograms (bin 0 = trials)
   uint32_t *d_cfg_group = nullptr;
-  unsigned long long *d_hist = nullptr;
+  unsigned long long *d_hist = nullptr;   // H | prefix of H | (TTFT) H1, hist_len each
+  uint32_t *d_ttft_cfgs = nullptr;
   std::vector<std::pair<uint64_t, uint64_t>> cfg_ranges;  // means-only: configs evaluated here
 };
 
@@ -184,6 +185,7 @@ struct dsi_sim {
   std::vector<uint64_t> seg_prefix;       // groups + 1 histogram units
   std::vector<uint32_t> cfg_group;
   uint64_t hist_len = 0;
+  std::vector<uint32_t> ttft_cfgs;        // means-only + TTFT: configs with a first-segment correction
   bool use_nccl = false;                  // per-config moments summed with ncclAllReduce
   std::vector<uint32_t> perm;
   std::vector<dsi::CrnGroup> groups;
@@ -570,6 +572,7 @@ void free_device(DeviceState &d) {
   cudaFree(d.d_seg_prefix);
   cudaFree(d.d_cfg_group);
   cudaFree(d.d_hist);
+  cudaFree(d.d_ttft_cfgs);
   if (d.ev0) cudaEventDestroy(d.ev0);
   if (d.ev1) cudaEventDestroy(d.ev1);
   if (d.own_stream && d.stream) cudaStreamDestroy(d.stream);
@@ -602,6 +605,9 @@ dsi_status upload(dsi_sim *h, bool plan = true) {
                                   cudaMemcpyHostToDevice, d.stream));
       CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg_group, h->cfg_group.data(), h->cfg_group.size() * sizeof(uint32_t),
                                   cudaMemcpyHostToDevice, d.stream));
+      if (!h->ttft_cfgs.empty())
+        CUDA_TRY(h, cudaMemcpyAsync(d.d_ttft_cfgs, h->ttft_cfgs.data(), h->ttft_cfgs.size() * sizeof(uint32_t),
+                                    cudaMemcpyHostToDevice, d.stream));
       CUDA_TRY(h, cudaStreamSynchronize(d.stream));
     }
     if (h->shared && plan) {  // the shared-stream plan (unchanged by an update that keeps its keys)
@@ -664,6 +670,9 @@ dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_uni
     i = j;
   }
   h->hist_len = off;
+  h->ttft_cfgs.clear();
+  for (size_t i = 0; i < n; ++i)
+    if (h->ticks[i].t_t1 != h->ticks[i].t_t || h->ticks[i].t_d1 != h->ticks[i].t_d) h->ttft_cfgs.push_back((uint32_t)i);
   // tiles: multiples of 128 trials, enough units to fill the devices
   uint64_t r = trials / (128ull * std::max<uint64_t>(1, target_units));
   r = std::min<uint64_t>(128, std::max<uint64_t>(1, r));
@@ -1102,8 +1111,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   // ---- work units: (config, tile of tile_trials trials), or shared-stream (group, config slice)
   std::vector<double> crn_cost;
   if (means_only) {
-    if (h->any_ttft || h->max_n > kMeansMaxN) {
-      h->err = "DSI_F_MEANS_ONLY: no TTFT configs";
+    if (h->max_n > kMeansMaxN) {
+      h->err = "DSI_F_MEANS_ONLY: N too large";
       return abort_create(DSI_E_RANGE);
     }
     s = plan_means(h, crn_cost, 148ull * 16 * (uint64_t)total_devices);
@@ -1229,7 +1238,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       e = cudaMalloc(&d.d_seg_groups, h->seg_groups.size() * sizeof(dsi::SegGroup));
       if (e == cudaSuccess) e = cudaMalloc(&d.d_seg_prefix, h->seg_prefix.size() * sizeof(uint64_t));
       if (e == cudaSuccess) e = cudaMalloc(&d.d_cfg_group, n_cfg * sizeof(uint32_t));
-      if (e == cudaSuccess) e = cudaMalloc(&d.d_hist, 2 * h->hist_len * sizeof(unsigned long long));
+      if (e == cudaSuccess) e = cudaMalloc(&d.d_hist, 3 * h->hist_len * sizeof(unsigned long long));
+      if (e == cudaSuccess && !h->ttft_cfgs.empty())
+        e = cudaMalloc(&d.d_ttft_cfgs, h->ttft_cfgs.size() * sizeof(uint32_t));
     }
     if (e == cudaSuccess && shared) {
       e = cudaMalloc(&d.d_perm, n_cfg * sizeof(uint32_t));
@@ -1308,10 +1319,11 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   if (s == DSI_OK) s = derive_limits(h, h->ticks_next);  // the new configs may need a larger launch shape
   if (s != DSI_OK) return s;                              // derive_limits only commits on success
   if (h->means_only) {  // the histogram groups are fixed at create: their keys must not change
-    bool same = !h->any_ttft && h->max_n <= kMeansMaxN;
+    bool same = h->max_n <= kMeansMaxN;
     for (size_t i = 0; same && i < n_cfg; ++i) {
       const CfgTicks &a = h->ticks[i], &b = h->ticks_next[i];
-      same = a.stream_id == b.stream_id && a.thr == b.thr && a.n == b.n && a.trials == b.trials;
+      const bool ta = a.t_t1 != a.t_t || a.t_d1 != a.t_d, tb = b.t_t1 != b.t_t || b.t_d1 != b.t_d;
+      same = a.stream_id == b.stream_id && a.thr == b.thr && a.n == b.n && a.trials == b.trials && ta == tb;
     }
     if (!same) {
       h->max_n = old_n;
@@ -1319,7 +1331,8 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
       h->any_ttft = old_ttft;
       h->any_fresh = old_fresh;
       return fail(h, DSI_E_RANGE,
-                  "DSI_F_MEANS_ONLY: (stream_id, accept_rate, N, n_trials) changed or TTFT; create a new handle");
+                  "DSI_F_MEANS_ONLY: (stream_id, accept_rate, N, n_trials) or the TTFT configs changed; "
+                  "create a new handle");
     }
   }
   const bool replan = h->shared && !same_plan_keys(h->ticks, h->ticks_next);
@@ -1397,6 +1410,8 @@ static dsi::SegParams seg_params(dsi_sim *h, DeviceState &d, const dsi::Keys &ke
   q.tile_trials = h->tile_trials;
   q.hist = d.d_hist;
   q.pre = d.d_hist + h->hist_len;
+  q.hist1 = h->ttft_cfgs.empty() ? nullptr : d.d_hist + 2 * h->hist_len;
+  q.ttft_cfgs = d.d_ttft_cfgs;
   q.acc = d.d_acc;
   q.max_n = h->max_n;
   q.keys = keys;
@@ -1444,6 +1459,9 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     if (d.ev0) CUDA_TRY(h, cudaEventRecord(d.ev0, d.stream));
     if (h->means_only) {  // pass 1 here; the histogram all-reduce and pass 2 after the loop
       CUDA_TRY(h, cudaMemsetAsync(d.d_hist, 0, h->hist_len * sizeof(unsigned long long), d.stream));
+      if (!h->ttft_cfgs.empty())
+        CUDA_TRY(h, cudaMemsetAsync(d.d_hist + 2 * h->hist_len, 0, h->hist_len * sizeof(unsigned long long),
+                                    d.stream));
       dsi::SegParams q = seg_params(h, d, p.keys);
       for (const auto &rg : d.ranges) {
         if (rg.second <= rg.first) continue;
@@ -1521,6 +1539,9 @@ dsi_status dsi_sim_run(dsi_sim *h) {
         if (r != ncclSuccess) break;
         cudaSetDevice(d.ordinal);
         r = api.AllReduce(d.d_hist, d.d_hist, h->hist_len, ncclUint64, ncclSum, d.comm, d.stream);
+        if (r == ncclSuccess && !h->ttft_cfgs.empty())
+          r = api.AllReduce(d.d_hist + 2 * h->hist_len, d.d_hist + 2 * h->hist_len, h->hist_len, ncclUint64,
+                            ncclSum, d.comm, d.stream);
       }
       const ncclResult_t r2 = api.GroupEnd();
       if (r != ncclSuccess || r2 != ncclSuccess)
@@ -1541,6 +1562,14 @@ dsi_status dsi_sim_run(dsi_sim *h) {
         const int e = dsi::launch_seg_eval(q, d.stream);
         if (e) return cuda_fail(h, (cudaError_t)e, "segment evaluation launch");
         h->launches += cr.second > cr.first;
+        if (!h->ttft_cfgs.empty()) {  // first-segment corrections of this range's TTFT configs
+          const auto &L = h->ttft_cfgs;
+          const uint64_t b = std::lower_bound(L.begin(), L.end(), (uint32_t)cr.first) - L.begin();
+          const uint64_t en = std::lower_bound(L.begin(), L.end(), (uint32_t)cr.second) - L.begin();
+          const int e2 = dsi::launch_seg_ttft(q, b, en, d.stream);
+          if (e2) return cuda_fail(h, (cudaError_t)e2, "TTFT correction launch");
+          h->launches += en > b;
+        }
       }
       if (d.ev1) CUDA_TRY(h, cudaEventRecord(d.ev1, d.stream));
     }

@@ -24,7 +24,7 @@
 namespace dsi {
 namespace {
 
-constexpr int SEG_SMEM_MAX_N = 8192;  // 4(N+1) + 16 N/4 bytes = 64 KB of shared memory
+constexpr int SEG_SMEM_MAX_N = 8192;  // 8(N+1) + 16 N/4 bytes = 96 KB of shared memory
 
 // SMEM: the block's histogram and q halves in shared memory (N <= 8192); else segments go to
 // the group's histogram in global memory with 64-bit atomics and the q halves are per call.
@@ -54,13 +54,22 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
 
   uint32_t *H = reinterpret_cast<uint32_t *>(smem);           // N + 1 bins
   uint4 *U = reinterpret_cast<uint4 *>(smem + (((size_t)(N + 1) * 4 + 15) & ~(size_t)15));
+  uint32_t *H1 = reinterpret_cast<uint32_t *>(U + nq + 1);     // TTFT: first-segment lengths
   unsigned long long *out = P.hist + G.hist_off;
+  unsigned long long *out1 = P.hist1 ? P.hist1 + G.hist_off : nullptr;
+  auto add1 = [&](int g) {  // the trial's first segment has length g
+    if (!out1) return;
+    if (SMEM) atomicAdd(&H1[g], 1u);
+    else atomicAdd(out1 + g, 1ull);
+  };
   auto add = [&](int g) {
     if (SMEM) atomicAdd(&H[g], 1u);
     else atomicAdd(out + g, 1ull);
   };
   if (SMEM) {
     for (int g = threadIdx.x; g <= N; g += blockDim.x) H[g] = 0u;
+    if (out1)
+      for (int g = threadIdx.x; g <= N; g += blockDim.x) H1[g] = 0u;
     if (G.mode == MODE_STREAM)
       for (int q = threadIdx.x; q < nq; q += blockDim.x) U[q] = philox_q_half((uint32_t)q, G.stream_id, P.keys);
     __syncthreads();
@@ -72,10 +81,12 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
       if (G.mode == MODE_ALL_REJECT) ones += (uint32_t)N;
       else if (N == 1) ones += 1u;
       else add(N);
+      add1(G.mode == MODE_ALL_REJECT ? 1 : N);
       continue;
     }
     const TrialHalf th = philox_trial_half((uint32_t)t, P.keys);
     int lastz = 0;     // position of the last zero (0: the sentinel before position 1)
+    int g1 = 0;        // TTFT: the first zero's position = the first segment's length
     uint32_t cin = 1;  // position 32w is a zero (the sentinel for w = 0)
     for (int w = 0; w < nwords; ++w) {
       uint32_t R = 0u;
@@ -105,9 +116,11 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
         const int prev = below ? 32 * w + 32 - __clz(below) : lastz;  // the previous zero
         add(32 * w + b + 1 - prev);
       }
+      if (g1 == 0 && R) g1 = 32 * w + __ffs(R);
       if (R) lastz = 32 * w + 32 - __clz(R);
       cin = R >> 31;
     }
+    add1(g1 ? g1 : N);
     const int gl = N - lastz;  // the final segment ends at N
     if (gl == 1) ones += 1u;
     else add(gl);
@@ -124,6 +137,61 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
   for (int g = threadIdx.x; g <= N; g += blockDim.x) {
     const uint32_t v = g == 0 ? (uint32_t)(t1 - t0) : H[g];
     if (v) atomicAdd(out + g, (unsigned long long)v);
+    if (out1 && g > 0 && H1[g]) atomicAdd(out1 + g, (unsigned long long)H1[g]);
+  }
+}
+
+// TTFT variant (R23, 6.4): L_DSI gains D1(g1) = C1(g1) - C(g1) where g1 is the trial's
+// first segment, so a config's sum gains sum_g H1[g] D1(g).  One block per TTFT config: thread 0
+// runs the first segment's FIFO schedule exactly as dsi_kernel.cu (F[b]: completion of thread b
+// with the target's first forward t_t1 and drafts late by t_d1 - t_d), then the block sums.
+__global__ void __launch_bounds__(128) dsi_seg_ttft_kernel(const SegParams P, uint64_t begin) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t c = P.ttft_cfgs[begin + blockIdx.x];
+  const DevCfg cfg = P.cfg[c];
+  const SegGroup G = P.groups[P.cfg_group[c]];
+  const unsigned long long *H1 = P.hist1 + G.hist_off;
+  const SegCtx s = make_segctx(cfg);
+  const int N = cfg.n_tokens;
+  int *F = reinterpret_cast<int *>(smem);
+  if (threadIdx.x == 0) {
+    const int B = N > 1 ? (N - 2) / cfg.k_eff + 1 : 0;  // ceil((N-1)/k)
+    int zero_servers = cfg.sp_eff - 1, h = 1;
+    bool first_unused = true;
+    F[0] = cfg.t_t1;
+    for (int b = 1; b <= B; ++b) {
+      const int r = cfg.ttft_shift + b * cfg.kd;  // t_d1 + (b k - 1) t_d
+      int free_at;
+      if (zero_servers > 0) {
+        free_at = 0;
+        --zero_servers;
+      } else if (first_unused && (h >= b || cfg.t_t1 <= F[h])) {
+        free_at = cfg.t_t1;
+        first_unused = false;
+      } else {
+        free_at = F[h++];
+      }
+      F[b] = max(r, free_at) + cfg.t_t;
+    }
+    for (int b = 1; b <= B; ++b) F[b] = max(F[b], F[b - 1]);  // positions settle in order
+  }
+  __syncthreads();
+  long long part = 0;
+  for (int g = 1 + threadIdx.x; g <= N; g += blockDim.x) {
+    const unsigned long long h1 = H1[g];
+    if (!h1) continue;
+    const uint32_t b = magic_div((uint32_t)g + s.k_eff - 2u, s.m_k_lo, s.m_k_hi);  // ceil((g-1)/k)
+    const int S = g >= 2 ? (int)seg_extra(g, s).y : 0;
+    part += (long long)h1 * (long long)(F[b] - (cfg.t_t + S));
+  }
+  __shared__ long long red[4];
+  part = (long long)warp_sum((unsigned long long)part);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    P.acc[(size_t)c * NF + F_DSI] += (unsigned long long)t;  // one block per config: no race
   }
 }
 
@@ -198,8 +266,21 @@ __global__ void __launch_bounds__(128) dsi_seg_eval_kernel(const SegParams P) {
 
 }  // namespace
 
-size_t seg_hist_smem(int max_n) {
-  return (((size_t)(max_n + 1) * 4 + 15) & ~(size_t)15) + (size_t)((max_n - 1 + 3) / 4 + 1) * sizeof(uint4);
+size_t seg_hist_smem(int max_n) {  // H, U and (TTFT) H1
+  return (((size_t)(max_n + 1) * 4 + 15) & ~(size_t)15) + (size_t)((max_n - 1 + 3) / 4 + 1) * sizeof(uint4) +
+         (size_t)(max_n + 1) * 4;
+}
+
+int launch_seg_ttft(const SegParams &p, uint64_t begin, uint64_t end, void *stream) {
+  if (end <= begin) return 0;
+  const size_t smem = (size_t)(p.max_n + 2) * sizeof(int);
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(dsi_seg_ttft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  dsi_seg_ttft_kernel<<<(unsigned)(end - begin), 128, smem, (cudaStream_t)stream>>>(p, begin);
+  return (int)cudaGetLastError();
 }
 
 int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream) {

@@ -45,6 +45,11 @@ for flags in (D.DSI_F_MEANS_ONLY, D.DSI_F_MEANS_ONLY | FRESH):
 with D.Simulator(W.rows([(1.0, 0.1, 0.97, 5, 2, 8192, 2, 40), (1.0, 0.1, 0.5, 1, 2, 300, 0, 1000)]),
                  tick=0.01, seed=W.SEED, flags=D.DSI_F_MEANS_ONLY, n_shards=3) as sim:
     sim.run().reduce()
+with D.Simulator(ttft[:9], tick=ttick, seed=W.SEED, flags=D.DSI_F_MEANS_ONLY, n_shards=2) as sim:
+    sim.run().reduce()  # TTFT first-segment histograms and corrections
+with D.Simulator(W.rows([(1.0, 0.1, 0.6, 3, 2, 9000, 0, 30)]), tick=0.01, seed=W.SEED,
+                 flags=D.DSI_F_MEANS_ONLY) as sim:
+    sim.run().reduce()  # global-memory histograms (N > 8192)
 # multi-drafter kernel (dsi_multi.cu): D = 1, 2, 4, 7 variants, table and per-call q halves,
 # pattern mode and per-trial records, ragged tiles
 mf, mtick = W.multi_fuzz(20, seed=4, n_max=40, trials=70)

@@ -50,7 +50,7 @@ def assert_cells_equal(a, b, ctx=""):
             assert np.array_equal(x, y), (ctx, f)
 
 
-@pytest.mark.parametrize("name", ["fuzz", "cfg2", "cfg3", "cfg4", "long", "maxn", "fresh"])
+@pytest.mark.parametrize("name", ["fuzz", "cfg2", "cfg3", "cfg4", "long", "maxn", "fresh", "ttft", "ttft_mixed"])
 def test_sums_and_heatmap_bit_identical_to_default(name):
     flags = 0
     if name == "fuzz":
@@ -70,6 +70,16 @@ def test_sums_and_heatmap_bit_identical_to_default(name):
         cfgs = W.rows([(1.0, 0.1, 0.9, 4, 3, 32768, 0, 40), (1.0, 0.5, 0.6, 1, 1, 20000, 5, 33),
                        (1.0, 0.05, 0.3, 2, 7, 8193, 1, 70), (1.0, 0.2, 0.0, 1, 2, 32768, 0, 3)])
         tick = 0.01
+    elif name == "ttft":  # the Table-2 protocol with prefill (first forwards cost TTFT, R23)
+        cfgs, tick = W.cfg2_ttft(trials=3000)
+    elif name == "ttft_mixed":  # TTFT and plain configs sharing indicator groups, N up to 2000
+        rows = []
+        for i, (N, a) in enumerate([(50, 0.9), (300, 0.6), (2000, 0.8), (1, 0.5), (7, 0.0), (40, 1.0)]):
+            for k in (1, 3, 8):
+                rows.append((2.0, 0.3, a, k, 1 + i % 4, N, 0, 900, 0.0, 0.0))
+                rows.append((2.0, 0.3, a, k, 1 + i % 4, N, 0, 900, 9.5, 1.1))
+        cfgs = np.array(rows, dtype=W.CONFIG_DTYPE)
+        tick = 0.1
     else:
         cfgs, tick = W.cfg4(trials=500)
         flags = D.DSI_F_FRESH_VERIFIER
@@ -88,9 +98,14 @@ def test_sample_against_oracle():
         assert int(got[i]["sum_segments"]) == want["sum_m"] and int(got[i]["sum_accepts"]) == want["sum_acc"]
 
 
-@pytest.mark.parametrize("kw", [{"n_shards": 3}, {"n_shards": 11}, {"nccl": True}])
+@pytest.mark.parametrize("kw", [{"n_shards": 3}, {"n_shards": 11}, {"nccl": True}, {"n_shards": 5, "ttft": True},
+                                {"nccl": True, "ttft": True}])
 def test_partition_and_one_rank_nccl(kw):
-    cfgs, tick = W.cfg3(trials=700, k_max=20, cells=slice(2, 10100, 97))
+    kw = dict(kw)
+    if kw.pop("ttft", False):  # the TTFT list split across the parts' config ranges
+        cfgs, tick = W.cfg2_ttft(trials=2000)
+    else:
+        cfgs, tick = W.cfg3(trials=700, k_max=20, cells=slice(2, 10100, 97))
     want, want_cells = results(cfgs, tick, MEANS)
     extra = {"nccl_id": D.dsi_nccl_unique_id()} if kw.get("nccl") else kw
     got, got_cells = results(cfgs, tick, MEANS, **extra)
@@ -126,10 +141,6 @@ def test_options_validated():
         with pytest.raises(D.DsiError) as e:
             D.Simulator(cfgs, tick=tick, seed=SEED, flags=MEANS | flags)
         assert e.value.status == D.DSI_E_RANGE
-    ttft, ttick = W.cfg2_ttft(trials=10)
-    with pytest.raises(D.DsiError) as e:
-        D.Simulator(ttft, tick=ttick, seed=SEED, flags=MEANS)
-    assert e.value.status == D.DSI_E_RANGE
 
 
 def test_exact_expectation_at_2_pow_32_trials():
