@@ -163,3 +163,29 @@ def test_exact_expectation_at_2_pow_32_trials():
         for mean, std, ex in ((got[i]["mean_dsi"], ref[i]["std_dsi"], e["dsi"]),
                               (got[i]["mean_si"], ref[i]["std_si"], e["si"])):
             assert abs(float(mean) / 0.01 - float(ex)) < 6 * (float(std) / 0.01) / math.sqrt(T), (i, mean, ex)
+
+
+def test_full_heatmap_at_1e6_trials_against_exact_expectations():
+    """The whole paper grid (10 100 cells x k 1..200 = 2.02e6 configs, N = 100) at 1e6 trials per
+    config -- cheap in this mode -- against the exact expectations (tests/exact_math.py): every
+    per-config SI and DSI mean within 7 sigma / sqrt(T) (sigma from a 1e4-trial default run), and
+    Fig. 3(a)'s boundary on every cell whose exact SI/non-SI ratio is not within noise of 1."""
+    from test_heatmap import exact_results
+    cfgs, tick = W.cfg3()
+    ref, _ = results(cfgs, tick, 0)           # 1e4 trials: per-config std
+    big = cfgs.copy()
+    big["n_trials"] = 1_000_000
+    got, cells = results(big, tick, MEANS)
+    ex = exact_results(cfgs, tick)
+    T = 1_000_000
+    for f, sf in (("mean_si", "std_si"), ("mean_dsi", "std_dsi")):
+        tol = 7.0 * ref[sf] / np.sqrt(T) + 1e-9 * ex[f]
+        err = np.abs(got[f] - ex[f])
+        assert np.all(err <= tol), (f, int(np.argmax(err - tol)), float(np.max(err / np.maximum(tol, 1e-300))))
+    exact_cells = D.dsi_heatmap(cfgs, ex)
+    faster = cells["r_nonsi_si"] > 1.0
+    expect = exact_cells["accept_rate"] > exact_cells["t_drafter"] / exact_cells["t_target"]
+    # a cell may flip only if its exact non-SI/SI ratio is within 1e-3 of 1 (MC noise at 1e6 trials)
+    near = np.abs(exact_cells["r_nonsi_si"] - 1.0) < 1e-3
+    assert np.array_equal(faster[~near], expect[~near])
+    assert np.all(cells["r_nonsi_dsi"] >= 1.0 - 1e-3)
