@@ -1891,6 +1891,9 @@ void dsi_sim_destroy(dsi_sim *h) {
 }
 
 // ---- multi-drafter DSI: one-shot, one device -------------------------------
+#ifndef DSI_MULTI_WARP_LANES
+#define DSI_MULTI_WARP_LANES 32.0  // (A/B: 1.0 restores the per-lane rule)
+#endif
 #ifndef DSI_MULTI_TILE
 #define DSI_MULTI_TILE 2048  // trials per block (1024..8192 within 3%, profiles/r01_ab_multi.txt)
 #endif
@@ -1984,12 +1987,14 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     d.t_t = (int32_t)t_t;
     {
       // P(a quad still has an open position when drafter j is reached) = 1 - (1 - r)^4,
-      // r = prod_{i<j} (1 - a_i) the chance a position is open: call 4 quads together when
-      // that is >= 0.9 (<= ~10% extra calls), pairs when >= 0.6, else quad by quad
+      // r = prod_{i<j} (1 - a_i) the chance a position is open.  A warp makes a call when any
+      // of its 32 lanes needs it, so calling per quad saves work only when open quads are rare
+      // in the whole warp; otherwise 4 independent calls at once (ILP) win.
       double r = 1.0;
       for (int j = 0; j < c.n_drafters; ++j) {
         const double open = 1.0 - std::pow(1.0 - r, 4.0);
-        d.width[j] = open >= 0.9 ? 4 : (open >= 0.6 ? 2 : 1);
+        const double warp_needs = 1.0 - std::pow(1.0 - open, DSI_MULTI_WARP_LANES);
+        d.width[j] = warp_needs >= 0.9 ? 4 : (warp_needs >= 0.5 ? 2 : 1);
         r *= d.mode[j] == dsi::MODE_ALL_ACCEPT ? 0.0 : 1.0 - (double)d.thr[j] / 4294967296.0;
       }
     }
