@@ -94,7 +94,7 @@ def cmd_multi(a) -> dict:
         ds.append((float(t), float(acc)))
     cfg = W.multi_rows([(a.t_target, tuple(t for t, _ in ds), tuple(x for _, x in ds))], a.trials, a.n_tokens,
                        a.stream)
-    r = D.dsi_multi_simulate(cfg, tick=a.tick, seed=a.seed)[0][0]
+    r = D.dsi_multi_simulate(cfg, tick=a.tick, seed=a.seed, flags=D.DSI_F_MEANS_ONLY if a.means else 0)[0][0]
     m = len(ds) + 1
     return {"models": m, "mean_dsi": float(r["mean_dsi"]), "std_dsi": float(r["std_dsi"]),
             "mean_nonsi": float(r["mean_nonsi"]), "speedup_vs_nonsi": float(r["mean_nonsi"] / r["mean_dsi"]),
@@ -145,6 +145,7 @@ def main(argv=None) -> int:
     p.add_argument("--trials", type=int, default=100_000)
     p.add_argument("--tick", type=float, default=0.01)
     p.add_argument("--stream", type=int, default=0)
+    p.add_argument("--means", action="store_true", help="DSI_F_MEANS_ONLY (no std)")
     a = ap.parse_args(argv)
     try:
         out = {"plan": cmd_plan, "simulate": cmd_simulate, "table2": cmd_table2, "heatmap": cmd_heatmap,
