@@ -186,6 +186,7 @@ struct dsi_sim {
   std::vector<uint32_t> cfg_group;
   uint64_t hist_len = 0;
   std::vector<uint32_t> ttft_cfgs;        // means-only + TTFT: configs with a first-segment correction
+  std::vector<uint64_t> cfg_bounds;       // means-only: parts' config ranges (all ranks), cell-aligned
   bool use_nccl = false;                  // per-config moments summed with ncclAllReduce
   std::vector<uint32_t> perm;
   std::vector<dsi::CrnGroup> groups;
@@ -951,6 +952,32 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
 }  // namespace
 
 // ============================================================================= C ABI
+// Heatmap cells: maximal runs of consecutive configs with equal (t_target, t_drafter, a, SP, N).
+static void plan_heat_cells(dsi_sim *h) {
+  h->heat_cells.clear();
+  const auto &t = h->ticks;
+  for (size_t i = 0; i < h->n_cfg;) {
+    size_t j = i + 1;
+    while (j < h->n_cfg && t[j].ut == t[i].ut && t[j].ud == t[i].ud && t[j].a == t[i].a && t[j].sp == t[i].sp &&
+           t[j].n == t[i].n)
+      ++j;
+    h->heat_cells.push_back(dsi::HeatCell{(uint64_t)i, (uint32_t)(j - i), 0u});
+    i = j;
+  }
+}
+
+// Means-only, one device per process: every part's config range starts at a cell, so each
+// part's cells can be evaluated from its own moments (no all-reduce of the moments).
+static bool cells_aligned(const dsi_sim *h) {
+  if (!h->means_only || h->opt.n_devices != 1 || h->cfg_bounds.empty()) return false;
+  size_t ci = 0;
+  for (const uint64_t b : h->cfg_bounds) {
+    while (ci < h->heat_cells.size() && h->heat_cells[ci].first < b) ++ci;
+    if (b < h->n_cfg && (ci == h->heat_cells.size() || h->heat_cells[ci].first != b)) return false;
+  }
+  return true;
+}
+
 extern "C" {
 
 uint32_t dsi_abi_version(void) { return DSI_ABI_VERSION; }
@@ -1165,6 +1192,28 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   }
   tr.mark("plan+shard");
 
+  // means-only: the parts' config ranges, snapped to heatmap cell starts (dsi_sim_heatmap then
+  // evaluates each part's cells from its own moments)
+  if (means_only) {
+    try {
+      plan_heat_cells(h);
+      h->cfg_bounds.assign(parts + 1, 0);
+      size_t ci = 0;
+      for (int q = 0; q <= parts; ++q) {
+        const uint64_t want = (uint64_t)n_cfg * q / parts;
+        while (ci + 1 < h->heat_cells.size() && h->heat_cells[ci + 1].first <= want) ++ci;
+        uint64_t b = h->heat_cells.empty() ? want : h->heat_cells[ci].first;  // the cell start at or below
+        if (q == parts) b = n_cfg;
+        h->cfg_bounds[q] = std::max<uint64_t>(b, q ? h->cfg_bounds[q - 1] : 0);
+      }
+      h->heat_planned = true;
+      h->heat_uploaded = false;
+    } catch (...) {
+      h->err = "host tables";
+      return abort_create(DSI_E_NOMEM);
+    }
+  }
+
   // ---- devices
   int visible = 0;
   if (cudaGetDeviceCount(&visible) != cudaSuccess || visible < opt->device + opt->n_devices) {
@@ -1208,8 +1257,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     for (int sh = 0; sh < shards_per_dev; ++sh) {
       const int part = global_dev * shards_per_dev + sh;
       d.ranges.emplace_back(bounds[part], bounds[part + 1]);
-      // means-only: part p also evaluates configs [p n / parts, (p+1) n / parts)
-      d.cfg_ranges.emplace_back((uint64_t)n_cfg * part / parts, (uint64_t)n_cfg * (part + 1) / parts);
+      // means-only: part p also evaluates configs [cfg_bounds[p], cfg_bounds[p+1])
+      if (means_only) d.cfg_ranges.emplace_back(h->cfg_bounds[part], h->cfg_bounds[part + 1]);
     }
     if (e == cudaSuccess) {
       if (di == 0 && opt->stream) {
@@ -1709,16 +1758,7 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
   if (!n_cells) return fail(h, DSI_E_NULL, "n_cells is NULL");
   if (!h->heat_planned) {  // cells: maximal runs of equal (t_target, t_drafter, a, SP, N)
     try {
-      h->heat_cells.clear();
-      const auto &t = h->ticks;
-      for (size_t i = 0; i < h->n_cfg;) {
-        size_t j = i + 1;
-        while (j < h->n_cfg && t[j].ut == t[i].ut && t[j].ud == t[i].ud && t[j].a == t[i].a &&
-               t[j].sp == t[i].sp && t[j].n == t[i].n)
-          ++j;
-        h->heat_cells.push_back(dsi::HeatCell{(uint64_t)i, (uint32_t)(j - i), 0u});
-        i = j;
-      }
+      plan_heat_cells(h);
     } catch (...) {
       return fail(h, DSI_E_NOMEM, "host tables");
     }
@@ -1730,8 +1770,11 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
   if (!cells) return DSI_OK;
   if (cap < nc) return fail(h, DSI_E_RANGE, "cap is smaller than the number of cells");
   if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_heatmap before dsi_sim_run");
-  dsi_status st = sum_across(h, false);
-  if (st != DSI_OK) return st;
+  const bool local = cells_aligned(h);
+  if (!local) {
+    dsi_status st = sum_across(h, false);
+    if (st != DSI_OK) return st;
+  }
   DeviceState &d0 = h->dev[0];
   CUDA_TRY(h, cudaSetDevice(d0.ordinal));
   if (!h->heat_uploaded) {
@@ -1759,9 +1802,37 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
   p.tick = h->opt.tick;
   p.out = d0.d_heat_out;
   p.bad = d0.d_heat_bad;
-  const int e = dsi::launch_heatmap_kernel(p, d0.stream);
-  if (e) return cuda_fail(h, (cudaError_t)e, "heatmap kernel launch");
-  h->launches += 1;
+  if (!local) {
+    const int e = dsi::launch_heatmap_kernel(p, d0.stream);
+    if (e) return cuda_fail(h, (cudaError_t)e, "heatmap kernel launch");
+    h->launches += 1;
+  } else {
+    // this process's parts hold whole cells: evaluate them from the local moments, then (several
+    // ranks) one all-reduce of the 64-byte cell records, zero where another rank owns the cell
+    p.acc = d0.d_acc;
+    if (h->use_nccl) CUDA_TRY(h, cudaMemsetAsync(d0.d_heat_out, 0, nc * sizeof(dsi::HeatOut), d0.stream));
+    for (const auto &cr : d0.cfg_ranges) {
+      const auto lo = std::lower_bound(h->heat_cells.begin(), h->heat_cells.end(), cr.first,
+                                       [](const dsi::HeatCell &c, uint64_t v) { return c.first < v; });
+      const auto hi = std::lower_bound(h->heat_cells.begin(), h->heat_cells.end(), cr.second,
+                                       [](const dsi::HeatCell &c, uint64_t v) { return c.first < v; });
+      if (hi <= lo) continue;
+      dsi::HeatParams q = p;
+      q.cells = d0.d_heat_cells + (lo - h->heat_cells.begin());
+      q.out = d0.d_heat_out + (lo - h->heat_cells.begin());
+      q.n_cells = (uint32_t)(hi - lo);
+      const int e = dsi::launch_heatmap_kernel(q, d0.stream);
+      if (e) return cuda_fail(h, (cudaError_t)e, "heatmap kernel launch");
+      h->launches += 1;
+    }
+    if (h->use_nccl) {
+      static_assert(sizeof(dsi::HeatOut) == 64, "HeatOut is 8 words");
+      NcclApi &api = nccl();
+      const ncclResult_t r = api.AllReduce(d0.d_heat_out, d0.d_heat_out, nc * 8, ncclUint64, ncclSum, d0.comm,
+                                           d0.stream);
+      if (r != ncclSuccess) return fail(h, DSI_E_COMM, std::string("heatmap all-reduce: ") + api.GetErrorString(r));
+    }
+  }
   unsigned int bad = 0;
   CUDA_TRY(h, cudaMemcpyAsync(h->heat_out.p, d0.d_heat_out, nc * sizeof(dsi::HeatOut), cudaMemcpyDeviceToHost,
                               d0.stream));
