@@ -273,7 +273,9 @@ dsi_status dsi_heatmap(const dsi_config *cfg, const dsi_result *res, size_t n,
 /* On-device form: after dsi_sim_run, sums the moments across devices and
  * ranks (the all-reduce of dsi_sim_reduce; every rank must call it), evaluates every cell on
  * device 0 -- one warp per cell -- and copies only the cells back (64 B each instead of
- * 64 B per config).  Cells group consecutive configs with equal (t_target, t_drafter,
+ * 64 B per config).  With DSI_F_MEANS_ONLY and one device per process the ranks' config
+ * ranges hold whole cells: each rank evaluates its own cells and only the cell records are
+ * all-reduced (while the cells keep the layout they had at create).  Cells group consecutive configs with equal (t_target, t_drafter,
  * accept_rate, sp_degree, n_tokens) as given to create/update; the values are bit-identical
  * to dsi_heatmap over dsi_sim_reduce's results.  cells == NULL: *n_cells receives the
  * count (no device work).  DSI_E_RANGE if cap is too small, DSI_E_STATE before a run. */
