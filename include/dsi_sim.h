@@ -355,6 +355,15 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
  * host thread (CUDA events on the launching stream); launches of it in *launches. */
 dsi_status dsi_multi_last_kernel(float *ms, int32_t *launches);
 
+/* Test hook: cross-rank sums through a host function instead of NCCL.  While set (fn != NULL),
+ * handles and dsi_multi_simulate calls created with world > 1 need no nccl_id and one device per
+ * process; every cross-rank sum (moments, histograms, heatmap cells) copies the u64 words to the
+ * host, calls fn(buf, n, user) -- which must replace buf by the element-wise sum over all ranks
+ * and return 0 -- and copies them back.  It lets several ranks share one GPU (which NCCL refuses),
+ * e.g. with a torch.distributed gloo all_reduce.  Process-global; pass NULL to clear. */
+typedef int (*dsi_host_allreduce_fn)(uint64_t *buf, size_t n, void *user);
+dsi_status dsi_set_host_allreduce(dsi_host_allreduce_fn fn, void *user);
+
 /* Pure sharder (host only, no device): split per-unit costs into `parts`
  * contiguous ranges of near-equal total cost.  cost_units[i] >= 0.
  * bounds must hold parts+1 entries; bounds[0] = 0, bounds[parts] = n.

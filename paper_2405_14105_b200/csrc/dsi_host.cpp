@@ -187,7 +187,8 @@ struct dsi_sim {
   uint64_t hist_len = 0;
   std::vector<uint32_t> ttft_cfgs;        // means-only + TTFT: configs with a first-segment correction
   std::vector<uint64_t> cfg_bounds;       // means-only: parts' config ranges (all ranks), cell-aligned
-  bool use_nccl = false;                  // per-config moments summed with ncclAllReduce
+  bool use_nccl = false;                  // per-config moments summed across devices/ranks
+  bool host_coll = false;                 // ... through the host all-reduce hook instead of NCCL
   std::vector<uint32_t> perm;
   std::vector<dsi::CrnGroup> groups;
   std::vector<dsi::CrnUnit> crn_units;
@@ -211,6 +212,14 @@ struct dsi_sim {
 };
 
 namespace {
+// Test hook (dsi_set_host_allreduce): cross-rank sums through a caller-supplied host function
+// instead of NCCL, so multi-rank runs can be exercised where NCCL cannot form a communicator
+// (several ranks on one GPU).
+dsi_host_allreduce_fn g_host_ar = nullptr;
+void *g_host_ar_user = nullptr;
+}  // namespace
+
+namespace {
 
 dsi_status fail(dsi_sim *h, dsi_status s, const std::string &msg) {
   if (h) h->err = msg; else g_create_error = msg;
@@ -227,6 +236,24 @@ dsi_status cuda_fail(dsi_sim *h, cudaError_t e, const char *what) {
     cudaError_t e_ = (call);                               \
     if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
   } while (0)
+
+// In-place-or-copy sum of count u64 words across the ranks through the host hook (one device per
+// process): device -> host, hook, host -> device, synchronous on the stream.
+dsi_status host_allreduce(dsi_sim *h, cudaStream_t st, const void *src, void *dst, size_t count) {
+  std::vector<uint64_t> buf;
+  try {
+    buf.resize(count);
+  } catch (...) {
+    return fail(h, DSI_E_NOMEM, "host all-reduce buffer");
+  }
+  CUDA_TRY(h, cudaMemcpyAsync(buf.data(), src, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  if (!g_host_ar || g_host_ar(buf.data(), count, g_host_ar_user) != 0)
+    return fail(h, DSI_E_COMM, "host all-reduce hook failed");
+  CUDA_TRY(h, cudaMemcpyAsync(dst, buf.data(), count * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  return DSI_OK;
+}
 
 dsi_status to_ticks(double x, double tick, int64_t *out) {
   if (!std::isfinite(x) || x <= 0.0) return DSI_E_RANGE;
@@ -749,6 +776,13 @@ bool same_plan_keys(const std::vector<CfgTicks> &a, const std::vector<CfgTicks> 
 dsi_status sum_across(dsi_sim *h, bool hist) {
   if (!h->use_nccl) return DSI_OK;
   const size_t n_cfg = h->n_cfg;
+  if (h->host_coll) {
+    DeviceState &d = h->dev[0];
+    dsi_status st = host_allreduce(h, d.stream, d.d_acc, d.d_red, n_cfg * dsi::NF);
+    if (st == DSI_OK && hist) st = host_allreduce(h, d.stream, d.d_seg, d.d_seg_red, n_cfg * 64);
+    if (st == DSI_OK && hist) st = host_allreduce(h, d.stream, d.d_si, d.d_si_red, h->si_bins_total);
+    return st;
+  }
   NcclApi &api = nccl();
   ncclResult_t r = api.GroupStart();
   for (auto &d : h->dev) {
@@ -1075,7 +1109,10 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       (opt->block_threads < 32 || opt->block_threads > 128 || opt->block_threads % 32))
     return fail(nullptr, DSI_E_RANGE, "block_threads must be a multiple of 32 in [32, 128]");
   const int total_devices = opt->world * opt->n_devices;
-  if (total_devices > 1 && !opt->nccl_id)
+  const bool host_coll = g_host_ar != nullptr && opt->world > 1;
+  if (host_coll && opt->n_devices != 1)
+    return fail(nullptr, DSI_E_RANGE, "the host all-reduce hook needs one device per process");
+  if (total_devices > 1 && !opt->nccl_id && !host_coll)
     return fail(nullptr, DSI_E_NULL, "nccl_id is required when world*n_devices > 1");
   // NCCL whenever several devices take part, or when the caller passes an id for a
   // one-rank communicator (exercises the collective path on one GPU)
@@ -1105,6 +1142,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   h->shared = shared;
   h->means_only = means_only;
   h->use_nccl = use_nccl;
+  h->host_coll = host_coll;
   h->block_threads = shared ? kCrnThreads : (opt->block_threads ? opt->block_threads : kDefaultThreads);
   try {
     h->ticks.resize(n_cfg);
@@ -1326,7 +1364,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
 
   tr.mark("upload");
   // ---- NCCL: one communicator per device over world * n_devices ranks
-  if (use_nccl) {
+  if (use_nccl && !host_coll) {
     NcclApi &api = nccl();
     if (!api.ok) {
       h->err = "libnccl.so.2 could not be loaded";
@@ -1581,7 +1619,13 @@ dsi_status dsi_sim_run(dsi_sim *h) {
   }
   if (h->means_only) {
     // every device needs every group's full histogram: one (grouped) all-reduce, in place
-    if (h->use_nccl) {
+    if (h->use_nccl && h->host_coll) {
+      DeviceState &d = h->dev[0];
+      dsi_status st = host_allreduce(h, d.stream, d.d_hist, d.d_hist, h->hist_len);
+      if (st == DSI_OK && !h->ttft_cfgs.empty())
+        st = host_allreduce(h, d.stream, d.d_hist + 2 * h->hist_len, d.d_hist + 2 * h->hist_len, h->hist_len);
+      if (st != DSI_OK) return st;
+    } else if (h->use_nccl) {
       NcclApi &api = nccl();
       ncclResult_t r = api.GroupStart();
       for (auto &d : h->dev) {
@@ -1825,7 +1869,10 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
       if (e) return cuda_fail(h, (cudaError_t)e, "heatmap kernel launch");
       h->launches += 1;
     }
-    if (h->use_nccl) {
+    if (h->use_nccl && h->host_coll) {
+      const dsi_status st = host_allreduce(h, d0.stream, d0.d_heat_out, d0.d_heat_out, nc * 8);
+      if (st != DSI_OK) return st;
+    } else if (h->use_nccl) {
       static_assert(sizeof(dsi::HeatOut) == 64, "HeatOut is 8 words");
       NcclApi &api = nccl();
       const ncclResult_t r = api.AllReduce(d0.d_heat_out, d0.d_heat_out, nc * 8, ncclUint64, ncclSum, d0.comm,
@@ -2005,9 +2052,10 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     return fail(nullptr, DSI_E_RANGE, "need 0 <= rank < world");
   if (opt->n_shards < 0 || opt->n_shards > 4096 || (opt->n_shards > 1 && opt->world > 1))
     return fail(nullptr, DSI_E_RANGE, "n_shards must be 0..4096 and > 1 only with world == 1");
-  if (opt->world > 1 && !opt->nccl_id)
+  const bool host_coll = g_host_ar != nullptr && opt->world > 1;
+  if (opt->world > 1 && !opt->nccl_id && !host_coll)
     return fail(nullptr, DSI_E_NULL, "nccl_id is required when world > 1");
-  const bool use_nccl = opt->world > 1 || opt->nccl_id != nullptr;
+  const bool use_nccl = (opt->world > 1 || opt->nccl_id != nullptr) && !host_coll;
   const bool per_trial = opt->flags & DSI_F_PER_TRIAL;
   if (per_trial && opt->world > 1)
     return fail(nullptr, DSI_E_RANGE, "DSI_F_PER_TRIAL needs world == 1");
@@ -2221,6 +2269,15 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   }
   g_multi_launches = launches;
   if (timing) MULTI_TRY(cudaEventRecord(ev.e1, stream));
+  if (host_coll) {
+    std::vector<uint64_t> hb(nk * dsi::MF);
+    MULTI_TRY(cudaMemcpyAsync(hb.data(), b_acc.p, acc_bytes, cudaMemcpyDeviceToHost, stream));
+    MULTI_TRY(cudaStreamSynchronize(stream));
+    if (g_host_ar(hb.data(), hb.size(), g_host_ar_user) != 0)
+      return fail(nullptr, DSI_E_COMM, "host all-reduce hook failed");
+    MULTI_TRY(cudaMemcpyAsync(b_acc.p, hb.data(), acc_bytes, cudaMemcpyHostToDevice, stream));
+    MULTI_TRY(cudaStreamSynchronize(stream));
+  }
   if (use_nccl) {
     // one communicator for this call (ranks of the world, one device each), one all-reduce
     NcclApi &api = nccl();
@@ -2288,6 +2345,12 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
     r.std_dsi = means ? std::nan("") : std::sqrt((double)num) / Td * tick;
   }
   tr.mark("finalize");
+  return DSI_OK;
+}
+
+dsi_status dsi_set_host_allreduce(dsi_host_allreduce_fn fn, void *user) {
+  g_host_ar = fn;
+  g_host_ar_user = user;
   return DSI_OK;
 }
 

@@ -99,6 +99,7 @@ def _load():
         "dsi_heatmap_csv": ([V, sz, ctypes.c_char_p], ctypes.c_int),
         "dsi_multi_simulate": ([P(dsi_options), V, sz, V, V, V], ctypes.c_int),
         "dsi_multi_last_kernel": ([P(ctypes.c_float), P(i32)], ctypes.c_int),
+        "dsi_set_host_allreduce": ([V, V], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         if "DSI_SIM_LIB" in os.environ and not hasattr(lib, name):
@@ -115,7 +116,8 @@ EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce",
             "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
             "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
             "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
-            "dsi_heatmap_csv", "dsi_sim_heatmap", "dsi_multi_simulate", "dsi_multi_last_kernel")
+            "dsi_heatmap_csv", "dsi_sim_heatmap", "dsi_multi_simulate", "dsi_multi_last_kernel",
+            "dsi_set_host_allreduce")
 
 
 class DsiError(RuntimeError):
@@ -208,6 +210,32 @@ def dsi_multi_simulate(configs: np.ndarray, *, tick: float, seed: int, flags: in
                                   dsi.ctypes.data if dsi is not None else None,
                                   settled.ctypes.data if settled is not None else None), create=True)
     return out, dsi, settled
+
+
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.c_size_t,
+                                     ctypes.c_void_p)
+_host_allreduce_ref = None  # keeps the ctypes callback alive while registered
+
+
+def dsi_set_host_allreduce(fn) -> None:
+    """Test hook: cross-rank sums through fn(words: np.ndarray[uint64]) -> None, which must sum
+    the array element-wise over all ranks in place (e.g. a torch.distributed gloo all_reduce).
+    None clears it.  See include/dsi_sim.h."""
+    global _host_allreduce_ref
+    if fn is None:
+        _host_allreduce_ref = None
+        _check(lib.dsi_set_host_allreduce(None, None))
+        return
+
+    def cb(buf, n, _user):
+        try:
+            fn(np.ctypeslib.as_array(buf, shape=(n,)))
+            return 0
+        except Exception:  # noqa: BLE001  (reported to the library as a failed hook)
+            return 1
+
+    _host_allreduce_ref = HOST_ALLREDUCE_FN(cb)
+    _check(lib.dsi_set_host_allreduce(ctypes.cast(_host_allreduce_ref, ctypes.c_void_p), None))
 
 
 def dsi_multi_last_kernel() -> tuple:
