@@ -367,8 +367,23 @@ def ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DSI_BENCH_ONE_GPU=1 (test mode, numbers meaningless): every rank on GPU 0, gloo process
+    # group, the library's cross-rank sums through the host all-reduce hook -- exercises the
+    # whole multi-rank flow on a one-GPU box (NCCL refuses two ranks on one GPU)
+    one_gpu = world > 1 and os.environ.get("DSI_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    coll_dev = "cpu" if one_gpu else "cuda"
+    if world > 1 and one_gpu:
+        dist.init_process_group("gloo")
+
+        def _host_allreduce(words):
+            t = torch.from_numpy(words.view(np.int64))  # u64 sums as wrapping int64 sums
+            dist.all_reduce(t)
+
+        D.dsi_set_host_allreduce(_host_allreduce)
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfgs, tick = workload(args.workload, D.dsi_min_lookahead)
 
@@ -379,21 +394,21 @@ def ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: int) -> int:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.int64, device="cuda")
+        t = torch.tensor([x], dtype=torch.int64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return int(t.item())
 
     def fresh_nccl_id():
         """A new NCCL unique id for each handle (an id serves one communicator): made on rank 0,
         broadcast to all ranks (every rank calls this in the same order)."""
-        if world == 1:
+        if world == 1 or one_gpu:
             return None
         obj = [D.dsi_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)

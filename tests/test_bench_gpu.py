@@ -31,3 +31,28 @@ def test_bench_json_line_small_workload():
     assert d["multi_drafter"]["value"] > 0 and 0 < d["multi_drafter"]["roofline"]["frac"] <= 1.0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """The multi-rank bench flow (torchrun, fresh ids per handle, REDUCE_TO_ROOT, max over ranks,
+    every block's consistency checks) with both ranks on GPU 0: DSI_BENCH_ONE_GPU=1 puts the
+    library's cross-rank sums on a gloo host all-reduce (NCCL refuses two ranks on one GPU)."""
+    import socket
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, DSI_BENCH_ONE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--workload", "cfg2", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2" and d["value"] > 0
+    assert d["heatmap"]["device_cells_equal_host_product"] is True
+    assert d["shared_streams"]["bit_identical_to_value_run"] is True
+    assert d["means_only"]["sums_and_means_identical_to_value_run"] is True
