@@ -1682,7 +1682,6 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   if (n != n_cfg) return fail(h, DSI_E_RANGE, "n must equal n_cfg");
   if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_reduce before dsi_sim_run");
   const bool hist = h->opt.flags & DSI_F_HIST;
-  const size_t nacc = n_cfg * dsi::NF;
   dsi_status st = sum_across(h, hist);
   if (st != DSI_OK) return st;
   tr.mark("allreduce-enqueue");
