@@ -12,6 +12,8 @@
 rows offline with lookahead in {1, 5, 10}, SI over all of them and DSI over the
 Eq.-1-feasible ones (the protocol of P:273); `heatmap` is Fig. 3 (P:290-311, P:525-535);
 `multi` is Algorithm 1 with several drafters (latency:acceptance, fastest first), lookahead 1.
+`heatmap` also runs sharded over GPUs under torchrun (one process per GPU; rank 0 writes the CSV):
+    python -m torch.distributed.run --nproc-per-node 8 -m paper_2405_14105_b200 heatmap --means --csv h.csv
 Exit codes: 0 success, 2 invalid arguments (DSI_E_RANGE / DSI_E_TICK / ...), 3 device error.
 """
 from __future__ import annotations
@@ -68,6 +70,31 @@ def cmd_table2(a) -> list:
     return table2(a.trials, a.sp, a.n_tokens, a.seed, prefill=a.prefill)
 
 
+def _distributed_kw():
+    """Under torchrun (WORLD_SIZE > 1): one process per GPU, a torch.distributed process group for
+    the plumbing and a fresh NCCL unique id for the library's communicator.  DSI_BENCH_ONE_GPU=1
+    (tests) keeps every rank on GPU 0 with gloo and the library's host all-reduce hook."""
+    import os
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world == 1:
+        return {}, 0
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("DSI_BENCH_ONE_GPU") == "1":
+        local = 0
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+        D.dsi_set_host_allreduce(lambda w: dist.all_reduce(torch.from_numpy(w.view(np.int64))))
+        return dict(device=local, rank=rank, world=world), rank
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [D.dsi_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return dict(device=local, rank=rank, world=world, nccl_id=obj[0]), rank
+
+
 def cmd_heatmap(a) -> dict:
     if a.k:  # one lookahead for SI and DSI: the static panels of Fig. 5 (P:670-693)
         cfgs, tick = W.cfg3(trials=a.trials, k_min=a.k, k_max=a.k, sp=a.sp, n_tokens=a.n_tokens)
@@ -75,9 +102,10 @@ def cmd_heatmap(a) -> dict:
         cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
     flags = ((D.DSI_F_SHARED_STREAMS if a.shared else 0) | (D.DSI_F_FRESH_VERIFIER if a.fresh else 0) |
              (D.DSI_F_MEANS_ONLY if a.means else 0))
-    with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags) as sim:
-        cells = sim.run().heatmap()
-    if a.csv:
+    kw, rank = _distributed_kw()  # torchrun: the grid is sharded over the ranks' GPUs
+    with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags, **kw) as sim:
+        cells = sim.run().heatmap()  # collective: every rank gets every cell
+    if a.csv and rank == 0:
         D.dsi_heatmap_csv(cells, a.csv)
     i = int(np.nanargmax(cells["r_min_dsi"]))
     return {"cells": int(cells.size), "csv": a.csv,
@@ -153,5 +181,7 @@ def main(argv=None) -> int:
     except D.DsiError as e:
         print(str(e), file=sys.stderr)
         return 3 if e.status in (D.DSI_E_DEVICE, D.DSI_E_COMM, D.DSI_E_NOMEM) else 2
-    print(json.dumps(out, indent=1))
+    import os
+    if os.environ.get("RANK", "0") == "0":  # under torchrun only rank 0 reports
+        print(json.dumps(out, indent=1))
     return 0

@@ -148,3 +148,26 @@ def test_heatmap_cli_means_only_matches_shared(tmp_path):
         rc, out, err = run_cli("heatmap", "--trials", "400", "--k-max", "20", "--csv", str(path), flag)
         assert rc == 0, err
     assert a.read_text() == b.read_text()
+
+
+@pytest.mark.gpu
+def test_heatmap_cli_under_torchrun_matches_one_process(tmp_path):
+    """The CLI heatmap sharded over 2 ranks (torchrun; both on GPU 0 through the host all-reduce
+    hook, DSI_BENCH_ONE_GPU=1) writes the same CSV as one process."""
+    import os
+    import socket
+    one, two = tmp_path / "one.csv", tmp_path / "two.csv"
+    rc, out, err = run_cli("heatmap", "--trials", "500", "--k-max", "20", "--means", "--csv", str(one))
+    assert rc == 0, err
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "-m", "paper_2405_14105_b200",
+                        "heatmap", "--trials", "500", "--k-max", "20", "--means", "--csv", str(two)],
+                       capture_output=True, text=True, cwd=ROOT, env=dict(os.environ, DSI_BENCH_ONE_GPU="1"),
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert one.read_text() == two.read_text()
+    assert json.loads(r.stdout)["cells"] == 10100
