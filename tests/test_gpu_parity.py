@@ -656,3 +656,21 @@ def test_reduce_to_root_flag_on_rank_zero():
     for f in want.dtype.names:
         assert np.array_equal(got[f], want[f]) or np.allclose(got[f], want[f], equal_nan=True), f
     sim.close()
+
+
+@pytest.mark.parametrize("case", ["worst_case", "best_case"])
+def test_table1_on_the_gpu(case):
+    """Table 1 straight from the GPU path: tokens generated by t1..t4 with a 14%
+    drafter, lookahead 1, SP 7 (tests/golden/table1.json), from one trial per N = 1..79."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table1.json")))
+    a = g[case]["accept_rate"]
+    rows = [(float(g["t_target"]), float(g["t_drafter"]), a, g["lookahead"], g["sp_degree"], n, 0, 1)
+            for n in range(1, 80)]
+    sim, res = run_sim(W.rows(rows), 1.0, flags=0)
+    lat = {"nonsi": res["nonsi_ticks"], "si": res["sum_si_ticks"], "dsi": res["sum_dsi_ticks"]}
+    for alg in ("nonsi", "si", "dsi"):
+        counts = [max(n for n in range(1, 80) if lat[alg][n - 1] <= t) for t in g["times"]]
+        assert counts == g[case][alg], (case, alg, counts)
+    sim.close()
