@@ -674,3 +674,32 @@ def test_table1_on_the_gpu(case):
         counts = [max(n for n in range(1, 80) if lat[alg][n - 1] <= t) for t in g["times"]]
         assert counts == g[case][alg], (case, alg, counts)
     sim.close()
+
+
+def test_worked_examples_on_the_gpu():
+    """The hand-derived examples of tests/golden/worked_examples.json (Prop. 1's 426, the SP=2 / SP=1
+    schedules 540 / 700, S:202's 1020 ms, ...) straight from the GPU path: pattern mode reads
+    the example's acceptance pattern from the trial index (A_p = bit p-1), a = 0 / 1 otherwise."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))["examples"]
+    for e in g:
+        N = e["n_tokens"]
+        A = e["A"]
+        if isinstance(A, list):
+            idx = sum(bit << p for p, bit in enumerate(A))
+            row = [(float(e["t_target"]), float(e["t_drafter"]), 0.5, e["lookahead"], e["sp_degree"], N, 0, idx + 1)]
+            sim, res = run_sim(W.rows(row), 1.0, flags=D.DSI_F_PATTERN | D.DSI_F_PER_TRIAL)
+            tr = sim.trials(0, idx, 1)
+            got = {"dsi": int(tr["dsi"][0]), "si": int(tr["si"][0]), "iters": int(tr["iters"][0])}
+        else:
+            a = 1.0 if A == "all1" else 0.0
+            row = [(float(e["t_target"]), float(e["t_drafter"]), a, e["lookahead"], e["sp_degree"], N, 0, 1)]
+            sim, res = run_sim(W.rows(row), 1.0, flags=D.DSI_F_PER_TRIAL)
+            tr = sim.trials(0)
+            got = {"dsi": int(tr["dsi"][0]), "si": int(tr["si"][0]), "iters": int(tr["iters"][0])}
+        got["nonsi"] = int(res[0]["nonsi_ticks"])
+        for key in ("dsi", "si", "iters", "nonsi"):
+            if key in e:
+                assert got[key] == e[key], (e["name"], key, got[key])
+        sim.close()
