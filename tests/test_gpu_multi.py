@@ -210,3 +210,20 @@ def test_means_only_shares_passes_across_latencies(name):
     assert (got["sumsq_dsi_ticks"] == 0).all() and np.isnan(got["std_dsi"]).all()
     with pytest.raises(D.DsiError):
         D.dsi_multi_simulate(cfgs[:2], tick=tick, seed=SEED, flags=D.DSI_F_MEANS_ONLY, per_trial=True)
+
+
+def test_golden_hand_traced_trees_on_the_gpu():
+    """tests/golden/multi_drafter.json (hand-traced thread trees of Alg. 1, P:418's sum) from the
+    GPU path in pattern mode (digit p-1 of the trial index in base m is j*(p) - 1)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "multi_drafter.json")))["examples"]
+    for e in g:
+        m = len(e["t_drafters"]) + 1
+        idx = sum((j - 1) * m ** p for p, j in enumerate(e["j_star"]))
+        cfgs = W.multi_rows([(float(e["t_target"]), tuple(float(x) for x in e["t_drafters"]),
+                              (0.5,) * (m - 1))], idx + 1, e["n_tokens"])
+        res, dsi, settled = D.dsi_multi_simulate(cfgs, tick=1.0, seed=SEED, per_trial=True, flags=D.DSI_F_PATTERN)
+        assert int(dsi[idx]) == e["dsi"], e["name"]
+        assert [int(x) for x in settled[idx, :m]] == e["settled"], e["name"]
+        assert int(res[0]["nonsi_ticks"]) == e["nonsi"]
