@@ -703,3 +703,29 @@ def test_worked_examples_on_the_gpu():
             if key in e:
                 assert got[key] == e[key], (e["name"], key, got[key])
         sim.close()
+
+
+def test_fresh_verifier_golden_on_the_gpu():
+    """tests/golden/fresh_verifier.json (hand-derived schedules of R24) from the GPU path, with and
+    without DSI_F_FRESH_VERIFIER."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fresh_verifier.json")))["examples"]
+    e = g[0]
+    rows = [(float(e["t_target"]), float(e["t_drafter"]), 1.0, e["lookahead"], e["sp_degree"], n, 0, 1)
+            for n in range(1, len(e["dsi_by_n_tokens"]) + 1)]
+    for flags, want in ((FRESH, e["dsi_by_n_tokens"]), (0, e["default_dsi_by_n_tokens"])):
+        sim, res = run_sim(W.rows(rows), 1.0, flags=flags)
+        assert [int(x) for x in res["sum_dsi_ticks"]] == want, flags
+        sim.close()
+    e = g[1]
+    idx = sum(bit << p for p, bit in enumerate(e["A"]))
+    row = [(float(e["t_target"]), float(e["t_drafter"]), 0.5, e["lookahead"], e["sp_degree"], e["n_tokens"], 0,
+            idx + 1)]
+    for flags, key in ((FRESH, "dsi"), (0, "default_dsi")):
+        sim, _ = run_sim(W.rows(row), 1.0, flags=flags | D.DSI_F_PATTERN | D.DSI_F_PER_TRIAL)
+        tr = sim.trials(0, idx, 1)
+        assert int(tr["dsi"][0]) == e[key], key
+        if key == "dsi":
+            assert int(tr["si"][0]) == e["si"]
+        sim.close()
