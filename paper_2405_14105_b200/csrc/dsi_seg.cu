@@ -195,16 +195,33 @@ __global__ void __launch_bounds__(128) dsi_seg_ttft_kernel(const SegParams P, ui
   }
 }
 
-// P[g] = H[1] + ... + H[g] (P[0] = 0) per group, for the bucketed evaluation below.
-__global__ void dsi_seg_prefix_kernel(const SegParams P) {
-  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gi >= P.n_groups) return;
-  const SegGroup G = P.groups[gi];
+// P[g] = H[1] + ... + H[g] (P[0] = 0) per group, for the bucketed evaluation below: one block
+// per group, each thread scans a contiguous chunk, chunk totals scanned across the block.
+__global__ void __launch_bounds__(128) dsi_seg_prefix_kernel(const SegParams P) {
+  __shared__ unsigned long long warp_tot[4];
+  const SegGroup G = P.groups[blockIdx.x];
   const unsigned long long *H = P.hist + G.hist_off;
   unsigned long long *pre = P.pre + G.hist_off;
-  unsigned long long run = 0;
-  pre[0] = 0;
-  for (int g = 1; g <= G.n_tokens; ++g) {
+  const int N = G.n_tokens;
+  const int per = (N + blockDim.x - 1) / blockDim.x;  // bins 1..N in chunks
+  const int lo = 1 + (int)threadIdx.x * per, hi = min(lo + per - 1, N);
+  unsigned long long sum = 0;
+  for (int g = lo; g <= hi; ++g) sum += H[g];
+  // inclusive scan of the chunk sums: within the warp, then across the four warps
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  unsigned long long inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (unsigned)o) inc += v;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  unsigned long long base = 0;
+  for (unsigned w = 0; w < warp; ++w) base += warp_tot[w];
+  unsigned long long run = base + inc - sum;  // exclusive prefix of this chunk
+  if (threadIdx.x == 0) pre[0] = 0;
+  for (int g = lo; g <= hi; ++g) {
     run += H[g];
     pre[g] = run;
   }
@@ -308,7 +325,8 @@ int launch_seg_hist(const SegParams &p, uint64_t n_units, void *stream) {
 }
 
 int launch_seg_prefix(const SegParams &p, void *stream) {
-  dsi_seg_prefix_kernel<<<(p.n_groups + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
+  if (p.n_groups == 0) return 0;
+  dsi_seg_prefix_kernel<<<p.n_groups, 128, 0, (cudaStream_t)stream>>>(p);
   return (int)cudaGetLastError();
 }
 
