@@ -634,6 +634,16 @@ def ours(args):
     except OSError:
         pass
     traffic = prof.get("dram_bytes_per_launch") if prof.get("workload") == args.workload else None
+    ncu = None  # the pipe and issue utilisation ncu measured for this kernel (north_star: >= 60% issue)
+    sf = prof.get("set_full_stride20") if prof.get("workload") == args.workload else None
+    if sf:
+        def _pct(key):
+            v = sf.get(key)
+            return float(v[1]) if v else None
+        ncu = {"issue_active_pct": _pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+               "fmaheavy_pct": _pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+               "alu_pct": _pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+               "source": f"profiles/{prof.get('round', '?')}_ncu_summary.json (--set full, 1/20 of the grid)"}
 
     multi = None
     if rank == 0 and not args.no_multi:
@@ -677,6 +687,7 @@ def ours(args):
                          "frac_at_measured_clock": (mults / (kern_ms / 1000.0) /
                                                     (mul_peak(sm_max) * clk["sm_mhz"] / sm_max)
                                                     if clk.get("sm_mhz") else None),
+                         "ncu": ncu,
                          "issue_slots": {"achieved": achieved / 1e9, "peak": peak_instr / 1e9,
                                          "unit": "Ginstr/s", "frac": achieved / peak_instr,
                                          "work": "11 + 10(1-a) thread-instructions per trial-token "
