@@ -189,3 +189,24 @@ def test_full_heatmap_at_1e6_trials_against_exact_expectations():
     near = np.abs(exact_cells["r_nonsi_si"] - 1.0) < 1e-3
     assert np.array_equal(faster[~near], expect[~near])
     assert np.all(cells["r_nonsi_dsi"] >= 1.0 - 1e-3)
+
+
+def test_degenerate_sizes_every_mode():
+    """n_trials = 1 and N in {1, 2, 33} with a in {0, 0.5, 1}: the default, shared-stream and
+    means-only modes give the oracle's sums (one trial per config, one-token runs, a = 0 / 1 groups)."""
+    from helpers import oracle_sums
+    rows = []
+    for N in (1, 2, 33):
+        for a in (0.0, 0.5, 1.0):
+            for k in (1, 4):
+                rows.append((1.0, 0.2, a, k, 3, N, 0, 1))
+    cfgs = W.rows(rows)
+    outs = {}
+    for name, flags in (("default", 0), ("shared", D.DSI_F_SHARED_STREAMS), ("means", MEANS)):
+        outs[name], _ = results(cfgs, 0.01, flags)
+    for i, row in enumerate(cfgs):
+        want = oracle_sums(row, 0.01, SEED)
+        for name, got in outs.items():
+            assert int(got[i]["sum_dsi_ticks"]) == want["sum_dsi"], (name, i)
+            assert int(got[i]["sum_si_ticks"]) == want["sum_si"], (name, i)
+            assert int(got[i]["sum_segments"]) == want["sum_m"], (name, i)
