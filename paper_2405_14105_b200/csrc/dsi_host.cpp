@@ -178,6 +178,7 @@ struct dsi_sim {
   int32_t max_n = 1, max_keff = 1;
   bool any_ttft = false;
   bool any_fresh = false;                 // DSI_F_FRESH_VERIFIER and some k t_d > t_t
+  bool k1_fast = false;                   // trial kernel variant with the k = 1 no-queue fast path
   uint64_t si_bins_total = 0;
   bool shared = false;                    // DSI_F_SHARED_STREAMS
   bool means_only = false;                // DSI_F_MEANS_ONLY (dsi_seg.cu)
@@ -726,6 +727,7 @@ dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks) {
   struct Lim {
     int32_t max_n = 1, max_keff = 1;
     bool ttft = false, fresh = false;
+    double work = 0.0, work_k1 = 0.0;  // trial-tokens in all configs / in k = 1 configs without queueing
   } lim;
   std::mutex mu;
   const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
@@ -737,12 +739,17 @@ dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks) {
       l.max_keff = std::max(l.max_keff, std::min(t.k, t.n));
       l.ttft = l.ttft || t.t_t1 != t.t_t || t.t_d1 != t.t_d;
       l.fresh = l.fresh || (fresh && t.kd > t.t_t);
+      const double w = (double)t.trials * (double)t.n;
+      l.work += w;
+      if (std::min(t.k, t.n) == 1 && config_noqueue(t)) l.work_k1 += w;
     }
     std::lock_guard<std::mutex> lock(mu);
     lim.max_n = std::max(lim.max_n, l.max_n);
     lim.max_keff = std::max(lim.max_keff, l.max_keff);
     lim.ttft = lim.ttft || l.ttft;
     lim.fresh = lim.fresh || l.fresh;
+    lim.work += l.work;
+    lim.work_k1 += l.work_k1;
   });
   if (lim.ttft && lim.max_n > 4096) return fail(h, DSI_E_RANGE, "the TTFT variant supports n_tokens <= 4096");
   if (dsi::trial_kernel_smem(lim.max_n, lim.max_keff, h->opt.flags & DSI_F_HIST, lim.ttft) > 200 * 1024)
@@ -753,6 +760,10 @@ dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks) {
   h->max_keff = lim.max_keff;
   h->any_ttft = lim.ttft;
   h->any_fresh = lim.fresh;
+  // the k = 1 fast path (dsi_kernel.cu, VAR 3) pays for its extra code only when such configs carry
+  // a good share of the work (measured: config 5, 86% of its configs, -14%; config 3, 0.5%, +2% if on)
+  h->k1_fast = !lim.ttft && !lim.fresh && lim.work_k1 >= 0.25 * lim.work;
+  if (const char *f = std::getenv("DSI_K1_FAST")) h->k1_fast = !lim.ttft && !lim.fresh && std::atoi(f) != 0;
   return DSI_OK;
 }
 
@@ -1538,6 +1549,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     p.max_keff = h->max_keff;
     p.any_ttft = h->any_ttft ? 1 : 0;
     p.any_fresh = h->any_fresh ? 1 : 0;
+    p.k1_fast = h->k1_fast ? 1 : 0;
     const uint32_t s_lo = (uint32_t)h->opt.seed, s_hi = (uint32_t)(h->opt.seed >> 32);
     for (int r = 0; r < 10; ++r) {
       p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;

@@ -107,7 +107,8 @@ __device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint
 __host__ __device__ __forceinline__ size_t t_table_bytes(int n) { return (size_t)((n + 2) & ~1) * 8; }
 __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t)((n - 1 + 3) / 4 + 1) * 16; }
 
-// VAR: 0 = default model, 1 = TTFT variant present, 2 = fresh-verifier variant present
+// VAR: 0 = default model, 1 = TTFT variant present, 2 = fresh-verifier variant present,
+//      3 = default model with the k = 1 no-queue fast path compiled in (LaunchParams.k1_fast)
 template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, int VAR>
 __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kernel(const LaunchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -155,6 +156,11 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
   // every zero is walked, as in the HIST walk (R24)
   const bool fresh = VAR == 2 && (cfg.flags & CFG_FRESH) != 0;
   const bool walk_all = HIST || fresh;
+  // k = 1 without queueing (Eq. 1 holds at k = 1: most of config 5): C(g) = t_t + (g-1) t_d, so
+  // L_DSI = m t_t + (N-m) t_d, and I = sum ceil(g/2) = (N + #odd segments)/2, where a segment is odd
+  // iff its two ends (consecutive zeros, or N) differ in parity: counted per word with bit
+  // operations instead of walking the runs (block-uniform choice)
+  const bool fast1 = VAR == 3 && !walk_all && cfg.k_eff == 1 && (cfg.flags & CFG_NOQUEUE) != 0;
   const int t_d = cfg.t_d;
 
   // shared memory: TABLE -> T[g] (g = 0..N) then U[q] (q < nq); HIST -> histograms
@@ -243,6 +249,8 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
     uint32_t cin = 1;  // HIST walk: position 32w is a zero (the sentinel for w = 0)
     uint32_t ai = 0, ay = 0;  // summed extra costs (HIST: seg_extra of every g >= 2 segment;
                               // production: seg_long of every segment with g >= k+2)
+    int odd = 0;       // fast1: segments of odd length so far
+    uint32_t lzp = 0;  // fast1: parity of the last zero's position (the sentinel 0 is even)
     for (int w = 0; w < nwords; ++w) {
       uint32_t R;
       if (PATTERN) {
@@ -286,6 +294,17 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
           }
           lastz = z;
         }
+      } else if (fast1) {
+        // bit i is position 32w + i + 1: odd positions at even i
+        const uint32_t Eo = R & 0x55555555u, Ee = R & 0xAAAAAAAAu, NR = ~R;
+        // bits after each odd (even) zero up to and including the next zero of this word
+        const uint32_t Fo = (NR + (Eo << 1)) ^ NR, Fe = (NR + (Ee << 1)) ^ NR;
+        odd += __popc(Fo & Ee) + __popc(Fe & Eo);  // consecutive zeros of different parity
+        if (R) {
+          const uint32_t first_odd = (R & (0u - R) & 0x55555555u) != 0u;  // first zero of the word
+          odd += (int)(first_odd ^ lzp);
+          lzp = ((31 - __clz(R)) & 1) ^ 1u;  // the word's last zero: bit b is odd iff b even
+        }
       } else {
         walk_word<TABLE>(R, rem >= 32 ? 32 : rem, Lk, T, s, run, n2, ai, ay);
       }
@@ -312,8 +331,13 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
     }
 
     const int m = nz + 1;
-    const int iters = m + (int)ai;
+    int iters = m + (int)ai;
     int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)n2 * cfg.s1 + (int64_t)ay;
+    if (fast1) {  // the final segment ends at N
+      odd += (int)(((uint32_t)N & 1u) ^ lzp);
+      iters = (N + odd) >> 1;
+      dsi = (int64_t)m * cfg.t_t + (int64_t)(N - m) * cfg.kd;
+    }
     int64_t si = (int64_t)iters * cfg.si_cost;
     if (ttft) {  // first forwards: SI's first iteration and DSI's first segment
       dsi += D1[g1 ? g1 : N];
@@ -390,6 +414,7 @@ template <bool A, bool B, bool C, bool D>
 int launch_variant(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
   if (p.any_fresh) return launch_variant_t<A, B, C, D, 2>(p, n_units, threads, smem, st);
   if (p.any_ttft) return launch_variant_t<A, B, C, D, 1>(p, n_units, threads, smem, st);
+  if (p.k1_fast) return launch_variant_t<A, B, C, D, 3>(p, n_units, threads, smem, st);
   return launch_variant_t<A, B, C, D, 0>(p, n_units, threads, smem, st);
 }
 

@@ -729,3 +729,36 @@ def test_fresh_verifier_golden_on_the_gpu():
         if key == "dsi":
             assert int(tr["si"][0]) == e["si"]
         sim.close()
+
+
+@pytest.fixture
+def k1_fast_forced(monkeypatch):
+    monkeypatch.setenv("DSI_K1_FAST", "1")
+
+
+def test_k1_fast_path_fuzz_bit_exact(k1_fast_forced):
+    """The k = 1 no-queue fast path (parity of segment ends instead of the run walk, VAR 3), forced
+    on for the fuzz set: every trial bit-exact against the oracle."""
+    cfgs, tick = W.fuzz(160, seed=11, trials=300)
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_PER_TRIAL)
+    check_against_oracle(sim, res, cfgs, tick, hist=False, ctx="k1fast")
+    sim.close()
+
+
+@pytest.mark.parametrize("N", [2, 5, 12, 33])
+def test_k1_fast_path_every_pattern(k1_fast_forced, N):
+    rows = [(1.0, 0.2, 0.5, 1, 7, N, 0, min(1 << (N - 1), 1 << 16)), (1.0, 1.0, 0.5, 1, 1, N, 0, min(1 << (N - 1), 1 << 16))]
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 0.01, flags=D.DSI_F_PER_TRIAL | D.DSI_F_PATTERN)
+    check_against_oracle(sim, res, cfgs, 0.01, hist=False, pattern=True, ctx=f"k1fast N={N}")
+    sim.close()
+
+
+def test_cfg5_subsample_bit_exact():
+    """Config 5 (k = Eq.-1 minimum at SP 7: mostly k = 1 without queueing, so the fast-path variant
+    is chosen automatically), N = 1000: every trial of a 50-config sample bit-exact."""
+    cfgs, tick = W.cfg5(D.dsi_min_lookahead, trials=200)
+    cfgs = cfgs[::202].copy()
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_PER_TRIAL)
+    check_against_oracle(sim, res, cfgs, tick, hist=False, ctx="cfg5")
+    sim.close()
