@@ -296,12 +296,14 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
   int64_t fresh_id = 0;
   int32_t segments = 0, peak_busy = 0, max_queue = 0, forwards = 0;
   int rc = -1;
+  const int ttft = t_t1 != t_t || t_d1 != t_d;
 
   for (;;) { /* one iteration per segment */
     int64_t r = c + 1;          /* next unresolved position */
     int64_t next_done = 0;      /* the next thread whose tokens are settled (the verifier) */
     int32_t busy = 0;
     int64_t b;
+    int64_t n_fin = 0;          /* threads of this segment finished so far */
     int restarted = 0;
     /* fresh variant: the live fresh forward covers [f_lo, f_hi], completes at f_end */
     int f_live = 0, f_done = 0;
@@ -364,6 +366,11 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
         if (e.b != fresh_id) continue; /* superseded */
         f_done = 1;
       } else { /* EV_TARGET_DONE */
+        /* Threads complete in index order: start times strictly increase and every
+           service takes t_t (SURVEY 8(c).2 asks the oracle to assert it).  Only the
+           TTFT variant's slower first forward can break it, in the first segment only. */
+        if (!(ttft && segments == 1) && e.b != n_fin) goto done;
+        n_fin += 1;
         busy -= 1;
         if (q.head < q.tail) { /* FIFO: the head of the queue starts now */
           int64_t nb = q.v[q.head++];

@@ -195,3 +195,40 @@ def expectations_fresh(N, k, t_d, t_t, sp, a):
     out = expectations(N, k, t_d, t_t, sp, a)
     out["dsi"] = sum(h(g, N, a) * C_fresh(g, k, t_d, t_t, sp) for g in range(1, N + 1))
     return out
+
+
+def moments_dp(N, a, cost):
+    """Exact (E[L], E[L^2]) of L = sum_s cost(g_s) by a renewal recursion over the positions of
+    the zeros (written independently of h(g) and of any enumeration): z = 0 is the start; from
+    a zero at z the next zero is at z' <= N-1 with probability a^(z'-z-1) (1-a), and with
+    probability a^(N-1-z) there is none and the final segment ends at N.  Carries
+    P_z = P(zero at z), M1_z = E[partial L; zero at z], M2_z = E[partial L^2; zero at z]."""
+    a = Fraction(a)
+    P = [Fraction(0)] * N
+    M1 = [Fraction(0)] * N
+    M2 = [Fraction(0)] * N
+    P[0] = Fraction(1)
+    e1 = e2 = Fraction(0)
+    for z in range(N):  # P, M1, M2 at z are final once every z0 < z has been pushed
+        if P[z] == 0 and M1[z] == 0:
+            continue
+        for z2 in range(z + 1, N):
+            w = a ** (z2 - z - 1) * (1 - a)
+            c = cost(z2 - z)
+            P[z2] += w * P[z]
+            M1[z2] += w * (M1[z] + c * P[z])
+            M2[z2] += w * (M2[z] + 2 * c * M1[z] + c * c * P[z])
+        w = a ** (N - 1 - z)
+        c = cost(N - z)
+        e1 += w * (M1[z] + c * P[z])
+        e2 += w * (M2[z] + 2 * c * M1[z] + c * c * P[z])
+    return e1, e2
+
+
+def moments_dsi_si(N, k, t_d, t_t, sp, a, fresh=False):
+    """Exact (E, E^2) of L_DSI and L_SI: L_DSI = sum C(g) (or C_fresh), L_SI = (k t_d + t_t)
+    sum ceil(g/(k+1))."""
+    cd = (lambda g: C_fresh(g, k, t_d, t_t, sp)) if fresh else (lambda g: C(g, k, t_d, t_t, sp))
+    si_cost = k * t_d + t_t
+    return {"dsi": moments_dp(N, a, cd),
+            "si": moments_dp(N, a, lambda g: si_cost * (-(-g // (k + 1))))}

@@ -246,7 +246,13 @@ def test_c_abi_example_on_gpu(tmp_path):
         pytest.skip("no CUDA device")
     r = subprocess.run([str(_build_c_example(tmp_path))], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "mean non-SI 50.000000 SI 21.231000 DSI 16.941000 over 1000 trials" in r.stdout, r.stdout
+    # expected means computed by the CPU oracle on the example's config (cfg1, tick 0.01:
+    # t_t 100, t_d 10 ticks, a 0.8, k 5, SP 2, N 50, 1000 trials, seed 2405141050)
+    import oracle as O
+    want = O.means(O.run(O.Config(100, 10, 0.8, 5, 2, 50), 2405141050, 0, 1000, per_trial=False), 0.01)
+    line = (f"mean non-SI {want['mean_nonsi']:.6f} SI {want['mean_si']:.6f} DSI {want['mean_dsi']:.6f} "
+            f"over 1000 trials")
+    assert line in r.stdout, (line, r.stdout)
 
 
 def test_multi_drafter_options_validated_before_device_work():

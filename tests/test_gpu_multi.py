@@ -63,10 +63,52 @@ def check(cfgs, tick, res, dsi, settled, pattern=False, tree=False):
                 assert int(got_d[t]) == lit["dsi"] and list(got_s[t, :m]) == lit["settled"], (i, t)
 
 
+def tree_check(cfgs, tick, dsi, settled, per_cfg, budget=1 << 16, pattern=False):
+    """Per-trial GPU results against the LITERAL thread tree of Alg. 1 (oracle_multi_tree, every
+    thread spawned, terminated and relabelled as P:112-142 says), on up to per_cfg evenly spaced
+    trials of each config; trials whose tree exceeds the thread budget are skipped.  Returns the
+    number of trials checked (the chain simulation is never consulted here)."""
+    off = offsets(cfgs)
+    checked = 0
+    for i, row in enumerate(cfgs):
+        oc = oracle_cfg(row, tick)
+        T = int(row["n_trials"])
+        for t in np.unique(np.linspace(0, T - 1, min(per_cfg, T)).astype(int)):
+            try:
+                lit = O.multi_tree(oc, SEED, int(t), pattern=pattern, max_threads=budget)
+            except OverflowError:
+                continue
+            assert int(dsi[off[i] + t]) == lit["dsi"], (i, int(t), oc)
+            assert [int(x) for x in settled[off[i] + t, :oc.m]] == lit["settled"], (i, int(t), oc)
+            checked += 1
+    return checked
+
+
 def test_fuzz_bit_exact_per_trial():
     cfgs, tick = W.multi_fuzz(60, n_max=70, trials=300)
     res, dsi, settled = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED, per_trial=True)
     check(cfgs, tick, res, dsi, settled)
+    # the same trials against the literal thread tree wherever it fits a 65 536-thread budget
+    assert tree_check(cfgs, tick, dsi, settled, per_cfg=40) >= 1500
+
+
+# Latencies for which the literal thread tree stays small at N = 30..60 (drafters within ~4x of
+# the target: the live tree is the set of model sequences whose summed latency fits in one
+# target forward), m = 2..5, acceptance rates across [0, 1].
+TREE_ROWS = [(1.0, (0.25, 0.5), (0.5, 0.8)), (1.0, (0.3, 0.6), (0.9, 0.9)),
+             (1.0, (0.2, 0.4, 0.6), (0.2, 0.5, 0.7)), (1.0, (0.34,), (0.6,)),
+             (1.0, (0.4, 0.7), (0.3, 0.6)), (1.0, (0.3, 0.3, 0.5, 0.9), (0.5, 0.0, 0.4, 1.0)),
+             (0.9, (0.45, 0.9), (0.95, 0.5)), (1.0, (0.5,), (0.1,))]
+
+
+@pytest.mark.parametrize("N", [30, 45, 60])
+def test_literal_thread_tree_per_trial_at_n_30_to_60(N):
+    """the multi-drafter kernel per trial against the literal thread tree
+    (not the closed-form chain) at N = 30..60, 400 trials per config, ragged tile."""
+    cfgs = W.multi_rows(TREE_ROWS, 1100, N, stream_id=N)
+    res, dsi, settled = D.dsi_multi_simulate(cfgs, tick=0.01, seed=SEED, per_trial=True)
+    assert tree_check(cfgs, 0.01, dsi, settled, per_cfg=400, budget=1 << 20) == 400 * len(TREE_ROWS)
+    assert (res["n_dsi_gt_nonsi"] == 0).all()
 
 
 def test_ragged_tiles_and_large_n():

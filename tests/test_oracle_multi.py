@@ -180,3 +180,18 @@ def test_invalid_inputs_rejected():
         O.multi_chain(O.MultiConfig(10, (1,), (1.5,), 4), SEED, 0)
     with pytest.raises(OverflowError):
         O.multi_tree(O.MultiConfig(100, (1, 2), (0.9, 0.9), 40), SEED, 0, max_threads=10000)
+
+
+@pytest.mark.parametrize("N", [30, 60])
+def test_tree_equals_chain_on_long_stream_trials(N):
+    """The literal thread tree (every thread of Alg. 1) and the verified-chain
+    simulation agree per trial at N = 30 and 60 on Philox-stream trials, for m = 2..5 and
+    drafters slow enough (>= 0.2 t_m) for the tree to stay small."""
+    rows = [(100, (25, 50), (0.5, 0.8)), (100, (20, 40, 60), (0.2, 0.5, 0.7)),
+            (100, (30, 30, 50, 90), (0.5, 0.0, 0.4, 1.0)), (90, (45, 90), (0.95, 0.5)), (100, (50,), (0.1,))]
+    for tt, tds, rates in rows:
+        cfg = O.MultiConfig(tt, tds, rates, N, stream_id=N)
+        for t in range(0, 2000, 13):
+            lit = O.multi_tree(cfg, SEED, t, max_threads=1 << 20)
+            ch = O.multi_chain(cfg, SEED, t)
+            assert (lit["dsi"], lit["settled"]) == (ch["dsi"], ch["settled"]), (cfg, t)
