@@ -45,6 +45,13 @@ extern "C" {
 
 #define DSI_ABI_VERSION 2u
 
+/* every entry point is exported with default visibility (the library hides the rest) */
+#if defined(__GNUC__)
+#define DSI_API __attribute__((visibility("default")))
+#else
+#define DSI_API
+#endif
+
 typedef enum {
   DSI_OK = 0,
   DSI_E_NULL = 1,       /* a required pointer was NULL                                   */
@@ -126,10 +133,11 @@ typedef struct {
   double tick;            /* time quantum in latency units, > 0 (e.g. 0.01 relative, 0.1 ms) */
   uint64_t seed;          /* Philox key                                                     */
   int32_t device;         /* first CUDA device ordinal of this process (e.g. LOCAL_RANK)    */
-  int32_t n_devices;      /* 1..8 devices [device, device+n) driven by this process         */
+  int32_t n_devices;      /* must be 1: one process drives one GPU; several GPUs run one
+                             process each (torchrun), ranks joined by NCCL  */
   int32_t rank, world;    /* multi-process mode: this process is rank of world (world >= 1) */
-  const uint8_t *nccl_id; /* 128-byte ncclUniqueId shared by all ranks; required when the
-                             total device count world*n_devices > 1.  With one device, a
+  const uint8_t *nccl_id; /* 128-byte ncclUniqueId shared by all ranks; required when
+                             world > 1.  With one device, a
                              non-NULL id still routes the reduction through a one-rank NCCL
                              communicator.  Obtain it with dsi_nccl_unique_id on one rank
                              and broadcast it; use a fresh id for every handle (an id serves
@@ -167,7 +175,7 @@ typedef struct dsi_sim dsi_sim; /* opaque handle */
 /* Validate options and configs, convert to ticks, plan shards, allocate device
  * memory, upload the config table, initialise NCCL when world*n_devices > 1
  * (collective: every rank must call it).  On error *out is set to NULL. */
-dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t n_cfg,
+DSI_API dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t n_cfg,
                           dsi_sim **out);
 
 /* Replace the configuration values of an existing handle (same n_cfg, same
@@ -178,32 +186,32 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
  * t_target, t_drafter, SP) are unchanged, else rebuilt; an update that changes the
  * number of groups or units returns DSI_E_RANGE ("create a new handle").  On error
  * the handle keeps its previous configs. */
-dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg);
+DSI_API dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg);
 
 /* Enqueue one full simulation on every device of this process (asynchronous). */
-dsi_status dsi_sim_run(dsi_sim *h);
+DSI_API dsi_status dsi_sim_run(dsi_sim *h);
 
 /* Wait for the run, sum the per-config integer moments across devices and ranks
  * (one NCCL all-reduce), check on the device that every trial was simulated exactly
  * once (DSI_E_DEVICE otherwise, nothing written), copy the moments to the host in
  * chunks and derive FP64 means/std (overlapped).  n must equal n_cfg.  Blocking.
  * Every rank must call it. */
-dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n);
+DSI_API dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n);
 
 /* Per-trial records of trials [first, first+count) of config cfg (needs
  * DSI_F_PER_TRIAL, one device, world == 1).  Any output pointer may be NULL. */
-dsi_status dsi_sim_trials(dsi_sim *h, size_t cfg, uint64_t first, uint64_t count,
+DSI_API dsi_status dsi_sim_trials(dsi_sim *h, size_t cfg, uint64_t first, uint64_t count,
                           int32_t *acc, int32_t *m, int32_t *iters, int32_t *si_ticks,
                           int32_t *dsi_ticks);
 
 /* Histograms of config cfg after reduce (needs DSI_F_HIST).  seg_hist: 64 bins,
  * bin g = segments of length g (bin 63 = length >= 63, bin 0 unused).
  * si_hist: si_bins must be k+1; bin j = SI iterations with j accepted drafts. */
-dsi_status dsi_sim_hist(dsi_sim *h, size_t cfg, int64_t *seg_hist, int64_t *si_hist,
+DSI_API dsi_status dsi_sim_hist(dsi_sim *h, size_t cfg, int64_t *seg_hist, int64_t *si_hist,
                         size_t si_bins);
 
 /* CUDA stream of the i-th device of this handle (cudaStream_t as void*). */
-dsi_status dsi_sim_stream(dsi_sim *h, int32_t device_index, void **stream);
+DSI_API dsi_status dsi_sim_stream(dsi_sim *h, int32_t device_index, void **stream);
 
 /* Environment: DSI_TRACE=1 makes create / update / run / reduce / heatmap print their host-side
  * phases (wall clock, ms) to stderr on return. */
@@ -211,37 +219,37 @@ dsi_status dsi_sim_stream(dsi_sim *h, int32_t device_index, void **stream);
 /* Kernel launches enqueued on this process since the last dsi_sim_run began: its trial
  * kernels, plus the partition check of dsi_sim_reduce and the heatmap kernel of
  * dsi_sim_heatmap when those were called. */
-dsi_status dsi_sim_launches(dsi_sim *h, int32_t *launches);
+DSI_API dsi_status dsi_sim_launches(dsi_sim *h, int32_t *launches);
 
 /* With DSI_F_TIMING: device time (ms) of the trial kernels of the last run on
  * device_index, measured with CUDA events on the launching stream (blocks). */
-dsi_status dsi_sim_kernel_ms(dsi_sim *h, int32_t device_index, float *ms);
+DSI_API dsi_status dsi_sim_kernel_ms(dsi_sim *h, int32_t device_index, float *ms);
 
 /* Host<->device bytes moved per create+run+reduce on this process: the config
  * table and unit prefix uploaded by create (h2d) and the per-config moments (and
  * histograms) read back by reduce (d2h). */
-dsi_status dsi_sim_io_bytes(dsi_sim *h, uint64_t *h2d, uint64_t *d2h);
+DSI_API dsi_status dsi_sim_io_bytes(dsi_sim *h, uint64_t *h2d, uint64_t *d2h);
 
 /* Work units (config, trial tile) of this process: [first, first+count) of total. */
-dsi_status dsi_sim_units(dsi_sim *h, uint64_t *first, uint64_t *count, uint64_t *total);
+DSI_API dsi_status dsi_sim_units(dsi_sim *h, uint64_t *first, uint64_t *count, uint64_t *total);
 
-void dsi_sim_destroy(dsi_sim *h); /* NULL-safe */
+DSI_API void dsi_sim_destroy(dsi_sim *h); /* NULL-safe */
 
-const char *dsi_status_str(dsi_status s);
-const char *dsi_sim_last_error(const dsi_sim *h); /* handle-owned; "" if none */
-const char *dsi_last_create_error(void);          /* thread-local message of the last failed
+DSI_API const char *dsi_status_str(dsi_status s);
+DSI_API const char *dsi_sim_last_error(const dsi_sim *h); /* handle-owned; "" if none */
+DSI_API const char *dsi_last_create_error(void);          /* thread-local message of the last failed
                                                      dsi_sim_create                          */
-uint32_t dsi_abi_version(void);
+DSI_API uint32_t dsi_abi_version(void);
 
 /* 128-byte NCCL unique id for multi-GPU runs (call on one rank, broadcast); one per handle
  * (or per dsi_multi_simulate call). */
-dsi_status dsi_nccl_unique_id(uint8_t id[128]);
+DSI_API dsi_status dsi_nccl_unique_id(uint8_t id[128]);
 
 /* Pure planner helpers of Eq. 1, exact integers.
  * Return -1 on invalid input (ticks < 1, sp < 1, k < 1). */
-int32_t dsi_min_lookahead(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t sp);
-int32_t dsi_required_processors(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k);
-int32_t dsi_eq1_feasible(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k, int32_t sp);
+DSI_API int32_t dsi_min_lookahead(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t sp);
+DSI_API int32_t dsi_required_processors(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k);
+DSI_API int32_t dsi_eq1_feasible(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k, int32_t sp);
 
 /* ---- Heatmap product (Fig. 3 / Fig. 5) ----------------
  * A cell is a maximal run of consecutive configs with equal (t_target, t_drafter,
@@ -267,7 +275,7 @@ typedef struct {
 
 /* Host-only.  cells may be NULL to count: *n_cells receives the number of cells;
  * otherwise at most cap cells are written (DSI_E_RANGE if cap is too small). */
-dsi_status dsi_heatmap(const dsi_config *cfg, const dsi_result *res, size_t n,
+DSI_API dsi_status dsi_heatmap(const dsi_config *cfg, const dsi_result *res, size_t n,
                        dsi_heatmap_cell *cells, size_t cap, size_t *n_cells);
 
 /* On-device form: after dsi_sim_run, sums the moments across devices and
@@ -279,10 +287,10 @@ dsi_status dsi_heatmap(const dsi_config *cfg, const dsi_result *res, size_t n,
  * accept_rate, sp_degree, n_tokens) as given to create/update; the values are bit-identical
  * to dsi_heatmap over dsi_sim_reduce's results.  cells == NULL: *n_cells receives the
  * count (no device work).  DSI_E_RANGE if cap is too small, DSI_E_STATE before a run. */
-dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size_t *n_cells);
+DSI_API dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size_t *n_cells);
 
 /* CSV of cells (SPEC S:450-458 columns; fixed formatting, %.6f; rows in input order). */
-dsi_status dsi_heatmap_csv(const dsi_heatmap_cell *cells, size_t n, const char *path);
+DSI_API dsi_status dsi_heatmap_csv(const dsi_heatmap_cell *cells, size_t n, const char *path);
 
 /* ---- Multi-drafter DSI: Algorithm 1 with m > 2 models ------------------
  * Algorithm 1 as stated: models f_1..f_m, f_m the target, lookahead 1 ("set to 1
@@ -348,27 +356,24 @@ typedef struct {
  * trials follow those of configs < c), either pointer may be NULL.  Validation as
  * dsi_sim_create (DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW when N t_m >= 2^31 ticks or
  * T (N t_m)^2 >= 2^64); the message is in dsi_last_create_error(). */
-dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cfg, size_t n_cfg,
+DSI_API dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cfg, size_t n_cfg,
                               dsi_multi_result *out, int32_t *trial_dsi, int32_t *trial_settled);
 
 /* With DSI_F_TIMING: device time (ms) of the kernel of the last dsi_multi_simulate on this
  * host thread (CUDA events on the launching stream); launches of it in *launches. */
-dsi_status dsi_multi_last_kernel(float *ms, int32_t *launches);
+DSI_API dsi_status dsi_multi_last_kernel(float *ms, int32_t *launches);
 
-/* Test hook: cross-rank sums through a host function instead of NCCL.  While set (fn != NULL),
- * handles and dsi_multi_simulate calls created with world > 1 need no nccl_id and one device per
- * process; every cross-rank sum (moments, histograms, heatmap cells) copies the u64 words to the
- * host, calls fn(buf, n, user) -- which must replace buf by the element-wise sum over all ranks
- * and return 0 -- and copies them back.  It lets several ranks share one GPU (which NCCL refuses),
- * e.g. with a torch.distributed gloo all_reduce.  Process-global; pass NULL to clear. */
-typedef int (*dsi_host_allreduce_fn)(uint64_t *buf, size_t n, void *user);
-dsi_status dsi_set_host_allreduce(dsi_host_allreduce_fn fn, void *user);
+/* Build identity: the SHA-256 (hex) of the sources and flags this library was compiled from
+ * (paper_2405_14105_b200/build.py embeds it), e.g. to prove a test ran a build of HEAD.
+ * Static storage, never NULL. */
+DSI_API const char *dsi_build_id(void);
+
 
 /* Pure sharder (host only, no device): split per-unit costs into `parts`
  * contiguous ranges of near-equal total cost.  cost_units[i] >= 0.
  * bounds must hold parts+1 entries; bounds[0] = 0, bounds[parts] = n.
  * Used by dsi_sim_create for devices x ranks x shards; exported for tests. */
-dsi_status dsi_shard_bounds(const double *cost_units, uint64_t n, int32_t parts,
+DSI_API dsi_status dsi_shard_bounds(const double *cost_units, uint64_t n, int32_t parts,
                             uint64_t *bounds);
 
 #ifdef __cplusplus

@@ -1,22 +1,41 @@
-"""Build libdsi_sim.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+"""Build the simulator library in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+Three builds of the same sources:
+  libdsi_sim.so         the product (no test hooks, no developer knobs)
+  libdsi_sim_test.so    -DDSI_TEST_HOOKS: adds include/dsi_sim_testing.h (host all-reduce hook,
+                        A/B knobs) for the multi-rank-on-one-GPU tests and A/B runs
+  libdsi_sim_mutant.so  -DDSI_TEST_HOOKS -DDSI_MUTANT_CG: every DSI segment cost C(g), g >= 2,
+                        one tick too large -- the mutation test (tests/test_mutation.py) checks
+                        that GPU parity against the oracle FAILS with it
+Each library embeds the SHA-256 of its sources and flags (dsi_build_id()); a build is redone
+whenever the embedded id differs from that of the current sources, so a snapshot shipped to a
+GPU box always runs a build of exactly the tree it carries.  Objects compile in parallel.
+"""
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libdsi_sim.so")
-SOURCES = [os.path.join(CSRC, "dsi_host.cpp"), os.path.join(CSRC, "dsi_heatmap.cpp"),
-           os.path.join(CSRC, "dsi_kernel.cu"), os.path.join(CSRC, "dsi_crn.cu"),
-           os.path.join(CSRC, "dsi_reduce_dev.cu"), os.path.join(CSRC, "dsi_crn2.cu"),
-           os.path.join(CSRC, "dsi_multi.cu"), os.path.join(CSRC, "dsi_seg.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "dsi_device.h"), os.path.join(CSRC, "dsi_common.cuh"),
-                  os.path.join(CSRC, "dsi_crn_common.cuh"),
-                  os.path.join(ROOT, "include", "dsi_sim.h")]
+HOST = ["dsi_validate.cpp", "dsi_plan.cpp", "dsi_collective.cpp", "dsi_runtime.cpp",
+        "dsi_multi_host.cpp", "dsi_heatmap.cpp"]
+DEVICE = ["dsi_kernel.cu", "dsi_crn.cu", "dsi_reduce_dev.cu", "dsi_crn2.cu", "dsi_multi.cu", "dsi_seg.cu"]
+SOURCES = [os.path.join(CSRC, f) for f in HOST + DEVICE]
+HEADERS = [os.path.join(CSRC, f) for f in ("dsi_host.h", "dsi_device.h", "dsi_common.cuh", "dsi_crn_common.cuh")] + \
+          [os.path.join(ROOT, "include", f) for f in ("dsi_sim.h", "dsi_sim_testing.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+VARIANTS = {"product": ("libdsi_sim.so", []),
+            "test": ("libdsi_sim_test.so", ["-DDSI_TEST_HOOKS"]),
+            "mutant": ("libdsi_sim_mutant.so", ["-DDSI_TEST_HOOKS", "-DDSI_MUTANT_CG"])}
+LIB = os.path.join(PKG, VARIANTS["product"][0])
+TEST_LIB = os.path.join(PKG, VARIANTS["test"][0])
+MUTANT_LIB = os.path.join(PKG, VARIANTS["mutant"][0])
+COMMON = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden"]
 
 
 def nvcc() -> str:
@@ -26,28 +45,78 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def command(out: str = LIB, extra=()) -> list:
-    return [nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-shared",
-            "-I" + os.path.join(ROOT, "include"), "-o", out, *SOURCES, "-ldl", *extra]
+def build_id(variant: str = "product") -> str:
+    """SHA-256 over the source and header contents and the variant's flags."""
+    h = hashlib.sha256()
+    for p in SOURCES + HEADERS:
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(COMMON + VARIANTS[variant][1]).encode())
+    return h.hexdigest()
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in DEPS)
+def embedded_id(lib: str):
+    """The id a built library carries (read from its bytes, without loading it)."""
+    try:
+        data = open(lib, "rb").read()
+    except OSError:
+        return None
+    i = data.find(b"DSI_BUILD_ID=")
+    return data[i + 13:i + 77].decode(errors="replace") if i >= 0 else None
 
 
-def build_library(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
-        cmd = command(extra=["-Xptxas", "-v"] if verbose else [])
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("nvcc failed building libdsi_sim.so")
-        if verbose:
-            sys.stderr.write(r.stderr)
+def stale(variant: str = "product") -> bool:
+    lib = os.path.join(PKG, VARIANTS[variant][0])
+    return embedded_id(lib) != build_id(variant)
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed: " + os.path.basename(cmd[-1]))
+    return r.stderr
+
+
+def build_variant(variant: str = "product", force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
+    name, flags = VARIANTS[variant]
+    lib = os.path.join(PKG, name)
+    if not force and not stale(variant):
+        return lib
+    bid = build_id(variant)
+    odir = os.path.join(PKG, "build", variant)
+    os.makedirs(odir, exist_ok=True)
+    extra = ["-Xptxas", "-v"] if verbose else []
+
+    def compile_one(src):
+        obj = os.path.join(odir, os.path.basename(src) + ".o")
+        defs = ["-DDSI_BUILD_ID=\"" + bid + "\""] if src.endswith("dsi_validate.cpp") else []
+        return _run([nvcc(), *COMMON, *flags, *defs, *extra, "-I" + os.path.join(ROOT, "include"), "-c",
+                     "-o", obj, src]), obj
+
+    with ThreadPoolExecutor(max_workers=jobs or min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    if verbose:
+        for log, _ in results:
+            sys.stderr.write(log)
+    tmp = lib + ".tmp"
+    _run([nvcc(), *ARCH, "-shared", "-o", tmp, *[o for _, o in results], "-ldl"])
+    os.replace(tmp, lib)
+    return lib
+
+
+def build_library(force: bool = False, verbose: bool = False, variants=("product", "test", "mutant")) -> str:
+    """Build every variant whose embedded id is not the current one; returns the product path."""
+    with ThreadPoolExecutor(max_workers=len(variants)) as ex:
+        list(ex.map(lambda v: build_variant(v, force=force, verbose=verbose and v == "product",
+                                            jobs=max(2, (os.cpu_count() or 4) // len(variants))), variants))
     return LIB
+
+
+def command(out: str = LIB, extra=()) -> list:
+    """One-shot nvcc command of the product library (profiles/ scripts)."""
+    return [nvcc(), *COMMON, "-shared", "-I" + os.path.join(ROOT, "include"), "-o", out, *SOURCES, "-ldl", *extra]
 
 
 if __name__ == "__main__":

@@ -105,7 +105,10 @@ __device__ __forceinline__ uint2 seg_extra(int g, const SegCtx &s) {
   const uint32_t b = magic_div((uint32_t)g + s.k_eff - 2u, s.m_k_lo, s.m_k_hi);  // ceil((g-1)/k)
   const uint32_t qq = magic_div(b, s.m_sp_lo, s.m_sp_hi);
   const int rr = (int)b - (int)qq * s.sp_eff;
-  const int S = max((int)b * s.kd, rr * s.kd + (int)qq * s.t_t);
+  int S = max((int)b * s.kd, rr * s.kd + (int)qq * s.t_t);
+#ifdef DSI_MUTANT_CG
+  S += 1;  // mutation-test build only (libdsi_sim_mutant.so): C(g) one tick too large
+#endif
   return make_uint2(M - 1u, (uint32_t)S);
 }
 

@@ -1,0 +1,290 @@
+// dsi_plan.cpp -- work plans: the device config table, means-only histogram groups,
+// shared-stream groups/slices/units (and the two-pass record plan), heatmap cells.
+#include "dsi_host.h"
+
+using namespace dsih;
+
+namespace dsih {
+
+// Fill the pinned device-config staging table from h->ticks.
+void fill_dev_cfg(dsi_sim *h) {
+  const bool pattern = h->opt.flags & DSI_F_PATTERN;
+  const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
+  const size_t n = h->n_cfg;
+  // prefix offsets (per-trial records, SI-histogram bins) in two passes over fixed chunks
+  constexpr size_t K = 64;
+  uint64_t rec[K + 1] = {}, sib[K + 1] = {};
+  parallel_for(K, [&](size_t b, size_t e) {
+    for (size_t c = b; c < e; ++c) {
+      uint64_t r = 0, q = 0;  // in registers: the neighbouring chunks' sums share cache lines
+      for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) {
+        r += h->ticks[i].trials;
+        q += (uint64_t)std::min(h->ticks[i].k, h->ticks[i].n) + 1;
+      }
+      rec[c + 1] = r;
+      sib[c + 1] = q;
+    }
+  }, 1);
+  for (size_t c = 0; c < K; ++c) {
+    rec[c + 1] += rec[c];
+    sib[c + 1] += sib[c];
+  }
+  parallel_for(K, [&](size_t b, size_t e) {
+    for (size_t c = b; c < e; ++c) {
+      uint64_t r = rec[c], q = sib[c];
+      for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) {
+        DevCfg &d = h->dev_cfg.p[i];
+        d = make_dev_cfg(h->ticks[i], pattern, fresh);
+        d.rec_off = r;
+        r += h->ticks[i].trials;
+        d.si_hist_off = (uint32_t)q;
+        q += (uint64_t)d.k_eff + 1;
+      }
+    }
+  }, 1);
+}
+
+// Shared-stream plan: group configs by (stream_id, threshold, N, n_trials) -- equal keys
+// draw identical indicators -- ordered lookahead-major inside a group (so the lanes of a
+// warp mostly share k), then cut each group into slices of cfg_per_block configs.
+// Launch-shape limits that follow from the configs (max N, max min(k, N), TTFT present),
+// and the shared-memory bounds they imply.  Called by create and again by update, whose
+// new configs may change them (the kernels size shared memory from these values).
+// Means-only plan: groups of configs with equal (stream_id, threshold, N, n_trials) -- they
+// draw identical indicators -- each with its segment-length histogram; histogram units are
+// (group, tile of tile_trials trials).  cost[u] feeds the sharder.
+dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_units) {
+  const size_t n = h->n_cfg;
+  std::vector<uint32_t> order(n);
+  for (size_t i = 0; i < n; ++i) order[i] = (uint32_t)i;
+  auto key = [&](uint32_t i) {
+    const CfgTicks &t = h->ticks[i];
+    return std::make_tuple(t.stream_id, t.thr, t.n, t.trials);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return key(a) < key(b); });
+  h->seg_groups.clear();
+  h->cfg_group.assign(n, 0u);
+  uint64_t off = 0, trials = 0;
+  for (size_t i = 0; i < n;) {
+    size_t j = i + 1;
+    while (j < n && key(order[j]) == key(order[i])) ++j;
+    const CfgTicks &t = h->ticks[order[i]];
+    dsi::SegGroup g{};
+    g.n_trials = t.trials;
+    g.hist_off = off;
+    g.n_tokens = t.n;
+    g.stream_id = t.stream_id;
+    g.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
+    g.mode = t.thr >= (1ull << 32) ? dsi::MODE_ALL_ACCEPT : (t.thr == 0 ? dsi::MODE_ALL_REJECT : dsi::MODE_STREAM);
+    for (size_t q = i; q < j; ++q) h->cfg_group[order[q]] = (uint32_t)h->seg_groups.size();
+    h->seg_groups.push_back(g);
+    off += (uint64_t)t.n + 1;
+    trials += t.trials;
+    i = j;
+  }
+  h->hist_len = off;
+  h->ttft_cfgs.clear();
+  for (size_t i = 0; i < n; ++i)
+    if (h->ticks[i].t_t1 != h->ticks[i].t_t || h->ticks[i].t_d1 != h->ticks[i].t_d) h->ttft_cfgs.push_back((uint32_t)i);
+  // tiles: multiples of 128 trials, enough units to fill the devices
+  uint64_t r = trials / (128ull * std::max<uint64_t>(1, target_units));
+  r = std::min<uint64_t>(128, std::max<uint64_t>(1, r));
+  h->tile_trials = (uint32_t)(128 * r);
+  h->seg_prefix.assign(h->seg_groups.size() + 1, 0);
+  for (size_t gi = 0; gi < h->seg_groups.size(); ++gi)
+    h->seg_prefix[gi + 1] = h->seg_prefix[gi] + (h->seg_groups[gi].n_trials + h->tile_trials - 1) / h->tile_trials;
+  h->total_units = h->seg_prefix.back();
+  cost.assign(h->total_units, 0.0);
+  for (size_t gi = 0; gi < h->seg_groups.size(); ++gi) {
+    const dsi::SegGroup &g = h->seg_groups[gi];
+    const double a = (double)g.thr / 4294967296.0;
+    for (uint64_t u = h->seg_prefix[gi]; u < h->seg_prefix[gi + 1]; ++u) {
+      const uint64_t t0 = (u - h->seg_prefix[gi]) * h->tile_trials;
+      const double tr = (double)std::min<uint64_t>(h->tile_trials, g.n_trials - t0);
+      cost[u] = tr * (double)g.n_tokens * (g.mode == dsi::MODE_STREAM ? 11.0 + 10.0 * (1.0 - a) : 1.0);
+    }
+  }
+  return DSI_OK;
+}
+
+// Two-pass shared-stream mode (dsi_crn2.cu): records of (group, tile of TH trials), and
+// for every device the tiles its units read (pass 1 writes exactly those).  Requires
+// h->crn_units and the devices' unit ranges.
+dsi_status plan_two_pass(dsi_sim *h) {
+  const int th = h->cfg_per_block;
+  h->two_pass = th == 256 && dsi::crn_eval_smem(h->max_runs, th) <= 76 * 1024;
+  if (knobs().crn_two_pass >= 0) h->two_pass = h->two_pass && knobs().crn_two_pass != 0;
+  if (!h->two_pass) return DSI_OK;
+  try {
+    h->rec_bytes = (uint32_t)dsi::crn_record_bytes(h->max_runs, th);
+    h->group_tile0.assign(h->groups.size() + 1, 0);
+    for (size_t g = 0; g < h->groups.size(); ++g)
+      h->group_tile0[g + 1] = h->group_tile0[g] + (h->groups[g].n_trials + th - 1) / th;
+    h->total_records = h->group_tile0.back();
+    for (auto &d : h->dev) {
+      std::vector<char> seen(h->total_records, 0);
+      d.tiles.clear();
+      for (const auto &rg : d.ranges)
+        for (uint64_t u = rg.first; u < rg.second; ++u) {
+          const dsi::CrnUnit &un = h->crn_units[u];
+          for (uint64_t t = un.t0 / th; t * th < un.t1; ++t) {
+            const uint64_t r = h->group_tile0[un.group] + t;
+            if (!seen[r]) {
+              seen[r] = 1;
+              d.tiles.push_back(dsi::CrnTile{un.group, (uint32_t)t});
+            }
+          }
+        }
+    }
+  } catch (...) {
+    return fail(h, DSI_E_NOMEM, "two-pass plan");
+  }
+  return DSI_OK;
+}
+
+dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
+  const size_t n = h->n_cfg;
+  try {
+    h->perm.resize(n);
+    for (size_t i = 0; i < n; ++i) h->perm[i] = (uint32_t)i;
+    const auto &t = h->ticks;
+    std::stable_sort(h->perm.begin(), h->perm.end(), [&](uint32_t a, uint32_t b) {
+      const CfgTicks &x = t[a], &y = t[b];
+      if (x.stream_id != y.stream_id) return x.stream_id < y.stream_id;
+      if (x.thr != y.thr) return x.thr < y.thr;
+      if (x.n != y.n) return x.n < y.n;
+      if (x.trials != y.trials) return x.trials < y.trials;
+      if (x.k != y.k) return x.k < y.k;
+      if (x.t_t != y.t_t) return x.t_t < y.t_t;
+      if (x.t_d != y.t_d) return x.t_d < y.t_d;
+      return x.sp < y.sp;
+    });
+    h->max_runs = h->max_n / 3 + 2;  // runs of >= 2 accepted drafts in one trial
+    // groups first, then the block shape: configs per block follow the typical group size
+    h->groups.clear();
+    for (size_t i = 0; i < n;) {
+      const CfgTicks &k0 = t[h->perm[i]];
+      size_t j = i + 1;
+      while (j < n) {
+        const CfgTicks &kj = t[h->perm[j]];
+        if (kj.stream_id != k0.stream_id || kj.thr != k0.thr || kj.n != k0.n || kj.trials != k0.trials) break;
+        ++j;
+      }
+      dsi::CrnGroup g{};
+      g.first = (uint32_t)i;
+      g.count = (uint32_t)(j - i);
+      g.n_tokens = k0.n;
+      g.stream_id = k0.stream_id;
+      g.thr = (uint32_t)std::min<uint64_t>(k0.thr, 0xffffffffull);
+      g.mode = k0.thr >= (1ull << 32) ? dsi::MODE_ALL_ACCEPT : (k0.thr == 0 ? dsi::MODE_ALL_REJECT : dsi::MODE_STREAM);
+      g.n_trials = k0.trials;
+      h->groups.push_back(g);
+      i = j;
+    }
+    // one config per thread, one trial per thread per tile; 256-thread blocks halve the
+    // phase-1 (Philox) passes per trial of a group -- worth it when groups are large (>= 256
+    // configs on average) and the shared memory still leaves room for 4 blocks per SM; else
+    // 128 (profiles/r01_ab_crn_th.jsonl: cfg3 30.5 -> 26.0 ms; forced on cfg2/cfg4/cfg5, whose
+    // groups hold 3 / 140 / 100 configs, 1.8-1.9x slower; 2 or 4 configs per thread were
+    // slower too, profiles/r01_ab_crn*.jsonl)
+    const bool big_groups = n >= 256 * h->groups.size();
+    int th = (big_groups && dsi::crn_kernel_smem(h->max_n, 256, 256, h->max_runs) <= 48 * 1024) ? 256 : kCrnThreads;
+    if (knobs().crn_threads == 128 || knobs().crn_threads == 256) th = knobs().crn_threads;
+    h->cfg_per_block = th;
+    h->block_threads = th;
+    // units: (group, slice of cfg_per_block configs, range of trials); trials are split
+    // until there are enough blocks to fill every SM of every device a few times.  With
+    // 128-thread blocks a group's configs are first cut into maximal runs of "sums-only"
+    // configs (k_eff = 1 and no queueing: every run of >= 2 accepted drafts is long and
+    // the corrections are linear in per-trial sums, no run list needed) and the others;
+    // sums-only units go first and run a kernel variant without run lists in shared memory
+    // (so many more blocks fit an SM; large N, e.g. config 5, gains most).
+    const bool split_sums = th == kCrnThreads && knobs().crn_sums_split != 0;
+    auto sums_only = [&](uint32_t pos) {
+      const CfgTicks &c = t[h->perm[pos]];
+      return split_sums && std::min(c.k, c.n) == 1 && config_noqueue(c);
+    };
+    struct Slice {
+      uint32_t group, begin, count;
+      bool sums;
+    };
+    std::vector<Slice> slices_v;
+    for (uint32_t gi = 0; gi < h->groups.size(); ++gi) {
+      const dsi::CrnGroup &g = h->groups[gi];
+      for (uint32_t b = g.first; b < g.first + g.count;) {
+        const bool kind = sums_only(b);
+        uint32_t e = b + 1;
+        while (e < g.first + g.count && e - b < (uint32_t)th && sums_only(e) == kind) ++e;
+        slices_v.push_back(Slice{gi, b, e - b, kind});
+        b = e;
+      }
+    }
+    const size_t slices = slices_v.size();
+    const int total_devices = h->opt.world * h->opt.n_devices;
+    const uint64_t target = 148ull * 4 * 4 * (uint64_t)total_devices;
+    const uint64_t split = std::max<uint64_t>(1, (target + slices - 1) / slices);
+    h->crn_units.clear();
+    cost.clear();
+    h->n_sums_units = 0;
+    h->max_runs_normal = 1;
+    for (int pass = 0; pass < 2; ++pass) {  // sums-only units first
+      for (const Slice &sl : slices_v) {
+        if (sl.sums != (pass == 0)) continue;
+        const dsi::CrnGroup &g = h->groups[sl.group];
+        const uint64_t tiles = (g.n_trials + th - 1) / th;
+        const uint64_t nchunks = std::min<uint64_t>(split, tiles);
+        for (uint64_t c = 0; c < nchunks; ++c) {
+          dsi::CrnUnit u{};
+          u.group = sl.group;
+          u.begin = sl.begin;
+          u.count = sl.count;
+          u.kind = sl.sums ? 1u : 0u;
+          u.t0 = (tiles * c / nchunks) * th;
+          u.t1 = std::min<uint64_t>((tiles * (c + 1) / nchunks) * th, g.n_trials);
+          h->crn_units.push_back(u);
+          if (sl.sums) ++h->n_sums_units;
+          else {  // stored runs have L > the slice's smallest k_eff: each takes >= kmin + 2 positions
+            int32_t kmin = 1 << 30;
+            for (uint32_t q = sl.begin; q < sl.begin + sl.count; ++q)
+              kmin = std::min(kmin, std::min(t[h->perm[q]].k, t[h->perm[q]].n));
+            h->max_runs_normal = std::max<int32_t>(h->max_runs_normal, (g.n_tokens - 1) / (kmin + 2) + 1);
+          }
+          // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
+          cost.push_back((double)(u.t1 - u.t0) * ((double)g.n_tokens * 12.0 + (double)sl.count * 25.0));
+        }
+      }
+    }
+  } catch (...) {
+    return fail(h, DSI_E_NOMEM, "shared-stream plan");
+  }
+  h->total_units = h->crn_units.size();
+  return DSI_OK;
+}
+
+// Heatmap cells: maximal runs of consecutive configs with equal (t_target, t_drafter, a, SP, N).
+void plan_heat_cells(dsi_sim *h) {
+  h->heat_cells.clear();
+  const auto &t = h->ticks;
+  for (size_t i = 0; i < h->n_cfg;) {
+    size_t j = i + 1;
+    while (j < h->n_cfg && t[j].ut == t[i].ut && t[j].ud == t[i].ud && t[j].a == t[i].a && t[j].sp == t[i].sp &&
+           t[j].n == t[i].n)
+      ++j;
+    h->heat_cells.push_back(dsi::HeatCell{(uint64_t)i, (uint32_t)(j - i), 0u});
+    i = j;
+  }
+}
+
+// Means-only, one device per process: every part's config range starts at a cell, so each
+// part's cells can be evaluated from its own moments (no all-reduce of the moments).
+bool cells_aligned(const dsi_sim *h) {
+  if (!h->means_only || h->opt.n_devices != 1 || h->cfg_bounds.empty()) return false;
+  size_t ci = 0;
+  for (const uint64_t b : h->cfg_bounds) {
+    while (ci < h->heat_cells.size() && h->heat_cells[ci].first < b) ++ci;
+    if (b < h->n_cfg && (ci == h->heat_cells.size() || h->heat_cells[ci].first != b)) return false;
+  }
+  return true;
+}
+
+}  // namespace dsih

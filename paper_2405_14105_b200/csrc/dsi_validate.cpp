@@ -1,0 +1,318 @@
+// dsi_validate.cpp -- validation and tick conversion of the configs (R15), the device
+// config rows, launch limits and the Eq. 1 planner helpers.
+#include "dsi_host.h"
+
+using namespace dsih;
+
+namespace dsih {
+
+thread_local std::string g_create_error;
+
+// ceil(2^32 / d) split into low word and bit 32 (d >= 1).
+void magic(uint32_t d, uint32_t &lo, uint32_t &hi) {
+  // divisors below 2^16 (every lookahead, SP and N the planner sees in practice) come from a
+  // table built once: make_dev_cfg needs three per config, millions of times per update
+  static const std::vector<uint64_t> table = [] {
+    std::vector<uint64_t> t(1u << 16, 0);
+    for (uint32_t x = 1; x < (1u << 16); ++x) t[x] = ((1ull << 32) + x - 1) / x;
+    return t;
+  }();
+  const uint64_t m = d < (1u << 16) ? table[d] : ((1ull << 32) + d - 1) / d;
+  lo = (uint32_t)m;
+  hi = (uint32_t)(m >> 32);
+}
+
+dsi_status to_ticks(double x, double tick, int64_t *out) {
+  if (!std::isfinite(x) || x <= 0.0) return DSI_E_RANGE;
+  const double r = x / tick;
+  if (!(r < 9.0e18)) return DSI_E_OVERFLOW;
+  const int64_t t = std::llround(r);
+  if (t < 1 || std::fabs(r - (double)t) > 1e-9 * std::fabs(r)) return DSI_E_TICK;
+  *out = t;
+  return DSI_OK;
+}
+
+dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTicks &o,
+                   std::string &msg) {
+  char buf[256];
+  auto bad = [&](dsi_status s, const char *what) {
+    std::snprintf(buf, sizeof buf, "config %zu: %s", i, what);
+    msg = buf;
+    return s;
+  };
+  if (!(c.accept_rate >= 0.0 && c.accept_rate <= 1.0))
+    return bad(DSI_E_RANGE, "accept_rate must be in [0, 1]");
+  if (c.lookahead < 1) return bad(DSI_E_RANGE, "lookahead must be >= 1");
+  if (c.sp_degree < 1) return bad(DSI_E_RANGE, "sp_degree must be >= 1");
+  if (c.n_tokens < 1 || c.n_tokens > kMaxTokens)
+    return bad(DSI_E_RANGE, "n_tokens must be in [1, 32768]");
+  if (c.n_trials < 1 || c.n_trials > kMaxTrials)
+    return bad(DSI_E_RANGE, "n_trials must be in [1, 2^32]");
+  if ((opt.flags & DSI_F_PATTERN) && c.n_tokens > 33)
+    return bad(DSI_E_RANGE, "DSI_F_PATTERN needs n_tokens <= 33");
+  dsi_status s = to_ticks(c.t_target, opt.tick, &o.t_t);
+  if (s != DSI_OK) return bad(s, "t_target is not a positive whole number of ticks");
+  s = to_ticks(c.t_drafter, opt.tick, &o.t_d);
+  if (s != DSI_OK) return bad(s, "t_drafter is not a positive whole number of ticks");
+  if (o.t_d > o.t_t) return bad(DSI_E_RANGE, "t_drafter > t_target violates Assumption 2 (P:187-189)");
+  o.t_t1 = o.t_t;
+  o.t_d1 = o.t_d;
+  if (c.ttft_target != 0.0) {
+    s = to_ticks(c.ttft_target, opt.tick, &o.t_t1);
+    if (s != DSI_OK) return bad(s, "ttft_target is not 0 or a positive whole number of ticks");
+  }
+  if (c.ttft_drafter != 0.0) {
+    s = to_ticks(c.ttft_drafter, opt.tick, &o.t_d1);
+    if (s != DSI_OK) return bad(s, "ttft_drafter is not 0 or a positive whole number of ticks");
+  }
+  if (o.t_d1 > o.t_t1) return bad(DSI_E_RANGE, "ttft_drafter > ttft_target violates Assumption 2");
+  if ((opt.flags & DSI_F_SHARED_STREAMS) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d))
+    return bad(DSI_E_RANGE, "DSI_F_SHARED_STREAMS does not support the TTFT variant");
+  if ((opt.flags & DSI_F_FRESH_VERIFIER) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d))
+    return bad(DSI_E_RANGE, "DSI_F_FRESH_VERIFIER does not support the TTFT variant");
+  // every per-trial latency is <= N (k t_d + t_t) plus the first-forward surcharges
+  // (kernel overflow bound)
+  const unsigned __int128 kd = (unsigned __int128)c.lookahead * (uint64_t)o.t_d;
+  const unsigned __int128 bound = (unsigned __int128)c.n_tokens * (kd + (uint64_t)o.t_t) +
+                                  (uint64_t)std::max<int64_t>(0, o.t_t1 - o.t_t) +
+                                  (uint64_t)std::max<int64_t>(0, o.t_d1 - o.t_d);
+  if (bound >= ((unsigned __int128)1 << 31))
+    return bad(DSI_E_OVERFLOW, "N*(k*t_drafter + t_target) must stay below 2^31 ticks");
+  if ((unsigned __int128)c.n_trials * bound * bound >= ((unsigned __int128)1 << 64))
+    return bad(DSI_E_OVERFLOW, "n_trials * bound^2 must stay below 2^64");
+  o.kd = (int64_t)kd;
+  if ((opt.flags & DSI_F_STRICT_EQ1) && ceil_div(o.t_t, o.kd) > c.sp_degree)
+    return bad(DSI_E_STRICT_EQ1, "Eq. 1 violated: ceil(t_t/(k t_d)) > SP");
+  o.a = c.accept_rate;
+  o.ut = c.t_target;
+  o.ud = c.t_drafter;
+  o.eq1 = dsi_eq1_feasible(o.t_t, o.t_d, c.lookahead, c.sp_degree);
+  o.min_k = dsi_min_lookahead(o.t_t, o.t_d, c.sp_degree);
+  o.thr = (uint64_t)(c.accept_rate * 4294967296.0);  // exact: a * 2^32, then floor
+  o.k = c.lookahead;
+  o.sp = c.sp_degree;
+  o.n = c.n_tokens;
+  o.stream_id = c.stream_id;
+  o.trials = c.n_trials;
+  return DSI_OK;
+}
+
+// S(b) = b k t_d for every b: Eq. 1 holds at min(SP, N), or SP >= N (no thread ever waits).
+bool config_noqueue(const CfgTicks &t) {
+  const int32_t sp_eff = std::min(t.sp, t.n);
+  return (t.t_t <= (int64_t)sp_eff * t.kd) || sp_eff >= t.n;
+}
+
+DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
+  DevCfg d{};
+  uint32_t mode = dsi::MODE_STREAM;
+  if (!pattern) {
+    if (t.thr >= (1ull << 32)) mode = dsi::MODE_ALL_ACCEPT;
+    else if (t.thr == 0) mode = dsi::MODE_ALL_REJECT;
+  }
+  const int32_t k_eff = std::min(t.k, t.n);
+  const int32_t sp_eff = std::min(t.sp, t.n);
+  const bool noqueue = config_noqueue(t);
+  d.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
+  const bool ttft = t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+  // fresh-verifier variant: with k t_d <= t_t a fresh forward never finishes sooner than
+  // the regular thread (R24), so only k t_d > t_t configs take its cost table
+  const bool fresh_cfg = fresh && t.kd > t.t_t;
+  d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u) | (ttft ? dsi::CFG_TTFT : 0u) |
+            (fresh_cfg ? dsi::CFG_FRESH : 0u);
+  d.t_d = (int32_t)t.t_d;
+  d.k = t.k;
+  if (t.eq1 == 1) d.flags |= dsi::CFG_EQ1;
+  d.nonsi = (int32_t)(t.t_t1 + (int64_t)(t.n - 1) * t.t_t);
+  d.e_si = (int32_t)((t.t_d1 - t.t_d) + (t.t_t1 - t.t_t));
+  d.t_t1 = (int32_t)t.t_t1;
+  d.ttft_shift = (int32_t)(t.t_d1 - t.t_d);
+  d.n_tokens = t.n;
+  d.k_eff = k_eff;
+  d.sp_eff = sp_eff;
+  d.t_t = (int32_t)t.t_t;
+  d.kd = (int32_t)t.kd;
+  d.si_cost = (int32_t)(t.kd + t.t_t);
+  // S(1) = max(k t_d, (1 mod SP) k t_d + floor(1/SP) t_t): k t_d, or max(k t_d, t_t) if SP = 1
+  d.s1 = (int32_t)(t.sp >= 2 ? t.kd : std::max(t.kd, t.t_t));
+  d.stream_id = t.stream_id;
+  uint32_t hi;
+  magic((uint32_t)k_eff + 1u, d.m_si, hi);  // k_eff + 1 >= 2: hi == 0
+  magic((uint32_t)k_eff, d.m_k_lo, d.m_k_hi);
+  magic((uint32_t)sp_eff, d.m_sp_lo, d.m_sp_hi);
+  d.n_trials = t.trials;
+  return d;
+}
+
+// Relative cost of one trial-token: Philox (~10 instr) + compare (~1) + segment walk
+// (~10 instr per rejection, expected (1-a) per token), SURVEY 8(d).4.
+double unit_cost(const CfgTicks &t, uint64_t trials) {
+  return (double)trials * (double)t.n * (11.0 + 10.0 * (1.0 - t.a));
+}
+
+// Validate every config into ticks; on failure h->err names the first bad config.
+// Validate every config into `out`; on failure h->err names the first bad config.  With
+// `prev` (dsi_sim_update), also checks what an update must keep: n_trials, and with
+// DSI_F_HIST min(k, N) (the histogram layout).
+dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n, std::vector<CfgTicks> &out,
+                        const std::vector<CfgTicks> *prev) {
+  std::mutex mu;
+  size_t bad = n;
+  dsi_status bad_s = DSI_OK;
+  std::string bad_msg;
+  const bool hist = h->opt.flags & DSI_F_HIST;
+  parallel_for(n, [&](size_t b, size_t e) {
+    for (size_t i = b; i < e; ++i) {
+      std::string msg;
+      dsi_status s = convert(h->opt, cfg[i], i, out[i], msg);
+      if (s == DSI_OK && prev) {
+        const CfgTicks &o = (*prev)[i], &t = out[i];
+        if (t.trials != o.trials || (hist && std::min(t.k, t.n) != std::min(o.k, o.n))) {
+          s = DSI_E_RANGE;
+          msg = "config " + std::to_string(i) + ": n_trials (and, with DSI_F_HIST, min(k, N)) must not change";
+        }
+      }
+      if (s != DSI_OK) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (i < bad) {
+          bad = i;
+          bad_s = s;
+          bad_msg = msg;
+        }
+        return;
+      }
+    }
+  });
+  if (bad < n) return fail(h, bad_s, bad_msg);
+  return DSI_OK;
+}
+
+dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks) {
+  struct Lim {
+    int32_t max_n = 1, max_keff = 1;
+    bool ttft = false, fresh = false;
+    double work = 0.0, work_k1 = 0.0;  // trial-tokens in all configs / in k = 1 configs without queueing
+  } lim;
+  std::mutex mu;
+  const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
+  parallel_for(ticks.size(), [&](size_t b, size_t e) {
+    Lim l;
+    for (size_t i = b; i < e; ++i) {
+      const CfgTicks &t = ticks[i];
+      l.max_n = std::max(l.max_n, t.n);
+      l.max_keff = std::max(l.max_keff, std::min(t.k, t.n));
+      l.ttft = l.ttft || t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+      l.fresh = l.fresh || (fresh && t.kd > t.t_t);
+      const double w = (double)t.trials * (double)t.n;
+      l.work += w;
+      if (std::min(t.k, t.n) == 1 && config_noqueue(t)) l.work_k1 += w;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    lim.max_n = std::max(lim.max_n, l.max_n);
+    lim.max_keff = std::max(lim.max_keff, l.max_keff);
+    lim.ttft = lim.ttft || l.ttft;
+    lim.fresh = lim.fresh || l.fresh;
+    lim.work += l.work;
+    lim.work_k1 += l.work_k1;
+  });
+  if (lim.ttft && lim.max_n > 4096) return fail(h, DSI_E_RANGE, "the TTFT variant supports n_tokens <= 4096");
+  if (dsi::trial_kernel_smem(lim.max_n, lim.max_keff, h->opt.flags & DSI_F_HIST, lim.ttft) > 200 * 1024)
+    return fail(h, DSI_E_RANGE, "DSI_F_HIST needs (64 + k + 1) * 4 bytes of shared memory <= 200 KiB");
+  if (h->shared && lim.max_n > kCrnMaxN)
+    return fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS supports n_tokens <= " + std::to_string(kCrnMaxN));
+  h->max_n = lim.max_n;
+  h->max_keff = lim.max_keff;
+  h->any_ttft = lim.ttft;
+  h->any_fresh = lim.fresh;
+  // the k = 1 fast path (dsi_kernel.cu, VAR 3) pays for its extra code only when such configs carry
+  // a good share of the work (measured: config 5, 86% of its configs, -14%; config 3, 0.5%, +2% if on)
+  h->k1_fast = !lim.ttft && !lim.fresh && lim.work_k1 >= 0.25 * lim.work;
+  if (knobs().k1_fast >= 0) h->k1_fast = !lim.ttft && !lim.fresh && knobs().k1_fast != 0;
+  return DSI_OK;
+}
+
+// The shared-stream plan orders configs by these fields (plan_shared): an update that
+// keeps all of them keeps the plan.
+bool same_plan_keys(const std::vector<CfgTicks> &a, const std::vector<CfgTicks> &b) {
+  std::atomic<bool> same{true};
+  parallel_for(a.size(), [&](size_t lo, size_t hi) {
+    for (size_t i = lo; i < hi && same.load(std::memory_order_relaxed); ++i) {
+      const CfgTicks &x = a[i], &y = b[i];
+      if (x.stream_id != y.stream_id || x.thr != y.thr || x.n != y.n || x.trials != y.trials || x.k != y.k ||
+          x.t_t != y.t_t || x.t_d != y.t_d || x.sp != y.sp)
+        same = false;
+    }
+  });
+  return same;
+}
+
+}  // namespace dsih
+
+extern "C" {
+
+uint32_t dsi_abi_version(void) { return DSI_ABI_VERSION; }
+
+const char *dsi_status_str(dsi_status s) {
+  switch (s) {
+    case DSI_OK: return "DSI_OK";
+    case DSI_E_NULL: return "DSI_E_NULL: required pointer was NULL";
+    case DSI_E_RANGE: return "DSI_E_RANGE: argument out of range";
+    case DSI_E_TICK: return "DSI_E_TICK: latency is not a whole number of ticks";
+    case DSI_E_OVERFLOW: return "DSI_E_OVERFLOW: tick sums would overflow";
+    case DSI_E_STRICT_EQ1: return "DSI_E_STRICT_EQ1: Eq. 1 violated under DSI_F_STRICT_EQ1";
+    case DSI_E_DEVICE: return "DSI_E_DEVICE: CUDA error or missing sm_100 device";
+    case DSI_E_COMM: return "DSI_E_COMM: NCCL error";
+    case DSI_E_STATE: return "DSI_E_STATE: call order violated";
+    case DSI_E_NOMEM: return "DSI_E_NOMEM: allocation failed";
+  }
+  return "unknown dsi_status";
+}
+
+const char *dsi_sim_last_error(const dsi_sim *h) { return h ? h->err.c_str() : ""; }
+const char *dsi_last_create_error(void) { return g_create_error.c_str(); }
+
+int32_t dsi_eq1_feasible(int64_t t_t, int64_t t_d, int32_t k, int32_t sp) {
+  if (t_t < 1 || t_d < 1 || k < 1 || sp < 1) return -1;
+  return ceil_div(t_t, (int64_t)k * t_d) <= sp ? 1 : 0;
+}
+
+int32_t dsi_min_lookahead(int64_t t_t, int64_t t_d, int32_t sp) {
+  if (t_t < 1 || t_d < 1 || sp < 1) return -1;
+  // smallest k with ceil(t_t/(k t_d)) <= sp  <=>  k t_d sp >= t_t
+  const int64_t k = ceil_div(t_t, t_d * (int64_t)sp);
+  return (int32_t)std::max<int64_t>(1, k);
+}
+
+int32_t dsi_required_processors(int64_t t_t, int64_t t_d, int32_t k) {
+  if (t_t < 1 || t_d < 1 || k < 1) return -1;
+  return (int32_t)(1 + ceil_div(t_t, (int64_t)k * t_d));
+}
+
+dsi_status dsi_shard_bounds(const double *cost, uint64_t n, int32_t parts, uint64_t *bounds) {
+  if (!bounds || (!cost && n)) return DSI_E_NULL;
+  if (parts < 1) return DSI_E_RANGE;
+  double total = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (!(cost[i] >= 0.0)) return DSI_E_RANGE;
+    total += cost[i];
+  }
+  bounds[0] = 0;
+  uint64_t i = 0;
+  double run = 0.0;
+  for (int32_t j = 1; j < parts; ++j) {
+    const double target = total * (double)j / (double)parts;
+    // advance while taking unit i keeps the prefix closer to the target
+    while (i < n && run + 0.5 * cost[i] <= target) run += cost[i++];
+    bounds[j] = i;
+  }
+  bounds[parts] = n;
+  return DSI_OK;
+}
+
+}  // extern "C"
+
+// Build identity (build.py passes -DDSI_BUILD_ID=<sha256 of the sources and flags>).
+#ifndef DSI_BUILD_ID
+#define DSI_BUILD_ID "unknown"
+#endif
+extern "C" const char *dsi_build_id(void) { return "DSI_BUILD_ID=" DSI_BUILD_ID + 13; }

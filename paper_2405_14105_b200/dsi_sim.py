@@ -14,8 +14,13 @@ import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libdsi_sim.so")
-# developer A/B runs only: load an alternative in-tree build of the same library
-LIB_PATH = os.environ.get("DSI_SIM_LIB", LIB_PATH)
+# Builds of the same sources (paper_2405_14105_b200/build.py): the product, and two test builds
+# that add include/dsi_sim_testing.h (the host all-reduce hook, A/B knobs) -- the second with a
+# deliberately wrong C(g) for the mutation test.  The product is what every call uses unless a
+# test selects another build with use_library() (or DSI_SIM_LIB=test|mutant|<path> for a whole
+# process, e.g. an A/B run).
+VARIANT_PATHS = {"product": LIB_PATH, "test": os.path.join(_PKG, "libdsi_sim_test.so"),
+                 "mutant": os.path.join(_PKG, "libdsi_sim_mutant.so")}
 
 DSI_ABI_VERSION = 2
 DSI_OK, DSI_E_NULL, DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW, DSI_E_STRICT_EQ1, DSI_E_DEVICE, \
@@ -66,10 +71,10 @@ class dsi_options(ctypes.Structure):
                 ("block_threads", ctypes.c_int32), ("stream", ctypes.c_void_p)]
 
 
-def _load():
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
-    lib = ctypes.CDLL(LIB_PATH)
+def _load(path: str):
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
     P, V = ctypes.POINTER, ctypes.c_void_p
     u64, i32, i64, sz = ctypes.c_uint64, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
     sigs = {
@@ -99,25 +104,77 @@ def _load():
         "dsi_heatmap_csv": ([V, sz, ctypes.c_char_p], ctypes.c_int),
         "dsi_multi_simulate": ([P(dsi_options), V, sz, V, V, V], ctypes.c_int),
         "dsi_multi_last_kernel": ([P(ctypes.c_float), P(i32)], ctypes.c_int),
-        "dsi_set_host_allreduce": ([V, V], ctypes.c_int),
+        "dsi_build_id": ([], ctypes.c_char_p),
     }
-    for name, (args, res) in sigs.items():
-        if "DSI_SIM_LIB" in os.environ and not hasattr(lib, name):
-            continue  # an older build under A/B test may lack newer entry points
+    testing = {"dsi_set_host_allreduce": ([V, V], ctypes.c_int),
+               "dsi_test_set_knob": ([ctypes.c_char_p, i32], ctypes.c_int)}
+    for name, (args, res) in list(sigs.items()) + list(testing.items()):
+        if name in testing and not hasattr(lib, name):
+            continue  # the product build has no test hooks
         f = getattr(lib, name)
         f.argtypes = args
         f.restype = res
     return lib
 
 
-lib = _load()
+_libs = {}
+
+
+def load_library(variant: str = "product"):
+    """The ctypes handle of one build ("product", "test", "mutant" or a path), loaded once."""
+    path = VARIANT_PATHS.get(variant, variant)
+    if path not in _libs:
+        _libs[path] = _load(path)
+    return _libs[path]
+
+
+lib = load_library(os.environ.get("DSI_SIM_LIB", "product"))
+
+
+class use_library:
+    """Context manager: calls made inside use the given build (handles keep the build they were
+    created with).  Tests use it for the test build's hooks and for the mutation test."""
+
+    def __init__(self, variant: str):
+        self.variant = variant
+
+    def __enter__(self):
+        global lib
+        self._prev = lib
+        lib = load_library(self.variant)
+        return lib
+
+    def __exit__(self, *exc):
+        global lib
+        lib = self._prev
+
+
+def select_library(variant: str) -> None:
+    """Use another build for the rest of the process (multi-rank test runs on one GPU)."""
+    global lib
+    lib = load_library(variant)
+
+
+class _Handle(ctypes.c_void_p):
+    """A dsi_sim* that remembers the library build it belongs to."""
+    _lib = None
+
+
+def _L(h):
+    return h._lib if isinstance(h, _Handle) and h._lib is not None else lib
+
+
+def dsi_build_id() -> str:
+    """SHA-256 of the sources the loaded product library was built from (dsi_build_id)."""
+    return lib.dsi_build_id().decode()
 EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce", "dsi_sim_trials", "dsi_sim_hist",
             "dsi_sim_stream", "dsi_sim_launches", "dsi_sim_kernel_ms", "dsi_sim_units", "dsi_sim_io_bytes",
             "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
             "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
             "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
             "dsi_heatmap_csv", "dsi_sim_heatmap", "dsi_multi_simulate", "dsi_multi_last_kernel",
-            "dsi_set_host_allreduce")
+            "dsi_build_id")
+TEST_EXPORTED = ("dsi_set_host_allreduce", "dsi_test_set_knob")  # include/dsi_sim_testing.h
 
 
 class DsiError(RuntimeError):
@@ -131,8 +188,19 @@ def _check(status: int, handle=None, create: bool = False):
         if create:
             msg = lib.dsi_last_create_error().decode()
         else:
-            msg = lib.dsi_sim_last_error(handle).decode() if handle else ""
+            msg = _L(handle).dsi_sim_last_error(handle).decode() if handle else ""
         raise DsiError(status, msg)
+
+
+def _testing():
+    if not hasattr(lib, "dsi_test_set_knob"):
+        raise RuntimeError("test hooks exist only in the test build: wrap the call in use_library('test')")
+    return lib
+
+
+def dsi_test_set_knob(name: str, value: int) -> None:
+    """Test build only (include/dsi_sim_testing.h): a launch-planner A/B knob."""
+    _check(_testing().dsi_test_set_knob(name.encode(), int(value)))
 
 
 # ----------------------------------------------------------------------------- same names as the C ABI
@@ -224,7 +292,7 @@ def dsi_set_host_allreduce(fn) -> None:
     global _host_allreduce_ref
     if fn is None:
         _host_allreduce_ref = None
-        _check(lib.dsi_set_host_allreduce(None, None))
+        _check(_testing().dsi_set_host_allreduce(None, None))
         return
 
     def cb(buf, n, _user):
@@ -235,7 +303,7 @@ def dsi_set_host_allreduce(fn) -> None:
             return 1
 
     _host_allreduce_ref = HOST_ALLREDUCE_FN(cb)
-    _check(lib.dsi_set_host_allreduce(ctypes.cast(_host_allreduce_ref, ctypes.c_void_p), None))
+    _check(_testing().dsi_set_host_allreduce(ctypes.cast(_host_allreduce_ref, ctypes.c_void_p), None))
 
 
 def dsi_multi_last_kernel() -> tuple:
@@ -255,41 +323,42 @@ def dsi_sim_create(configs: np.ndarray, *, tick: float, seed: int, flags: int = 
     opt = dsi_options(DSI_ABI_VERSION, flags, tick, seed, device, n_devices, rank, world,
                       ctypes.addressof(idbuf) if idbuf is not None else None, n_shards,
                       block_threads, stream)
-    h = ctypes.c_void_p()
+    h = _Handle()
     _check(lib.dsi_sim_create(ctypes.byref(opt), configs.ctypes.data, configs.size, ctypes.byref(h)),
            create=True)
+    h._lib = lib
     return h
 
 
 def dsi_sim_update(h, configs: np.ndarray) -> None:
     configs = np.ascontiguousarray(configs, dtype=CONFIG_DTYPE)
-    _check(lib.dsi_sim_update(h, configs.ctypes.data, configs.size), h)
+    _check(_L(h).dsi_sim_update(h, configs.ctypes.data, configs.size), h)
 
 
 def dsi_sim_run(h) -> None:
-    _check(lib.dsi_sim_run(h), h)
+    _check(_L(h).dsi_sim_run(h), h)
 
 
 def dsi_sim_reduce(h, n: int, out: np.ndarray | None = None) -> np.ndarray:
     if out is None:
         out = np.zeros(n, RESULT_DTYPE)
-    _check(lib.dsi_sim_reduce(h, out.ctypes.data, n), h)
+    _check(_L(h).dsi_sim_reduce(h, out.ctypes.data, n), h)
     return out
 
 
 def dsi_sim_heatmap(h, out: np.ndarray | None = None) -> np.ndarray:
     """On-device heatmap product after a run (every rank must call it)."""
     n = ctypes.c_size_t()
-    _check(lib.dsi_sim_heatmap(h, None, 0, ctypes.byref(n)), h)
+    _check(_L(h).dsi_sim_heatmap(h, None, 0, ctypes.byref(n)), h)
     if out is None or out.size != n.value:
         out = np.zeros(n.value, HEATMAP_DTYPE)
-    _check(lib.dsi_sim_heatmap(h, out.ctypes.data, out.size, ctypes.byref(n)), h)
+    _check(_L(h).dsi_sim_heatmap(h, out.ctypes.data, out.size, ctypes.byref(n)), h)
     return out
 
 
 def dsi_sim_trials(h, cfg: int, first: int, count: int) -> dict:
     arrs = {k: np.zeros(count, np.int32) for k in ("acc", "m", "iters", "si", "dsi")}
-    _check(lib.dsi_sim_trials(h, cfg, first, count, *[arrs[k].ctypes.data for k in
+    _check(_L(h).dsi_sim_trials(h, cfg, first, count, *[arrs[k].ctypes.data for k in
                                                       ("acc", "m", "iters", "si", "dsi")]), h)
     return arrs
 
@@ -297,43 +366,43 @@ def dsi_sim_trials(h, cfg: int, first: int, count: int) -> dict:
 def dsi_sim_hist(h, cfg: int, k: int) -> tuple:
     seg = np.zeros(64, np.int64)
     si = np.zeros(k + 1, np.int64)
-    _check(lib.dsi_sim_hist(h, cfg, seg.ctypes.data, si.ctypes.data, k + 1), h)
+    _check(_L(h).dsi_sim_hist(h, cfg, seg.ctypes.data, si.ctypes.data, k + 1), h)
     return seg, si
 
 
 def dsi_sim_stream(h, device_index: int = 0) -> int:
     s = ctypes.c_void_p()
-    _check(lib.dsi_sim_stream(h, device_index, ctypes.byref(s)), h)
+    _check(_L(h).dsi_sim_stream(h, device_index, ctypes.byref(s)), h)
     return s.value or 0
 
 
 def dsi_sim_launches(h) -> int:
     n = ctypes.c_int32()
-    _check(lib.dsi_sim_launches(h, ctypes.byref(n)), h)
+    _check(_L(h).dsi_sim_launches(h, ctypes.byref(n)), h)
     return n.value
 
 
 def dsi_sim_kernel_ms(h, device_index: int = 0) -> float:
     ms = ctypes.c_float()
-    _check(lib.dsi_sim_kernel_ms(h, device_index, ctypes.byref(ms)), h)
+    _check(_L(h).dsi_sim_kernel_ms(h, device_index, ctypes.byref(ms)), h)
     return ms.value
 
 
 def dsi_sim_units(h) -> tuple:
     a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
-    _check(lib.dsi_sim_units(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), h)
+    _check(_L(h).dsi_sim_units(h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)), h)
     return a.value, b.value, c.value
 
 
 def dsi_sim_io_bytes(h) -> tuple:
     a, b = ctypes.c_uint64(), ctypes.c_uint64()
-    _check(lib.dsi_sim_io_bytes(h, ctypes.byref(a), ctypes.byref(b)), h)
+    _check(_L(h).dsi_sim_io_bytes(h, ctypes.byref(a), ctypes.byref(b)), h)
     return a.value, b.value
 
 
 def dsi_sim_destroy(h) -> None:
     if h:
-        lib.dsi_sim_destroy(h)
+        _L(h).dsi_sim_destroy(h)
 
 
 class Simulator:

@@ -15,13 +15,13 @@ def pytest_configure(config):
 
 
 def pytest_sessionstart(session):
-    """Build libdsi_sim.so and the oracle in-tree if they are missing or older than their sources
-    (a fresh checkout on a GPU box), before the test modules import the binding.  A no-op when
+    """Build the libraries (product, test, mutant) and the oracle in-tree unless each already
+    embeds the SHA-256 of the current sources (dsi_build_id), before the test modules import the
+    binding -- so the tests always run a build of the tree they came with.  A no-op when
     __graft_entry__.build() already ran; a failed build is left to the tests to report."""
     try:
         from paper_2405_14105_b200 import build as B
-        if B.stale():
-            B.build_library()
+        B.build_library()
         import oracle
         oracle.build()
     except Exception as e:  # noqa: BLE001

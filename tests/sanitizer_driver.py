@@ -38,11 +38,12 @@ for flags in (0, FRESH):
     with D.Simulator(long_n, tick=0.01, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
 # the k = 1 no-queue fast-path variant of the trial kernel (VAR 3), forced on
-os.environ["DSI_K1_FAST"] = "1"
-for flags in (0, D.DSI_F_PER_TRIAL):
-    with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
-        sim.run().reduce()
-del os.environ["DSI_K1_FAST"]
+with D.use_library("test"):
+    D.dsi_test_set_knob("k1_fast", 1)
+    for flags in (0, D.DSI_F_PER_TRIAL):
+        with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
+            sim.run().reduce()
+    D.dsi_test_set_knob("k1_fast", -1)
 # means-only mode (dsi_seg.cu): histogram and evaluation passes, smem above 48 KB at N 8192
 for flags in (D.DSI_F_MEANS_ONLY, D.DSI_F_MEANS_ONLY | FRESH):
     with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:

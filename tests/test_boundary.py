@@ -34,6 +34,22 @@ def test_every_header_symbol_is_exported_and_bound():
                                       "dsi_last_create_error", "dsi_abi_version"), n
 
 
+def test_test_hooks_only_in_the_test_builds():
+    """include/dsi_sim_testing.h exists in libdsi_sim_test.so / _mutant.so only; the product
+    exports none of it.  Every build embeds the SHA-256 of the current sources (build.py)."""
+    from paper_2405_14105_b200 import build as B
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "dsi_sim_testing.h")).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(dsi_[a-z_0-9]+)\s*\(", src)))
+    assert names == sorted(D.TEST_EXPORTED)
+    prod, test = D.load_library("product"), D.load_library("test")
+    for n in names:
+        assert not hasattr(prod, n), n
+        assert hasattr(test, n), n
+    for variant in ("product", "test", "mutant"):
+        assert not B.stale(variant), variant
+    assert D.dsi_build_id() == B.build_id("product")
+
+
 def test_abi_version_and_status_strings():
     assert D.lib.dsi_abi_version() == D.DSI_ABI_VERSION
     for s in range(10):
@@ -104,7 +120,7 @@ def test_create_validation_errors(over, status):
 
 def test_create_option_errors():
     cfgs = _one()
-    bad = [dict(tick=0.0), dict(tick=-1.0), dict(flags=0x200), dict(n_devices=0), dict(n_devices=9),
+    bad = [dict(tick=0.0), dict(tick=-1.0), dict(flags=0x200), dict(n_devices=0), dict(n_devices=9), dict(n_devices=2),
            dict(world=2, rank=2), dict(world=0), dict(block_threads=48), dict(block_threads=256),
            dict(n_shards=2, n_devices=2), dict(flags=D.DSI_F_SHARED_STREAMS | D.DSI_F_PER_TRIAL),
            dict(flags=D.DSI_F_SHARED_STREAMS | D.DSI_F_HIST),

@@ -732,8 +732,15 @@ def test_fresh_verifier_golden_on_the_gpu():
 
 
 @pytest.fixture
-def k1_fast_forced(monkeypatch):
-    monkeypatch.setenv("DSI_K1_FAST", "1")
+def k1_fast_forced():
+    """The test build with the planner's k1_fast knob on (include/dsi_sim_testing.h); its kernels
+    are compiled from the same sources as the product's."""
+    with D.use_library("test"):
+        D.dsi_test_set_knob("k1_fast", 1)
+        try:
+            yield
+        finally:
+            D.dsi_test_set_knob("k1_fast", -1)
 
 
 def test_k1_fast_path_fuzz_bit_exact(k1_fast_forced):
