@@ -89,7 +89,10 @@ typedef enum {
                                  extra server, on the committed prefix plus the drafts done by
                                  tau (at most k).  Identical to the default when k t_d <= t_t;
                                  otherwise L_DSI <= N t_t on every trial (Thm 1).
-                                 Not with SHARED_STREAMS or TTFT configs.                       */
+                                 Every mode (per-config, SHARED_STREAMS, MEANS_ONLY, heatmap)
+                                 gives the same integers under it.  Not with TTFT configs.
+                                 DESIGN.md 2.1: the reading the paper's theorems and figures
+                                 require when k t_d > t_t; the bench and CLI products use it. */
 
 #define DSI_F_MEANS_ONLY 0x80u /* means only ("aggregate H[g]"): per group of
                                  configs drawing identical indicators (as SHARED_STREAMS), one

@@ -131,6 +131,24 @@ __device__ __forceinline__ uint32_t fresh_saving(int g, const SegCtx &s, int t_d
   return (uint32_t)max(0, s.kd - v);
 }
 
+// floor(x / d) for 0 <= x < 2^31 and a divisor d with magic (m, sh) from the host
+// (Granlund-Montgomery: m = floor(2^32 (2^sh - d) / d) + 1, sh = ceil(log2 d)); the sum
+// umulhi(x, m) + x < 2^32 because x < 2^31.
+__device__ __forceinline__ uint32_t divu31(uint32_t x, uint32_t m, int sh) {
+  return (__umulhi(x, m) + x) >> sh;
+}
+
+// Fresh-verifier saving (as fresh_saving) of a segment of L = g - 1 >= 1 accepted drafts, from
+// per-config constants only (no integer division): b = ceil(L/k), j = L - (b-1) k,
+// saving = k t_d - min(k t_d, t_t ceil(j t_d / t_t)).  Only for k t_d > t_t (CFG_FRESH).
+__device__ __forceinline__ int fresh_saving_L(int L, int k_eff, uint32_t m_k_lo, uint32_t m_k_hi, int kd, int t_t,
+                                              int t_d, uint32_t m_tt, int sh_tt) {
+  const uint32_t b = magic_div((uint32_t)(L + k_eff - 1), m_k_lo, m_k_hi);  // ceil(L / k)
+  const int j = L - ((int)b - 1) * k_eff;
+  const int v = t_t * (int)divu31((uint32_t)(j * t_d + t_t - 1), m_tt, sh_tt);
+  return kd - min(kd, v);
+}
+
 // Bits i of x such that bits i-n+1 .. i are all ones (runs of at least n ones),
 // by log-doubling: y_s marks runs >= s, then y_s & (y_s << (n - s)) for s <= n < 2s.
 __device__ __forceinline__ uint32_t runs_at_least(uint32_t x, int n) {

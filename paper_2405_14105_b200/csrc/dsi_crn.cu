@@ -68,11 +68,12 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   sp += (size_t)CRN_THREADS * sizeof(uint4);
   uint16_t *runs = reinterpret_cast<uint16_t *>(sp);  // runs[i * CRN_THREADS + slot]
 
-  __shared__ int s_kmin, s_nfast;
+  __shared__ int s_kmin, s_nfast, s_fresh;
   if (threadIdx.x < 5) s_bsum[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) {
     s_kmin = 1 << 30;
     s_nfast = 0;
+    s_fresh = 0;
   }
   __syncthreads();
   if (mode == MODE_STREAM)
@@ -80,7 +81,10 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   for (int j = threadIdx.x; j < CPT * CRN_THREADS; j += CRN_THREADS) {
     const CfgLite l = load_cfglite(P.cfg, P.perm, un, j, N);
     cl[j] = l;
-    if (j < (int)un.count) atomicMin(&s_kmin, l.k_eff);
+    if (j < (int)un.count) {
+      atomicMin(&s_kmin, l.k_eff);
+      if (l.fresh) s_fresh = 1;
+    }
   }
   __syncthreads();
   // a run of L accepted drafts is long for a config iff L > k_eff: runs of at most the
@@ -89,12 +93,16 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   // every stored run, and their corrections are linear in per-trial sums over the runs:
   //   ai = sum floor(L/(k+1)),  ay = sum (S(ceil(L/k)) - S(1)) = kd sum ceil(L/k) - nr S(1)
   const int kmin = s_kmin;
+  // fresh-verifier configs (k t_d > t_t) correct every segment with g >= 2: a block holding one
+  // stores every run of L >= 2 (runs of L = 1 are counted as n2 - nr)
+  const bool any_fresh = s_fresh != 0;
+  const int store_min = any_fresh ? 1 : kmin;
   for (int j = threadIdx.x; j < (int)un.count; j += CRN_THREADS)
     if (cl[j].noqueue && cl[j].k_eff == kmin) atomicAdd(&s_nfast, 1);
   __syncthreads();
   // the per-trial sums cost two divisions per stored run in phase 1: worth it only when
   // enough of the block's configs use them
-  const bool sums = s_nfast * 8 >= (int)un.count;
+  const bool sums = !any_fresh && s_nfast * 8 >= (int)un.count;
   const uint32_t mk_lo = (uint32_t)((0x100000000ull + (unsigned)kmin - 1) / (unsigned)kmin);
   const uint32_t mk_hi = kmin == 1 ? 1u : 0u;  // ceil(2^32 / kmin) = lo + hi 2^32
   const uint32_t mk1 = (uint32_t)((0x100000000ull + (unsigned)kmin) / (unsigned)(kmin + 1));
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
           const uint32_t below = Rw & ((1u << zb) - 1u);
           const int prev = below ? base + 31 - __clz(below) : lastz;
           const int L = base + zb - prev - 1;  // accepted drafts in this segment
-          if (L > kmin) {
+          if (L > store_min) {
             if (!SUMS) myruns[nr * CRN_THREADS] = (uint16_t)L;
             ++nr;
             maxL = max(maxL, L);
@@ -174,7 +182,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
         run = nv - 1 - (31 - __clz(Rw));
       }
       n2 += run >= 1;  // the final segment (the trailing run, then position N)
-      if (run > kmin) {
+      if (run > store_min) {
         if (!SUMS) myruns[nr * CRN_THREADS] = (uint16_t)run;
         ++nr;
         maxL = max(maxL, run);
@@ -205,7 +213,8 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
         const int m = (int)v.x, n2 = (int)v.y, maxL = (int)v.z;
         int dsi = m * l.t_t + n2 * l.s1;
         int si = m * l.si_cost;
-        if (maxL > l.k_eff) {  // some run is long for this config: corrections
+        // corrections: a run long for this config, or (fresh variant) any segment with g >= 2
+        if (maxL > l.k_eff || (!SUMS && l.fresh && n2 > 0)) {
           const int nr = (int)(v.w & 0x3ffu);
           int ai = 0, ay = 0;
           if (SUMS || (sums && l.noqueue && l.k_eff == kmin)) {  // every stored run, S linear in b
@@ -215,14 +224,17 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
             for (int r = 0; r < nr; ++r) {  // the stored runs, in trial order
               const int L = runs[r * CRN_THREADS + s];
               if (L > l.k_eff) long_run(L, l, ai, ay);
+              if (l.fresh) ay -= fresh_saving_lite(L, l);
             }
+            if (l.fresh) ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
           }
           p_ai += (unsigned)ai;
           p_ai2 += (unsigned)(ai * ai);
           p_mai += (unsigned)(m * ai);
-          c_ay[0] += (unsigned)ay;
-          c_ay2[0] += (unsigned long long)ay * (unsigned)ay;
-          c_ydl[0] += (unsigned long long)ay * (unsigned)dsi;
+          // ay may be negative (fresh savings): signed products, wrapped into the u64 sums
+          c_ay[0] += (unsigned long long)(long long)ay;
+          c_ay2[0] += (unsigned long long)((long long)ay * ay);
+          c_ydl[0] += (unsigned long long)((long long)ay * dsi);
           dsi += ay;
           si += ai * l.si_cost;
         }

@@ -209,35 +209,47 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
       const int m = (int)v.x, n2 = (int)v.y, maxL = (int)v.z;
       int dsi = m * l.t_t + n2 * l.s1;
       int si = m * l.si_cost;
-      if (maxL > l.k_eff) {  // some run is long for this config: corrections
+      // corrections: some run is long for this config, or (fresh-verifier variant) some
+      // segment has g >= 2 -- every one of them saves time (R24)
+      if (maxL > l.k_eff || (l.fresh && n2 > 0)) {
         const int nr = (int)(v.w & 0x3ffu);
         int ai = 0, ay = 0;
         if (fast) {  // k = 1: ai = sum floor(L/2), ay = k t_d sum L - nr S(1)
           ai = (int)(v.w >> 21);
           ay = (int)((v.w >> 10) & 0x7ffu) * l.kd - nr * l.s1;
         } else if (warp_noqueue) {  // S(b) = b k t_d: ay = k t_d sum ceil(L/k) - n S(1)
-          int sb = 0, cnt = 0;
+          int sb = 0, cnt = 0, sv = 0;
           for (int r = 0; r < nr; ++r) {  // runs in decreasing order: stop at the first short one
             const int L = runs[r * TH + s];
-            if (L <= l.k_eff) break;
-            ai += (int)magic_div((uint32_t)L, l.m_si, 0u);
-            sb += (int)magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
-            ++cnt;
+            if (L <= l.k_eff) {
+              if (!l.fresh) break;  // (fresh: every stored run L >= 2 saves)
+            } else {
+              ai += (int)magic_div((uint32_t)L, l.m_si, 0u);
+              sb += (int)magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
+              ++cnt;
+            }
+            if (l.fresh) sv += fresh_saving_lite(L, l);
           }
-          ay = sb * l.kd - cnt * l.s1;
+          ay = sb * l.kd - cnt * l.s1 - sv;
         } else {
           for (int r = 0; r < nr; ++r) {
             const int L = runs[r * TH + s];
-            if (L <= l.k_eff) break;
-            long_run(L, l, ai, ay);
+            if (L <= l.k_eff) {
+              if (!l.fresh) break;
+            } else {
+              long_run(L, l, ai, ay);
+            }
+            if (l.fresh) ay -= fresh_saving_lite(L, l);
           }
         }
+        if (l.fresh) ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
         p_ai += (unsigned)ai;
         p_ai2 += (unsigned)(ai * ai);
         p_mai += (unsigned)(m * ai);
-        c_ay += (unsigned)ay;
-        c_ay2 += (unsigned long long)ay * (unsigned)ay;
-        c_ydl += (unsigned long long)ay * (unsigned)dsi;
+        // ay may be negative (fresh savings): signed products, wrapped into the u64 sums
+        c_ay += (unsigned long long)(long long)ay;
+        c_ay2 += (unsigned long long)((long long)ay * ay);
+        c_ydl += (unsigned long long)((long long)ay * dsi);
         dsi += ay;
         si += ai * l.si_cost;
         if (decltype(gts_long_only)::value) p_gts += (uint32_t)(si - dsi) >> 31;

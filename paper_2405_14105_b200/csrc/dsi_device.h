@@ -45,7 +45,8 @@ struct alignas(16) DevCfg {
   int32_t ttft_shift;    // t_d1 - t_d: first-segment drafts are late by this (TTFT variant)
   int32_t t_d;           // drafter latency, ticks (fresh-verifier variant)
   int32_t k;             // the lookahead as given (heatmap argmin reports it)
-  int32_t reserved[2];
+  uint32_t m_tt;         // floor(x / t_t) = (umulhi(x, m_tt) + x) >> sh_tt for x < 2^31
+  int32_t sh_tt;         //   (Granlund-Montgomery; fresh-verifier savings, dsi_common.cuh)
 };
 static_assert(sizeof(DevCfg) == 112, "DevCfg layout");
 

@@ -17,8 +17,8 @@
 //        I = m + sum_long x(g),  L_DSI = m t_t + n2 S(1) + sum_long y(g),
 //      with n2 = popc(zeros preceded by an accepted draft, E = R & ~(R << 1 | carry))
 //      and only the "long" segments (runs of >= k+1 accepted drafts) walked, found by
-//      a log-doubling run detector (walk_word).  HIST and the fresh-verifier variant
-//      walk every zero instead.
+//      a log-doubling run detector (walk_word).  The fresh-verifier variant walks every
+//      segment with g >= 2 (Lk = 1); HIST walks every zero.
 //   3. Integer moments are reduced with warp shuffles and added to the
 //      per-config accumulators with 64-bit integer atomics (exact, order-free).
 //
@@ -71,8 +71,18 @@ __device__ __forceinline__ void seg_hist(int g, int seg_start, const SegCtx &s, 
 // base+i, nv valid bits, bits >= nv are zero).  Segments with g >= 2 end at a zero
 // whose predecessor is a one (mask E) and each costs (0, S(1)) unless its run of
 // ones is long (L = g-1 >= Lk = k+1); long segments add T[g] = seg_long(g).
-template <bool TABLE>
-__device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint2 *T, const SegCtx &s,
+// FRESH (the fresh-verifier variant, k t_d > t_t, Lk = 1): every segment with g >= 2 is walked
+// and its cost is lowered by the fresh forwards' saving (the table already holds it).
+template <bool TABLE, bool FRESH>
+__device__ __forceinline__ uint2 long_cost(int g, const uint2 *T, const SegCtx &s, int t_d) {
+  if (TABLE) return T[g];
+  uint2 e = seg_long(g, s);
+  if (FRESH) e.y -= fresh_saving(g, s, t_d);
+  return e;
+}
+
+template <bool TABLE, bool FRESH>
+__device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint2 *T, const SegCtx &s, int t_d,
                                           int &run, int &n2, uint32_t &ai, uint32_t &ay) {
   if (R == 0) {
     run += nv;  // the run of accepted drafts continues through the word
@@ -82,7 +92,7 @@ __device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint
   n2 += __popc(E);
   const int z0 = __ffs(R) - 1;  // the first zero closes the run carried in
   if (run + z0 >= Lk) {
-    const uint2 e = TABLE ? T[run + z0 + 1] : seg_long(run + z0 + 1, s);
+    const uint2 e = long_cost<TABLE, FRESH>(run + z0 + 1, T, s, t_d);
     ai += e.x;
     ay += e.y;
   }
@@ -95,7 +105,7 @@ __device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint
       const int zb = 31 - __clz(El);
       El ^= 1u << zb;
       const int g = zb - (31 - __clz(R & ((1u << zb) - 1u)));
-      const uint2 e = TABLE ? T[g] : seg_long(g, s);
+      const uint2 e = long_cost<TABLE, FRESH>(g, T, s, t_d);
       ai += e.x;
       ay += e.y;
     }
@@ -149,13 +159,14 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
   s.t_t = cfg.t_t;
   s.n_tokens = N;
   s.s1 = cfg.s1;
-  const int Lk = cfg.k_eff + 1;  // a run of >= k+1 accepted drafts makes a long segment
   const uint32_t nthr = 0u - cfg.thr;  // carry of u + nthr <=> u >= thr (thr >= 1 in stream mode)
   const bool stream = !PATTERN && mode == MODE_STREAM;
-  // fresh-verifier variant (k t_d > t_t): every segment's cost differs from C(g), so
-  // every zero is walked, as in the HIST walk (R24)
+  // fresh-verifier variant (k t_d > t_t, R24): every segment with g >= 2 costs
+  // C_fresh(g) != C(g), so the production walk visits all of them (Lk = 1, "long" = g >= 2)
+  // with the saving folded into the table
   const bool fresh = VAR == 2 && (cfg.flags & CFG_FRESH) != 0;
-  const bool walk_all = HIST || fresh;
+  const bool walk_all = HIST;
+  const int Lk = fresh ? 1 : cfg.k_eff + 1;  // a run of >= Lk accepted drafts is walked
   // k = 1 without queueing (Eq. 1 holds at k = 1: most of config 5): C(g) = t_t + (g-1) t_d, so
   // L_DSI = m t_t + (N-m) t_d, and I = sum ceil(g/2) = (N + #odd segments)/2, where a segment is odd
   // iff its two ends (consecutive zeros, or N) differ in parity: counted per word with bit
@@ -172,12 +183,8 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
     for (int g = threadIdx.x; g <= N; g += blockDim.x) {
       uint2 e = make_uint2(0u, 0u);
       if (g >= 2) {
-        if (HIST || fresh) {
-          e = seg_extra(g, s);
-          if (fresh) e.y -= fresh_saving(g, s, t_d);
-        } else {
-          e = seg_long(g, s);
-        }
+        e = HIST ? seg_extra(g, s) : seg_long(g, s);
+        if (fresh) e.y -= fresh_saving(g, s, t_d);  // may wrap: sums are read as int32
       }
       T[g] = e;
     }
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
       nz += __popc(R);
       if (ttft && g1 == 0 && R) g1 = 32 * w + __ffs(R);
       if (walk_all) {
-        // test mode (HIST) and the fresh-verifier variant: walk every zero
+        // test mode (HIST): walk every zero
         uint32_t Z = R;
         while (Z) {
           const int z = base + __ffs(Z) - 1;
@@ -305,8 +312,10 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
           odd += (int)(first_odd ^ lzp);
           lzp = ((31 - __clz(R)) & 1) ^ 1u;  // the word's last zero: bit b is odd iff b even
         }
+      } else if (VAR == 2 && fresh) {
+        walk_word<TABLE, true>(R, rem >= 32 ? 32 : rem, Lk, T, s, t_d, run, n2, ai, ay);
       } else {
-        walk_word<TABLE>(R, rem >= 32 ? 32 : rem, Lk, T, s, run, n2, ai, ay);
+        walk_word<TABLE, false>(R, rem >= 32 ? 32 : rem, Lk, T, s, t_d, run, n2, ai, ay);
       }
       if (HIST) cin = R >> 31;
     }
@@ -324,7 +333,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
       gl = run + 1;  // the final segment: the trailing run of ones, then position N
       n2 += gl >= 2;
       if (run >= Lk) {
-        const uint2 e = TABLE ? T[gl] : seg_long(gl, s);
+        const uint2 e = (VAR == 2 && fresh) ? long_cost<TABLE, true>(gl, T, s, t_d) : long_cost<TABLE, false>(gl, T, s, t_d);
         ai += e.x;
         ay += e.y;
       }
@@ -332,7 +341,9 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
 
     const int m = nz + 1;
     int iters = m + (int)ai;
-    int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)n2 * cfg.s1 + (int64_t)ay;
+    // ay is a sum of signed 32-bit terms (fresh savings may exceed S(b) - S(1)) with
+    // |sum| <= N k t_d < 2^31 (create's overflow bound): read it as int32
+    int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)n2 * cfg.s1 + (int64_t)(int32_t)ay;
     if (fast1) {  // the final segment ends at N
       odd += (int)(((uint32_t)N & 1u) ^ lzp);
       iters = (N + odd) >> 1;

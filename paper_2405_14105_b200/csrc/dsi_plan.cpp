@@ -245,8 +245,12 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
           if (sl.sums) ++h->n_sums_units;
           else {  // stored runs have L > the slice's smallest k_eff: each takes >= kmin + 2 positions
             int32_t kmin = 1 << 30;
-            for (uint32_t q = sl.begin; q < sl.begin + sl.count; ++q)
-              kmin = std::min(kmin, std::min(t[h->perm[q]].k, t[h->perm[q]].n));
+            // (a fresh-verifier config, k t_d > t_t, makes the block store every run of L >= 2)
+            const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
+            for (uint32_t q = sl.begin; q < sl.begin + sl.count; ++q) {
+              const CfgTicks &c = t[h->perm[q]];
+              kmin = std::min(kmin, (fresh && c.kd > c.t_t) ? 1 : std::min(c.k, c.n));
+            }
             h->max_runs_normal = std::max<int32_t>(h->max_runs_normal, (g.n_tokens - 1) / (kmin + 2) + 1);
           }
           // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)

@@ -167,9 +167,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (per_trial && total_devices > 1)
     return fail(nullptr, DSI_E_RANGE, "DSI_F_PER_TRIAL needs a single device and world == 1");
   const bool shared = opt->flags & DSI_F_SHARED_STREAMS;
-  if (shared && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_FRESH_VERIFIER)))
-    return fail(nullptr, DSI_E_RANGE,
-                "DSI_F_SHARED_STREAMS excludes PER_TRIAL, HIST, PATTERN and FRESH_VERIFIER");
+  if (shared && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN)))
+    return fail(nullptr, DSI_E_RANGE, "DSI_F_SHARED_STREAMS excludes PER_TRIAL, HIST and PATTERN");
 
   const bool means_only = opt->flags & DSI_F_MEANS_ONLY;
   if (means_only && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_SHARED_STREAMS)))

@@ -141,6 +141,14 @@ DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
   magic((uint32_t)k_eff, d.m_k_lo, d.m_k_hi);
   magic((uint32_t)sp_eff, d.m_sp_lo, d.m_sp_hi);
   d.n_trials = t.trials;
+  // floor(x / t_t) for x < 2^31: l = ceil(log2 t_t), m' = floor(2^32 (2^l - t_t) / t_t) + 1
+  {
+    const uint64_t tt = (uint64_t)t.t_t;
+    int l = 0;
+    while ((1ull << l) < tt) ++l;
+    d.m_tt = (uint32_t)((((1ull << 32) * ((1ull << l) - tt)) / tt + 1) & 0xffffffffull);
+    d.sh_tt = l;
+  }
   return d;
 }
 

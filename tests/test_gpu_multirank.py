@@ -35,7 +35,8 @@ def _cases():
     return [("default", fz, ftick, 0), ("root", fz, ftick, D.DSI_F_REDUCE_TO_ROOT),
             ("hist", fz, ftick, D.DSI_F_HIST), ("shared", c3, tick3, D.DSI_F_SHARED_STREAMS),
             ("means", c3, tick3, D.DSI_F_MEANS_ONLY), ("means_ttft", ttft, ttick, D.DSI_F_MEANS_ONLY),
-            ("fresh", fz, ftick, D.DSI_F_FRESH_VERIFIER)]
+            ("fresh", fz, ftick, D.DSI_F_FRESH_VERIFIER),
+            ("shared_fresh", c3, tick3, D.DSI_F_SHARED_STREAMS | D.DSI_F_FRESH_VERIFIER)]
 
 
 CURRENT = {"case": None}

@@ -218,11 +218,13 @@ MOMENTS = ("sum_dsi_ticks", "sum_si_ticks", "sumsq_dsi_ticks", "sumsq_si_ticks",
            "sum_si_iters", "sum_accepts", "n_dsi_gt_nonsi", "n_dsi_gt_si", "trials", "mean_dsi", "std_dsi")
 
 
+@pytest.mark.parametrize("fresh", [False, True], ids=["R1", "R24"])
 @pytest.mark.parametrize("name", ["fuzz", "cfg2", "cfg3", "cfg4", "cfg5", "ragged"])
-def test_shared_streams_bit_identical_to_default(name):
+def test_shared_streams_bit_identical_to_default(name, fresh):
     """DSI_F_SHARED_STREAMS: one Philox pass per trial per group of configs
-    with equal (stream, threshold, N, T); every per-config moment must equal the default
-    mode's bit for bit (and so the oracle's, which the default mode matches)."""
+    with equal (stream, threshold, N, T); every per-config moment must equal the per-config
+    mode's bit for bit (and so the oracle's, which that mode matches), under the literal
+    reading (R1) and the fresh-verifier reading (R24) alike."""
     if name == "fuzz":
         cfgs, tick = W.fuzz(300, seed=31, trials=400)
     elif name == "cfg2":
@@ -239,18 +241,25 @@ def test_shared_streams_bit_identical_to_default(name):
                 for sp in (1, 7)]
         cfgs = W.rows(rows)
         tick = 0.01
-    _, base = run_sim(cfgs, tick, flags=0)
-    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    base_flags = FRESH if fresh else 0
+    _, base = run_sim(cfgs, tick, flags=base_flags)
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS | base_flags)
     for f in MOMENTS:
-        assert np.array_equal(res[f], base[f]), (name, f)
+        assert np.array_equal(res[f], base[f]), (name, fresh, f)
+    if fresh and name in ("cfg3", "cfg4"):  # the variant acts on these (k t_d > t_t) ...
+        _, lit = run_sim(cfgs, tick, flags=0)
+        assert not np.array_equal(res["sum_dsi_ticks"], lit["sum_dsi_ticks"])
+        assert (res["n_dsi_gt_nonsi"] == 0).all()  # ... and restores Thm 1
     sim.close()
 
 
-def test_shared_streams_against_oracle_sample():
+@pytest.mark.parametrize("fresh", [False, True], ids=["R1", "R24"])
+def test_shared_streams_against_oracle_sample(fresh):
     cfgs, tick = W.cfg3(trials=700, k_max=200, cells=slice(5, 10100, 1001))
-    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    flags = D.DSI_F_SHARED_STREAMS | (FRESH if fresh else 0)
+    sim, res = run_sim(cfgs, tick, flags=flags)
     for i in range(0, cfgs.size, 97):
-        assert_result_equals_oracle(res[i], oracle_sums(cfgs[i], tick, SEED), tick, ctx=f"crn {i}")
+        assert_result_equals_oracle(res[i], oracle_sums(cfgs[i], tick, SEED, fresh=fresh), tick, ctx=f"crn {i}")
     sim.close()
 
 
@@ -406,6 +415,26 @@ def test_update_matches_a_fresh_handle(flags, dn, ttft):
     if flags & D.DSI_F_PER_TRIAL:
         for i in range(0, new.size, 9):
             assert_result_equals_oracle(got[i], oracle_sums(new[i], tick, SEED), tick, ctx=f"upd {i}")
+    sim.close()
+
+
+def test_update_growing_n_in_the_two_pass_shared_stream_form():
+    """the two-pass shared-stream form (groups of >= 256 configs: here 101
+    acceptance groups of 400 (t_d, k) configs) keeps per-trial run records whose size grows
+    with N; an update from N = 100 to 160 keeps the record count but not the bytes, and must
+    equal a fresh handle (the buffer is re-sized by bytes, not records)."""
+    cfgs, tick = W.cfg3(trials=512, k_max=20, cells=slice(0, 2020))
+    new = cfgs.copy()
+    new["n_tokens"] = 160
+    flags = D.DSI_F_SHARED_STREAMS
+    sim, _ = run_sim(cfgs, tick, flags=flags)
+    sim.update(new).run()
+    got = sim.reduce()
+    _, want = run_sim(new, tick, flags=flags)
+    _, plain = run_sim(new, tick, flags=0)
+    for f in MOMENTS:
+        assert np.array_equal(got[f], want[f]), f
+        assert np.array_equal(got[f], plain[f]), f
     sim.close()
 
 
