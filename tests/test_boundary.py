@@ -162,8 +162,8 @@ def test_fresh_verifier_validation():
     with pytest.raises(D.DsiError) as e:
         _create(_one(ttft_target=2.0), flags=D.DSI_F_FRESH_VERIFIER)
     assert e.value.status == D.DSI_E_RANGE
-    with pytest.raises(D.DsiError) as e:
-        _create(_one(), flags=D.DSI_F_FRESH_VERIFIER | D.DSI_F_SHARED_STREAMS)
+    with pytest.raises(D.DsiError) as e:  # with shared streams too (validated, then no device here)
+        _create(_one(ttft_target=2.0), flags=D.DSI_F_FRESH_VERIFIER | D.DSI_F_SHARED_STREAMS)
     assert e.value.status == D.DSI_E_RANGE
 
 
