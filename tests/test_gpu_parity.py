@@ -421,11 +421,11 @@ def test_update_matches_a_fresh_handle(flags, dn, ttft):
 def test_update_growing_n_in_the_two_pass_shared_stream_form():
     """the two-pass shared-stream form (groups of >= 256 configs: here 101
     acceptance groups of 400 (t_d, k) configs) keeps per-trial run records whose size grows
-    with N; an update from N = 100 to 160 keeps the record count but not the bytes, and must
+    with N; an update from N = 100 to 120 keeps the record count but not the bytes, and must
     equal a fresh handle (the buffer is re-sized by bytes, not records)."""
     cfgs, tick = W.cfg3(trials=512, k_max=20, cells=slice(0, 2020))
     new = cfgs.copy()
-    new["n_tokens"] = 160
+    new["n_tokens"] = 120  # (keeps 256-thread blocks: the group and unit counts stay)
     flags = D.DSI_F_SHARED_STREAMS
     sim, _ = run_sim(cfgs, tick, flags=flags)
     sim.update(new).run()
