@@ -541,10 +541,15 @@ def test_fresh_verifier_long_sequences_arithmetic_path():
 
 
 def test_fresh_verifier_options():
+    """The fresh-verifier reading is accepted in every mode (round 2) but not with TTFT configs."""
     cfgs, tick = W.cfg1(trials=10)
-    with pytest.raises(D.DsiError) as e:
-        D.Simulator(cfgs, tick=tick, seed=SEED, flags=FRESH | D.DSI_F_SHARED_STREAMS)
-    assert e.value.status == D.DSI_E_RANGE
+    for extra in (0, D.DSI_F_SHARED_STREAMS, D.DSI_F_MEANS_ONLY):
+        D.Simulator(cfgs, tick=tick, seed=SEED, flags=FRESH | extra).close()
+    ttft, ttick = W.cfg2_ttft(trials=10)
+    for extra in (0, D.DSI_F_SHARED_STREAMS):
+        with pytest.raises(D.DsiError) as e:
+            D.Simulator(ttft, tick=ttick, seed=SEED, flags=FRESH | extra)
+        assert e.value.status == D.DSI_E_RANGE
 
 
 def _assert_cells_equal(got, want, ctx=""):
