@@ -10,7 +10,9 @@ workload is BASELINE configs[2], the paper's heatmap: 100 drafter
 latencies x 101 acceptance rates x k = 1..200 at SP 7, N = 100, 1e4 trials per
 point = 2.02e6 configs, 2.02e12 trial-tokens.  Metric: simulated trial-tokens/s.
 
-N > 1 is launched with torch.distributed.run; each rank simulates a cost-balanced
+N > 1 runs one process per GPU under torch.distributed.run (the driver launches it
+that way; `python bench.py --gpus N` without a torchrun environment re-executes itself
+under torch.distributed.run with N processes); each rank simulates a cost-balanced
 contiguous share of the (config, trial-tile) units and the per-config integer
 moments are summed with one NCCL all-reduce inside dsi_sim_reduce.  Total work is
 fixed as N grows, so the line reports "scaling": "strong".
@@ -90,6 +92,70 @@ def cells_equal(a, b) -> bool:
         elif not np.array_equal(x, y):
             return False
     return True
+
+
+def fig_summary(cfgs, res, cells) -> dict:
+    """The paper's heatmap claims on one run's results (rank 0): Fig. 3 (SI over all k,
+    DSI over the Eq.-1-feasible k at SP 7) from the cells, and Fig. 5 (App. F.7; SI and
+    DSI both at lookahead 5) from the k = 5 configs: the cells where SI is slower than non-SI
+    (Fig. 5(a)'s pink) and where DSI is slower than SI or than non-SI ("DSI is never slower than
+    either SI or non-SI")."""
+    out = {"fig3": {"cells": int(cells.size),
+                    "max_min_si_nonsi_over_dsi": float(np.nanmax(cells["r_min_dsi"])),
+                    "cells_dsi_slower_than_si": int(np.sum(cells["r_si_dsi"] < 1.0)),
+                    "cells_dsi_slower_than_nonsi": int(np.sum(cells["r_nonsi_dsi"] < 1.0))}}
+    k5 = cfgs["lookahead"] == 5
+    if np.any(k5):
+        r = res[k5]
+        out["fig5_k5"] = {"cells": int(np.sum(k5)),
+                          "si_slower_than_nonsi": int(np.sum(r["mean_si"] > r["mean_nonsi"])),
+                          "dsi_slower_than_si": int(np.sum(r["mean_dsi"] > r["mean_si"])),
+                          "dsi_slower_than_nonsi": int(np.sum(r["mean_dsi"] > r["mean_nonsi"]))}
+    return out
+
+
+def fresh_verifier_block(D, cfgs, tick, base_kw, root, fresh_id, flush, steps, res_default) -> dict:
+    """The fresh-verifier reading (R24, Thm 2's proof P:445) on the same workload: the
+    per-config kernel once (its sums are the reference for the fast modes), then the
+    shared-stream and means-only heatmap grid times; the fast modes' sums and cells must be
+    bit-identical to the per-config R24 run, and every config with k t_d <= t_t identical to
+    the default reading's."""
+    flags = D.DSI_F_TIMING | D.DSI_F_FRESH_VERIFIER | root
+    simf = D.Simulator(cfgs, flags=flags, nccl_id=fresh_id(), **base_kw)
+    simf.run()
+    resf = simf.reduce()
+    kern_ms = simf.kernel_ms()
+    simf.close()
+    simfs = D.Simulator(cfgs, flags=flags | D.DSI_F_SHARED_STREAMS, nccl_id=fresh_id(), **base_kw)
+    simfs.run()
+    ress = simfs.reduce()
+    heat_s, cells_s = heatmap_grid_times(simfs, flush, steps)
+    simfs.close()
+    simfm = D.Simulator(cfgs, flags=flags | D.DSI_F_MEANS_ONLY, nccl_id=fresh_id(), **base_kw)
+    simfm.run()
+    resm = simfm.reduce()
+    heat_m, cells_m = heatmap_grid_times(simfm, flush, steps)
+    simfm.close()
+    out = {"reading": "R24 fresh verifier (DSI_F_FRESH_VERIFIER)",
+           "per_config_kernel_ms": kern_ms,
+           "grid_time_shared_streams_s": statistics.median(heat_s),
+           "grid_time_means_only_s": statistics.median(heat_m)}
+    if res_default is not None and resf.size:  # rank 0 (REDUCE_TO_ROOT)
+        cells_f = D.dsi_heatmap(cfgs, resf)
+        sums = ("sum_si_ticks", "sum_dsi_ticks", "sum_segments", "sum_si_iters", "trials")
+        out["shared_streams_bit_identical"] = bool(
+            all(np.array_equal(ress[f], resf[f]) for f in sums + ("sumsq_dsi_ticks", "n_dsi_gt_nonsi", "n_dsi_gt_si"))
+            and cells_equal(cells_s, cells_f))
+        out["means_only_bit_identical"] = bool(all(np.array_equal(resm[f], resf[f]) for f in sums)
+                                               and cells_equal(cells_m, cells_f))
+        # the readings differ only where k t_d > t_t (integer ticks)
+        same = cfgs["lookahead"] * np.rint(cfgs["t_drafter"] / tick) <= np.rint(cfgs["t_target"] / tick)
+        out["configs_where_readings_differ"] = int(np.sum(~same))
+        out["identical_to_default_where_k_td_le_tt"] = bool(
+            np.array_equal(resf["sum_dsi_ticks"][same], res_default["sum_dsi_ticks"][same]))
+        out["trials_dsi_slower_than_nonsi"] = int(np.sum(resf["n_dsi_gt_nonsi"]))
+        out["figures"] = fig_summary(cfgs, resf, cells_f)
+    return out
 
 
 def trial_tokens(cfgs) -> int:
@@ -175,17 +241,30 @@ def multi_drafter_block(steps: int, sm_max: float) -> dict:
                                  "unsettled position), expected over the configs"}}
 
 
+def imad_wide_cycles() -> float:
+    """Cycles per warp-wide IMAD.WIDE.U32 on one SMSP, measured by profiles/pipe_peaks.cu (the
+    Philox half round IMAD.WIDE + LOP3, profiles/r02_pipe_peaks.jsonl); 4.0 if the file is absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_pipe_peaks.jsonl")) as f:
+            for ln in f:
+                d = json.loads(ln)
+                if d.get("op", "").startswith("IMAD.WIDE + LOP3"):
+                    return 2.0 * float(d["cycles_per_warp_instr"])  # two instructions per step
+    except (OSError, ValueError):
+        pass
+    return 4.0
+
+
 def mul_peak(sm_mhz: float) -> float:
-    """The fmaheavy pipe's multiply rate: 148 SMs x 4 SMSPs x 8 lanes per clock (one warp
-    IMAD.WIDE.U32 per 4 cycles, profiles/r01_philox_ceiling.txt, B300_MICROARCH IMAD rate / 2)."""
-    return SM_COUNT * 4 * 8 * sm_mhz * 1e6
+    """The fmaheavy pipe's 32x32->64 multiply rate: 148 SMs x 4 SMSPs x 32 lanes per IMAD.WIDE
+    issue interval (measured, imad_wide_cycles)."""
+    return SM_COUNT * 4 * 32 / imad_wide_cycles() * sm_mhz * 1e6
 
 
 def _imad_ceiling(sm_mhz: float) -> float:
-    """Trial-tokens/s if the fmaheavy pipe did nothing but Philox multiplies: 148 SMs x 4 SMSPs,
-    one warp IMAD.WIDE per 4 cycles, 16 per Philox call of 4 tokens (rounds 2-9)."""
-    wide_per_s = SM_COUNT * 4 * 32 / 4.0 * sm_mhz * 1e6
-    return wide_per_s / 4.0
+    """Trial-tokens/s if the fmaheavy pipe did nothing but Philox multiplies: the measured
+    IMAD.WIDE rate, 16 per Philox call of 4 tokens (rounds 2-9; rounds 0-1 are hoisted)."""
+    return mul_peak(sm_mhz) / 16.0 * 4.0
 
 
 def measured_peaks() -> dict:
@@ -367,12 +446,17 @@ def ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:  # the library's NCCL communicator prints its rank count at init (stderr)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     # DSI_BENCH_ONE_GPU=1 (test mode, numbers meaningless): every rank on GPU 0, gloo process
     # group, the library's cross-rank sums through the host all-reduce hook -- exercises the
     # whole multi-rank flow on a one-GPU box (NCCL refuses two ranks on one GPU)
     one_gpu = world > 1 and os.environ.get("DSI_BENCH_ONE_GPU") == "1"
     if one_gpu:
         local = 0
+    elif local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local} but {torch.cuda.device_count()} are visible")
     torch.cuda.set_device(local)
     coll_dev = "cpu" if one_gpu else "cuda"
     if world > 1 and one_gpu:
@@ -424,6 +508,9 @@ def ours(args):
     t_create = time.perf_counter()
     sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING | root, **kw)
     create_s = time.perf_counter() - t_create
+    comm = sim.comm_info()
+    if comm["nranks"] != world:
+        raise SystemExit(f"bench.py: the library's communicator has {comm['nranks']} ranks, WORLD_SIZE is {world}")
     stream = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", local))
     # result buffers allocated (and their pages touched) once, outside the timed region
     res = np.empty(cfgs.size, D.RESULT_DTYPE)
@@ -577,6 +664,13 @@ def ours(args):
     grid_s = max_over_ranks(statistics.median(heat_s))
     grid_shared_s = max_over_ranks(statistics.median(heat_shared_s)) if crn is not None else None
     grid_means_s = max_over_ranks(statistics.median(heat_means_s)) if heat_means_s else None  # (collective)
+    # the other DSI reading (R24) on the same workload, every mode (collective: all ranks)
+    fresh = None
+    if not args.no_fresh:
+        fresh = fresh_verifier_block(D, cfgs, tick, base_kw, root, fresh_nccl_id, flush, args.steps,
+                                     res if rank == 0 else None)
+        for k in ("per_config_kernel_ms", "grid_time_shared_streams_s", "grid_time_means_only_s"):
+            fresh[k] = max_over_ranks(fresh[k])
     heat = None
     if rank == 0:
         t0 = time.perf_counter()
@@ -598,6 +692,11 @@ def ours(args):
                 "at": {"t_drafter": float(cells["t_drafter"][i]), "accept_rate": float(cells["accept_rate"][i]),
                        "si_lookahead": int(cells["si_lookahead"][i]),
                        "dsi_lookahead": int(cells["dsi_lookahead"][i])},
+                "reading": "default: literal Alg. 1 (P:112-142) + App. D (P:392-401), R5/R6 -- the "
+                           "`value` run's; fresh_verifier: R24 (Thm 2's proof, P:445). They differ only "
+                           "where k t_d > t_t (DESIGN.md 2.1)",
+                "figures": fig_summary(cfgs, res, cells),
+                "fresh_verifier": fresh,
                 "note": "grid time = dsi_sim_run + dsi_sim_heatmap (all-reduce, one warp per cell on "
                         "the device, D2H of 10100 cells), host wall clock, median of the timed steps; "
                         "per-config, shared-stream and means-only modes, cells compared with the host "
@@ -627,6 +726,7 @@ def ours(args):
     # dominant kernel = the trial kernel; algorithmic instructions of this rank's share
     achieved = alg_instructions(cfgs) / world / (kern_ms / 1000.0)
     mults = alg_multiplies(cfgs) / world  # this rank's share
+    executed_wide = mults * 16.0 / 20.0    # rounds 2-9 of each call
     clk = clocks.summary()
     prof = {}
     try:
@@ -636,7 +736,9 @@ def ours(args):
         pass
     traffic = prof.get("dram_bytes_per_launch") if prof.get("workload") == args.workload else None
     ncu = None  # the pipe and issue utilisation ncu measured for this kernel (north_star: >= 60% issue)
-    sf = prof.get("set_full_stride20") if prof.get("workload") == args.workload else None
+    sf = None
+    if prof.get("workload") == args.workload:
+        sf = prof.get("set_full") or prof.get("set_full_stride20")
     if sf:
         def _pct(key):
             v = sf.get(key)
@@ -644,7 +746,8 @@ def ours(args):
         ncu = {"issue_active_pct": _pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                "fmaheavy_pct": _pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                "alu_pct": _pct("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
-               "source": f"profiles/{prof.get('round', '?')}_ncu_summary.json (--set full, 1/20 of the grid)"}
+               "source": f"profiles/{prof.get('round', '?')}_ncu_summary.json (--set full, "
+                         + ("a full bench launch)" if prof.get("set_full") else "1/20 of the grid)")}
 
     multi = None
     if rank == 0 and not args.no_multi:
@@ -668,39 +771,46 @@ def ours(args):
                        "configs": int(cfgs.size), "trials": int(cfgs["n_trials"].sum()),
                        "trial_tokens_per_step": tt, "tick": tick, "seed": W.SEED,
                        "l2": "flushed between timed steps (256 MiB memset)", "parallelism": f"dp{world}"},
-            # the unit that binds in ncu is the fmaheavy pipe (89.9% busy, profiles/*_ncu_summary.json),
-            # where Philox's 32x32->64 multiplies (IMAD.WIDE.U32) take 4 cycles per warp instruction;
-            # algorithmic work = the multiplies Philox4x32-10 defines (20 per 4 indicators; the kernel
-            # executes 16 of them per call after hoisting rounds 0-1)
-            "roofline": {"bound": "alu", "achieved": mults / (kern_ms / 1000.0) / 1e9,
-                         "peak": mul_peak(sm_max) / 1e9, "unit": "Gmul/s",
-                         "frac": mults / (kern_ms / 1000.0) / mul_peak(sm_max), "traffic": traffic,
+            # SURVEY 8(d).4's accounting: 11 + 10(1-a) algorithmic thread-instructions per
+            # trial-token against the issue peak (148 SM x 4 SMSP x 32 lanes x clock); the
+            # fmaheavy pipe that binds in ncu (Philox's IMAD.WIDE at a measured 4.1 cycles per
+            # warp instruction) is the "fmaheavy" sub-object
+            "roofline": {"bound": "alu", "achieved": achieved / 1e9, "peak": peak_instr / 1e9,
+                         "unit": "Ginstr/s", "frac": achieved / peak_instr, "traffic": traffic,
+                         "kernel": "dsi_trial_kernel", "kernel_ms": kern_ms,
+                         "kernel_share_of_step": kern_ms / (total_ms / args.steps),
+                         "work": "11 + 10(1-a) thread-instructions per trial-token (SURVEY 8(d).4): 10 for "
+                                 "Philox4x32-10 (10 rounds x (2 mul-wide + 2 xor) / 4 words), 1 Bernoulli "
+                                 "compare, 10 per rejection (segment walk + SI/DSI cost); per launch "
+                                 f"{alg_instructions(cfgs) / world:.4e} instructions",
+                         "peak_source": f"issue: 148 SM x 4 SMSP x 32 lanes x sm_max_mhz {sm_max:.0f} "
+                                        "(MEASURED_PEAKS.json), one warp-instruction per SMSP per clock",
+                         "frac_at_measured_clock": (achieved / (peak_instr * clk["sm_mhz"] / sm_max)
+                                                    if clk.get("sm_mhz") else None),
                          # what a launch must move: the config table (112 B), the unit prefix (8 B) and
                          # the moment accumulators read and written by the L2 atomics (2 x 64 B)
                          "algorithmic_bytes": int(cfgs.size) * (112 + 8 + 2 * 64),
-                         "kernel": "dsi_trial_kernel", "kernel_ms": kern_ms,
-                         "kernel_share_of_step": kern_ms / (total_ms / args.steps),
-                         "peak_source": f"fmaheavy pipe: 148 SM x 4 SMSP x 8 lanes/clk (one warp IMAD.WIDE "
-                                        f"per 4 cycles, measured, profiles/r01_philox_ceiling.txt) x sm_max_mhz "
-                                        f"{sm_max:.0f} (MEASURED_PEAKS.json)",
-                         "work": "Philox4x32-10: 20 multiplies per call of 4 indicators, ceil((N-1)/4) calls "
-                                 "per trial, configs with 0 < a < 1",
-                         "frac_at_measured_clock": (mults / (kern_ms / 1000.0) /
-                                                    (mul_peak(sm_max) * clk["sm_mhz"] / sm_max)
-                                                    if clk.get("sm_mhz") else None),
                          "ncu": ncu,
-                         "issue_slots": {"achieved": achieved / 1e9, "peak": peak_instr / 1e9,
-                                         "unit": "Ginstr/s", "frac": achieved / peak_instr,
-                                         "work": "11 + 10(1-a) thread-instructions per trial-token "
-                                                 "(SURVEY 8(d).4)",
-                                         "peak_source": "148 SM x 4 SMSP x 32 lanes x sm_max_mhz"},
-                         "trial_tokens_ceiling": {
-                             "pipe": "fmaheavy, 16 IMAD.WIDE per call executed",
-                             "ceiling_trial_tokens_per_s": _imad_ceiling(sm_max),
-                             "frac": (tt / world / (kern_ms / 1000.0)) / _imad_ceiling(sm_max)}},
+                         "fmaheavy": {
+                             "achieved": executed_wide / (kern_ms / 1000.0) / 1e9,
+                             "peak": mul_peak(sm_max) / 1e9, "unit": "G IMAD.WIDE/s",
+                             "frac": executed_wide / (kern_ms / 1000.0) / mul_peak(sm_max),
+                             "work": "the 32x32->64 multiplies the kernel must issue: Philox4x32-10 rounds "
+                                     "2-9 (rounds 0-1 hoisted, DESIGN.md 6.1), 16 per call of 4 indicators, "
+                                     "ceil((N-1)/4) calls per trial, configs with 0 < a < 1",
+                             "peak_source": f"148 SM x 4 SMSP x 32 lanes / {imad_wide_cycles():.2f} cycles per "
+                                            "warp IMAD.WIDE (profiles/r02_pipe_peaks.jsonl) x sm_max_mhz",
+                             "trial_tokens_ceiling": _imad_ceiling(sm_max),
+                             "trial_tokens_frac": (tt / world / (kern_ms / 1000.0)) / _imad_ceiling(sm_max)},
+                         "multiplies_defined": {
+                             "achieved": mults / (kern_ms / 1000.0) / 1e9, "peak": mul_peak(sm_max) / 1e9,
+                             "unit": "Gmul/s", "frac": mults / (kern_ms / 1000.0) / mul_peak(sm_max),
+                             "work": "all 20 multiplies per call Philox4x32-10 defines (a normalised speed, "
+                                     "not a pipe utilisation: 4 of them are hoisted)"}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches,
+            "comm": comm,
             "heatmap": heat,
             "shared_streams": crn,
             "means_only": means,
@@ -730,10 +840,42 @@ def main():
     ap.add_argument("--no-shared-streams", action="store_true")
     ap.add_argument("--no-multi", action="store_true", help="skip the multi-drafter block")
     ap.add_argument("--no-means", action="store_true", help="skip the means-only block")
+    ap.add_argument("--no-fresh", action="store_true", help="skip the fresh-verifier (R24) heatmap block")
     args = ap.parse_args()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return relaunch(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: launch one process per GPU "
+                         f"(torch.distributed.run --nproc-per-node {args.gpus}) or drop the torchrun wrapper")
     if args.impl == "reference":
         return reference_arm(args)
     return ours(args)
+
+
+def relaunch_command(gpus: int, argv, port: int) -> list:
+    """torch.distributed.run command that runs this script on `gpus` processes of one node, as
+    the driver launches it (the same flags)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def relaunch(gpus: int) -> int:
+    """--gpus N > 1 outside torchrun: one process per GPU under torch.distributed.run (rank 0
+    prints the line).  NCCL_DEBUG=INFO (INIT) makes each communicator's size visible in stderr."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = relaunch_command(gpus, sys.argv[1:], port)
+    sys.stdout.flush()
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":

@@ -236,6 +236,13 @@ DSI_API dsi_status dsi_sim_io_bytes(dsi_sim *h, uint64_t *h2d, uint64_t *d2h);
 /* Work units (config, trial tile) of this process: [first, first+count) of total. */
 DSI_API dsi_status dsi_sim_units(dsi_sim *h, uint64_t *first, uint64_t *count, uint64_t *total);
 
+/* The cross-rank exchange of this handle: *nranks and *rank as the NCCL
+ * communicator itself reports them (ncclCommCount / ncclCommUserRank), *transport 1 = NCCL,
+ * 2 = the test build's host all-reduce hook, 0 = none (one rank: nothing to exchange, *nranks
+ * = 1, *rank = 0).  Lets a caller check that a multi-process run formed one communicator of
+ * the expected size. */
+DSI_API dsi_status dsi_sim_comm_info(dsi_sim *h, int32_t *nranks, int32_t *rank, int32_t *transport);
+
 DSI_API void dsi_sim_destroy(dsi_sim *h); /* NULL-safe */
 
 DSI_API const char *dsi_status_str(dsi_status s);

@@ -26,6 +26,8 @@ NcclApi &nccl() {
       api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
       api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
       api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.CommCount = (decltype(api.CommCount))dlsym(h, "ncclCommCount");
+      api.CommUserRank = (decltype(api.CommUserRank))dlsym(h, "ncclCommUserRank");
       api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce &&
                api.GroupStart && api.GroupEnd && api.GetErrorString;
     }
@@ -109,6 +111,30 @@ dsi_status dsi_nccl_unique_id(uint8_t id[128]) {
   if (api.GetUniqueId(&u) != ncclSuccess) return DSI_E_COMM;
   static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
   std::memcpy(id, &u, 128);
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_comm_info(dsi_sim *h, int32_t *nranks, int32_t *rank, int32_t *transport) {
+  if (!h || !nranks || !rank || !transport) return DSI_E_NULL;
+  *nranks = 1;
+  *rank = 0;
+  *transport = 0;
+  if (!h->use_nccl) return DSI_OK;
+  if (h->host_coll) {
+    *nranks = h->opt.world;
+    *rank = h->opt.rank;
+    *transport = 2;
+    return DSI_OK;
+  }
+  NcclApi &api = nccl();
+  const DeviceState &d = h->dev[0];
+  if (!api.CommCount || !api.CommUserRank || !d.comm) return fail(h, DSI_E_COMM, "no NCCL communicator to query");
+  int n = 0, r = 0;
+  if (api.CommCount(d.comm, &n) != ncclSuccess || api.CommUserRank(d.comm, &r) != ncclSuccess)
+    return fail(h, DSI_E_COMM, "ncclCommCount / ncclCommUserRank failed");
+  *nranks = n;
+  *rank = r;
+  *transport = 1;
   return DSI_OK;
 }
 

@@ -42,7 +42,9 @@ namespace {
 // thread measured slower, profiles/r01_ab_crn_cpt_unroll.jsonl)
 // SUMS: a sums-only unit (CrnUnit::kind 1, every config k_eff = 1 without queueing): no
 // run lists -- the corrections come from the per-trial sums alone (plan_shared)
-template <int TH, int CPT, bool SUMS>
+// FRESH: the launch holds a fresh-verifier config (R24): its constants (CfgFr) are staged and
+// its corrections compiled in; launches without one compile them out
+template <int TH, int CPT, bool SUMS, bool FRESH>
 __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnParams P) {
   constexpr int CRN_THREADS = TH;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -62,6 +64,8 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   sp += (size_t)P.max_nq * sizeof(uint4);
   CfgLite *cl = reinterpret_cast<CfgLite *>(sp);
   sp += (size_t)CPT * CRN_THREADS * sizeof(CfgLite);
+  CfgFr *cf = reinterpret_cast<CfgFr *>(sp);
+  if (FRESH) sp += (size_t)CPT * CRN_THREADS * sizeof(CfgFr);
   // per trial slot: (m, n2, max stored L, nr | sum ceil(L/kmin) << 10 | sum floor(L/(kmin+1)) << 21)
   // (nr <= N/3 + 2 < 2^10, both sums <= N - 1 < 2^11: N <= 2048)
   uint4 *summ = reinterpret_cast<uint4 *>(sp);
@@ -81,9 +85,10 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   for (int j = threadIdx.x; j < CPT * CRN_THREADS; j += CRN_THREADS) {
     const CfgLite l = load_cfglite(P.cfg, P.perm, un, j, N);
     cl[j] = l;
+    if (FRESH) cf[j] = load_cfgfr(P.cfg, P.perm, un, j);
     if (j < (int)un.count) {
       atomicMin(&s_kmin, l.k_eff);
-      if (l.fresh) s_fresh = 1;
+      if (FRESH && cf[j].fresh) s_fresh = 1;
     }
   }
   __syncthreads();
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   const int kmin = s_kmin;
   // fresh-verifier configs (k t_d > t_t) correct every segment with g >= 2: a block holding one
   // stores every run of L >= 2 (runs of L = 1 are counted as n2 - nr)
-  const bool any_fresh = s_fresh != 0;
+  const bool any_fresh = FRESH && s_fresh != 0;
   const int store_min = any_fresh ? 1 : kmin;
   for (int j = threadIdx.x; j < (int)un.count; j += CRN_THREADS)
     if (cl[j].noqueue && cl[j].k_eff == kmin) atomicAdd(&s_nfast, 1);
@@ -207,6 +212,9 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
     const int ntr = (int)min((uint64_t)CRN_THREADS, T - tile0);
     if (active) {
       const CfgLite l = cl[my_c];
+      CfgFr f{};
+      if (FRESH) f = cf[my_c];
+      const bool fresh = FRESH && f.fresh != 0;
       // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 2048, <= 256 trials: no overflow)
       uint32_t p_gtn = 0, p_gts = 0, p_ai = 0, p_ai2 = 0, p_mai = 0;
       auto visit = [&](const uint4 v, const int s) {
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
         int dsi = m * l.t_t + n2 * l.s1;
         int si = m * l.si_cost;
         // corrections: a run long for this config, or (fresh variant) any segment with g >= 2
-        if (maxL > l.k_eff || (!SUMS && l.fresh && n2 > 0)) {
+        if (maxL > l.k_eff || (!SUMS && fresh && n2 > 0)) {
           const int nr = (int)(v.w & 0x3ffu);
           int ai = 0, ay = 0;
           if (SUMS || (sums && l.noqueue && l.k_eff == kmin)) {  // every stored run, S linear in b
@@ -224,9 +232,9 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
             for (int r = 0; r < nr; ++r) {  // the stored runs, in trial order
               const int L = runs[r * CRN_THREADS + s];
               if (L > l.k_eff) long_run(L, l, ai, ay);
-              if (l.fresh) ay -= fresh_saving_lite(L, l);
+              if (fresh) ay -= fresh_saving_lite(L, l, f);
             }
-            if (l.fresh) ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
+            if (fresh) ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
           }
           p_ai += (unsigned)ai;
           p_ai2 += (unsigned)(ai * ai);
@@ -300,11 +308,11 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   if (a_gts[0]) atomicAdd(dst + F_GT_SI, a_gts[0]);
 }
 
-template <int TH, bool SUMS>
+template <int TH, bool SUMS, bool FRESH>
 int launch_th(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(dsi_crn_kernel<TH, 1, SUMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = cudaFuncSetAttribute(dsi_crn_kernel<TH, 1, SUMS, FRESH>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
   const uint64_t max_grid = 0x7fffffffull;
@@ -312,7 +320,7 @@ int launch_th(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_crn_kernel<TH, 1, SUMS><<<(unsigned)n, TH, smem, st>>>(q);
+    dsi_crn_kernel<TH, 1, SUMS, FRESH><<<(unsigned)n, TH, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
@@ -322,10 +330,10 @@ int launch_th(const CrnParams &p, uint64_t n_units, size_t smem, cudaStream_t st
 
 }  // namespace
 
-size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs) {
+size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs, bool fresh) {
   const int max_nq = (max_n - 1 + 3) / 4 + 1;
   const size_t runs = ((size_t)block_threads * max_runs * sizeof(uint16_t) + 7) & ~(size_t)7;
-  return (size_t)max_nq * sizeof(uint4) + (size_t)cfg_per_block * sizeof(CfgLite) +
+  return (size_t)max_nq * sizeof(uint4) + (size_t)cfg_per_block * (sizeof(CfgLite) + (fresh ? sizeof(CfgFr) : 0)) +
          (size_t)block_threads * sizeof(uint4) + runs;
 }
 
@@ -333,12 +341,18 @@ int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, v
   if (n_units == 0) return 0;
   if (p.cfg_per_block != block_threads) return (int)cudaErrorInvalidValue;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t smem = crn_kernel_smem(p.max_n, block_threads, p.cfg_per_block, sums_only ? 0 : p.max_runs);
-  switch (block_threads) {
-    case 128: return sums_only ? launch_th<128, true>(p, n_units, smem, st) : launch_th<128, false>(p, n_units, smem, st);
-    case 256: return sums_only ? launch_th<256, true>(p, n_units, smem, st) : launch_th<256, false>(p, n_units, smem, st);
-    default: return (int)cudaErrorInvalidValue;
-  }
+  const bool fresh = p.any_fresh != 0;
+  const size_t smem = crn_kernel_smem(p.max_n, block_threads, p.cfg_per_block, sums_only ? 0 : p.max_runs, fresh);
+  // (sums-only units have every config k_eff = 1 without queueing: never fresh, k t_d <= t_t)
+  if (block_threads != 128 && block_threads != 256) return (int)cudaErrorInvalidValue;
+  if (sums_only)
+    return block_threads == 128 ? launch_th<128, true, false>(p, n_units, smem, st)
+                                : launch_th<256, true, false>(p, n_units, smem, st);
+  if (fresh)
+    return block_threads == 128 ? launch_th<128, false, true>(p, n_units, smem, st)
+                                : launch_th<256, false, true>(p, n_units, smem, st);
+  return block_threads == 128 ? launch_th<128, false, false>(p, n_units, smem, st)
+                              : launch_th<256, false, false>(p, n_units, smem, st);
 }
 
 }  // namespace dsi

@@ -146,7 +146,9 @@ __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
   for (int r = 0; r < nr; ++r) runs[r * TH + threadIdx.x] = my[r * TH];
 }
 
-template <int TH>
+// FRESH: the launch holds a fresh-verifier config (R24); compiled out otherwise (88 registers
+// against 72 without: 2 blocks per SM instead of 3)
+template <int TH, bool FRESH>
 __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const CrnParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_bsum[5];
@@ -156,21 +158,23 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
   const int N = G.n_tokens;
   // buffer b of the two tile buffers is smem + b * rec_bytes (computed from the shared array
   // itself, so the loads stay shared-memory loads)
-  CfgLite *cl = reinterpret_cast<CfgLite *>(smem + 2 * (size_t)P.rec_bytes);
   if (threadIdx.x < 5) s_bsum[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  cl[threadIdx.x] = load_cfglite(P.cfg, P.perm, un, threadIdx.x, N);
+  // each thread's own config, straight into registers
+  const CfgLite l = load_cfglite(P.cfg, P.perm, un, threadIdx.x, N);
+  CfgFr f{};
+  if (FRESH) f = load_cfgfr(P.cfg, P.perm, un, threadIdx.x);
+  const bool fresh = FRESH && f.fresh != 0;
   __syncthreads();
 
   const uint64_t tile_a = un.t0 / TH, tile_b = (un.t1 + TH - 1) / TH;  // un.t0 is tile-aligned
   const unsigned char *rec0 = P.records + (P.group_tile0[un.group] + tile_a) * (uint64_t)P.rec_bytes;
   if (threadIdx.x == 0) bulk_load(smem, rec0, P.rec_bytes, &bar[0]);
 
-  const CfgLite l = cl[threadIdx.x];
   const bool fast = l.noqueue && l.k_eff == 1;  // every run is long; S(b) = b k t_d
   // the lanes of a warp share k (lookahead-major order) and differ in t_d: where none of
   // them queues, the long-run loop needs no SP division (warp-uniform, so no divergence)
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
       int si = m * l.si_cost;
       // corrections: some run is long for this config, or (fresh-verifier variant) some
       // segment has g >= 2 -- every one of them saves time (R24)
-      if (maxL > l.k_eff || (l.fresh && n2 > 0)) {
+      if (maxL > l.k_eff || (fresh && n2 > 0)) {
         const int nr = (int)(v.w & 0x3ffu);
         int ai = 0, ay = 0;
         if (fast) {  // k = 1: ai = sum floor(L/2), ay = k t_d sum L - nr S(1)
@@ -222,27 +226,27 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
           for (int r = 0; r < nr; ++r) {  // runs in decreasing order: stop at the first short one
             const int L = runs[r * TH + s];
             if (L <= l.k_eff) {
-              if (!l.fresh) break;  // (fresh: every stored run L >= 2 saves)
+              if (!fresh) break;  // (fresh: every stored run L >= 2 saves)
             } else {
               ai += (int)magic_div((uint32_t)L, l.m_si, 0u);
               sb += (int)magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
               ++cnt;
             }
-            if (l.fresh) sv += fresh_saving_lite(L, l);
+            if (fresh) sv += fresh_saving_lite(L, l, f);
           }
           ay = sb * l.kd - cnt * l.s1 - sv;
         } else {
           for (int r = 0; r < nr; ++r) {
             const int L = runs[r * TH + s];
             if (L <= l.k_eff) {
-              if (!l.fresh) break;
+              if (!fresh) break;
             } else {
               long_run(L, l, ai, ay);
             }
-            if (l.fresh) ay -= fresh_saving_lite(L, l);
+            if (fresh) ay -= fresh_saving_lite(L, l, f);
           }
         }
-        if (l.fresh) ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
+        if (fresh) ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
         p_ai += (unsigned)ai;
         p_ai2 += (unsigned)(ai * ai);
         p_mai += (unsigned)(m * ai);
@@ -334,9 +338,7 @@ size_t crn_record_bytes(int max_runs, int threads) {
   return ((size_t)threads * sizeof(uint4) + (size_t)max_runs * threads * sizeof(uint16_t) + 15) & ~(size_t)15;
 }
 
-size_t crn_eval_smem(int max_runs, int threads) {
-  return 2 * crn_record_bytes(max_runs, threads) + (size_t)threads * sizeof(CfgLite);
-}
+size_t crn_eval_smem(int max_runs, int threads) { return 2 * crn_record_bytes(max_runs, threads); }
 
 int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, int threads, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -346,8 +348,11 @@ int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, 
     const int e = launch_grid(dsi_crn_stream_kernel<256>, p, n_tiles, threads, smem, st, true);
     if (e) return e;
   }
-  if (n_units) return launch_grid(dsi_crn_eval_kernel<256>, p, n_units, threads, crn_eval_smem(p.max_runs, threads),
-                                  st, false);
+  if (n_units) {
+    const size_t smem = crn_eval_smem(p.max_runs, threads);
+    return p.any_fresh ? launch_grid(dsi_crn_eval_kernel<256, true>, p, n_units, threads, smem, st, false)
+                       : launch_grid(dsi_crn_eval_kernel<256, false>, p, n_units, threads, smem, st, false);
+  }
   return 0;
 }
 

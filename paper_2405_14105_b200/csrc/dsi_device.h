@@ -122,6 +122,7 @@ struct CrnParams {
   const CrnTile *tiles;        // pass-1 work list of this device
   uint64_t tile_begin;
   uint32_t rec_bytes;
+  int32_t any_fresh;  // some config of the launch has CFG_FRESH (template FRESH variants)
   Keys keys;
 };
 // On-device heatmap product: one warp per cell, a cell being a run of
@@ -149,7 +150,7 @@ int launch_heatmap_kernel(const HeatParams &p, void *stream);
 int launch_check_trials(const DevCfg *cfg, const unsigned long long *acc, uint64_t n, unsigned int *bad,
                         void *stream);
 
-size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs);
+size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs, bool fresh);
 size_t crn_record_bytes(int max_runs, int threads);
 size_t crn_eval_smem(int max_runs, int threads);
 // pass 1 over n_tiles records (p.tiles from p.tile_begin), then pass 2 over n_units units

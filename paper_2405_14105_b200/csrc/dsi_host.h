@@ -10,6 +10,7 @@
 // inputs and combines exact integer sums.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // NVTX ranges of the API calls (header-only, see Trace)
 #include <nccl.h>  // types and enums only; libnccl is loaded with dlopen at first use
 
 #include <algorithm>
@@ -57,6 +58,8 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*CommCount)(const ncclComm_t, int *) = nullptr;     // optional (comm info)
+  ncclResult_t (*CommUserRank)(const ncclComm_t, int *) = nullptr;  // optional (comm info)
   bool ok = false;
 };
 
@@ -225,14 +228,20 @@ bool config_noqueue(const CfgTicks &t);
 DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh);
 double unit_cost(const CfgTicks &t, uint64_t trials);
 
-// DSI_TRACE=1 in the environment: each API call prints its phases (host wall clock, ms)
-// to stderr on return -- e.g. where dsi_sim_update's time goes.
+// Every API call is an NVTX range (nvtx3, header-only: a no-op unless a profiler such as
+// ncu or nsys injects its NVTX handler), and each phase an NVTX mark; with DSI_TRACE=1 in the
+// environment each call also prints its phases (host wall clock, ms) to stderr on return --
+// e.g. where dsi_sim_update's time goes.
 class Trace {
  public:
   explicit Trace(const char *call) : call_(call), on_(enabled()) {
+    nvtxRangePushA(call);
     if (on_) t0_ = last_ = std::chrono::steady_clock::now();
   }
+  Trace(const Trace &) = delete;
+  Trace &operator=(const Trace &) = delete;
   void mark(const char *phase) {
+    nvtxMarkA(phase);
     if (!on_) return;
     const auto t = std::chrono::steady_clock::now();
     char b[96];
@@ -241,6 +250,7 @@ class Trace {
     last_ = t;
   }
   ~Trace() {
+    nvtxRangePop();
     if (!on_) return;
     const double total =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();

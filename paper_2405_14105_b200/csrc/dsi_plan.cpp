@@ -112,7 +112,8 @@ dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_uni
 // h->crn_units and the devices' unit ranges.
 dsi_status plan_two_pass(dsi_sim *h) {
   const int th = h->cfg_per_block;
-  h->two_pass = th == 256 && dsi::crn_eval_smem(h->max_runs, th) <= 76 * 1024;
+  // pass 2's two tile buffers must leave room for 3 blocks per SM (its register budget)
+  h->two_pass = th == 256 && dsi::crn_eval_smem(h->max_runs, th) <= 64 * 1024;
   if (knobs().crn_two_pass >= 0) h->two_pass = h->two_pass && knobs().crn_two_pass != 0;
   if (!h->two_pass) return DSI_OK;
   try {
@@ -188,7 +189,7 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
     // groups hold 3 / 140 / 100 configs, 1.8-1.9x slower; 2 or 4 configs per thread were
     // slower too, profiles/r01_ab_crn*.jsonl)
     const bool big_groups = n >= 256 * h->groups.size();
-    int th = (big_groups && dsi::crn_kernel_smem(h->max_n, 256, 256, h->max_runs) <= 48 * 1024) ? 256 : kCrnThreads;
+    int th = (big_groups && dsi::crn_kernel_smem(h->max_n, 256, 256, h->max_runs, h->any_fresh) <= 48 * 1024) ? 256 : kCrnThreads;
     if (knobs().crn_threads == 128 || knobs().crn_threads == 256) th = knobs().crn_threads;
     h->cfg_per_block = th;
     h->block_threads = th;

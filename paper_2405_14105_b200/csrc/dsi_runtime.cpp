@@ -613,6 +613,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       q.max_nq = (h->max_n - 1 + 3) / 4 + 1;
       q.max_runs = h->max_runs;
       q.cfg_per_block = h->cfg_per_block;
+      q.any_fresh = h->any_fresh ? 1 : 0;
       q.keys = p.keys;
       if (h->two_pass) {
         q.records = d.d_records;

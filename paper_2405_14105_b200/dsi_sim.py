@@ -89,6 +89,7 @@ def _load(path: str):
         "dsi_sim_kernel_ms": ([V, i32, P(ctypes.c_float)], ctypes.c_int),
         "dsi_sim_units": ([V, P(u64), P(u64), P(u64)], ctypes.c_int),
         "dsi_sim_io_bytes": ([V, P(u64), P(u64)], ctypes.c_int),
+        "dsi_sim_comm_info": ([V, P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)], ctypes.c_int),
         "dsi_sim_destroy": ([V], None),
         "dsi_status_str": ([ctypes.c_int], ctypes.c_char_p),
         "dsi_sim_last_error": ([V], ctypes.c_char_p),
@@ -169,7 +170,7 @@ def dsi_build_id() -> str:
     return lib.dsi_build_id().decode()
 EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce", "dsi_sim_trials", "dsi_sim_hist",
             "dsi_sim_stream", "dsi_sim_launches", "dsi_sim_kernel_ms", "dsi_sim_units", "dsi_sim_io_bytes",
-            "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
+            "dsi_sim_comm_info", "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
             "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
             "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
             "dsi_heatmap_csv", "dsi_sim_heatmap", "dsi_multi_simulate", "dsi_multi_last_kernel",
@@ -394,6 +395,13 @@ def dsi_sim_units(h) -> tuple:
     return a.value, b.value, c.value
 
 
+def dsi_sim_comm_info(h) -> dict:
+    """The handle's cross-rank exchange as the communicator reports it (transport: none, nccl, host)."""
+    n, r, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(_L(h).dsi_sim_comm_info(h, ctypes.byref(n), ctypes.byref(r), ctypes.byref(t)), h)
+    return {"nranks": n.value, "rank": r.value, "transport": ("none", "nccl", "host")[t.value]}
+
+
 def dsi_sim_io_bytes(h) -> tuple:
     a, b = ctypes.c_uint64(), ctypes.c_uint64()
     _check(_L(h).dsi_sim_io_bytes(h, ctypes.byref(a), ctypes.byref(b)), h)
@@ -444,6 +452,9 @@ class Simulator:
 
     def launches(self) -> int:
         return dsi_sim_launches(self.h)
+
+    def comm_info(self) -> dict:
+        return dsi_sim_comm_info(self.h)
 
     def io_bytes(self) -> tuple:
         return dsi_sim_io_bytes(self.h)

@@ -29,6 +29,11 @@ def test_bench_json_line_small_workload():
     assert d["shared_streams"]["bit_identical_to_value_run"] is True
     assert d["means_only"]["sums_and_means_identical_to_value_run"] is True
     assert d["multi_drafter"]["value"] > 0 and 0 < d["multi_drafter"]["roofline"]["frac"] <= 1.0
+    assert 0 < d["roofline"]["fmaheavy"]["frac"] <= 1.0 and d["roofline"]["unit"] == "Ginstr/s"
+    assert d["comm"] == {"nranks": 1, "rank": 0, "transport": "none"}
+    fv = d["heatmap"]["fresh_verifier"]
+    assert fv["shared_streams_bit_identical"] is True and fv["means_only_bit_identical"] is True
+    assert fv["identical_to_default_where_k_td_le_tt"] is True
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 
@@ -53,6 +58,24 @@ def test_bench_two_ranks_on_one_gpu():
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2" and d["value"] > 0
+    assert d["comm"] == {"nranks": 2, "rank": 0, "transport": "host"}
+    assert d["heatmap"]["fresh_verifier"]["shared_streams_bit_identical"] is True
     assert d["heatmap"]["device_cells_equal_host_product"] is True
     assert d["shared_streams"]["bit_identical_to_value_run"] is True
     assert d["means_only"]["sums_and_means_identical_to_value_run"] is True
+
+
+def test_bench_gpus_flag_relaunches_itself():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under torch.distributed.run with
+    2 processes (here both on GPU 0 through the test transport)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["DSI_BENCH_ONE_GPU"] = "1"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--workload", "cfg1",
+                        "--steps", "1", "--warmup", "3", "--no-multi", "--no-fresh"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 2 and d["comm"]["nranks"] == 2
