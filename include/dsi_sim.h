@@ -257,6 +257,11 @@ DSI_API dsi_status dsi_nccl_unique_id(uint8_t id[128]);
 
 /* Pure planner helpers of Eq. 1, exact integers.
  * Return -1 on invalid input (ticks < 1, sp < 1, k < 1). */
+/* R15's time quantisation, the one create applies to every latency: *out = round(x / tick) when
+ * x and tick are finite and positive and x / tick is within 1e-9 (relative) of an integer >= 1;
+ * else DSI_E_RANGE (x or tick not finite / not positive), DSI_E_TICK (not a whole number of
+ * ticks) or DSI_E_OVERFLOW, and *out is not written. */
+DSI_API dsi_status dsi_ticks(double x, double tick, int64_t *out);
 DSI_API int32_t dsi_min_lookahead(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t sp);
 DSI_API int32_t dsi_required_processors(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k);
 DSI_API int32_t dsi_eq1_feasible(int64_t t_target_ticks, int64_t t_drafter_ticks, int32_t k, int32_t sp);

@@ -28,15 +28,26 @@ from . import dsi_sim as D
 from . import workloads as W
 
 
-def _ticks(x: float, tick: float) -> int:
-    return int(round(x / tick))
+class UsageError(Exception):
+    """Invalid arguments (exit code 2)."""
 
 
 def cmd_plan(a) -> dict:
-    tt, td = _ticks(a.t_target, a.tick), _ticks(a.t_drafter, a.tick)
+    """Eq. 1, every number from the library: latencies in whole ticks
+    (R15, dsi_ticks), Assumption 2 (t_drafter <= t_target), SP >= 1."""
+    tt, td = D.dsi_ticks(a.t_target, a.tick), D.dsi_ticks(a.t_drafter, a.tick)
+    if td > tt:
+        raise UsageError("t_drafter must not exceed t_target (Assumption 2)")
+    if a.sp < 1:
+        raise UsageError("sp must be >= 1")
     k = D.dsi_min_lookahead(tt, td, a.sp)
-    return {"min_lookahead": k, "processors": D.dsi_required_processors(tt, td, k),
-            "max_useful_sp": -(-tt // td), "eq1_feasible_at_k": bool(D.dsi_eq1_feasible(tt, td, k, a.sp))}
+    procs = D.dsi_required_processors(tt, td, k)
+    # beyond ceil(t_t / t_d) target servers (the k = 1 requirement) no lookahead needs more
+    max_sp = D.dsi_required_processors(tt, td, 1) - 1
+    feasible = D.dsi_eq1_feasible(tt, td, k, a.sp)
+    if min(k, procs, max_sp, feasible) < 0:
+        raise UsageError("invalid planner arguments")
+    return {"min_lookahead": k, "processors": procs, "max_useful_sp": max_sp, "eq1_feasible_at_k": bool(feasible)}
 
 
 def cmd_simulate(a) -> dict:
@@ -67,7 +78,11 @@ def table2(trials: int, sp: int, n_tokens: int, seed: int = W.SEED, device: int 
 
 
 def cmd_table2(a) -> list:
-    return table2(a.trials, a.sp, a.n_tokens, a.seed, prefill=a.prefill)
+    """--sp / --n-tokens default to the protocol's own values: SP 8, N 100 (BASELINE configs[1])
+    without --prefill; SP 7, N 50 with it."""
+    sp = a.sp if a.sp is not None else (7 if a.prefill else 8)
+    n = a.n_tokens if a.n_tokens is not None else (50 if a.prefill else 100)
+    return table2(a.trials, sp, n, a.seed, prefill=a.prefill)
 
 
 def _distributed_kw():
@@ -153,8 +168,8 @@ def main(argv=None) -> int:
     p.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER (DESIGN.md R24)")
     p = sub.add_parser("table2", help="Table 2 pairs offline, lookahead in {1, 5, 10}")
     p.add_argument("--trials", type=int, default=100_000)
-    p.add_argument("--sp", type=int, default=8)
-    p.add_argument("--n-tokens", type=int, default=100)
+    p.add_argument("--sp", type=int, default=None, help="default 8, or 7 with --prefill (P:273)")
+    p.add_argument("--n-tokens", type=int, default=None, help="default 100, or 50 with --prefill (P:273)")
     p.add_argument("--prefill", action="store_true",
                    help="TTFT = Table-3 ratio x TPOT for each model's first forward (use --trials <= 1e4)")
     p = sub.add_parser("heatmap", help="Fig. 3 grid; optional CSV")
@@ -179,6 +194,9 @@ def main(argv=None) -> int:
     try:
         out = {"plan": cmd_plan, "simulate": cmd_simulate, "table2": cmd_table2, "heatmap": cmd_heatmap,
                "multi": cmd_multi}[a.cmd](a)
+    except UsageError as e:
+        print(str(e), file=sys.stderr)
+        return 2
     except D.DsiError as e:
         print(str(e), file=sys.stderr)
         return 3 if e.status in (D.DSI_E_DEVICE, D.DSI_E_COMM, D.DSI_E_NOMEM) else 2

@@ -279,6 +279,12 @@ const char *dsi_status_str(dsi_status s) {
 const char *dsi_sim_last_error(const dsi_sim *h) { return h ? h->err.c_str() : ""; }
 const char *dsi_last_create_error(void) { return g_create_error.c_str(); }
 
+dsi_status dsi_ticks(double x, double tick, int64_t *out) {
+  if (!out) return DSI_E_NULL;
+  if (!std::isfinite(tick) || tick <= 0.0) return DSI_E_RANGE;
+  return to_ticks(x, tick, out);
+}
+
 int32_t dsi_eq1_feasible(int64_t t_t, int64_t t_d, int32_t k, int32_t sp) {
   if (t_t < 1 || t_d < 1 || k < 1 || sp < 1) return -1;
   return ceil_div(t_t, (int64_t)k * t_d) <= sp ? 1 : 0;

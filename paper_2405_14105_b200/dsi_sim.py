@@ -96,6 +96,7 @@ def _load(path: str):
         "dsi_last_create_error": ([], ctypes.c_char_p),
         "dsi_abi_version": ([], ctypes.c_uint32),
         "dsi_nccl_unique_id": ([V], ctypes.c_int),
+        "dsi_ticks": ([ctypes.c_double, ctypes.c_double, P(ctypes.c_int64)], ctypes.c_int),
         "dsi_min_lookahead": ([i64, i64, i32], i32),
         "dsi_required_processors": ([i64, i64, i32], i32),
         "dsi_eq1_feasible": ([i64, i64, i32, i32], i32),
@@ -171,7 +172,7 @@ def dsi_build_id() -> str:
 EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce", "dsi_sim_trials", "dsi_sim_hist",
             "dsi_sim_stream", "dsi_sim_launches", "dsi_sim_kernel_ms", "dsi_sim_units", "dsi_sim_io_bytes",
             "dsi_sim_comm_info", "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
-            "dsi_abi_version", "dsi_nccl_unique_id", "dsi_min_lookahead",
+            "dsi_abi_version", "dsi_nccl_unique_id", "dsi_ticks", "dsi_min_lookahead",
             "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
             "dsi_heatmap_csv", "dsi_sim_heatmap", "dsi_multi_simulate", "dsi_multi_last_kernel",
             "dsi_build_id")
@@ -205,6 +206,13 @@ def dsi_test_set_knob(name: str, value: int) -> None:
 
 
 # ----------------------------------------------------------------------------- same names as the C ABI
+def dsi_ticks(x: float, tick: float) -> int:
+    """R15: round(x / tick), raising DsiError (DSI_E_RANGE / DSI_E_TICK) like dsi_sim_create."""
+    out = ctypes.c_int64()
+    _check(lib.dsi_ticks(float(x), float(tick), ctypes.byref(out)))
+    return out.value
+
+
 def dsi_min_lookahead(t_target_ticks: int, t_drafter_ticks: int, sp: int) -> int:
     return lib.dsi_min_lookahead(t_target_ticks, t_drafter_ticks, sp)
 

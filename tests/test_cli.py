@@ -34,6 +34,31 @@ def test_plan_matches_paper_examples():
     assert json.loads(out)["min_lookahead"] == 7
 
 
+def test_plan_validates_like_create():
+    """plan converts latencies with the library's R15 rule (dsi_ticks) and checks Assumption 2:
+    a non-whole number of ticks, a nonpositive latency or t_drafter > t_target exit 2."""
+    rc, _, err = run_cli("plan", "--t-target", "1.0", "--t-drafter", "0.004", "--sp", "4")
+    assert rc == 2 and "DSI_E_TICK" in err
+    rc, _, err = run_cli("plan", "--t-target", "-1.0", "--t-drafter", "0.05", "--sp", "4")
+    assert rc == 2 and "DSI_E_RANGE" in err
+    rc, _, err = run_cli("plan", "--t-target", "0.5", "--t-drafter", "1.0", "--sp", "4")
+    assert rc == 2 and "Assumption 2" in err
+    rc, _, err = run_cli("plan", "--t-target", "1.0", "--t-drafter", "0.05", "--sp", "0")
+    assert rc == 2
+    rc, out, _ = run_cli("plan", "--t-target", "1.0", "--t-drafter", "0.1", "--sp", "2")
+    d = json.loads(out)
+    assert rc == 0 and d["max_useful_sp"] == 10 and d["min_lookahead"] == 5 and d["processors"] == 3
+
+
+def test_ticks_rule():
+    assert D.dsi_ticks(0.3, 0.1) == 3 and D.dsi_ticks(20.6, 0.1) == 206
+    for x, tick, st in ((0.004, 0.01, D.DSI_E_TICK), (0.0, 0.01, D.DSI_E_RANGE), (1.0, -0.01, D.DSI_E_RANGE),
+                        (float("nan"), 0.01, D.DSI_E_RANGE)):
+        with pytest.raises(D.DsiError) as e:
+            D.dsi_ticks(x, tick)
+        assert e.value.status == st
+
+
 def test_invalid_arguments_exit_2():
     rc, _, err = run_cli("simulate", "--t-target", "1.0", "--t-drafter", "2.0", "--accept", "0.5",
                          "--lookahead", "1", "--sp", "2", "--n-tokens", "10")
