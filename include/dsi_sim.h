@@ -201,6 +201,21 @@ DSI_API dsi_status dsi_sim_run(dsi_sim *h);
  * Every rank must call it. */
 DSI_API dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n);
 
+/* The exchange step of dsi_sim_reduce without bringing anything to the host: the cross-rank
+ * all-reduce of the moments and the device-side partition check, enqueued on the library's
+ * stream (asynchronous; every rank must call it).  The exact per-config moments stay in device
+ * memory; dsi_sim_fetch derives any range of results, dsi_sim_heatmap the cells, without a
+ * second all-reduce.  P:531's averaging is deferred to what the caller reads.  DSI_E_STATE
+ * before dsi_sim_run or with DSI_F_HIST (histograms come back with dsi_sim_reduce). */
+DSI_API dsi_status dsi_sim_reduce_device(dsi_sim *h);
+
+/* Results [first, first + count) after dsi_sim_reduce_device (or dsi_sim_reduce): blocks, checks
+ * the partition flag (DSI_E_DEVICE, nothing written), copies those configs' moments to the host
+ * and derives the FP64 fields exactly as dsi_sim_reduce does -- out[i] is config first + i.
+ * DSI_E_RANGE if the range exceeds n_cfg; DSI_E_STATE before a reduce, or on a rank != 0 with
+ * DSI_F_REDUCE_TO_ROOT. */
+DSI_API dsi_status dsi_sim_fetch(dsi_sim *h, size_t first, size_t count, dsi_result *out);
+
 /* Per-trial records of trials [first, first+count) of config cfg (needs
  * DSI_F_PER_TRIAL, one device, world == 1).  Any output pointer may be NULL. */
 DSI_API dsi_status dsi_sim_trials(dsi_sim *h, size_t cfg, uint64_t first, uint64_t count,

@@ -188,6 +188,7 @@ struct dsi_sim {
   std::vector<DeviceState> dev;
   Pinned<unsigned long long> host_acc, host_seg, host_si;  // D2H targets
   bool ran = false, reduced = false;
+  bool reduced_device = false;  // the moments of the last run are summed (dsi_sim_reduce[_device])
   std::vector<dsi::HeatCell> heat_cells;  // heatmap cells (planned on first use, reset by update)
   bool heat_planned = false, heat_uploaded = false;
   Pinned<dsi::HeatOut> heat_out;

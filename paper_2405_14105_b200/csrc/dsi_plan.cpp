@@ -268,16 +268,35 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
 
 // Heatmap cells: maximal runs of consecutive configs with equal (t_target, t_drafter, a, SP, N).
 void plan_heat_cells(dsi_sim *h) {
-  h->heat_cells.clear();
+  // a cell starts at config i when i = 0 or (t_target, t_drafter, a, SP, N) differ from config
+  // i - 1's: the starts are found per chunk in parallel, then written at their prefix offsets
   const auto &t = h->ticks;
-  for (size_t i = 0; i < h->n_cfg;) {
-    size_t j = i + 1;
-    while (j < h->n_cfg && t[j].ut == t[i].ut && t[j].ud == t[i].ud && t[j].a == t[i].a && t[j].sp == t[i].sp &&
-           t[j].n == t[i].n)
-      ++j;
-    h->heat_cells.push_back(dsi::HeatCell{(uint64_t)i, (uint32_t)(j - i), 0u});
-    i = j;
-  }
+  const size_t n = h->n_cfg;
+  auto starts = [&](size_t i) {
+    return i == 0 || !(t[i].ut == t[i - 1].ut && t[i].ud == t[i - 1].ud && t[i].a == t[i - 1].a &&
+                       t[i].sp == t[i - 1].sp && t[i].n == t[i - 1].n);
+  };
+  constexpr size_t K = 64;
+  size_t cnt[K + 1] = {};
+  parallel_for(K, [&](size_t b, size_t e) {
+    for (size_t c = b; c < e; ++c) {
+      size_t m = 0;
+      for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) m += starts(i);
+      cnt[c + 1] = m;
+    }
+  }, 1);
+  for (size_t c = 0; c < K; ++c) cnt[c + 1] += cnt[c];
+  h->heat_cells.assign(cnt[K], dsi::HeatCell{0, 0, 0u});
+  parallel_for(K, [&](size_t b, size_t e) {
+    for (size_t c = b; c < e; ++c) {
+      size_t w = cnt[c];
+      for (size_t i = n * c / K; i < n * (c + 1) / K; ++i)
+        if (starts(i)) h->heat_cells[w++].first = i;
+    }
+  }, 1);
+  const size_t nc = h->heat_cells.size();
+  for (size_t j = 0; j < nc; ++j)
+    h->heat_cells[j].count = (uint32_t)((j + 1 < nc ? h->heat_cells[j + 1].first : n) - h->heat_cells[j].first);
 }
 
 // Means-only, one device per process: every part's config range starts at a cell, so each

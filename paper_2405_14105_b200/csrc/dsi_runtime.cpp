@@ -3,6 +3,8 @@
 // finalize), the device heatmap product, and the accessors / measurement hooks.
 #include "dsi_host.h"
 
+#include <atomic>
+
 using namespace dsih;
 
 namespace dsih {
@@ -448,12 +450,16 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   if (s == DSI_OK) s = derive_limits(h, h->ticks_next);  // the new configs may need a larger launch shape
   if (s != DSI_OK) return s;                              // derive_limits only commits on success
   if (h->means_only) {  // the histogram groups are fixed at create: their keys must not change
-    bool same = h->max_n <= kMeansMaxN;
-    for (size_t i = 0; same && i < n_cfg; ++i) {
-      const CfgTicks &a = h->ticks[i], &b = h->ticks_next[i];
-      const bool ta = a.t_t1 != a.t_t || a.t_d1 != a.t_d, tb = b.t_t1 != b.t_t || b.t_d1 != b.t_d;
-      same = a.stream_id == b.stream_id && a.thr == b.thr && a.n == b.n && a.trials == b.trials && ta == tb;
-    }
+    std::atomic<bool> keys_same{h->max_n <= kMeansMaxN};
+    parallel_for(n_cfg, [&](size_t lo, size_t hi) {
+      for (size_t i = lo; i < hi && keys_same.load(std::memory_order_relaxed); ++i) {
+        const CfgTicks &a = h->ticks[i], &b = h->ticks_next[i];
+        const bool ta = a.t_t1 != a.t_t || a.t_d1 != a.t_d, tb = b.t_t1 != b.t_t || b.t_d1 != b.t_d;
+        if (!(a.stream_id == b.stream_id && a.thr == b.thr && a.n == b.n && a.trials == b.trials && ta == tb))
+          keys_same = false;
+      }
+    });
+    const bool same = keys_same;
     if (!same) {
       h->max_n = old_n;
       h->max_keff = old_keff;
@@ -522,7 +528,7 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   tr.mark(replan ? "replan+sync" : "sync");
   fill_dev_cfg(h);
   tr.mark("fill");
-  h->ran = h->reduced = false;
+  h->ran = h->reduced = h->reduced_device = false;
   h->heat_planned = h->heat_uploaded = false;
   const dsi_status su = upload(h, replan);
   tr.mark("upload");
@@ -712,35 +718,19 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     }
   }
   h->ran = true;
-  h->reduced = false;
+  h->reduced = h->reduced_device = false;
   return DSI_OK;
 }
 
-dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
-  if (!h) return DSI_E_NULL;
-  Trace tr("dsi_sim_reduce");
-  h->err.clear();
-  const bool root_only = (h->opt.flags & DSI_F_REDUCE_TO_ROOT) && h->opt.rank != 0;
-  if (!out && !root_only) return fail(h, DSI_E_NULL, "out is NULL");
-  const size_t n_cfg = h->n_cfg;
-  if (n != n_cfg) return fail(h, DSI_E_RANGE, "n must equal n_cfg");
-  if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_reduce before dsi_sim_run");
-  const bool hist = h->opt.flags & DSI_F_HIST;
+namespace {
+
+// The exchange step, enqueued: the cross-rank all-reduce of the moments, the partition check
+// (every trial simulated exactly once) on the device and its flag copied back.  Asynchronous
+// on device 0's stream; with DSI_F_REDUCE_TO_ROOT on a rank != 0 only the all-reduce.
+dsi_status reduce_enqueue(dsi_sim *h, bool hist) {
   dsi_status st = sum_across(h, hist);
   if (st != DSI_OK) return st;
-  tr.mark("allreduce-enqueue");
-  if (root_only) {  // DSI_F_REDUCE_TO_ROOT: this rank contributed its sums; rank 0 checks and finalizes
-    for (auto &d : h->dev) {
-      CUDA_TRY(h, cudaSetDevice(d.ordinal));
-      CUDA_TRY(h, cudaStreamSynchronize(d.stream));
-    }
-    h->reduced = true;
-    return DSI_OK;
-  }
-  // every device now holds the global sums (or there is one device): read device 0.
-  // The partition check (every trial simulated exactly once) runs on the device before the
-  // copies; the moments come back in chunks so the host finalizes chunk i while chunk i+1
-  // is in flight.
+  if ((h->opt.flags & DSI_F_REDUCE_TO_ROOT) && h->opt.rank != 0) return DSI_OK;
   DeviceState &d0 = h->dev[0];
   CUDA_TRY(h, cudaSetDevice(d0.ordinal));
   const unsigned long long *src = h->use_nccl ? d0.d_red : d0.d_acc;
@@ -748,23 +738,33 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   if (!h->chunk_ev[0])
     for (auto &ev : h->chunk_ev) CUDA_TRY(h, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   CUDA_TRY(h, cudaMemsetAsync(d0.d_heat_bad, 0, sizeof(unsigned int), d0.stream));
-  {
-    const int e = dsi::launch_check_trials(d0.d_cfg, src, n_cfg, d0.d_heat_bad, d0.stream);
-    if (e) return cuda_fail(h, (cudaError_t)e, "partition check launch");
-    h->launches += 1;
-  }
+  const int e = dsi::launch_check_trials(d0.d_cfg, src, h->n_cfg, d0.d_heat_bad, d0.stream);
+  if (e) return cuda_fail(h, (cudaError_t)e, "partition check launch");
+  h->launches += 1;
   CUDA_TRY(h, cudaMemcpyAsync(h->host_bad.p, d0.d_heat_bad, sizeof(unsigned int), cudaMemcpyDeviceToHost,
                               d0.stream));
-  if (hist) {
-    CUDA_TRY(h, cudaMemcpyAsync(h->host_seg.p, h->use_nccl ? d0.d_seg_red : d0.d_seg,
-                                n_cfg * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d0.stream));
-    CUDA_TRY(h, cudaMemcpyAsync(h->host_si.p, h->use_nccl ? d0.d_si_red : d0.d_si,
-                                h->si_bins_total * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                                d0.stream));
+  return DSI_OK;
+}
+
+// Wait for every device's stream (the all-reduce ran on each).
+dsi_status sync_all(dsi_sim *h) {
+  for (auto &d : h->dev) {
+    CUDA_TRY(h, cudaSetDevice(d.ordinal));
+    CUDA_TRY(h, cudaStreamSynchronize(d.stream));
   }
-  const size_t n_chunks = n_cfg < (1u << 16) ? 1 : kReduceChunks;
+  return DSI_OK;
+}
+
+// Results [first, first + count) from the reduced moments on device 0: chunked D2H into the
+// pinned mirror, the host finalizing chunk i while chunk i+1 is in flight.  The partition flag
+// (reduce_enqueue) is checked before any result is written.
+dsi_status finalize_range(dsi_sim *h, size_t first, size_t count, dsi_result *out, Trace &tr) {
+  DeviceState &d0 = h->dev[0];
+  CUDA_TRY(h, cudaSetDevice(d0.ordinal));
+  const unsigned long long *src = h->use_nccl ? d0.d_red : d0.d_acc;
+  const size_t n_chunks = count < (1u << 16) ? 1 : kReduceChunks;
   for (size_t c = 0; c < n_chunks; ++c) {
-    const size_t b = n_cfg * c / n_chunks, e = n_cfg * (c + 1) / n_chunks;
+    const size_t b = first + count * c / n_chunks, e = first + count * (c + 1) / n_chunks;
     CUDA_TRY(h, cudaMemcpyAsync(h->host_acc.p + b * dsi::NF, src + b * dsi::NF,
                                 (e - b) * dsi::NF * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                 d0.stream));
@@ -784,13 +784,13 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   }
   const double tick = h->opt.tick;
   for (size_t c = 0; c < n_chunks; ++c) {
-  const size_t cb = n_cfg * c / n_chunks, ce = n_cfg * (c + 1) / n_chunks;
+  const size_t cb = first + count * c / n_chunks, ce = first + count * (c + 1) / n_chunks;
   if (c) CUDA_TRY(h, cudaEventSynchronize(h->chunk_ev[c]));
   parallel_for(ce - cb, [&](size_t b, size_t e) {
   for (size_t i = cb + b; i < cb + e; ++i) {
     const unsigned long long *a = &h->host_acc.p[i * dsi::NF];
     const CfgTicks &t = h->ticks[i];
-    dsi_result &r = out[i];
+    dsi_result &r = out[i - first];
     const uint64_t T = t.trials;
     const uint64_t si_cost = (uint64_t)(t.kd + t.t_t);
     // L_SI = I (k t_d + t_t) + e, e = SI's first-iteration surcharge (TTFT variant, else 0)
@@ -832,10 +832,71 @@ dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
   }
   });
   }
+  return DSI_OK;
+}
+
+}  // namespace
+
+dsi_status dsi_sim_reduce(dsi_sim *h, dsi_result *out, size_t n) {
+  if (!h) return DSI_E_NULL;
+  Trace tr("dsi_sim_reduce");
+  h->err.clear();
+  const bool root_only = (h->opt.flags & DSI_F_REDUCE_TO_ROOT) && h->opt.rank != 0;
+  if (!out && !root_only) return fail(h, DSI_E_NULL, "out is NULL");
+  const size_t n_cfg = h->n_cfg;
+  if (n != n_cfg) return fail(h, DSI_E_RANGE, "n must equal n_cfg");
+  if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_reduce before dsi_sim_run");
+  const bool hist = h->opt.flags & DSI_F_HIST;
+  dsi_status st = reduce_enqueue(h, hist);
+  if (st != DSI_OK) return st;
+  tr.mark("allreduce-enqueue");
+  if (root_only) {  // DSI_F_REDUCE_TO_ROOT: this rank contributed its sums; rank 0 checks and finalizes
+    st = sync_all(h);
+    if (st != DSI_OK) return st;
+    h->reduced = h->reduced_device = true;
+    return DSI_OK;
+  }
+  // every device now holds the global sums (or there is one device): read device 0
+  DeviceState &d0 = h->dev[0];
+  CUDA_TRY(h, cudaSetDevice(d0.ordinal));
+  if (hist) {
+    CUDA_TRY(h, cudaMemcpyAsync(h->host_seg.p, h->use_nccl ? d0.d_seg_red : d0.d_seg,
+                                n_cfg * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, d0.stream));
+    CUDA_TRY(h, cudaMemcpyAsync(h->host_si.p, h->use_nccl ? d0.d_si_red : d0.d_si,
+                                h->si_bins_total * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                d0.stream));
+  }
+  st = finalize_range(h, 0, n_cfg, out, tr);
+  if (st != DSI_OK) return st;
   CUDA_TRY(h, cudaStreamSynchronize(d0.stream));  // the histogram copies (HIST), if any
   tr.mark("finalize");
-  h->reduced = true;
+  h->reduced = h->reduced_device = true;
   return DSI_OK;
+}
+
+dsi_status dsi_sim_reduce_device(dsi_sim *h) {
+  if (!h) return DSI_E_NULL;
+  Trace tr("dsi_sim_reduce_device");
+  h->err.clear();
+  if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_reduce_device before dsi_sim_run");
+  if (h->opt.flags & DSI_F_HIST) return fail(h, DSI_E_STATE, "DSI_F_HIST needs dsi_sim_reduce");
+  const dsi_status st = reduce_enqueue(h, false);
+  if (st != DSI_OK) return st;
+  h->reduced_device = true;
+  return DSI_OK;
+}
+
+dsi_status dsi_sim_fetch(dsi_sim *h, size_t first, size_t count, dsi_result *out) {
+  if (!h) return DSI_E_NULL;
+  Trace tr("dsi_sim_fetch");
+  h->err.clear();
+  if (!out && count) return fail(h, DSI_E_NULL, "out is NULL");
+  if (first > h->n_cfg || count > h->n_cfg - first) return fail(h, DSI_E_RANGE, "[first, first + count) exceeds n_cfg");
+  if (!h->reduced_device) return fail(h, DSI_E_STATE, "dsi_sim_fetch before dsi_sim_reduce_device");
+  if ((h->opt.flags & DSI_F_REDUCE_TO_ROOT) && h->opt.rank != 0)
+    return fail(h, DSI_E_STATE, "DSI_F_REDUCE_TO_ROOT: results are on rank 0");
+  if (!count) return DSI_OK;
+  return finalize_range(h, first, count, out, tr);
 }
 
 dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size_t *n_cells) {
@@ -858,7 +919,7 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
   if (cap < nc) return fail(h, DSI_E_RANGE, "cap is smaller than the number of cells");
   if (!h->ran) return fail(h, DSI_E_STATE, "dsi_sim_heatmap before dsi_sim_run");
   const bool local = cells_aligned(h);
-  if (!local) {
+  if (!local && !h->reduced_device) {  // (dsi_sim_reduce_device already summed the moments)
     dsi_status st = sum_across(h, false);
     if (st != DSI_OK) return st;
   }

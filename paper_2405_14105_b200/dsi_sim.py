@@ -87,6 +87,8 @@ def _load(path: str):
         "dsi_sim_stream": ([V, i32, P(V)], ctypes.c_int),
         "dsi_sim_launches": ([V, P(i32)], ctypes.c_int),
         "dsi_sim_kernel_ms": ([V, i32, P(ctypes.c_float)], ctypes.c_int),
+        "dsi_sim_reduce_device": ([V], ctypes.c_int),
+        "dsi_sim_fetch": ([V, ctypes.c_size_t, ctypes.c_size_t, V], ctypes.c_int),
         "dsi_sim_units": ([V, P(u64), P(u64), P(u64)], ctypes.c_int),
         "dsi_sim_io_bytes": ([V, P(u64), P(u64)], ctypes.c_int),
         "dsi_sim_comm_info": ([V, P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)], ctypes.c_int),
@@ -170,7 +172,7 @@ def dsi_build_id() -> str:
     """SHA-256 of the sources the loaded product library was built from (dsi_build_id)."""
     return lib.dsi_build_id().decode()
 EXPORTED = ("dsi_sim_create", "dsi_sim_update", "dsi_sim_run", "dsi_sim_reduce", "dsi_sim_trials", "dsi_sim_hist",
-            "dsi_sim_stream", "dsi_sim_launches", "dsi_sim_kernel_ms", "dsi_sim_units", "dsi_sim_io_bytes",
+            "dsi_sim_stream", "dsi_sim_launches", "dsi_sim_kernel_ms", "dsi_sim_units", "dsi_sim_io_bytes", "dsi_sim_reduce_device", "dsi_sim_fetch",
             "dsi_sim_comm_info", "dsi_sim_destroy", "dsi_status_str", "dsi_sim_last_error", "dsi_last_create_error",
             "dsi_abi_version", "dsi_nccl_unique_id", "dsi_ticks", "dsi_min_lookahead",
             "dsi_required_processors", "dsi_eq1_feasible", "dsi_shard_bounds", "dsi_heatmap",
@@ -355,6 +357,18 @@ def dsi_sim_reduce(h, n: int, out: np.ndarray | None = None) -> np.ndarray:
     return out
 
 
+def dsi_sim_reduce_device(h) -> None:
+    _check(_L(h).dsi_sim_reduce_device(h), h)
+
+
+def dsi_sim_fetch(h, first: int, count: int, out: np.ndarray | None = None) -> np.ndarray:
+    if out is None:
+        out = np.zeros(count, RESULT_DTYPE)
+    assert out.dtype == RESULT_DTYPE and out.size >= count and out.flags["C_CONTIGUOUS"]
+    _check(_L(h).dsi_sim_fetch(h, first, count, out.ctypes.data), h)
+    return out[:count]
+
+
 def dsi_sim_heatmap(h, out: np.ndarray | None = None) -> np.ndarray:
     """On-device heatmap product after a run (every rank must call it)."""
     n = ctypes.c_size_t()
@@ -442,6 +456,13 @@ class Simulator:
     def reduce(self, out: np.ndarray | None = None) -> np.ndarray:
         """Per-config results; pass a preallocated RESULT_DTYPE array to reuse its pages."""
         return dsi_sim_reduce(self.h, self.n, out)
+
+    def reduce_device(self) -> "Simulator":
+        dsi_sim_reduce_device(self.h)
+        return self
+
+    def fetch(self, first: int = 0, count: int | None = None, out: np.ndarray | None = None) -> np.ndarray:
+        return dsi_sim_fetch(self.h, first, self.n - first if count is None else count, out)
 
     def trials(self, cfg: int, first: int = 0, count: int | None = None) -> dict:
         if count is None:
