@@ -583,6 +583,7 @@ def ours(args):
     # trial per group of configs drawing identical indicators; reported beside `value`
     # because it changes what a simulated trial-token costs.  Its sums must be bit-identical.
     crn = None
+    crn_exchange = None
     if not args.no_shared_streams:
         simc = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_SHARED_STREAMS | root, nccl_id=fresh_nccl_id(),
                            **base_kw)
@@ -621,6 +622,7 @@ def ours(args):
         heat_shared_s, cells_shared = heatmap_grid_times(simc, flush, args.steps)
         crn["e2e"], crn["e2e_all_results"] = fast_mode_e2e(simc, cfgs, resc, tt, args.steps, barrier,
                                                            max_over_ranks)
+        crn_exchange = simc.comm_info()["heatmap_exchange"]
         simc.close()
 
     # means-only mode (DSI_F_MEANS_ONLY): segment-length histograms per indicator group,
@@ -825,7 +827,7 @@ def ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches,
-            "comm": comm,
+            "comm": dict(sim.comm_info(), shared_streams_heatmap_exchange=crn_exchange),
             "heatmap": heat,
             "shared_streams": crn,
             "means_only": means,

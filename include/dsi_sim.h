@@ -255,8 +255,13 @@ DSI_API dsi_status dsi_sim_units(dsi_sim *h, uint64_t *first, uint64_t *count, u
  * communicator itself reports them (ncclCommCount / ncclCommUserRank), *transport 1 = NCCL,
  * 2 = the test build's host all-reduce hook, 0 = none (one rank: nothing to exchange, *nranks
  * = 1, *rank = 0).  Lets a caller check that a multi-process run formed one communicator of
- * the expected size. */
-DSI_API dsi_status dsi_sim_comm_info(dsi_sim *h, int32_t *nranks, int32_t *rank, int32_t *transport);
+ * the expected size.  *cell_local (may be NULL) = 1 when every heatmap cell's configs are
+ * simulated by one part (the shards are snapped to cell or group starts), so dsi_sim_heatmap
+ * evaluates each part's cells from its own moments and exchanges only the 64-byte cells; 0 when
+ * it all-reduces every config's moments first (the cells are planned on first use: query after
+ * a dsi_sim_heatmap call for the handle's final answer). */
+DSI_API dsi_status dsi_sim_comm_info(dsi_sim *h, int32_t *nranks, int32_t *rank, int32_t *transport,
+                                     int32_t *cell_local);
 
 DSI_API void dsi_sim_destroy(dsi_sim *h); /* NULL-safe */
 

@@ -114,8 +114,9 @@ dsi_status dsi_nccl_unique_id(uint8_t id[128]) {
   return DSI_OK;
 }
 
-dsi_status dsi_sim_comm_info(dsi_sim *h, int32_t *nranks, int32_t *rank, int32_t *transport) {
+dsi_status dsi_sim_comm_info(dsi_sim *h, int32_t *nranks, int32_t *rank, int32_t *transport, int32_t *cell_local) {
   if (!h || !nranks || !rank || !transport) return DSI_E_NULL;
+  if (cell_local) *cell_local = cells_aligned(h) ? 1 : 0;
   *nranks = 1;
   *rank = 0;
   *transport = 0;

@@ -140,6 +140,7 @@ struct HeatParams {
   const DevCfg *cfg;
   const unsigned long long *acc;  // n_cfg * NF global sums
   const HeatCell *cells;
+  const uint32_t *idx;  // NULL: cells [0, n_cells); else the n_cells cell indices to evaluate
   uint32_t n_cells;
   double tick;
   HeatOut *out;

@@ -147,6 +147,9 @@ struct DeviceState {
   unsigned long long *d_hist = nullptr;   // H | prefix of H | (TTFT) H1, hist_len each
   uint32_t *d_ttft_cfgs = nullptr;
   std::vector<std::pair<uint64_t, uint64_t>> cfg_ranges;  // means-only: configs evaluated here
+  std::vector<uint32_t> owned_cells;      // cell-local heatmap: the cells this device's parts own
+  uint32_t *d_owned = nullptr;            //   ... on the device
+  size_t owned_cap = 0;
 };
 
 struct dsi_sim {
@@ -173,6 +176,8 @@ struct dsi_sim {
   uint64_t hist_len = 0;
   std::vector<uint32_t> ttft_cfgs;        // means-only + TTFT: configs with a first-segment correction
   std::vector<uint64_t> cfg_bounds;       // means-only: parts' config ranges (all ranks), cell-aligned
+  std::vector<uint64_t> part_bounds;      // every part's unit range [b[p], b[p+1]) (all ranks)
+  bool cell_local = false;                // every heatmap cell's configs lie in one part (plan_cell_owners)
   bool use_nccl = false;                  // per-config moments summed across devices/ranks
   bool host_coll = false;                 // ... through the host all-reduce hook instead of NCCL
   std::vector<uint32_t> perm;
@@ -366,6 +371,8 @@ dsi_status plan_two_pass(dsi_sim *h);
 dsi_status alloc_two_pass(dsi_sim *h);
 dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost);
 void plan_heat_cells(dsi_sim *h);
+bool snap_bounds(std::vector<uint64_t> &bounds, const std::vector<double> &cost, const std::vector<uint64_t> &cand);
+void plan_cell_owners(dsi_sim *h);
 bool cells_aligned(const dsi_sim *h);
 
 }  // namespace dsih

@@ -2,6 +2,8 @@
 // shared-stream groups/slices/units (and the two-pass record plan), heatmap cells.
 #include "dsi_host.h"
 
+#include <algorithm>
+
 using namespace dsih;
 
 namespace dsih {
@@ -299,16 +301,86 @@ void plan_heat_cells(dsi_sim *h) {
     h->heat_cells[j].count = (uint32_t)((j + 1 < nc ? h->heat_cells[j + 1].first : n) - h->heat_cells[j].first);
 }
 
-// Means-only, one device per process: every part's config range starts at a cell, so each
-// part's cells can be evaluated from its own moments (no all-reduce of the moments).
-bool cells_aligned(const dsi_sim *h) {
-  if (!h->means_only || h->opt.n_devices != 1 || h->cfg_bounds.empty()) return false;
-  size_t ci = 0;
-  for (const uint64_t b : h->cfg_bounds) {
-    while (ci < h->heat_cells.size() && h->heat_cells[ci].first < b) ++ci;
-    if (b < h->n_cfg && (ci == h->heat_cells.size() || h->heat_cells[ci].first != b)) return false;
+// Snap the interior shard bounds to candidate unit indices (sorted) -- each to the candidate
+// nearest in cumulative cost -- if that raises the largest part's cost by at most 4%.  The
+// candidates are heatmap-cell starts (per-config mode) or group starts (shared-stream mode), so a
+// snapped part holds whole cells (SURVEY 8(e)'s cell-aligned option).  Returns whether it snapped.
+bool snap_bounds(std::vector<uint64_t> &bounds, const std::vector<double> &cost, const std::vector<uint64_t> &cand) {
+  const size_t parts = bounds.size() - 1, n = cost.size();
+  if (parts < 2 || cand.empty()) return parts < 2;
+  std::vector<double> pre(n + 1, 0.0);
+  for (size_t u = 0; u < n; ++u) pre[u + 1] = pre[u] + cost[u];
+  auto max_part = [&](const std::vector<uint64_t> &b) {
+    double m = 0.0;
+    for (size_t q = 0; q < parts; ++q) m = std::max(m, pre[b[q + 1]] - pre[b[q]]);
+    return m;
+  };
+  std::vector<uint64_t> nb(bounds);
+  for (size_t q = 1; q < parts; ++q) {
+    auto it = std::lower_bound(cand.begin(), cand.end(), bounds[q]);
+    uint64_t best = it == cand.end() ? n : *it;
+    if (it != cand.begin()) {
+      const uint64_t below = *(it - 1);
+      if (it == cand.end() || pre[bounds[q]] - pre[below] < pre[best] - pre[bounds[q]]) best = below;
+    }
+    nb[q] = std::max(best, nb[q - 1]);
   }
+  nb[parts] = n;
+  if (max_part(nb) > 1.04 * max_part(bounds)) return false;
+  bounds.swap(nb);
   return true;
 }
+
+// Which part owns each heatmap cell: the cell-local heatmap (dsi_sim_heatmap evaluates a part's
+// cells from that part's own moments and exchanges only the 64-byte cells) needs every config of
+// a cell simulated by one part.  Sets h->cell_local and each device's owned_cells.
+void plan_cell_owners(dsi_sim *h) {
+  h->cell_local = false;
+  for (auto &d : h->dev) d.owned_cells.clear();
+  if (h->dev.size() != 1) return;
+  const size_t n = h->n_cfg;
+  const std::vector<uint64_t> &pb = h->means_only ? h->cfg_bounds : h->part_bounds;
+  if (pb.size() < 2) return;
+  const int parts = (int)pb.size() - 1;
+  std::vector<int32_t> owner(n, -1);  // -2: split between parts
+  auto mark = [&](size_t c, int32_t q) {
+    int32_t &o = owner[c];
+    o = (o == -1 || o == q) ? q : -2;
+  };
+  if (h->means_only) {  // parts evaluate config ranges
+    for (int q = 0; q < parts; ++q)
+      for (uint64_t c = pb[q]; c < pb[q + 1]; ++c) owner[c] = q;
+  } else if (h->shared) {  // a unit touches every config of its slice
+    for (int q = 0; q < parts; ++q)
+      for (uint64_t u = pb[q]; u < pb[q + 1]; ++u) {
+        const dsi::CrnUnit &un = h->crn_units[u];
+        for (uint32_t i = un.begin; i < un.begin + un.count; ++i) mark(h->perm[i], q);
+      }
+  } else {  // config c's units [prefix[c], prefix[c+1])
+    for (size_t c = 0; c < n; ++c) {
+      if (h->prefix[c + 1] == h->prefix[c]) continue;
+      const int32_t q0 = (int32_t)(std::upper_bound(pb.begin(), pb.end(), h->prefix[c]) - pb.begin()) - 1;
+      const int32_t q1 = (int32_t)(std::upper_bound(pb.begin(), pb.end(), h->prefix[c + 1] - 1) - pb.begin()) - 1;
+      owner[c] = q0 == q1 ? q0 : -2;
+    }
+  }
+  const int per_rank = parts / std::max(1, h->opt.world);
+  const int lo = h->opt.rank * per_rank, hi = lo + per_rank;
+  std::vector<uint32_t> mine;
+  for (size_t j = 0; j < h->heat_cells.size(); ++j) {
+    const dsi::HeatCell &c = h->heat_cells[j];
+    const int32_t o = owner[c.first];
+    if (o < 0) return;
+    for (uint64_t i = c.first + 1; i < c.first + c.count; ++i)
+      if (owner[i] != o) return;
+    if (o >= lo && o < hi) mine.push_back((uint32_t)j);
+  }
+  h->dev[0].owned_cells.swap(mine);
+  h->cell_local = true;
+}
+
+// One device per process and every cell owned by one part: dsi_sim_heatmap evaluates this
+// process's cells from its own moments (no all-reduce of the moments).
+bool cells_aligned(const dsi_sim *h) { return h->cell_local && h->dev.size() == 1; }
 
 }  // namespace dsih

@@ -26,9 +26,10 @@ __device__ __forceinline__ bool better(double v, int k, double bv, int bk) {
 }
 
 __global__ void __launch_bounds__(256) dsi_heatmap_kernel(const HeatParams P) {
-  const uint32_t cell = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (cell >= P.n_cells) return;  // warp-uniform
+  if (slot >= P.n_cells) return;  // warp-uniform
+  const uint32_t cell = P.idx ? P.idx[slot] : slot;  // (cell-local heatmap: this rank's cells)
   const HeatCell c = P.cells[cell];
   double si_v = INFINITY, dsi_v = INFINITY;
   int si_k = 0x7fffffff, dsi_k = 0x7fffffff;

@@ -30,6 +30,7 @@ void free_device(DeviceState &d) {
   cudaFree(d.d_tiles);
   cudaFree(d.d_heat_cells);
   cudaFree(d.d_heat_out);
+  cudaFree(d.d_owned);
   cudaFree(d.d_heat_bad);
   cudaFree(d.d_seg_groups);
   cudaFree(d.d_seg_prefix);
@@ -253,6 +254,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   std::vector<uint64_t> bounds(parts + 1);
   {
     std::vector<double> cost;
+    std::vector<uint64_t> cand;  // unit indices a part may start at and still hold whole heatmap cells
     try {
       cost.resize(h->total_units);
     } catch (...) {
@@ -271,6 +273,31 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       }
     }
     dsi_shard_bounds(cost.data(), h->total_units, parts, bounds.data());
+    // SURVEY 8(e)'s cell-aligned option: parts snapped to heatmap-cell starts (per-config mode:
+    // the first unit of each cell) or group starts (shared-stream mode, units in group order: a
+    // cell's configs are all in one group) when that costs <= 4% balance; dsi_sim_heatmap then
+    // exchanges the cells instead of every config's moments (means-only snaps its config ranges
+    // below)
+    if (parts > 1 && !means_only) {
+      try {
+        plan_heat_cells(h);
+        h->heat_planned = true;
+        if (shared) {
+          bool ordered = true;
+          for (size_t u = 1; u < h->crn_units.size() && ordered; ++u)
+            ordered = h->crn_units[u].group >= h->crn_units[u - 1].group;
+          for (size_t u = 0; ordered && u < h->crn_units.size(); ++u)
+            if (u == 0 || h->crn_units[u].group != h->crn_units[u - 1].group) cand.push_back(u);
+        } else {
+          for (const dsi::HeatCell &c : h->heat_cells) cand.push_back(h->prefix[c.first]);
+        }
+        snap_bounds(bounds, cost, cand);
+      } catch (...) {
+        h->err = "host tables";
+        return abort_create(DSI_E_NOMEM);
+      }
+    }
+    h->part_bounds = bounds;
   }
   tr.mark("plan+shard");
 
@@ -391,6 +418,14 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     }
   }
   tr.mark("devices");
+  if (h->heat_planned) {
+    try {
+      plan_cell_owners(h);
+    } catch (...) {
+      h->err = "host tables";
+      return abort_create(DSI_E_NOMEM);
+    }
+  }
   if (shared) {
     s = plan_two_pass(h);
     if (s == DSI_OK) s = alloc_two_pass(h);
@@ -907,6 +942,7 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
   if (!h->heat_planned) {  // cells: maximal runs of equal (t_target, t_drafter, a, SP, N)
     try {
       plan_heat_cells(h);
+      plan_cell_owners(h);
     } catch (...) {
       return fail(h, DSI_E_NOMEM, "host tables");
     }
@@ -938,7 +974,18 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
     if (!d0.d_heat_bad) CUDA_TRY(h, cudaMalloc((void **)&d0.d_heat_bad, sizeof(unsigned int)));
     CUDA_TRY(h, cudaMemcpyAsync(d0.d_heat_cells, h->heat_cells.data(), nc * sizeof(dsi::HeatCell),
                                 cudaMemcpyHostToDevice, d0.stream));
-    CUDA_TRY(h, cudaStreamSynchronize(d0.stream));  // the vector is pageable
+    const size_t no = d0.owned_cells.size();
+    if (no > d0.owned_cap) {
+      cudaFree(d0.d_owned);
+      d0.d_owned = nullptr;
+      d0.owned_cap = 0;
+      CUDA_TRY(h, cudaMalloc((void **)&d0.d_owned, no * sizeof(uint32_t)));
+      d0.owned_cap = no;
+    }
+    if (no)
+      CUDA_TRY(h, cudaMemcpyAsync(d0.d_owned, d0.owned_cells.data(), no * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                  d0.stream));
+    CUDA_TRY(h, cudaStreamSynchronize(d0.stream));  // the vectors are pageable
     h->heat_uploaded = true;
   }
   CUDA_TRY(h, cudaMemsetAsync(d0.d_heat_bad, 0, sizeof(unsigned int), d0.stream));
@@ -959,17 +1006,10 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
     // ranks) one all-reduce of the 64-byte cell records, zero where another rank owns the cell
     p.acc = d0.d_acc;
     if (h->use_nccl) CUDA_TRY(h, cudaMemsetAsync(d0.d_heat_out, 0, nc * sizeof(dsi::HeatOut), d0.stream));
-    for (const auto &cr : d0.cfg_ranges) {
-      const auto lo = std::lower_bound(h->heat_cells.begin(), h->heat_cells.end(), cr.first,
-                                       [](const dsi::HeatCell &c, uint64_t v) { return c.first < v; });
-      const auto hi = std::lower_bound(h->heat_cells.begin(), h->heat_cells.end(), cr.second,
-                                       [](const dsi::HeatCell &c, uint64_t v) { return c.first < v; });
-      if (hi <= lo) continue;
-      dsi::HeatParams q = p;
-      q.cells = d0.d_heat_cells + (lo - h->heat_cells.begin());
-      q.out = d0.d_heat_out + (lo - h->heat_cells.begin());
-      q.n_cells = (uint32_t)(hi - lo);
-      const int e = dsi::launch_heatmap_kernel(q, d0.stream);
+    p.idx = d0.d_owned;
+    p.n_cells = (uint32_t)d0.owned_cells.size();
+    if (p.n_cells) {
+      const int e = dsi::launch_heatmap_kernel(p, d0.stream);
       if (e) return cuda_fail(h, (cudaError_t)e, "heatmap kernel launch");
       h->launches += 1;
     }

@@ -91,7 +91,8 @@ def _load(path: str):
         "dsi_sim_fetch": ([V, ctypes.c_size_t, ctypes.c_size_t, V], ctypes.c_int),
         "dsi_sim_units": ([V, P(u64), P(u64), P(u64)], ctypes.c_int),
         "dsi_sim_io_bytes": ([V, P(u64), P(u64)], ctypes.c_int),
-        "dsi_sim_comm_info": ([V, P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)], ctypes.c_int),
+        "dsi_sim_comm_info": ([V, P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32), P(ctypes.c_int32)],
+                              ctypes.c_int),
         "dsi_sim_destroy": ([V], None),
         "dsi_status_str": ([ctypes.c_int], ctypes.c_char_p),
         "dsi_sim_last_error": ([V], ctypes.c_char_p),
@@ -419,9 +420,10 @@ def dsi_sim_units(h) -> tuple:
 
 def dsi_sim_comm_info(h) -> dict:
     """The handle's cross-rank exchange as the communicator reports it (transport: none, nccl, host)."""
-    n, r, t = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
-    _check(_L(h).dsi_sim_comm_info(h, ctypes.byref(n), ctypes.byref(r), ctypes.byref(t)), h)
-    return {"nranks": n.value, "rank": r.value, "transport": ("none", "nccl", "host")[t.value]}
+    n, r, t, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(_L(h).dsi_sim_comm_info(h, ctypes.byref(n), ctypes.byref(r), ctypes.byref(t), ctypes.byref(c)), h)
+    return {"nranks": n.value, "rank": r.value, "transport": ("none", "nccl", "host")[t.value],
+            "heatmap_exchange": "cells" if c.value else "moments"}
 
 
 def dsi_sim_io_bytes(h) -> tuple:

@@ -30,7 +30,7 @@ def test_bench_json_line_small_workload():
     assert d["means_only"]["sums_and_means_identical_to_value_run"] is True
     assert d["multi_drafter"]["value"] > 0 and 0 < d["multi_drafter"]["roofline"]["frac"] <= 1.0
     assert 0 < d["roofline"]["fmaheavy"]["frac"] <= 1.0 and d["roofline"]["unit"] == "Ginstr/s"
-    assert d["comm"] == {"nranks": 1, "rank": 0, "transport": "none"}
+    assert (d["comm"]["nranks"], d["comm"]["rank"], d["comm"]["transport"]) == (1, 0, "none")
     fv = d["heatmap"]["fresh_verifier"]
     assert fv["shared_streams_bit_identical"] is True and fv["means_only_bit_identical"] is True
     assert fv["identical_to_default_where_k_td_le_tt"] is True
@@ -58,7 +58,9 @@ def test_bench_two_ranks_on_one_gpu():
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dp2" and d["value"] > 0
-    assert d["comm"] == {"nranks": 2, "rank": 0, "transport": "host"}
+    assert (d["comm"]["nranks"], d["comm"]["rank"], d["comm"]["transport"]) == (2, 0, "host")
+    # cfg2's 10 cells cannot be split in two within the 4% balance bound: the moments are exchanged
+    assert d["comm"]["heatmap_exchange"] in ("cells", "moments")
     assert d["heatmap"]["fresh_verifier"]["shared_streams_bit_identical"] is True
     assert d["heatmap"]["device_cells_equal_host_product"] is True
     assert d["shared_streams"]["bit_identical_to_value_run"] is True
