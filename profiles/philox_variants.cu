@@ -79,6 +79,12 @@ __device__ __forceinline__ uint32_t pack4(uint32_t rej, const uint4 &u, uint32_t
     rej = __funnelshift_l((u.y >> 1) - t, rej, 1);
     return __funnelshift_l((u.x >> 1) - t, rej, 1);
   }
+  if (P == 4) {  // NOT a Bernoulli pack: the cheapest dependent fold (one LOP3 per call) -- an upper
+                 // bound on what any pack could gain over the carry chain
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(u.x), "r"(u.y), "r"(u.z ^ u.w));
+    return (rej << 1) ^ r;
+  }
   // P == 3: exact for any thr, x and y on the ALU (borrow = MSB of maj(~u, thr, d), d = u - thr),
   // z and w by the carry chain (builds the REJECT mask like P == 0)
   asm("{\n\t.reg .u32 t;\n\t"
@@ -212,6 +218,7 @@ int main() {
   run<false, false, 2>("W W, sign-funnel pack (even threshold)", K, ref, sms);
   run<false, false, 3>("W W, 2 carry + 2 borrow-funnel bits (exact)", K, ref, sms);
   run<false, false, 1>("W W, compare pack", K, ref, sms);
+  run<false, false, 4>("W W, xor fold (upper bound: not a Bernoulli pack)", K, 0, sms);
   if (getenv("PV_ALL")) {
     run<false, true, 0>("W D, carry pack", K, ref, sms);
     run<true, false, 0>("D W, carry pack", K, ref, sms);
