@@ -81,6 +81,9 @@ def _load():
         lib.oracle_trial.argtypes = [P(_Config), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
                                      P(_TrialOut), ctypes.c_void_p, ctypes.c_void_p]
         lib.oracle_trial.restype = ctypes.c_int
+        lib.oracle_trace_trial.argtypes = [P(_Config), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                           P(_TrialOut), ctypes.c_char_p, ctypes.c_size_t, P(ctypes.c_size_t)]
+        lib.oracle_trace_trial.restype = ctypes.c_int
         lib.oracle_run.argtypes = [P(_Config), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                    ctypes.c_int, P(_Sums)] + [ctypes.c_void_p] * 7
         lib.oracle_run.restype = ctypes.c_int
@@ -146,6 +149,33 @@ def trial(cfg: Config, seed: int, index: int, pattern: bool = False, hist: bool 
     if hist:
         d["si_hist"], d["seg_hist"] = si_hist, seg_hist
     return d
+
+
+# The documented total order of trace events (SPEC S:178 asks for one): time, then segment (a
+# rejection at t ends segment s before segment s+1 starts at t), then kind in this order --
+# releases before claims at equal times (R8) -- then position and thread
+TRACE_KINDS = ("SegmentStart", "DraftDone", "VerifyDone", "ServerFreed", "Accept", "Reject", "TokenEmitted",
+               "VerifyQueued", "VerifyDispatch", "FreshDispatch")
+
+
+def trace(cfg: Config, seed: int, index: int, pattern: bool = False, cap: int = 1 << 22) -> tuple:
+    """One trial's DSI event trace (Fig. 1-style timeline; debug output):
+    (trial record as trial(), events in TRACE_KINDS' total order).  Times in
+    ticks; thread -1 = no verification thread (drafts, fresh forwards, segment starts)."""
+    import json
+
+    lib = _load()
+    out = _TrialOut()
+    buf = ctypes.create_string_buffer(cap)
+    n = ctypes.c_size_t()
+    rc = lib.oracle_trace_trial(ctypes.byref(cfg._c()), seed, index, int(pattern), ctypes.byref(out), buf, cap,
+                                ctypes.byref(n))
+    if rc:
+        raise ValueError(f"oracle_trace_trial failed ({rc}) for {cfg}")
+    events = [json.loads(ln) for ln in buf.raw[:n.value].decode().splitlines()]
+    order = {k: i for i, k in enumerate(TRACE_KINDS)}
+    events.sort(key=lambda e: (e["time"], e["segment"], order[e["kind"]], e["position"], e["thread"]))
+    return {f: getattr(out, f) for f, _ in _TrialOut._fields_}, events
 
 
 def run(cfg: Config, seed: int, first: int = 0, count: int = 1, pattern: bool = False,

@@ -11,6 +11,7 @@
  */
 #include "dsi_oracle.h"
 
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -284,6 +285,29 @@ static int64_t time_get(const timeset *f, int64_t i) { return (size_t)i < f->cap
 /* last draft done by tau) at tau + t_t.  A newer fresh forward supersedes an */
 /* older one (which no longer covers p+1); a rejection cancels it like every  */
 /* other thread.                                                              */
+/* Optional event trace (oracle_trace_trial; SPEC S:177-180 TraceEvent, SURVEY 8(c).2 "optional
+   debug outputs"): one JSON object per line appended to a caller buffer, in processing order
+   (the caller sorts by time).  NULL outside oracle_trace_trial. */
+typedef struct {
+  char *buf;
+  size_t cap, len;
+  int overflow;
+} trace_sink;
+static trace_sink *g_trace = NULL;
+
+static void trace_ev(const char *kind, int64_t t, int64_t pos, int64_t thread, int64_t seg) {
+  int n;
+  if (!g_trace) return;
+  n = snprintf(g_trace->buf + g_trace->len, g_trace->cap - g_trace->len,
+               "{\"kind\": \"%s\", \"time\": %lld, \"position\": %lld, \"thread\": %lld, \"segment\": %lld}\n",
+               kind, (long long)t, (long long)pos, (long long)thread, (long long)seg);
+  if (n < 0 || (size_t)n >= g_trace->cap - g_trace->len) {
+    g_trace->overflow = 1;
+    return;
+  }
+  g_trace->len += (size_t)n;
+}
+
 static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_t SP, int64_t t_t,
                          int64_t t_d, int64_t t_t1, int64_t t_d1, int fresh, oracle_trial_out *out) {
   heap h = {0, 0, 0};
@@ -317,6 +341,7 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
     if (ends.v) memset(ends.v, 0, ends.cap * sizeof(int64_t));
 
     h.n = 0; /* cancellation: every pending thread, task and draft is dropped */
+    trace_ev("SegmentStart", T, c + 1, -1, segments);
     if (heap_push(&h, (event){T, EV_REQUEST, 0, epoch})) goto done;
 
     while (!restarted) {
@@ -336,10 +361,12 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
           busy += 1;
           forwards += 1;
           if (busy > peak_busy) peak_busy = busy;
+          trace_ev("VerifyDispatch", e.time, e.b == 0 ? c + 1 : c + e.b * (int64_t)k + 1, e.b, segments);
           const int64_t service = (segments == 1 && e.b == 0) ? t_t1 : t_t;
           if (heap_push(&h, (event){e.time + service, EV_TARGET_DONE, e.b, epoch})) goto done;
           if (fresh && time_set(&ends, e.b, e.time + service)) goto done;
         } else {
+          trace_ev("VerifyQueued", e.time, c + e.b * (int64_t)k + 1, e.b, segments);
           if (fifo_push(&q, e.b)) goto done;
           if ((int32_t)(q.tail - q.head) > max_queue) max_queue = (int32_t)(q.tail - q.head);
         }
@@ -352,6 +379,7 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
         if (time_get(&ends, bb) && time_get(&ends, bb) <= e.time + t_t) continue;
         if (f_live && !f_done && f_lo <= r && r <= f_hi && f_end <= e.time + t_t) continue;
         d = c + (e.time - T) / t_d; /* the last draft done by now */
+        trace_ev("FreshDispatch", e.time, r, -1, segments);
         f_live = 1;
         f_done = 0;
         f_lo = r;
@@ -372,8 +400,11 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
         if (!(ttft && segments == 1) && e.b != n_fin) goto done;
         n_fin += 1;
         busy -= 1;
+        trace_ev("VerifyDone", e.time, e.b == 0 ? c + 1 : c + e.b * (int64_t)k + 1, e.b, segments);
+        trace_ev("ServerFreed", e.time, -1, e.b, segments);
         if (q.head < q.tail) { /* FIFO: the head of the queue starts now */
           int64_t nb = q.v[q.head++];
+          trace_ev("VerifyDispatch", e.time, c + nb * (int64_t)k + 1, nb, segments);
           busy += 1;
           forwards += 1;
           if (busy > peak_busy) peak_busy = busy;
@@ -393,18 +424,24 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
           hi = (bb == 0) ? c + 1 : c + bb * (int64_t)k + 1;
           for (p = r; p <= hi; p++) {
             if (p == N) { /* the N-th token is committed: L_DSI */
+              trace_ev("TokenEmitted", e.time, p, bb, segments);
               out->dsi = e.time;
               rc = 0;
               goto done;
             }
             /* assertion: the draft of position p exists by now (t_d <= t_t, t_d1 <= t_t1) */
             if (T + lag + (p - c) * t_d > e.time) goto done;
+            trace_ev("DraftDone", T + lag + (p - c) * t_d, p, -1, segments);
             if (indicator(s, p) == 0) { /* rejection: restart from the target's token */
+              trace_ev("Reject", e.time, p, bb, segments);
+              trace_ev("TokenEmitted", e.time, p, bb, segments);
               T = e.time;
               c = p;
               restarted = 1;
               break;
             }
+            trace_ev("Accept", e.time, p, bb, segments);
+            trace_ev("TokenEmitted", e.time, p, bb, segments);
           }
           if (!restarted) r = hi + 1;
         }
@@ -417,17 +454,23 @@ static int dsi_event_sim(const indicator_stream *s, int32_t N, int32_t k, int32_
           const int64_t bb = (j == 1) ? 0 : (j - 1 + k - 1) / k;
           if (!flag_get(&fin, bb) && !(f_live && f_done && f_lo <= r && r <= f_hi)) break;
           if (r == N) {
+            trace_ev("TokenEmitted", e.time, r, bb, segments);
             out->dsi = e.time;
             rc = 0;
             goto done;
           }
           if (T + (r - c) * t_d > e.time) goto done; /* the draft exists (t_d <= t_t) */
+          trace_ev("DraftDone", T + (r - c) * t_d, r, -1, segments);
           if (indicator(s, r) == 0) {
+            trace_ev("Reject", e.time, r, bb, segments);
+            trace_ev("TokenEmitted", e.time, r, bb, segments);
             T = e.time;
             c = r;
             restarted = 1;
             break;
           }
+          trace_ev("Accept", e.time, r, bb, segments);
+          trace_ev("TokenEmitted", e.time, r, bb, segments);
           r += 1;
         }
         if (!restarted && r != r_before)
@@ -503,6 +546,21 @@ int oracle_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pa
   }
   if (out->dsi_segments != out->m) return -1;
   return 0;
+}
+
+/* One trial with its DSI event trace written to buf (JSON lines, NUL-terminated); *len = bytes
+   written.  Returns oracle_trial's code, or -2 if buf is too small. */
+int oracle_trace_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pattern,
+                       oracle_trial_out *out, char *buf, size_t cap, size_t *len) {
+  trace_sink t = {buf, cap, 0, 0};
+  int rc;
+  if (!buf || cap == 0 || !len) return -1;
+  buf[0] = 0;
+  g_trace = &t;
+  rc = oracle_trial(cfg, seed, trial, pattern, out, NULL, NULL);
+  g_trace = NULL;
+  *len = t.len;
+  return t.overflow ? -2 : rc;
 }
 
 int oracle_run(const oracle_config *cfg, uint64_t seed, uint64_t first, uint64_t count,

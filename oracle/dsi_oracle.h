@@ -21,6 +21,7 @@
  */
 #ifndef DSI_ORACLE_H
 #define DSI_ORACLE_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -83,6 +84,13 @@ uint64_t oracle_threshold(double a);
  * Returns 0, or -1 on invalid input / internal assertion failure. */
 int oracle_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pattern,
                  oracle_trial_out *out, int64_t *si_hist, int64_t *seg_hist);
+
+/* oracle_trial with the DSI event simulation's trace: one JSON object per line, kinds
+   SegmentStart, VerifyDispatch, VerifyQueued, VerifyDone, ServerFreed, FreshDispatch, DraftDone,
+   Accept, Reject, TokenEmitted (time in ticks, position, verification thread, segment), in
+   processing order.  Debug output only; -2 when cap is too small. */
+int oracle_trace_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pattern,
+                       oracle_trial_out *out, char *buf, size_t cap, size_t *len);
 
 /* Trials first..first+count-1: optional per-trial arrays (may be NULL),
  * sums accumulated into *sums (zero it first).  Returns 0 or -1. */

@@ -119,8 +119,9 @@ try:
 except OSError as e:
     out["dram_error"] = str(e)
 try:
-    out["set_full_stride20"], out["instruction_mix_stride20"] = full()
-    out["source_hotspots_stride20"] = hotspots(os.path.join(OUT, f"prof_{R}.ncu-rep"))
+    # --set full over one full bench launch (cfg3, every config; profiles/profile_round.sh)
+    out["set_full"], out["instruction_mix"] = full()
+    out["source_hotspots"] = hotspots(os.path.join(OUT, f"prof_{R}.ncu-rep"))
 except (OSError, ValueError, IndexError) as e:
     out["full_error"] = str(e)
 try:  # the shared-stream kernel on the full cfg3 grid (profiles/profile_round.sh)
