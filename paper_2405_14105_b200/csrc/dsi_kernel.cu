@@ -341,25 +341,27 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
 
     const int m = nz + 1;
     int iters = m + (int)ai;
-    // ay is a sum of signed 32-bit terms (fresh savings may exceed S(b) - S(1)) with
-    // |sum| <= N k t_d < 2^31 (create's overflow bound): read it as int32
-    int64_t dsi = (int64_t)m * cfg.t_t + (int64_t)n2 * cfg.s1 + (int64_t)(int32_t)ay;
+    // Every per-trial latency is < 2^31 ticks (create's overflow bound), so L_DSI and L_SI are
+    // formed in 32-bit modular arithmetic -- exact, whatever the partial sums -- and squared with one
+    // 32x32->64 multiply each.  (ay is a sum of signed 32-bit terms: fresh savings may exceed
+    // S(b) - S(1).)
+    uint32_t dsi = (uint32_t)m * (uint32_t)cfg.t_t + (uint32_t)n2 * (uint32_t)cfg.s1 + ay;
     if (fast1) {  // the final segment ends at N
       odd += (int)(((uint32_t)N & 1u) ^ lzp);
       iters = (N + odd) >> 1;
-      dsi = (int64_t)m * cfg.t_t + (int64_t)(N - m) * cfg.kd;
+      dsi = (uint32_t)m * (uint32_t)cfg.t_t + (uint32_t)(N - m) * (uint32_t)cfg.kd;
     }
-    int64_t si = (int64_t)iters * cfg.si_cost;
+    uint32_t si = (uint32_t)iters * (uint32_t)cfg.si_cost;
     if (ttft) {  // first forwards: SI's first iteration and DSI's first segment
-      dsi += D1[g1 ? g1 : N];
-      si += cfg.e_si;
+      dsi += (uint32_t)D1[g1 ? g1 : N];
+      si += (uint32_t)cfg.e_si;
     }
     a_m += (unsigned)m;
     a_i += (unsigned)iters;
-    a_i2 += (unsigned long long)iters * (unsigned long long)iters;
-    a_dsi += (unsigned long long)dsi;
-    a_dsi2 += (unsigned long long)dsi * (unsigned long long)dsi;
-    a_gtn += dsi > nonsi;
+    a_i2 += (unsigned long long)((uint32_t)iters * (uint32_t)iters);  // I <= N: I^2 < 2^32
+    a_dsi += dsi;
+    a_dsi2 += (unsigned long long)dsi * dsi;
+    a_gtn += dsi > (uint32_t)nonsi;
     a_gts += dsi > si;
     a_trials += 1;
     if (PER_TRIAL) {
