@@ -357,12 +357,18 @@ inline void parallel_for(size_t n, Fn fn, size_t min_parallel = (1u << 15)) {
   pool.run((uint32_t)chunks, job);
 }
 
+// What an update keeps (validate_all with prev): the shared-stream plan's keys (stream, a, N, T, k,
+// t_t, t_d, SP), the means-only groups' keys (stream, a, N, T, TTFT or not), the heatmap cells' keys
+// (t_target, t_drafter, a as given, SP, N).
+struct UpdateKeys {
+  bool plan_same = false, groups_same = false, cells_same = false;
+};
 dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n, std::vector<CfgTicks> &out,
-                        const std::vector<CfgTicks> *prev = nullptr);
-void fill_dev_cfg(dsi_sim *h);
+                        const std::vector<CfgTicks> *prev = nullptr, UpdateKeys *keys = nullptr);
+cudaError_t fill_dev_cfg(dsi_sim *h, bool upload_chunks = false);
 void free_device(DeviceState &d);
 void free_handle(dsi_sim *h);
-dsi_status upload(dsi_sim *h, bool plan = true);
+dsi_status upload(dsi_sim *h, bool plan = true, bool cfg_table = true);
 dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_units);
 dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks);
 bool same_plan_keys(const std::vector<CfgTicks> &a, const std::vector<CfgTicks> &b);

@@ -8,14 +8,17 @@ using namespace dsih;
 
 namespace dsih {
 
-// Fill the pinned device-config staging table from h->ticks.
-void fill_dev_cfg(dsi_sim *h) {
+// Fill the pinned device-config staging table from h->ticks.  upload_chunks (dsi_sim_update,
+// after validation succeeded and the streams are idle): the table is filled in kSlices slices and
+// each slice's H2D copy is enqueued on every device's stream as soon as it is filled, so the DMA
+// overlaps the filling of the rest.  Returns the first CUDA error of those copies.
+cudaError_t fill_dev_cfg(dsi_sim *h, bool upload_chunks) {
   const bool pattern = h->opt.flags & DSI_F_PATTERN;
   const bool fresh = h->opt.flags & DSI_F_FRESH_VERIFIER;
   const size_t n = h->n_cfg;
   // prefix offsets (per-trial records, SI-histogram bins) in two passes over fixed chunks
-  constexpr size_t K = 64;
-  uint64_t rec[K + 1] = {}, sib[K + 1] = {};
+  constexpr size_t K = 256, kSlices = 8;
+  std::vector<uint64_t> rec(K + 1, 0), sib(K + 1, 0);
   parallel_for(K, [&](size_t b, size_t e) {
     for (size_t c = b; c < e; ++c) {
       uint64_t r = 0, q = 0;  // in registers: the neighbouring chunks' sums share cache lines
@@ -31,19 +34,34 @@ void fill_dev_cfg(dsi_sim *h) {
     rec[c + 1] += rec[c];
     sib[c + 1] += sib[c];
   }
-  parallel_for(K, [&](size_t b, size_t e) {
-    for (size_t c = b; c < e; ++c) {
-      uint64_t r = rec[c], q = sib[c];
-      for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) {
-        DevCfg &d = h->dev_cfg.p[i];
-        d = make_dev_cfg(h->ticks[i], pattern, fresh);
-        d.rec_off = r;
-        r += h->ticks[i].trials;
-        d.si_hist_off = (uint32_t)q;
-        q += (uint64_t)d.k_eff + 1;
+  for (size_t sl = 0; sl < kSlices; ++sl) {
+    const size_t c0 = K * sl / kSlices, c1 = K * (sl + 1) / kSlices;
+    parallel_for(c1 - c0, [&](size_t b, size_t e) {
+      for (size_t c = c0 + b; c < c0 + e; ++c) {
+        uint64_t r = rec[c], q = sib[c];
+        for (size_t i = n * c / K; i < n * (c + 1) / K; ++i) {
+          DevCfg &d = h->dev_cfg.p[i];
+          d = make_dev_cfg(h->ticks[i], pattern, fresh);
+          d.rec_off = r;
+          r += h->ticks[i].trials;
+          d.si_hist_off = (uint32_t)q;
+          q += (uint64_t)d.k_eff + 1;
+        }
+      }
+    }, 1);
+    if (upload_chunks) {
+      const size_t i0 = n * c0 / K, i1 = n * c1 / K;
+      for (auto &d : h->dev) {
+        if (i1 <= i0) continue;
+        cudaError_t e = cudaSetDevice(d.ordinal);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(d.d_cfg + i0, h->dev_cfg.p + i0, (i1 - i0) * sizeof(DevCfg), cudaMemcpyHostToDevice,
+                              d.stream);
+        if (e != cudaSuccess) return e;
       }
     }
-  }, 1);
+  }
+  return cudaSuccess;
 }
 
 // Shared-stream plan: group configs by (stream_id, threshold, N, n_trials) -- equal keys

@@ -57,11 +57,12 @@ void free_handle(dsi_sim *h) {
 }
 
 // Upload the staging table to every device (async on each device's stream).
-dsi_status upload(dsi_sim *h, bool plan) {
+dsi_status upload(dsi_sim *h, bool plan, bool cfg_table) {
   for (auto &d : h->dev) {
     CUDA_TRY(h, cudaSetDevice(d.ordinal));
-    CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg, h->dev_cfg.p, h->n_cfg * sizeof(DevCfg),
-                                cudaMemcpyHostToDevice, d.stream));
+    if (cfg_table)
+      CUDA_TRY(h, cudaMemcpyAsync(d.d_cfg, h->dev_cfg.p, h->n_cfg * sizeof(DevCfg), cudaMemcpyHostToDevice,
+                                  d.stream));
     if (h->means_only && plan) {
       CUDA_TRY(h, cudaMemcpyAsync(d.d_seg_groups, h->seg_groups.data(), h->seg_groups.size() * sizeof(dsi::SegGroup),
                                   cudaMemcpyHostToDevice, d.stream));
@@ -194,6 +195,9 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   h->block_threads = shared ? kCrnThreads : (opt->block_threads ? opt->block_threads : kDefaultThreads);
   try {
     h->ticks.resize(n_cfg);
+    // dsi_sim_update validates into this spare table: allocated (and its pages touched by the
+    // zero fill) here, so the first update does not pay ~0.1 s of page faults for 2.02e6 configs
+    h->ticks_next.resize(n_cfg);
     h->prefix.resize(n_cfg + 1);
   } catch (...) {
     h->err = "host tables";
@@ -480,21 +484,13 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   }
   const int32_t old_n = h->max_n, old_keff = h->max_keff;
   const bool old_ttft = h->any_ttft, old_fresh = h->any_fresh;
-  dsi_status s = validate_all(h, cfg, n_cfg, h->ticks_next, &h->ticks);
+  UpdateKeys keys;
+  dsi_status s = validate_all(h, cfg, n_cfg, h->ticks_next, &h->ticks, &keys);
   tr.mark("validate");
   if (s == DSI_OK) s = derive_limits(h, h->ticks_next);  // the new configs may need a larger launch shape
   if (s != DSI_OK) return s;                              // derive_limits only commits on success
   if (h->means_only) {  // the histogram groups are fixed at create: their keys must not change
-    std::atomic<bool> keys_same{h->max_n <= kMeansMaxN};
-    parallel_for(n_cfg, [&](size_t lo, size_t hi) {
-      for (size_t i = lo; i < hi && keys_same.load(std::memory_order_relaxed); ++i) {
-        const CfgTicks &a = h->ticks[i], &b = h->ticks_next[i];
-        const bool ta = a.t_t1 != a.t_t || a.t_d1 != a.t_d, tb = b.t_t1 != b.t_t || b.t_d1 != b.t_d;
-        if (!(a.stream_id == b.stream_id && a.thr == b.thr && a.n == b.n && a.trials == b.trials && ta == tb))
-          keys_same = false;
-      }
-    });
-    const bool same = keys_same;
+    const bool same = h->max_n <= kMeansMaxN && keys.groups_same;
     if (!same) {
       h->max_n = old_n;
       h->max_keff = old_keff;
@@ -505,7 +501,7 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
                   "create a new handle");
     }
   }
-  const bool replan = h->shared && !same_plan_keys(h->ticks, h->ticks_next);
+  const bool replan = h->shared && !keys.plan_same;
   tr.mark("limits");
   if (replan) {
     // re-plan on the host first: the unit table's size is fixed at create
@@ -561,11 +557,12 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     CUDA_TRY(h, cudaStreamSynchronize(d.stream));
   }
   tr.mark(replan ? "replan+sync" : "sync");
-  fill_dev_cfg(h);
-  tr.mark("fill");
+  // the staging table is filled in slices, each slice's DMA enqueued as soon as it is filled
+  CUDA_TRY(h, fill_dev_cfg(h, /*upload_chunks=*/true));
+  tr.mark("fill+upload");
   h->ran = h->reduced = h->reduced_device = false;
-  h->heat_planned = h->heat_uploaded = false;
-  const dsi_status su = upload(h, replan);
+  if (!keys.cells_same || replan) h->heat_planned = h->heat_uploaded = false;  // else the cells stand
+  const dsi_status su = upload(h, replan, /*cfg_table=*/false);
   tr.mark("upload");
   return su;
 }

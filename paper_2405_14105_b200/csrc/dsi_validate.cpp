@@ -2,6 +2,8 @@
 // config rows, launch limits and the Eq. 1 planner helpers.
 #include "dsi_host.h"
 
+#include <atomic>
+
 using namespace dsih;
 
 namespace dsih {
@@ -163,13 +165,17 @@ double unit_cost(const CfgTicks &t, uint64_t trials) {
 // `prev` (dsi_sim_update), also checks what an update must keep: n_trials, and with
 // DSI_F_HIST min(k, N) (the histogram layout).
 dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n, std::vector<CfgTicks> &out,
-                        const std::vector<CfgTicks> *prev) {
+                        const std::vector<CfgTicks> *prev, UpdateKeys *keys) {
   std::mutex mu;
   size_t bad = n;
   dsi_status bad_s = DSI_OK;
   std::string bad_msg;
   const bool hist = h->opt.flags & DSI_F_HIST;
+  // (update) which plans survive, compared in the same pass: the shared-stream plan's keys, the
+  // means-only groups' keys and the heatmap cells' keys
+  std::atomic<bool> plan_same{true}, groups_same{true}, cells_same{true};
   parallel_for(n, [&](size_t b, size_t e) {
+    bool ps = true, gs = true, cs = true;
     for (size_t i = b; i < e; ++i) {
       std::string msg;
       dsi_status s = convert(h->opt, cfg[i], i, out[i], msg);
@@ -179,6 +185,11 @@ dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n, std::vector
           s = DSI_E_RANGE;
           msg = "config " + std::to_string(i) + ": n_trials (and, with DSI_F_HIST, min(k, N)) must not change";
         }
+        const bool same_stream = t.stream_id == o.stream_id && t.thr == o.thr && t.n == o.n && t.trials == o.trials;
+        ps = ps && same_stream && t.k == o.k && t.t_t == o.t_t && t.t_d == o.t_d && t.sp == o.sp;
+        const bool to = o.t_t1 != o.t_t || o.t_d1 != o.t_d, tn = t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+        gs = gs && same_stream && to == tn;
+        cs = cs && t.ut == o.ut && t.ud == o.ud && t.a == o.a && t.sp == o.sp && t.n == o.n;
       }
       if (s != DSI_OK) {
         std::lock_guard<std::mutex> lock(mu);
@@ -190,8 +201,16 @@ dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n, std::vector
         return;
       }
     }
+    if (!ps) plan_same = false;
+    if (!gs) groups_same = false;
+    if (!cs) cells_same = false;
   });
   if (bad < n) return fail(h, bad_s, bad_msg);
+  if (keys) {
+    keys->plan_same = plan_same;
+    keys->groups_same = groups_same;
+    keys->cells_same = cells_same;
+  }
   return DSI_OK;
 }
 
