@@ -20,8 +20,16 @@ big, btick = W.cfg3(trials=300, k_max=8)
 a100 = (big["accept_rate"] * 100).round().astype(int)
 big = big[(a100 == 50) | (a100 == 90)].copy()
 big["n_trials"] = 300 + 7 * (a100[(a100 == 50) | (a100 == 90)] == 90)
-with D.Simulator(big, tick=btick, seed=W.SEED, flags=D.DSI_F_SHARED_STREAMS) as sim:
-    sim.run().reduce()
+for flags in (D.DSI_F_SHARED_STREAMS, D.DSI_F_SHARED_STREAMS | FRESH):  # (FRESH: the template variant)
+    with D.Simulator(big, tick=btick, seed=W.SEED, flags=flags) as sim:
+        sim.run().reduce()
+# cell-aligned shards: the heatmap kernel over an owned-cell index list; the deferred reduce
+cells3, ctick3 = W.cfg3(trials=200, k_max=6, cells=slice(0, 60))
+for flags in (0, D.DSI_F_SHARED_STREAMS):
+    with D.Simulator(cells3, tick=ctick3, seed=W.SEED, flags=flags, n_shards=3) as sim:
+        sim.run().heatmap()
+        sim.run().reduce_device()
+        sim.fetch(5, 20)
 ttft, ttick = W.cfg2_ttft(trials=50)  # the TTFT variant (first-segment tables)
 for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
     with D.Simulator(ttft[:6], tick=ttick, seed=W.SEED, flags=flags) as sim:
