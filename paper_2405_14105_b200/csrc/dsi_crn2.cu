@@ -14,8 +14,12 @@
 //     tile's trials: the same closed form and moment algebra as the fused kernel, the long
 //     runs walked in decreasing order until L <= k, and configs with k = 1 and no queueing
 //     taking the per-trial sums (O(1)).
-// Records are tile-major: [TH x uint4 summaries][max_runs x TH uint16 runs, run-major], so
-// one tile is one contiguous copy of rec_bytes (a multiple of 16).
+// Records are tile-major: [TH x uint4 summaries][FRESH: TH x uint2 short-run counts][max_runs x TH
+// uint16 runs, run-major], so one tile is one contiguous copy of rec_bytes (a multiple of 16).
+// FRESH (a launch with fresh-verifier configs, R24, which correct every segment): pass 1
+// also counts each trial's runs of L = 2..kShortL accepted drafts (6-bit fields; a trial has at
+// most max_runs <= 63 stored runs), and pass 2 prices them with kShortL - 1 per-config savings
+// instead of walking them (cfg3 under R24: 211.5 -> 94.0 ms, profiles/r02_ab_freshcnt*.jsonl).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -64,7 +68,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
-template <int TH>
+constexpr int kShortL = 11;  // FRESH: runs of L = 2..kShortL accepted drafts are counted, not walked
+
+template <int TH, bool FRESH>
 __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   const CrnTile tile = P.tiles[P.tile_begin + blockIdx.x];
@@ -83,14 +89,17 @@ __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
 
   unsigned char *rec = P.records + (P.group_tile0[tile.group] + tile.tile) * (uint64_t)P.rec_bytes;
   uint4 *summ = reinterpret_cast<uint4 *>(rec);
-  uint16_t *runs = reinterpret_cast<uint16_t *>(rec + (size_t)TH * sizeof(uint4));
+  uint2 *cnts = reinterpret_cast<uint2 *>(rec + (size_t)TH * sizeof(uint4));
+  uint16_t *runs = reinterpret_cast<uint16_t *>(rec + (size_t)TH * (sizeof(uint4) + (FRESH ? sizeof(uint2) : 0)));
   const uint64_t t = (uint64_t)tile.tile * TH + threadIdx.x;
   if (t >= G.n_trials) return;
   const TrialHalf th = philox_trial_half((uint32_t)t, P.keys);
   uint16_t *my = runs_s + threadIdx.x;
   int nz = 0, n2 = 0, run = 0, lastz = 0, nr = 0;
   uint32_t sum_l = 0, sum_half = 0;  // sum L, sum floor(L/2) over the runs (k = 1 corrections)
+  uint64_t short_cnt = 0;            // FRESH: 6-bit counts of the runs with L = 2..kShortL
   auto push = [&](int L) {         // insertion into my[0..nr) kept in decreasing order
+    if (FRESH && L <= kShortL) short_cnt += 1ull << (6 * (L - 2));
     int i = nr++;
     while (i > 0) {
       const int prev = my[(i - 1) * TH];
@@ -143,6 +152,7 @@ __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
   const uint32_t maxL = nr ? my[0] : 0u;
   summ[threadIdx.x] = make_uint4((uint32_t)(nz + 1), (uint32_t)n2, maxL,
                                  (uint32_t)nr | (sum_l << 10) | (sum_half << 21));
+  if (FRESH) cnts[threadIdx.x] = make_uint2((uint32_t)short_cnt, (uint32_t)(short_cnt >> 32));
   for (int r = 0; r < nr; ++r) runs[r * TH + threadIdx.x] = my[r * TH];
 }
 
@@ -169,6 +179,10 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
   CfgFr f{};
   if (FRESH) f = load_cfgfr(P.cfg, P.perm, un, threadIdx.x);
   const bool fresh = FRESH && f.fresh != 0;
+  // FRESH: the savings of runs of L = 2..kShortL accepted drafts, this config's (0 if not fresh)
+  int sv_short[kShortL - 1];
+#pragma unroll
+  for (int i = 0; i < kShortL - 1; ++i) sv_short[i] = fresh ? fresh_saving_lite(i + 2, l, f) : 0;
   __syncthreads();
 
   const uint64_t tile_a = un.t0 / TH, tile_b = (un.t1 + TH - 1) / TH;  // un.t0 is tile-aligned
@@ -196,7 +210,9 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
     mbar_wait(&bar[cur], (uint32_t)(((ti - tile_a) >> 1) & 1));
     const unsigned char *bufc = smem + (size_t)cur * P.rec_bytes;
     const uint4 *summ = reinterpret_cast<const uint4 *>(bufc);
-    const uint16_t *runs = reinterpret_cast<const uint16_t *>(bufc + (size_t)TH * sizeof(uint4));
+    const uint2 *cnts = reinterpret_cast<const uint2 *>(bufc + (size_t)TH * sizeof(uint4));
+    const uint16_t *runs =
+        reinterpret_cast<const uint16_t *>(bufc + (size_t)TH * (sizeof(uint4) + (FRESH ? sizeof(uint2) : 0)));
     const uint64_t tile0 = ti * TH;
     const int ntr = (int)(min(un.t1, tile0 + TH) - tile0);
     if ((int)threadIdx.x < ntr) {  // the config-independent block sums, one trial per thread
@@ -225,28 +241,31 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
           int sb = 0, cnt = 0, sv = 0;
           for (int r = 0; r < nr; ++r) {  // runs in decreasing order: stop at the first short one
             const int L = runs[r * TH + s];
-            if (L <= l.k_eff) {
-              if (!fresh) break;  // (fresh: every stored run L >= 2 saves)
-            } else {
+            // (fresh: every run saves; those of L <= kShortL are priced from their counts below)
+            if (L <= l.k_eff && (!fresh || L <= kShortL)) break;
+            if (L > l.k_eff) {
               ai += (int)magic_div((uint32_t)L, l.m_si, 0u);
               sb += (int)magic_div((uint32_t)L + (uint32_t)l.k_eff - 1u, l.m_k_lo, l.m_k_hi);
               ++cnt;
             }
-            if (fresh) sv += fresh_saving_lite(L, l, f);
+            if (fresh && L > kShortL) sv += fresh_saving_lite(L, l, f);
           }
           ay = sb * l.kd - cnt * l.s1 - sv;
         } else {
           for (int r = 0; r < nr; ++r) {
             const int L = runs[r * TH + s];
-            if (L <= l.k_eff) {
-              if (!fresh) break;
-            } else {
-              long_run(L, l, ai, ay);
-            }
-            if (fresh) ay -= fresh_saving_lite(L, l, f);
+            if (L <= l.k_eff && (!fresh || L <= kShortL)) break;
+            if (L > l.k_eff) long_run(L, l, ai, ay);
+            if (fresh && L > kShortL) ay -= fresh_saving_lite(L, l, f);
           }
         }
-        if (fresh) ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
+        if (fresh) {
+          ay -= (n2 - nr) * (l.kd - l.t_t);  // the runs of L = 1 (not stored)
+          const uint2 c = cnts[s];
+          const uint64_t c64 = (uint64_t)c.x | ((uint64_t)c.y << 32);
+#pragma unroll
+          for (int i = 0; i < kShortL - 1; ++i) ay -= (int)((c64 >> (6 * i)) & 63u) * sv_short[i];
+        }
         p_ai += (unsigned)ai;
         p_ai2 += (unsigned)(ai * ai);
         p_mai += (unsigned)(m * ai);
@@ -334,22 +353,25 @@ int launch_grid(K kernel, const CrnParams &p, uint64_t n_blocks, int threads, si
 
 }  // namespace
 
-size_t crn_record_bytes(int max_runs, int threads) {
-  return ((size_t)threads * sizeof(uint4) + (size_t)max_runs * threads * sizeof(uint16_t) + 15) & ~(size_t)15;
+size_t crn_record_bytes(int max_runs, int threads, bool fresh) {
+  return ((size_t)threads * (sizeof(uint4) + (fresh ? sizeof(uint2) : 0)) + (size_t)max_runs * threads * sizeof(uint16_t) +
+          15) &
+         ~(size_t)15;
 }
 
-size_t crn_eval_smem(int max_runs, int threads) { return 2 * crn_record_bytes(max_runs, threads); }
+size_t crn_eval_smem(int max_runs, int threads, bool fresh) { return 2 * crn_record_bytes(max_runs, threads, fresh); }
 
 int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, int threads, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (threads != 256) return (int)cudaErrorInvalidValue;
   if (n_tiles) {
     const size_t smem = (size_t)p.max_nq * sizeof(uint4) + (size_t)p.max_runs * threads * sizeof(uint16_t);
-    const int e = launch_grid(dsi_crn_stream_kernel<256>, p, n_tiles, threads, smem, st, true);
+    const int e = p.any_fresh ? launch_grid(dsi_crn_stream_kernel<256, true>, p, n_tiles, threads, smem, st, true)
+                              : launch_grid(dsi_crn_stream_kernel<256, false>, p, n_tiles, threads, smem, st, true);
     if (e) return e;
   }
   if (n_units) {
-    const size_t smem = crn_eval_smem(p.max_runs, threads);
+    const size_t smem = crn_eval_smem(p.max_runs, threads, p.any_fresh != 0);
     return p.any_fresh ? launch_grid(dsi_crn_eval_kernel<256, true>, p, n_units, threads, smem, st, false)
                        : launch_grid(dsi_crn_eval_kernel<256, false>, p, n_units, threads, smem, st, false);
   }

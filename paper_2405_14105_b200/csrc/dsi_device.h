@@ -152,8 +152,8 @@ int launch_check_trials(const DevCfg *cfg, const unsigned long long *acc, uint64
                         void *stream);
 
 size_t crn_kernel_smem(int max_n, int block_threads, int cfg_per_block, int max_runs, bool fresh);
-size_t crn_record_bytes(int max_runs, int threads);
-size_t crn_eval_smem(int max_runs, int threads);
+size_t crn_record_bytes(int max_runs, int threads, bool fresh);
+size_t crn_eval_smem(int max_runs, int threads, bool fresh);
 // pass 1 over n_tiles records (p.tiles from p.tile_begin), then pass 2 over n_units units
 int launch_crn_two_pass(const CrnParams &p, uint64_t n_tiles, uint64_t n_units, int threads, void *stream);
 int launch_crn_kernel(const CrnParams &p, uint64_t n_units, int block_threads, void *stream,

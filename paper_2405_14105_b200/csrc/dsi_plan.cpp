@@ -133,11 +133,13 @@ dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_uni
 dsi_status plan_two_pass(dsi_sim *h) {
   const int th = h->cfg_per_block;
   // pass 2's two tile buffers must leave room for 3 blocks per SM (its register budget)
-  h->two_pass = th == 256 && dsi::crn_eval_smem(h->max_runs, th) <= 64 * 1024;
+  // (the fresh-verifier layout's 6-bit short-run counts need at most 63 stored runs per trial)
+  h->two_pass = th == 256 && dsi::crn_eval_smem(h->max_runs, th, h->any_fresh) <= 64 * 1024 &&
+                (!h->any_fresh || h->max_runs <= 63);
   if (knobs().crn_two_pass >= 0) h->two_pass = h->two_pass && knobs().crn_two_pass != 0;
   if (!h->two_pass) return DSI_OK;
   try {
-    h->rec_bytes = (uint32_t)dsi::crn_record_bytes(h->max_runs, th);
+    h->rec_bytes = (uint32_t)dsi::crn_record_bytes(h->max_runs, th, h->any_fresh);
     h->group_tile0.assign(h->groups.size() + 1, 0);
     for (size_t g = 0; g < h->groups.size(); ++g)
       h->group_tile0[g + 1] = h->group_tile0[g] + (h->groups[g].n_trials + th - 1) / th;

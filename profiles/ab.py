@@ -24,6 +24,7 @@ ap.add_argument("--stride", type=int, default=5)
 ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--runs", type=int, default=5)
 ap.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
+ap.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER")
 args = ap.parse_args()
 if args.workload == "cfg3":
     cfgs, tick = W.cfg3(cells=slice(None, None, args.stride))
@@ -35,7 +36,8 @@ elif args.workload == "cfg4":
 else:
     cfgs, tick = W.cfg2()
 tt = int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"]))
-with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING | (D.DSI_F_SHARED_STREAMS if args.shared else 0),
+with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING | (D.DSI_F_SHARED_STREAMS if args.shared else 0)
+                 | (D.DSI_F_FRESH_VERIFIER if args.fresh else 0),
                  block_threads=args.threads) as sim:
     sim.run()
     sim.reduce()
