@@ -300,6 +300,39 @@ def test_seed_and_stream_change_the_draws():
     assert r1["sum_dsi_ticks"][0] != r3["sum_dsi_ticks"][0]
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4", "cfg5"])
+def test_other_baseline_configs_full_size_sampled(name):
+    """BASELINE configs[1], [3], [4] at their full sizes (cfg2: Table-2 pairs x k {1,5,10}, 1e5
+    trials, N 100; cfg4: k 1..20 x SP 2..8, 1e5 trials, N 500; cfg5: 10 100 cells at the Eq.-1
+    lookahead, 1e5 trials, N 1000) in the per-config mode and in the shared-stream mode; sampled
+    configs recomputed by the oracle over all their trials (exact sums), the partition and the
+    theorem counters checked on every config."""
+    if name == "cfg2":
+        cfgs, tick = W.cfg2()
+        pick = [0, 17, 29]
+    elif name == "cfg4":
+        cfgs, tick = W.cfg4()
+        pick = [3, 131]
+    else:
+        cfgs, tick = W.cfg5(D.dsi_min_lookahead)
+        pick = [50 * 101 + 80]  # t_d 0.51, a 0.80
+    for flags in (0, D.DSI_F_SHARED_STREAMS):
+        sim = D.Simulator(cfgs, tick=tick, seed=SEED, flags=flags)
+        res = sim.run().reduce()
+        sim.close()
+        assert np.all(res["trials"] == cfgs["n_trials"])
+        kd = res["t_drafter_ticks"] * cfgs["lookahead"]
+        inside = kd <= res["t_target_ticks"]
+        assert np.all(res["n_dsi_gt_nonsi"][inside] == 0)
+        if flags == 0:
+            base = res
+            for i in pick:
+                assert_result_equals_oracle(res[i], oracle_sums(cfgs[i], tick, SEED), tick, ctx=f"{name}[{i}]")
+        else:
+            for f in MOMENTS:
+                assert np.array_equal(res[f], base[f]), (name, f)
+
+
 def test_bench_workload_full_size_sampled():
     """The bench's workload (cfg3 heatmap, k <= 200, T = 1e4, N = 100) in the bench's launch
     configuration; a sample of configs is recomputed by the oracle one by one (exact sums),
