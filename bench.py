@@ -186,6 +186,66 @@ def fast_mode_e2e(sim, cfgs, res, tt, steps, barrier, max_over_ranks):
     return out[0], out[1]
 
 
+def other_workloads_block(D, names, args, base_kw, root, fresh_id, flush, barrier, max_over_ranks, world) -> dict:
+    """BASELINE.json's other configs on the same GPUs (collective: every rank runs its share):
+    per workload the per-config mode (run + reduce, CUDA events, as `value`) with its SURVEY 8(d).4
+    issue fraction, and the shared-stream and means-only modes (run + reduce_device) with whether
+    their sums equal the per-config run's."""
+    import torch
+
+    sm_max = float(measured_peaks().get("sm_max_mhz", 1965.0))
+    peak_instr = SM_COUNT * LANES_PER_SM_CLK * sm_max * 1e6
+    out = {}
+    for name in names:
+        cfgs, tick = workload(name, D.dsi_min_lookahead)
+        kw = dict(base_kw, tick=tick)
+        tt = trial_tokens(cfgs)
+        entry = {"desc": WORKLOAD_DESC[name], "configs": int(cfgs.size), "trial_tokens_per_step": tt}
+        ref = None
+        for mode, flags in (("per_config", 0), ("shared_streams", D.DSI_F_SHARED_STREAMS),
+                            ("means_only", D.DSI_F_MEANS_ONLY)):
+            sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING | root | flags, nccl_id=fresh_id(), **kw)
+            st = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", base_kw["device"]))
+            res = np.zeros(cfgs.size, D.RESULT_DTYPE)
+            for _ in range(args.warmup):
+                sim.run()
+                sim.reduce(res)
+            barrier()
+            ms, kms = [], []
+            for _ in range(args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                sim.run()
+                if flags:
+                    sim.reduce_device()
+                else:
+                    sim.reduce(res)
+                e1.record(st)
+                e1.synchronize()
+                ms.append(e0.elapsed_time(e1))
+                kms.append(sim.kernel_ms())
+            barrier()
+            total = max_over_ranks(sum(ms))
+            kern = max_over_ranks(statistics.mean(kms))
+            d = {"value": tt * args.steps / (total / 1000.0), "unit": UNIT, "ms_per_step": total / args.steps,
+                 "kernel_ms": kern}
+            if flags == 0:
+                ach = alg_instructions(cfgs) / world / (kern / 1000.0)
+                d["roofline_issue_frac"] = ach / peak_instr
+                ref = res
+            elif base_kw["rank"] == 0:
+                sim.fetch(0, cfgs.size, res)
+                d["sums_identical_to_per_config"] = bool(all(
+                    np.array_equal(res[f], ref[f]) for f in ("sum_si_ticks", "sum_dsi_ticks", "sum_segments",
+                                                             "sum_si_iters", "trials")))
+            sim.close()
+            entry[mode] = d
+        out[name] = entry
+    return out
+
+
 def trial_tokens(cfgs) -> int:
     return int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"].astype(np.int64)))
 
@@ -771,6 +831,12 @@ def ours(args):
         multi = multi_drafter_block(args.steps, sm_max)
     barrier()
 
+    # BASELINE configs[1], [3], [4] (cfg2, cfg4, cfg5: the large Monte Carlo) on the same GPUs
+    others = None
+    if not args.no_others and args.workload == "cfg3":
+        others = other_workloads_block(D, ("cfg5", "cfg4", "cfg2"), args, base_kw, root, fresh_nccl_id, flush,
+                                       barrier, max_over_ranks, world)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O
@@ -832,6 +898,7 @@ def ours(args):
             "shared_streams": crn,
             "means_only": means,
             "multi_drafter": multi,
+            "other_workloads": others,
             "clocks": clk,
             "create_s": create_s,
             "wall_s_timed": wall,
@@ -858,6 +925,7 @@ def main():
     ap.add_argument("--no-multi", action="store_true", help="skip the multi-drafter block")
     ap.add_argument("--no-means", action="store_true", help="skip the means-only block")
     ap.add_argument("--no-fresh", action="store_true", help="skip the fresh-verifier (R24) heatmap block")
+    ap.add_argument("--no-others", action="store_true", help="skip BASELINE's other configs (cfg5, cfg4, cfg2)")
     args = ap.parse_args()
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")

@@ -34,6 +34,7 @@ def test_bench_json_line_small_workload():
     fv = d["heatmap"]["fresh_verifier"]
     assert fv["shared_streams_bit_identical"] is True and fv["means_only_bit_identical"] is True
     assert fv["identical_to_default_where_k_td_le_tt"] is True
+    assert d["other_workloads"] is None  # (run on the cfg3 bench only)
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 
