@@ -183,8 +183,13 @@ DSI_API dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg,
 
 /* Replace the configuration values of an existing handle (same n_cfg, same
  * n_trials per config; with DSI_F_HIST also the same min(k, N)).  Validates like
- * create, waits for any previous run, then copies the table host -> device from
- * pinned staging.  N may grow (shared-memory tables are sized per launch).  With
+ * create.  Device path (one device, no test-mode flag): the configurations are copied as
+ * given (straight from a page-locked cfg, else through pinned staging) and validated and
+ * converted on the GPU, ordered after any previous run on the library's stream; committed when
+ * every config is valid, the launch limits (max N, max min(k, N), TTFT / fresh-verifier
+ * present) are unchanged and no plan below needs rebuilding -- otherwise, and always for the
+ * test modes, the host path validates, re-plans and uploads (and reports any error with its
+ * message).  N may grow (shared-memory tables are sized per launch).  With
  * DSI_F_SHARED_STREAMS the plan is kept when (stream_id, threshold, N, n_trials, k,
  * t_target, t_drafter, SP) are unchanged, else rebuilt; an update that changes the
  * number of groups or units returns DSI_E_RANGE ("create a new handle").  On error
@@ -243,9 +248,10 @@ DSI_API dsi_status dsi_sim_launches(dsi_sim *h, int32_t *launches);
  * device_index, measured with CUDA events on the launching stream (blocks). */
 DSI_API dsi_status dsi_sim_kernel_ms(dsi_sim *h, int32_t device_index, float *ms);
 
-/* Host<->device bytes moved per create+run+reduce on this process: the config
- * table and unit prefix uploaded by create (h2d) and the per-config moments (and
- * histograms) read back by reduce (d2h). */
+/* Host<->device bytes moved per update+run+reduce on this process: what dsi_sim_update uploads
+ * (h2d: the configurations as given, validated on the device, or -- with DSI_F_PER_TRIAL,
+ * DSI_F_HIST or DSI_F_PATTERN -- the host-built device table) and the per-config moments (and
+ * histograms) dsi_sim_reduce reads back (d2h). */
 DSI_API dsi_status dsi_sim_io_bytes(dsi_sim *h, uint64_t *h2d, uint64_t *d2h);
 
 /* Work units (config, trial tile) of this process: [first, first+count) of total. */

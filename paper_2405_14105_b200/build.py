@@ -24,9 +24,11 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 HOST = ["dsi_validate.cpp", "dsi_plan.cpp", "dsi_collective.cpp", "dsi_runtime.cpp",
         "dsi_multi_host.cpp", "dsi_heatmap.cpp"]
-DEVICE = ["dsi_kernel.cu", "dsi_crn.cu", "dsi_reduce_dev.cu", "dsi_crn2.cu", "dsi_multi.cu", "dsi_seg.cu"]
+DEVICE = ["dsi_kernel.cu", "dsi_crn.cu", "dsi_reduce_dev.cu", "dsi_crn2.cu", "dsi_multi.cu", "dsi_seg.cu",
+          "dsi_stage.cu"]
 SOURCES = [os.path.join(CSRC, f) for f in HOST + DEVICE]
-HEADERS = [os.path.join(CSRC, f) for f in ("dsi_host.h", "dsi_device.h", "dsi_common.cuh", "dsi_crn_common.cuh")] + \
+HEADERS = [os.path.join(CSRC, f) for f in ("dsi_host.h", "dsi_device.h", "dsi_convert.h", "dsi_common.cuh",
+                                                  "dsi_crn_common.cuh")] + \
           [os.path.join(ROOT, "include", f) for f in ("dsi_sim.h", "dsi_sim_testing.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 VARIANTS = {"product": ("libdsi_sim.so", []),

@@ -31,15 +31,16 @@
 
 #include "../../include/dsi_sim.h"
 #include "../../include/dsi_sim_testing.h"
+#include "dsi_convert.h"
 #include "dsi_device.h"
 
 namespace dsih {
 
+using dsi::CfgTicks;
 using dsi::DevCfg;
 using dsi::LaunchParams;
-
-constexpr int kMaxTokens = 32768;  // keeps every magic division exact (x * d <= 2^32)
-constexpr uint64_t kMaxTrials = 1ull << 32;
+using dsi::kMaxTokens;
+using dsi::kMaxTrials;
 constexpr int kDefaultThreads = 128;
 constexpr int kCrnThreads = 128;   // dsi_crn_kernel block size when 256 does not fit (see plan_shared)
 constexpr size_t kReduceChunks = 8;  // dsi_sim_reduce: D2H chunks overlapped with the finalize
@@ -66,22 +67,7 @@ struct NcclApi {
 NcclApi &nccl();
 
 // ----------------------------------------------------------------------------- helpers
-struct CfgTicks {
-  int64_t t_t, t_d, kd;
-  int64_t t_t1, t_d1;  // first-forward latencies (TTFT variant; equal to t_t, t_d when off)
-  uint64_t thr;
-  int32_t k, sp, n;
-  uint32_t stream_id;
-  uint64_t trials;
-  double a;
-  double ut, ud;  // t_target, t_drafter as given (heatmap cells group on the user values)
-  int32_t eq1, min_k;  // Eq. 1 holds at (k, SP); the minimal lookahead at SP
-};
-
-// ceil(2^32 / d) split into low word and bit 32 (d >= 1).
-void magic(uint32_t d, uint32_t &lo, uint32_t &hi);
-
-inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return dsi::ceil_div64(a, b); }
 
 template <class T>
 struct Pinned {  // page-locked host buffer (true async DMA for H2D/D2H)
@@ -150,6 +136,11 @@ struct DeviceState {
   std::vector<uint32_t> owned_cells;      // cell-local heatmap: the cells this device's parts own
   uint32_t *d_owned = nullptr;            //   ... on the device
   size_t owned_cap = 0;
+  // device path of dsi_sim_update (dsi_stage.cu): the configurations as given, current and spare,
+  // the spare device table and the staging status
+  dsi_config *d_raw = nullptr, *d_raw_next = nullptr;
+  DevCfg *d_cfg_next = nullptr;
+  dsi::StageStatus *d_stage = nullptr;
 };
 
 struct dsi_sim {
@@ -193,6 +184,10 @@ struct dsi_sim {
   std::vector<DeviceState> dev;
   Pinned<unsigned long long> host_acc, host_seg, host_si;  // D2H targets
   bool ran = false, reduced = false;
+  bool raw_valid = false;    // dev[0].d_raw holds the current configurations (device update path)
+  bool ticks_stale = false;  // a device update committed: ticks / dev_cfg staging refreshed on demand
+  Pinned<dsi_config> raw_pinned;        // staging of configurations (H2D from pageable memory, D2H)
+  Pinned<dsi::StageStatus> stage_host;
   bool reduced_device = false;  // the moments of the last run are summed (dsi_sim_reduce[_device])
   std::vector<dsi::HeatCell> heat_cells;  // heatmap cells (planned on first use, reset by update)
   bool heat_planned = false, heat_uploaded = false;
@@ -230,8 +225,9 @@ dsi_status host_allreduce(dsi_sim *h, cudaStream_t st, const void *src, void *ds
 
 dsi_status to_ticks(double x, double tick, int64_t *out);
 dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTicks &o, std::string &msg);
-bool config_noqueue(const CfgTicks &t);
-DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh);
+std::string convert_message(size_t i, int code);
+using dsi::config_noqueue;
+using dsi::make_dev_cfg;
 double unit_cost(const CfgTicks &t, uint64_t trials);
 
 // Every API call is an NVTX range (nvtx3, header-only: a no-op unless a profiler such as
@@ -379,6 +375,7 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost);
 void plan_heat_cells(dsi_sim *h);
 bool snap_bounds(std::vector<uint64_t> &bounds, const std::vector<double> &cost, const std::vector<uint64_t> &cand);
 void plan_cell_owners(dsi_sim *h);
+dsi_status ensure_ticks(dsi_sim *h);
 bool cells_aligned(const dsi_sim *h);
 
 }  // namespace dsih

@@ -31,6 +31,10 @@ void free_device(DeviceState &d) {
   cudaFree(d.d_heat_cells);
   cudaFree(d.d_heat_out);
   cudaFree(d.d_owned);
+  cudaFree(d.d_raw);
+  cudaFree(d.d_raw_next);
+  cudaFree(d.d_cfg_next);
+  cudaFree(d.d_stage);
   cudaFree(d.d_heat_bad);
   cudaFree(d.d_seg_groups);
   cudaFree(d.d_seg_prefix);
@@ -46,6 +50,8 @@ void free_device(DeviceState &d) {
 void free_handle(dsi_sim *h) {
   for (auto &d : h->dev) free_device(d);
   h->dev_cfg.release();
+  h->raw_pinned.release();
+  h->stage_host.release();
   h->host_acc.release();
   h->host_seg.release();
   h->host_si.release();
@@ -126,6 +132,123 @@ dsi_status alloc_two_pass(dsi_sim *h) {
       d.tiles_cap = d.tiles.size();
     }
   }
+  return DSI_OK;
+}
+
+namespace {
+
+constexpr dsi_status kHostPath = (dsi_status)-1;  // update_on_device: take the host path
+
+bool device_update_eligible(const dsi_sim *h) {
+  return h->dev.size() == 1 && !(h->opt.flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN));
+}
+
+// The configurations as given into device memory `dst` on device 0's stream: straight from a
+// caller's page-locked buffer, else through the pinned staging in slices (a parallel host copy of
+// slice i while slice i-1 is in flight).  Asynchronous; the staging is reused by the next call
+// only after a stream synchronization.
+dsi_status copy_raw(dsi_sim *h, const dsi_config *cfg, dsi_config *dst) {
+  DeviceState &d = h->dev[0];
+  const size_t n = h->n_cfg;
+  cudaPointerAttributes attr{};
+  const bool pinned = cudaPointerGetAttributes(&attr, cfg) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // (a pageable pointer may leave an error behind on older drivers)
+  if (pinned) {
+    CUDA_TRY(h, cudaMemcpyAsync(dst, cfg, n * sizeof(dsi_config), cudaMemcpyHostToDevice, d.stream));
+    return DSI_OK;
+  }
+  if (h->raw_pinned.n < n) CUDA_TRY(h, h->raw_pinned.alloc(n));
+  constexpr size_t kSlices = 8;
+  for (size_t sl = 0; sl < kSlices; ++sl) {
+    const size_t b = n * sl / kSlices, e = n * (sl + 1) / kSlices;
+    if (e <= b) continue;
+    parallel_for(e - b, [&](size_t lo, size_t hi) {
+      std::memcpy(h->raw_pinned.p + b + lo, cfg + b + lo, (hi - lo) * sizeof(dsi_config));
+    }, 1u << 14);
+    CUDA_TRY(h, cudaMemcpyAsync(dst + b, h->raw_pinned.p + b, (e - b) * sizeof(dsi_config), cudaMemcpyHostToDevice,
+                                d.stream));
+  }
+  return DSI_OK;
+}
+
+dsi_status alloc_device_update(dsi_sim *h) {
+  DeviceState &d = h->dev[0];
+  CUDA_TRY(h, cudaSetDevice(d.ordinal));
+  const size_t n = std::max<size_t>(1, h->n_cfg);
+  if (!d.d_raw) CUDA_TRY(h, cudaMalloc((void **)&d.d_raw, n * sizeof(dsi_config)));
+  if (!d.d_raw_next) CUDA_TRY(h, cudaMalloc((void **)&d.d_raw_next, n * sizeof(dsi_config)));
+  if (!d.d_cfg_next) CUDA_TRY(h, cudaMalloc((void **)&d.d_cfg_next, n * sizeof(DevCfg)));
+  if (!d.d_stage) CUDA_TRY(h, cudaMalloc((void **)&d.d_stage, sizeof(dsi::StageStatus)));
+  if (!h->stage_host.p) CUDA_TRY(h, h->stage_host.alloc(1));
+  return DSI_OK;
+}
+
+// The device path of dsi_sim_update: copy the configurations as given, validate and convert them on
+// the GPU into the spare table (dsi_stage.cu), and commit -- swap the tables -- when every config
+// is valid, n_trials unchanged, the launch limits unchanged and no plan needs rebuilding (the
+// shared-stream plan or the means-only groups).  kHostPath otherwise: the host path then reports
+// the error (with its message) or re-plans.  On commit the host tick table becomes stale; it is
+// rebuilt from the device copy of the configurations when a host step needs it (ensure_ticks).
+dsi_status update_on_device(dsi_sim *h, const dsi_config *cfg, Trace &tr) {
+  if (!h->raw_valid) return kHostPath;
+  dsi_status s = alloc_device_update(h);
+  if (s != DSI_OK) return s;
+  DeviceState &d = h->dev[0];
+  s = copy_raw(h, cfg, d.d_raw_next);
+  if (s != DSI_OK) return s;
+  dsi::StageStatus init{};
+  init.first_bad = ~0ull;
+  init.max_n = init.max_keff = 1;
+  *h->stage_host.p = init;
+  CUDA_TRY(h, cudaMemcpyAsync(d.d_stage, h->stage_host.p, sizeof init, cudaMemcpyHostToDevice, d.stream));
+  dsi::StageParams p{};
+  p.raw = d.d_raw_next;
+  p.prev = d.d_raw;
+  p.out = d.d_cfg_next;
+  p.n = h->n_cfg;
+  p.tick = h->opt.tick;
+  p.flags = h->opt.flags;
+  p.st = d.d_stage;
+  const int e = dsi::launch_stage_kernel(p, d.stream);
+  if (e) return cuda_fail(h, (cudaError_t)e, "config staging launch");
+  CUDA_TRY(h, cudaMemcpyAsync(h->stage_host.p, d.d_stage, sizeof init, cudaMemcpyDeviceToHost, d.stream));
+  CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+  tr.mark("device-stage");
+  const dsi::StageStatus st = *h->stage_host.p;
+  const bool ttft = st.flags & dsi::STAGE_TTFT, fresh = st.flags & dsi::STAGE_FRESH;
+  if (st.first_bad != ~0ull) return kHostPath;
+  if (st.max_n != h->max_n || st.max_keff != h->max_keff || ttft != h->any_ttft || fresh != h->any_fresh)
+    return kHostPath;
+  if (h->shared && (st.flags & dsi::STAGE_PLAN_CHANGED)) return kHostPath;
+  if (h->means_only && (st.flags & dsi::STAGE_GROUPS_CHANGED)) return kHostPath;
+  // commit
+  std::swap(d.d_cfg, d.d_cfg_next);
+  std::swap(d.d_raw, d.d_raw_next);
+  h->ticks_stale = true;
+  h->k1_fast = !ttft && !fresh && st.work_k1 >= 0.25 * st.work;
+  if (knobs().k1_fast >= 0) h->k1_fast = !ttft && !fresh && knobs().k1_fast != 0;
+  h->ran = h->reduced = h->reduced_device = false;
+  if (st.flags & dsi::STAGE_CELLS_CHANGED) h->heat_planned = h->heat_uploaded = false;
+  return DSI_OK;
+}
+
+}  // namespace
+
+// The host tick table after device updates: rebuilt from the device copy of the current
+// configurations, which were validated when they were committed.
+dsi_status ensure_ticks(dsi_sim *h) {
+  if (!h->ticks_stale) return DSI_OK;
+  DeviceState &d = h->dev[0];
+  CUDA_TRY(h, cudaSetDevice(d.ordinal));
+  if (h->raw_pinned.n < h->n_cfg) CUDA_TRY(h, h->raw_pinned.alloc(h->n_cfg));
+  CUDA_TRY(h, cudaMemcpyAsync(h->raw_pinned.p, d.d_raw, h->n_cfg * sizeof(dsi_config), cudaMemcpyDeviceToHost,
+                              d.stream));
+  CUDA_TRY(h, cudaStreamSynchronize(d.stream));
+  const dsi_status s = validate_all(h, h->raw_pinned.p, h->n_cfg, h->ticks);
+  if (s != DSI_OK) return s;
+  // (the pinned device-table staging is read only by the test modes' accessors, which never take
+  // the device path, and rewritten by every host-path update)
+  h->ticks_stale = false;
   return DSI_OK;
 }
 
@@ -437,6 +560,12 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   }
   s = upload(h);
   if (s != DSI_OK) return abort_create(s);
+  if (device_update_eligible(h)) {  // the device copy a device update compares with (dsi_stage.cu)
+    s = alloc_device_update(h);
+    if (s == DSI_OK) s = copy_raw(h, cfg, h->dev[0].d_raw);
+    if (s != DSI_OK) return abort_create(s);
+    h->raw_valid = true;
+  }
   for (auto &d : h->dev) {
     cudaSetDevice(d.ordinal);
     if (cudaStreamSynchronize(d.stream) != cudaSuccess) {
@@ -476,6 +605,14 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   h->err.clear();
   if (!cfg) return fail(h, DSI_E_NULL, "cfg is NULL");
   if (n_cfg != h->n_cfg) return fail(h, DSI_E_RANGE, "n_cfg must equal the handle's");
+  if (device_update_eligible(h)) {
+    const dsi_status sd = update_on_device(h, cfg, tr);
+    if (sd != kHostPath) return sd;
+  }
+  {  // the host path compares with the current ticks
+    const dsi_status se = ensure_ticks(h);
+    if (se != DSI_OK) return se;
+  }
   // validate into the spare table; h->ticks (and the whole handle) stay as they are on failure
   try {
     h->ticks_next.resize(n_cfg);
@@ -562,8 +699,14 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
   tr.mark("fill+upload");
   h->ran = h->reduced = h->reduced_device = false;
   if (!keys.cells_same || replan) h->heat_planned = h->heat_uploaded = false;  // else the cells stand
-  const dsi_status su = upload(h, replan, /*cfg_table=*/false);
+  dsi_status su = upload(h, replan, /*cfg_table=*/false);
   tr.mark("upload");
+  if (su == DSI_OK && device_update_eligible(h)) {  // the device copy the next device update compares with
+    su = alloc_device_update(h);
+    if (su == DSI_OK) su = copy_raw(h, cfg, h->dev[0].d_raw);
+    if (su == DSI_OK) CUDA_TRY(h, cudaStreamSynchronize(h->dev[0].stream));  // (the staging is reused)
+    h->raw_valid = su == DSI_OK;
+  }
   return su;
 }
 
@@ -791,6 +934,10 @@ dsi_status sync_all(dsi_sim *h) {
 // pinned mirror, the host finalizing chunk i while chunk i+1 is in flight.  The partition flag
 // (reduce_enqueue) is checked before any result is written.
 dsi_status finalize_range(dsi_sim *h, size_t first, size_t count, dsi_result *out, Trace &tr) {
+  {
+    const dsi_status se = ensure_ticks(h);  // (after device updates: the finalize reads the ticks)
+    if (se != DSI_OK) return se;
+  }
   DeviceState &d0 = h->dev[0];
   CUDA_TRY(h, cudaSetDevice(d0.ordinal));
   const unsigned long long *src = h->use_nccl ? d0.d_red : d0.d_acc;
@@ -937,6 +1084,8 @@ dsi_status dsi_sim_heatmap(dsi_sim *h, dsi_heatmap_cell *cells, size_t cap, size
   h->err.clear();
   if (!n_cells) return fail(h, DSI_E_NULL, "n_cells is NULL");
   if (!h->heat_planned) {  // cells: maximal runs of equal (t_target, t_drafter, a, SP, N)
+    const dsi_status se = ensure_ticks(h);
+    if (se != DSI_OK) return se;
     try {
       plan_heat_cells(h);
       plan_cell_owners(h);
@@ -1123,7 +1272,8 @@ dsi_status dsi_sim_kernel_ms(dsi_sim *h, int32_t i, float *ms) {
 dsi_status dsi_sim_io_bytes(dsi_sim *h, uint64_t *h2d, uint64_t *d2h) {
   if (!h || !h2d || !d2h) return DSI_E_NULL;
   const uint64_t n = h->n_cfg;
-  *h2d = (uint64_t)h->dev.size() * n * sizeof(DevCfg);
+  // an update's upload: the configurations as given (device path) or the device table (host path)
+  *h2d = (uint64_t)h->dev.size() * n * (device_update_eligible(h) ? sizeof(dsi_config) : sizeof(DevCfg));
   uint64_t back = n * dsi::NF * sizeof(unsigned long long);
   if (h->opt.flags & DSI_F_HIST) back += (n * 64 + h->si_bins_total) * sizeof(unsigned long long);
   *d2h = back;

@@ -10,10 +10,13 @@ namespace dsih {
 
 thread_local std::string g_create_error;
 
-// ceil(2^32 / d) split into low word and bit 32 (d >= 1).
-void magic(uint32_t d, uint32_t &lo, uint32_t &hi) {
-  // divisors below 2^16 (every lookahead, SP and N the planner sees in practice) come from a
-  // table built once: make_dev_cfg needs three per config, millions of times per update
+}  // namespace dsih
+
+namespace dsi {
+// ceil(2^32 / d) split into low word and bit 32 (d >= 1): divisors below 2^16 (every lookahead,
+// SP and N the planner sees in practice) come from a table built once -- make_dev_cfg needs
+// three per config, millions of times per update
+void magic_table(uint32_t d, uint32_t &lo, uint32_t &hi) {
   static const std::vector<uint64_t> table = [] {
     std::vector<uint64_t> t(1u << 16, 0);
     for (uint32_t x = 1; x < (1u << 16); ++x) t[x] = ((1ull << 32) + x - 1) / x;
@@ -23,135 +26,44 @@ void magic(uint32_t d, uint32_t &lo, uint32_t &hi) {
   lo = (uint32_t)m;
   hi = (uint32_t)(m >> 32);
 }
+}  // namespace dsi
 
-dsi_status to_ticks(double x, double tick, int64_t *out) {
-  if (!std::isfinite(x) || x <= 0.0) return DSI_E_RANGE;
-  const double r = x / tick;
-  if (!(r < 9.0e18)) return DSI_E_OVERFLOW;
-  const int64_t t = std::llround(r);
-  if (t < 1 || std::fabs(r - (double)t) > 1e-9 * std::fabs(r)) return DSI_E_TICK;
-  *out = t;
-  return DSI_OK;
-}
+namespace dsih {
 
-dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTicks &o,
-                   std::string &msg) {
+dsi_status to_ticks(double x, double tick, int64_t *out) { return (dsi_status)dsi::to_ticks(x, tick, out); }
+
+// The message of convert_config's code for config i.
+std::string convert_message(size_t i, int code) {
+  const char *what = "invalid configuration";
+  switch (code >> 8) {
+    case dsi::CV_ACCEPT: what = "accept_rate must be in [0, 1]"; break;
+    case dsi::CV_LOOKAHEAD: what = "lookahead must be >= 1"; break;
+    case dsi::CV_SP: what = "sp_degree must be >= 1"; break;
+    case dsi::CV_N: what = "n_tokens must be in [1, 32768]"; break;
+    case dsi::CV_TRIALS: what = "n_trials must be in [1, 2^32]"; break;
+    case dsi::CV_PATTERN_N: what = "DSI_F_PATTERN needs n_tokens <= 33"; break;
+    case dsi::CV_T_TARGET: what = "t_target is not a positive whole number of ticks"; break;
+    case dsi::CV_T_DRAFTER: what = "t_drafter is not a positive whole number of ticks"; break;
+    case dsi::CV_ASSUMPTION2: what = "t_drafter > t_target violates Assumption 2 (P:187-189)"; break;
+    case dsi::CV_TTFT_TARGET: what = "ttft_target is not 0 or a positive whole number of ticks"; break;
+    case dsi::CV_TTFT_DRAFTER: what = "ttft_drafter is not 0 or a positive whole number of ticks"; break;
+    case dsi::CV_ASSUMPTION2_FIRST: what = "ttft_drafter > ttft_target violates Assumption 2"; break;
+    case dsi::CV_SHARED_TTFT: what = "DSI_F_SHARED_STREAMS does not support the TTFT variant"; break;
+    case dsi::CV_FRESH_TTFT: what = "DSI_F_FRESH_VERIFIER does not support the TTFT variant"; break;
+    case dsi::CV_BOUND: what = "N*(k*t_drafter + t_target) must stay below 2^31 ticks"; break;
+    case dsi::CV_BOUND_SQ: what = "n_trials * bound^2 must stay below 2^64"; break;
+    case dsi::CV_STRICT_EQ1: what = "Eq. 1 violated: ceil(t_t/(k t_d)) > SP"; break;
+  }
   char buf[256];
-  auto bad = [&](dsi_status s, const char *what) {
-    std::snprintf(buf, sizeof buf, "config %zu: %s", i, what);
-    msg = buf;
-    return s;
-  };
-  if (!(c.accept_rate >= 0.0 && c.accept_rate <= 1.0))
-    return bad(DSI_E_RANGE, "accept_rate must be in [0, 1]");
-  if (c.lookahead < 1) return bad(DSI_E_RANGE, "lookahead must be >= 1");
-  if (c.sp_degree < 1) return bad(DSI_E_RANGE, "sp_degree must be >= 1");
-  if (c.n_tokens < 1 || c.n_tokens > kMaxTokens)
-    return bad(DSI_E_RANGE, "n_tokens must be in [1, 32768]");
-  if (c.n_trials < 1 || c.n_trials > kMaxTrials)
-    return bad(DSI_E_RANGE, "n_trials must be in [1, 2^32]");
-  if ((opt.flags & DSI_F_PATTERN) && c.n_tokens > 33)
-    return bad(DSI_E_RANGE, "DSI_F_PATTERN needs n_tokens <= 33");
-  dsi_status s = to_ticks(c.t_target, opt.tick, &o.t_t);
-  if (s != DSI_OK) return bad(s, "t_target is not a positive whole number of ticks");
-  s = to_ticks(c.t_drafter, opt.tick, &o.t_d);
-  if (s != DSI_OK) return bad(s, "t_drafter is not a positive whole number of ticks");
-  if (o.t_d > o.t_t) return bad(DSI_E_RANGE, "t_drafter > t_target violates Assumption 2 (P:187-189)");
-  o.t_t1 = o.t_t;
-  o.t_d1 = o.t_d;
-  if (c.ttft_target != 0.0) {
-    s = to_ticks(c.ttft_target, opt.tick, &o.t_t1);
-    if (s != DSI_OK) return bad(s, "ttft_target is not 0 or a positive whole number of ticks");
-  }
-  if (c.ttft_drafter != 0.0) {
-    s = to_ticks(c.ttft_drafter, opt.tick, &o.t_d1);
-    if (s != DSI_OK) return bad(s, "ttft_drafter is not 0 or a positive whole number of ticks");
-  }
-  if (o.t_d1 > o.t_t1) return bad(DSI_E_RANGE, "ttft_drafter > ttft_target violates Assumption 2");
-  if ((opt.flags & DSI_F_SHARED_STREAMS) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d))
-    return bad(DSI_E_RANGE, "DSI_F_SHARED_STREAMS does not support the TTFT variant");
-  if ((opt.flags & DSI_F_FRESH_VERIFIER) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d))
-    return bad(DSI_E_RANGE, "DSI_F_FRESH_VERIFIER does not support the TTFT variant");
-  // every per-trial latency is <= N (k t_d + t_t) plus the first-forward surcharges
-  // (kernel overflow bound)
-  const unsigned __int128 kd = (unsigned __int128)c.lookahead * (uint64_t)o.t_d;
-  const unsigned __int128 bound = (unsigned __int128)c.n_tokens * (kd + (uint64_t)o.t_t) +
-                                  (uint64_t)std::max<int64_t>(0, o.t_t1 - o.t_t) +
-                                  (uint64_t)std::max<int64_t>(0, o.t_d1 - o.t_d);
-  if (bound >= ((unsigned __int128)1 << 31))
-    return bad(DSI_E_OVERFLOW, "N*(k*t_drafter + t_target) must stay below 2^31 ticks");
-  if ((unsigned __int128)c.n_trials * bound * bound >= ((unsigned __int128)1 << 64))
-    return bad(DSI_E_OVERFLOW, "n_trials * bound^2 must stay below 2^64");
-  o.kd = (int64_t)kd;
-  if ((opt.flags & DSI_F_STRICT_EQ1) && ceil_div(o.t_t, o.kd) > c.sp_degree)
-    return bad(DSI_E_STRICT_EQ1, "Eq. 1 violated: ceil(t_t/(k t_d)) > SP");
-  o.a = c.accept_rate;
-  o.ut = c.t_target;
-  o.ud = c.t_drafter;
-  o.eq1 = dsi_eq1_feasible(o.t_t, o.t_d, c.lookahead, c.sp_degree);
-  o.min_k = dsi_min_lookahead(o.t_t, o.t_d, c.sp_degree);
-  o.thr = (uint64_t)(c.accept_rate * 4294967296.0);  // exact: a * 2^32, then floor
-  o.k = c.lookahead;
-  o.sp = c.sp_degree;
-  o.n = c.n_tokens;
-  o.stream_id = c.stream_id;
-  o.trials = c.n_trials;
-  return DSI_OK;
+  std::snprintf(buf, sizeof buf, "config %zu: %s", i, what);
+  return buf;
 }
 
-// S(b) = b k t_d for every b: Eq. 1 holds at min(SP, N), or SP >= N (no thread ever waits).
-bool config_noqueue(const CfgTicks &t) {
-  const int32_t sp_eff = std::min(t.sp, t.n);
-  return (t.t_t <= (int64_t)sp_eff * t.kd) || sp_eff >= t.n;
-}
-
-DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
-  DevCfg d{};
-  uint32_t mode = dsi::MODE_STREAM;
-  if (!pattern) {
-    if (t.thr >= (1ull << 32)) mode = dsi::MODE_ALL_ACCEPT;
-    else if (t.thr == 0) mode = dsi::MODE_ALL_REJECT;
-  }
-  const int32_t k_eff = std::min(t.k, t.n);
-  const int32_t sp_eff = std::min(t.sp, t.n);
-  const bool noqueue = config_noqueue(t);
-  d.thr = (uint32_t)std::min<uint64_t>(t.thr, 0xffffffffull);
-  const bool ttft = t.t_t1 != t.t_t || t.t_d1 != t.t_d;
-  // fresh-verifier variant: with k t_d <= t_t a fresh forward never finishes sooner than
-  // the regular thread (R24), so only k t_d > t_t configs take its cost table
-  const bool fresh_cfg = fresh && t.kd > t.t_t;
-  d.flags = mode | (noqueue ? dsi::CFG_NOQUEUE : 0u) | (ttft ? dsi::CFG_TTFT : 0u) |
-            (fresh_cfg ? dsi::CFG_FRESH : 0u);
-  d.t_d = (int32_t)t.t_d;
-  d.k = t.k;
-  if (t.eq1 == 1) d.flags |= dsi::CFG_EQ1;
-  d.nonsi = (int32_t)(t.t_t1 + (int64_t)(t.n - 1) * t.t_t);
-  d.e_si = (int32_t)((t.t_d1 - t.t_d) + (t.t_t1 - t.t_t));
-  d.t_t1 = (int32_t)t.t_t1;
-  d.ttft_shift = (int32_t)(t.t_d1 - t.t_d);
-  d.n_tokens = t.n;
-  d.k_eff = k_eff;
-  d.sp_eff = sp_eff;
-  d.t_t = (int32_t)t.t_t;
-  d.kd = (int32_t)t.kd;
-  d.si_cost = (int32_t)(t.kd + t.t_t);
-  // S(1) = max(k t_d, (1 mod SP) k t_d + floor(1/SP) t_t): k t_d, or max(k t_d, t_t) if SP = 1
-  d.s1 = (int32_t)(t.sp >= 2 ? t.kd : std::max(t.kd, t.t_t));
-  d.stream_id = t.stream_id;
-  uint32_t hi;
-  magic((uint32_t)k_eff + 1u, d.m_si, hi);  // k_eff + 1 >= 2: hi == 0
-  magic((uint32_t)k_eff, d.m_k_lo, d.m_k_hi);
-  magic((uint32_t)sp_eff, d.m_sp_lo, d.m_sp_hi);
-  d.n_trials = t.trials;
-  // floor(x / t_t) for x < 2^31: l = ceil(log2 t_t), m' = floor(2^32 (2^l - t_t) / t_t) + 1
-  {
-    const uint64_t tt = (uint64_t)t.t_t;
-    int l = 0;
-    while ((1ull << l) < tt) ++l;
-    d.m_tt = (uint32_t)((((1ull << 32) * ((1ull << l) - tt)) / tt + 1) & 0xffffffffull);
-    d.sh_tt = l;
-  }
-  return d;
+dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTicks &o, std::string &msg) {
+  const int code = dsi::convert_config(opt.tick, opt.flags, c, o);
+  if (code == 0) return DSI_OK;
+  msg = convert_message(i, code);
+  return (dsi_status)(code & 0xff);
 }
 
 // Relative cost of one trial-token: Philox (~10 instr) + compare (~1) + segment walk
@@ -304,17 +216,9 @@ dsi_status dsi_ticks(double x, double tick, int64_t *out) {
   return to_ticks(x, tick, out);
 }
 
-int32_t dsi_eq1_feasible(int64_t t_t, int64_t t_d, int32_t k, int32_t sp) {
-  if (t_t < 1 || t_d < 1 || k < 1 || sp < 1) return -1;
-  return ceil_div(t_t, (int64_t)k * t_d) <= sp ? 1 : 0;
-}
+int32_t dsi_eq1_feasible(int64_t t_t, int64_t t_d, int32_t k, int32_t sp) { return dsi::eq1_feasible(t_t, t_d, k, sp); }
 
-int32_t dsi_min_lookahead(int64_t t_t, int64_t t_d, int32_t sp) {
-  if (t_t < 1 || t_d < 1 || sp < 1) return -1;
-  // smallest k with ceil(t_t/(k t_d)) <= sp  <=>  k t_d sp >= t_t
-  const int64_t k = ceil_div(t_t, t_d * (int64_t)sp);
-  return (int32_t)std::max<int64_t>(1, k);
-}
+int32_t dsi_min_lookahead(int64_t t_t, int64_t t_d, int32_t sp) { return dsi::min_lookahead(t_t, t_d, sp); }
 
 int32_t dsi_required_processors(int64_t t_t, int64_t t_d, int32_t k) {
   if (t_t < 1 || t_d < 1 || k < 1) return -1;
