@@ -30,6 +30,18 @@ for flags in (0, D.DSI_F_SHARED_STREAMS):
         sim.run().heatmap()
         sim.run().reduce_device()
         sim.fetch(5, 20)
+# the device path of dsi_sim_update (dsi_stage.cu): validate + convert on the GPU, commit, and a
+# failing update (host path)
+upd = cells3.copy()
+upd["t_drafter"] = upd["t_drafter"] + 0.01
+with D.Simulator(cells3, tick=ctick3, seed=W.SEED) as sim:
+    sim.run().reduce()
+    sim.update(upd).run().reduce()
+    upd["t_drafter"][3] = 7.0
+    try:
+        sim.update(upd)
+    except D.DsiError:
+        pass
 ttft, ttick = W.cfg2_ttft(trials=50)  # the TTFT variant (first-segment tables)
 for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
     with D.Simulator(ttft[:6], tick=ttick, seed=W.SEED, flags=flags) as sim:
