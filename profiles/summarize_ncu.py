@@ -110,6 +110,14 @@ def full(name=None):
 out = {"round": R, "workload": "cfg3"}
 try:
     out["launch_list"] = launches()
+    # the bench line's value step is dsi_sim_run + dsi_sim_reduce: the default trial kernel plus the
+    # partition check; the trial kernel's share of that step (compare roofline.kernel_share_of_step)
+    ll = out["launch_list"]
+    trial = [v for k, v in ll.items() if "dsi_trial_kernel<0, 0, 0, 1, 0>" in k]
+    check = [v for k, v in ll.items() if "dsi_check_trials_kernel" in k]
+    if trial and check:
+        t, c = trial[0]["mean_ms"], check[0]["mean_ms"]
+        out["value_step_kernel_share"] = {"trial_kernel_mean_ms": t, "check_kernel_mean_ms": c, "share": t / (t + c)}
 except OSError as e:
     out["launch_list_error"] = str(e)
 try:
