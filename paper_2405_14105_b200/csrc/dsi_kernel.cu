@@ -49,6 +49,9 @@ constexpr int TABLE_MAX_N = 4096;
 #ifndef DSI_TRIAL_MINB
 #define DSI_TRIAL_MINB 5
 #endif
+#ifndef DSI_PIPE_WALK
+#define DSI_PIPE_WALK 1  // (cfg3 sample 243.16 -> 242.38 ms, profiles/r02_ab_pipewalk.jsonl)
+#endif
 #ifndef DSI_TRIAL_MAXT
 #define DSI_TRIAL_MAXT 128
 #endif  // larger N: arithmetic segment costs, per-call rounds 0-1
@@ -111,6 +114,21 @@ __device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint
     }
   }
   run = nv - 1 - (31 - __clz(R));  // ones above the last zero
+}
+
+// walk_word for a full word (32 valid positions) when no run strictly inside a word can be long
+// (Lk > 30): branch-free, so the compiler can schedule it among the next word's Philox calls.
+// T[0] = (0, 0) absorbs the common "no long run" case.
+__device__ __forceinline__ void walk_full_word_nb(uint32_t R, int Lk, const uint2 *T, int &run, int &n2, uint32_t &ai,
+                                                  uint32_t &ay) {
+  const uint32_t E = R & ~((R << 1) | (run == 0 ? 1u : 0u));
+  n2 += __popc(E);
+  const int z0 = __ffs(R) - 1;  // -1 when R == 0
+  const bool lng = (R != 0u) & (run + z0 >= Lk);
+  const uint2 e = T[lng ? run + z0 + 1 : 0];
+  ai += e.x;
+  ay += e.y;
+  run = R ? (int)__clz(R) : run + 32;  // ones above the last zero
 }
 
 // Shared-memory layout of the TABLE variant for a config with N tokens.
@@ -258,7 +276,32 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
                               // production: seg_long of every segment with g >= k+2)
     int odd = 0;       // fast1: segments of odd length so far
     uint32_t lzp = 0;  // fast1: parity of the last zero's position (the sentinel 0 is even)
-    for (int w = 0; w < nwords; ++w) {
+    int w_start = 0;
+#if DSI_PIPE_WALK
+    if (VAR == 0 && TABLE && !HIST && !PATTERN && stream && Lk > 30) {
+      // full words with the walk of word w-1 after the generation of word w, one straight-line block
+      auto gen_word = [&](int w) {
+        uint32_t R = 0u;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) R = pack4(R, philox_call(U[8 * w + j], th, P.keys), nthr);
+        return R;
+      };
+      const int nfull = npos >> 5;
+      if (nfull >= 1) {
+        uint32_t Rp = gen_word(0);
+        nz += __popc(Rp);
+        for (int w = 1; w < nfull; ++w) {
+          const uint32_t R = gen_word(w);
+          walk_full_word_nb(Rp, Lk, T, run, n2, ai, ay);
+          nz += __popc(R);
+          Rp = R;
+        }
+        walk_full_word_nb(Rp, Lk, T, run, n2, ai, ay);
+        w_start = nfull;
+      }
+    }
+#endif
+    for (int w = w_start; w < nwords; ++w) {
       uint32_t R;
       if (PATTERN) {
         R = ~trial;  // N <= 33: one word, A_p = bit p-1 of the trial index
