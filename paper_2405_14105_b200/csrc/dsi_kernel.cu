@@ -42,7 +42,8 @@ namespace {
 
 constexpr int TABLE_MAX_N = 4096;
 // Launch bounds: blocks of at most 128 threads, at least 5 per SM -- a register budget of
-// ~100 per thread, of which ptxas takes 78.  Measured (profiles/r01_ab_lb.jsonl, cfg3): 78
+// ~100 per thread, of which ptxas takes 91 with the pipelined walk (78 before it); round 2: a
+// minimum of 6 blocks (80 registers) 1.8% slower, of 4 the same (profiles/r02_ab_minb*.jsonl).  Measured (profiles/r01_ab_lb.jsonl, cfg3): 78
 // registers 244.1 ms, 84 (bounds (256, 1)) 246.0 ms, 58 (bounds (256), no minimum) 251.3 ms,
 // 70 / 64 / 48 registers 248.5 / 250.0 / 257.5 ms: more registers than the occupancy
 // heuristic picks keep more independent Philox calls in flight.
