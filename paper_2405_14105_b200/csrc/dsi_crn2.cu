@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_bsum[5];
   __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int s_kmin, s_nlong, s_wcnt[TH / 32];
+  __shared__ uint16_t s_long[TH];  // (non-FRESH) the tile's trials with a run longer than s_kmin
   const CrnUnit un = P.units[P.unit_begin + blockIdx.x];
   const CrnGroup G = P.groups[un.group];
   const int N = G.n_tokens;
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
   // itself, so the loads stay shared-memory loads)
   if (threadIdx.x < 5) s_bsum[threadIdx.x] = 0ull;
   if (threadIdx.x == 0) {
+    s_kmin = 1 << 30;
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -184,6 +187,9 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
 #pragma unroll
   for (int i = 0; i < kShortL - 1; ++i) sv_short[i] = fresh ? fresh_saving_lite(i + 2, l, f) : 0;
   __syncthreads();
+  if (!FRESH && (int)threadIdx.x < (int)un.count) atomicMin(&s_kmin, l.k_eff);
+  __syncthreads();
+  const int kmin = s_kmin;  // the block's smallest lookahead: shorter runs are long for none of it
 
   const uint64_t tile_a = un.t0 / TH, tile_b = (un.t1 + TH - 1) / TH;  // un.t0 is tile-aligned
   const unsigned char *rec0 = P.records + (P.group_tile0[un.group] + tile_a) * (uint64_t)P.rec_bytes;
@@ -215,6 +221,7 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
         reinterpret_cast<const uint16_t *>(bufc + (size_t)TH * (sizeof(uint4) + (FRESH ? sizeof(uint2) : 0)));
     const uint64_t tile0 = ti * TH;
     const int ntr = (int)(min(un.t1, tile0 + TH) - tile0);
+    bool has_long = false;
     if ((int)threadIdx.x < ntr) {  // the config-independent block sums, one trial per thread
       const uint4 v = summ[threadIdx.x];
       my_m += v.x;
@@ -222,6 +229,22 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
       my_mm += v.x * v.x;
       my_nn += v.y * v.y;
       my_mn += v.x * v.y;
+      has_long = (int)v.z > kmin;
+    }
+    if (!FRESH) {  // compact the trials that need a correction for some config of the block
+      const unsigned bal = __ballot_sync(0xffffffffu, has_long);
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      if (lane == 0) s_wcnt[warp] = __popc(bal);
+      __syncthreads();
+      int off = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < TH / 32; ++w) {
+        off += w < warp ? s_wcnt[w] : 0;
+        tot += s_wcnt[w];
+      }
+      if (has_long) s_long[off + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)threadIdx.x;
+      if (threadIdx.x == 0) s_nlong = tot;
+      __syncthreads();
     }
     // per-tile 32-bit partial sums (ai <= N/2, m <= N <= 2048, 256 trials: no overflow)
     uint32_t p_gtn = 0, p_gts = 0, p_ai = 0, p_ai2 = 0, p_mai = 0;
@@ -290,8 +313,42 @@ __global__ void __launch_bounds__(TH, DSI_EVAL_MINB) dsi_crn_eval_kernel(const C
       }
       if (s < ntr) visit(summ[s], s, gts_long_only);
     };
-    if (warp_gts_long_only) trials(std::true_type{});
-    else trials(std::false_type{});
+    // non-FRESH: a branch-free pass over every trial with the uncorrected latencies, then the
+    // corrections over the compacted trials with a run longer than the block's smallest k (the
+    // threshold counters re-decided there); the same integers as visit()
+    auto base = [&](const uint4 v, auto gts_long_only) {
+      const int dsi = (int)v.x * l.t_t + (int)v.y * l.s1;
+      p_gtn += (uint32_t)(l.nonsi - dsi) >> 31;
+      if (!decltype(gts_long_only)::value) p_gts += (uint32_t)(dsi > (int)v.x * l.si_cost);
+    };
+    auto split = [&](auto gts_long_only) {
+      int s = 0;
+      for (; s + 1 < ntr; s += 2) {
+        const uint4 v0 = summ[s], v1 = summ[s + 1];
+        base(v0, gts_long_only);
+        base(v1, gts_long_only);
+      }
+      if (s < ntr) base(summ[s], gts_long_only);
+      const int nl = s_nlong;
+      for (int j = 0; j < nl; ++j) {
+        const int s2 = s_long[j];
+        const uint4 v = summ[s2];
+        if ((int)v.z <= l.k_eff) continue;  // no run is long for this config
+        const int m = (int)v.x, n2 = (int)v.y;
+        const int dsi0 = m * l.t_t + n2 * l.s1, si0 = m * l.si_cost;
+        const uint32_t g0n = (uint32_t)(l.nonsi - dsi0) >> 31, g0s = (uint32_t)(si0 - dsi0) >> 31;
+        visit(v, s2, gts_long_only);  // adds the corrections and the corrected counters ...
+        p_gtn -= g0n;                 // ... the base pass counted the uncorrected ones
+        if (!decltype(gts_long_only)::value) p_gts -= g0s;
+      }
+    };
+    if (FRESH) {
+      if (warp_gts_long_only) trials(std::true_type{});
+      else trials(std::false_type{});
+    } else {
+      if (warp_gts_long_only) split(std::true_type{});
+      else split(std::false_type{});
+    }
     a_gtn += p_gtn;
     a_gts += p_gts;
     c_ai += p_ai;
