@@ -51,7 +51,21 @@ def _run_all(rank, world):
             res = sim.reduce()  # collective: every rank calls it (with REDUCE_TO_ROOT only rank 0's is filled)
             cells = sim.heatmap()
             hist = sim.hist(1) if flags & D.DSI_F_HIST else None
-        out[name] = (res, cells, hist)
+            # the heatmap's own exchange (cells, or the moments first) with no reduce before it, the
+            # deferred reduce, and an update (device path where eligible) of the drafter latencies
+            cells_first = sim.run().heatmap()
+            if not flags & D.DSI_F_HIST:
+                sim.run().reduce_device()
+                fetched = sim.fetch() if rank == 0 or not flags & D.DSI_F_REDUCE_TO_ROOT else None
+                new = cfgs.copy()
+                # (a new shared-stream plan may change the unit count, and a TTFT config may stop being
+                # one: both need a new handle by contract)
+                if not flags & D.DSI_F_SHARED_STREAMS and not np.any(cfgs["ttft_drafter"]):
+                    new["t_drafter"] = np.minimum(new["t_target"], new["t_drafter"] + tick)
+                upd = sim.update(new).run().reduce()
+            else:
+                fetched = upd = None
+        out[name] = (res, cells, hist, cells_first, fetched if rank == 0 else None, upd)
     mc, mtick = W.multi_fuzz(15, seed=5, trials=900)
     out["multi"] = (D.dsi_multi_simulate(mc, tick=mtick, seed=SEED, rank=rank, world=world)[0], None, None)
     return out
@@ -116,9 +130,12 @@ def test_two_ranks_on_one_gpu_equal_one_process():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    for name, (res, cells, hist) in want.items():
-        gres, gcells, ghist = got[0][name]
-        assert _same(gres, res), name
-        assert _same(gcells, cells), name
-        if hist is not None:
-            assert all(np.array_equal(x, y) for x, y in zip(ghist, hist)), name
+    for name, w in want.items():
+        g = got[0][name]
+        assert _same(g[0], w[0]), name
+        assert _same(g[1], w[1]), name
+        if w[2] is not None:
+            assert all(np.array_equal(x, y) for x, y in zip(g[2], w[2])), name
+        for i, what in ((3, "cells (heatmap exchange only)"), (4, "fetch after reduce_device"), (5, "after update")):
+            if i < len(w):
+                assert _same(g[i], w[i]), (name, what)
