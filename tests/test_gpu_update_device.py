@@ -110,3 +110,40 @@ def test_errors_are_the_host_paths_and_nothing_changes(flags):
             same(sim.run().reduce(), mid, ctx=field)  # the failed update changed nothing
         sim.update(cfgs)
         same(sim.run().reduce(), before, ctx="restored")
+
+
+@pytest.mark.parametrize("flags", [0, D.DSI_F_MEANS_ONLY, D.DSI_F_FRESH_VERIFIER])
+def test_random_update_sequence(flags):
+    """A sequence of random updates -- valid ones (new latencies, lookaheads, SP, acceptance) and
+    invalid ones (one field broken in one config) -- against fresh handles: every valid update
+    gives the fresh handle's results, every invalid one create's status and message, and leaves
+    the handle as it was."""
+    rng = np.random.default_rng(99)
+    cfgs, tick = W.fuzz(60, seed=21, trials=300)
+    cfgs["ttft_target"] = 0.0
+    cfgs["ttft_drafter"] = 0.0
+    cur = cfgs.copy()
+    with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
+        sim.run().reduce()
+        for step in range(10):
+            new = cur.copy()
+            if flags & D.DSI_F_MEANS_ONLY:  # (the groups: stream, a, N, T must stay)
+                new["t_drafter"] = np.maximum(1.0, np.minimum(new["t_target"], new["t_drafter"] + rng.integers(-3, 4, new.size)))
+                new["sp_degree"] = rng.integers(1, 9, new.size)
+            else:
+                new["accept_rate"] = np.round(rng.random(new.size), 2)
+                new["lookahead"] = np.minimum(new["lookahead"], rng.integers(1, 13, new.size))
+                new["t_drafter"] = np.maximum(1.0, np.minimum(new["t_target"], new["t_drafter"] + rng.integers(-3, 4, new.size)))
+            if step % 3 == 2:  # break one config
+                i = int(rng.integers(0, new.size))
+                new["t_drafter"][i] = new["t_target"][i] + 1.0
+                with pytest.raises(D.DsiError) as e:
+                    sim.update(new)
+                with pytest.raises(D.DsiError) as e2:
+                    D.Simulator(new, tick=tick, seed=W.SEED, flags=flags)
+                assert e.value.status == e2.value.status and str(e.value) == str(e2.value)
+                same(sim.run().reduce(), fresh(cur, tick, flags)[0], ctx=("kept", step))
+                continue
+            sim.update(new)
+            same(sim.run().reduce(), fresh(new, tick, flags)[0], ctx=("step", step))
+            cur = new
