@@ -80,7 +80,9 @@ typedef enum {
                                  draw identical indicators (the RNG contract): generate each
                                  trial's stream once per group and evaluate every config of the
                                  group on it.  Results are bit-identical to the default mode.
-                                 Not with PER_TRIAL, HIST or PATTERN; N <= 2048; no TTFT.      */
+                                 TTFT configs join no group: the per-config kernel runs them in
+                                 the same dsi_sim_run.  Not with PER_TRIAL, HIST or PATTERN;
+                                 N <= 2048.                                                     */
 #define DSI_F_FRESH_VERIFIER 0x40u /* fresh-verifier DSI variant (R24; Thm 2's proof
                                  P:445, "DSI either invokes a new current verifier thread or
                                  labels an existing thread"): whenever the committed prefix

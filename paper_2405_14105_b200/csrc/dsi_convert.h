@@ -89,7 +89,6 @@ DSI_HD int convert_config(double tick, uint32_t flags, const dsi_config &c, CfgT
     if (s != DSI_OK) DSI_CV_FAIL(CV_TTFT_DRAFTER, s);
   }
   if (o.t_d1 > o.t_t1) DSI_CV_FAIL(CV_ASSUMPTION2_FIRST, DSI_E_RANGE);
-  if ((flags & DSI_F_SHARED_STREAMS) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d)) DSI_CV_FAIL(CV_SHARED_TTFT, DSI_E_RANGE);
   if ((flags & DSI_F_FRESH_VERIFIER) && (o.t_t1 != o.t_t || o.t_d1 != o.t_d)) DSI_CV_FAIL(CV_FRESH_TTFT, DSI_E_RANGE);
   // every per-trial latency is <= N (k t_d + t_t) plus the first-forward surcharges
   // (kernel overflow bound)
@@ -192,7 +191,7 @@ DSI_HD DevCfg make_dev_cfg(const CfgTicks &t, bool pattern, bool fresh) {
 enum : unsigned int {
   STAGE_TTFT = 1u,             // some config has first-forward latencies (TTFT variant)
   STAGE_FRESH = 2u,            // some config is fresh-verifier (DSI_F_FRESH_VERIFIER and k t_d > t_t)
-  STAGE_PLAN_CHANGED = 4u,     // a shared-stream plan key changed (stream, a, N, T, k, t_t, t_d, SP)
+  STAGE_PLAN_CHANGED = 4u,     // a shared-stream plan key changed (stream, a, N, T, k, t_t, t_d, SP, TTFT)
   STAGE_GROUPS_CHANGED = 8u,   // a means-only group key changed (stream, a, N, T, TTFT or not)
   STAGE_CELLS_CHANGED = 16u,   // a heatmap-cell key changed (t_target, t_drafter, a as given, SP, N)
 };

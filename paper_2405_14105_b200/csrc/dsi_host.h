@@ -127,6 +127,7 @@ struct DeviceState {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ncclComm_t comm = nullptr;
   std::vector<std::pair<uint64_t, uint64_t>> ranges;  // [begin, end) units, one per shard
+  std::vector<std::pair<uint64_t, uint64_t>> ttft_ranges;  // shared-stream mode: per-config units of the TTFT configs
   dsi::SegGroup *d_seg_groups = nullptr;  // means-only mode: groups, unit prefix, config -> group,
   uint64_t *d_seg_prefix = nullptr;       //   segment-length histograms (bin 0 = trials)
   uint32_t *d_cfg_group = nullptr;
@@ -172,6 +173,8 @@ struct dsi_sim {
   bool use_nccl = false;                  // per-config moments summed across devices/ranks
   bool host_coll = false;                 // ... through the host all-reduce hook instead of NCCL
   std::vector<uint32_t> perm;
+  std::vector<uint32_t> shared_ttft;      // shared-stream mode: the TTFT configs (not shared; per-config kernel)
+  uint64_t ttft_units = 0;                //   their (config, tile) units, h->prefix / h->tile_trials
   std::vector<dsi::CrnGroup> groups;
   std::vector<dsi::CrnUnit> crn_units;
   int32_t cfg_per_block = 0, max_runs = 0;
@@ -367,7 +370,6 @@ void free_handle(dsi_sim *h);
 dsi_status upload(dsi_sim *h, bool plan = true, bool cfg_table = true);
 dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_units);
 dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks);
-bool same_plan_keys(const std::vector<CfgTicks> &a, const std::vector<CfgTicks> &b);
 dsi_status sum_across(dsi_sim *h, bool hist);
 dsi_status plan_two_pass(dsi_sim *h);
 dsi_status alloc_two_pass(dsi_sim *h);

@@ -171,8 +171,13 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
     h->perm.resize(n);
     for (size_t i = 0; i < n; ++i) h->perm[i] = (uint32_t)i;
     const auto &t = h->ticks;
+    // TTFT configs (first forwards cost more, R23) are not shared: their first segment has its own
+    // cost table per config, so they run through the per-config kernel (create plans their units);
+    // they sort to the end of the order and join no group
+    auto ttft = [&](uint32_t i) { return t[i].t_t1 != t[i].t_t || t[i].t_d1 != t[i].t_d; };
     std::stable_sort(h->perm.begin(), h->perm.end(), [&](uint32_t a, uint32_t b) {
       const CfgTicks &x = t[a], &y = t[b];
+      if (ttft(a) != ttft(b)) return !ttft(a);
       if (x.stream_id != y.stream_id) return x.stream_id < y.stream_id;
       if (x.thr != y.thr) return x.thr < y.thr;
       if (x.n != y.n) return x.n < y.n;
@@ -182,13 +187,17 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
       if (x.t_d != y.t_d) return x.t_d < y.t_d;
       return x.sp < y.sp;
     });
+    size_t n_plain = 0;
+    while (n_plain < n && !ttft(h->perm[n_plain])) ++n_plain;
+    h->shared_ttft.assign(h->perm.begin() + n_plain, h->perm.end());
+    std::sort(h->shared_ttft.begin(), h->shared_ttft.end());
     h->max_runs = h->max_n / 3 + 2;  // runs of >= 2 accepted drafts in one trial
     // groups first, then the block shape: configs per block follow the typical group size
     h->groups.clear();
-    for (size_t i = 0; i < n;) {
+    for (size_t i = 0; i < n_plain;) {
       const CfgTicks &k0 = t[h->perm[i]];
       size_t j = i + 1;
-      while (j < n) {
+      while (j < n_plain) {
         const CfgTicks &kj = t[h->perm[j]];
         if (kj.stream_id != k0.stream_id || kj.thr != k0.thr || kj.n != k0.n || kj.trials != k0.trials) break;
         ++j;
@@ -210,7 +219,7 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
     // 128 (profiles/r01_ab_crn_th.jsonl: cfg3 30.5 -> 26.0 ms; forced on cfg2/cfg4/cfg5, whose
     // groups hold 3 / 140 / 100 configs, 1.8-1.9x slower; 2 or 4 configs per thread were
     // slower too, profiles/r01_ab_crn*.jsonl)
-    const bool big_groups = n >= 256 * h->groups.size();
+    const bool big_groups = n_plain >= 256 * h->groups.size();
     int th = (big_groups && dsi::crn_kernel_smem(h->max_n, 256, 256, h->max_runs, h->any_fresh) <= 48 * 1024) ? 256 : kCrnThreads;
     if (knobs().crn_threads == 128 || knobs().crn_threads == 256) th = knobs().crn_threads;
     h->cfg_per_block = th;
@@ -245,7 +254,7 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
     const size_t slices = slices_v.size();
     const int total_devices = h->opt.world * h->opt.n_devices;
     const uint64_t target = 148ull * 4 * 4 * (uint64_t)total_devices;
-    const uint64_t split = std::max<uint64_t>(1, (target + slices - 1) / slices);
+    const uint64_t split = slices ? std::max<uint64_t>(1, (target + slices - 1) / slices) : 1;  // (all TTFT: no slice)
     h->crn_units.clear();
     cost.clear();
     h->n_sums_units = 0;
@@ -371,6 +380,7 @@ void plan_cell_owners(dsi_sim *h) {
     for (int q = 0; q < parts; ++q)
       for (uint64_t c = pb[q]; c < pb[q + 1]; ++c) owner[c] = q;
   } else if (h->shared) {  // a unit touches every config of its slice
+    if (!h->shared_ttft.empty()) return;  // (the TTFT configs' own units: the moments are exchanged)
     for (int q = 0; q < parts; ++q)
       for (uint64_t u = pb[q]; u < pb[q + 1]; ++u) {
         const dsi::CrnUnit &un = h->crn_units[u];

@@ -360,6 +360,18 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   } else if (shared) {
     s = plan_shared(h, crn_cost);
     if (s != DSI_OK) return abort_create(s);
+    // the TTFT configs' own (config, tile) units for the per-config kernel (zero units elsewhere)
+    uint64_t ttft_trials = 0;
+    for (const uint32_t c : h->shared_ttft) ttft_trials += h->ticks[c].trials;
+    const uint64_t r = std::min<uint64_t>(
+        128, std::max<uint64_t>(1, ttft_trials / ((uint64_t)kDefaultThreads * 148ull * 16 * 8 * total_devices)));
+    h->tile_trials = (uint32_t)(kDefaultThreads * r);
+    std::vector<char> is_ttft(n_cfg, 0);
+    for (const uint32_t c : h->shared_ttft) is_ttft[c] = 1;
+    h->prefix[0] = 0;
+    for (size_t i = 0; i < n_cfg; ++i)
+      h->prefix[i + 1] = h->prefix[i] + (is_ttft[i] ? (h->ticks[i].trials + h->tile_trials - 1) / h->tile_trials : 0);
+    h->ttft_units = h->prefix[n_cfg];
   } else {
     const uint64_t threads = (uint64_t)h->block_threads;
     const uint64_t target_blocks = 148ull * 16 * 8 * (uint64_t)total_devices;
@@ -425,6 +437,22 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
       }
     }
     h->part_bounds = bounds;
+  }
+  // shared-stream mode: the TTFT configs' per-config units, cost-balanced over the same parts
+  std::vector<uint64_t> ttft_bounds(parts + 1, 0);
+  if (shared && h->ttft_units) {
+    try {
+      std::vector<double> tc(h->ttft_units);
+      for (const uint32_t c : h->shared_ttft)
+        for (uint64_t u = h->prefix[c]; u < h->prefix[c + 1]; ++u) {
+          const uint64_t first = (u - h->prefix[c]) * h->tile_trials;
+          tc[u] = unit_cost(h->ticks[c], std::min<uint64_t>(h->tile_trials, h->ticks[c].trials - first));
+        }
+      dsi_shard_bounds(tc.data(), h->ttft_units, parts, ttft_bounds.data());
+    } catch (...) {
+      h->err = "host tables";
+      return abort_create(DSI_E_NOMEM);
+    }
   }
   tr.mark("plan+shard");
 
@@ -493,6 +521,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
     for (int sh = 0; sh < shards_per_dev; ++sh) {
       const int part = global_dev * shards_per_dev + sh;
       d.ranges.emplace_back(bounds[part], bounds[part + 1]);
+      if (shared && h->ttft_units) d.ttft_ranges.emplace_back(ttft_bounds[part], ttft_bounds[part + 1]);
       // means-only: part p also evaluates configs [cfg_bounds[p], cfg_bounds[p+1])
       if (means_only) d.cfg_ranges.emplace_back(h->cfg_bounds[part], h->cfg_bounds[part + 1]);
     }
@@ -646,17 +675,20 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
     std::vector<uint32_t> old_perm;
     std::vector<dsi::CrnGroup> old_groups;
     std::vector<dsi::CrnUnit> old_units;
+    std::vector<uint32_t> old_shared_ttft;
     h->ticks.swap(h->ticks_next);
     try {
       old_perm = h->perm;
       old_groups = h->groups;
       old_units = h->crn_units;
+      old_shared_ttft = h->shared_ttft;
       std::vector<double> cost;
       s = plan_shared(h, cost);
     } catch (...) {
       s = fail(h, DSI_E_NOMEM, "host tables");
     }
-    if (s == DSI_OK && (h->groups.size() != old_groups.size() || h->crn_units.size() != old_units.size()))
+    if (s == DSI_OK && (h->groups.size() != old_groups.size() || h->crn_units.size() != old_units.size() ||
+                        h->shared_ttft != old_shared_ttft))
       s = fail(h, DSI_E_RANGE, "DSI_F_SHARED_STREAMS: the stream grouping changed; create a new handle");
     if (s == DSI_OK) s = plan_two_pass(h);
     if (s == DSI_OK) {  // the buffers may grow: wait for any run still reading them
@@ -667,10 +699,11 @@ dsi_status dsi_sim_update(dsi_sim *h, const dsi_config *cfg, size_t n_cfg) {
       s = alloc_two_pass(h);
     }
     if (s != DSI_OK) {  // the handle keeps its previous configs and plan
-      if (!old_groups.empty()) {
+      if (!old_groups.empty() || !old_shared_ttft.empty()) {
         h->perm.swap(old_perm);
         h->groups.swap(old_groups);
         h->crn_units.swap(old_units);
+        h->shared_ttft.swap(old_shared_ttft);
       }
       h->cfg_per_block = old_cpb;
       h->max_runs = old_runs;
@@ -828,6 +861,13 @@ dsi_status dsi_sim_run(dsi_sim *h) {
           if (e) return cuda_fail(h, (cudaError_t)e, "shared-stream kernel launch");
           h->launches += 1;
         }
+      }
+      for (const auto &rg : d.ttft_ranges) {  // the TTFT configs: per-config kernel (TTFT variant)
+        if (rg.second <= rg.first) continue;
+        p.unit_begin = rg.first;
+        const int e = dsi::launch_trial_kernel(p, rg.second - rg.first, kDefaultThreads, false, false, false, d.stream);
+        if (e) return cuda_fail(h, (cudaError_t)e, "trial kernel launch (TTFT configs)");
+        h->launches += 1;
       }
     }
     for (const auto &rg : d.ranges) {

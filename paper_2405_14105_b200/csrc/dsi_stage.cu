@@ -42,7 +42,8 @@ __global__ void __launch_bounds__(256) dsi_stage_kernel(const StageParams P) {
     if (min(t.k, t.n) == 1 && config_noqueue(t)) work_k1 += w;
     // the keys dsi_sim_update compares on the host path (validate_all's UpdateKeys)
     const bool same_stream = t.stream_id == o.stream_id && t.thr == o.thr && t.n == o.n && t.trials == o.trials;
-    if (!(same_stream && t.k == o.k && t.t_t == o.t_t && t.t_d == o.t_d && t.sp == o.sp)) flags |= STAGE_PLAN_CHANGED;
+    if (!(same_stream && t.k == o.k && t.t_t == o.t_t && t.t_d == o.t_d && t.sp == o.sp && ttft_of(t) == ttft_of(o)))
+      flags |= STAGE_PLAN_CHANGED;
     if (!(same_stream && ttft_of(t) == ttft_of(o))) flags |= STAGE_GROUPS_CHANGED;
     if (!(t.ut == o.ut && t.ud == o.ud && t.a == o.a && t.sp == o.sp && t.n == o.n)) flags |= STAGE_CELLS_CHANGED;
   }

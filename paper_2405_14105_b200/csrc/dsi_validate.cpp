@@ -98,8 +98,9 @@ dsi_status validate_all(dsi_sim *h, const dsi_config *cfg, size_t n, std::vector
           msg = "config " + std::to_string(i) + ": n_trials (and, with DSI_F_HIST, min(k, N)) must not change";
         }
         const bool same_stream = t.stream_id == o.stream_id && t.thr == o.thr && t.n == o.n && t.trials == o.trials;
-        ps = ps && same_stream && t.k == o.k && t.t_t == o.t_t && t.t_d == o.t_d && t.sp == o.sp;
         const bool to = o.t_t1 != o.t_t || o.t_d1 != o.t_d, tn = t.t_t1 != t.t_t || t.t_d1 != t.t_d;
+        // (shared-stream mode: a TTFT config is not shared, so the flag is a plan key too)
+        ps = ps && same_stream && t.k == o.k && t.t_t == o.t_t && t.t_d == o.t_d && t.sp == o.sp && to == tn;
         gs = gs && same_stream && to == tn;
         cs = cs && t.ut == o.ut && t.ud == o.ud && t.a == o.a && t.sp == o.sp && t.n == o.n;
       }
@@ -168,21 +169,6 @@ dsi_status derive_limits(dsi_sim *h, const std::vector<CfgTicks> &ticks) {
   h->k1_fast = !lim.ttft && !lim.fresh && lim.work_k1 >= 0.25 * lim.work;
   if (knobs().k1_fast >= 0) h->k1_fast = !lim.ttft && !lim.fresh && knobs().k1_fast != 0;
   return DSI_OK;
-}
-
-// The shared-stream plan orders configs by these fields (plan_shared): an update that
-// keeps all of them keeps the plan.
-bool same_plan_keys(const std::vector<CfgTicks> &a, const std::vector<CfgTicks> &b) {
-  std::atomic<bool> same{true};
-  parallel_for(a.size(), [&](size_t lo, size_t hi) {
-    for (size_t i = lo; i < hi && same.load(std::memory_order_relaxed); ++i) {
-      const CfgTicks &x = a[i], &y = b[i];
-      if (x.stream_id != y.stream_id || x.thr != y.thr || x.n != y.n || x.trials != y.trials || x.k != y.k ||
-          x.t_t != y.t_t || x.t_d != y.t_d || x.sp != y.sp)
-        same = false;
-    }
-  });
-  return same;
 }
 
 }  // namespace dsih

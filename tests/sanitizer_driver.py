@@ -43,7 +43,7 @@ with D.Simulator(cells3, tick=ctick3, seed=W.SEED) as sim:
     except D.DsiError:
         pass
 ttft, ttick = W.cfg2_ttft(trials=50)  # the TTFT variant (first-segment tables)
-for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST):
+for flags in (0, D.DSI_F_PER_TRIAL | D.DSI_F_HIST, D.DSI_F_SHARED_STREAMS):
     with D.Simulator(ttft[:6], tick=ttick, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
 pat, _ = W.fuzz(4, seed=2, trials=64)

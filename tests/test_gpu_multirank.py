@@ -36,7 +36,8 @@ def _cases():
             ("hist", fz, ftick, D.DSI_F_HIST), ("shared", c3, tick3, D.DSI_F_SHARED_STREAMS),
             ("means", c3, tick3, D.DSI_F_MEANS_ONLY), ("means_ttft", ttft, ttick, D.DSI_F_MEANS_ONLY),
             ("fresh", fz, ftick, D.DSI_F_FRESH_VERIFIER),
-            ("shared_fresh", c3, tick3, D.DSI_F_SHARED_STREAMS | D.DSI_F_FRESH_VERIFIER)]
+            ("shared_fresh", c3, tick3, D.DSI_F_SHARED_STREAMS | D.DSI_F_FRESH_VERIFIER),
+            ("shared_ttft", ttft, ttick, D.DSI_F_SHARED_STREAMS)]
 
 
 CURRENT = {"case": None}

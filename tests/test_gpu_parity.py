@@ -253,6 +253,55 @@ def test_shared_streams_bit_identical_to_default(name, fresh):
     sim.close()
 
 
+@pytest.mark.parametrize("mix", ["ttft_only", "mixed", "mixed_big_groups"])
+def test_shared_streams_with_ttft_configs(mix):
+    """TTFT configs (first forwards, R23) in the shared-stream mode: they join no group and run
+    through the per-config kernel's TTFT variant in the same dsi_sim_run, the other configs share
+    their streams; every moment equals the per-config mode's, heatmap cells too, and an update
+    that keeps which configs are TTFT works (one that changes it asks for a new handle)."""
+    ttft, ttick = W.cfg2_ttft(trials=900)
+    if mix == "ttft_only":
+        cfgs, tick = ttft, ttick
+    else:
+        plain = ttft.copy()
+        plain["ttft_target"] = 0.0
+        plain["ttft_drafter"] = 0.0
+        plain["stream_id"] = 1
+        if mix == "mixed_big_groups":  # 256-thread two-pass plan for the shared part
+            big, _ = W.cfg3(trials=900, k_max=12, cells=slice(0, 2525))
+            big["t_target"] *= 10.0
+            big["t_drafter"] *= 10.0  # (ticks of 0.001 ms: 0.1 ms steps)
+            plain = np.concatenate([plain, big])
+        cfgs = np.concatenate([ttft[::2], plain, ttft[1::2]])
+        tick = ttick
+    _, base = run_sim(cfgs, tick, flags=0)
+    sim, res = run_sim(cfgs, tick, flags=D.DSI_F_SHARED_STREAMS)
+    for f in MOMENTS:
+        assert np.array_equal(res[f], base[f]), (mix, f)
+    base_cells = D.dsi_heatmap(cfgs, base)
+    cells = sim.run().heatmap()
+    for f in cells.dtype.names:
+        assert np.array_equal(cells[f], base_cells[f], equal_nan=cells[f].dtype.kind == "f"), (mix, f)
+    new = cfgs.copy()
+    # (a TTFT config is one whose first forwards differ from the later ones: R23)
+    is_ttft = (((new["ttft_target"] != 0) & (np.abs(new["ttft_target"] - new["t_target"]) > 1e-9)) |
+               ((new["ttft_drafter"] != 0) & (np.abs(new["ttft_drafter"] - new["t_drafter"]) > 1e-9)))
+    new["t_target"] = new["t_target"] + 0.1 * is_ttft  # (the shared part's plan stays)
+    sim.update(new)
+    got = sim.run().reduce()
+    _, want = run_sim(new, tick, flags=0)
+    for f in MOMENTS:
+        assert np.array_equal(got[f], want[f]), (mix, "update", f)
+    flip = new.copy()
+    i0 = int(np.nonzero(is_ttft)[0][0])
+    flip["ttft_target"][i0] = 0.0  # config i0 stops being a TTFT config
+    flip["ttft_drafter"][i0] = 0.0
+    with pytest.raises(D.DsiError) as e:
+        sim.update(flip)
+    assert e.value.status == D.DSI_E_RANGE and "create a new handle" in str(e.value)
+    sim.close()
+
+
 @pytest.mark.parametrize("fresh", [False, True], ids=["R1", "R24"])
 def test_shared_streams_against_oracle_sample(fresh):
     cfgs, tick = W.cfg3(trials=700, k_max=200, cells=slice(5, 10100, 1001))
