@@ -1,4 +1,4 @@
-// dsi_device.h -- layout shared by the host runtime (dsi_host.cpp) and the
+// dsi_device.h -- layout shared by the host runtime (dsi_*.cpp) and the
 // sm_100a trial kernel (dsi_kernel.cu).  Internal: not part of the C ABI.
 #pragma once
 #include <stddef.h>
