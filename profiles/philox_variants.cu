@@ -105,6 +105,59 @@ __device__ __forceinline__ uint32_t pack4(uint32_t rej, const uint4 &u, uint32_t
   return rej;
 }
 
+// Two words' calls (16) in one unrolled block before either is packed: more independent chains
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) kern2(Keys K, int trials, uint32_t thr, unsigned long long *out) {
+  __shared__ uint4 U[26];
+  if (threadIdx.x < 25) {
+    const uint32_t q = threadIdx.x;
+    const uint64_t p = (uint64_t)M0 * q;
+    const uint32_t n2 = (uint32_t)(p >> 32) ^ 0u ^ K.k1[0];
+    const uint64_t b = (uint64_t)M1 * n2;
+    U[q] = make_uint4((uint32_t)(b >> 32) ^ K.k0[1], (uint32_t)b, (uint32_t)p ^ K.k1[1], 0u);
+  }
+  __syncthreads();
+  const uint32_t nthr = 0u - thr;
+  uint32_t acc = 0;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int t = 0; t < trials; ++t) {
+    const uint32_t trial = tid * trials + t;
+    const uint64_t p = (uint64_t)M1 * trial;
+    const uint32_t n1 = (uint32_t)p, n0 = (uint32_t)(p >> 32) ^ K.k0[0];
+    const uint64_t a = (uint64_t)M0 * n0;
+    const uint32_t ha = (uint32_t)(a >> 32), la = (uint32_t)a;
+    // words 0 and 1 together, then word 2 alone, then the last (1 call)
+    {
+      uint4 w[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint4 u = U[j];
+        w[j] = rounds_2_9<false, false>(u.x ^ n1, u.y, ha ^ u.z, la, K);
+      }
+      uint32_t R0 = 0, R1 = 0;
+#pragma unroll
+      for (int j = 7; j >= 0; --j) R0 = pack4<0>(R0, w[j], nthr, thr);
+#pragma unroll
+      for (int j = 15; j >= 8; --j) R1 = pack4<0>(R1, w[j], nthr, thr);
+      acc += __popc(R0) + __popc(R1);
+    }
+    {
+      uint32_t R = 0;
+#pragma unroll
+      for (int j = 7; j >= 0; --j) {
+        const uint4 u = U[16 + j];
+        R = pack4<0>(R, rounds_2_9<false, false>(u.x ^ n1, u.y, ha ^ u.z, la, K), nthr, thr);
+      }
+      acc += __popc(R);
+    }
+    {
+      const uint4 u = U[24];
+      acc += __popc(pack4<0>(0, rounds_2_9<false, false>(u.x ^ n1, u.y, ha ^ u.z, la, K), nthr, thr) & 7u);
+    }
+  }
+  atomicAdd(out, (unsigned long long)acc);
+}
+
 template <bool DA, bool DB, int P>
 __global__ void __launch_bounds__(128, 5) kern(Keys K, int trials, uint32_t thr, unsigned long long *out) {
   __shared__ uint4 U[26];
@@ -187,6 +240,33 @@ void run(const char *name, const Keys &K, unsigned long long want, int sms) {
   cudaFree(d);
 }
 
+template <int MINB>
+void run2(const char *name, const Keys &K, unsigned long long want, int sms) {
+  unsigned long long *d;
+  cudaMalloc(&d, 8);
+  const int trials = 64, blocks = sms * 5 * 8;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  unsigned long long got = 0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaMemset(d, 0, 8);
+    cudaEventRecord(a);
+    kern2<MINB><<<blocks, 128>>>(K, trials, THR, d);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep) best = ms < best ? ms : best;
+    cudaMemcpy(&got, d, 8, cudaMemcpyDeviceToHost);
+  }
+  const double tt = (double)blocks * 128 * trials * 100;
+  printf("{\"variant\": \"%s\", \"ms\": %.3f, \"trial_tokens_per_s\": %.4e, \"popcount\": %llu, \"ok\": %s}\n", name,
+         best, tt / (best * 1e-3), got, (want == 0 || got == want) ? "true" : "false");
+  cudaFree(d);
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -215,6 +295,9 @@ int main() {
     cudaFree(d);
   }
   run<false, false, 0>("W W, carry pack (current)", K, ref, sms);
+  run2<5>("W W, carry pack, two words' 16 calls before packing (min 5 blocks)", K, ref, sms);
+  run2<4>("W W, carry pack, two words' 16 calls before packing (min 4 blocks)", K, ref, sms);
+  run2<3>("W W, carry pack, two words' 16 calls before packing (min 3 blocks)", K, ref, sms);
   run<false, false, 2>("W W, sign-funnel pack (even threshold)", K, ref, sms);
   run<false, false, 3>("W W, 2 carry + 2 borrow-funnel bits (exact)", K, ref, sms);
   run<false, false, 1>("W W, compare pack", K, ref, sms);
