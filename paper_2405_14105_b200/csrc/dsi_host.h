@@ -232,6 +232,7 @@ std::string convert_message(size_t i, int code);
 using dsi::config_noqueue;
 using dsi::make_dev_cfg;
 double unit_cost(const CfgTicks &t, uint64_t trials);
+double shared_eval_cost(const CfgTicks &t, bool fresh, bool two_pass);
 
 // Every API call is an NVTX range (nvtx3, header-only: a no-op unless a profiler such as
 // ncu or nsys injects its NVTX handler), and each phase an NVTX mark; with DSI_TRACE=1 in the
@@ -375,7 +376,8 @@ dsi_status plan_two_pass(dsi_sim *h);
 dsi_status alloc_two_pass(dsi_sim *h);
 dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost);
 void plan_heat_cells(dsi_sim *h);
-bool snap_bounds(std::vector<uint64_t> &bounds, const std::vector<double> &cost, const std::vector<uint64_t> &cand);
+bool snap_bounds(std::vector<uint64_t> &bounds, const std::vector<double> &cost, const std::vector<uint64_t> &cand,
+                 double slack);
 void plan_cell_owners(dsi_sim *h);
 dsi_status ensure_ticks(dsi_sim *h);
 bool cells_aligned(const dsi_sim *h);

@@ -3,6 +3,7 @@
 #include "dsi_host.h"
 
 #include <algorithm>
+#include <cmath>
 
 using namespace dsih;
 
@@ -127,16 +128,21 @@ dsi_status plan_means(dsi_sim *h, std::vector<double> &cost, uint64_t target_uni
   return DSI_OK;
 }
 
+// The two-pass form needs 256-thread blocks, pass 2's two tile buffers within room for 3 blocks
+// per SM (its register budget) and, with the fresh-verifier layout's 6-bit short-run counts, at
+// most 63 stored runs per trial.
+static bool two_pass_eligible(const dsi_sim *h, int th) {
+  const bool ok = th == 256 && dsi::crn_eval_smem(h->max_runs, th, h->any_fresh) <= 64 * 1024 &&
+                  (!h->any_fresh || h->max_runs <= 63);
+  return knobs().crn_two_pass >= 0 ? ok && knobs().crn_two_pass != 0 : ok;
+}
+
 // Two-pass shared-stream mode (dsi_crn2.cu): records of (group, tile of TH trials), and
 // for every device the tiles its units read (pass 1 writes exactly those).  Requires
 // h->crn_units and the devices' unit ranges.
 dsi_status plan_two_pass(dsi_sim *h) {
   const int th = h->cfg_per_block;
-  // pass 2's two tile buffers must leave room for 3 blocks per SM (its register budget)
-  // (the fresh-verifier layout's 6-bit short-run counts need at most 63 stored runs per trial)
-  h->two_pass = th == 256 && dsi::crn_eval_smem(h->max_runs, th, h->any_fresh) <= 64 * 1024 &&
-                (!h->any_fresh || h->max_runs <= 63);
-  if (knobs().crn_two_pass >= 0) h->two_pass = h->two_pass && knobs().crn_two_pass != 0;
+  h->two_pass = two_pass_eligible(h, th);
   if (!h->two_pass) return DSI_OK;
   try {
     h->rec_bytes = (uint32_t)dsi::crn_record_bytes(h->max_runs, th, h->any_fresh);
@@ -252,9 +258,33 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
       }
     }
     const size_t slices = slices_v.size();
+    // unit costs per trial (unit_cost's picoseconds): pass 2 sums its configs' shared_eval_cost;
+    // the stream pass (Philox only when 0 < a < 1) runs once per group in the two-pass form
+    // (~1.3 ps per token with the record writes: cfg3's pass 1, 0.134 ms for 10^8 trial-tokens;
+    // each slice takes its share) and once per slice in the fused form (~0.62 ps per token)
+    const bool two = two_pass_eligible(h, th);
+    std::vector<double> eval_cost(slices, 0.0);
+    for (size_t q = 0; q < slices; ++q)
+      for (uint32_t p = slices_v[q].begin; p < slices_v[q].begin + slices_v[q].count; ++p)
+        eval_cost[q] += shared_eval_cost(t[h->perm[p]], (h->opt.flags & DSI_F_FRESH_VERIFIER) != 0, two);
+    auto stream_cost = [&](const Slice &sl) {
+      const dsi::CrnGroup &g = h->groups[sl.group];
+      const bool st = g.mode == dsi::MODE_STREAM;
+      return two ? (double)g.n_tokens * (st ? 1.3 : 0.05) * sl.count / g.count
+                 : (double)g.n_tokens * (st ? 0.62 : 0.05);
+    };
     const int total_devices = h->opt.world * h->opt.n_devices;
     const uint64_t target = 148ull * 4 * 4 * (uint64_t)total_devices;
     const uint64_t split = slices ? std::max<uint64_t>(1, (target + slices - 1) / slices) : 1;  // (all TTFT: no slice)
+    // a slice's trials are also cut until no unit costs more than 1/8 of a wave of blocks
+    // (148 SMs x 3 resident blocks) on every device: one block is one unit, so the costliest
+    // slices (a ~ 0.5-0.9 at small k: ~10x the cheapest) would otherwise run as a tail of long
+    // blocks that no shard count shortens (profiles/r02_split_probe*: cfg3, half the blocks
+    // took 80% of the time)
+    double total_cost = 0.0;
+    for (size_t q = 0; q < slices; ++q)
+      total_cost += (double)h->groups[slices_v[q].group].n_trials * (stream_cost(slices_v[q]) + eval_cost[q]);
+    const double cap = total_cost / (148.0 * 3 * 8 * total_devices);
     h->crn_units.clear();
     cost.clear();
     h->n_sums_units = 0;
@@ -264,7 +294,9 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
         if (sl.sums != (pass == 0)) continue;
         const dsi::CrnGroup &g = h->groups[sl.group];
         const uint64_t tiles = (g.n_trials + th - 1) / th;
-        const uint64_t nchunks = std::min<uint64_t>(split, tiles);
+        const double sc = (double)g.n_trials * (stream_cost(sl) + eval_cost[&sl - slices_v.data()]);
+        const uint64_t by_cost = cap > 0.0 ? (uint64_t)std::ceil(sc / cap) : 1;
+        const uint64_t nchunks = std::min<uint64_t>(std::max(split, by_cost), tiles);
         for (uint64_t c = 0; c < nchunks; ++c) {
           dsi::CrnUnit u{};
           u.group = sl.group;
@@ -285,8 +317,7 @@ dsi_status plan_shared(dsi_sim *h, std::vector<double> &cost) {
             }
             h->max_runs_normal = std::max<int32_t>(h->max_runs_normal, (g.n_tokens - 1) / (kmin + 2) + 1);
           }
-          // phase 1 (one stream pass per trial) + phase 2 (each config on every trial)
-          cost.push_back((double)(u.t1 - u.t0) * ((double)g.n_tokens * 12.0 + (double)sl.count * 25.0));
+          cost.push_back((double)(u.t1 - u.t0) * (stream_cost(sl) + eval_cost[&sl - slices_v.data()]));
         }
       }
     }
@@ -330,32 +361,50 @@ void plan_heat_cells(dsi_sim *h) {
     h->heat_cells[j].count = (uint32_t)((j + 1 < nc ? h->heat_cells[j + 1].first : n) - h->heat_cells[j].first);
 }
 
-// Snap the interior shard bounds to candidate unit indices (sorted) -- each to the candidate
-// nearest in cumulative cost -- if that raises the largest part's cost by at most 4%.  The
-// candidates are heatmap-cell starts (per-config mode) or group starts (shared-stream mode), so a
-// snapped part holds whole cells (SURVEY 8(e)'s cell-aligned option).  Returns whether it snapped.
-bool snap_bounds(std::vector<uint64_t> &bounds, const std::vector<double> &cost, const std::vector<uint64_t> &cand) {
+// Snap the shard bounds to candidate unit indices (sorted): the partition whose bounds are all
+// candidates and whose largest part costs least (bisection on that cost; a part is extended
+// greedily to the furthest candidate within it), taken if its largest part costs at most 4% or
+// `slack` (the exchange it saves, in cost units) more than the unsnapped one's.  The candidates
+// are heatmap-cell starts (per-config mode) or group starts (shared-stream mode), so a snapped
+// part holds whole cells (SURVEY 8(e)'s cell-aligned option).  Returns whether it snapped.
+bool snap_bounds(std::vector<uint64_t> &bounds, const std::vector<double> &cost, const std::vector<uint64_t> &cand,
+                 double slack) {
   const size_t parts = bounds.size() - 1, n = cost.size();
   if (parts < 2 || cand.empty()) return parts < 2;
   std::vector<double> pre(n + 1, 0.0);
   for (size_t u = 0; u < n; ++u) pre[u + 1] = pre[u] + cost[u];
-  auto max_part = [&](const std::vector<uint64_t> &b) {
-    double m = 0.0;
-    for (size_t q = 0; q < parts; ++q) m = std::max(m, pre[b[q + 1]] - pre[b[q]]);
-    return m;
-  };
-  std::vector<uint64_t> nb(bounds);
-  for (size_t q = 1; q < parts; ++q) {
-    auto it = std::lower_bound(cand.begin(), cand.end(), bounds[q]);
-    uint64_t best = it == cand.end() ? n : *it;
-    if (it != cand.begin()) {
-      const uint64_t below = *(it - 1);
-      if (it == cand.end() || pre[bounds[q]] - pre[below] < pre[best] - pre[bounds[q]]) best = below;
+  double cur = 0.0;
+  for (size_t q = 0; q < parts; ++q) cur = std::max(cur, pre[bounds[q + 1]] - pre[bounds[q]]);
+  std::vector<uint64_t> cuts;  // the candidates strictly inside (0, n), then n
+  for (const uint64_t c : cand)
+    if (c > 0 && c < n && (cuts.empty() || c > cuts.back())) cuts.push_back(c);
+  cuts.push_back(n);
+  // greedy partition with parts of cost <= T; false if it needs more than `parts` parts
+  auto fit = [&](double T, std::vector<uint64_t> *out) {
+    uint64_t s = 0;
+    size_t q = 0;
+    if (out) out->assign(parts + 1, n), (*out)[0] = 0;
+    while (s < n) {
+      if (q == parts) return false;
+      // the furthest cut c > s with pre[c] - pre[s] <= T
+      auto it = std::upper_bound(cuts.begin(), cuts.end(), s);
+      auto lim = std::upper_bound(it, cuts.end(), pre[s] + T, [&](double v, uint64_t c) { return v < pre[c]; });
+      if (lim == it) return false;
+      s = *(lim - 1);
+      if (out) (*out)[++q] = s;
+      else ++q;
     }
-    nb[q] = std::max(best, nb[q - 1]);
+    return true;
+  };
+  double lo = pre[n] / parts, hi = pre[n];
+  if (!fit(hi, nullptr)) return false;
+  for (int it = 0; it < 100 && hi - lo > 1e-9 * hi; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    (fit(mid, nullptr) ? hi : lo) = mid;
   }
-  nb[parts] = n;
-  if (max_part(nb) > 1.04 * max_part(bounds)) return false;
+  if (hi > std::max(1.04 * cur, cur + slack)) return false;
+  std::vector<uint64_t> nb;
+  fit(hi, &nb);
   bounds.swap(nb);
   return true;
 }

@@ -430,7 +430,10 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
         } else {
           for (const dsi::HeatCell &c : h->heat_cells) cand.push_back(h->prefix[c.first]);
         }
-        snap_bounds(bounds, cost, cand);
+        // the exchange a snapped partition saves: the 64-byte moments of every config through an
+        // all-reduce at ~400 GB/s, 0.16 ns per config -- 160 cost units (1 unit ~ 1 ps of kernel
+        // time, profiles/r02_cost_probe*.jsonl)
+        snap_bounds(bounds, cost, cand, 160.0 * (double)n_cfg);
       } catch (...) {
         h->err = "host tables";
         return abort_create(DSI_E_NOMEM);

@@ -2,7 +2,9 @@
 // config rows, launch limits and the Eq. 1 planner helpers.
 #include "dsi_host.h"
 
+#include <algorithm>
 #include <atomic>
+#include <cmath>
 
 using namespace dsih;
 
@@ -66,10 +68,44 @@ dsi_status convert(const dsi_options &opt, const dsi_config &c, size_t i, CfgTic
   return (dsi_status)(code & 0xff);
 }
 
-// Relative cost of one trial-token: Philox (~10 instr) + compare (~1) + segment walk
-// (~10 instr per rejection, expected (1-a) per token), SURVEY 8(d).4.
+// The sharder's cost models, in picoseconds of kernel time on one B200, fitted to measured
+// launches of >= ~1 ms (profiles/r02_cost_probe_v2.jsonl, r02_cost_probe_shared_v2.jsonl: grids
+// of identical-shape configs, a in {0 .. 1}, k in {1, 2, 5, 20, 200}, N in {100, 1000}).
+//
+// Per-config kernel, one trial of N tokens: the Philox draw dominates and is paid only when
+// 0 < a < 1 (~0.6-0.75 ps per token, almost independent of a); all-reject and all-accept
+// configs cost ~0.03-0.15.  A lookahead 2 <= k_eff <= 30 adds the segment walk (+0.07, most at
+// a ~ 0.5-0.7); k = 1 and k_eff > 30 (the closed per-word path) do not.
 double unit_cost(const CfgTicks &t, uint64_t trials) {
-  return (double)trials * (double)t.n * (11.0 + 10.0 * (1.0 - t.a));
+  const int32_t keff = std::min(t.k, t.n);
+  const bool walk = keff >= 2 && keff <= 30;
+  double c;
+  if (t.thr == 0) c = keff == 1 ? 0.075 : (walk ? 0.13 : 0.09);  // all reject
+  else if (t.thr >= (1ull << 32)) c = keff == 1 ? 0.03 : 0.06;    // all accept
+  else c = 0.62 + (walk ? 0.07 + 0.2 * t.a * (1.0 - t.a) : 0.0);
+  return (double)trials * (double)t.n * c;
+}
+
+// Shared-stream mode, pass 2, one trial of one config: the record scan (linear in N, more with
+// a run list: 0 < a < 1), then per trial with a stored run of L > k_eff (every run of L >= 2
+// for a fresh-verifier config; P = 1 - exp(-E[runs]), E[runs] = (N(1-a) + 1) a^(k+1)) a visit
+// growing with the runs' length, plus a correction per run.  The two forms differ (two-pass:
+// N = 100 fit, median model/measured 1.01, range 0.88-1.10; fused 128-thread form: N = 1000
+// fit, 1.00, 0.75-1.26); the fused form's own stream pass is costed per slice by the caller.
+double shared_eval_cost(const CfgTicks &t, bool fresh, bool two_pass) {
+  const double n = t.n, a = t.a;
+  const int32_t keff = (fresh && t.kd > t.t_t) ? 1 : std::min(t.k, t.n);
+  const bool stream = t.thr != 0 && t.thr < (1ull << 32);
+  const double runs = (t.thr == 0 || keff + 1 > t.n)
+                          ? 0.0 : std::min(n / (keff + 1.0), (n * (1.0 - a) + 1.0) * std::pow(a, keff + 1.0));
+  const double p_any = 1.0 - std::exp(-runs);
+  const double len = a < 1.0 ? std::min(n, 1.0 / (1.0 - a)) : n;
+  const bool one = keff == 1;
+  if (two_pass)
+    return n * (0.0040 + (stream ? 0.00011 : 0.0)) + p_any * ((one ? 1.78 : 2.43) + 0.0063 * len) +
+           runs * (one ? 0.143 : 0.68);
+  return n * (0.00185 + (stream ? 0.0014 : 0.0)) + p_any * ((one ? 1.155 : 0.196) + 0.0006 * len) +
+         runs * (one ? 0.30 : 0.18);
 }
 
 // Validate every config into ticks; on failure h->err names the first bad config.
