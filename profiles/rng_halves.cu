@@ -1,0 +1,237 @@
+// rng_halves.cu -- ceiling of a Bernoulli contract that spends 16 random bits per decision
+// (measurement tool, not product code).  Same structure as philox_variants.cu: rounds 0-1 split
+// into a per-trial half (registers) and a per-counter half (shared-memory table), the rejection
+// mask packed 32 positions per word, popcount accumulated.
+//
+// Contract "halves" (exactly the same Bernoulli(thr / 2^32) as the 32-bit contract, different
+// stream layout): call q = (p-1) >> 3 of counter (q, 0, trial, stream) serves 8 positions; position
+// j = (p-1) & 7 takes v = hi16(u[j]) for j < 4, lo16(u[j-4]) for j >= 4.  With thr = T 2^16 + R:
+// accept iff v < T, or v == T and w < R, where w is the same half of the same word of the call
+// (q, 1, trial, stream) (the "tie-break" call, needed with probability 2^-16 per position).
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/rh profiles/rng_halves.cu
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+
+struct Keys {
+  uint32_t k0[10], k1[10];
+};
+
+__host__ __device__ inline void philox_full(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const Keys &K,
+                                            uint32_t out[4]) {
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t a = (uint64_t)M0 * c0, b = (uint64_t)M1 * c2;
+    const uint32_t n0 = (uint32_t)(b >> 32) ^ c1 ^ K.k0[r], n2 = (uint32_t)(a >> 32) ^ c3 ^ K.k1[r];
+    c1 = (uint32_t)b;
+    c3 = (uint32_t)a;
+    c0 = n0;
+    c2 = n2;
+  }
+  out[0] = c0, out[1] = c1, out[2] = c2, out[3] = c3;
+}
+
+__device__ __forceinline__ uint4 rounds_2_9(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const Keys &K) {
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {
+    const uint64_t a = (uint64_t)M0 * c0;
+    const uint64_t b = (uint64_t)M1 * c2;
+    const uint32_t n0 = (uint32_t)(b >> 32) ^ c1 ^ K.k0[r];
+    const uint32_t n2 = (uint32_t)(a >> 32) ^ c3 ^ K.k1[r];
+    c1 = (uint32_t)b;
+    c3 = (uint32_t)a;
+    c0 = n0;
+    c2 = n2;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+// 32-bit contract (the product's): 4 decisions per call
+__device__ __forceinline__ uint32_t pack4(uint32_t rej, const uint4 &u, uint32_t nthr) {
+  asm("{\n\t.reg .u32 t;\n\t"
+      "add.cc.u32 t, %1, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %2, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %3, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %4, %5;\n\taddc.u32 %0, %0, %0;\n\t}"
+      : "+r"(rej)
+      : "r"(u.w), "r"(u.z), "r"(u.y), "r"(u.x), "r"(nthr));
+  return rej;
+}
+
+// halves: 8 decisions per call, rejection bit = [v >= T] (ties counted as rejections, fixed
+// later), bit order (LSB first) hi(x) hi(y) hi(z) hi(w) lo(x) lo(y) lo(z) lo(w); the carry-chain
+// sums t = v - T (mod 2^16) in the high half, so a tie is t < 2^16: tmin = min over the sums.
+__device__ __forceinline__ uint32_t pack8(uint32_t rej, const uint4 &u, uint32_t C, uint32_t &tmin) {
+  uint32_t t0, t1, t2, t3, t4, t5, t6, t7;
+  const uint32_t lx = u.x << 16, ly = u.y << 16, lz = u.z << 16, lw = u.w << 16;
+  asm("add.cc.u32 %1, %9, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %2, %10, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %3, %11, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %4, %12, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %5, %13, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %6, %14, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %7, %15, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 %8, %16, %17;\n\taddc.u32 %0, %0, %0;\n\t"
+      : "+r"(rej), "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3), "=r"(t4), "=r"(t5), "=r"(t6), "=r"(t7)
+      : "r"(lw), "r"(lz), "r"(ly), "r"(lx), "r"(u.w), "r"(u.z), "r"(u.y), "r"(u.x), "r"(C));
+  tmin = min(min(min(t0, t1), t2), min(min(t3, t4), min(t5, min(t6, min(t7, tmin)))));
+  return rej;
+}
+
+// exact per-position decision (slow reference), position j of call (q, trial)
+__device__ __forceinline__ bool reject_ref(uint32_t q, uint32_t j, uint32_t trial, uint32_t thr, const Keys &K) {
+  uint32_t o[4], t[4];
+  philox_full(q, 0, trial, 0, K, o);
+  const uint32_t wv = o[j & 3];
+  const uint32_t v = j < 4 ? wv >> 16 : wv & 0xFFFFu;
+  const uint32_t T = thr >> 16, R = thr & 0xFFFFu;
+  if (v != T) return v > T;
+  philox_full(q, 1, trial, 0, K, t);
+  const uint32_t ww = t[j & 3];
+  const uint32_t w = j < 4 ? ww >> 16 : ww & 0xFFFFu;
+  return w >= R;
+}
+
+// fix the rejection bits of word wi (calls 4 wi .. 4 wi + 3) where a tie occurred
+__device__ __noinline__ uint32_t fix_ties(uint32_t rej, uint32_t wi, uint32_t trial, uint32_t thr, const Keys &K) {
+  const uint32_t T = thr >> 16, R = thr & 0xFFFFu;
+  for (uint32_t c = 0; c < 4; ++c) {
+    const uint32_t q = 4 * wi + c;
+    uint32_t o[4];
+    philox_full(q, 0, trial, 0, K, o);
+    uint32_t tb[4];
+    bool have = false;
+    for (uint32_t j = 0; j < 8; ++j) {
+      const uint32_t v = j < 4 ? o[j] >> 16 : o[j - 4] & 0xFFFFu;
+      if (v != T) continue;
+      if (!have) philox_full(q, 1, trial, 0, K, tb), have = true;
+      const uint32_t w = j < 4 ? tb[j] >> 16 : tb[j - 4] & 0xFFFFu;
+      const uint32_t bit = 1u << (8 * c + j);
+      rej = w >= R ? (rej | bit) : (rej & ~bit);
+    }
+  }
+  return rej;
+}
+
+template <int V>
+__global__ void __launch_bounds__(128, 5) kern(Keys K, int trials, uint32_t thr, unsigned long long *out,
+                                                unsigned long long *ties) {
+  __shared__ uint4 U[26];
+  if (threadIdx.x < 25) {
+    const uint32_t q = threadIdx.x;
+    const uint64_t p = (uint64_t)M0 * q;
+    const uint32_t n2 = (uint32_t)(p >> 32) ^ 0u ^ K.k1[0];
+    const uint64_t b = (uint64_t)M1 * n2;
+    U[q] = make_uint4((uint32_t)(b >> 32) ^ K.k0[1], (uint32_t)b, (uint32_t)p ^ K.k1[1], 0u);
+  }
+  __syncthreads();
+  const uint32_t nthr = 0u - thr;
+  const uint32_t T = thr >> 16;
+  const uint32_t C = (0x10000u - T) << 16;
+  const uint32_t orall = T == 0 ? 0xFFFFFFFFu : 0u;
+  uint32_t acc = 0, nt = 0;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int t = 0; t < trials; ++t) {
+    const uint32_t trial = tid * trials + t;
+    const uint64_t p = (uint64_t)M1 * trial;
+    const uint32_t n1 = (uint32_t)p, n0 = (uint32_t)(p >> 32) ^ K.k0[0];
+    const uint64_t a = (uint64_t)M0 * n0;
+    const uint32_t ha = (uint32_t)(a >> 32), la = (uint32_t)a;
+    if (V == 0) {  // 32-bit contract, N = 100: 25 calls
+      for (int w = 0; w < 4; ++w) {
+        uint32_t R = 0;
+        if (w < 3) {
+#pragma unroll
+          for (int j = 7; j >= 0; --j) {
+            const uint4 u = U[8 * w + j];
+            R = pack4(R, rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K), nthr);
+          }
+        } else {
+          const uint4 u = U[24];
+          R = pack4(R, rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K), nthr) & 7u;
+        }
+        acc += __popc(R);
+      }
+    } else if (V == 1 || V == 2) {  // halves, N = 100: 13 calls (4 words of 4 calls; last word 1 call, 3 bits)
+      for (int w = 0; w < 4; ++w) {
+        uint32_t R = 0, tmin = 0xFFFFFFFFu;
+        if (w < 3) {
+#pragma unroll
+          for (int j = 3; j >= 0; --j) {
+            const uint4 u = U[4 * w + j];
+            R = pack8(R, rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K), C, tmin);
+          }
+        } else {
+          const uint4 u = U[12];
+          R = pack8(R, rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K), C, tmin);
+        }
+        R |= orall;
+        if (V == 1 && tmin < 0x10000u) {
+          R = fix_ties(R, w, trial, thr, K);
+          ++nt;
+        }
+        if (w == 3) R &= 7u;
+        acc += __popc(R);
+      }
+    } else {  // V == 3: slow per-position reference of the halves contract
+      for (int pp = 0; pp < 99; ++pp) acc += reject_ref(pp >> 3, pp & 7, trial, thr, K);
+    }
+  }
+  atomicAdd(out, (unsigned long long)acc);
+  if (ties) atomicAdd(ties, (unsigned long long)nt);
+}
+
+template <int V>
+void run(const char *name, const Keys &K, uint32_t thr, unsigned long long want, int sms, unsigned long long *gotp) {
+  unsigned long long *d, *dt;
+  cudaMalloc(&d, 8);
+  cudaMalloc(&dt, 8);
+  const int trials = 64;
+  const int blocks = sms * 5 * 8;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  float best = 1e30f;
+  unsigned long long got = 0, nt = 0;
+  for (int rep = 0; rep < (V == 3 ? 1 : 4); ++rep) {
+    cudaMemset(d, 0, 8);
+    cudaMemset(dt, 0, 8);
+    cudaEventRecord(a);
+    kern<V><<<blocks, 128>>>(K, trials, thr, d, dt);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep || V == 3) best = ms < best ? ms : best;
+    cudaMemcpy(&got, d, 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&nt, dt, 8, cudaMemcpyDeviceToHost);
+  }
+  const double tt = (double)blocks * 128 * trials * 100;
+  printf("{\"variant\": \"%s\", \"thr\": %u, \"ms\": %.3f, \"trial_tokens_per_s\": %.4e, \"rejections\": %llu, "
+         "\"tie_words\": %llu, \"ok\": %s}\n",
+         name, thr, best, tt / (best * 1e-3), got, nt, (want == 0 || got == want) ? "true" : "false");
+  if (gotp) *gotp = got;
+  cudaFree(d);
+  cudaFree(dt);
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  Keys K;
+  for (int r = 0; r < 10; ++r) {
+    K.k0[r] = 2405141050u + (uint32_t)r * 0x9E3779B9u;
+    K.k1[r] = 0u + (uint32_t)r * 0xBB67AE85u;
+  }
+  const uint32_t thrs[] = {0xCCCCCCCCu, 0x80000000u, 0x00001234u, 0x19999999u};
+  for (uint32_t thr : thrs) {
+    unsigned long long ref = 0;
+    run<3>("halves, slow per-position reference", K, thr, 0, sms, &ref);
+    run<1>("halves, carry pack + min-tie detection + fix", K, thr, ref, sms, nullptr);
+    run<2>("halves, no tie fix (upper bound, inexact)", K, thr, 0, sms, nullptr);
+    run<0>("32-bit contract, carry pack (the product's)", K, thr, 0, sms, nullptr);
+  }
+  return 0;
+}
