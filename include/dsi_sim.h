@@ -115,6 +115,19 @@ typedef enum {
                                  without the device-to-host copy and FP64 finalize (out may be
                                  NULL there).  Without it every rank gets every result.       */
 
+#define DSI_F_RNG_HALVES 0x200u /* the "halves" layout of the indicator stream (R26):
+                                 call q = (p-1) >> 3 of Philox counter (q, 0, trial, stream_id)
+                                 serves positions 8q+1..8q+8, offset j = (p-1) & 7 reading
+                                 v = the high 16 bits of output word j (j < 4) or the low 16
+                                 bits of word j-4; with thr = floor(a 2^32) = T 2^16 + R,
+                                 A_p = [v < T], or on a tie (v == T) [w < R], w the same half of
+                                 the same word of call (q, 1, trial, stream_id).  So A_p =
+                                 [v 2^16 + w < thr]: the same Bernoulli(thr / 2^32) law as the
+                                 default layout from half the Philox calls, but different
+                                 indicators (results are not comparable trial by trial with
+                                 the default layout).  Per-config kernel only: not with
+                                 SHARED_STREAMS or MEANS_ONLY (DSI_E_RANGE).                  */
+
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {
   double t_target;    /* target forward latency (t_2, "Target Latency"), user units > 0   */

@@ -48,7 +48,7 @@ class _Config(ctypes.Structure):
                 ("sp_degree", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
                 ("stream_id", ctypes.c_uint32), ("t_target_first", ctypes.c_int64),
                 ("t_drafter_first", ctypes.c_int64), ("fresh_verifier", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("rng_halves", ctypes.c_int32)]
 
 
 class _TrialOut(ctypes.Structure):
@@ -104,12 +104,13 @@ class Config:
     t_target_first: int = 0   # TTFT variant: 0 = same as t_target
     t_drafter_first: int = 0  # TTFT variant: 0 = same as t_drafter
     fresh_verifier: bool = False  # N4 variant (R24)
+    rng_halves: bool = False  # the halves layout of the indicator stream (R26)
 
     def _c(self) -> _Config:
         return _Config(int(self.t_target), int(self.t_drafter), float(self.accept_rate),
                        int(self.lookahead), int(self.sp_degree), int(self.n_tokens),
                        int(self.stream_id), int(self.t_target_first), int(self.t_drafter_first),
-                       int(bool(self.fresh_verifier)), 0)
+                       int(bool(self.fresh_verifier)), int(bool(self.rng_halves)))
 
 
 def ticks(x: float, tick: float) -> int:

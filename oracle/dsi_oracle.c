@@ -65,7 +65,42 @@ typedef struct {
   uint64_t thr;
   int pattern;
   uint64_t pattern_bits;
+  int halves;
 } indicator_stream;
+
+/* The "halves" layout (R26; an alternative RNG contract, not the paper's -- the paper */
+/* leaves the generator unspecified).  Position p >= 1 has call q = (p-1) >> 3 and     */
+/* offset j = (p-1) & 7; its 16-bit draw v is the high half of output word j (j < 4) or the low   */
+/* half of word j-4 of Philox at counter (q, 0, trial, stream_id).  With thr = T * 2^16 + R:      */
+/*   v < T  -> accepted;   v > T -> rejected;                                                    */
+/*   v == T -> accepted iff w < R, w the same half of the same word of counter (q, 1, trial,     */
+/*             stream_id).                                                                       */
+/* thr = 2^32 (a = 1) has T = 2^16 > v: always accepted; thr = 0 never.                          */
+static uint32_t half16(const uint32_t out[4], int j) {
+  uint32_t word = out[j & 3];
+  if (j < 4) return word >> 16;
+  return word & 0xFFFFu;
+}
+
+static int indicator_halves(const indicator_stream *s, int64_t p) {
+  uint32_t ctr[4], out[4];
+  uint64_t q = (uint64_t)(p - 1) >> 3;
+  int j = (int)((p - 1) & 7);
+  uint64_t T = s->thr >> 16, R = s->thr & 0xFFFFu;
+  uint32_t v, w;
+  ctr[0] = (uint32_t)q;
+  ctr[1] = 0;
+  ctr[2] = s->trial_lo;
+  ctr[3] = s->stream_id;
+  oracle_philox4x32_10(ctr, s->key, out);
+  v = half16(out, j);
+  if (v < T) return 1;
+  if (v > T) return 0;
+  ctr[1] = 1; /* the tie-break draw */
+  oracle_philox4x32_10(ctr, s->key, out);
+  w = half16(out, j);
+  return w < R;
+}
 
 static int indicator(const indicator_stream *s, int64_t p) {
   uint32_t ctr[4], out[4];
@@ -75,6 +110,7 @@ static int indicator(const indicator_stream *s, int64_t p) {
     if (p - 1 >= 64) return 0;
     return (int)((s->pattern_bits >> (p - 1)) & 1u);
   }
+  if (s->halves) return indicator_halves(s, p);
   q = (uint64_t)(p - 1) >> 2;
   ctr[0] = (uint32_t)q;
   ctr[1] = (uint32_t)(q >> 32);
@@ -502,6 +538,7 @@ static int valid(const oracle_config *cfg) {
     if (cfg->fresh_verifier && (tt1 != cfg->t_target || td1 != cfg->t_drafter)) return 0;
   }
   if (!(cfg->accept_rate >= 0.0 && cfg->accept_rate <= 1.0)) return 0;
+  if (cfg->rng_halves != 0 && cfg->rng_halves != 1) return 0;
   return 1;
 }
 
@@ -520,6 +557,7 @@ int oracle_trial(const oracle_config *cfg, uint64_t seed, uint64_t trial, int pa
   s.thr = oracle_threshold(cfg->accept_rate);
   s.pattern = pattern;
   s.pattern_bits = trial;
+  s.halves = cfg->rng_halves;
 
   /* per-trial counts over positions 1..N-1 (position N has no indicator) */
   out->m = 1;

@@ -45,7 +45,9 @@ typedef struct {
      "DSI either invokes a new current verifier thread or labels an existing thread
      as the current verifier"): non-zero enables it.  Not with the TTFT variant. */
   int32_t  fresh_verifier;
-  int32_t  reserved;     /* 0 */
+  /* Indicator-stream layout: 0 = one 32-bit word per position; 1 = the
+     "halves" layout (R26): 16 bits per position plus a tie-break draw. */
+  int32_t  rng_halves;
 } oracle_config;
 
 typedef struct {

@@ -83,6 +83,149 @@ __device__ __forceinline__ uint32_t pack4(uint32_t rej, const Word4 &u, uint32_t
   return rej;
 }
 
+// ---- Halves layout (DSI_F_RNG_HALVES, R26) ----------------------------------------
+// Call q = (p-1) >> 3 of counter (q, 0, trial, stream) serves positions 8q+1 .. 8q+8: offset
+// j = (p-1) & 7 reads v_j = the high 16 bits of word j (j < 4; words x, y, z, w) or the low 16
+// bits of word j-4.  With thr = T 2^16 + R: A_p = [v < T], and on a tie (v == T, probability
+// 2^-16) A_p = [w < R], w the same half of the same word of the tie-break call (q, 1, trial,
+// stream) -- i.e. A_p = [v 2^16 + w < thr]: the 32-bit layout's law with half its Philox calls.
+// The rejection mask keeps its meaning (bit i of word W = position 32W + i + 1); word W holds
+// calls 4W .. 4W+3, call 4W + c in bits 8c .. 8c+7.
+
+struct HalvesCtx {
+  uint32_t C;       // (2^16 - T) << 16 mod 2^32: the carry of (v << 16) + C is [v >= T] (T >= 1)
+  uint32_t TT;      // T in both halves (the tie test)
+  uint32_t orall;   // T == 0: every v >= T (no carry ever comes), so all bits are set
+  uint32_t thr;     // threshold (mode MODE_STREAM: 1 <= thr < 2^32)
+  uint32_t stream;  // counter word 3
+  bool direct;      // T is not an f16 NaN pattern: ties by u == TT as f16x2
+};
+
+__device__ __forceinline__ HalvesCtx make_halves(uint32_t thr, uint32_t stream) {
+  HalvesCtx h;
+  const uint32_t T = thr >> 16;
+  h.C = (0x10000u - T) << 16;
+  h.TT = T | (T << 16);
+  h.orall = T == 0u ? 0xffffffffu : 0u;
+  h.thr = thr;
+  h.stream = stream;
+  h.direct = !((T & 0x7C00u) == 0x7C00u && (T & 0x3FFu) != 0u);
+  return h;
+}
+
+// rej = (rej << 8) | [lo(w) >= T] << 7 | ... | [lo(x) >= T] << 4 | [hi(w) >= T] << 3 | ... | [hi(x) >= T]
+// (ties counted as rejections; the caller fixes them): 1 shift/LEA + IADD3 + IMAD.X per bit.
+__device__ __forceinline__ uint32_t pack8(uint32_t rej, const Word4 &u, uint32_t C) {
+  asm("{\n\t"
+      ".reg .u32 t, l;\n\t"
+      "shl.b32 l, %4, 16;\n\tadd.cc.u32 t, l, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "shl.b32 l, %3, 16;\n\tadd.cc.u32 t, l, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "shl.b32 l, %2, 16;\n\tadd.cc.u32 t, l, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "shl.b32 l, %1, 16;\n\tadd.cc.u32 t, l, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %4, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %3, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %2, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %1, %5;\n\taddc.u32 %0, %0, %0;\n\t"
+      "}"
+      : "+r"(rej)
+      : "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w), "r"(C));
+  return rej;
+}
+
+// Per-half equality as f16x2 (HSET2: lanes 0xFFFF where equal).  +0 and -0 compare equal and
+// NaN never does, so: DIRECT (u == TT, T not a NaN pattern) flags every tie, plus lanes 0x0000 /
+// 0x8000 when T is -0 / +0; the XOR form (u ^ TT == 0) flags every tie plus lanes 0x8000 of
+// u ^ TT.  Flags are a superset of the ties: the fix re-decides exactly.
+__device__ __forceinline__ uint32_t heq2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("set.eq.u32.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+template <bool DIRECT>
+__device__ __forceinline__ uint32_t tie_flags(const Word4 &u, uint32_t TT, uint32_t acc) {
+  if (DIRECT) return acc | heq2(u.x, TT) | heq2(u.y, TT) | heq2(u.z, TT) | heq2(u.w, TT);
+  return acc | heq2(u.x ^ TT, 0u) | heq2(u.y ^ TT, 0u) | heq2(u.z ^ TT, 0u) | heq2(u.w ^ TT, 0u);
+}
+
+// All ten rounds of Philox4x32-10 at counter (c0, c1, c2, c3) (the rare tie path).
+__device__ __forceinline__ Word4 philox_full(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const Keys &K) {
+#pragma unroll 1
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t a = (uint64_t)PHILOX_M0 * c0;
+    const uint64_t b = (uint64_t)PHILOX_M1 * c2;
+    const uint32_t n0 = (uint32_t)(b >> 32) ^ c1 ^ K.k0[r];
+    const uint32_t n2 = (uint32_t)(a >> 32) ^ c3 ^ K.k1[r];
+    c1 = (uint32_t)b;
+    c3 = (uint32_t)a;
+    c0 = n0;
+    c2 = n2;
+  }
+  return Word4{c0, c1, c2, c3};
+}
+
+__device__ __forceinline__ uint32_t half_of(const Word4 &o, int j) {
+  const int i = j & 3;
+  const uint32_t x = i == 0 ? o.x : i == 1 ? o.y : i == 2 ? o.z : o.w;
+  return j < 4 ? x >> 16 : x & 0xFFFFu;
+}
+
+// Exact decisions of every tied position among calls q0 .. q0 + ncalls - 1 (bits 8c + j of R):
+// rejected iff w >= R_low, w from the tie-break call (q, 1, trial, stream).
+static __device__ __noinline__ uint32_t halves_fix(uint32_t R, int q0, int ncalls, uint32_t trial, uint32_t stream,
+                                            uint32_t thr, const Keys &K) {
+  const uint32_t T = thr >> 16, Rl = thr & 0xFFFFu;
+  for (int c = 0; c < ncalls; ++c) {
+    const uint32_t q = (uint32_t)(q0 + c);
+    const Word4 o = philox_full(q, 0u, trial, stream, K);
+    bool have = false;
+    Word4 tb{0u, 0u, 0u, 0u};
+    for (int j = 0; j < 8; ++j) {
+      if (half_of(o, j) != T) continue;
+      if (!have) {
+        tb = philox_full(q, 1u, trial, stream, K);
+        have = true;
+      }
+      const uint32_t bit = 1u << (8 * c + j);
+      R = half_of(tb, j) >= Rl ? (R | bit) : (R & ~bit);
+    }
+  }
+  return R;
+}
+
+// Rejection mask of word w in the halves layout: calls 4w .. 4w + ncalls - 1 (ncalls = min(4,
+// nq - 4w), nq = ceil((N-1)/8)), U[q] the per-counter half of rounds 0-1 (TABLE) or computed.
+template <bool DIRECT, bool TABLE>
+__device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4 *U, const TrialHalf &th,
+                                                      uint32_t trial, const HalvesCtx &h, const Keys &K) {
+  uint32_t R = 0u, tf = 0u;
+  const int ncalls = min(4, nq - 4 * w);
+  if (ncalls == 4) {
+#pragma unroll
+    for (int j = 3; j >= 0; --j) {
+      const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
+      const Word4 o = philox_call(u, th, K);
+      R = pack8(R, o, h.C);
+      tf = tie_flags<DIRECT>(o, h.TT, tf);
+    }
+  } else {
+    for (int j = ncalls - 1; j >= 0; --j) {
+      const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
+      const Word4 o = philox_call(u, th, K);
+      R = pack8(R, o, h.C);
+      tf = tie_flags<DIRECT>(o, h.TT, tf);
+    }
+  }
+  R |= h.orall;
+  if (tf) R = halves_fix(R, 4 * w, ncalls, trial, h.stream, h.thr, K);
+  return R;
+}
+template <bool TABLE>
+__device__ __forceinline__ uint32_t gen_word_halves(int w, int nq, const uint4 *U, const TrialHalf &th, uint32_t trial,
+                                                    const HalvesCtx &h, const Keys &K) {
+  return h.direct ? gen_word_halves_t<true, TABLE>(w, nq, U, th, trial, h, K)
+                  : gen_word_halves_t<false, TABLE>(w, nq, U, th, trial, h, K);
+}
+
 // floor(x / d) for x * d <= 2^32 with M = ceil(2^32 / d) = lo + hi * 2^32.
 __device__ __forceinline__ uint32_t magic_div(uint32_t x, uint32_t lo, uint32_t hi) {
   return __umulhi(x, lo) + x * hi;

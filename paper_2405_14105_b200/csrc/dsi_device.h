@@ -83,7 +83,8 @@ struct LaunchParams {
   int32_t any_ttft;              // some config uses the TTFT variant (first-segment tables)
   int32_t any_fresh;             // some config has CFG_FRESH (every segment walked)
   int32_t k1_fast;               // launch the variant with the k = 1 no-queue fast path (VAR 3)
-  int32_t pad_[3];               // keeps keys 16-byte aligned in the parameter bank (LDCU.128 loads)
+  int32_t halves;                // DSI_F_RNG_HALVES: the halves layout of the indicator stream
+  int32_t pad_[2];               // keeps keys 16-byte aligned in the parameter bank (LDCU.128 loads)
   Keys keys;
 };
 

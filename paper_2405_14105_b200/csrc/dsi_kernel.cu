@@ -138,7 +138,8 @@ __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t
 
 // VAR: 0 = default model, 1 = TTFT variant present, 2 = fresh-verifier variant present,
 //      3 = default model with the k = 1 no-queue fast path compiled in (LaunchParams.k1_fast)
-template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, int VAR>
+// HALVES: the halves layout of the indicator stream (DSI_F_RNG_HALVES, dsi_common.cuh)
+template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, int VAR, bool HALVES>
 __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kernel(const LaunchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
 
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
   const int N = cfg.n_tokens;
   const int npos = N - 1;  // positions carrying an indicator
   const int nwords = (npos + 31) >> 5;
-  const int nq = (npos + 3) >> 2;
+  const int nq = HALVES ? (npos + 7) >> 3 : (npos + 3) >> 2;  // Philox calls per trial
   SegCtx s;
   s.k_eff = (uint32_t)cfg.k_eff;
   s.m_si = cfg.m_si;
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
   // operations instead of walking the runs (block-uniform choice)
   const bool fast1 = VAR == 3 && !walk_all && cfg.k_eff == 1 && (cfg.flags & CFG_NOQUEUE) != 0;
   const int t_d = cfg.t_d;
+  const HalvesCtx hc = make_halves(cfg.thr, cfg.stream_id);
 
   // shared memory: TABLE -> T[g] (g = 0..N) then U[q] (q < nq); HIST -> histograms
   uint2 *T = reinterpret_cast<uint2 *>(smem);
@@ -282,6 +284,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
     if (VAR == 0 && TABLE && !HIST && !PATTERN && stream && Lk > 30) {
       // full words with the walk of word w-1 after the generation of word w, one straight-line block
       auto gen_word = [&](int w) {
+        if (HALVES) return gen_word_halves<true>(w, nq, U, th, trial, hc, P.keys);
         uint32_t R = 0u;
 #pragma unroll
         for (int j = 7; j >= 0; --j) R = pack4(R, philox_call(U[8 * w + j], th, P.keys), nthr);
@@ -306,6 +309,8 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
       uint32_t R;
       if (PATTERN) {
         R = ~trial;  // N <= 33: one word, A_p = bit p-1 of the trial index
+      } else if (mode == MODE_STREAM && HALVES) {
+        R = gen_word_halves<TABLE>(w, nq, U, th, trial, hc, P.keys);
       } else if (mode == MODE_STREAM) {
         R = 0u;
         const int ncalls = min(8, nq - 8 * w);
@@ -447,10 +452,10 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kern
   }
 }
 
-template <bool A, bool B, bool C, bool D, int E>
-int launch_variant_t(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
+template <bool A, bool B, bool C, bool D, int E, bool H>
+int launch_variant_h(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
   if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(dsi_trial_kernel<A, B, C, D, E>,
+    const cudaError_t e = cudaFuncSetAttribute(dsi_trial_kernel<A, B, C, D, E, H>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
   }
@@ -459,12 +464,21 @@ int launch_variant_t(const LaunchParams &p, uint64_t n_units, int threads, size_
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_trial_kernel<A, B, C, D, E><<<(unsigned)n, threads, smem, st>>>(q);
+    dsi_trial_kernel<A, B, C, D, E, H><<<(unsigned)n, threads, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
   }
   return 0;
+}
+
+// the halves layout is instantiated only where the stream is read (not in PATTERN launches)
+template <bool A, bool B, bool C, bool D, int E>
+int launch_variant_t(const LaunchParams &p, uint64_t n_units, int threads, size_t smem, cudaStream_t st) {
+  if constexpr (!C) {
+    if (p.halves) return launch_variant_h<A, B, C, D, E, true>(p, n_units, threads, smem, st);
+  }
+  return launch_variant_h<A, B, C, D, E, false>(p, n_units, threads, smem, st);
 }
 
 template <bool A, bool B, bool C, bool D>

@@ -268,7 +268,7 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
   const uint32_t known = DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_STRICT_EQ1 | DSI_F_TIMING |
                          DSI_F_SHARED_STREAMS | DSI_F_FRESH_VERIFIER | DSI_F_MEANS_ONLY |
-                         DSI_F_REDUCE_TO_ROOT;
+                         DSI_F_REDUCE_TO_ROOT | DSI_F_RNG_HALVES;
   if (opt->flags & ~known) return fail(nullptr, DSI_E_RANGE, "unknown flag");
   if (opt->n_devices != 1)
     return fail(nullptr, DSI_E_RANGE, "n_devices must be 1: run one process per GPU (rank/world/nccl_id)");
@@ -300,6 +300,8 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   const bool means_only = opt->flags & DSI_F_MEANS_ONLY;
   if (means_only && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_SHARED_STREAMS)))
     return fail(nullptr, DSI_E_RANGE, "DSI_F_MEANS_ONLY excludes PER_TRIAL, HIST, PATTERN and SHARED_STREAMS");
+  if ((opt->flags & DSI_F_RNG_HALVES) && (opt->flags & (DSI_F_SHARED_STREAMS | DSI_F_MEANS_ONLY)))
+    return fail(nullptr, DSI_E_RANGE, "DSI_F_RNG_HALVES is not supported with SHARED_STREAMS or MEANS_ONLY");
 
   dsi_sim *h = new (std::nothrow) dsi_sim;
   if (!h) return fail(nullptr, DSI_E_NOMEM, "handle allocation");
@@ -798,6 +800,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
     p.any_ttft = h->any_ttft ? 1 : 0;
     p.any_fresh = h->any_fresh ? 1 : 0;
     p.k1_fast = h->k1_fast ? 1 : 0;
+    p.halves = (h->opt.flags & DSI_F_RNG_HALVES) ? 1 : 0;
     const uint32_t s_lo = (uint32_t)h->opt.seed, s_hi = (uint32_t)(h->opt.seed >> 32);
     for (int r = 0; r < 10; ++r) {
       p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;

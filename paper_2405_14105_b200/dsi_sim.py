@@ -30,6 +30,7 @@ DSI_F_SHARED_STREAMS = 0x20
 DSI_F_FRESH_VERIFIER = 0x40
 DSI_F_MEANS_ONLY = 0x80
 DSI_F_REDUCE_TO_ROOT = 0x100
+DSI_F_RNG_HALVES = 0x200
 
 # Structured dtypes with the exact C layouts (numpy arrays are passed by pointer).
 CONFIG_DTYPE = np.dtype([("t_target", "<f8"), ("t_drafter", "<f8"), ("accept_rate", "<f8"),

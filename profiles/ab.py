@@ -25,6 +25,7 @@ ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--runs", type=int, default=5)
 ap.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
 ap.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER")
+ap.add_argument("--halves", action="store_true", help="DSI_F_RNG_HALVES")
 args = ap.parse_args()
 if args.workload == "cfg3":
     cfgs, tick = W.cfg3(cells=slice(None, None, args.stride))
@@ -37,7 +38,7 @@ else:
     cfgs, tick = W.cfg2()
 tt = int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"]))
 with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING | (D.DSI_F_SHARED_STREAMS if args.shared else 0)
-                 | (D.DSI_F_FRESH_VERIFIER if args.fresh else 0),
+                 | (D.DSI_F_FRESH_VERIFIER if args.fresh else 0) | (D.DSI_F_RNG_HALVES if args.halves else 0),
                  block_threads=args.threads) as sim:
     sim.run()
     sim.reduce()
@@ -47,7 +48,7 @@ with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING | (D.DSI_F_S
         ms.append(sim.kernel_ms())
     res = sim.reduce()
 print(json.dumps({"lib": os.environ.get("DSI_SIM_LIB", "default"), "workload": args.workload,
-                  "shared": args.shared,
+                  "shared": args.shared, "halves": args.halves,
                   "stride": args.stride, "threads": args.threads, "kernel_ms": ms,
                   "tt_per_s": tt / (statistics.median(ms) / 1e3),
                   "checksum": int(res["sum_dsi_ticks"].sum() % (1 << 61))}))

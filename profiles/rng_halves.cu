@@ -80,6 +80,55 @@ __device__ __forceinline__ uint32_t pack8(uint32_t rej, const uint4 &u, uint32_t
   return rej;
 }
 
+// 8 decisions by the carry chain only (no sums kept)
+__device__ __forceinline__ uint32_t pack8c(uint32_t rej, const uint4 &u, uint32_t C) {
+  const uint32_t lx = u.x << 16, ly = u.y << 16, lz = u.z << 16, lw = u.w << 16;
+  asm("{\n\t.reg .u32 t;\n\t"
+      "add.cc.u32 t, %1, %9;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %2, %9;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %3, %9;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %4, %9;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %5, %9;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %6, %9;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %7, %9;\n\taddc.u32 %0, %0, %0;\n\t"
+      "add.cc.u32 t, %8, %9;\n\taddc.u32 %0, %0, %0;\n\t}"
+      : "+r"(rej)
+      : "r"(lw), "r"(lz), "r"(ly), "r"(lx), "r"(u.w), "r"(u.z), "r"(u.y), "r"(u.x), "r"(C));
+  return rej;
+}
+
+// tie flags of the 8 halves: half-precision equality (lanes 0xFFFF on equality; +0 and -0 compare
+// equal, so a lane 0x8000 of d is a false positive, resolved exactly by the fix)
+__device__ __forceinline__ uint32_t heq(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("set.eq.u32.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// XOR form: d = u ^ TT has a zero half exactly where a tie is (any T)
+__device__ __forceinline__ uint32_t ties_xor(const uint4 &u, uint32_t TT, uint32_t acc) {
+  return acc | heq(u.x ^ TT, 0u) | heq(u.y ^ TT, 0u) | heq(u.z ^ TT, 0u) | heq(u.w ^ TT, 0u);
+}
+// direct form: u == TT as f16x2 (valid when T is not a NaN pattern)
+__device__ __forceinline__ uint32_t ties_direct(const uint4 &u, uint32_t TT, uint32_t acc) {
+  return acc | heq(u.x, TT) | heq(u.y, TT) | heq(u.z, TT) | heq(u.w, TT);
+}
+// predicate form: 8 scalar half compares OR-accumulated into one predicate
+__device__ __forceinline__ uint32_t ties_pred(const uint4 &u, uint32_t TT, uint32_t acc) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p;\n\t.reg .b16 a0, a1, b0, b1, c0, c1, d0, d1, t0, t1;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "mov.b32 {a0, a1}, %2;\n\tmov.b32 {b0, b1}, %3;\n\tmov.b32 {c0, c1}, %4;\n\tmov.b32 {d0, d1}, %5;\n\t"
+      "mov.b32 {t0, t1}, %6;\n\t"
+      "setp.eq.or.f16 p, a0, t0, p;\n\tsetp.eq.or.f16 p, a1, t0, p;\n\t"
+      "setp.eq.or.f16 p, b0, t0, p;\n\tsetp.eq.or.f16 p, b1, t0, p;\n\t"
+      "setp.eq.or.f16 p, c0, t0, p;\n\tsetp.eq.or.f16 p, c1, t0, p;\n\t"
+      "setp.eq.or.f16 p, d0, t0, p;\n\tsetp.eq.or.f16 p, d1, t0, p;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(r)
+      : "r"(acc), "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w), "r"(TT));
+  return r;
+}
+
 // exact per-position decision (slow reference), position j of call (q, trial)
 __device__ __forceinline__ bool reject_ref(uint32_t q, uint32_t j, uint32_t trial, uint32_t thr, const Keys &K) {
   uint32_t o[4], t[4];
@@ -152,6 +201,32 @@ __global__ void __launch_bounds__(128, 5) kern(Keys K, int trials, uint32_t thr,
           const uint4 u = U[24];
           R = pack4(R, rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K), nthr) & 7u;
         }
+        acc += __popc(R);
+      }
+    } else if (V >= 4) {  // halves, carry pack + half-precision tie flags
+      const uint32_t TT = T | (T << 16);
+      for (int w = 0; w < 4; ++w) {
+        uint32_t R = 0, tf = 0;
+        if (w < 3) {
+#pragma unroll
+          for (int j = 3; j >= 0; --j) {
+            const uint4 u = U[4 * w + j];
+            const uint4 o = rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K);
+            R = pack8c(R, o, C);
+            tf = V == 4 ? ties_xor(o, TT, tf) : V == 5 ? ties_direct(o, TT, tf) : ties_pred(o, TT, tf);
+          }
+        } else {
+          const uint4 u = U[12];
+          const uint4 o = rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K);
+          R = pack8c(R, o, C);
+          tf = V == 4 ? ties_xor(o, TT, tf) : V == 5 ? ties_direct(o, TT, tf) : ties_pred(o, TT, tf);
+        }
+        R |= orall;
+        if (tf) {
+          R = fix_ties(R, w, trial, thr, K);
+          ++nt;
+        }
+        if (w == 3) R &= 7u;
         acc += __popc(R);
       }
     } else if (V == 1 || V == 2) {  // halves, N = 100: 13 calls (4 words of 4 calls; last word 1 call, 3 bits)
@@ -231,6 +306,9 @@ int main() {
     run<3>("halves, slow per-position reference", K, thr, 0, sms, &ref);
     run<1>("halves, carry pack + min-tie detection + fix", K, thr, ref, sms, nullptr);
     run<2>("halves, no tie fix (upper bound, inexact)", K, thr, 0, sms, nullptr);
+    run<4>("halves, carry pack + xor/HSET2 tie flags + fix", K, thr, ref, sms, nullptr);
+    run<5>("halves, carry pack + direct HSET2 tie flags + fix (T not NaN)", K, thr, ref, sms, nullptr);
+    run<6>("halves, carry pack + HSETP2.OR predicate tie flag + fix (T not NaN)", K, thr, ref, sms, nullptr);
     run<0>("32-bit contract, carry pack (the product's)", K, thr, 0, sms, nullptr);
   }
   return 0;

@@ -4,7 +4,7 @@ import numpy as np
 import oracle as O
 
 
-def oracle_config(row, tick: float, fresh: bool = False) -> O.Config:
+def oracle_config(row, tick: float, fresh: bool = False, halves: bool = False) -> O.Config:
     names = row.dtype.names
     tt1 = float(row["ttft_target"]) if "ttft_target" in names else 0.0
     td1 = float(row["ttft_drafter"]) if "ttft_drafter" in names else 0.0
@@ -12,13 +12,13 @@ def oracle_config(row, tick: float, fresh: bool = False) -> O.Config:
                     float(row["accept_rate"]), int(row["lookahead"]), int(row["sp_degree"]),
                     int(row["n_tokens"]), int(row["stream_id"]),
                     O.ticks(tt1, tick) if tt1 else 0, O.ticks(td1, tick) if td1 else 0,
-                    fresh_verifier=fresh)
+                    fresh_verifier=fresh, rng_halves=halves)
 
 
 def oracle_sums(row, tick: float, seed: int, first: int = 0, count=None, pattern=False, hist=False,
-                per_trial=False, fresh=False):
+                per_trial=False, fresh=False, halves=False):
     T = int(row["n_trials"]) if count is None else count
-    return O.run(oracle_config(row, tick, fresh), seed, first, T, pattern=pattern, hist=hist,
+    return O.run(oracle_config(row, tick, fresh, halves), seed, first, T, pattern=pattern, hist=hist,
                  per_trial=per_trial)
 
 

@@ -120,14 +120,15 @@ def test_create_validation_errors(over, status):
 
 def test_create_option_errors():
     cfgs = _one()
-    bad = [dict(tick=0.0), dict(tick=-1.0), dict(flags=0x200), dict(n_devices=0), dict(n_devices=9), dict(n_devices=2),
+    bad = [dict(tick=0.0), dict(tick=-1.0), dict(flags=0x400), dict(n_devices=0), dict(n_devices=9), dict(n_devices=2),
            dict(world=2, rank=2), dict(world=0), dict(block_threads=48), dict(block_threads=256),
            dict(n_shards=2, n_devices=2), dict(flags=D.DSI_F_SHARED_STREAMS | D.DSI_F_PER_TRIAL),
            dict(flags=D.DSI_F_SHARED_STREAMS | D.DSI_F_HIST),
            dict(flags=D.DSI_F_SHARED_STREAMS | D.DSI_F_PATTERN),
            dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_PER_TRIAL), dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_HIST),
            dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_PATTERN),
-           dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_SHARED_STREAMS)]
+           dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_SHARED_STREAMS),
+           dict(flags=D.DSI_F_RNG_HALVES | D.DSI_F_SHARED_STREAMS), dict(flags=D.DSI_F_RNG_HALVES | D.DSI_F_MEANS_ONLY)]
     for kw in bad:
         tick = kw.pop("tick", 0.01)
         with pytest.raises(D.DsiError) as e:

@@ -1,0 +1,166 @@
+"""GPU parity of the halves layout of the indicator stream (DSI_F_RNG_HALVES, R26).
+
+Same bar as test_gpu_parity.py: per-trial records bit-exact against the oracle evaluating the
+halves layout, integer sums exact, FP64 means within 1e-9.  The cases cover the tie path the
+kernel takes with probability 2^-16 per position: thresholds whose T = thr >> 16 is an f16 NaN
+pattern (the XOR form of the tie test), +-0 / +inf patterns (false-positive flags), T = 0 (every
+acceptance a tie), T = 0xFFFF, thresholds built from the Philox outputs themselves so that given
+positions tie, and enough trials that random ties occur.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import assert_result_equals_oracle, assert_trials_equal, oracle_sums
+
+pytestmark = pytest.mark.gpu
+
+D = pytest.importorskip("paper_2405_14105_b200.dsi_sim")
+from paper_2405_14105_b200 import workloads as W  # noqa: E402
+
+SEED = W.SEED
+H = D.DSI_F_RNG_HALVES
+ALL = D.DSI_F_PER_TRIAL | D.DSI_F_HIST
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run_sim(cfgs, tick, flags, **kw):
+    sim = D.Simulator(cfgs, tick=tick, seed=kw.pop("seed", SEED), flags=flags | H, **kw)
+    sim.run()
+    return sim, sim.reduce()
+
+
+def check(sim, res, cfgs, tick, per_trial=True, hist=False, fresh=False, ctx="", idx=None):
+    for i in (range(len(cfgs)) if idx is None else idx):
+        want = oracle_sums(cfgs[i], tick, SEED, hist=hist, per_trial=per_trial, fresh=fresh, halves=True)
+        assert_result_equals_oracle(res[i], want, tick, ctx=f"{ctx} cfg {i}")
+        if per_trial:
+            assert_trials_equal(sim.trials(i), want, ctx=f"{ctx} cfg {i}")
+        if hist:
+            seg, si = sim.hist(i)
+            assert np.array_equal(seg, want["seg_hist"]), (ctx, i, "seg_hist")
+            assert np.array_equal(si, want["si_hist"]), (ctx, i, "si_hist")
+
+
+@pytest.mark.parametrize("flags", [ALL, D.DSI_F_PER_TRIAL])
+def test_halves_fuzz_bit_exact(flags):
+    cfgs, tick = W.fuzz(120, seed=31, trials=300)
+    sim, res = run_sim(cfgs, tick, flags)
+    check(sim, res, cfgs, tick, hist=bool(flags & D.DSI_F_HIST), ctx=f"fuzz {flags}")
+    sim.close()
+
+
+def test_halves_long_runs_and_pipelined_walk():
+    """a in [0.85, 0.999], k up to 45 (k >= 30: the pipelined branch-free walk), N up to 300."""
+    rng = np.random.default_rng(41)
+    rows = []
+    for i in range(60):
+        t_t = int(rng.integers(2, 101))
+        t_d = int(rng.integers(1, t_t + 1))
+        k = int(rng.integers(30, 46)) if i % 2 else int(rng.integers(1, 30))
+        rows.append((float(t_t), float(t_d), float(rng.uniform(0.85, 0.999)), k, int(rng.integers(1, 9)),
+                     int(rng.integers(33, 301)), int(rng.integers(0, 3)), 200))
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 1.0, D.DSI_F_PER_TRIAL)
+    check(sim, res, cfgs, 1.0, ctx="longruns")
+    sim.close()
+
+
+def test_halves_threshold_patterns():
+    """T = thr >> 16 as an f16 bit pattern: NaN (0.49, 0.99: the XOR tie test), +inf
+    (0x7C00), -0 (a = 0.5), +0 (a < 2^-16: every acceptance through a tie), 0xFFFF."""
+    accs = [0.49, 0.99, 0.4844, 0x7C00 / 65536, 0.5, 2.0 ** -17, 3e-6, 1 - 2.0 ** -17, 0.8, 0.01]
+    rows = [(1.0, 0.1, a, k, sp, n, s, 3000) for a in accs for (k, sp, n, s) in ((3, 4, 100, 0), (1, 7, 70, 1))]
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 0.01, D.DSI_F_PER_TRIAL)
+    check(sim, res, cfgs, 0.01, ctx="thresholds")
+    sim.close()
+
+
+def _half(words, j):
+    w = words[j % 4]
+    return (w >> 16) if j < 4 else (w & 0xFFFF)
+
+
+def test_halves_forced_ties():
+    """Each config's threshold is built from the Philox outputs of one (trial, call) so that a
+    chosen offset ties (v == T), with the tie-break deciding both ways; every call position in
+    the 32-position word and a later word are covered."""
+    key = (SEED & 0xFFFFFFFF, SEED >> 32)
+    rows, N = [], 100
+    for trial in (0, 3, 64):
+        for q in (0, 1, 3, 6, 12):
+            for j in range(8):
+                v = _half(O.philox4x32_10((q, 0, trial, 0), key), j)
+                w = _half(O.philox4x32_10((q, 1, trial, 0), key), j)
+                for R in (w, min(w + 1, 0xFFFF)):
+                    thr = (v << 16) | R
+                    if 0 < thr:
+                        rows.append((1.0, 0.2, thr / 2 ** 32, 2 + j % 5, 3, N, 0, 70))
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 0.01, D.DSI_F_PER_TRIAL)
+    check(sim, res, cfgs, 0.01, ctx="forced ties")
+    sim.close()
+
+
+def test_halves_many_trials_random_ties():
+    """2e5 trials x 99 positions: ~300 random ties on the kernel's rare path, per trial."""
+    cfgs = W.rows([(1.0, 0.1, 0.8, 5, 2, 100, 0, 200_000), (1.0, 0.05, 0.37, 2, 7, 100, 2, 200_000)])
+    sim, res = run_sim(cfgs, 0.01, D.DSI_F_PER_TRIAL)
+    check(sim, res, cfgs, 0.01, ctx="many")
+    sim.close()
+
+
+def test_halves_long_sequences_and_arithmetic_path():
+    """N = 1000 and N = 4097 (no shared-memory tables: per-call rounds 0-1, arithmetic costs)."""
+    rows = [(1.0, 0.05, 0.9, 3, 7, 1000, 0, 257), (1.0, 0.3, 0.5, 2, 3, 4097, 1, 65),
+            (1.0, 1.0, 0.97, 1, 1, 1000, 2, 130), (1.0, 0.3, 0.49, 40, 3, 4099, 0, 33)]
+    cfgs = W.rows(rows)
+    sim, res = run_sim(cfgs, 0.01, D.DSI_F_PER_TRIAL)
+    check(sim, res, cfgs, 0.01, ctx="long")
+    sim.close()
+
+
+def test_halves_variants_ttft_fresh_k1():
+    """The kernel's variants under the halves layout: TTFT configs, the fresh verifier
+    (k t_d > t_t) and the k = 1 no-queue fast path (chosen when such configs carry the work)."""
+    ttft = W.rows([(1.0, 0.1, 0.7, 4, 3, 80, 0, 500, 2.5, 0.3), (1.0, 0.2, 0.85, 2, 7, 64, 1, 500, 1.4, 0.2)])
+    sim, res = run_sim(ttft, 0.01, D.DSI_F_PER_TRIAL)
+    check(sim, res, ttft, 0.01, ctx="ttft")
+    sim.close()
+    fresh = W.rows([(1.0, 0.3, 0.9, 6, 3, 100, 0, 500), (1.0, 0.5, 0.6, 3, 2, 90, 1, 500)])
+    sim, res = run_sim(fresh, 0.01, D.DSI_F_PER_TRIAL | D.DSI_F_FRESH_VERIFIER)
+    check(sim, res, fresh, 0.01, fresh=True, ctx="fresh")
+    sim.close()
+    k1 = W.rows([(1.0, 0.2, a, 1, 7, 200, 0, 400) for a in (0.3, 0.6, 0.9, 0.99)])
+    sim, res = run_sim(k1, 0.01, D.DSI_F_PER_TRIAL)
+    check(sim, res, k1, 0.01, ctx="k1")
+    sim.close()
+
+
+def test_halves_bench_workload_sample():
+    """cfg3 (the bench workload; every 40th heatmap cell, all k) in the bench's launch
+    configuration (no test flags); 12 sampled configs against the oracle over all their trials."""
+    cfgs, tick = W.cfg3(cells=slice(None, None, 40))
+    sim, res = run_sim(cfgs, tick, 0)
+    idx = np.random.default_rng(3).choice(len(cfgs), 12, replace=False)
+    check(sim, res, cfgs, tick, per_trial=False, ctx="cfg3", idx=idx)
+    # the law: mean acceptance within 6 sigma of a per config, pooled over the sample
+    acc = res["sum_accepts"].astype(np.float64) / (cfgs["n_trials"] * 99.0)
+    a = cfgs["accept_rate"]
+    sd = np.sqrt(a * (1 - a) / (cfgs["n_trials"] * 99.0)) + 1e-12
+    assert np.all(np.abs(acc - a) <= 6.5 * sd)
+    sim.close()
+
+
+def test_halves_options_are_validated():
+    cfgs, tick = W.cfg1(trials=10)
+    for bad in (D.DSI_F_SHARED_STREAMS, D.DSI_F_MEANS_ONLY):
+        with pytest.raises(D.DsiError):
+            D.Simulator(cfgs, tick=tick, seed=SEED, flags=H | bad)
