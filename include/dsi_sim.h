@@ -125,8 +125,9 @@ typedef enum {
                                  [v 2^16 + w < thr]: the same Bernoulli(thr / 2^32) law as the
                                  default layout from half the Philox calls, but different
                                  indicators (results are not comparable trial by trial with
-                                 the default layout).  Per-config kernel only: not with
-                                 SHARED_STREAMS or MEANS_ONLY (DSI_E_RANGE).                  */
+                                 the default layout).  Every mode (per-config, SHARED_STREAMS,
+                                 MEANS_ONLY, the heatmap) gives the same integers under it;
+                                 dsi_multi_simulate keeps the default layout.                 */
 
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {

@@ -54,9 +54,11 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
   const int N = G.n_tokens;
   const int npos = N - 1;
   const int nwords = (npos + 31) >> 5;
-  const int nq = (npos + 3) >> 2;
+  const bool halves = P.halves != 0;
+  const int nq = halves ? (npos + 7) >> 3 : (npos + 3) >> 2;
   const uint32_t mode = G.mode;
   const uint32_t nthr = 0u - G.thr;
+  const HalvesCtx hc = make_halves(G.thr, G.stream_id);
 
   // shared memory layout
   unsigned char *sp = smem;
@@ -144,7 +146,9 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
       uint32_t sumb = 0, sumx = 0;  // sum ceil(L/kmin), sum floor(L/(kmin+1)) over stored runs
       for (int w = 0; w < nwords; ++w) {
         uint32_t Rw;
-        if (mode == MODE_STREAM) {
+        if (mode == MODE_STREAM && halves) {
+          Rw = gen_word_halves<true>(w, nq, U, th, trial, hc, P.keys);
+        } else if (mode == MODE_STREAM) {
           Rw = 0u;
           const int ncalls = min(8, nq - 8 * w);
           if (ncalls == 8) {

@@ -78,9 +78,11 @@ __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
   const int N = G.n_tokens;
   const int npos = N - 1;
   const int nwords = (npos + 31) >> 5;
-  const int nq = (npos + 3) >> 2;
+  const bool halves = P.halves != 0;
+  const int nq = halves ? (npos + 7) >> 3 : (npos + 3) >> 2;
   const uint32_t mode = G.mode;
   const uint32_t nthr = 0u - G.thr;
+  const HalvesCtx hc = make_halves(G.thr, G.stream_id);
   uint4 *U = reinterpret_cast<uint4 *>(smem);
   uint16_t *runs_s = reinterpret_cast<uint16_t *>(smem + (size_t)P.max_nq * sizeof(uint4));  // [r * TH + tid]
   if (mode == MODE_STREAM)
@@ -113,7 +115,9 @@ __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
   };
   for (int w = 0; w < nwords; ++w) {
     uint32_t Rw;
-    if (mode == MODE_STREAM) {
+    if (mode == MODE_STREAM && halves) {
+      Rw = gen_word_halves<true>(w, nq, U, th, (uint32_t)t, hc, P.keys);
+    } else if (mode == MODE_STREAM) {
       Rw = 0u;
       const int ncalls = min(8, nq - 8 * w);
       if (ncalls == 8) {

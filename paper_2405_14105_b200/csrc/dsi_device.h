@@ -124,6 +124,8 @@ struct CrnParams {
   uint64_t tile_begin;
   uint32_t rec_bytes;
   int32_t any_fresh;  // some config of the launch has CFG_FRESH (template FRESH variants)
+  int32_t halves;     // DSI_F_RNG_HALVES: the halves layout of the indicator stream
+  int32_t pad_[2];
   Keys keys;
 };
 // On-device heatmap product: one warp per cell, a cell being a run of
@@ -184,6 +186,8 @@ struct SegParams {
   const uint32_t *ttft_cfgs;    // TTFT: sorted indices of the TTFT configs of this launch
   unsigned long long *acc;      // n_cfg * NF
   int32_t max_n;
+  int32_t halves;               // DSI_F_RNG_HALVES: the halves layout of the indicator stream
+  int32_t pad_[2];
   Keys keys;
 };
 size_t seg_hist_smem(int max_n);

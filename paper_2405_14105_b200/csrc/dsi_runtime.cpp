@@ -300,8 +300,6 @@ dsi_status dsi_sim_create(const dsi_options *opt, const dsi_config *cfg, size_t 
   const bool means_only = opt->flags & DSI_F_MEANS_ONLY;
   if (means_only && (opt->flags & (DSI_F_PER_TRIAL | DSI_F_HIST | DSI_F_PATTERN | DSI_F_SHARED_STREAMS)))
     return fail(nullptr, DSI_E_RANGE, "DSI_F_MEANS_ONLY excludes PER_TRIAL, HIST, PATTERN and SHARED_STREAMS");
-  if ((opt->flags & DSI_F_RNG_HALVES) && (opt->flags & (DSI_F_SHARED_STREAMS | DSI_F_MEANS_ONLY)))
-    return fail(nullptr, DSI_E_RANGE, "DSI_F_RNG_HALVES is not supported with SHARED_STREAMS or MEANS_ONLY");
 
   dsi_sim *h = new (std::nothrow) dsi_sim;
   if (!h) return fail(nullptr, DSI_E_NOMEM, "handle allocation");
@@ -763,6 +761,7 @@ static dsi::SegParams seg_params(dsi_sim *h, DeviceState &d, const dsi::Keys &ke
   q.acc = d.d_acc;
   q.max_n = h->max_n;
   q.keys = keys;
+  q.halves = (h->opt.flags & DSI_F_RNG_HALVES) ? 1 : 0;
   return q;
 }
 
@@ -834,6 +833,7 @@ dsi_status dsi_sim_run(dsi_sim *h) {
       q.max_runs = h->max_runs;
       q.cfg_per_block = h->cfg_per_block;
       q.any_fresh = h->any_fresh ? 1 : 0;
+      q.halves = p.halves;
       q.keys = p.keys;
       if (h->two_pass) {
         q.records = d.d_records;

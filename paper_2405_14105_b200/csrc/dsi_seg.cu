@@ -49,8 +49,10 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
   const int N = G.n_tokens;
   const int npos = N - 1;
   const int nwords = (npos + 31) >> 5;
-  const int nq = (npos + 3) >> 2;
+  const bool halves = P.halves != 0;
+  const int nq = halves ? (npos + 7) >> 3 : (npos + 3) >> 2;
   const uint32_t nthr = 0u - G.thr;
+  const HalvesCtx hc = make_halves(G.thr, G.stream_id);
 
   uint32_t *H = reinterpret_cast<uint32_t *>(smem);           // N + 1 bins
   uint4 *U = reinterpret_cast<uint4 *>(smem + (((size_t)(N + 1) * 4 + 15) & ~(size_t)15));
@@ -90,8 +92,10 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
     uint32_t cin = 1;  // position 32w is a zero (the sentinel for w = 0)
     for (int w = 0; w < nwords; ++w) {
       uint32_t R = 0u;
-      const int ncalls = min(8, nq - 8 * w);
-      if (ncalls == 8) {
+      const int ncalls = halves ? 0 : min(8, nq - 8 * w);
+      if (halves) {
+        R = gen_word_halves<SMEM>(w, nq, U, th, (uint32_t)t, hc, P.keys);
+      } else if (ncalls == 8) {
 #pragma unroll
         for (int j = 7; j >= 0; --j) {
           const uint4 u = SMEM ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), G.stream_id, P.keys);

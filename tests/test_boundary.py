@@ -127,8 +127,7 @@ def test_create_option_errors():
            dict(flags=D.DSI_F_SHARED_STREAMS | D.DSI_F_PATTERN),
            dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_PER_TRIAL), dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_HIST),
            dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_PATTERN),
-           dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_SHARED_STREAMS),
-           dict(flags=D.DSI_F_RNG_HALVES | D.DSI_F_SHARED_STREAMS), dict(flags=D.DSI_F_RNG_HALVES | D.DSI_F_MEANS_ONLY)]
+           dict(flags=D.DSI_F_MEANS_ONLY | D.DSI_F_SHARED_STREAMS)]
     for kw in bad:
         tick = kw.pop("tick", 0.01)
         with pytest.raises(D.DsiError) as e:

@@ -159,8 +159,32 @@ def test_halves_bench_workload_sample():
     sim.close()
 
 
-def test_halves_options_are_validated():
-    cfgs, tick = W.cfg1(trials=10)
-    for bad in (D.DSI_F_SHARED_STREAMS, D.DSI_F_MEANS_ONLY):
-        with pytest.raises(D.DsiError):
-            D.Simulator(cfgs, tick=tick, seed=SEED, flags=H | bad)
+MOMENTS = ("sum_dsi_ticks", "sum_si_ticks", "sumsq_dsi_ticks", "sumsq_si_ticks", "sum_segments",
+           "sum_si_iters", "sum_accepts", "n_dsi_gt_nonsi", "n_dsi_gt_si", "trials")
+MEANS = ("sum_dsi_ticks", "sum_si_ticks", "sum_segments", "sum_si_iters", "sum_accepts", "trials")
+
+
+@pytest.mark.parametrize("name", ["cfg3_sample", "cfg4", "fuzz", "ttft_mix"])
+@pytest.mark.parametrize("fresh", [False, True])
+def test_halves_every_mode_bit_identical(name, fresh):
+    """SHARED_STREAMS (fused and two-pass kernels) and MEANS_ONLY under the halves layout give the
+    per-config kernel's integers (which the tests above pin to the oracle)."""
+    if name == "cfg3_sample":
+        cfgs, tick = W.cfg3(trials=2000, cells=slice(None, None, 11))
+    elif name == "cfg4":
+        cfgs, tick = W.cfg4(trials=3000)
+    elif name == "fuzz":
+        cfgs, tick = W.fuzz(150, seed=71, trials=500)
+    else:
+        cfgs = W.rows([(1.0, 0.1, 0.7, 4, 3, 80, 0, 500, 2.5, 0.3), (1.0, 0.2, 0.7, 2, 7, 80, 0, 500),
+                       (1.0, 0.05, 0.49, 6, 5, 80, 1, 500, 1.5, 0.1), (1.0, 0.3, 0.49, 1, 7, 80, 1, 500)])
+        tick = 0.01
+        if fresh:
+            pytest.skip("the fresh verifier excludes TTFT configs")
+    base = D.DSI_F_FRESH_VERIFIER if fresh else 0
+    _, want = run_sim(cfgs, tick, base)
+    for mode, fields in ((D.DSI_F_SHARED_STREAMS, MOMENTS), (D.DSI_F_MEANS_ONLY, MEANS)):
+        sim, got = run_sim(cfgs, tick, base | mode)
+        for f in fields:
+            assert np.array_equal(got[f], want[f]), (name, fresh, mode, f)
+        sim.close()
