@@ -247,6 +247,84 @@ def other_workloads_block(D, names, args, base_kw, root, fresh_id, flush, barrie
     return out
 
 
+def alg_instructions_halves(cfgs) -> float:
+    """As alg_instructions for the halves layout (DSI_F_RNG_HALVES, R26): Philox4x32-10
+    serves 8 positions per call (40 instructions / 8 = 5 per trial-token), 1 compare, 10 per
+    rejection; the tie-break call (probability 2^-16 per position) adds < 0.001 per token."""
+    tt = cfgs["n_trials"].astype(np.float64) * cfgs["n_tokens"].astype(np.float64)
+    return float(np.sum(tt * (6.0 + 10.0 * (1.0 - cfgs["accept_rate"]))))
+
+
+def rng_halves_block(D, cfgs, tick, args, base_kw, root, fresh_id, flush, barrier, max_over_ranks, world,
+                     peak_instr) -> dict:
+    """The same workload under the halves layout of the indicator stream (DSI_F_RNG_HALVES):
+    the per-config mode timed exactly as `value` (run + reduce, CUDA events, L2 flushed), and
+    the shared-stream and means-only modes (run + reduce_device) checked bit-identical to it."""
+    import torch
+
+    tt = trial_tokens(cfgs)
+    out = {"layout": "DSI_F_RNG_HALVES (DESIGN.md R26): 16 bits per Bernoulli from Philox at (q, 0, trial, "
+                     "stream), q = (p-1) >> 3, plus an exact tie-break draw at (q, 1, trial, stream) when the 16 "
+                     "bits equal the threshold's high half: A_p = [v 2^16 + w < floor(a 2^32)], the same law as "
+                     "`value`'s layout with half the Philox calls (different draws, so different sums)"}
+    ref = None
+    for mode, flags in (("per_config", 0), ("shared_streams", D.DSI_F_SHARED_STREAMS),
+                        ("means_only", D.DSI_F_MEANS_ONLY)):
+        sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING | D.DSI_F_RNG_HALVES | root | flags, nccl_id=fresh_id(),
+                          **dict(base_kw, tick=tick))
+        st = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", base_kw["device"]))
+        res = np.zeros(cfgs.size, D.RESULT_DTYPE)
+        for _ in range(args.warmup):
+            sim.run()
+            sim.reduce(res)
+        barrier()
+        torch.cuda.synchronize()
+        ms, kms = [], []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            sim.run()
+            if flags:
+                sim.reduce_device()
+            else:
+                sim.reduce(res)
+            e1.record(st)
+            e1.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            kms.append(sim.kernel_ms())
+        barrier()
+        total = max_over_ranks(sum(ms))
+        kern = max_over_ranks(statistics.mean(kms))
+        d = {"value": tt * args.steps / (total / 1000.0), "unit": UNIT, "ms_per_step": total / args.steps,
+             "kernel_ms": kern, "launches_per_step": sim.launches()}
+        if flags == 0:
+            ach = alg_instructions_halves(cfgs) / world / (kern / 1000.0)
+            d["roofline"] = {"bound": "alu", "achieved": ach / 1e9, "peak": peak_instr / 1e9, "unit": "Ginstr/s",
+                             "frac": ach / peak_instr, "kernel": "dsi_trial_kernel<..., HALVES>",
+                             "work": "6 + 10(1-a) thread-instructions per trial-token: 5 for Philox4x32-10 (40 "
+                                     "per call of 8 indicators), 1 compare, 10 per rejection"}
+            ref = res
+        elif base_kw["rank"] == 0:
+            sim.fetch(0, cfgs.size, res)
+            fields = ("sum_si_ticks", "sum_dsi_ticks", "sum_segments", "sum_si_iters", "trials")
+            if flags == D.DSI_F_SHARED_STREAMS:
+                fields += ("sumsq_si_ticks", "sumsq_dsi_ticks", "n_dsi_gt_nonsi", "n_dsi_gt_si")
+            d["sums_identical_to_per_config"] = bool(all(np.array_equal(res[f], ref[f]) for f in fields))
+        sim.close()
+        out[mode] = d
+    if base_kw["rank"] == 0:
+        a = cfgs["accept_rate"]
+        acc = ref["sum_accepts"].astype(np.float64) / (cfgs["n_trials"] * (cfgs["n_tokens"] - 1.0))
+        sd = np.sqrt(a * (1 - a) / (cfgs["n_trials"] * (cfgs["n_tokens"] - 1.0))) + 1e-12
+        z = np.abs(acc - a) / sd
+        out["acceptance_law"] = {"max_abs_z": float(np.max(z)), "mean_z2": float(np.mean(z * z)),
+                                 "note": "per config, realised acceptance fraction vs a in units of its binomial "
+                                         "sd (mean z^2 ~ 1 for the exact law)"}
+    return out
+
+
 def trial_tokens(cfgs) -> int:
     return int(np.sum(cfgs["n_trials"].astype(np.int64) * cfgs["n_tokens"].astype(np.int64)))
 
@@ -842,6 +920,11 @@ def ours(args):
         others = other_workloads_block(D, ("cfg5", "cfg4", "cfg2"), args, base_kw, root, fresh_nccl_id, flush,
                                        barrier, max_over_ranks, world)
 
+    halves = None
+    if not args.no_halves:
+        halves = rng_halves_block(D, cfgs, tick, args, base_kw, root, fresh_nccl_id, flush, barrier,
+                                  max_over_ranks, world, peak_instr)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O
@@ -904,6 +987,7 @@ def ours(args):
             "means_only": means,
             "multi_drafter": multi,
             "other_workloads": others,
+            "rng_halves": halves,
             "clocks": clk,
             "create_s": create_s,
             "wall_s_timed": wall,
@@ -931,6 +1015,7 @@ def main():
     ap.add_argument("--no-means", action="store_true", help="skip the means-only block")
     ap.add_argument("--no-fresh", action="store_true", help="skip the fresh-verifier (R24) heatmap block")
     ap.add_argument("--no-others", action="store_true", help="skip BASELINE's other configs (cfg5, cfg4, cfg2)")
+    ap.add_argument("--no-halves", action="store_true", help="skip the DSI_F_RNG_HALVES block")
     args = ap.parse_args()
     if args.gpus < 1:
         raise SystemExit("--gpus must be >= 1")

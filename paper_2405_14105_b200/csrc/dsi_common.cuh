@@ -147,10 +147,26 @@ __device__ __forceinline__ uint32_t tie_flags(const Word4 &u, uint32_t TT, uint3
   return acc | heq2(u.x ^ TT, 0u) | heq2(u.y ^ TT, 0u) | heq2(u.z ^ TT, 0u) | heq2(u.w ^ TT, 0u);
 }
 
-// All ten rounds of Philox4x32-10 at counter (c0, c1, c2, c3) (the rare tie path).
-__device__ __forceinline__ Word4 philox_full(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const Keys &K) {
+__device__ __forceinline__ uint32_t half_of(const Word4 &o, int j) {
+  const int i = j & 3;
+  const uint32_t x = i == 0 ? o.x : i == 1 ? o.y : i == 2 ? o.z : o.w;
+  return j < 4 ? x >> 16 : x & 0xFFFFu;
+}
+
+// Exact decisions of every tied position among calls 4w .. 4w + ncalls - 1 (bits 8c + j of R):
+// rejected iff w >= R_low, w from the tie-break call (q, 1, trial, stream).  Rare (a warp takes
+// it for ~1.6% of its words): the word's calls are regenerated one by one (rounds 2-9 from the
+// per-counter half, as a loop: few registers, so no spills in the caller), and the tie-break call shares
+// the main call's per-counter half of rounds 0-1 (counter word 1 enters round 0 only through
+// the trial half: n0 = hi(M1 trial) ^ 1 ^ k0[0]).  Few scalar arguments (the trial half is
+// recomputed): a reference to a caller's local would force it to the stack, and every argument
+// register is one more value the hot loop must keep around the call.
+// Rounds 2-9 as a loop (few registers: the callee's register count is what the caller must
+// save around the call).
+__device__ __forceinline__ Word4 philox_call_rolled(const uint4 &u, const TrialHalf &t, const Keys &K) {
+  uint32_t c0 = u.x ^ t.n1, c1 = u.y, c2 = t.ha ^ u.z, c3 = t.la;
 #pragma unroll 1
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 2; r < 10; ++r) {
     const uint64_t a = (uint64_t)PHILOX_M0 * c0;
     const uint64_t b = (uint64_t)PHILOX_M1 * c2;
     const uint32_t n0 = (uint32_t)(b >> 32) ^ c1 ^ K.k0[r];
@@ -163,26 +179,25 @@ __device__ __forceinline__ Word4 philox_full(uint32_t c0, uint32_t c1, uint32_t 
   return Word4{c0, c1, c2, c3};
 }
 
-__device__ __forceinline__ uint32_t half_of(const Word4 &o, int j) {
-  const int i = j & 3;
-  const uint32_t x = i == 0 ? o.x : i == 1 ? o.y : i == 2 ? o.z : o.w;
-  return j < 4 ? x >> 16 : x & 0xFFFFu;
-}
-
-// Exact decisions of every tied position among calls q0 .. q0 + ncalls - 1 (bits 8c + j of R):
-// rejected iff w >= R_low, w from the tie-break call (q, 1, trial, stream).
-static __device__ __noinline__ uint32_t halves_fix(uint32_t R, int q0, int ncalls, uint32_t trial, uint32_t stream,
-                                            uint32_t thr, const Keys &K) {
+template <bool TABLE>
+static __device__ __noinline__ uint32_t halves_fix(uint32_t R, int w, int ncalls, const uint4 *U, uint32_t trial,
+                                                   uint32_t stream, uint32_t thr, const Keys &K) {
   const uint32_t T = thr >> 16, Rl = thr & 0xFFFFu;
+  const TrialHalf th = philox_trial_half(trial, K);
+  const uint64_t p = (uint64_t)PHILOX_M1 * trial;
+  const uint32_t n0 = (uint32_t)(p >> 32) ^ 1u ^ K.k0[0];
+  const uint64_t a = (uint64_t)PHILOX_M0 * n0;
+  const TrialHalf tb_half{(uint32_t)p, (uint32_t)(a >> 32), (uint32_t)a};
   for (int c = 0; c < ncalls; ++c) {
-    const uint32_t q = (uint32_t)(q0 + c);
-    const Word4 o = philox_full(q, 0u, trial, stream, K);
+    const int q = 4 * w + c;
+    const uint4 u = TABLE ? U[q] : philox_q_half((uint32_t)q, stream, K);
+    const Word4 o = philox_call_rolled(u, th, K);
     bool have = false;
     Word4 tb{0u, 0u, 0u, 0u};
     for (int j = 0; j < 8; ++j) {
       if (half_of(o, j) != T) continue;
       if (!have) {
-        tb = philox_full(q, 1u, trial, stream, K);
+        tb = philox_call_rolled(u, tb_half, K);
         have = true;
       }
       const uint32_t bit = 1u << (8 * c + j);
@@ -216,7 +231,7 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
     }
   }
   R |= h.orall;
-  if (tf) R = halves_fix(R, 4 * w, ncalls, trial, h.stream, h.thr, K);
+  if (tf) R = halves_fix<TABLE>(R, w, ncalls, U, trial, h.stream, h.thr, K);
   return R;
 }
 template <bool TABLE>
@@ -224,6 +239,35 @@ __device__ __forceinline__ uint32_t gen_word_halves(int w, int nq, const uint4 *
                                                     const HalvesCtx &h, const Keys &K) {
   return h.direct ? gen_word_halves_t<true, TABLE>(w, nq, U, th, trial, h, K)
                   : gen_word_halves_t<false, TABLE>(w, nq, U, th, trial, h, K);
+}
+
+// Words w and w+1 (both full: 8 calls) in one straight-line block, one tie test for both.
+template <bool DIRECT, bool TABLE>
+__device__ __forceinline__ void gen_2words_halves_t(int w, const uint4 *U, const TrialHalf &th, uint32_t trial,
+                                                    const HalvesCtx &h, const Keys &K, uint32_t &R0, uint32_t &R1) {
+  uint32_t a = 0u, b = 0u, tf = 0u;
+#pragma unroll
+  for (int j = 7; j >= 0; --j) {
+    const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
+    const Word4 o = philox_call(u, th, K);
+    if (j >= 4) b = pack8(b, o, h.C);
+    else a = pack8(a, o, h.C);
+    tf = tie_flags<DIRECT>(o, h.TT, tf);
+  }
+  a |= h.orall;
+  b |= h.orall;
+  if (tf) {
+    a = halves_fix<TABLE>(a, w, 4, U, trial, h.stream, h.thr, K);
+    b = halves_fix<TABLE>(b, w + 1, 4, U, trial, h.stream, h.thr, K);
+  }
+  R0 = a;
+  R1 = b;
+}
+template <bool TABLE>
+__device__ __forceinline__ void gen_2words_halves(int w, const uint4 *U, const TrialHalf &th, uint32_t trial,
+                                                  const HalvesCtx &h, const Keys &K, uint32_t &R0, uint32_t &R1) {
+  if (h.direct) gen_2words_halves_t<true, TABLE>(w, U, th, trial, h, K, R0, R1);
+  else gen_2words_halves_t<false, TABLE>(w, U, th, trial, h, K, R0, R1);
 }
 
 // floor(x / d) for x * d <= 2^32 with M = ceil(2^32 / d) = lo + hi * 2^32.

@@ -21,6 +21,7 @@ ap.add_argument("--stride", type=int, default=10)
 ap.add_argument("--runs", type=int, default=1)
 ap.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
 ap.add_argument("--means", action="store_true", help="DSI_F_MEANS_ONLY")
+ap.add_argument("--halves", action="store_true", help="DSI_F_RNG_HALVES")
 args = ap.parse_args()
 if args.workload == "cfg3":
     cfgs, tick = W.cfg3(cells=slice(None, None, args.stride))
@@ -29,7 +30,8 @@ elif args.workload == "cfg5":
     cfgs = cfgs[:: args.stride]
 else:
     raise SystemExit("workload")
-flags = (D.DSI_F_SHARED_STREAMS if args.shared else 0) | (D.DSI_F_MEANS_ONLY if args.means else 0)
+flags = (D.DSI_F_SHARED_STREAMS if args.shared else 0) | (D.DSI_F_MEANS_ONLY if args.means else 0) | \
+    (D.DSI_F_RNG_HALVES if args.halves else 0)
 with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
     for _ in range(args.runs):
         sim.run()
