@@ -50,6 +50,9 @@ constexpr int TABLE_MAX_N = 4096;
 #ifndef DSI_TRIAL_MINB
 #define DSI_TRIAL_MINB 5
 #endif
+#ifndef DSI_TRIAL_MINB_HALVES
+#define DSI_TRIAL_MINB_HALVES 4  // halves layout: min 4 blocks 1.3% faster than 5, 6 1.0% slower
+#endif                           // (profiles/r02c_ab_halves_minb.jsonl)
 #ifndef DSI_PIPE_WALK
 #define DSI_PIPE_WALK 1  // (cfg3 sample 243.16 -> 242.38 ms, profiles/r02_ab_pipewalk.jsonl)
 #endif
@@ -143,7 +146,8 @@ __host__ __device__ __forceinline__ size_t u_table_bytes(int n) { return (size_t
 //      3 = default model with the k = 1 no-queue fast path compiled in (LaunchParams.k1_fast)
 // HALVES: the halves layout of the indicator stream (DSI_F_RNG_HALVES, dsi_common.cuh)
 template <bool PER_TRIAL, bool HIST, bool PATTERN, bool TABLE, int VAR, bool HALVES>
-__global__ void __launch_bounds__(DSI_TRIAL_MAXT, DSI_TRIAL_MINB) dsi_trial_kernel(const LaunchParams P) {
+__global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES : DSI_TRIAL_MINB)
+    dsi_trial_kernel(const LaunchParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
 
   __shared__ uint32_t s_cfg;
