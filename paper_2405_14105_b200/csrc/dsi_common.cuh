@@ -215,13 +215,42 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
   uint32_t R = 0u, tf = 0u;
   const int ncalls = min(4, nq - 4 * w);
   if (ncalls == 4) {
+    Word4 o[4];
 #pragma unroll
     for (int j = 3; j >= 0; --j) {
       const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
-      const Word4 o = philox_call(u, th, K);
-      R = pack8(R, o, h.C);
-      tf = tie_flags<DIRECT>(o, h.TT, tf);
+      o[j] = philox_call(u, th, K);
+      R = pack8(R, o[j], h.C);
+      tf = tie_flags<DIRECT>(o[j], h.TT, tf);
     }
+    R |= h.orall;
+    // rare (~1.6% of warp-words): the word's outputs are still in registers, so only the tie-break
+    // calls are computed (inline: 187.1 ms vs 188.0 with halves_fix's regeneration; guarding it
+    // with a warp vote 195.8 ms -- profiles/r02c_ab_halves_inl.jsonl, r02c_ab_halves_vote.jsonl)
+    if (tf) {
+      const uint32_t T = h.thr >> 16, Rl = h.thr & 0xFFFFu;
+      const uint64_t p = (uint64_t)PHILOX_M1 * trial;
+      const uint32_t n0 = (uint32_t)(p >> 32) ^ 1u ^ K.k0[0];
+      const uint64_t a = (uint64_t)PHILOX_M0 * n0;
+      const TrialHalf tb_half{(uint32_t)p, (uint32_t)(a >> 32), (uint32_t)a};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t m = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m |= (half_of(o[c], j) == T ? 1u : 0u) << j;
+        if (m) {
+          const int q = 4 * w + c;
+          const uint4 u = TABLE ? U[q] : philox_q_half((uint32_t)q, h.stream, K);
+          const Word4 tb = philox_call_rolled(u, tb_half, K);
+          for (int j = 0; j < 8; ++j)
+            if ((m >> j) & 1u) {
+              const uint32_t bit = 1u << (8 * c + j);
+              R = half_of(tb, j) >= Rl ? (R | bit) : (R & ~bit);
+            }
+        }
+      }
+    }
+    return R;
   } else {
     for (int j = ncalls - 1; j >= 0; --j) {
       const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
