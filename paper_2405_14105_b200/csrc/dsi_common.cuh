@@ -270,35 +270,6 @@ __device__ __forceinline__ uint32_t gen_word_halves(int w, int nq, const uint4 *
                   : gen_word_halves_t<false, TABLE>(w, nq, U, th, trial, h, K);
 }
 
-// Words w and w+1 (both full: 8 calls) in one straight-line block, one tie test for both.
-template <bool DIRECT, bool TABLE>
-__device__ __forceinline__ void gen_2words_halves_t(int w, const uint4 *U, const TrialHalf &th, uint32_t trial,
-                                                    const HalvesCtx &h, const Keys &K, uint32_t &R0, uint32_t &R1) {
-  uint32_t a = 0u, b = 0u, tf = 0u;
-#pragma unroll
-  for (int j = 7; j >= 0; --j) {
-    const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
-    const Word4 o = philox_call(u, th, K);
-    if (j >= 4) b = pack8(b, o, h.C);
-    else a = pack8(a, o, h.C);
-    tf = tie_flags<DIRECT>(o, h.TT, tf);
-  }
-  a |= h.orall;
-  b |= h.orall;
-  if (tf) {
-    a = halves_fix<TABLE>(a, w, 4, U, trial, h.stream, h.thr, K);
-    b = halves_fix<TABLE>(b, w + 1, 4, U, trial, h.stream, h.thr, K);
-  }
-  R0 = a;
-  R1 = b;
-}
-template <bool TABLE>
-__device__ __forceinline__ void gen_2words_halves(int w, const uint4 *U, const TrialHalf &th, uint32_t trial,
-                                                  const HalvesCtx &h, const Keys &K, uint32_t &R0, uint32_t &R1) {
-  if (h.direct) gen_2words_halves_t<true, TABLE>(w, U, th, trial, h, K, R0, R1);
-  else gen_2words_halves_t<false, TABLE>(w, U, th, trial, h, K, R0, R1);
-}
-
 // floor(x / d) for x * d <= 2^32 with M = ceil(2^32 / d) = lo + hi * 2^32.
 __device__ __forceinline__ uint32_t magic_div(uint32_t x, uint32_t lo, uint32_t hi) {
   return __umulhi(x, lo) + x * hi;

@@ -56,9 +56,6 @@ constexpr int TABLE_MAX_N = 4096;
 #ifndef DSI_PIPE_WALK
 #define DSI_PIPE_WALK 1  // (cfg3 sample 243.16 -> 242.38 ms, profiles/r02_ab_pipewalk.jsonl)
 #endif
-#ifndef DSI_HALVES_PAIR
-#define DSI_HALVES_PAIR 0  // halves layout: generate two full words per straight-line block
-#endif
 #ifndef DSI_TRIAL_MAXT
 #define DSI_TRIAL_MAXT 128
 #endif  // larger N: arithmetic segment costs, per-call rounds 0-1
@@ -312,22 +309,12 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
       }
     }
 #endif
-    uint32_t R_next = 0u;
-    bool have_next = false;
     for (int w = w_start; w < nwords; ++w) {
       uint32_t R;
       if (PATTERN) {
         R = ~trial;  // N <= 33: one word, A_p = bit p-1 of the trial index
       } else if (mode == MODE_STREAM && HALVES) {
-        if (DSI_HALVES_PAIR && have_next) {
-          R = R_next;
-          have_next = false;
-        } else if (DSI_HALVES_PAIR && 4 * w + 8 <= nq) {
-          gen_2words_halves<TABLE>(w, U, th, trial, hc, P.keys, R, R_next);
-          have_next = true;
-        } else {
-          R = gen_word_halves<TABLE>(w, nq, U, th, trial, hc, P.keys);
-        }
+        R = gen_word_halves<TABLE>(w, nq, U, th, trial, hc, P.keys);
       } else if (mode == MODE_STREAM) {
         R = 0u;
         const int ncalls = min(8, nq - 8 * w);
