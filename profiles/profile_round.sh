@@ -2,7 +2,8 @@
 #   1. launch list of the bench command (every launch with its device time);
 #   2. DRAM bytes of one full bench launch (cfg3, 6.06 M blocks) -> roofline.traffic;
 #   3. --set full on one full bench launch of the same kernel (cfg3, every config);
-#   4. --set full on the shared-stream kernel, the multi-drafter kernel and the means-only kernels.
+#   4. --set full on one full launch of the halves-layout trial kernel (DSI_F_RNG_HALVES);
+#   5. --set full on the shared-stream kernel, the multi-drafter kernel and the means-only kernels.
 # Then profiles/summarize_ncu.py turns them into profiles/latest_ncu_summary.json.
 set -u
 R=${1:-r01}
@@ -16,6 +17,9 @@ timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:dsi_trial_kernel -c 1 \
   -o gpurun_out/prof_${R} python profiles/ncu_driver.py --workload cfg3 --stride 1 \
   > gpurun_out/ncu_full_${R}.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:dsi_trial_kernel -c 1 \
+  -o gpurun_out/prof_halves_${R} python profiles/ncu_driver.py --workload cfg3 --stride 1 --halves \
+  > gpurun_out/ncu_full_halves_${R}.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:dsi_crn -c 2 \
   -o gpurun_out/prof_crn_${R} python profiles/ncu_driver.py --workload cfg3 --stride 1 --shared \
   > gpurun_out/ncu_full_crn_${R}.log 2>&1

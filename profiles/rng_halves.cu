@@ -129,6 +129,18 @@ __device__ __forceinline__ uint32_t ties_pred(const uint4 &u, uint32_t TT, uint3
   return r;
 }
 
+// 16x2 integer min form: d = u ^ TT has a zero lane exactly at a tie; a running lane-wise min over
+// the word's calls (VIMNMX3.U16x2 on the ALU pipe) has a zero lane iff some call tied
+__device__ __forceinline__ uint32_t ties_min16(const uint4 &u, uint32_t TT, uint32_t acc) {
+  acc = __vimin3_u16x2(u.x ^ TT, u.y ^ TT, acc);
+  return __vimin3_u16x2(u.z ^ TT, u.w ^ TT, acc);
+}
+// hybrid: x, y by HSET2 (fma pipe) into acc_h, z, w by the 16x2 min (ALU) into acc_m
+__device__ __forceinline__ void ties_hybrid(const uint4 &u, uint32_t TT, uint32_t &acc_h, uint32_t &acc_m) {
+  acc_h = acc_h | heq(u.x, TT) | heq(u.y, TT);
+  acc_m = __vimin3_u16x2(u.z ^ TT, u.w ^ TT, acc_m);
+}
+
 // exact per-position decision (slow reference), position j of call (q, trial)
 __device__ __forceinline__ bool reject_ref(uint32_t q, uint32_t j, uint32_t trial, uint32_t thr, const Keys &K) {
   uint32_t o[4], t[4];
@@ -229,6 +241,29 @@ __global__ void __launch_bounds__(128, 5) kern(Keys K, int trials, uint32_t thr,
         if (w == 3) R &= 7u;
         acc += __popc(R);
       }
+    } else if (V == 7 || V == 8) {  // halves, carry pack + 16x2-min (7) or hybrid (8) tie test
+      const uint32_t TT = T | (T << 16);
+      for (int w = 0; w < 4; ++w) {
+        uint32_t R = 0, am = 0xFFFFFFFFu, ah = 0u;
+        const int nc = w < 3 ? 4 : 1;
+#pragma unroll
+        for (int j = 3; j >= 0; --j) {
+          if (j >= nc) continue;
+          const uint4 u = U[4 * w + j];
+          const uint4 o = rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K);
+          R = pack8c(R, o, C);
+          if (V == 7) am = ties_min16(o, TT, am);
+          else ties_hybrid(o, TT, ah, am);
+        }
+        R |= orall;
+        const bool tied = ((am & 0xFFFFu) == 0u) | ((am >> 16) == 0u) | (ah != 0u);
+        if (tied) {
+          R = fix_ties(R, w, trial, thr, K);
+          ++nt;
+        }
+        if (w == 3) R &= 7u;
+        acc += __popc(R);
+      }
     } else if (V == 1 || V == 2) {  // halves, N = 100: 13 calls (4 words of 4 calls; last word 1 call, 3 bits)
       for (int w = 0; w < 4; ++w) {
         uint32_t R = 0, tmin = 0xFFFFFFFFu;
@@ -309,6 +344,8 @@ int main() {
     run<4>("halves, carry pack + xor/HSET2 tie flags + fix", K, thr, ref, sms, nullptr);
     run<5>("halves, carry pack + direct HSET2 tie flags + fix (T not NaN)", K, thr, ref, sms, nullptr);
     run<6>("halves, carry pack + HSETP2.OR predicate tie flag + fix (T not NaN)", K, thr, ref, sms, nullptr);
+    run<7>("halves, carry pack + xor/16x2-min tie test + fix", K, thr, ref, sms, nullptr);
+    run<8>("halves, carry pack + hybrid HSET2 / 16x2-min tie test + fix (T not NaN)", K, thr, ref, sms, nullptr);
     run<0>("32-bit contract, carry pack (the product's)", K, thr, 0, sms, nullptr);
   }
   return 0;
