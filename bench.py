@@ -255,8 +255,8 @@ def alg_instructions_halves(cfgs) -> float:
     return float(np.sum(tt * (6.0 + 10.0 * (1.0 - cfgs["accept_rate"]))))
 
 
-def rng_halves_block(D, cfgs, tick, args, base_kw, root, fresh_id, flush, barrier, max_over_ranks, world,
-                     peak_instr) -> dict:
+def rng_halves_block(D, cfgs, cfgs_pinned, tick, args, base_kw, root, fresh_id, flush, barrier, max_over_ranks,
+                     world, peak_instr) -> dict:
     """The same workload under the halves layout of the indicator stream (DSI_F_RNG_HALVES):
     the per-config mode timed exactly as `value` (run + reduce, CUDA events, L2 flushed), and
     the shared-stream and means-only modes (run + reduce_device) checked bit-identical to it."""
@@ -300,6 +300,21 @@ def rng_halves_block(D, cfgs, tick, args, base_kw, root, fresh_id, flush, barrie
         d = {"value": tt * args.steps / (total / 1000.0), "unit": UNIT, "ms_per_step": total / args.steps,
              "kernel_ms": kern, "launches_per_step": sim.launches()}
         if flags == 0:
+            # end to end as `e2e`: update (configs from pinned host memory) + run + reduce to the host
+            h2d, d2h = sim.io_bytes()
+            sim.update(cfgs_pinned)
+            sim.run()
+            sim.reduce(res)
+            barrier()
+            ts = []
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                sim.update(cfgs_pinned)
+                sim.run()
+                sim.reduce(res)
+                ts.append(time.perf_counter() - t0)
+            d["e2e"] = {"value": tt * args.steps / max_over_ranks(sum(ts)), "unit": UNIT,
+                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
             ach = alg_instructions_halves(cfgs) / world / (kern / 1000.0)
             d["roofline"] = {"bound": "alu", "achieved": ach / 1e9, "peak": peak_instr / 1e9, "unit": "Ginstr/s",
                              "frac": ach / peak_instr, "kernel": "dsi_trial_kernel<..., HALVES>",
@@ -319,9 +334,15 @@ def rng_halves_block(D, cfgs, tick, args, base_kw, root, fresh_id, flush, barrie
         acc = ref["sum_accepts"].astype(np.float64) / (cfgs["n_trials"] * (cfgs["n_tokens"] - 1.0))
         sd = np.sqrt(a * (1 - a) / (cfgs["n_trials"] * (cfgs["n_tokens"] - 1.0))) + 1e-12
         z = np.abs(acc - a) / sd
-        out["acceptance_law"] = {"max_abs_z": float(np.max(z)), "mean_z2": float(np.mean(z * z)),
-                                 "note": "per config, realised acceptance fraction vs a in units of its binomial "
-                                         "sd (mean z^2 ~ 1 for the exact law)"}
+        _, first = np.unique(np.stack([cfgs["accept_rate"], cfgs["stream_id"].astype(np.float64),
+                                       cfgs["n_tokens"].astype(np.float64), cfgs["n_trials"].astype(np.float64)]),
+                             axis=1, return_index=True)
+        zi = z[first]  # one per distinct indicator stream (configs of a group draw identical indicators)
+        out["acceptance_law"] = {"streams": int(first.size), "max_abs_z": float(np.max(zi)),
+                                 "mean_z2": float(np.mean(zi * zi)),
+                                 "note": "per distinct (a, stream, N, T) -- every config of such a group draws the "
+                                         "same indicators -- the realised acceptance fraction vs a in units of its "
+                                         "binomial sd (mean z^2 ~ 1 for the exact law)"}
     return out
 
 
@@ -922,7 +943,7 @@ def ours(args):
 
     halves = None
     if not args.no_halves:
-        halves = rng_halves_block(D, cfgs, tick, args, base_kw, root, fresh_nccl_id, flush, barrier,
+        halves = rng_halves_block(D, cfgs, cfgs_pinned, tick, args, base_kw, root, fresh_nccl_id, flush, barrier,
                                   max_over_ranks, world, peak_instr)
 
     cpu = None
