@@ -54,7 +54,7 @@ def cmd_simulate(a) -> dict:
     cfg = np.zeros(1, D.CONFIG_DTYPE)
     cfg[0] = (a.t_target, a.t_drafter, a.accept, a.lookahead, a.sp, a.n_tokens, a.stream, a.trials,
               a.ttft_target, a.ttft_drafter)
-    flags = D.DSI_F_FRESH_VERIFIER if a.fresh else 0
+    flags = (D.DSI_F_FRESH_VERIFIER if a.fresh else 0) | (D.DSI_F_RNG_HALVES if a.rng_halves else 0)
     with D.Simulator(cfg, tick=a.tick, seed=a.seed, flags=flags) as sim:
         r = sim.run().reduce()[0]
     return {k: (float(r[k]) if r.dtype[k].kind == "f" else int(r[k])) for k in r.dtype.names}
@@ -117,7 +117,7 @@ def cmd_heatmap(a) -> dict:
     else:
         cfgs, tick = W.cfg3(trials=a.trials, k_max=a.k_max, sp=a.sp, n_tokens=a.n_tokens)
     flags = ((D.DSI_F_SHARED_STREAMS if a.shared else 0) | (D.DSI_F_FRESH_VERIFIER if a.fresh else 0) |
-             (D.DSI_F_MEANS_ONLY if a.means else 0))
+             (D.DSI_F_MEANS_ONLY if a.means else 0) | (D.DSI_F_RNG_HALVES if a.rng_halves else 0))
     kw, rank = _distributed_kw()  # torchrun: the grid is sharded over the ranks' GPUs
     with D.Simulator(cfgs, tick=tick, seed=a.seed, flags=flags, **kw) as sim:
         cells = sim.run().heatmap()  # collective: every rank gets every cell
@@ -166,6 +166,7 @@ def main(argv=None) -> int:
     p.add_argument("--ttft-target", type=float, default=0.0, help="first target forward (0 = TPOT)")
     p.add_argument("--ttft-drafter", type=float, default=0.0, help="first drafter forward (0 = TPOT)")
     p.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER (DESIGN.md R24)")
+    p.add_argument("--rng-halves", action="store_true", help="DSI_F_RNG_HALVES (DESIGN.md R26)")
     p = sub.add_parser("table2", help="Table 2 pairs offline, lookahead in {1, 5, 10}")
     p.add_argument("--trials", type=int, default=100_000)
     p.add_argument("--sp", type=int, default=None, help="default 8, or 7 with --prefill (P:273)")
@@ -182,6 +183,7 @@ def main(argv=None) -> int:
     p.add_argument("--shared", action="store_true", help="DSI_F_SHARED_STREAMS")
     p.add_argument("--means", action="store_true", help="DSI_F_MEANS_ONLY (segment histograms; no std)")
     p.add_argument("--fresh", action="store_true", help="DSI_F_FRESH_VERIFIER (DESIGN.md R24)")
+    p.add_argument("--rng-halves", action="store_true", help="DSI_F_RNG_HALVES (DESIGN.md R26)")
     p = sub.add_parser("multi", help="Alg. 1 with several drafters (lookahead 1, unbounded threads)")
     p.add_argument("--t-target", type=float, required=True)
     p.add_argument("--drafter", action="append", required=True, help="latency:acceptance, fastest first")
