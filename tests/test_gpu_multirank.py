@@ -37,7 +37,10 @@ def _cases():
             ("means", c3, tick3, D.DSI_F_MEANS_ONLY), ("means_ttft", ttft, ttick, D.DSI_F_MEANS_ONLY),
             ("fresh", fz, ftick, D.DSI_F_FRESH_VERIFIER),
             ("shared_fresh", c3, tick3, D.DSI_F_SHARED_STREAMS | D.DSI_F_FRESH_VERIFIER),
-            ("shared_ttft", ttft, ttick, D.DSI_F_SHARED_STREAMS)]
+            ("shared_ttft", ttft, ttick, D.DSI_F_SHARED_STREAMS),
+            ("halves", fz, ftick, D.DSI_F_RNG_HALVES),
+            ("halves_shared", c3, tick3, D.DSI_F_SHARED_STREAMS | D.DSI_F_RNG_HALVES),
+            ("halves_means", c3, tick3, D.DSI_F_MEANS_ONLY | D.DSI_F_RNG_HALVES)]
 
 
 CURRENT = {"case": None}
