@@ -188,3 +188,42 @@ def test_halves_every_mode_bit_identical(name, fresh):
         for f in fields:
             assert np.array_equal(got[f], want[f]), (name, fresh, mode, f)
         sim.close()
+
+
+def test_halves_bench_workload_full_size():
+    """The bench workload (cfg3: 2.02 M configs x 1e4 trials, N 100) under the halves layout in the
+    bench's launch configuration: sampled configs recomputed by the oracle over all their trials, the
+    theorem counters on every config, and every one of the 2.02 M Monte Carlo means within 6 sigma of
+    its exact expectation (the halves layout's law, Bernoulli(floor(a 2^32) / 2^32), at full scale)."""
+    cfgs, tick = W.cfg3()
+    sim, res = run_sim(cfgs, tick, D.DSI_F_TIMING)
+    sim.close()
+    assert np.all(res["trials"] == 10_000)
+    idx = np.unique(np.concatenate([np.linspace(0, cfgs.size - 1, 16).round().astype(int),
+                                    np.random.default_rng(5).integers(0, cfgs.size, 8)]))
+    for i in idx:
+        assert_result_equals_oracle(res[i], oracle_sums(cfgs[i], tick, SEED, halves=True), tick, ctx=f"cfg3[{i}]")
+    kd = res["t_drafter_ticks"] * cfgs["lookahead"]
+    inside = kd <= res["t_target_ticks"]
+    assert np.all(res["n_dsi_gt_nonsi"][inside] == 0)
+    assert np.all(res["n_dsi_gt_si"][inside & (res["eq1_feasible"] == 1)] == 0)
+    from test_heatmap import exact_results
+    ex = exact_results(cfgs, tick)
+    for f, s in (("mean_si", "std_si"), ("mean_dsi", "std_dsi")):
+        dev = np.abs(res[f] - ex[f])
+        lim = 6.0 * res[s] / np.sqrt(10_000.0) + 1e-9 * ex[f]
+        assert np.all(dev <= lim), (f, int(np.sum(dev > lim)))
+
+
+def test_halves_large_monte_carlo_sampled():
+    """BASELINE configs[4] (cfg5: 10 100 cells at the Eq.-1 lookahead, 1e5 trials, N 1000; mostly the
+    k = 1 fast-path variant) under the halves layout; one config against the oracle over all its
+    trials, the partition and Thm 1 on every config."""
+    cfgs, tick = W.cfg5(D.dsi_min_lookahead)
+    sim, res = run_sim(cfgs, tick, 0)
+    sim.close()
+    assert np.all(res["trials"] == cfgs["n_trials"])
+    kd = res["t_drafter_ticks"] * cfgs["lookahead"]
+    assert np.all(res["n_dsi_gt_nonsi"][kd <= res["t_target_ticks"]] == 0)
+    i = 50 * 101 + 80  # t_d 0.51, a 0.80
+    assert_result_equals_oracle(res[i], oracle_sums(cfgs[i], tick, SEED, halves=True), tick, ctx="cfg5")
