@@ -227,3 +227,23 @@ def test_halves_large_monte_carlo_sampled():
     assert np.all(res["n_dsi_gt_nonsi"][kd <= res["t_target_ticks"]] == 0)
     i = 50 * 101 + 80  # t_d 0.51, a 0.80
     assert_result_equals_oracle(res[i], oracle_sums(cfgs[i], tick, SEED, halves=True), tick, ctx="cfg5")
+
+
+@pytest.mark.parametrize("mode", [0, D.DSI_F_SHARED_STREAMS, D.DSI_F_MEANS_ONLY])
+def test_halves_update_equals_a_fresh_handle(mode):
+    """dsi_sim_update under the halves layout (device path where eligible): a handle updated to new
+    config values gives the integers of a handle created with them."""
+    a, tick = W.cfg3(trials=400, k_max=12, cells=slice(0, 404))  # 4 t_d x 101 a x k 1..12
+    b = a.copy()  # new drafter latencies and lookaheads (as test_gpu_update_device.py)
+    b["t_drafter"] = np.round(b["t_drafter"] * 2 + 0.01, 2)
+    b["lookahead"] = np.maximum(1, 13 - b["lookahead"])
+    sim = D.Simulator(a, tick=tick, seed=SEED, flags=mode | H)
+    sim.run()
+    sim.reduce()
+    sim.update(b)
+    got = sim.run().reduce()
+    sim.close()
+    _, want = run_sim(b, tick, mode)
+    fields = MEANS if mode == D.DSI_F_MEANS_ONLY else MOMENTS
+    for f in fields:
+        assert np.array_equal(got[f], want[f]), (mode, f)
