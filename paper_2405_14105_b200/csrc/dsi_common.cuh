@@ -252,7 +252,11 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
     }
     return R;
   } else {
-    for (int j = ncalls - 1; j >= 0; --j) {
+    // the last word: 1 to 3 calls, unrolled with warp-uniform guards (cfg3 sample 187.1 -> 184.8 ms
+    // against a loop, profiles/r02e_ab_halves_tail.jsonl)
+#pragma unroll
+    for (int j = 2; j >= 0; --j) {
+      if (j >= ncalls) continue;
       const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
       const Word4 o = philox_call(u, th, K);
       R = pack8(R, o, h.C);

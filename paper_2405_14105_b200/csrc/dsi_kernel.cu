@@ -325,6 +325,8 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
             R = pack4(R, philox_call(u, th, P.keys), nthr);
           }
         } else {
+          // (a loop: unrolled with warp-uniform guards it was 1% slower on cfg3, equal on cfg5,
+          //  profiles/r02e_ab_words_tail*.jsonl -- unlike the halves layout's last word)
           for (int j = ncalls - 1; j >= 0; --j) {
             const uint4 u = TABLE ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), cfg.stream_id, P.keys);
             R = pack4(R, philox_call(u, th, P.keys), nthr);
