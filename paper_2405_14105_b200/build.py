@@ -1,12 +1,15 @@
 """Build the simulator library in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-Three builds of the same sources:
+Four builds of the same sources:
   libdsi_sim.so         the product (no test hooks, no developer knobs)
   libdsi_sim_test.so    -DDSI_TEST_HOOKS: adds include/dsi_sim_testing.h (host all-reduce hook,
                         A/B knobs) for the multi-rank-on-one-GPU tests and A/B runs
   libdsi_sim_mutant.so  -DDSI_TEST_HOOKS -DDSI_MUTANT_CG: every DSI segment cost C(g), g >= 2,
                         one tick too large -- the mutation test (tests/test_mutation.py) checks
                         that GPU parity against the oracle FAILS with it
+  libdsi_sim_checked.so -DDSI_TEST_HOOKS -DDSI_BOUNDS_CHECK: the kernels' computed indices checked
+                        (DSI_CHECK traps) -- tests/test_bounds_checked.py runs every kernel variant
+                        under it (compute-sanitizer is closed on the GPU pool)
 Each library embeds the SHA-256 of its sources and flags (dsi_build_id()); a build is redone
 whenever the embedded id differs from that of the current sources, so a snapshot shipped to a
 GPU box always runs a build of exactly the tree it carries.  Objects compile in parallel.
@@ -33,7 +36,8 @@ HEADERS = [os.path.join(CSRC, f) for f in ("dsi_host.h", "dsi_device.h", "dsi_co
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 VARIANTS = {"product": ("libdsi_sim.so", []),
             "test": ("libdsi_sim_test.so", ["-DDSI_TEST_HOOKS"]),
-            "mutant": ("libdsi_sim_mutant.so", ["-DDSI_TEST_HOOKS", "-DDSI_MUTANT_CG"])}
+            "mutant": ("libdsi_sim_mutant.so", ["-DDSI_TEST_HOOKS", "-DDSI_MUTANT_CG"]),
+            "checked": ("libdsi_sim_checked.so", ["-DDSI_TEST_HOOKS", "-DDSI_BOUNDS_CHECK"])}
 LIB = os.path.join(PKG, VARIANTS["product"][0])
 TEST_LIB = os.path.join(PKG, VARIANTS["test"][0])
 MUTANT_LIB = os.path.join(PKG, VARIANTS["mutant"][0])
@@ -108,7 +112,8 @@ def build_variant(variant: str = "product", force: bool = False, verbose: bool =
     return lib
 
 
-def build_library(force: bool = False, verbose: bool = False, variants=("product", "test", "mutant")) -> str:
+def build_library(force: bool = False, verbose: bool = False,
+                  variants=("product", "test", "mutant", "checked")) -> str:
     """Build every variant whose embedded id is not the current one; returns the product path."""
     with ThreadPoolExecutor(max_workers=len(variants)) as ex:
         list(ex.map(lambda v: build_variant(v, force=force, verbose=verbose and v == "product",

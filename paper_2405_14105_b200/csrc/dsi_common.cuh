@@ -218,6 +218,7 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
     Word4 o[4];
 #pragma unroll
     for (int j = 3; j >= 0; --j) {
+      DSI_CHECK(4 * w + j < nq);
       const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
       o[j] = philox_call(u, th, K);
       R = pack8(R, o[j], h.C);
@@ -257,6 +258,7 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
 #pragma unroll
     for (int j = 2; j >= 0; --j) {
       if (j >= ncalls) continue;
+      DSI_CHECK(4 * w + j < nq);
       const uint4 u = TABLE ? U[4 * w + j] : philox_q_half((uint32_t)(4 * w + j), h.stream, K);
       const Word4 o = philox_call(u, th, K);
       R = pack8(R, o, h.C);

@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
 #pragma unroll
             for (int j = 7; j >= 0; --j) Rw = pack4(Rw, philox_call(U[8 * w + j], th, P.keys), nthr);
           } else {
+            DSI_CHECK(8 * w + ncalls <= nq && nq <= P.max_nq);
             for (int j = ncalls - 1; j >= 0; --j) Rw = pack4(Rw, philox_call(U[8 * w + j], th, P.keys), nthr);
           }
         } else {
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
           const int prev = below ? base + 31 - __clz(below) : lastz;
           const int L = base + zb - prev - 1;  // accepted drafts in this segment
           if (L > store_min) {
+            DSI_CHECK(SUMS || nr < P.max_runs);
             if (!SUMS) myruns[nr * CRN_THREADS] = (uint16_t)L;
             ++nr;
             maxL = max(maxL, L);
@@ -192,6 +194,7 @@ __global__ void __launch_bounds__(TH, DSI_CRN_MINB) dsi_crn_kernel(const CrnPara
       }
       n2 += run >= 1;  // the final segment (the trailing run, then position N)
       if (run > store_min) {
+        DSI_CHECK(SUMS || nr < P.max_runs);
         if (!SUMS) myruns[nr * CRN_THREADS] = (uint16_t)run;
         ++nr;
         maxL = max(maxL, run);

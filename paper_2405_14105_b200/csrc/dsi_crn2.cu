@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(TH) dsi_crn_stream_kernel(const CrnParams P) {
   uint64_t short_cnt = 0;            // FRESH: 6-bit counts of the runs with L = 2..kShortL
   auto push = [&](int L) {         // insertion into my[0..nr) kept in decreasing order
     if (FRESH && L <= kShortL) short_cnt += 1ull << (6 * (L - 2));
+    DSI_CHECK(nr < P.max_runs);
     int i = nr++;
     while (i > 0) {
       const int prev = my[(i - 1) * TH];

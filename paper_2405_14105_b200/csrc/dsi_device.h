@@ -4,6 +4,24 @@
 #include <stddef.h>
 #include <stdint.h>
 
+// Bounds checks of the kernels' computed indices: compiled in only by the checked test build
+// (libdsi_sim_checked.so, -DDSI_BOUNDS_CHECK; tests/test_bounds_checked.py), which traps with the
+// failing line -- the substitute for compute-sanitizer memcheck where the GPU pool has it closed.
+#ifdef DSI_BOUNDS_CHECK
+#include <cstdio>
+#define DSI_CHECK(c)                                                            \
+  do {                                                                          \
+    if (!(c)) {                                                                 \
+      printf("DSI_CHECK failed: %s at %s:%d\n", #c, __FILE__, __LINE__);       \
+      __trap();                                                                 \
+    }                                                                           \
+  } while (0)
+#else
+#define DSI_CHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 namespace dsi {
 
 // Indicator mode of a configuration (uniform per block).

@@ -68,9 +68,11 @@ __device__ __forceinline__ void seg_hist(int g, int seg_start, const SegCtx &s, 
   // accepts r-1 and is counted only if its k-draft window ends before N
   const int kk = (int)s.k_eff;
   const int M = (int)magic_div((uint32_t)g + s.k_eff, s.m_si, 0u);
+  DSI_CHECK(g >= 1 && g <= s.n_tokens);
   if (M > 1) atomicAdd(&sh_si[kk], (unsigned)(M - 1));
   const int last_start = seg_start + (M - 1) * (kk + 1);
   const int r = g - (M - 1) * (kk + 1);
+  DSI_CHECK(r >= 1 && r - 1 <= kk);
   if (last_start + kk + 1 <= s.n_tokens) atomicAdd(&sh_si[r - 1], 1u);
 }
 
@@ -82,7 +84,10 @@ __device__ __forceinline__ void seg_hist(int g, int seg_start, const SegCtx &s, 
 // and its cost is lowered by the fresh forwards' saving (the table already holds it).
 template <bool TABLE, bool FRESH>
 __device__ __forceinline__ uint2 long_cost(int g, const uint2 *T, const SegCtx &s, int t_d) {
-  if (TABLE) return T[g];
+  if (TABLE) {
+    DSI_CHECK(g >= 0 && g <= s.n_tokens);
+    return T[g];
+  }
   uint2 e = seg_long(g, s);
   if (FRESH) e.y -= fresh_saving(g, s, t_d);
   return e;
@@ -124,11 +129,12 @@ __device__ __forceinline__ void walk_word(uint32_t R, int nv, int Lk, const uint
 // (Lk > 30): branch-free, so the compiler can schedule it among the next word's Philox calls.
 // T[0] = (0, 0) absorbs the common "no long run" case.
 __device__ __forceinline__ void walk_full_word_nb(uint32_t R, int Lk, const uint2 *T, int &run, int &n2, uint32_t &ai,
-                                                  uint32_t &ay) {
+                                                  uint32_t &ay, int n) {
   const uint32_t E = R & ~((R << 1) | (run == 0 ? 1u : 0u));
   n2 += __popc(E);
   const int z0 = __ffs(R) - 1;  // -1 when R == 0
   const bool lng = (R != 0u) & (run + z0 >= Lk);
+  DSI_CHECK(!lng || run + z0 + 1 <= n);
   const uint2 e = T[lng ? run + z0 + 1 : 0];
   ai += e.x;
   ay += e.y;
@@ -162,6 +168,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
   // (A/B measured, profiles/r01_ab.jsonl: balanced tiles, a direct unit -> config
   //  division and a host-built unit -> config map were each 1-5% slower than this)
   const uint32_t c = s_cfg;
+  DSI_CHECK(c < P.n_cfg);
   const DevCfg cfg = P.cfg[c];
   const uint64_t t0 = (unit - __ldg(&P.tile_prefix[c])) * P.tile_trials;
   const uint64_t t1 = min(t0 + P.tile_trials, cfg.n_trials);
@@ -300,11 +307,11 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
         nz += __popc(Rp);
         for (int w = 1; w < nfull; ++w) {
           const uint32_t R = gen_word(w);
-          walk_full_word_nb(Rp, Lk, T, run, n2, ai, ay);
+          walk_full_word_nb(Rp, Lk, T, run, n2, ai, ay, N);
           nz += __popc(R);
           Rp = R;
         }
-        walk_full_word_nb(Rp, Lk, T, run, n2, ai, ay);
+        walk_full_word_nb(Rp, Lk, T, run, n2, ai, ay, N);
         w_start = nfull;
       }
     }
@@ -321,6 +328,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
         if (ncalls == 8) {
 #pragma unroll
           for (int j = 7; j >= 0; --j) {
+            DSI_CHECK(8 * w + j < nq);
             const uint4 u = TABLE ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), cfg.stream_id, P.keys);
             R = pack4(R, philox_call(u, th, P.keys), nthr);
           }
@@ -328,6 +336,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
           // (a loop: unrolled with warp-uniform guards it was 1% slower on cfg3, equal on cfg5,
           //  profiles/r02e_ab_words_tail*.jsonl -- unlike the halves layout's last word)
           for (int j = ncalls - 1; j >= 0; --j) {
+            DSI_CHECK(8 * w + j < nq);
             const uint4 u = TABLE ? U[8 * w + j] : philox_q_half((uint32_t)(8 * w + j), cfg.stream_id, P.keys);
             R = pack4(R, philox_call(u, th, P.keys), nthr);
           }
@@ -349,6 +358,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
           const int g = z - lastz;
           if (HIST) seg_hist(g, lastz, s, sh_seg, sh_si);
           if (g >= 2) {
+            DSI_CHECK(g >= 2 && g <= N);
             uint2 e = TABLE ? T[g] : seg_extra(g, s);
             if (!TABLE && VAR == 2 && fresh) e.y -= fresh_saving(g, s, t_d);
             ai += e.x;
@@ -379,6 +389,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
       gl = N - lastz;  // the final segment ends at N
       if (HIST) seg_hist(gl, lastz, s, sh_seg, sh_si);
       if (gl >= 2) {
+        DSI_CHECK(gl >= 2 && gl <= N);
         uint2 e = TABLE ? T[gl] : seg_extra(gl, s);
         if (!TABLE && VAR == 2 && fresh) e.y -= fresh_saving(gl, s, t_d);
         ai += e.x;
@@ -388,6 +399,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
       gl = run + 1;  // the final segment: the trailing run of ones, then position N
       n2 += gl >= 2;
       if (run >= Lk) {
+        DSI_CHECK(gl <= N);
         const uint2 e = (VAR == 2 && fresh) ? long_cost<TABLE, true>(gl, T, s, t_d) : long_cost<TABLE, false>(gl, T, s, t_d);
         ai += e.x;
         ay += e.y;
@@ -408,6 +420,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
     }
     uint32_t si = (uint32_t)iters * (uint32_t)cfg.si_cost;
     if (ttft) {  // first forwards: SI's first iteration and DSI's first segment
+      DSI_CHECK(g1 >= 0 && g1 <= N);
       dsi += (uint32_t)D1[g1 ? g1 : N];
       si += (uint32_t)cfg.e_si;
     }
@@ -421,6 +434,7 @@ __global__ void __launch_bounds__(DSI_TRIAL_MAXT, HALVES ? DSI_TRIAL_MINB_HALVES
     a_trials += 1;
     if (PER_TRIAL) {
       const uint64_t r = cfg.rec_off + t;
+      DSI_CHECK(t < cfg.n_trials);
       P.rec_acc[r] = npos - nz;
       P.rec_m[r] = m;
       P.rec_iters[r] = iters;

@@ -61,10 +61,12 @@ __global__ void __launch_bounds__(128) dsi_seg_hist_kernel(const SegParams P) {
   unsigned long long *out1 = P.hist1 ? P.hist1 + G.hist_off : nullptr;
   auto add1 = [&](int g) {  // the trial's first segment has length g
     if (!out1) return;
+    DSI_CHECK(g >= 1 && g <= N);
     if (SMEM) atomicAdd(&H1[g], 1u);
     else atomicAdd(out1 + g, 1ull);
   };
   auto add = [&](int g) {
+    DSI_CHECK(g >= 1 && g <= N);
     if (SMEM) atomicAdd(&H[g], 1u);
     else atomicAdd(out + g, 1ull);
   };

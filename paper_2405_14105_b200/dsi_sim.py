@@ -17,10 +17,11 @@ LIB_PATH = os.path.join(_PKG, "libdsi_sim.so")
 # Builds of the same sources (paper_2405_14105_b200/build.py): the product, and two test builds
 # that add include/dsi_sim_testing.h (the host all-reduce hook, A/B knobs) -- the second with a
 # deliberately wrong C(g) for the mutation test.  The product is what every call uses unless a
-# test selects another build with use_library() (or DSI_SIM_LIB=test|mutant|<path> for a whole
+# test selects another build with use_library() (or DSI_SIM_LIB=test|mutant|checked|<path> for a whole
 # process, e.g. an A/B run).
 VARIANT_PATHS = {"product": LIB_PATH, "test": os.path.join(_PKG, "libdsi_sim_test.so"),
-                 "mutant": os.path.join(_PKG, "libdsi_sim_mutant.so")}
+                 "mutant": os.path.join(_PKG, "libdsi_sim_mutant.so"),
+                 "checked": os.path.join(_PKG, "libdsi_sim_checked.so")}
 
 DSI_ABI_VERSION = 2
 DSI_OK, DSI_E_NULL, DSI_E_RANGE, DSI_E_TICK, DSI_E_OVERFLOW, DSI_E_STRICT_EQ1, DSI_E_DEVICE, \

@@ -58,7 +58,7 @@ for flags in (0, FRESH):
     with D.Simulator(long_n, tick=0.01, seed=W.SEED, flags=flags) as sim:
         sim.run().reduce()
 # the k = 1 no-queue fast-path variant of the trial kernel (VAR 3), forced on
-with D.use_library("test"):
+with D.use_library("checked" if os.environ.get("DSI_SIM_LIB") == "checked" else "test"):
     D.dsi_test_set_knob("k1_fast", 1)
     for flags in (0, D.DSI_F_PER_TRIAL):
         with D.Simulator(cfgs, tick=tick, seed=W.SEED, flags=flags) as sim:
@@ -87,4 +87,17 @@ for m in (2, 3, 5, 8):
     D.dsi_multi_simulate(W.multi_rows(rows, m ** 3, 4), tick=1.0, seed=W.SEED,
                          flags=D.DSI_F_PATTERN | D.DSI_F_PER_TRIAL)
 D.dsi_multi_simulate(W.multi_rows([(1.0, (0.1, 0.3), (0.6, 0.8))], 2100, 5000), tick=0.01, seed=W.SEED)
+# the halves layout (DSI_F_RNG_HALVES): every mode; thresholds whose high half is an f16 NaN pattern
+# (XOR tie test) or 0 (all acceptances through ties), the pipelined walk (k >= 30), N > 4096
+H = D.DSI_F_RNG_HALVES
+hz = W.rows([(1.0, 0.1, a, k, 3, 100, 0, 300) for a in (0.49, 0.8, 2.0 ** -17) for k in (3, 40)])
+hlong = W.rows([(1.0, 0.3, 0.5, 2, 3, 4097, 1, 65), (1.0, 0.1, 0.49, 40, 3, 4099, 0, 33)])
+for grid in (hz, hlong, cfgs):
+    for flags in (H, H | D.DSI_F_PER_TRIAL | D.DSI_F_HIST, H | FRESH):
+        with D.Simulator(grid, tick=0.01 if grid is not cfgs else tick, seed=W.SEED, flags=flags) as sim:
+            sim.run().reduce()
+for grid, gt in ((hz, 0.01), (big, btick)):
+    for flags in (H | D.DSI_F_SHARED_STREAMS, H | D.DSI_F_SHARED_STREAMS | FRESH, H | D.DSI_F_MEANS_ONLY):
+        with D.Simulator(grid, tick=gt, seed=W.SEED, flags=flags) as sim:
+            sim.run().reduce()
 print("sanitizer driver ok")
