@@ -153,16 +153,8 @@ __device__ __forceinline__ uint32_t half_of(const Word4 &o, int j) {
   return j < 4 ? x >> 16 : x & 0xFFFFu;
 }
 
-// Exact decisions of every tied position among calls 4w .. 4w + ncalls - 1 (bits 8c + j of R):
-// rejected iff w >= R_low, w from the tie-break call (q, 1, trial, stream).  Rare (a warp takes
-// it for ~1.6% of its words): the word's calls are regenerated one by one (rounds 2-9 from the
-// per-counter half, as a loop: few registers, so no spills in the caller), and the tie-break call shares
-// the main call's per-counter half of rounds 0-1 (counter word 1 enters round 0 only through
-// the trial half: n0 = hi(M1 trial) ^ 1 ^ k0[0]).  Few scalar arguments (the trial half is
-// recomputed): a reference to a caller's local would force it to the stack, and every argument
-// register is one more value the hot loop must keep around the call.
-// Rounds 2-9 as a loop (few registers: the callee's register count is what the caller must
-// save around the call).
+// Rounds 2-9 as a loop (few registers: the rare tie paths run it, and a callee's register count is
+// what its caller must save around the call).
 __device__ __forceinline__ Word4 philox_call_rolled(const uint4 &u, const TrialHalf &t, const Keys &K) {
   uint32_t c0 = u.x ^ t.n1, c1 = u.y, c2 = t.ha ^ u.z, c3 = t.la;
 #pragma unroll 1
@@ -179,15 +171,27 @@ __device__ __forceinline__ Word4 philox_call_rolled(const uint4 &u, const TrialH
   return Word4{c0, c1, c2, c3};
 }
 
+// The trial half of rounds 0-1 for the tie-break counter (q, 1, trial, stream): counter word 1
+// enters round 0 only through n0 = hi(M1 trial) ^ c1 ^ k0[0], so the tie-break call shares the
+// main call's per-counter half U[q].
+__device__ __forceinline__ TrialHalf tiebreak_trial_half(uint32_t trial, const Keys &K) {
+  const uint64_t p = (uint64_t)PHILOX_M1 * trial;
+  const uint32_t n0 = (uint32_t)(p >> 32) ^ 1u ^ K.k0[0];
+  const uint64_t a = (uint64_t)PHILOX_M0 * n0;
+  return TrialHalf{(uint32_t)p, (uint32_t)(a >> 32), (uint32_t)a};
+}
+
+// Exact decisions of every tied position among calls 4w .. 4w + ncalls - 1 (bits 8c + j of R):
+// rejected iff w >= R_low, w from the tie-break call.  For the last (partial) word of a trial; full
+// words fix their ties inline (gen_word_halves_t).  The calls are regenerated one by one, and the
+// arguments are few scalars (the trial half is recomputed): a reference to a caller's local would
+// force it to the stack, and every argument is one more value the hot loop keeps around the call.
 template <bool TABLE>
 static __device__ __noinline__ uint32_t halves_fix(uint32_t R, int w, int ncalls, const uint4 *U, uint32_t trial,
                                                    uint32_t stream, uint32_t thr, const Keys &K) {
   const uint32_t T = thr >> 16, Rl = thr & 0xFFFFu;
   const TrialHalf th = philox_trial_half(trial, K);
-  const uint64_t p = (uint64_t)PHILOX_M1 * trial;
-  const uint32_t n0 = (uint32_t)(p >> 32) ^ 1u ^ K.k0[0];
-  const uint64_t a = (uint64_t)PHILOX_M0 * n0;
-  const TrialHalf tb_half{(uint32_t)p, (uint32_t)(a >> 32), (uint32_t)a};
+  const TrialHalf tb_half = tiebreak_trial_half(trial, K);
   for (int c = 0; c < ncalls; ++c) {
     const int q = 4 * w + c;
     const uint4 u = TABLE ? U[q] : philox_q_half((uint32_t)q, stream, K);
@@ -230,10 +234,7 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
     // with a warp vote 195.8 ms -- profiles/r02c_ab_halves_inl.jsonl, r02c_ab_halves_vote.jsonl)
     if (tf) {
       const uint32_t T = h.thr >> 16, Rl = h.thr & 0xFFFFu;
-      const uint64_t p = (uint64_t)PHILOX_M1 * trial;
-      const uint32_t n0 = (uint32_t)(p >> 32) ^ 1u ^ K.k0[0];
-      const uint64_t a = (uint64_t)PHILOX_M0 * n0;
-      const TrialHalf tb_half{(uint32_t)p, (uint32_t)(a >> 32), (uint32_t)a};
+      const TrialHalf tb_half = tiebreak_trial_half(trial, K);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t m = 0u;
