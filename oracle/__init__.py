@@ -14,7 +14,10 @@ Pins (tests/test_oracle_pins.py): Philox known-answer vectors, Table 1 (P:85-105
 Proposition 1, Theorem 1, the non-SI example,
 the SI closed form E[n+1] = (1-a^{k+1})/(1-a), exhaustive
 enumeration of acceptance patterns against exact rational expectations, and
-hand-derived worked examples.  No function here is "parity unpinned".
+hand-derived worked examples; the halves indicator layout (R26) by
+tests/test_oracle_halves.py (equal to the plain 32-bit comparison of the concatenated
+halves, forced ties both ways, the Bernoulli law where every acceptance or rejection is a
+tie).  No function here is "parity unpinned".
 """
 from __future__ import annotations
 

@@ -10,7 +10,8 @@
  * What it computes, for one configuration (target latency t_t, drafter latency
  * t_d, acceptance rate a, lookahead k, SP degree, N tokens) and one trial:
  *   - the acceptance indicators A_1..A_{N-1} (paper P:434: i.i.d.
- *     Bernoulli(a) per draft token) drawn from a Philox4x32-10 stream;
+ *     Bernoulli(a) per draft token) drawn from a Philox4x32-10 stream, one
+ *     32-bit word per position or (rng_halves) 16 bits plus a tie-break draw;
  *   - non-SI latency  N*t_t;
  *   - SI latency by the literal pseudocode loop;
  *   - DSI latency by a literal event simulation of Algorithm 1
