@@ -4,9 +4,10 @@ Four builds of the same sources:
   libdsi_sim.so         the product (no test hooks, no developer knobs)
   libdsi_sim_test.so    -DDSI_TEST_HOOKS: adds include/dsi_sim_testing.h (host all-reduce hook,
                         A/B knobs) for the multi-rank-on-one-GPU tests and A/B runs
-  libdsi_sim_mutant.so  -DDSI_TEST_HOOKS -DDSI_MUTANT_CG: every DSI segment cost C(g), g >= 2,
-                        one tick too large -- the mutation test (tests/test_mutation.py) checks
-                        that GPU parity against the oracle FAILS with it
+  libdsi_sim_mutant.so  -DDSI_TEST_HOOKS -DDSI_MUTANT_CG -DDSI_MUTANT_TIES: every DSI segment cost
+                        C(g), g >= 2, one tick too large, and the halves layout's tie-break dropped
+                        (ties left as rejections) -- the mutation test (tests/test_mutation.py)
+                        checks that GPU parity against the oracle FAILS with it
   libdsi_sim_checked.so -DDSI_TEST_HOOKS -DDSI_BOUNDS_CHECK: the kernels' computed indices checked
                         (DSI_CHECK traps) -- tests/test_bounds_checked.py runs every kernel variant
                         under it (compute-sanitizer is closed on the GPU pool)
@@ -36,7 +37,7 @@ HEADERS = [os.path.join(CSRC, f) for f in ("dsi_host.h", "dsi_device.h", "dsi_co
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 VARIANTS = {"product": ("libdsi_sim.so", []),
             "test": ("libdsi_sim_test.so", ["-DDSI_TEST_HOOKS"]),
-            "mutant": ("libdsi_sim_mutant.so", ["-DDSI_TEST_HOOKS", "-DDSI_MUTANT_CG"]),
+            "mutant": ("libdsi_sim_mutant.so", ["-DDSI_TEST_HOOKS", "-DDSI_MUTANT_CG", "-DDSI_MUTANT_TIES"]),
             "checked": ("libdsi_sim_checked.so", ["-DDSI_TEST_HOOKS", "-DDSI_BOUNDS_CHECK"])}
 LIB = os.path.join(PKG, VARIANTS["product"][0])
 TEST_LIB = os.path.join(PKG, VARIANTS["test"][0])

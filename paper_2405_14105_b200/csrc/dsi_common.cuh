@@ -232,6 +232,9 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
     // rare (~1.6% of warp-words): the word's outputs are still in registers, so only the tie-break
     // calls are computed (inline: 187.1 ms vs 188.0 with halves_fix's regeneration; guarding it
     // with a warp vote 195.8 ms -- profiles/r02c_ab_halves_inl.jsonl, r02c_ab_halves_vote.jsonl)
+#ifdef DSI_MUTANT_TIES
+    tf = 0u;  // mutation probe only: ties left as rejections (the tie-break dropped)
+#endif
     if (tf) {
       const uint32_t T = h.thr >> 16, Rl = h.thr & 0xFFFFu;
       const TrialHalf tb_half = tiebreak_trial_half(trial, K);
@@ -267,6 +270,9 @@ __device__ __forceinline__ uint32_t gen_word_halves_t(int w, int nq, const uint4
     }
   }
   R |= h.orall;
+#ifdef DSI_MUTANT_TIES
+  tf = 0u;
+#endif
   if (tf) R = halves_fix<TABLE>(R, w, ncalls, U, trial, h.stream, h.thr, K);
   return R;
 }

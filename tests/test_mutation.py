@@ -48,6 +48,43 @@ def test_parity_catches_a_wrong_segment_cost():
             assert (n2 >= 0).all() and int(r["sum_dsi_ticks"]) - w["sum_dsi"] == int(n2.sum())
 
 
+def _half(words, j):
+    w = words[j % 4]
+    return (w >> 16) if j < 4 else (w & 0xFFFF)
+
+
+@pytest.mark.gpu
+def test_halves_parity_catches_a_dropped_tie_break():
+    """The mutant also drops the halves layout's tie-break (-DDSI_MUTANT_TIES: ties stay
+    rejections).  On thresholds built so that chosen positions tie and the tie-break accepts, the
+    per-trial accept counts -- which the C(g) mutation does not touch -- must differ from the
+    oracle's with the mutant and equal them with the product."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    key = (SEED & 0xFFFFFFFF, SEED >> 32)
+    rows = []
+    for q, j in ((0, 0), (0, 5), (1, 3), (6, 7), (12, 2)):
+        v = _half(O.philox4x32_10((q, 0, 0, 0), key), j)
+        w = _half(O.philox4x32_10((q, 1, 0, 0), key), j)
+        if w < 0xFFFF:
+            rows.append((1.0, 0.2, ((v << 16) | (w + 1)) / 2 ** 32, 3, 3, 100, 0, 40))  # tie, accepted
+    cfgs = W.rows(rows)
+    want = [oracle_sums(row, 0.01, SEED, per_trial=True, halves=True) for row in cfgs]
+    for variant in ("product", "mutant"):
+        with D.use_library(variant):
+            with D.Simulator(cfgs, tick=0.01, seed=SEED, flags=D.DSI_F_PER_TRIAL | D.DSI_F_RNG_HALVES) as sim:
+                sim.run()
+                sim.reduce()
+                acc = [sim.trials(i)["acc"].astype(np.int64) for i in range(len(cfgs))]
+        same = [np.array_equal(a, w["acc"]) for a, w in zip(acc, want)]
+        if variant == "product":
+            assert all(same)
+        else:  # trial 0 ties at the chosen position in every config
+            assert not any(same)
+            assert all(int(a[0]) == int(w["acc"][0]) - 1 for a, w in zip(acc, want))
+
+
 def test_oracle_pins_catch_a_wrong_segment_cost():
     """CPU: which oracle pins would catch C(g) + 1.  Prop. 1's per-trial identity (P:211-213,
     L_DSI = t_d acc + t_t (N - acc) at k = 1 with enough servers) does, on every trial that has a
