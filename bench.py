@@ -191,7 +191,7 @@ def other_workloads_block(D, names, args, base_kw, root, fresh_id, flush, barrie
     """BASELINE.json's other configs on the same GPUs (collective: every rank runs its share):
     per workload the per-config mode (run + reduce, CUDA events, as `value`) with its SURVEY 8(d).4
     issue fraction, and the shared-stream and means-only modes (run + reduce_device) with whether
-    their sums equal the per-config run's."""
+    their sums equal the per-config run's; and the per-config mode under the halves layout (R26)."""
     import torch
 
     sm_max = float(measured_peaks().get("sm_max_mhz", 1965.0))
@@ -204,7 +204,7 @@ def other_workloads_block(D, names, args, base_kw, root, fresh_id, flush, barrie
         entry = {"desc": WORKLOAD_DESC[name], "configs": int(cfgs.size), "trial_tokens_per_step": tt}
         ref = None
         for mode, flags in (("per_config", 0), ("shared_streams", D.DSI_F_SHARED_STREAMS),
-                            ("means_only", D.DSI_F_MEANS_ONLY)):
+                            ("means_only", D.DSI_F_MEANS_ONLY), ("per_config_rng_halves", D.DSI_F_RNG_HALVES)):
             sim = D.Simulator(cfgs, flags=D.DSI_F_TIMING | root | flags, nccl_id=fresh_id(), **kw)
             st = torch.cuda.ExternalStream(sim.stream(), device=torch.device("cuda", base_kw["device"]))
             res = np.zeros(cfgs.size, D.RESULT_DTYPE)
@@ -219,7 +219,7 @@ def other_workloads_block(D, names, args, base_kw, root, fresh_id, flush, barrie
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(st)
                 sim.run()
-                if flags:
+                if flags & (D.DSI_F_SHARED_STREAMS | D.DSI_F_MEANS_ONLY):
                     sim.reduce_device()
                 else:
                     sim.reduce(res)
@@ -236,6 +236,9 @@ def other_workloads_block(D, names, args, base_kw, root, fresh_id, flush, barrie
                 ach = alg_instructions(cfgs) / world / (kern / 1000.0)
                 d["roofline_issue_frac"] = ach / peak_instr
                 ref = res
+            elif flags == D.DSI_F_RNG_HALVES:  # the halves layout (R26): its own accounting, its own draws
+                ach = alg_instructions_halves(cfgs) / world / (kern / 1000.0)
+                d["roofline_issue_frac"] = ach / peak_instr
             elif base_kw["rank"] == 0:
                 sim.fetch(0, cfgs.size, res)
                 d["sums_identical_to_per_config"] = bool(all(
