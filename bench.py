@@ -414,10 +414,19 @@ def multi_drafter_block(steps: int, sm_max: float) -> dict:
         D.dsi_multi_simulate(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING | D.DSI_F_MEANS_ONLY)
         ms_means.append(D.dsi_multi_last_kernel()[0])
     mults = multi_alg_multiplies(cfgs)
+    # the halves layout (R26): drafter j on counter word 1 = 2(j-1), 8 positions per call
+    ms_h = []
+    for _ in range(steps):
+        D.dsi_multi_simulate(cfgs, tick=tick, seed=W.SEED, flags=D.DSI_F_TIMING | D.DSI_F_RNG_HALVES)
+        ms_h.append(D.dsi_multi_last_kernel()[0])
     return {"workload": "W.multi_heatmap: m = 3, f_1 (t 0.01, a 0.5) ahead of cfg3's 10100 (t_d, a) "
                         "points as f_2, t_m 1.0, N 100, 1e4 trials, lookahead 1 (Alg. 1 as stated)",
             "value": tt / (k_ms / 1000.0), "unit": UNIT, "kernel_ms": k_ms,
             "trial_tokens_per_step": tt, "gpu_launches": D.dsi_multi_last_kernel()[1],
+            "rng_halves": {"value": tt / (statistics.median(ms_h) / 1000.0), "unit": UNIT,
+                           "kernel_ms": statistics.median(ms_h),
+                           "note": "DSI_F_RNG_HALVES (DESIGN.md R26): 16 bits per indicator plus an exact "
+                                   "tie-break draw, one Philox call per 8 positions and drafter"},
             "means_only": {"value": tt / (statistics.median(ms_means) / 1000.0), "unit": UNIT,
                            "kernel_ms": statistics.median(ms_means),
                            "note": "DSI_F_MEANS_ONLY: one pass per acceptance group, sums for every "

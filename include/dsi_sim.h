@@ -126,8 +126,10 @@ typedef enum {
                                  default layout from half the Philox calls, but different
                                  indicators (results are not comparable trial by trial with
                                  the default layout).  Every mode (per-config, SHARED_STREAMS,
-                                 MEANS_ONLY, the heatmap) gives the same integers under it;
-                                 dsi_multi_simulate keeps the default layout.                 */
+                                 MEANS_ONLY, the heatmap) gives the same integers under it.
+                                 dsi_multi_simulate takes it too: drafter j on counter word 1
+                                 = 2(j-1), its tie-break on 2(j-1)+1 (drafter 1 draws exactly
+                                 the single-drafter stream).                                  */
 
 /* One grid point: the paper's quantities (Table 2 columns P:249-256; Sec. 3.1). */
 typedef struct {

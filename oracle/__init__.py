@@ -244,7 +244,7 @@ class _MultiConfig(ctypes.Structure):
     _fields_ = [("t_target", ctypes.c_int64), ("t_drafter", ctypes.c_int64 * (MAX_MODELS - 1)),
                 ("accept_rate", ctypes.c_double * (MAX_MODELS - 1)),
                 ("n_drafters", ctypes.c_int32), ("n_tokens", ctypes.c_int32),
-                ("stream_id", ctypes.c_uint32), ("reserved", ctypes.c_int32)]
+                ("stream_id", ctypes.c_uint32), ("rng_halves", ctypes.c_int32)]
 
 
 class _MultiOut(ctypes.Structure):
@@ -292,6 +292,7 @@ class MultiConfig:
     accept_rates: tuple
     n_tokens: int
     stream_id: int = 0
+    rng_halves: bool = False  # the halves layout (R26); drafter j on counter word 2(j-1)
 
     @property
     def m(self) -> int:
@@ -306,6 +307,7 @@ class MultiConfig:
         c.n_drafters = len(self.t_drafters)
         c.n_tokens = int(self.n_tokens)
         c.stream_id = int(self.stream_id)
+        c.rng_halves = int(bool(self.rng_halves))
         return c
 
 

@@ -129,7 +129,10 @@ typedef struct {
   int32_t  n_drafters;                        /* m - 1 in 1..7                        */
   int32_t  n_tokens;                          /* N >= 1                               */
   uint32_t stream_id;
-  int32_t  reserved;                          /* 0                                    */
+  /* 0: drafter j's indicator at p is word (p-1)&3 of counter (q=(p-1)>>2, j-1, trial, stream);
+     1: the halves layout (R26) with drafter j on counter word 1 = 2(j-1) and its
+     tie-break on 2(j-1)+1 -- drafter 1 draws exactly the single-drafter halves stream */
+  int32_t  rng_halves;
 } oracle_multi_config;
 
 typedef struct {

@@ -34,11 +34,23 @@ static int multi_valid(const oracle_multi_config *c) {
     if (j > 1 && t < c->t_drafter[j - 2]) return 0;         /* ordered by latency (R25) */
     if (!(c->accept_rate[j - 1] >= 0.0 && c->accept_rate[j - 1] <= 1.0)) return 0;
   }
+  if (c->rng_halves != 0 && c->rng_halves != 1) return 0;
   return 1;
 }
 
+/* 16-bit half j8 of a Philox output (the halves layout, R26): the high half of word
+ * j8 for j8 < 4, the low half of word j8 - 4 otherwise. */
+static uint32_t multi_half16(const uint32_t out[4], int j8) {
+  uint32_t word = out[j8 & 3];
+  if (j8 < 4) return word >> 16;
+  return word & 0xFFFFu;
+}
+
 /* A_{j,p}: does drafter j's token at position p (on the verified prefix) equal the
- * target's?  Philox at counter (q, j-1, trial, stream_id), word (p-1) & 3. */
+ * target's?  Philox at counter (q, j-1, trial, stream_id), word (p-1) & 3; with rng_halves,
+ * the 16-bit half (p-1) & 7 of counter (q = (p-1) >> 3, 2(j-1), trial, stream_id) against the
+ * threshold's high half T, a tie (v == T) decided by the same half of counter word 2(j-1)+1
+ * against its low half R:  A = [v 2^16 + w < floor(a_j 2^32)]. */
 int oracle_multi_indicator(const oracle_multi_config *cfg, uint64_t seed, uint64_t trial,
                            int pattern, int32_t j, int32_t p) {
   const int32_t m = cfg ? cfg->n_drafters + 1 : 0;
@@ -51,12 +63,28 @@ int oracle_multi_indicator(const oracle_multi_config *cfg, uint64_t seed, uint64
     for (i = 1; i < p; i++) x /= (uint64_t)m;
     return (int32_t)(x % (uint64_t)m) + 1 <= j;
   }
-  ctr[0] = (uint32_t)((p - 1) >> 2);
-  ctr[1] = (uint32_t)(j - 1);
-  ctr[2] = (uint32_t)trial;
-  ctr[3] = cfg->stream_id;
   key[0] = (uint32_t)seed;
   key[1] = (uint32_t)(seed >> 32);
+  ctr[2] = (uint32_t)trial;
+  ctr[3] = cfg->stream_id;
+  if (cfg->rng_halves) {
+    const uint64_t thr = oracle_threshold(cfg->accept_rate[j - 1]);
+    const uint64_t T = thr >> 16, R = thr & 0xFFFFu;
+    const int j8 = (int)((p - 1) & 7);
+    uint32_t v, w;
+    ctr[0] = (uint32_t)((p - 1) >> 3);
+    ctr[1] = (uint32_t)(2 * (j - 1));
+    oracle_philox4x32_10(ctr, key, out);
+    v = multi_half16(out, j8);
+    if (v < T) return 1;
+    if (v > T) return 0;
+    ctr[1] = (uint32_t)(2 * (j - 1) + 1); /* the tie-break draw */
+    oracle_philox4x32_10(ctr, key, out);
+    w = multi_half16(out, j8);
+    return w < R;
+  }
+  ctr[0] = (uint32_t)((p - 1) >> 2);
+  ctr[1] = (uint32_t)(j - 1);
   oracle_philox4x32_10(ctr, key, out);
   return (uint64_t)out[(p - 1) & 3] < oracle_threshold(cfg->accept_rate[j - 1]);
 }

@@ -243,6 +243,8 @@ struct MultiParams {
   int32_t *rec_settled;         // 8 per trial (or NULL)
   int32_t max_n;
   int32_t max_drafters;
+  int32_t halves;  // DSI_F_RNG_HALVES: drafter j on counter word 1 = 2j, its tie-break on 2j + 1
+  int32_t pad_[3];
   Keys keys;
 };
 int launch_multi_kernel(const MultiParams &p, uint64_t n_units, bool pattern, void *stream);

@@ -38,8 +38,40 @@ __device__ __forceinline__ uint32_t call4(const uint4 &u, uint32_t n1, uint32_t 
   return accept4(philox_rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K), thr);
 }
 
-template <int D, bool PATTERN, bool TABLE>
+// The halves layout (DSI_F_RNG_HALVES, R26) for drafter j (0-based): the call at counter
+// (q, 2j, trial, stream) gives 8 acceptance bits (bit i = position 8q + i + 1), a tie decided by
+// the call at (q, 2j + 1, ...): its trial half of rounds 0-1 differs only through c1 (n0 ^ (2j+1)).
+// Drafter 0 draws exactly the single-drafter halves stream (counter words 1 = 0 and 1).
+__device__ __forceinline__ uint32_t call8(const uint4 &u, uint32_t n1, uint32_t ha, uint32_t la, uint32_t thr,
+                                          const Keys &K, uint32_t pt_hi, uint32_t c1) {
+  const Word4 o = philox_rounds_2_9(u.x ^ n1, u.y, ha ^ u.z, la, K);
+  const uint32_t T = thr >> 16;
+  const uint32_t TT = T | (T << 16);
+  uint32_t rej = pack8(0u, o, (0x10000u - T) << 16) | (T == 0u ? 0xFFu : 0u);
+  if (tie_flags<false>(o, TT, 0u)) {  // rare: exact decisions of the tied positions
+    const uint32_t n0 = pt_hi ^ (c1 + 1u) ^ K.k0[0];
+    const uint64_t a = (uint64_t)PHILOX_M0 * n0;
+    const TrialHalf tb_half{n1, (uint32_t)(a >> 32), (uint32_t)a};
+    const Word4 tb = philox_call_rolled(u, tb_half, K);
+    const uint32_t Rl = thr & 0xFFFFu;
+    for (int j = 0; j < 8; ++j)
+      if (half_of(o, j) == T) rej = half_of(tb, j) >= Rl ? (rej | 1u << j) : (rej & ~(1u << j));
+  }
+  return ~rej & 0xFFu;
+}
+
+template <bool HALVES>
+__device__ __forceinline__ uint32_t callw(const uint4 &u, uint32_t n1, uint32_t ha, uint32_t la, uint32_t thr,
+                                          const Keys &K, uint32_t pt_hi, uint32_t c1) {
+  if (HALVES) return call8(u, n1, ha, la, thr, K, pt_hi, c1);
+  return call4(u, n1, ha, la, thr, K);
+}
+
+// HALVES: positions come in octets (one call = 8 positions) instead of quads.
+template <int D, bool PATTERN, bool TABLE, bool HALVES>
 __global__ void __launch_bounds__(128) dsi_multi_kernel(const MultiParams P) {
+  constexpr int W = HALVES ? 8 : 4;                  // positions per call
+  constexpr uint32_t FULL = HALVES ? 0xFFu : 0xFu;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t s_cfg;
   const uint64_t unit = P.unit_begin + blockIdx.x;
@@ -58,8 +90,8 @@ __global__ void __launch_bounds__(128) dsi_multi_kernel(const MultiParams P) {
   const uint64_t t1 = min(t0 + P.tile_trials, cfg.n_trials);
   const int nd = cfg.n_drafters;
   const int npos = cfg.n_tokens - 1;
-  const int nq = (npos + 3) >> 2;
-  const uint32_t tail = npos & 3 ? (1u << (npos & 3)) - 1u : 0xfu;  // open bits of the last quad
+  const int nq = (npos + W - 1) / W;
+  const uint32_t tail = npos % W ? (1u << (npos % W)) - 1u : FULL;  // open bits of the last call
 
   uint4 *U = reinterpret_cast<uint4 *>(smem);
   if (TABLE && !PATTERN) {
@@ -91,10 +123,11 @@ __global__ void __launch_bounds__(128) dsi_multi_kernel(const MultiParams P) {
       // per-trial halves of rounds 0-1, one per drafter (counter word 1 = j)
       const uint64_t pt = (uint64_t)PHILOX_M1 * (uint32_t)t;
       const uint32_t n1 = (uint32_t)pt;
+      const uint32_t pt_hi = (uint32_t)(pt >> 32);
       uint32_t ha[D], la[D];
 #pragma unroll
       for (int j = 0; j < D; ++j) {
-        const uint32_t n0 = (uint32_t)(pt >> 32) ^ (uint32_t)j ^ P.keys.k0[0];
+        const uint32_t n0 = pt_hi ^ (uint32_t)(HALVES ? 2 * j : j) ^ P.keys.k0[0];
         const uint64_t a = (uint64_t)PHILOX_M0 * n0;
         ha[j] = (uint32_t)(a >> 32);
         la[j] = (uint32_t)a;
@@ -110,7 +143,7 @@ __global__ void __launch_bounds__(128) dsi_multi_kernel(const MultiParams P) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           u[i] = TABLE ? U[q + i] : philox_q_half((uint32_t)(q + i), cfg.stream_id, P.keys);
-          o[i] = q + i == nq - 1 ? tail : 0xfu;
+          o[i] = q + i == nq - 1 ? tail : FULL;
         }
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -121,20 +154,21 @@ __global__ void __launch_bounds__(128) dsi_multi_kernel(const MultiParams P) {
               for (int i = 0; i < 4; ++i) c[i] = cfg.mode[j] == MODE_ALL_ACCEPT ? o[i] : 0u;
             } else if (j == 0 || cfg.width[j] == 4) {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) c[i] = call4(u[i], n1, ha[j], la[j], cfg.thr[j], P.keys) & o[i];
+              for (int i = 0; i < 4; ++i)
+                c[i] = callw<HALVES>(u[i], n1, ha[j], la[j], cfg.thr[j], P.keys, pt_hi, 2 * j) & o[i];
             } else if (cfg.width[j] == 2) {
 #pragma unroll
               for (int i = 0; i < 4; i += 2)
                 if (o[i] | o[i + 1]) {
-                  c[i] = call4(u[i], n1, ha[j], la[j], cfg.thr[j], P.keys) & o[i];
-                  c[i + 1] = call4(u[i + 1], n1, ha[j], la[j], cfg.thr[j], P.keys) & o[i + 1];
+                  c[i] = callw<HALVES>(u[i], n1, ha[j], la[j], cfg.thr[j], P.keys, pt_hi, 2 * j) & o[i];
+                  c[i + 1] = callw<HALVES>(u[i + 1], n1, ha[j], la[j], cfg.thr[j], P.keys, pt_hi, 2 * j) & o[i + 1];
                 }
             } else {
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                if (o[i]) c[i] = call4(u[i], n1, ha[j], la[j], cfg.thr[j], P.keys) & o[i];
+                if (o[i]) c[i] = callw<HALVES>(u[i], n1, ha[j], la[j], cfg.thr[j], P.keys, pt_hi, 2 * j) & o[i];
             }
-            cnt[j] += __popc(c[0] | c[1] << 4 | c[2] << 8 | c[3] << 12);
+            cnt[j] += __popc(c[0] | c[1] << W | c[2] << (2 * W) | c[3] << (3 * W));
 #pragma unroll
             for (int i = 0; i < 4; ++i) o[i] &= ~c[i];
           }
@@ -142,13 +176,13 @@ __global__ void __launch_bounds__(128) dsi_multi_kernel(const MultiParams P) {
       }
       for (; q < nq; ++q) {  // the last nq mod 4 quads one at a time
         const uint4 uq = TABLE ? U[q] : philox_q_half((uint32_t)q, cfg.stream_id, P.keys);
-        uint32_t open = q == nq - 1 ? tail : 0xfu;
+        uint32_t open = q == nq - 1 ? tail : FULL;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           if (j < nd && open) {
             uint32_t acc;
             if (cfg.mode[j] == MODE_STREAM) {
-              acc = call4(uq, n1, ha[j], la[j], cfg.thr[j], P.keys) & open;
+              acc = callw<HALVES>(uq, n1, ha[j], la[j], cfg.thr[j], P.keys, pt_hi, 2 * j) & open;
             } else {
               acc = cfg.mode[j] == MODE_ALL_ACCEPT ? open : 0u;
             }
@@ -203,7 +237,7 @@ __global__ void __launch_bounds__(128) dsi_multi_kernel(const MultiParams P) {
   }
 }
 
-template <int D, bool PATTERN, bool TABLE>
+template <int D, bool PATTERN, bool TABLE, bool HALVES>
 int launch_multi_t(const MultiParams &p, uint64_t n_units, cudaStream_t st) {
   const size_t smem = TABLE && !PATTERN ? (size_t)((p.max_n - 1 + 3) / 4 + 1) * sizeof(uint4) : 0;
   const uint64_t max_grid = 0x7fffffffull;
@@ -211,7 +245,7 @@ int launch_multi_t(const MultiParams &p, uint64_t n_units, cudaStream_t st) {
   for (uint64_t done = 0; done < n_units;) {
     const uint64_t n = (n_units - done) < max_grid ? (n_units - done) : max_grid;
     q.unit_begin = p.unit_begin + done;
-    dsi_multi_kernel<D, PATTERN, TABLE><<<(unsigned)n, 128, smem, st>>>(q);
+    dsi_multi_kernel<D, PATTERN, TABLE, HALVES><<<(unsigned)n, 128, smem, st>>>(q);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
     done += n;
@@ -221,9 +255,13 @@ int launch_multi_t(const MultiParams &p, uint64_t n_units, cudaStream_t st) {
 
 template <int D>
 int launch_multi_d(const MultiParams &p, uint64_t n_units, bool pattern, cudaStream_t st) {
-  if (pattern) return launch_multi_t<D, true, false>(p, n_units, st);
-  if (p.max_n <= MULTI_TABLE_MAX_N) return launch_multi_t<D, false, true>(p, n_units, st);
-  return launch_multi_t<D, false, false>(p, n_units, st);
+  if (pattern) return launch_multi_t<D, true, false, false>(p, n_units, st);
+  if (p.halves) {
+    if (p.max_n <= MULTI_TABLE_MAX_N) return launch_multi_t<D, false, true, true>(p, n_units, st);
+    return launch_multi_t<D, false, false, true>(p, n_units, st);
+  }
+  if (p.max_n <= MULTI_TABLE_MAX_N) return launch_multi_t<D, false, true, false>(p, n_units, st);
+  return launch_multi_t<D, false, false, false>(p, n_units, st);
 }
 
 }  // namespace

@@ -39,8 +39,9 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   if (opt->abi_version != DSI_ABI_VERSION) return fail(nullptr, DSI_E_RANGE, "abi_version mismatch");
   if (n_cfg == 0 || n_cfg >= (1ull << 31)) return fail(nullptr, DSI_E_RANGE, "n_cfg out of range");
   if (!(std::isfinite(opt->tick) && opt->tick > 0.0)) return fail(nullptr, DSI_E_RANGE, "tick must be > 0");
-  if (opt->flags & ~(DSI_F_PER_TRIAL | DSI_F_PATTERN | DSI_F_TIMING | DSI_F_MEANS_ONLY))
-    return fail(nullptr, DSI_E_RANGE, "multi-drafter mode takes PER_TRIAL, PATTERN, TIMING and MEANS_ONLY only");
+  if (opt->flags & ~(DSI_F_PER_TRIAL | DSI_F_PATTERN | DSI_F_TIMING | DSI_F_MEANS_ONLY | DSI_F_RNG_HALVES))
+    return fail(nullptr, DSI_E_RANGE,
+                "multi-drafter mode takes PER_TRIAL, PATTERN, TIMING, MEANS_ONLY and RNG_HALVES only");
   const bool means = opt->flags & DSI_F_MEANS_ONLY;
   if (means && (opt->flags & DSI_F_PER_TRIAL))
     return fail(nullptr, DSI_E_RANGE, "DSI_F_MEANS_ONLY excludes DSI_F_PER_TRIAL");
@@ -238,6 +239,7 @@ dsi_status dsi_multi_simulate(const dsi_options *opt, const dsi_multi_config *cf
   p.rec_settled = (int32_t *)b_set.p;
   p.max_n = max_n;
   p.max_drafters = max_d;
+  p.halves = (opt->flags & DSI_F_RNG_HALVES) ? 1 : 0;
   const uint32_t s_lo = (uint32_t)opt->seed, s_hi = (uint32_t)(opt->seed >> 32);
   for (int r = 0; r < 10; ++r) {
     p.keys.k0[r] = s_lo + (uint32_t)r * 0x9E3779B9u;

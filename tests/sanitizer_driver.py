@@ -100,4 +100,7 @@ for grid, gt in ((hz, 0.01), (big, btick)):
     for flags in (H | D.DSI_F_SHARED_STREAMS, H | D.DSI_F_SHARED_STREAMS | FRESH, H | D.DSI_F_MEANS_ONLY):
         with D.Simulator(grid, tick=gt, seed=W.SEED, flags=flags) as sim:
             sim.run().reduce()
+for flags in (H, H | D.DSI_F_PER_TRIAL, H | D.DSI_F_MEANS_ONLY):
+    D.dsi_multi_simulate(mf, tick=mtick, seed=W.SEED, flags=flags)
+D.dsi_multi_simulate(W.multi_rows([(1.0, (0.1, 0.3), (0.49, 0.8))], 700, 5000), tick=0.01, seed=W.SEED, flags=H)
 print("sanitizer driver ok")

@@ -247,3 +247,50 @@ def test_halves_update_equals_a_fresh_handle(mode):
     fields = MEANS if mode == D.DSI_F_MEANS_ONLY else MOMENTS
     for f in fields:
         assert np.array_equal(got[f], want[f]), (mode, f)
+
+
+def _multi_oracle_cfg(row, tick):
+    nd = int(row["n_drafters"])
+    return O.MultiConfig(O.ticks(float(row["t_target"]), tick),
+                         tuple(O.ticks(float(x), tick) for x in row["t_drafter"][:nd]),
+                         tuple(float(x) for x in row["accept_rate"][:nd]),
+                         int(row["n_tokens"]), int(row["stream_id"]), rng_halves=True)
+
+
+@pytest.mark.parametrize("seed_fuzz", [17, 29])
+def test_halves_multi_drafter_per_trial(seed_fuzz):
+    """dsi_multi_simulate under the halves layout (drafter j on counter word 1 = 2(j-1), its
+    tie-break on 2(j-1)+1): per-trial L_DSI and settled-by counts bit-exact against the oracle's
+    chain, the literal thread tree on the small cases; thresholds with f16-NaN / zero high halves."""
+    mf, mtick = W.multi_fuzz(40, seed=seed_fuzz, n_max=70, trials=120)
+    rows = [(1.0, (0.02, 0.1), (0.49, 2.0 ** -17)), (1.0, (0.05, 0.2, 0.3), (0.99, 0.8, 0.5)),
+            (1.0, (0.1,), (1 - 2.0 ** -17,))]
+    extra = W.multi_rows(rows, 300, 90, stream_id=2)
+    for cfgs, tick in ((mf, mtick), (extra, 0.01)):
+        res, dsi, settled = D.dsi_multi_simulate(cfgs, tick=tick, seed=SEED, flags=H, per_trial=True)
+        off = np.concatenate([[0], np.cumsum(cfgs["n_trials"].astype(np.int64))])
+        for i, row in enumerate(cfgs):
+            oc = _multi_oracle_cfg(row, tick)
+            T = int(row["n_trials"])
+            want = O.multi_run(oc, SEED, 0, T)
+            got_d = dsi[off[i]:off[i + 1]].astype(np.int64)
+            assert np.array_equal(got_d, want["dsi"]), (i, oc)
+            assert np.array_equal(settled[off[i]:off[i + 1], :oc.m], want["settled"]), (i, oc)
+            assert int(res[i]["sum_dsi_ticks"]) == want["sum_dsi"]
+            if int(row["n_tokens"]) <= 9 and oc.m <= 4:
+                for t in range(min(T, 20)):
+                    assert int(got_d[t]) == O.multi_tree(oc, SEED, t)["dsi"], (i, t)
+
+
+def test_halves_multi_drafter_one_drafter_is_the_single_drafter_stream():
+    """m = 2 under the halves layout: the multi-drafter path at lookahead 1 equals the per-config
+    path's halves stream (drafter 1 draws counter words 1 = 0 and 1, as the single-drafter layout)."""
+    rows = [(1.0, (0.1,), (0.8,)), (1.0, (0.3,), (0.49,)), (1.0, (1.0,), (0.5,))]
+    mc = W.multi_rows(rows, 500, 77)
+    res, dsi, _ = D.dsi_multi_simulate(mc, tick=0.01, seed=SEED, flags=H, per_trial=True)
+    single = W.rows([(1.0, r[1][0], r[2][0], 1, 100, 77, 0, 500) for r in rows])
+    sim, sres = run_sim(single, 0.01, D.DSI_F_PER_TRIAL)
+    for i in range(len(rows)):
+        got = dsi[i * 500:(i + 1) * 500].astype(np.int64)
+        assert np.array_equal(got, sim.trials(i)["dsi"].astype(np.int64)), i
+    sim.close()

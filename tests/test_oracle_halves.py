@@ -92,3 +92,25 @@ def test_halves_degenerate_thresholds():
     for a, want in ((0.0, 0), (1.0, 1)):
         r = O.run(O.Config(3, 1, a, 2, 2, 64, 0, rng_halves=True), SEED, 0, 50)
         assert r["sum_acc"] == want * 63 * 50
+
+
+@pytest.mark.parametrize("j", [1, 2, 3])
+def test_multi_drafter_halves_equal_the_concatenated_comparison(j):
+    """The multi-drafter oracle's halves indicator (drafter j on counter word 1 = 2(j-1), its
+    tie-break on 2(j-1)+1) equals the plain 32-bit comparison of the concatenated halves."""
+    rates = (0.8, 0.49, 2.0 ** -17)
+    cfg = O.MultiConfig(100, (2, 5, 9), rates, 50, 1, rng_halves=True)
+    thr = O.threshold(rates[j - 1])
+    for trial in (0, 9):
+        for p in range(1, 41):
+            q, j8 = (p - 1) // 8, (p - 1) % 8
+            v = half(O.philox4x32_10((q, 2 * (j - 1), trial, 1), KEY), j8)
+            w = half(O.philox4x32_10((q, 2 * (j - 1) + 1, trial, 1), KEY), j8)
+            assert O.multi_indicator(cfg, SEED, trial, j, p) == int(((v << 16) | w) < thr), (j, trial, p)
+
+
+def test_multi_drafter_halves_drafter1_is_the_single_drafter_stream():
+    a = 0.49
+    cfg = O.MultiConfig(100, (5,), (a,), 41, 0, rng_halves=True)
+    got = [O.multi_indicator(cfg, SEED, 4, 1, p) for p in range(1, 41)]
+    assert got == indicators(a, 4, 40)
