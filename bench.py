@@ -974,7 +974,9 @@ def ours(args):
             "config": {"workload": args.workload, "desc": WORKLOAD_DESC[args.workload],
                        "configs": int(cfgs.size), "trials": int(cfgs["n_trials"].sum()),
                        "trial_tokens_per_step": tt, "tick": tick, "seed": W.SEED,
-                       "l2": "flushed between timed steps (256 MiB memset)", "parallelism": f"dp{world}"},
+                       "l2": "flushed between timed steps (256 MiB memset)", "parallelism": f"dp{world}",
+                       "rng_layout": "one 32-bit Philox word per position (SURVEY 0.1(9), DESIGN R14); the "
+                                     "halves layout (R26) is the rng_halves block"},
             # SURVEY 8(d).4's accounting: 11 + 10(1-a) algorithmic thread-instructions per
             # trial-token against the issue peak (148 SM x 4 SMSP x 32 lanes x clock); the
             # fmaheavy pipe that binds in ncu (Philox's IMAD.WIDE at a measured 4.1 cycles per
