@@ -319,8 +319,21 @@ def rng_halves_block(D, cfgs, cfgs_pinned, tick, args, base_kw, root, fresh_id, 
             d["e2e"] = {"value": tt * args.steps / max_over_ranks(sum(ts)), "unit": UNIT,
                         "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
             ach = alg_instructions_halves(cfgs) / world / (kern / 1000.0)
+            ncu_h = None  # --set full of one full bench launch of this kernel (profiles/, if captured)
+            try:
+                with open(os.path.join(ROOT, "profiles", "latest_halves_ncu_summary.json")) as f:
+                    k = json.load(f)["kernels"][0]
+                ncu_h = {"issue_active_pct": float(k["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]),
+                         "fmaheavy_pct": float(
+                             k["sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"][0]),
+                         "alu_pct": float(k["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"][0]),
+                         "registers": int(k["launch__registers_per_thread"][0]),
+                         "source": "profiles/latest_halves_ncu_summary.json (" + json.load(open(
+                             os.path.join(ROOT, "profiles", "latest_halves_ncu_summary.json")))["report"] + ")"}
+            except (OSError, KeyError, ValueError, IndexError):
+                pass
             d["roofline"] = {"bound": "alu", "achieved": ach / 1e9, "peak": peak_instr / 1e9, "unit": "Ginstr/s",
-                             "frac": ach / peak_instr, "kernel": "dsi_trial_kernel<..., HALVES>",
+                             "frac": ach / peak_instr, "kernel": "dsi_trial_kernel<..., HALVES>", "ncu": ncu_h,
                              "work": "6 + 10(1-a) thread-instructions per trial-token: 5 for Philox4x32-10 (40 "
                                      "per call of 8 indicators), 1 compare, 10 per rejection"}
             ref = res
