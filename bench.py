@@ -343,6 +343,8 @@ def rng_halves_block(D, cfgs, cfgs_pinned, tick, args, base_kw, root, fresh_id, 
             if flags == D.DSI_F_SHARED_STREAMS:
                 fields += ("sumsq_si_ticks", "sumsq_dsi_ticks", "n_dsi_gt_nonsi", "n_dsi_gt_si")
             d["sums_identical_to_per_config"] = bool(all(np.array_equal(res[f], ref[f]) for f in fields))
+        # the heatmap product under this layout (run + dsi_sim_heatmap, host wall clock, as heatmap.grid_time_*)
+        d["heatmap_grid_time_s"] = max_over_ranks(statistics.median(heatmap_grid_times(sim, flush, args.steps)[0]))
         sim.close()
         out[mode] = d
     if base_kw["rank"] == 0:
