@@ -46,8 +46,9 @@ COMMON = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O2,-fvi
 # per-source ptxas settings: the trial kernels' register allocation at -regUsageLevel=2 (default 5):
 # the 32-bit layout's kernel takes 80 registers instead of 91 and runs 1.7% faster on the cfg3
 # sample (cfg4 1.6%, cfg5 and the halves / fresh-verifier variants unchanged;
-# profiles/r02o_ab_*_ru2*.jsonl, r02o_ab_*_reglevel.jsonl)
-PER_SOURCE = {"dsi_kernel.cu": ["-Xptxas", "-regUsageLevel=2"]}
+# profiles/r02o_ab_*_ru2*.jsonl, r02o_ab_*_reglevel.jsonl); the two-pass shared-stream kernels at
+# -regUsageLevel=8: cfg3 12.77 -> 12.5 ms (profiles/r02s_ab_shared_reglevel.jsonl)
+PER_SOURCE = {"dsi_kernel.cu": ["-Xptxas", "-regUsageLevel=2"], "dsi_crn2.cu": ["-Xptxas", "-regUsageLevel=8"]}
 
 
 def nvcc() -> str:
